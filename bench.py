@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the batched access-mode-calculus evaluator (BASELINE.json metric).
+
+One step = one pass of the hot path over one batch: trace_eval over this rank's traces
+(BASELINE config 2 per GPU: 1M traces x 64 arrays x 256 calls, whole-array validity)
++ the counter reduction, + for N>1 the NCCL allreduce of the counter vector (config 4).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  See DESIGN.md §6 for every field.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "component-call transitions/sec at 1/2/4/8 B200; bitmap GB/s vs HBM peak"
+N_ARRAYS, N_CALLS, ADV, FUEL, SEED = 64, 256, 1, 10000, 1
+TRACES_PER_GPU = 1 << 20
+WORKLOAD = "C2/C4: 1M traces x 64 arrays x 256 whole-array component calls per GPU (BASELINE configs[1], sharded by trace id for N>1)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--traces", type=int, default=TRACES_PER_GPU, help="traces per GPU")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=3.0, help="wall seconds of the CPU baseline sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        loaded = [r for r in self.rows if r[2].isdigit() and int(r[2]) > 0] or self.rows
+        sm = [float(r[0]) for r in loaded if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in loaded if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in loaded for n, v in zip(names, r[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(loaded)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per trace_eval launch from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_trace_eval.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("traces_per_launch")
+    return None, None
+
+
+# ------------------------------------------------------------------- CPU baselines
+def cpu_eval_fn():
+    """(kind, fn) for the CPU baseline: the reference compiled in place (oracle/_ref) if it
+    shipped, else the C restatement (oracle/_build).  Test infrastructure, timed only."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_ffi as orc
+
+    if orc.have_ref():
+        return "reference", lambda recs, n, threads: orc.ref_eval(recs, n, N_CALLS, N_ARRAYS, FUEL, threads=threads, mode=1)
+    return "port", lambda recs, n, threads: orc.orc_eval(recs, n, N_CALLS, N_ARRAYS, FUEL)
+
+
+def evaluated_calls(res):
+    st = res["status"]
+    return int(res["calls_done"].astype(np.int64).sum() + (st != 0).sum())
+
+
+def cpu_sample(seconds, threads, trace0=0):
+    """Time the CPU evaluator on a bounded sample of the same workload (trace ids from
+    trace0), sized to ~`seconds` of wall time on `threads` host threads."""
+    import paper_1910_11110_b200 as coh
+
+    kind, fn = cpu_eval_fn()
+    cores = threads if kind == "reference" else 1
+    n = 64 if kind == "reference" else 2048
+    while True:
+        recs = coh.gen_records_host(SEED, trace0, n, N_CALLS, N_ARRAYS, ADV)
+        t0 = time.perf_counter()
+        res, _ = fn(recs, n, cores)
+        dt = time.perf_counter() - t0
+        if dt >= 0.25 * seconds or n >= (1 << 22):
+            if dt < seconds and n < (1 << 22):
+                n = int(n * seconds / max(dt, 1e-3))
+                recs = coh.gen_records_host(SEED, trace0, n, N_CALLS, N_ARRAYS, ADV)
+                t0 = time.perf_counter()
+                res, _ = fn(recs, n, cores)
+                dt = time.perf_counter() - t0
+            calls = evaluated_calls(res)
+            return {"value": calls / dt, "unit": "calls/s", "cores": cores, "kind": kind,
+                    "sample": f"{n} traces (ids {trace0}..{trace0 + n - 1}) of the same workload, {dt:.2f} s wall",
+                    "traces": n, "seconds": dt, "calls": calls}
+        n *= 4
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return  # rank 0 alone runs the reference arm
+    threads = os.cpu_count() or 1
+    # per-step sample sized so warmup + steps finish within ~2 minutes
+    per_step = max(0.2, min(5.0, 120.0 / max(1, args.steps + args.warmup)))
+    for w in range(args.warmup):
+        cpu_sample(per_step, threads, trace0=w * 4096)
+    t_calls, t_sec, last = 0, 0.0, None
+    for k in range(args.steps):
+        last = cpu_sample(per_step, threads, trace0=(1 << 30) + k * 65536)
+        t_calls += last["calls"]
+        t_sec += last["seconds"]
+    value = t_calls / t_sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "calls/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_sec / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
+        "data": "synthetic (splitmix64 call records, seed 1)",
+        "config": {"workload": WORKLOAD, "arrays": N_ARRAYS, "calls": N_CALLS, "adv_per1024": ADV, "fuel": FUEL},
+        "cpu_baseline": {"value": value, "unit": "calls/s", "cores": last["cores"], "kind": last["kind"],
+                         "sample": f"per step: {last['sample']}; run_annotated on all host threads"},
+        "e2e": {"value": value, "unit": "calls/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1910_11110_b200 as coh
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = coh.Context(local)
+    stream = torch.cuda.Stream()
+    s = stream.cuda_stream
+    N = args.traces
+    trace0 = rank * N  # contiguous trace-id shard per rank, generated on-device
+    with torch.cuda.stream(stream):
+        d_rec = torch.empty(coh.records_elems(N, N_CALLS), dtype=torch.int16, device="cuda")
+        d_res = torch.empty(N * 64, dtype=torch.uint8, device="cuda")
+        d_bnd = torch.empty(coh.boundary_words(N_CALLS) * N, dtype=torch.int32, device="cuda")
+        d_cnt = torch.zeros(16, dtype=torch.int64, device="cuda")
+    ctx.gen_records(SEED, trace0, N, N_CALLS, N_ARRAYS, ADV, d_rec, s)
+    stream.synchronize()
+
+    def step(ev0=None, ev1=None):
+        if ev0 is not None:
+            ev0.record(stream)
+        ctx.eval_traces(d_rec, N, N_CALLS, N_ARRAYS, FUEL, d_res, d_bnd, stream=s)
+        if ev1 is not None:
+            ev1.record(stream)
+        ctx.reduce_counters(d_res, N, d_cnt, s)
+        if world > 1:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(d_cnt[:10])  # exact: integer sums
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(max(3, args.warmup)):
+        step()
+    stream.synchronize()
+    counters = d_cnt.cpu().numpy().astype(np.uint64)  # whole-job counters of one step
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launch_count
+    t_start.record(stream)
+    for k in range(args.steps):
+        step(*kev[k])
+    t_end.record(stream)
+    stream.synchronize()
+    launches = ctx.launch_count - launches0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = t_start.elapsed_time(t_end)
+    kern_ms = [a.elapsed_time(b) for a, b in kev]
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    calls_per_step = int(counters[8] + counters[0] + counters[1] + counters[3])  # all ranks
+    value = calls_per_step * args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel (trace_eval) on this rank: algorithmic bytes per
+    # launch = 2 B per evaluated call (records) + 64 B result + 4 B per boundary word
+    local_calls = calls_per_step // world
+    alg_bytes = 2 * local_calls + N * (64 + 4 * coh.boundary_words(N_CALLS))
+    k_ms = statistics.mean(kern_ms)
+    peak, peak_src = peaks()
+    achieved = alg_bytes / (k_ms / 1e3) / 1e9
+    traffic, traffic_traces = ncu_traffic()
+    if traffic is not None and traffic_traces:
+        traffic = traffic * N / traffic_traces
+
+    # end-to-end through the public C-ABI host entry point (pinned host buffers,
+    # H2D of the step's records + D2H of results and boundary bitmaps inside the region)
+    e2e = None
+    if args.e2e_steps > 0:
+        rec_elems = coh.records_elems(N, N_CALLS)
+        L = coh.lib()
+        import ctypes as C
+
+        p_rec = L.coh_host_alloc(rec_elems * 2)
+        p_res = L.coh_host_alloc(N * 64)
+        p_bnd = L.coh_host_alloc(coh.boundary_words(N_CALLS) * N * 4)
+        h_rec = np.ctypeslib.as_array((C.c_uint16 * rec_elems).from_address(p_rec))
+        h_res = np.ctypeslib.as_array((C.c_uint8 * (N * 64)).from_address(p_res)).view(coh.RESULT_DTYPE)
+        h_bnd = np.ctypeslib.as_array((C.c_uint32 * (coh.boundary_words(N_CALLS) * N)).from_address(p_bnd))
+        h_rec[:] = d_rec.cpu().numpy().view(np.uint16)
+        ctx.eval_traces_host(h_rec, N, N_CALLS, N_ARRAYS, FUEL, results=h_res, boundary=h_bnd)  # warm
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            ctx.eval_traces_host(h_rec, N, N_CALLS, N_ARRAYS, FUEL, results=h_res, boundary=h_bnd)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        # e2e results equal the device-resident results
+        assert np.array_equal(h_res.view(np.uint8), d_res.cpu().numpy()), "host entry != device entry"
+        e2e = {"value": calls_per_step * args.e2e_steps / dt, "unit": "calls/s",
+               "h2d_bytes_per_step": rec_elems * 2, "d2h_bytes_per_step": N * 64 + coh.boundary_words(N_CALLS) * N * 4,
+               "ms_per_step": 1e3 * dt / args.e2e_steps}
+        for p in (p_rec, p_res, p_bnd):
+            L.coh_host_free(p)
+    clocks.stop()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sample(args.cpu_seconds, os.cpu_count() or 1)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "calls/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u16",
+            "data": "synthetic (counter-based splitmix64 call records generated in HBM, seed 1)",
+            "config": {"workload": WORKLOAD, "traces_per_gpu": N, "arrays": N_ARRAYS, "calls": N_CALLS,
+                       "adv_per1024": ADV, "fuel": FUEL, "parallelism": f"dp{world} (trace-id shards)",
+                       "l2": "inputs larger than L2 (records 512 MiB per GPU), no flush"},
+            "transitions_per_s": float(counters[4]) * args.steps / (ms / 1e3),
+            "counters_per_step": {n: int(v) for n, v in zip(coh.COUNTER_NAMES, counters[:10])},
+            "roofline": {"bound": "hbm", "kernel": "k_trace_eval", "achieved": achieved, "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "alg_bytes_per_launch": alg_bytes, "kernel_ms": k_ms,
+                         "note": "INT/LSU-issue bound in practice; see profiles/ for pipe utilisation"},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

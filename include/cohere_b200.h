@@ -1,0 +1,189 @@
+/*
+ * cohere_b200.h — C ABI of the B200-native batched evaluator for the access-mode
+ * calculus of arXiv 1910.11110 (reference: /root/reference/proj, namespace cohere).
+ *
+ * The reference has no FFI layer; its boundary is the header-only C++ API in
+ * namespace cohere (proj/include/cohere/cohere.hpp:5-14).  Every entry point below
+ * names the reference function(s) it replaces.  Plain pointers and sizes only; no
+ * exception crosses this ABI: failures are int status codes plus coh_last_error().
+ *
+ * Ordinals mirror the reference enums exactly:
+ *   coh_effect     <- cohere::EffectKind  (validity.hpp:35)   Push, Pull, Read, Write, Noop
+ *   coh_site       <- cohere::Site        (ast.hpp:22)         Local, Remote
+ *   coh_mode_kind  <- AccessMode::Kind    (program.hpp:188)    R, W, RW
+ *   coh_run_status <- cohere::RunStatus   (semantics.hpp:220)  Done, Stuck, FuelExhausted
+ *                     (+ COH_RUN_DEFECT: a malformed record; the reference would throw)
+ *
+ * Threading: thread-compatible (one host thread per ctx), stream-ordered; results are
+ * deterministic and independent of launch geometry and GPU count.
+ */
+#ifndef COHERE_B200_H
+#define COHERE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------ */
+enum {
+  COH_OK = 0,
+  COH_E_CONSTRUCTION = 1,     /* <= cohere::ConstructionError (program.hpp:16-18)       */
+  COH_E_DEFECT = 2,           /* <= std::logic_error (program.hpp:147-151, semantics.hpp:156) */
+  COH_E_OVERLAP_CONFLICT = 3, /* <= cohere::OverlapInferenceError (overlap.hpp:24-30)   */
+  COH_E_CUDA = 4,
+  COH_E_NCCL = 5,
+  COH_E_ARG = 6
+};
+
+enum { COH_PUSH = 0, COH_PULL = 1, COH_READ = 2, COH_WRITE = 3, COH_NOOP = 4 };
+enum { COH_LOCAL = 0, COH_REMOTE = 1 };
+enum { COH_R = 0, COH_W = 1, COH_RW = 2 };
+enum { COH_RUN_DONE = 0, COH_RUN_STUCK = 1, COH_RUN_FUEL_EXHAUSTED = 2, COH_RUN_DEFECT = 3 };
+enum { COH_KEY_CONCRETE = 0, COH_KEY_ABSTRACT = 1 }; /* VarKey::Kind Scalar / Abstract */
+
+/* ---- whole-array component-call records ------------------------------------------
+ * One uint16 per component call (one DeclBlock with a single AccessMode on one array,
+ * program.hpp:212-235), SURVEY §8(d):
+ *   bits 0-5  array id            (the scalar "a<id>" of the reference harness)
+ *   bits 6-7  mode kind R/W/RW    (3 is malformed -> COH_RUN_DEFECT)
+ *   bit  8    site (0 CPU/Local, 1 GPU/Remote)
+ *   bits 9-11 body variant        (0 = canonical well-declared body, 1..7 adversarial;
+ *                                  see DESIGN.md §3 / coh_body_variant_ops)
+ *   bits 12-15 zero
+ * Device layout, "call-major interleaved": rec(t, i) = records[((i/8)*n_traces + t)*8 + i%8]
+ * so one 128-bit load brings 8 calls of one trace and a warp's loads are contiguous.
+ * Padding records (i >= n_calls) are ignored.
+ */
+#define COH_REC_ARRAY(r) ((r) & 63u)
+#define COH_REC_KIND(r) (((r) >> 6) & 3u)
+#define COH_REC_SITE(r) (((r) >> 8) & 1u)
+#define COH_REC_VARIANT(r) (((r) >> 9) & 7u)
+#define COH_MAKE_REC(arr, kind, site, var) \
+  ((uint16_t)(((arr) & 63u) | (((kind) & 3u) << 6) | (((site) & 1u) << 8) | (((var) & 7u) << 9)))
+#define COH_MAX_ARRAYS 64
+#define COH_N_VARIANTS 8
+
+/* Per-array 4-bit state nibble: bit0 concrete local valid, bit1 concrete remote valid,
+ * bit2 abstract local valid, bit3 abstract remote valid.  initial_store (program.hpp:
+ * 174-184) puts every key at (V,I): nibble 0x5. */
+#define COH_STATE_INITIAL 0x5u
+
+/* Per-trace result: 64 bytes.  Replaces AnnotatedRun{status, store, stuck, boundary_ok,
+ * steps, ...} (modes.hpp:95-103) plus the transfer accounting the reference lacks
+ * (SURVEY §8(d) "transfer accounting rule").  Planes: bit a = array a is Valid. */
+typedef struct coh_trace_result {
+  uint64_t cl, cr;          /* concrete store:  store.at(scalar(a)).local/.remote     */
+  uint64_t al, ar;          /* abstract store:  store.at(abstract(a)).local/.remote   */
+  uint64_t transfer_bytes;  /* sum over executed concrete push/pull of array_bytes[a] */
+  uint32_t steps;           /* AnnotatedRun::steps                                    */
+  uint32_t transfers;       /* executed concrete Push/Pull steps                      */
+  uint32_t calls_done;      /* completed blocks == boundary_ok.size()                 */
+  uint32_t violations;      /* completed blocks whose boundary check failed           */
+  uint32_t stuck_call;      /* block index of the Stuck / FuelExhausted / defect call  */
+  uint8_t status;           /* COH_RUN_*                                              */
+  uint8_t stuck_array;      /* StuckInfo::key (array id)                              */
+  uint8_t stuck_effect;     /* StuckInfo::effect (COH_PUSH..)                         */
+  uint8_t stuck_flags;      /* bit0 StuckInfo::site, bit1 key kind (COH_KEY_*),
+                               bits2-3 StuckInfo::actual (bit2 local V, bit3 remote V)  */
+} coh_trace_result;
+
+typedef struct coh_trace_batch {
+  const uint16_t* records;     /* device, layout above                                 */
+  uint64_t n_traces;
+  uint32_t n_calls;            /* blocks per trace (>= 1)                              */
+  uint32_t n_arrays;           /* 1..64                                                */
+  int32_t fuel;                /* shared across blocks, as run_annotated (modes.hpp:110) */
+  uint32_t reserved;
+  const uint64_t* array_bytes; /* host, n_arrays entries (NULL => 1 byte each)         */
+} coh_trace_batch;
+
+/* boundary_ok bitmaps: word-major, boundary[(i/32)*n_traces + t] bit (i%32) is
+ * boundary_ok[i] of trace t; bits for calls >= calls_done are 0. */
+static inline uint32_t coh_boundary_words(uint32_t n_calls) { return (n_calls + 31u) / 32u; }
+
+/* ---- context -------------------------------------------------------------------- */
+typedef struct coh_ctx coh_ctx;
+int coh_ctx_create(int device, coh_ctx** out);
+void coh_ctx_destroy(coh_ctx* ctx);
+const char* coh_last_error(const coh_ctx* ctx);
+const char* coh_version(void);
+
+/* ---- host call-table compiler (no GPU needed) -------------------------------------
+ * Replaces translate_mode / translate_block (modes.hpp:31-59) + effect_signature /
+ * apply_signature (validity.hpp:79-120) + the swap rule of apply_effect_at
+ * (semantics.hpp:109-130), compiled into a (call type x 16 states) table.
+ * call type = record bits 6..11 (kind | site<<2 | variant<<3), 64 types.
+ * coh_calltable_describe fills, for one (type, state), what the reference run of that
+ * block from that store produces.  Returns COH_OK or COH_E_ARG. */
+typedef struct coh_call_outcome {
+  uint8_t status;        /* COH_RUN_DONE / COH_RUN_STUCK / COH_RUN_DEFECT         */
+  uint8_t state_after;   /* nibble after the block (store as left when stuck)     */
+  uint8_t steps;         /* completed reduction steps                              */
+  uint8_t transfers;     /* executed concrete Push/Pull                            */
+  uint8_t viol_before;   /* !leq(abstract, concrete) before (modes.hpp:71-75)      */
+  uint8_t viol_after;
+  uint8_t stuck_effect, stuck_flags; /* as coh_trace_result                        */
+} coh_call_outcome;
+int coh_calltable_describe(uint32_t call_type, uint32_t state, coh_call_outcome* out);
+/* Micro-op listing of one call type's translated block (guards then body). ops[k]:
+ * bits0-1 op (0 end,1 if-valid(x^) skip2,2 if-gvalid(x^) skip2,3 effect),
+ * bits2-4 effect, bit5 site, bit6 target abstract.  Returns op count. */
+int coh_calltable_program(uint32_t call_type, uint8_t ops[8]);
+
+/* ---- synthetic record generator -------------------------------------
+ * h = splitmix64(seed ^ (trace_id << 20) ^ call_idx)
+ *   array   = ((h & 0xffffffff) * n_arrays) >> 32
+ *   kind    = (((h >> 32) & 0xffff) * 3) >> 16
+ *   site    = (h >> 48) & 1
+ *   variant = ((h >> 49) & 0x3ff) < adv_per1024 ? 1 + ((((h >> 59) & 0x1f) * 7) >> 5) : 0
+ * Identical on host and device.  trace ids [trace0, trace0 + n_traces). */
+int coh_gen_records(coh_ctx* ctx, uint64_t seed, uint64_t trace0, uint64_t n_traces,
+                    uint32_t n_calls, uint32_t n_arrays, uint32_t adv_per1024,
+                    uint16_t* d_records, void* stream);
+int coh_gen_records_host(uint64_t seed, uint64_t trace0, uint64_t n_traces,
+                         uint32_t n_calls, uint32_t n_arrays, uint32_t adv_per1024,
+                         uint16_t* h_records);
+static inline size_t coh_records_elems(uint64_t n_traces, uint32_t n_calls) {
+  return (size_t)((n_calls + 7u) / 8u) * (size_t)n_traces * 8u;
+}
+
+/* ---- the hot path: batched trace evaluation ---------------------------------------
+ * Replaces, per trace, cohere::run_annotated (modes.hpp:105-125) over a program whose
+ * blocks are the trace's calls: translate_block (modes.hpp:53) -> run (semantics.hpp:
+ * 253-287, fuel shared, Done checked before fuel, Stuck consumes no step) ->
+ * abstraction_correct (modes.hpp:79-90) after each completed block.
+ * d_results: device, n_traces entries.  d_boundary: device, coh_boundary_words(n_calls)
+ * * n_traces words (may be NULL).  stream: cudaStream_t (NULL = legacy default). */
+int coh_eval_traces(coh_ctx* ctx, const coh_trace_batch* batch, coh_trace_result* d_results,
+                    uint32_t* d_boundary, void* stream);
+
+/* Same, from HOST buffers (records/results/boundary in host memory, ideally pinned):
+ * chunked H2D -> kernel -> D2H pipelined over two streams inside the call; returns
+ * after the results are on the host.  batch->records is a host pointer here. */
+int coh_eval_traces_host(coh_ctx* ctx, const coh_trace_batch* batch,
+                         coh_trace_result* h_results, uint32_t* h_boundary);
+
+/* Sum of per-trace counters into COH_N_COUNTERS uint64 (device):
+ * [0] traces stuck, [1] traces fuel-exhausted, [2] traces with >=1 boundary violation,
+ * [3] defect traces, [4] steps, [5] transfers, [6] transfer_bytes, [7] violating blocks,
+ * [8] completed blocks (sum of calls_done), [9] traces.
+ * Evaluated calls = [8] + [0] + [1] + [3].  This vector is what the multi-GPU path
+ * allreduces; integer sums make it exact and order-independent. */
+#define COH_N_COUNTERS 10
+int coh_reduce_counters(coh_ctx* ctx, const coh_trace_result* d_results, uint64_t n_traces,
+                        uint64_t* d_counters, void* stream);
+
+/* Kernels launched by this ctx since creation (the bench's gpu_launches claim). */
+uint64_t coh_launch_count(const coh_ctx* ctx);
+
+/* Pinned host memory for the host-buffer entry points. */
+void* coh_host_alloc(size_t bytes);
+void coh_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COHERE_B200_H */

@@ -1,0 +1,232 @@
+/*
+ * TEST INFRASTRUCTURE ONLY — the CPU oracle.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline leg may load it, and only as the checker.  The product path
+ * (paper_1910_11110_b200/) never links or calls it.
+ *
+ * Plain-C restatement of the reference evaluator (/root/reference/proj/include/cohere)
+ * for the whole-array trace path, written statement by statement from the reference:
+ *
+ *   orc_apply_cell      validity.hpp:73-120 (signature table, unification) and the
+ *                       swap rule of apply_effect_at, semantics.hpp:109-130
+ *   orc_leq             modes.hpp:71-75
+ *   translate_call      translate_mode / translate_block, modes.hpp:31-59 (guards use
+ *                       Local-site syncs, ast.hpp:144 Stmt::effect default)
+ *   run_block           run, semantics.hpp:253-287 (Done before fuel, Stuck takes no
+ *                       step, If = one step, eval_condition semantics.hpp:43-54)
+ *   orc_eval_traces     run_annotated, modes.hpp:105-125 + abstraction_correct
+ *                       modes.hpp:79-90 (full O(arrays) scan after every block)
+ *
+ * Pinned against the reference: tests/golden/ fixtures were produced by oracle/_ref (the
+ * reference compiled from its own headers) by tests/golden/make_golden.py, and
+ * tests/test_oracle.py checks this file against every one of them.
+ */
+#include <stdint.h>
+#include <string.h>
+
+#include "cohere_b200.h"
+
+/* pair bits: bit0 local Valid, bit1 remote Valid.  Returns -1 on NoUnify. */
+int orc_apply_cell(int eff, int site, int pair) {
+  int p = pair;
+  if (site == COH_REMOTE) p = ((p & 1) << 1) | ((p >> 1) & 1); /* swapped(before) */
+  int r;
+  switch (eff) {
+    case COH_PUSH: r = (p & 1) ? 3 : -1; break;  /* push : (V,X) -> (V,V) */
+    case COH_PULL: r = (p & 2) ? 3 : -1; break;  /* pull : (X,V) -> (V,V) */
+    case COH_READ: r = (p & 1) ? p : -1; break;  /* r    : (V,X) -> (V,X) */
+    case COH_WRITE: r = 1; break;                /* w    : (X,Y) -> (V,I) */
+    case COH_NOOP: r = p; break;                 /* noop : (X,Y) -> (X,Y) */
+    default: return -1;
+  }
+  if (r < 0) return -1;
+  if (site == COH_REMOTE) r = ((r & 1) << 1) | ((r >> 1) & 1); /* swapped(post) */
+  return r;
+}
+
+/* leq(abstract, concrete), modes.hpp:71-75 */
+int orc_leq(int abs_pair, int conc) {
+  if (abs_pair == conc) return 1;
+  return conc == 3 && (abs_pair == 1 || abs_pair == 2);
+}
+
+/* statement of a translated block: kind 0 = effect, 1 = if (valid(x^)) {} else {next 2},
+ * 2 = if (gvalid(x^)) {} else {next 2} */
+typedef struct {
+  int kind, eff, site, abstract_target;
+} orc_stmt;
+
+static int push_eff(orc_stmt* s, int n, int eff, int site, int abs_t) {
+  s[n].kind = 0;
+  s[n].eff = eff;
+  s[n].site = site;
+  s[n].abstract_target = abs_t;
+  return n + 1;
+}
+
+/* Fig. 3 translation of one mode on one array + the body variant. */
+static int translate_call(uint16_t rec, orc_stmt* s) {
+  const int kind = (int)COH_REC_KIND(rec), site = (int)COH_REC_SITE(rec);
+  const int var = (int)COH_REC_VARIANT(rec), S = site, O = site ^ 1;
+  const int sync = site == COH_REMOTE ? COH_PUSH : COH_PULL;
+  int n = 0;
+  if (kind == 3) return -1;
+  if (kind == COH_R || kind == COH_RW) { /* ensure_valid, modes.hpp:36-41 */
+    s[n].kind = site == COH_REMOTE ? 2 : 1;
+    n++;
+    n = push_eff(s, n, sync, COH_LOCAL, 0);
+    n = push_eff(s, n, sync, COH_LOCAL, 1);
+  }
+  if (kind == COH_W || kind == COH_RW) n = push_eff(s, n, COH_WRITE, site, 1); /* mark_written */
+  switch (var) {
+    case 0:
+      if (kind == COH_R) n = push_eff(s, n, COH_READ, S, 0);
+      else if (kind == COH_W) n = push_eff(s, n, COH_WRITE, S, 0);
+      else { n = push_eff(s, n, COH_READ, S, 0); n = push_eff(s, n, COH_WRITE, S, 0); }
+      break;
+    case 1: break;
+    case 2: n = push_eff(s, n, COH_READ, O, 0); break;
+    case 3: n = push_eff(s, n, COH_WRITE, O, 0); break;
+    case 4: n = push_eff(s, n, COH_READ, S, 0); break;
+    case 5: n = push_eff(s, n, COH_WRITE, S, 0); n = push_eff(s, n, COH_READ, O, 0); break;
+    case 6: n = push_eff(s, n, COH_PUSH, S, 0); break;
+    case 7: n = push_eff(s, n, COH_PULL, S, 0); n = push_eff(s, n, COH_WRITE, O, 0); break;
+  }
+  return n;
+}
+
+typedef struct {
+  int status, steps, transfers, stuck_eff, stuck_flags;
+} orc_block_out;
+
+/* run() over one translated block on one array's (concrete, abstract) pairs. */
+static void run_block(const orc_stmt* s, int n, int* conc, int* abst, int fuel, orc_block_out* o) {
+  int k = 0;
+  memset(o, 0, sizeof *o);
+  if (n < 0) { o->status = COH_RUN_DEFECT; return; }
+  for (;;) {
+    if (k >= n) { o->status = COH_RUN_DONE; return; }
+    if (o->steps >= fuel) { o->status = COH_RUN_FUEL_EXHAUSTED; return; }
+    if (s[k].kind != 0) {
+      const int flag = s[k].kind == 1 ? (*abst & 1) : ((*abst >> 1) & 1);
+      o->steps++;
+      k += flag ? 3 : 1;
+      continue;
+    }
+    int* cell = s[k].abstract_target ? abst : conc;
+    const int after = orc_apply_cell(s[k].eff, s[k].site, *cell);
+    if (after < 0) {
+      o->status = COH_RUN_STUCK;
+      o->stuck_eff = s[k].eff;
+      o->stuck_flags = s[k].site | (s[k].abstract_target << 1) | (*cell << 2);
+      return;
+    }
+    *cell = after;
+    o->steps++;
+    if (!s[k].abstract_target && (s[k].eff == COH_PUSH || s[k].eff == COH_PULL)) o->transfers++;
+    k++;
+  }
+}
+
+/* One block from a state nibble (cl, cr, al, ar): the call-table KAT. */
+int orc_call_outcome(uint32_t call_type, uint32_t state, coh_call_outcome* out) {
+  orc_stmt s[8];
+  const int n = translate_call((uint16_t)(call_type << 6), s);
+  int conc = (int)(state & 3u), abst = (int)(state >> 2);
+  orc_block_out o;
+  memset(out, 0, sizeof *out);
+  out->viol_before = !orc_leq(abst, conc);
+  run_block(s, n, &conc, &abst, 1 << 30, &o);
+  out->status = (uint8_t)o.status;
+  out->steps = (uint8_t)o.steps;
+  out->transfers = (uint8_t)o.transfers;
+  out->state_after = (uint8_t)(conc | (abst << 2));
+  out->viol_after = !orc_leq(abst, conc);
+  out->stuck_effect = (uint8_t)o.stuck_eff;
+  out->stuck_flags = (uint8_t)o.stuck_flags;
+  return 0;
+}
+
+int orc_eval_traces(const uint16_t* records, uint64_t n_total, uint64_t t_begin, uint64_t t_end,
+                    uint32_t n_calls, uint32_t n_arrays, int32_t fuel, const uint64_t* array_bytes,
+                    coh_trace_result* out, uint32_t* boundary) {
+  if (n_arrays < 1 || n_arrays > COH_MAX_ARRAYS || t_end < t_begin) return -1;
+  const uint64_t m = t_end - t_begin;
+  const uint32_t n_words = (n_calls + 31) / 32;
+  for (uint64_t j = 0; j < m; ++j) {
+    const uint64_t t = t_begin + j;
+    int conc[COH_MAX_ARRAYS], abst[COH_MAX_ARRAYS];
+    coh_trace_result* r = &out[j];
+    memset(r, 0, sizeof *r);
+    for (uint32_t a = 0; a < n_arrays; ++a) conc[a] = abst[a] = 1; /* initial_store: (V,I) */
+    if (boundary)
+      for (uint32_t w = 0; w < n_words; ++w) boundary[(uint64_t)w * m + j] = 0;
+    int steps = 0, status = COH_RUN_DONE;
+    for (uint32_t i = 0; i < n_calls; ++i) {
+      const uint16_t rec = records[((uint64_t)(i / 8) * n_total + t) * 8 + i % 8];
+      const uint32_t a = COH_REC_ARRAY(rec);
+      orc_stmt s[8];
+      orc_block_out o;
+      int dummy_c = 1, dummy_a = 1; /* an unknown array is a construction defect */
+      const int n = a < n_arrays ? translate_call(rec, s) : -1;
+      run_block(s, n, a < n_arrays ? &conc[a] : &dummy_c, a < n_arrays ? &abst[a] : &dummy_a,
+                fuel - steps, &o);
+      steps += o.steps;
+      r->transfers += (uint32_t)o.transfers;
+      if (o.transfers) r->transfer_bytes += (uint64_t)o.transfers * (array_bytes ? array_bytes[a] : 1u);
+      if (o.status != COH_RUN_DONE) {
+        status = o.status;
+        r->stuck_call = i;
+        r->stuck_array = (uint8_t)a;
+        r->stuck_effect = (uint8_t)o.stuck_eff;
+        r->stuck_flags = (uint8_t)o.stuck_flags;
+        break;
+      }
+      /* abstraction_correct: every array's abstract pair bounds its concrete pair */
+      int ok = 1;
+      for (uint32_t b = 0; b < n_arrays; ++b)
+        if (!orc_leq(abst[b], conc[b])) { ok = 0; break; }
+      r->calls_done++;
+      if (!ok) r->violations++;
+      if (ok && boundary) boundary[(uint64_t)(i / 32) * m + j] |= 1u << (i % 32);
+    }
+    r->status = (uint8_t)status;
+    r->steps = (uint32_t)steps;
+    for (uint32_t a = 0; a < n_arrays; ++a) {
+      r->cl |= (uint64_t)(conc[a] & 1) << a;
+      r->cr |= (uint64_t)((conc[a] >> 1) & 1) << a;
+      r->al |= (uint64_t)(abst[a] & 1) << a;
+      r->ar |= (uint64_t)((abst[a] >> 1) & 1) << a;
+    }
+  }
+  return 0;
+}
+
+/* Generator restatement (include/cohere_b200.h) for record-checksum parity. */
+static uint64_t orc_splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+int orc_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
+                    uint32_t n_arrays, uint32_t adv_per1024, uint16_t* recs) {
+  const uint32_t n_chunks = (n_calls + 7) / 8;
+  for (uint32_t c = 0; c < n_chunks; ++c)
+    for (uint64_t t = 0; t < n_traces; ++t)
+      for (uint32_t k = 0; k < 8; ++k) {
+        const uint32_t i = c * 8 + k;
+        uint16_t v = 0;
+        if (i < n_calls) {
+          const uint64_t h = orc_splitmix64(seed ^ ((trace0 + t) << 20) ^ (uint64_t)i);
+          const uint32_t arr = (uint32_t)(((h & 0xFFFFFFFFull) * n_arrays) >> 32);
+          const uint32_t kind = (uint32_t)((((h >> 32) & 0xFFFFull) * 3ull) >> 16);
+          const uint32_t site = (uint32_t)((h >> 48) & 1ull);
+          const uint32_t adv = (uint32_t)((h >> 49) & 0x3FFull) < adv_per1024;
+          const uint32_t var = adv ? 1u + (uint32_t)((((h >> 59) & 0x1Full) * 7ull) >> 5) : 0u;
+          v = COH_MAKE_REC(arr, kind, site, var);
+        }
+        recs[((uint64_t)c * n_traces + t) * 8 + k] = v;
+      }
+  return 0;
+}

@@ -1,0 +1,253 @@
+"""ctypes binding of include/cohere_b200.h (the product C ABI)."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "lib", "libcohere_b200.so")
+
+COH_OK, COH_E_CONSTRUCTION, COH_E_DEFECT, COH_E_OVERLAP_CONFLICT, COH_E_CUDA, COH_E_NCCL, COH_E_ARG = range(7)
+_ERR_NAMES = {
+    1: "ConstructionError",
+    2: "DefectError",
+    3: "OverlapInferenceError",
+    4: "CudaError",
+    5: "NcclError",
+    6: "ArgumentError",
+}
+
+# struct coh_trace_result (64 bytes)
+RESULT_DTYPE = np.dtype(
+    [
+        ("cl", "<u8"),
+        ("cr", "<u8"),
+        ("al", "<u8"),
+        ("ar", "<u8"),
+        ("transfer_bytes", "<u8"),
+        ("steps", "<u4"),
+        ("transfers", "<u4"),
+        ("calls_done", "<u4"),
+        ("violations", "<u4"),
+        ("stuck_call", "<u4"),
+        ("status", "u1"),
+        ("stuck_array", "u1"),
+        ("stuck_effect", "u1"),
+        ("stuck_flags", "u1"),
+    ]
+)
+assert RESULT_DTYPE.itemsize == 64
+
+COUNTER_NAMES = (
+    "stuck_traces",
+    "fuel_exhausted_traces",
+    "violating_traces",
+    "defect_traces",
+    "steps",
+    "transfers",
+    "transfer_bytes",
+    "violating_blocks",
+    "completed_blocks",
+    "traces",
+)
+N_COUNTERS = len(COUNTER_NAMES)
+
+
+class CohError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_ERR_NAMES.get(code, 'Error')} ({code}): {msg}")
+        self.code = code
+
+
+class _Batch(C.Structure):
+    _fields_ = [
+        ("records", C.c_void_p),
+        ("n_traces", C.c_uint64),
+        ("n_calls", C.c_uint32),
+        ("n_arrays", C.c_uint32),
+        ("fuel", C.c_int32),
+        ("reserved", C.c_uint32),
+        ("array_bytes", C.c_void_p),
+    ]
+
+
+class _Outcome(C.Structure):
+    _fields_ = [
+        ("status", C.c_uint8),
+        ("state_after", C.c_uint8),
+        ("steps", C.c_uint8),
+        ("transfers", C.c_uint8),
+        ("viol_before", C.c_uint8),
+        ("viol_after", C.c_uint8),
+        ("stuck_effect", C.c_uint8),
+        ("stuck_flags", C.c_uint8),
+    ]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load the CUDA library; raise loudly if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(lib_path):
+            raise RuntimeError(
+                f"cohere-b200 CUDA library missing at {lib_path}; run `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        L = C.CDLL(lib_path)
+        vp, u64, u32, i32, i = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int32, C.c_int
+        sig = {
+            "coh_ctx_create": (i, [i, C.POINTER(vp)]),
+            "coh_ctx_destroy": (None, [vp]),
+            "coh_last_error": (C.c_char_p, [vp]),
+            "coh_version": (C.c_char_p, []),
+            "coh_calltable_describe": (i, [u32, u32, C.POINTER(_Outcome)]),
+            "coh_calltable_program": (i, [u32, C.POINTER(C.c_uint8)]),
+            "coh_gen_records": (i, [vp, u64, u64, u64, u32, u32, u32, vp, vp]),
+            "coh_gen_records_host": (i, [u64, u64, u64, u32, u32, u32, vp]),
+            "coh_eval_traces": (i, [vp, C.POINTER(_Batch), vp, vp, vp]),
+            "coh_eval_traces_host": (i, [vp, C.POINTER(_Batch), vp, vp]),
+            "coh_reduce_counters": (i, [vp, vp, u64, vp, vp]),
+            "coh_launch_count": (u64, [vp]),
+            "coh_host_alloc": (vp, [C.c_size_t]),
+            "coh_host_free": (None, [vp]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def records_elems(n_traces: int, n_calls: int) -> int:
+    return ((n_calls + 7) // 8) * n_traces * 8
+
+
+def boundary_words(n_calls: int) -> int:
+    return (n_calls + 31) // 32
+
+
+def calltable_describe(call_type: int, state: int) -> dict:
+    o = _Outcome()
+    rc = lib().coh_calltable_describe(call_type, state, C.byref(o))
+    if rc:
+        raise CohError(rc, "coh_calltable_describe")
+    return o.as_dict()
+
+
+def calltable_program(call_type: int) -> list[int]:
+    ops = (C.c_uint8 * 8)()
+    n = lib().coh_calltable_program(call_type, ops)
+    if n < 0:
+        raise CohError(-n, "coh_calltable_program")
+    return list(ops[:n])
+
+
+def gen_records_host(seed: int, trace0: int, n_traces: int, n_calls: int, n_arrays: int, adv_per1024: int) -> np.ndarray:
+    out = np.zeros(records_elems(n_traces, n_calls), dtype=np.uint16)
+    rc = lib().coh_gen_records_host(seed, trace0, n_traces, n_calls, n_arrays, adv_per1024, out.ctypes.data)
+    if rc:
+        raise CohError(rc, "coh_gen_records_host")
+    return out
+
+
+def _ptr(x) -> int:
+    """Raw address of a torch tensor / numpy array / int."""
+    if x is None:
+        return 0
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    return x.ctypes.data
+
+
+class Context:
+    """One device context (coh_ctx): compiled call table on the device, launch geometry."""
+
+    def __init__(self, device: int = 0):
+        self._L = lib()
+        h = C.c_void_p()
+        rc = self._L.coh_ctx_create(device, C.byref(h))
+        if rc:
+            raise CohError(rc, f"coh_ctx_create(device={device}) failed (no CUDA device?)")
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.coh_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int, what: str):
+        if rc:
+            msg = self._L.coh_last_error(self._h)
+            raise CohError(rc, f"{what}: {msg.decode() if msg else ''}")
+
+    @property
+    def launch_count(self) -> int:
+        return int(self._L.coh_launch_count(self._h))
+
+    @staticmethod
+    def _batch(records, n_traces, n_calls, n_arrays, fuel, array_bytes):
+        b = _Batch()
+        b.records = _ptr(records)
+        b.n_traces = n_traces
+        b.n_calls = n_calls
+        b.n_arrays = n_arrays
+        b.fuel = fuel
+        b.reserved = 0
+        if array_bytes is not None:
+            ab = np.ascontiguousarray(np.asarray(array_bytes, dtype=np.uint64))
+            b.array_bytes = ab.ctypes.data
+            b._keep = ab
+        else:
+            b.array_bytes = None
+        return b
+
+    def gen_records(self, seed, trace0, n_traces, n_calls, n_arrays, adv_per1024, d_records, stream=0):
+        self._check(
+            self._L.coh_gen_records(self._h, seed, trace0, n_traces, n_calls, n_arrays, adv_per1024, _ptr(d_records), _ptr(stream)),
+            "coh_gen_records",
+        )
+
+    def eval_traces(self, d_records, n_traces, n_calls, n_arrays, fuel, d_results, d_boundary=None, array_bytes=None, stream=0):
+        """Device-buffer entry point (coh_eval_traces); all pointers are device addresses."""
+        b = self._batch(d_records, n_traces, n_calls, n_arrays, fuel, array_bytes)
+        self._check(
+            self._L.coh_eval_traces(self._h, C.byref(b), _ptr(d_results), _ptr(d_boundary), _ptr(stream)),
+            "coh_eval_traces",
+        )
+
+    def eval_traces_host(self, records: np.ndarray, n_traces, n_calls, n_arrays, fuel=10000, array_bytes=None,
+                         results: np.ndarray | None = None, boundary: np.ndarray | None = None, want_boundary=True):
+        """Host-buffer entry point (coh_eval_traces_host): H2D, kernel and D2H inside the call."""
+        if records.dtype != np.uint16 or records.size < records_elems(n_traces, n_calls):
+            raise ValueError("records must be uint16 in the call-major interleaved layout")
+        if results is None:
+            results = np.zeros(n_traces, dtype=RESULT_DTYPE)
+        if boundary is None and want_boundary:
+            boundary = np.zeros(boundary_words(n_calls) * n_traces, dtype=np.uint32)
+        b = self._batch(records, n_traces, n_calls, n_arrays, fuel, array_bytes)
+        self._check(
+            self._L.coh_eval_traces_host(self._h, C.byref(b), _ptr(results), _ptr(boundary) if want_boundary else None),
+            "coh_eval_traces_host",
+        )
+        return results, boundary
+
+    def reduce_counters(self, d_results, n_traces, d_counters, stream=0):
+        self._check(self._L.coh_reduce_counters(self._h, _ptr(d_results), n_traces, _ptr(d_counters), _ptr(stream)),
+                    "coh_reduce_counters")

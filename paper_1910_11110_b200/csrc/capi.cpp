@@ -1,0 +1,278 @@
+// C ABI of the trace evaluator: context, validation, launch geometry, host-buffer
+// pipeline.  The reference equivalent is the by-value C++ API of namespace cohere
+// (semantics.hpp:253 run, modes.hpp:105 run_annotated); errors that the reference
+// throws come back here as status codes + coh_last_error.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "gen_common.h"
+#include "internal.hpp"
+
+struct coh_ctx {
+  int device = 0;
+  std::string err;
+  uint64_t* d_lut = nullptr;
+  uint64_t* d_prog = nullptr;
+  uint64_t* d_bytes = nullptr;
+  int sms = 148;
+  int blocks_per_sm = 1;
+  uint64_t launches = 0;
+  // host-buffer pipeline
+  cudaStream_t hs[2] = {nullptr, nullptr};
+  uint16_t* d_rec[2] = {nullptr, nullptr};
+  coh_trace_result* d_res[2] = {nullptr, nullptr};
+  uint32_t* d_bnd[2] = {nullptr, nullptr};
+  size_t rec_cap = 0, res_cap = 0, bnd_cap = 0;  // bytes per buffer
+};
+
+namespace {
+
+int cuda_fail(coh_ctx* ctx, cudaError_t e, const char* what) {
+  if (ctx) ctx->err = std::string(what) + ": " + cudaGetErrorString(e);
+  return COH_E_CUDA;
+}
+#define COH_CUDA(ctx, call)                                   \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+  } while (0)
+
+int arg_fail(coh_ctx* ctx, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return COH_E_ARG;
+}
+
+int validate(coh_ctx* ctx, const coh_trace_batch* b) {
+  if (!ctx) return COH_E_ARG;
+  if (!b) return arg_fail(ctx, "batch is NULL");
+  if (b->n_arrays < 1 || b->n_arrays > COH_MAX_ARRAYS)
+    return arg_fail(ctx, "n_arrays must be in [1, 64], got " + std::to_string(b->n_arrays));
+  if (b->n_traces && b->n_calls && !b->records) return arg_fail(ctx, "records is NULL");
+  return COH_OK;
+}
+
+// Uniform element sizes let the kernel fold bytes = transfers * size; otherwise the
+// per-array 12-bit transfer counters in shared memory bound the trace length.
+int bytes_mode(coh_ctx* ctx, const coh_trace_batch* b, bool* uniform, uint64_t* ub) {
+  *uniform = true;
+  *ub = 1;
+  if (!b->array_bytes) return COH_OK;
+  *ub = b->array_bytes[0];
+  for (uint32_t a = 1; a < b->n_arrays; ++a)
+    if (b->array_bytes[a] != *ub) *uniform = false;
+  if (!*uniform && (uint64_t)b->n_calls * 2u > 4095u)
+    return arg_fail(ctx, "non-uniform array_bytes supports n_calls <= 2047");
+  return COH_OK;
+}
+
+int eval_device(coh_ctx* ctx, const coh_trace_batch* b, const uint16_t* d_records,
+                uint64_t n_traces, coh_trace_result* d_results, uint32_t* d_boundary,
+                cudaStream_t s) {
+  bool uniform;
+  uint64_t ub;
+  int rc = bytes_mode(ctx, b, &uniform, &ub);
+  if (rc) return rc;
+  if (n_traces == 0) return COH_OK;
+  if (!uniform)
+    COH_CUDA(ctx, cudaMemcpyAsync(ctx->d_bytes, b->array_bytes, sizeof(uint64_t) * b->n_arrays,
+                                  cudaMemcpyHostToDevice, s));
+  cohb::TraceLaunch L;
+  L.records = d_records;
+  L.n_traces = n_traces;
+  L.n_calls = b->n_calls;
+  L.n_arrays = b->n_arrays;
+  L.fuel = b->fuel;
+  // fuel >= 6 steps x n_calls can never run out (max 6 steps per block): drop the check
+  L.check_fuel = (int64_t)b->fuel < 6 * (int64_t)b->n_calls;
+  L.uniform_bytes = uniform;
+  L.bytes_uniform = ub;
+  L.d_array_bytes = ctx->d_bytes;
+  L.d_lut = ctx->d_lut;
+  L.d_prog = ctx->d_prog;
+  L.results = d_results;
+  L.boundary = d_boundary;
+  // persistent grid, equal rounds per block
+  const uint64_t need = (n_traces + 127) / 128;
+  const uint64_t cap = (uint64_t)ctx->sms * (uint64_t)std::max(1, ctx->blocks_per_sm);
+  const uint64_t rounds = (need + cap - 1) / cap;
+  L.grid = (int)((need + rounds - 1) / rounds);
+  std::string err;
+  rc = cohb::launch_trace_eval(L, s, &err);
+  if (rc) {
+    ctx->err = err;
+    return rc;
+  }
+  ctx->launches++;
+  return COH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* coh_version(void) { return "cohere-b200 0.1 (sm_100a)"; }
+
+int coh_ctx_create(int device, coh_ctx** out) {
+  if (!out) return COH_E_ARG;
+  *out = nullptr;
+  coh_ctx* ctx = new coh_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return COH_E_CUDA;
+  }
+  static cohb::CallTable table;  // pure function of the rules; rebuilt per ctx
+  cohb::build_call_table(&table);
+  int rc = COH_OK;
+  do {
+    if ((e = cudaMalloc(&ctx->d_lut, sizeof table.lut)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&ctx->d_prog, sizeof table.prog)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&ctx->d_bytes, sizeof(uint64_t) * COH_MAX_ARRAYS)) != cudaSuccess) break;
+    if ((e = cudaMemcpy(ctx->d_lut, table.lut, sizeof table.lut, cudaMemcpyHostToDevice)) != cudaSuccess) break;
+    if ((e = cudaMemcpy(ctx->d_prog, table.prog, sizeof table.prog, cudaMemcpyHostToDevice)) != cudaSuccess) break;
+    if ((e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess) break;
+    cohb::trace_eval_set_smem_attr();
+    int tpb = 0;
+    std::string err;
+    rc = cohb::trace_eval_occupancy(&ctx->blocks_per_sm, &tpb, COH_MAX_ARRAYS, &err);
+  } while (0);
+  if (e != cudaSuccess || rc != COH_OK) {
+    coh_ctx_destroy(ctx);
+    return COH_E_CUDA;
+  }
+  *out = ctx;
+  return COH_OK;
+}
+
+void coh_ctx_destroy(coh_ctx* ctx) {
+  if (!ctx) return;
+  cudaFree(ctx->d_lut);
+  cudaFree(ctx->d_prog);
+  cudaFree(ctx->d_bytes);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(ctx->d_rec[k]);
+    cudaFree(ctx->d_res[k]);
+    cudaFree(ctx->d_bnd[k]);
+    if (ctx->hs[k]) cudaStreamDestroy(ctx->hs[k]);
+  }
+  delete ctx;
+}
+
+const char* coh_last_error(const coh_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+uint64_t coh_launch_count(const coh_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void* coh_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+  return p;
+}
+void coh_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int coh_gen_records(coh_ctx* ctx, uint64_t seed, uint64_t trace0, uint64_t n_traces,
+                    uint32_t n_calls, uint32_t n_arrays, uint32_t adv_per1024,
+                    uint16_t* d_records, void* stream) {
+  if (!ctx) return COH_E_ARG;
+  if (n_arrays < 1 || n_arrays > COH_MAX_ARRAYS) return arg_fail(ctx, "n_arrays must be in [1, 64]");
+  if (!d_records && n_traces && n_calls) return arg_fail(ctx, "d_records is NULL");
+  std::string err;
+  int rc = cohb::launch_gen_records(seed, trace0, n_traces, n_calls, n_arrays, adv_per1024,
+                                    d_records, stream, &err);
+  if (rc) ctx->err = err;
+  else ctx->launches++;
+  return rc;
+}
+
+int coh_gen_records_host(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
+                         uint32_t n_arrays, uint32_t adv_per1024, uint16_t* h_records) {
+  if (n_arrays < 1 || n_arrays > COH_MAX_ARRAYS) return COH_E_ARG;
+  if (!h_records && n_traces && n_calls) return COH_E_ARG;
+  const uint32_t n_chunks = (n_calls + 7u) / 8u;
+  for (uint32_t c = 0; c < n_chunks; ++c)
+    for (uint64_t t = 0; t < n_traces; ++t)
+      for (uint32_t k = 0; k < 8; ++k) {
+        const uint32_t i = c * 8u + k;
+        h_records[((uint64_t)c * n_traces + t) * 8u + k] =
+            i < n_calls ? coh_gen_record(seed, trace0 + t, i, n_arrays, adv_per1024) : 0;
+      }
+  return COH_OK;
+}
+
+int coh_eval_traces(coh_ctx* ctx, const coh_trace_batch* batch, coh_trace_result* d_results,
+                    uint32_t* d_boundary, void* stream) {
+  int rc = validate(ctx, batch);
+  if (rc) return rc;
+  if (batch->n_traces && !d_results) return arg_fail(ctx, "d_results is NULL");
+  return eval_device(ctx, batch, batch->records, batch->n_traces, d_results, d_boundary,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int coh_eval_traces_host(coh_ctx* ctx, const coh_trace_batch* batch, coh_trace_result* h_results,
+                         uint32_t* h_boundary) {
+  int rc = validate(ctx, batch);
+  if (rc) return rc;
+  const uint64_t n = batch->n_traces;
+  if (n == 0) return COH_OK;
+  if (!h_results) return arg_fail(ctx, "h_results is NULL");
+  const uint32_t n_chunks = (batch->n_calls + 7u) / 8u;
+  const uint32_t n_words = coh_boundary_words(batch->n_calls);
+  // Slices of S traces: H2D of slice k+1 overlaps the kernel and D2H of slice k.
+  uint64_t S = std::min<uint64_t>(n, 1ull << 17);
+  const size_t rec_b = (size_t)n_chunks * 16u * S, res_b = sizeof(coh_trace_result) * S,
+               bnd_b = (size_t)n_words * 4u * S;
+  for (int k = 0; k < 2; ++k) {
+    if (!ctx->hs[k]) COH_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->hs[k], cudaStreamNonBlocking));
+    if (ctx->rec_cap < rec_b) {
+      cudaFree(ctx->d_rec[k]);
+      COH_CUDA(ctx, cudaMalloc(&ctx->d_rec[k], std::max<size_t>(rec_b, 16)));
+    }
+    if (ctx->res_cap < res_b) {
+      cudaFree(ctx->d_res[k]);
+      COH_CUDA(ctx, cudaMalloc(&ctx->d_res[k], res_b));
+    }
+    if (ctx->bnd_cap < bnd_b) {
+      cudaFree(ctx->d_bnd[k]);
+      COH_CUDA(ctx, cudaMalloc(&ctx->d_bnd[k], std::max<size_t>(bnd_b, 4)));
+    }
+  }
+  ctx->rec_cap = std::max(ctx->rec_cap, rec_b);
+  ctx->res_cap = std::max(ctx->res_cap, res_b);
+  ctx->bnd_cap = std::max(ctx->bnd_cap, bnd_b);
+  int k = 0;
+  for (uint64_t t0 = 0; t0 < n; t0 += S, k ^= 1) {
+    const uint64_t m = std::min<uint64_t>(S, n - t0);
+    cudaStream_t s = ctx->hs[k];
+    if (n_chunks)
+      COH_CUDA(ctx, cudaMemcpy2DAsync(ctx->d_rec[k], m * 16u, batch->records + t0 * 8u, n * 16u,
+                                      m * 16u, n_chunks, cudaMemcpyHostToDevice, s));
+    rc = eval_device(ctx, batch, ctx->d_rec[k], m, ctx->d_res[k], h_boundary ? ctx->d_bnd[k] : nullptr, s);
+    if (rc) return rc;
+    COH_CUDA(ctx, cudaMemcpyAsync(h_results + t0, ctx->d_res[k], sizeof(coh_trace_result) * m,
+                                  cudaMemcpyDeviceToHost, s));
+    if (h_boundary && n_words)
+      COH_CUDA(ctx, cudaMemcpy2DAsync(h_boundary + t0, n * 4u, ctx->d_bnd[k], m * 4u, m * 4u,
+                                      n_words, cudaMemcpyDeviceToHost, s));
+  }
+  COH_CUDA(ctx, cudaStreamSynchronize(ctx->hs[0]));
+  COH_CUDA(ctx, cudaStreamSynchronize(ctx->hs[1]));
+  return COH_OK;
+}
+
+int coh_reduce_counters(coh_ctx* ctx, const coh_trace_result* d_results, uint64_t n_traces,
+                        uint64_t* d_counters, void* stream) {
+  if (!ctx) return COH_E_ARG;
+  if (!d_counters) return arg_fail(ctx, "d_counters is NULL");
+  std::string err;
+  int rc = cohb::launch_reduce_counters(d_results, n_traces, d_counters, stream, &err);
+  if (rc) ctx->err = err;
+  else if (n_traces) ctx->launches++;
+  return rc;
+}
+
+}  // extern "C"

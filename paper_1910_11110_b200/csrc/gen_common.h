@@ -1,0 +1,28 @@
+// Counter-based synthetic call generator shared by host (C++) and device (CUDA).
+// Definition: include/cohere_b200.h, "synthetic record generator".
+#pragma once
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define COH_HD __host__ __device__ __forceinline__
+#else
+#define COH_HD static inline
+#endif
+
+COH_HD uint64_t coh_splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+COH_HD uint16_t coh_gen_record(uint64_t seed, uint64_t trace_id, uint32_t call_idx,
+                               uint32_t n_arrays, uint32_t adv_per1024) {
+  const uint64_t h = coh_splitmix64(seed ^ (trace_id << 20) ^ (uint64_t)call_idx);
+  const uint32_t arr = (uint32_t)(((h & 0xFFFFFFFFull) * (uint64_t)n_arrays) >> 32);
+  const uint32_t kind = (uint32_t)((((h >> 32) & 0xFFFFull) * 3ull) >> 16);
+  const uint32_t site = (uint32_t)((h >> 48) & 1ull);
+  const uint32_t adv = ((uint32_t)((h >> 49) & 0x3FFull)) < adv_per1024;
+  const uint32_t var = adv ? 1u + (uint32_t)((((h >> 59) & 0x1Full) * 7ull) >> 5) : 0u;
+  return (uint16_t)(arr | (kind << 6) | (site << 8) | (var << 9));
+}

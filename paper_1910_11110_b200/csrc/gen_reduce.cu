@@ -1,0 +1,103 @@
+// Device-side synthetic record generator (records materialised in HBM)
+// and the per-batch counter reduction that feeds the multi-GPU allreduce (§8(e)).
+#include <cuda_runtime.h>
+
+#include "gen_common.h"
+#include "internal.hpp"
+
+namespace cohb {
+
+// One thread writes one 16-byte chunk (8 calls of one trace): coalesced across the warp.
+__global__ void k_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
+                              uint32_t n_arrays, uint32_t adv, uint4* out) {
+  const uint32_t n_chunks = (n_calls + 7u) / 8u;
+  const uint64_t total = (uint64_t)n_chunks * n_traces;
+  for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = (uint32_t)(idx / n_traces);
+    const uint64_t t = idx - (uint64_t)c * n_traces;
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t i0 = c * 8u + 2u * k, i1 = i0 + 1u;
+      const uint32_t r0 = i0 < n_calls ? coh_gen_record(seed, trace0 + t, i0, n_arrays, adv) : 0u;
+      const uint32_t r1 = i1 < n_calls ? coh_gen_record(seed, trace0 + t, i1, n_arrays, adv) : 0u;
+      w[k] = r0 | (r1 << 16);
+    }
+    out[idx] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+int launch_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
+                       uint32_t n_arrays, uint32_t adv, uint16_t* d_records, void* stream,
+                       std::string* err) {
+  const uint64_t total = (uint64_t)((n_calls + 7u) / 8u) * n_traces;
+  if (total == 0) return COH_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  uint64_t blocks = (total + 255) / 256;
+  const uint64_t cap = (uint64_t)sms * 16;
+  if (blocks > cap) blocks = cap;
+  k_gen_records<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      seed, trace0, n_traces, n_calls, n_arrays, adv, reinterpret_cast<uint4*>(d_records));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("gen_records launch: ") + cudaGetErrorString(e);
+    return COH_E_CUDA;
+  }
+  return COH_OK;
+}
+
+// Counters (include/cohere_b200.h, COH_N_COUNTERS).  Warp shuffle reduce, one atomic
+// per warp per counter.
+__global__ void k_reduce_counters(const coh_trace_result* __restrict__ r, uint64_t n,
+                                  unsigned long long* __restrict__ out) {
+  uint64_t c[COH_N_COUNTERS] = {0};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 q2 = __ldcs(reinterpret_cast<const uint4*>(r + i) + 2);
+    const uint4 q3 = __ldcs(reinterpret_cast<const uint4*>(r + i) + 3);
+    const uint32_t status = q3.w & 0xFFu;
+    c[0] += status == COH_RUN_STUCK;
+    c[1] += status == COH_RUN_FUEL_EXHAUSTED;
+    c[2] += q3.y != 0u;
+    c[3] += status == COH_RUN_DEFECT;
+    c[4] += q2.z;
+    c[5] += q2.w;
+    c[6] += (uint64_t)q2.x | ((uint64_t)q2.y << 32);
+    c[7] += q3.y;
+    c[8] += q3.x;
+    c[9] += 1;
+  }
+#pragma unroll
+  for (int k = 0; k < COH_N_COUNTERS; ++k) {
+    uint64_t v = c[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out + k, (unsigned long long)v);
+  }
+}
+
+int launch_reduce_counters(const coh_trace_result* d_results, uint64_t n_traces,
+                           uint64_t* d_counters, void* stream, std::string* err) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(d_counters, 0, sizeof(uint64_t) * COH_N_COUNTERS, s);
+  if (e == cudaSuccess && n_traces) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    uint64_t blocks = (n_traces + 255) / 256;
+    if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
+    k_reduce_counters<<<(unsigned)blocks, 256, 0, s>>>(
+        d_results, n_traces, reinterpret_cast<unsigned long long*>(d_counters));
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) {
+    *err = std::string("reduce_counters: ") + cudaGetErrorString(e);
+    return COH_E_CUDA;
+  }
+  return COH_OK;
+}
+
+}  // namespace cohb

@@ -1,0 +1,67 @@
+// Internal declarations shared by the host runtime (.cpp) and the CUDA sources (.cu).
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include "cohere_b200.h"
+
+namespace cohb {
+
+// ---- micro-op encoding of one translated block (see coh_calltable_program) ----------
+enum : uint8_t { OP_END = 0, OP_IF_VALID = 1, OP_IF_GVALID = 2, OP_EFFECT = 3 };
+constexpr uint8_t op_effect(uint32_t eff, uint32_t site, uint32_t abstract_target) {
+  return (uint8_t)(OP_EFFECT | (eff << 2) | (site << 5) | (abstract_target << 6));
+}
+// A malformed record (mode kind 3) compiles to this single op.
+constexpr uint8_t OP_DEFECT = 0x80;
+
+constexpr int kCallTypes = 64;   // record bits 6..11
+constexpr int kStates = 16;      // state nibble
+constexpr int kLutEntries = kCallTypes * kStates;
+
+// LUT entry (uint64):
+//   lo32 bits 0-15 : delta added (mod 2^16) to the per-array u16 word
+//                    (bits 0-3 state nibble, bits 4-15 per-array transfer count)
+//   lo32 bit 31    : slow path (stuck / defect) -> exact micro-op replay on device
+//   hi32           : accumulator addend = steps + (viol_delta << 8) + (transfers << 16)
+constexpr uint32_t kSlowBit = 0x80000000u;
+
+struct CallTable {
+  uint64_t lut[kLutEntries];
+  uint64_t prog[kCallTypes];   // 8 micro-ops per type, byte k = op k
+};
+
+// Builds the table by running the restated rules (calltable.cpp).
+void build_call_table(CallTable* t);
+
+// Host restatement used by the compiler: one block from one state.
+coh_call_outcome simulate_block(uint32_t call_type, uint32_t state, int fuel);
+
+// ---- device entry points (defined in .cu files) ------------------------------------
+struct TraceLaunch {
+  const uint16_t* records;
+  uint64_t n_traces;
+  uint32_t n_calls;
+  uint32_t n_arrays;
+  int32_t fuel;
+  bool check_fuel;
+  bool uniform_bytes;
+  uint64_t bytes_uniform;
+  const uint64_t* d_array_bytes;   // device, n_arrays (used when !uniform_bytes)
+  const uint64_t* d_lut;
+  const uint64_t* d_prog;
+  coh_trace_result* results;
+  uint32_t* boundary;
+  int grid;
+};
+int launch_trace_eval(const TraceLaunch& p, void* stream, std::string* err);
+void trace_eval_set_smem_attr();
+int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t n_arrays, std::string* err);
+int launch_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
+                       uint32_t n_arrays, uint32_t adv_per1024, uint16_t* d_records, void* stream,
+                       std::string* err);
+int launch_reduce_counters(const coh_trace_result* d_results, uint64_t n_traces,
+                           uint64_t* d_counters, void* stream, std::string* err);
+
+}  // namespace cohb

@@ -1,0 +1,108 @@
+"""Test-side loader for the CPU oracles (oracle/).  Never imported by the product.
+
+  oracle/_build/libcohere_oracle.so  plain-C restatement (cohere_oracle.c)
+  oracle/_ref/libcohere_ref.so       the unmodified reference headers compiled in place
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from paper_1910_11110_b200._ffi import RESULT_DTYPE, _Outcome, boundary_words, records_elems
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_SO = os.path.join(ROOT, "oracle", "_build", "libcohere_oracle.so")
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "libcohere_ref.so")
+
+_orc = None
+_ref = None
+
+
+def oracle():
+    global _orc
+    if _orc is None:
+        L = C.CDLL(ORACLE_SO)
+        u64, u32, i32, vp = C.c_uint64, C.c_uint32, C.c_int32, C.c_void_p
+        L.orc_apply_cell.restype = C.c_int
+        L.orc_apply_cell.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.orc_leq.restype = C.c_int
+        L.orc_leq.argtypes = [C.c_int, C.c_int]
+        L.orc_call_outcome.restype = C.c_int
+        L.orc_call_outcome.argtypes = [u32, u32, C.POINTER(_Outcome)]
+        L.orc_eval_traces.restype = C.c_int
+        L.orc_eval_traces.argtypes = [vp, u64, u64, u64, u32, u32, i32, vp, vp, vp]
+        L.orc_gen_records.restype = C.c_int
+        L.orc_gen_records.argtypes = [u64, u64, u64, u32, u32, u32, vp]
+        _orc = L
+    return _orc
+
+
+def have_ref() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def reference():
+    global _ref
+    if _ref is None:
+        L = C.CDLL(REF_SO)
+        u64, u32, i32, vp = C.c_uint64, C.c_uint32, C.c_int32, C.c_void_p
+        L.ref_eval_traces.restype = C.c_int
+        L.ref_eval_traces.argtypes = [vp, u64, u64, u64, u32, u32, i32, vp, vp, vp, C.c_int, C.c_int]
+        L.ref_call_outcome.restype = C.c_int
+        L.ref_call_outcome.argtypes = [u32, u32, C.POINTER(_Outcome)]
+        L.ref_selfcheck.restype = C.c_int
+        L.ref_selfcheck.argtypes = [vp, u64, u32, u32, i32]
+        _ref = L
+    return _ref
+
+
+def _ab(array_bytes):
+    if array_bytes is None:
+        return None, None
+    a = np.ascontiguousarray(np.asarray(array_bytes, dtype=np.uint64))
+    return a, a.ctypes.data
+
+
+def orc_eval(records, n_total, n_calls, n_arrays, fuel=10000, array_bytes=None, t_begin=0, t_end=None):
+    t_end = n_total if t_end is None else t_end
+    m = t_end - t_begin
+    out = np.zeros(m, dtype=RESULT_DTYPE)
+    bnd = np.zeros(boundary_words(n_calls) * m, dtype=np.uint32)
+    keep, abp = _ab(array_bytes)
+    rc = oracle().orc_eval_traces(records.ctypes.data, n_total, t_begin, t_end, n_calls, n_arrays, fuel, abp,
+                                  out.ctypes.data, bnd.ctypes.data)
+    assert rc == 0
+    return out, bnd
+
+
+def ref_eval(records, n_total, n_calls, n_arrays, fuel=10000, array_bytes=None, t_begin=0, t_end=None,
+             threads=None, mode=0):
+    t_end = n_total if t_end is None else t_end
+    m = t_end - t_begin
+    out = np.zeros(m, dtype=RESULT_DTYPE)
+    bnd = np.zeros(boundary_words(n_calls) * m, dtype=np.uint32)
+    keep, abp = _ab(array_bytes)
+    rc = reference().ref_eval_traces(records.ctypes.data, n_total, t_begin, t_end, n_calls, n_arrays, fuel, abp,
+                                     out.ctypes.data, bnd.ctypes.data, threads or os.cpu_count(), mode)
+    assert rc == 0
+    return out, bnd
+
+
+def orc_outcome(call_type, state):
+    o = _Outcome()
+    oracle().orc_call_outcome(call_type, state, C.byref(o))
+    return o.as_dict()
+
+
+def ref_outcome(call_type, state):
+    o = _Outcome()
+    reference().ref_call_outcome(call_type, state, C.byref(o))
+    return o.as_dict()
+
+
+def orc_gen(seed, trace0, n_traces, n_calls, n_arrays, adv):
+    out = np.zeros(records_elems(n_traces, n_calls), dtype=np.uint16)
+    oracle().orc_gen_records(seed, trace0, n_traces, n_calls, n_arrays, adv, out.ctypes.data)
+    return out

@@ -1,0 +1,102 @@
+"""CPU tests of the C ABI: the library loads, exports every symbol declared in include/*.h,
+the host-side compiler/generator agree with the reference, and device calls fail loudly
+(never silently on the CPU) when no GPU is present."""
+import ctypes
+import glob
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_1910_11110_b200 as coh
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"^\s*(?!static)[A-Za-z_][\w\s\*]*?\b(coh_\w+)\s*\(", src, flags=re.M):
+            names.add(m.group(1))
+    return names
+
+
+def test_header_symbols_exported():
+    names = declared_functions()
+    assert {"coh_eval_traces", "coh_eval_traces_host", "coh_ctx_create", "coh_gen_records"} <= names
+    L = ctypes.CDLL(coh.lib_path)
+    missing = [n for n in sorted(names) if not hasattr(L, n)]
+    assert not missing, missing
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", coh.lib_path], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_product_does_not_reference_oracle():
+    # the product never links, loads or names the CPU oracles (no CPU fallback path)
+    banned = ("libcohere_oracle", "libcohere_ref", "oracle_ffi", "orc_eval", "ref_eval")
+    for p in glob.glob(os.path.join(ROOT, "paper_1910_11110_b200", "**", "*"), recursive=True):
+        if p.endswith((".py", ".cpp", ".cu", ".h", ".hpp")):
+            src = open(p, errors="ignore").read()
+            assert not any(b in src for b in banned), p
+    blob = open(coh.lib_path, "rb").read()
+    assert not any(b.encode() in blob for b in banned)
+
+
+def test_calltable_program_renders_reference_translation():
+    # proj/tests/test_modes.cpp:28-39 "the six mode clauses produce exactly these cores",
+    # rendered from the product's compiled micro-ops (+ the canonical body for variant 0 is
+    # dropped by rendering only the mode part).
+    want = {
+        (0, 0): "if (valid(x^)) { } else { pull x; pull x^; }",
+        (0, 1): "if (gvalid(x^)) { } else { push x; push x^; }",
+        (2, 0): "if (valid(x^)) { } else { pull x; pull x^; } w x^;",
+        (2, 1): "if (gvalid(x^)) { } else { push x; push x^; } gw x^;",
+        (1, 0): "w x^;",
+        (1, 1): "gw x^;",
+    }
+    names = {0: "push", 1: "pull", 2: "r", 3: "w", 4: "noop"}
+    for (kind, site), text in want.items():
+        ops = coh.calltable_program(kind | (site << 2) | (1 << 3))  # variant 1 = empty body
+        parts, k = [], 0
+        while k < len(ops):
+            op = ops[k]
+            if op & 3 in (1, 2):
+                cond = "valid" if op & 3 == 1 else "gvalid"
+                e1, e2 = ops[k + 1], ops[k + 2]
+                def eff(o):
+                    return ("g" if (o >> 5) & 1 else "") + names[(o >> 2) & 7] + " x" + ("^" if (o >> 6) & 1 else "") + ";"
+                parts.append(f"if ({cond}(x^)) {{ }} else {{ {eff(e1)} {eff(e2)} }}")
+                k += 3
+            else:
+                parts.append(("g" if (op >> 5) & 1 else "") + names[(op >> 2) & 7] + " x" + ("^" if (op >> 6) & 1 else "") + ";")
+                k += 1
+        assert " ".join(parts) == text
+
+
+def test_host_generator_distribution():
+    recs = coh.gen_records_host(1, 0, 4096, 256, 64, 1)
+    arr = recs & 63
+    kind = (recs >> 6) & 3
+    var = (recs >> 9) & 7
+    assert np.bincount(arr, minlength=64).min() > 0.8 * recs.size / 64
+    assert set(np.unique(kind)) == {0, 1, 2}
+    frac_adv = (var != 0).mean()
+    assert 0.0005 < frac_adv < 0.0015  # adv_per1024 = 1
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(coh.CohError):
+        coh.Context(0)

@@ -1,0 +1,185 @@
+"""GPU parity tests for the trace_eval kernel: bit-exact against the reference's golden
+fixtures, the C oracle and (when oracle/_ref traveled) the live reference."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle_ffi as o
+import paper_1910_11110_b200 as coh
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def dev_eval(ctx, recs_np, nt, nc, na, fuel, array_bytes=None):
+    d_rec = torch.from_numpy(recs_np.view(np.int16).copy()).cuda()
+    d_res = torch.empty(max(nt, 1) * 64, dtype=torch.uint8, device="cuda")
+    d_bnd = torch.empty(max(coh.boundary_words(nc) * nt, 1), dtype=torch.int32, device="cuda")
+    ctx.eval_traces(d_rec, nt, nc, na, fuel, d_res, d_bnd, array_bytes=array_bytes,
+                    stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    res = d_res.cpu().numpy()[: nt * 64].view(coh.RESULT_DTYPE)
+    bnd = d_bnd.cpu().numpy()[: coh.boundary_words(nc) * nt].view(np.uint32)
+    return res, bnd
+
+
+def same(a, b):
+    return np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+def first_diff(a, b):
+    idx = np.nonzero((a.view(np.uint8).reshape(-1, 64) != b.view(np.uint8).reshape(-1, 64)).any(1))[0]
+    if not len(idx):
+        return None
+    i = idx[0]
+    return i, a[i], b[i]
+
+
+def golden():
+    z = np.load(os.path.join(GOLDEN, "traces.npz"))
+    for name in sorted({k.split(".")[0] for k in z.files}):
+        seed, trace0, nt, nc, na, adv, fuel = (int(x) for x in z[f"{name}.params"])
+        ab = z[f"{name}.array_bytes"]
+        yield name, z[f"{name}.records"], nt, nc, na, fuel, (ab if ab.size else None), \
+            z[f"{name}.results"].view(coh.RESULT_DTYPE), z[f"{name}.boundary"]
+
+
+def test_golden_device_entry(ctx):
+    for name, recs, nt, nc, na, fuel, ab, want, want_b in golden():
+        res, bnd = dev_eval(ctx, recs, nt, nc, na, fuel, ab)
+        assert same(res, want), (name, first_diff(res, want))
+        assert np.array_equal(bnd, want_b), name
+
+
+def test_golden_host_entry(ctx):
+    for name, recs, nt, nc, na, fuel, ab, want, want_b in golden():
+        res, bnd = ctx.eval_traces_host(recs, nt, nc, na, fuel, ab)
+        assert same(res, want), (name, first_diff(res, want))
+        assert np.array_equal(bnd, want_b), name
+
+
+def test_golden_reads_like_reference(ctx):
+    # c1_canonical: one array, 1000 canonical calls -> Done, every boundary OK
+    # (Theorems 1-2); the stuck cases describe() like StuckInfo.
+    for name, recs, nt, nc, na, fuel, ab, want, want_b in golden():
+        res, bnd = dev_eval(ctx, recs, nt, nc, na, fuel, ab)
+        if name == "c1_canonical":
+            run = coh.annotated_run(res, bnd, 0, nt, na)
+            assert run.status == "done" and len(run.boundary_ok) == 1000 and all(run.boundary_ok)
+        if name == "c2_adversarial":
+            stuck = [coh.annotated_run(res, bnd, t, nt, na) for t in range(nt)]
+            texts = {r.stuck.describe() for r in stuck if r.stuck}
+            assert any(t.startswith("gr ") and t.endswith("against the swapped pair") for t in texts)
+            assert any(t.startswith("r ") and "need (V,*)" in t for t in texts)
+
+
+def test_device_generator_matches_host(ctx):
+    for seed, trace0, nt, nc, na, adv in [(1, 0, 3000, 256, 64, 1), (9, 77, 1001, 37, 5, 500), (3, 0, 17, 1, 1, 1024)]:
+        d = torch.empty(coh.records_elems(nt, nc), dtype=torch.int16, device="cuda")
+        ctx.gen_records(seed, trace0, nt, nc, na, adv, d, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(d.cpu().numpy().view(np.uint16), coh.gen_records_host(seed, trace0, nt, nc, na, adv))
+
+
+CONFIGS = [
+    # (seed, n_traces, n_calls, n_arrays, adv_per1024, fuel, array_bytes)
+    (21, 20000, 256, 64, 1, 10000, None),
+    (22, 20000, 256, 64, 16, 10000, None),
+    (23, 5000, 256, 64, 4, 700, None),          # fuel runs out mid-trace (check_fuel path)
+    (24, 4000, 1000, 1, 8, 10000, None),
+    (25, 6000, 33, 2, 60, 10000, None),
+    (26, 6000, 31, 63, 30, 10000, None),
+    (27, 3000, 7, 5, 300, 10000, None),
+    (28, 3000, 1, 1, 1024, 10000, None),
+    (29, 7000, 256, 64, 3, 10000, list(range(1, 65))),     # non-uniform bytes
+    (30, 7000, 200, 33, 3, 500, [4096] * 33),              # uniform, scaled bytes, fuel
+    (31, 1000, 64, 64, 1024, 10000, None),                 # all adversarial
+    (32, 129, 2047, 3, 2, 20000, [8, 16, 24]),             # max length for non-uniform
+    (33, 1000, 96, 64, 0, 1, None),                        # fuel 1
+    (34, 1000, 96, 64, 0, 0, None),                        # fuel 0
+]
+
+
+@pytest.mark.parametrize("cfg", CONFIGS, ids=[f"s{c[0]}" for c in CONFIGS])
+def test_kernel_vs_oracle(ctx, cfg):
+    seed, nt, nc, na, adv, fuel, ab = cfg
+    recs = coh.gen_records_host(seed, 0, nt, nc, na, adv)
+    res, bnd = dev_eval(ctx, recs, nt, nc, na, fuel, ab)
+    want, want_b = o.orc_eval(recs, nt, nc, na, fuel, ab)
+    assert same(res, want), first_diff(res, want)
+    assert np.array_equal(bnd, want_b)
+
+
+def test_defect_records(ctx):
+    recs = np.zeros(coh.records_elems(2, 8), dtype=np.uint16)
+    recs[0:8] = [0, 0, 3 << 6, 0, 0, 0, 0, 0]
+    recs[8:16] = [0, 1, 2, 5, 0, 0, 0, 0]
+    res, bnd = dev_eval(ctx, recs, 2, 8, 4, 10000)
+    want, want_b = o.orc_eval(recs, 2, 8, 4)
+    assert same(res, want) and np.array_equal(bnd, want_b)
+    assert res["status"].tolist() == [3, 3]
+
+
+def test_argument_errors(ctx):
+    with pytest.raises(coh.CohError):
+        ctx.eval_traces(0, 10, 8, 65, 100, 0)
+    with pytest.raises(coh.CohError):
+        ctx.eval_traces(0, 10, 4096, 3, 100, 0, array_bytes=[1, 2, 3])
+
+
+@pytest.mark.skipif(not o.have_ref(), reason="oracle/_ref not shipped")
+def test_kernel_vs_live_reference_sample(ctx):
+    nt, nc, na = 512, 256, 64
+    recs = coh.gen_records_host(1, 0, nt, nc, na, 8)
+    res, bnd = dev_eval(ctx, recs, nt, nc, na, 10000)
+    want, want_b = o.ref_eval(recs, nt, nc, na, 10000)
+    assert same(res, want), first_diff(res, want)
+    assert np.array_equal(bnd, want_b)
+
+
+def test_full_size_c2_properties(ctx):
+    """BASELINE config 2 at full size (1M traces x 64 arrays x 256 calls): oracle on a
+    sample of trace ids, counters == sum of per-trace fields, determinism, and shard
+    invariance (the same ids evaluated as 4 contiguous shards give identical bytes)."""
+    N, nc, na, adv, seed = 1 << 20, 256, 64, 1, 1
+    s = torch.cuda.current_stream().cuda_stream
+    d_rec = torch.empty(coh.records_elems(N, nc), dtype=torch.int16, device="cuda")
+    ctx.gen_records(seed, 0, N, nc, na, adv, d_rec, s)
+    d_res = torch.empty(N * 64, dtype=torch.uint8, device="cuda")
+    d_bnd = torch.empty(coh.boundary_words(nc) * N, dtype=torch.int32, device="cuda")
+    ctx.eval_traces(d_rec, N, nc, na, 10000, d_res, d_bnd, stream=s)
+    d_cnt = torch.zeros(16, dtype=torch.int64, device="cuda")
+    ctx.reduce_counters(d_res, N, d_cnt, s)
+    torch.cuda.synchronize()
+    res = d_res.cpu().numpy().view(coh.RESULT_DTYPE)
+    bnd = d_bnd.cpu().numpy().view(np.uint32)
+    cnt = d_cnt.cpu().numpy().view(np.uint64)[:10]
+    # counters
+    st = res["status"]
+    assert cnt[0] == (st == 1).sum() and cnt[1] == (st == 2).sum() and cnt[3] == (st == 3).sum()
+    assert cnt[4] == res["steps"].astype(np.uint64).sum() and cnt[5] == res["transfers"].astype(np.uint64).sum()
+    assert cnt[7] == res["violations"].astype(np.uint64).sum() and cnt[8] == res["calls_done"].astype(np.uint64).sum()
+    assert cnt[9] == N
+    # sample vs oracle (every 997th id, generated per id on the host)
+    ids = np.arange(0, N, 997)
+    for t in ids[:600]:
+        r1 = coh.gen_records_host(seed, int(t), 1, nc, na, adv)
+        w, wb = o.orc_eval(r1, 1, nc, na, 10000)
+        assert same(res[t:t + 1], w), (t, first_diff(res[t:t + 1], w))
+        assert np.array_equal(bnd[t::N], wb), t
+    # determinism
+    h1 = torch.sum(d_res.view(torch.int64)).item()
+    ctx.eval_traces(d_rec, N, nc, na, 10000, d_res, d_bnd, stream=s)
+    torch.cuda.synchronize()
+    assert torch.sum(d_res.view(torch.int64)).item() == h1
+    # shard invariance: 4 contiguous shards generated from (seed, trace0)
+    shard = N // 4
+    for k in range(4):
+        r = torch.empty(coh.records_elems(shard, nc), dtype=torch.int16, device="cuda")
+        ctx.gen_records(seed, k * shard, shard, nc, na, adv, r, s)
+        o_res = torch.empty(shard * 64, dtype=torch.uint8, device="cuda")
+        ctx.eval_traces(r, shard, nc, na, 10000, o_res, None, stream=s)
+        torch.cuda.synchronize()
+        assert torch.equal(o_res, d_res[k * shard * 64:(k + 1) * shard * 64]), k
