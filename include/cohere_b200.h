@@ -73,10 +73,11 @@ enum { COH_KEY_CONCRETE = 0, COH_KEY_ABSTRACT = 1 }; /* VarKey::Kind Scalar / Ab
 
 /* Per-trace result: 64 bytes.  Replaces AnnotatedRun{status, store, stuck, boundary_ok,
  * steps, ...} (modes.hpp:95-103) plus the transfer accounting the reference lacks
- * (SURVEY §8(d) "transfer accounting rule").  Planes: bit a = array a is Valid. */
+ * (SURVEY §8(d) "transfer accounting rule").  state: the final store, one nibble per
+ * array a at state[a / 8] >> (4 * (a % 8)): bit0 store.at(scalar(a)).local == V,
+ * bit1 .remote == V, bit2 store.at(abstract(a)).local == V, bit3 .remote == V. */
 typedef struct coh_trace_result {
-  uint64_t cl, cr;          /* concrete store:  store.at(scalar(a)).local/.remote     */
-  uint64_t al, ar;          /* abstract store:  store.at(abstract(a)).local/.remote   */
+  uint32_t state[8];        /* nibble-packed final store (arrays >= n_arrays: 0)      */
   uint64_t transfer_bytes;  /* sum over executed concrete push/pull of array_bytes[a] */
   uint32_t steps;           /* AnnotatedRun::steps                                    */
   uint32_t transfers;       /* executed concrete Push/Pull steps                      */
@@ -89,6 +90,10 @@ typedef struct coh_trace_result {
   uint8_t stuck_flags;      /* bit0 StuckInfo::site, bit1 key kind (COH_KEY_*),
                                bits2-3 StuckInfo::actual (bit2 local V, bit3 remote V)  */
 } coh_trace_result;
+
+static inline uint32_t coh_result_nibble(const coh_trace_result* r, uint32_t a) {
+  return (r->state[a >> 3] >> (4u * (a & 7u))) & 15u;
+}
 
 typedef struct coh_trace_batch {
   const uint16_t* records;     /* device, layout above                                 */

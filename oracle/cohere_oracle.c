@@ -191,12 +191,8 @@ int orc_eval_traces(const uint16_t* records, uint64_t n_total, uint64_t t_begin,
     }
     r->status = (uint8_t)status;
     r->steps = (uint32_t)steps;
-    for (uint32_t a = 0; a < n_arrays; ++a) {
-      r->cl |= (uint64_t)(conc[a] & 1) << a;
-      r->cr |= (uint64_t)((conc[a] >> 1) & 1) << a;
-      r->al |= (uint64_t)(abst[a] & 1) << a;
-      r->ar |= (uint64_t)((abst[a] >> 1) & 1) << a;
-    }
+    for (uint32_t a = 0; a < n_arrays; ++a)
+      r->state[a / 8] |= (uint32_t)(conc[a] | (abst[a] << 2)) << (4 * (a % 8));
   }
   return 0;
 }

@@ -155,10 +155,7 @@ void eval_one(const uint16_t* recs, uint64_t n_total, uint64_t t, uint32_t n_cal
   for (uint32_t a = 0; a < n_arrays; ++a) {
     const uint32_t c = pair_bits(store.at(VarKey::scalar(array_names()[a])));
     const uint32_t ab = pair_bits(store.at(VarKey::abstract(array_names()[a])));
-    r.cl |= (uint64_t)(c & 1u) << a;
-    r.cr |= (uint64_t)((c >> 1) & 1u) << a;
-    r.al |= (uint64_t)(ab & 1u) << a;
-    r.ar |= (uint64_t)((ab >> 1) & 1u) << a;
+    r.state[a / 8] |= (c | (ab << 2)) << (4 * (a % 8));
   }
 }
 

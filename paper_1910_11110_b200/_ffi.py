@@ -22,10 +22,7 @@ _ERR_NAMES = {
 # struct coh_trace_result (64 bytes)
 RESULT_DTYPE = np.dtype(
     [
-        ("cl", "<u8"),
-        ("cr", "<u8"),
-        ("al", "<u8"),
-        ("ar", "<u8"),
+        ("state", "<u4", (8,)),
         ("transfer_bytes", "<u8"),
         ("steps", "<u4"),
         ("transfers", "<u4"),

@@ -154,14 +154,13 @@ void build_call_table(CallTable* t) {
       const coh_call_outcome o = simulate_block(type, s, 1 << 30);
       uint32_t lo, hi;
       if (o.status != COH_RUN_DONE) {
-        lo = kSlowBit;
+        lo = kSlowAddend;
         hi = 0;
       } else {
-        lo = ((uint32_t)((int)o.state_after - (int)s) + ((uint32_t)o.transfers << 4)) & 0xFFFFu;
-        hi = (uint32_t)o.steps + (uint32_t)(((int)o.viol_after - (int)o.viol_before) * 256) +
-             ((uint32_t)o.transfers << 16);
+        lo = ((uint32_t)o.steps + (uint32_t)(((int)o.viol_after - (int)o.viol_before) * 256)) & 0xFFFFu;
+        hi = (uint32_t)((((int)o.state_after - (int)s) << kStateShift) + ((int)o.transfers << kCountShift)) & 0xFFFFu;
       }
-      t->lut[type * kStates + s] = (uint64_t)lo | ((uint64_t)hi << 32);
+      t->lut[lut_slot(type, s)] = lo | (hi << 16);
     }
   }
 }

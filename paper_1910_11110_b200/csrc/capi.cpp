@@ -14,7 +14,7 @@
 struct coh_ctx {
   int device = 0;
   std::string err;
-  uint64_t* d_lut = nullptr;
+  uint32_t* d_lut = nullptr;
   uint64_t* d_prog = nullptr;
   uint64_t* d_bytes = nullptr;
   int sms = 148;
@@ -54,8 +54,8 @@ int validate(coh_ctx* ctx, const coh_trace_batch* b) {
   return COH_OK;
 }
 
-// Uniform element sizes let the kernel fold bytes = transfers * size; otherwise the
-// per-array 12-bit transfer counters in shared memory bound the trace length.
+// Uniform element sizes let the kernel fold bytes = transfers * size; otherwise it sums
+// the per-array transfer counters (26-bit) times the per-array sizes.
 int bytes_mode(coh_ctx* ctx, const coh_trace_batch* b, bool* uniform, uint64_t* ub) {
   *uniform = true;
   *ub = 1;
@@ -63,8 +63,8 @@ int bytes_mode(coh_ctx* ctx, const coh_trace_batch* b, bool* uniform, uint64_t* 
   *ub = b->array_bytes[0];
   for (uint32_t a = 1; a < b->n_arrays; ++a)
     if (b->array_bytes[a] != *ub) *uniform = false;
-  if (!*uniform && (uint64_t)b->n_calls * 2u > 4095u)
-    return arg_fail(ctx, "non-uniform array_bytes supports n_calls <= 2047");
+  if (!*uniform && (uint64_t)b->n_calls * 2u >= (1u << 26))
+    return arg_fail(ctx, "non-uniform array_bytes supports n_calls < 2^25");
   return COH_OK;
 }
 

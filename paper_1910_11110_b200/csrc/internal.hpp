@@ -20,15 +20,21 @@ constexpr int kCallTypes = 64;   // record bits 6..11
 constexpr int kStates = 16;      // state nibble
 constexpr int kLutEntries = kCallTypes * kStates;
 
-// LUT entry (uint64):
-//   lo32 bits 0-15 : delta added (mod 2^16) to the per-array u16 word
-//                    (bits 0-3 state nibble, bits 4-15 per-array transfer count)
-//   lo32 bit 31    : slow path (stuck / defect) -> exact micro-op replay on device
-//   hi32           : accumulator addend = steps + (viol_delta << 8) + (transfers << 16)
-constexpr uint32_t kSlowBit = 0x80000000u;
+// State word in shared memory (one u32 per array per trace):
+//   bits kStateShift..+3 : state nibble (bit0 cl, bit1 cr, bit2 al, bit3 ar)
+//   bits kCountShift..31 : executed concrete push/pull on this array (transfers)
+constexpr uint32_t kStateShift = 2;
+constexpr uint32_t kCountShift = 6;
+
+// LUT entry (uint32), stored at slot = type*16 + (state ^ (type & 15)) (bank swizzle):
+//   lo16 : accumulator addend = steps + viol_delta * 256   (mod 2^16)
+//          or kSlowAddend for a (type, state) that gets stuck / is malformed
+//   hi16 : signed delta of the state word = ((ns - s) << kStateShift) + (tr << kCountShift)
+constexpr uint32_t kSlowAddend = 0x8000u;
+constexpr uint32_t lut_slot(uint32_t type, uint32_t state) { return type * 16u + (state ^ (type & 15u)); }
 
 struct CallTable {
-  uint64_t lut[kLutEntries];
+  uint32_t lut[kLutEntries];
   uint64_t prog[kCallTypes];   // 8 micro-ops per type, byte k = op k
 };
 
@@ -49,7 +55,7 @@ struct TraceLaunch {
   bool uniform_bytes;
   uint64_t bytes_uniform;
   const uint64_t* d_array_bytes;   // device, n_arrays (used when !uniform_bytes)
-  const uint64_t* d_lut;
+  const uint32_t* d_lut;
   const uint64_t* d_prog;
   coh_trace_result* results;
   uint32_t* boundary;

@@ -4,25 +4,37 @@
 // shared fuel + abstraction_correct (modes.hpp:79-90).
 //
 // Layout:
-//   * per-thread store: one u16 word per array in shared memory, column-interleaved
-//     s_st[a][tid] (bank = tid mod 32 -> conflict-free for any array ids in a warp);
-//     bits 0-3 = state nibble (cl, cr, al, ar), bits 4-15 = per-array transfer count.
-//   * call table: 64 call types x 16 states of uint64 in shared memory (8 KB), compiled
-//     on the host by calltable.cpp from the restated rules.
-//   * records: call-major interleaved, 128-bit streaming loads of 8 calls, 32 calls
-//     (4 loads) prefetched one group ahead.
-//   * accumulator register: steps (bits 0-7, flushed every 32 calls), count of arrays
-//     whose abstraction is currently violated (bits 8-15; boundary_ok <=> zero),
-//     transfers (bits 16-22, flushed every 32 calls).
-//   * stuck / fuel / malformed calls leave the fast path and replay the call's micro-ops
-//     exactly (slow_call), which yields StuckInfo and the partial state.
+//   * per-thread store: one u32 word per array in shared memory, column-interleaved
+//     s_st[a][tid] (bank = tid mod 32: conflict-free whatever arrays a warp touches);
+//     bits 2-5 = state nibble (cl, cr, al, ar), bits 6-31 = per-array transfer count.
+//   * call table (calltable.cpp): 64 call types x 16 states of u32, XOR-swizzled
+//     (slot = type*16 + (state ^ (type & 15))) so the common (type, state) pairs of a
+//     warp land in distinct banks; lo16 = accumulator addend, hi16 = signed delta of
+//     the state word.
+//   * records: call-major interleaved, 128-bit streaming loads of 8 calls, a ring of
+//     4 loads (32 calls) in flight per thread.
+//   * accumulator: bits 0-7 steps since the last flush (flushed every 32 calls),
+//     bits 8-15 number of arrays whose abstraction is currently violated (boundary_ok
+//     <=> zero), bit 15 poisoned by slow entries (stuck / defect).
+//   * slow calls (stuck, fuel, malformed) replay the call's micro-ops exactly
+//     (slow_call) after leaving the unrolled loop; they yield StuckInfo + partial state.
 #include <cuda_runtime.h>
 
 #include "internal.hpp"
 
 namespace cohb {
 
-constexpr int kNT = 128;  // threads (traces in flight) per block
+constexpr int kNT = 128;  // traces (threads) per block
+
+// One static shared block so every access is [register + compile-time symbol offset]:
+//   words [0, 1024)            call table (4 KB)
+//   words [1024, 1024 + 64*NT) per-trace stores, s_st[a][tid] (32 KB)
+//   then 64 x u64              per-array sizes (non-uniform bytes only)
+constexpr int kStOff = kLutEntries;
+__shared__ __align__(16) uint32_t s_mem[kLutEntries + COH_MAX_ARRAYS * kNT + 2 * COH_MAX_ARRAYS];
+#define s_lut (s_mem)
+#define s_st (s_mem + kStOff)
+#define s_bytes (reinterpret_cast<uint64_t*>(s_mem + kStOff + COH_MAX_ARRAYS * kNT))
 
 struct KParams {
   const uint4* rec;
@@ -33,25 +45,24 @@ struct KParams {
   uint32_t pad;
   uint64_t bytes_uniform;
   const uint64_t* array_bytes;
-  const uint64_t* lut;
+  const uint32_t* lut;
   const uint64_t* prog;
   coh_trace_result* res;
   uint32_t* bnd;
 };
 
 struct SlowOut {
-  uint32_t status, word, steps, transfers, effect, flags;
+  uint32_t status, word, steps, effect, flags;
 };
 
-// Exact replay of one block's micro-ops from `state` with `rem` fuel left
-// (semantics.hpp:253-287: Done before fuel; Stuck consumes no step).
+// Exact replay of one block's micro-ops from the state word `old_word` with `rem` fuel
+// left (semantics.hpp:253-287: Done before fuel; Stuck consumes no step, store kept).
 __device__ __noinline__ void slow_call(uint64_t prog, uint32_t old_word, int rem, SlowOut* o) {
-  uint32_t s = old_word & 15u;
+  uint32_t s = (old_word >> kStateShift) & 15u;
   uint32_t steps = 0, tr = 0, status = COH_RUN_DONE, eff_out = 0, flags = 0;
-  int k = 0;
-  while (true) {
+  for (int k = 0; k < 8;) {
     const uint32_t op = (uint32_t)(prog >> (8 * k)) & 0xFFu;
-    if (k >= 8 || op == OP_END) break;
+    if (op == OP_END) break;
     if (op == OP_DEFECT) { status = COH_RUN_DEFECT; break; }  // construction defect first
     if ((int)steps >= rem) { status = COH_RUN_FUEL_EXHAUSTED; break; }
     const uint32_t kop = op & 3u;
@@ -64,13 +75,13 @@ __device__ __noinline__ void slow_call(uint64_t prog, uint32_t old_word, int rem
     const uint32_t eff = (op >> 2) & 7u, site = (op >> 5) & 1u, abs_t = (op >> 6) & 1u;
     const uint32_t sh = abs_t ? 2u : 0u;
     const uint32_t before = (s >> sh) & 3u;
-    uint32_t q = site ? (((before & 1u) << 1) | (before >> 1)) : before;  // swap if remote
+    uint32_t q = site ? (((before & 1u) << 1) | (before >> 1)) : before;  // swapped(before)
     int after;
     switch (eff) {
-      case COH_PUSH: after = (q & 1u) ? 3 : -1; break;
-      case COH_PULL: after = (q & 2u) ? 3 : -1; break;
+      case COH_PUSH: after = (q & 1u) ? 3 : -1; break;   // (V,X) -> (V,V)
+      case COH_PULL: after = (q & 2u) ? 3 : -1; break;   // (X,V) -> (V,V)
       case COH_READ: after = (q & 1u) ? (int)q : -1; break;
-      case COH_WRITE: after = 1; break;
+      case COH_WRITE: after = 1; break;                  // (X,Y) -> (V,I)
       default: after = (int)q; break;
     }
     if (after < 0) {
@@ -87,15 +98,32 @@ __device__ __noinline__ void slow_call(uint64_t prog, uint32_t old_word, int rem
     ++k;
   }
   o->status = status;
-  o->word = (old_word & ~15u) + (tr << 4) + s;
+  o->word = (old_word & ~(15u << kStateShift)) + (tr << kCountShift) + (s << kStateShift);
   o->steps = steps;
-  o->transfers = tr;
   o->effect = eff_out;
   o->flags = flags;
 }
 
+__device__ __forceinline__ uint32_t lds(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// bnd = 2*bnd + (acc & 0xFF00 != 0): the carry of (x + 0xFFFFFFFF) is (x != 0).
+__device__ __forceinline__ uint32_t shift_in_violation(uint32_t bnd, uint32_t acc) {
+  uint32_t out;
+  asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, 0xFFFFFFFF;\n\taddc.u32 %0, %2, %2;\n\t}"
+      : "=r"(out)
+      : "r"(acc & 0xFF00u), "r"(bnd));
+  return out;
+}
+
 // FLAGS: kFuel = fuel may run out (fuel < 6 x n_calls), kBytes = non-uniform array
-// sizes (per-array transfer counters), kArr = n_arrays < 64 (range-check array ids).
+// sizes, kArr = n_arrays < 64 (range-check array ids).
 enum : int { kFuel = 1, kBytes = 2, kArr = 4 };
 
 template <int FLAGS>
@@ -103,21 +131,21 @@ __global__ void __launch_bounds__(kNT) k_trace_eval(const KParams p) {
   constexpr bool CHECK_FUEL = FLAGS & kFuel;
   constexpr bool UNIFORM = !(FLAGS & kBytes);
   constexpr bool CHECK_ARR = FLAGS & kArr;
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint64_t* s_lut = reinterpret_cast<uint64_t*>(smem);   // 1024 entries
-  uint64_t* s_bytes = s_lut + kLutEntries;                // 64 entries
-  uint16_t* s_st = reinterpret_cast<uint16_t*>(s_bytes + COH_MAX_ARRAYS);
   const int tid = threadIdx.x;
   for (int i = tid; i < kLutEntries; i += kNT) s_lut[i] = p.lut[i];
   if (!UNIFORM)
     for (int i = tid; i < COH_MAX_ARRAYS; i += kNT)
       s_bytes[i] = i < (int)p.n_arrays ? p.array_bytes[i] : 0ull;
-  uint16_t* col = s_st + tid;  // this thread's column: col[a * kNT], all 64 arrays
-  for (uint32_t a = 0; a < COH_MAX_ARRAYS; ++a) col[a * kNT] = (uint16_t)COH_STATE_INITIAL;
+  constexpr uint32_t kInit = COH_STATE_INITIAL << kStateShift;
+#pragma unroll 8
+  for (int a = 0; a < COH_MAX_ARRAYS; ++a) s_st[a * kNT + tid] = kInit;
   __syncthreads();  // the only block barrier: afterwards each thread owns its column
 
+  const uint32_t col = (uint32_t)__cvta_generic_to_shared(s_st) + 4u * tid;
+  const uint32_t lut = (uint32_t)__cvta_generic_to_shared(s_lut);
+  char* const stc = reinterpret_cast<char*>(s_st) + 4 * tid;  // this thread's column
   const uint64_t n = p.n_traces;
-  const uint32_t n_calls = p.n_calls;
+  const uint32_t n_calls = p.n_calls, n_arrays = p.n_arrays;
   const uint32_t n_chunks = (n_calls + 7u) / 8u;
   const uint32_t n_groups = n_calls / 32u;
   const uint32_t n_words = (n_calls + 31u) / 32u;
@@ -125,151 +153,152 @@ __global__ void __launch_bounds__(kNT) k_trace_eval(const KParams p) {
 
   for (uint64_t base = (uint64_t)blockIdx.x * kNT; base < n; base += stride) {
     const uint64_t t = base + tid;
-    if (t < n) {
-      const uint4* rp = p.rec + t;
-      uint32_t acc = 0, bnd = 0, steps = 0, transfers = 0, viol_blocks = 0;
-      uint32_t status = COH_RUN_DONE, stuck_call = 0, stuck_arr = 0, stuck_eff = 0, stuck_flags = 0;
-      uint32_t calls_done = n_calls;
-      int fuel_left = p.fuel;
-      uint32_t g = 0;
+    if (t >= n) continue;
+    const uint4* rp = p.rec + t;
+    uint32_t acc = 0, steps = 0, viol_blocks = 0;
+    // bnd: shift register of boundary-VIOLATION bits of the current 32-call group,
+    // seeded with a sentinel 1: after k calls the sentinel sits at bit k (call 0's bit
+    // at k-1); the stored boundary_ok word is its reversed complement.
+    uint32_t bnd = 1u, i0 = 0;
+    uint32_t status = COH_RUN_DONE, stuck_call = 0, stuck_arr = 0, stuck_eff = 0, stuck_flags = 0;
+    uint32_t calls_done = n_calls;
+    int fuel_left = p.fuel;
 
-      // One call.  i = call index (compile-time within the unrolled group).
-#define COH_CALL(REC, I)                                                                  \
-  {                                                                                       \
-    const uint32_t r_ = (REC);                                                            \
-    uint16_t* sp_ = col + (r_ & 63u) * kNT;                                               \
-    const uint32_t old_ = *sp_;                                                           \
-    const uint64_t e_ = s_lut[((r_ >> 2) & 0x3F0u) | (old_ & 15u)];                       \
-    const uint32_t lo_ = (uint32_t)e_, hi_ = (uint32_t)(e_ >> 32);                        \
-    bool slow_ = (int)lo_ < 0;                                                            \
-    if (CHECK_FUEL) slow_ |= (int)((acc + hi_) & 0xFFu) > fuel_left;                      \
-    if (CHECK_ARR) slow_ |= (r_ & 63u) >= p.n_arrays;                                     \
-    if (slow_) {                                                                          \
-      SlowOut so_;                                                                        \
-      if (CHECK_ARR && (r_ & 63u) >= p.n_arrays)                                          \
-        so_ = SlowOut{COH_RUN_DEFECT, old_, 0u, 0u, 0u, 0u};                              \
-      else                                                                                \
-        slow_call(p.prog[(r_ >> 6) & 63u], old_, p.fuel - (int)steps - (int)(acc & 0xFFu), &so_); \
-      *sp_ = (uint16_t)so_.word;                                                          \
-      steps += (acc & 0xFFu) + so_.steps;                                                 \
-      transfers += ((acc >> 16) & 0x7Fu) + so_.transfers;                                 \
-      acc &= 0xFF00u;                                                                     \
-      status = so_.status;                                                                \
-      stuck_call = (I);                                                                   \
-      stuck_arr = r_ & 63u;                                                               \
-      stuck_eff = so_.effect;                                                             \
-      stuck_flags = so_.flags;                                                            \
-      calls_done = (I);                                                                   \
-      goto terminated;                                                                    \
-    }                                                                                     \
-    *sp_ = (uint16_t)(old_ + lo_);                                                        \
-    acc += hi_;                                                                           \
-    bnd |= ((acc & 0xFF00u) == 0u) ? (1u << ((I) & 31u)) : 0u;                            \
+    // One call; R = 16-bit record (bits above 15 may hold garbage).  Nothing per call
+    // site survives into the slow path (it re-derives the call from the sentinel), so
+    // the fast path carries no bookkeeping moves.
+#define COH_CALL(R)                                                                         \
+  {                                                                                         \
+    const uint32_t r_ = (R);                                                                \
+    uint32_t* sp_ = reinterpret_cast<uint32_t*>(stc + (r_ & 63u) * 512u); /* s_st[a][tid] */ \
+    const uint32_t old_ = *sp_;                                                             \
+    const uint32_t e_ = *reinterpret_cast<const uint32_t*>(                                 \
+        reinterpret_cast<const char*>(s_lut) + ((r_ & 0xFC0u) | (((r_ >> 4) ^ old_) & 0x3Cu))); \
+    acc += e_;                                                                              \
+    bool stop_ = false;                                                                     \
+    if (CHECK_FUEL) stop_ |= (int)(acc & 0xFFu) > fuel_left;                                \
+    if (CHECK_ARR) stop_ |= (r_ & 63u) >= n_arrays;                                         \
+    if (!stop_) *sp_ = old_ + (uint32_t)((int32_t)e_ >> 16); /* slow entries: +0 */         \
+    if (__builtin_expect(stop_ || (acc & 0x8000u) != 0u, 0)) goto slow_path;               \
+    bnd = shift_in_violation(bnd, acc);                                                     \
   }
+#define COH_CHUNK(W)            \
+  COH_CALL((W).x)               \
+  COH_CALL((W).x >> 16)         \
+  COH_CALL((W).y)               \
+  COH_CALL((W).y >> 16)         \
+  COH_CALL((W).z)               \
+  COH_CALL((W).z >> 16)         \
+  COH_CALL((W).w)               \
+  COH_CALL((W).w >> 16)
 
-      {
-        uint4 nxt[4];
+    {
+      uint4 ring[4];  // fully (re)initialised per trace so nothing stays live across traces
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if ((uint32_t)j < n_chunks) nxt[j] = __ldcs(rp + (uint64_t)j * n);
-        for (g = 0; g < n_groups; ++g) {
-          uint4 cur[4];
+      for (int j = 0; j < 4; ++j)
+        ring[j] = (uint32_t)j < n_chunks ? __ldcs(rp + (uint64_t)j * n) : make_uint4(0u, 0u, 0u, 0u);
+      for (uint32_t g = 0; g < n_groups; ++g) {
+        i0 = g * 32u;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) cur[j] = nxt[j];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t c = 4u * (g + 1u) + (uint32_t)j;
-            if (c < n_chunks) nxt[j] = __ldcs(rp + (uint64_t)c * n);
-          }
-          const uint32_t i0 = g * 32u;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            COH_CALL(cur[j].x & 0xFFFFu, i0 + 8 * j + 0);
-            COH_CALL(cur[j].x >> 16, i0 + 8 * j + 1);
-            COH_CALL(cur[j].y & 0xFFFFu, i0 + 8 * j + 2);
-            COH_CALL(cur[j].y >> 16, i0 + 8 * j + 3);
-            COH_CALL(cur[j].z & 0xFFFFu, i0 + 8 * j + 4);
-            COH_CALL(cur[j].z >> 16, i0 + 8 * j + 5);
-            COH_CALL(cur[j].w & 0xFFFFu, i0 + 8 * j + 6);
-            COH_CALL(cur[j].w >> 16, i0 + 8 * j + 7);
-          }
-          if (p.bnd) p.bnd[(uint64_t)g * n + t] = bnd;
-          viol_blocks += 32u - __popc(bnd);
-          bnd = 0;
-          steps += acc & 0xFFu;
-          transfers += (acc >> 16) & 0x7Fu;
-          acc &= 0xFF00u;
-          if (CHECK_FUEL) fuel_left = p.fuel - (int)steps;
+        for (int j = 0; j < 4; ++j) {
+          const uint4 cur = ring[j];
+          const uint32_t cn = 4u * (g + 1u) + (uint32_t)j;
+          if (cn < n_chunks) ring[j] = __ldcs(rp + (uint64_t)cn * n);
+          COH_CHUNK(cur)
         }
-        // tail: n_calls % 32 calls, chunks already prefetched into nxt
-        const uint32_t tail = n_calls - n_groups * 32u;
-        if (tail) {
-          const uint32_t i0 = n_groups * 32u;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t w[4] = {nxt[j].x, nxt[j].y, nxt[j].z, nxt[j].w};
-#pragma unroll
-            for (int h = 0; h < 8; ++h) {
-              const uint32_t i = i0 + 8u * j + h;
-              if (i < n_calls) COH_CALL((w[h >> 1] >> (16 * (h & 1))) & 0xFFFFu, i);
-            }
-          }
-          viol_blocks += tail - __popc(bnd);
-          steps += acc & 0xFFu;
-          transfers += (acc >> 16) & 0x7Fu;
-          acc &= 0xFF00u;
-          if (p.bnd) p.bnd[(uint64_t)n_groups * n + t] = bnd;
-        }
-        goto finished;
+        // 32 calls done: the sentinel was shifted out, call 0's violation bit is bit 31
+        bnd = ~__brev(bnd);
+        if (p.bnd) p.bnd[(uint64_t)g * n + t] = bnd;
+        viol_blocks += 32u - __popc(bnd);
+        bnd = 1u;
+        steps += acc & 0xFFu;
+        acc &= 0xFF00u;
+        if (CHECK_FUEL) fuel_left = p.fuel - (int)steps;
       }
+      const uint32_t tail = n_calls - n_groups * 32u;
+      if (tail) {
+        i0 = n_groups * 32u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t w4[4] = {ring[j].x, ring[j].y, ring[j].z, ring[j].w};
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            if (8u * j + h < tail) COH_CALL(w4[h >> 1] >> (16 * (h & 1)))
+          }
+        }
+        const uint32_t word = (~__brev(bnd ^ (1u << tail))) >> (32u - tail);
+        viol_blocks += tail - __popc(word);
+        steps += acc & 0xFFu;
+        acc &= 0xFF00u;
+        if (p.bnd) p.bnd[(uint64_t)n_groups * n + t] = word;
+      }
+      goto finished;
+    }
+#undef COH_CHUNK
 #undef COH_CALL
 
-    terminated : {
-      // completed calls of the current group are bits [0, calls_done % 32)
-      const uint32_t done_in_group = calls_done & 31u;
-      g = calls_done / 32u;
-      viol_blocks += done_in_group - __popc(bnd);
-      if (p.bnd) {
-        p.bnd[(uint64_t)g * n + t] = bnd;
-        for (uint32_t w = g + 1; w < n_words; ++w) p.bnd[(uint64_t)w * n + t] = 0u;
-      }
+  slow_path : {
+    // which call: k calls of this group completed (sentinel position)
+    const uint32_t k = 31u - __clz(bnd);
+    const uint32_t i = i0 + k;
+    const uint4 chunk = __ldcs(rp + (uint64_t)(i / 8u) * n);
+    const uint32_t w4[4] = {chunk.x, chunk.y, chunk.z, chunk.w};
+    const uint32_t r = (w4[(i & 7u) >> 1] >> (16u * (i & 1u))) & 0xFFFFu;
+    const uint32_t a = r & 63u;
+    const uint32_t old = lds(col + (a << 9));  // untouched: the fast path did not store
+    const uint32_t e = lds(lut + ((r & 0xFC0u) | (((r >> 4) ^ old) & 0x3Cu)));
+    acc -= e;  // undo the accumulate (low 16 bits exact)
+    SlowOut so;
+    if (CHECK_ARR && a >= n_arrays) {
+      so = SlowOut{COH_RUN_DEFECT, old, 0u, 0u, 0u};
+    } else {
+      slow_call(p.prog[(r >> 6) & 63u], old, p.fuel - (int)steps - (int)(acc & 0xFFu), &so);
     }
-    finished : {
-      uint64_t cl = 0, cr = 0, al = 0, ar = 0, tbytes = 0;
-#pragma unroll
-      for (int a = 0; a < COH_MAX_ARRAYS; ++a) {
-        if ((uint32_t)a < p.n_arrays) {
-          const uint32_t w = col[a * kNT];
-          cl |= (uint64_t)(w & 1u) << a;
-          cr |= (uint64_t)((w >> 1) & 1u) << a;
-          al |= (uint64_t)((w >> 2) & 1u) << a;
-          ar |= (uint64_t)((w >> 3) & 1u) << a;
-          if (!UNIFORM) tbytes += (uint64_t)(w >> 4) * s_bytes[a];
-        }
-      }
-      if (UNIFORM) tbytes = (uint64_t)transfers * p.bytes_uniform;
-      // reset this thread's column for its next trace (phantom arrays >= n_arrays
-      // are never written: a call naming one stops the trace as a defect first)
-      for (uint32_t a = 0; a < p.n_arrays; ++a) col[a * kNT] = (uint16_t)COH_STATE_INITIAL;
-      uint4* out = reinterpret_cast<uint4*>(p.res + t);
-      __stcs(out + 0, make_uint4((uint32_t)cl, (uint32_t)(cl >> 32), (uint32_t)cr, (uint32_t)(cr >> 32)));
-      __stcs(out + 1, make_uint4((uint32_t)al, (uint32_t)(al >> 32), (uint32_t)ar, (uint32_t)(ar >> 32)));
-      __stcs(out + 2, make_uint4((uint32_t)tbytes, (uint32_t)(tbytes >> 32), steps, transfers));
-      __stcs(out + 3, make_uint4(calls_done, viol_blocks, stuck_call,
-                                 status | (stuck_arr << 8) | (stuck_eff << 16) | (stuck_flags << 24)));
-    }
+    sts(col + (a << 9), so.word);
+    steps += (acc & 0xFFu) + so.steps;
+    status = so.status;
+    stuck_call = i;
+    stuck_arr = a;
+    stuck_eff = so.effect;
+    stuck_flags = so.flags;
+    calls_done = i;
+    const uint32_t word = k ? ((~__brev(bnd ^ (1u << k))) >> (32u - k)) : 0u;
+    viol_blocks += k - __popc(word);
+    if (p.bnd) {
+      const uint32_t g = i / 32u;
+      p.bnd[(uint64_t)g * n + t] = word;
+      for (uint32_t w = g + 1; w < n_words; ++w) p.bnd[(uint64_t)w * n + t] = 0u;
     }
   }
-}
-
-static size_t trace_smem_bytes(uint32_t) {
-  return sizeof(uint64_t) * (kLutEntries + COH_MAX_ARRAYS) + sizeof(uint16_t) * kNT * COH_MAX_ARRAYS;
+  finished : {
+    uint32_t sw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t transfers = 0;
+    uint64_t tbytes = 0;
+#pragma unroll
+    for (int a = 0; a < COH_MAX_ARRAYS; ++a) {
+      if (a < (int)n_arrays) {
+        const uint32_t w = lds(col + (a << 9));
+        sts(col + (a << 9), kInit);  // reset for this thread's next trace
+        const int sh = 4 * (a & 7) - (int)kStateShift;
+        sw[a >> 3] |= (sh >= 0 ? (w << sh) : (w >> -sh)) & (15u << (4 * (a & 7)));
+        transfers += w >> kCountShift;
+        if (!UNIFORM) tbytes += (uint64_t)(w >> kCountShift) * s_bytes[a];
+      }
+    }
+    if (UNIFORM) tbytes = (uint64_t)transfers * p.bytes_uniform;
+    uint4* out = reinterpret_cast<uint4*>(p.res + t);
+    __stcs(out + 0, make_uint4(sw[0], sw[1], sw[2], sw[3]));
+    __stcs(out + 1, make_uint4(sw[4], sw[5], sw[6], sw[7]));
+    __stcs(out + 2, make_uint4((uint32_t)tbytes, (uint32_t)(tbytes >> 32), steps, transfers));
+    __stcs(out + 3, make_uint4(calls_done, viol_blocks, stuck_call,
+                               status | (stuck_arr << 8) | (stuck_eff << 16) | (stuck_flags << 24)));
+  }
+  }
 }
 
 template <int F>
 static int launch_one(const TraceLaunch& L, const KParams& kp, cudaStream_t s, std::string* err) {
-  const size_t smem = trace_smem_bytes(L.n_arrays);
-  k_trace_eval<F><<<L.grid, kNT, smem, s>>>(kp);
+  k_trace_eval<F><<<L.grid, kNT, 0, s>>>(kp);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("trace_eval launch: ") + cudaGetErrorString(e);
@@ -278,11 +307,9 @@ static int launch_one(const TraceLaunch& L, const KParams& kp, cudaStream_t s, s
   return COH_OK;
 }
 
-int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t n_arrays,
-                         std::string* err) {
+int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t, std::string* err) {
   int b = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &b, k_trace_eval<0>, kNT, trace_smem_bytes(n_arrays));
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trace_eval<0>, kNT, 0);
   if (e != cudaSuccess) {
     *err = std::string("occupancy: ") + cudaGetErrorString(e);
     return COH_E_CUDA;
@@ -322,16 +349,6 @@ int launch_trace_eval(const TraceLaunch& L, void* stream, std::string* err) {
   }
 }
 
-void trace_eval_set_smem_attr() {
-  const int mx = (int)trace_smem_bytes(COH_MAX_ARRAYS);
-  cudaFuncSetAttribute(k_trace_eval<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(k_trace_eval<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(k_trace_eval<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(k_trace_eval<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(k_trace_eval<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(k_trace_eval<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(k_trace_eval<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(k_trace_eval<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-}
+void trace_eval_set_smem_attr() {}
 
 }  // namespace cohb

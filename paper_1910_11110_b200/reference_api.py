@@ -61,10 +61,9 @@ def annotated_run(results: np.ndarray, boundary: np.ndarray | None, t: int, n_tr
     r = results[t]
     store = {}
     for a in range(n_arrays):
-        c = ((int(r["cl"]) >> a) & 1) | (((int(r["cr"]) >> a) & 1) << 1)
-        ab = ((int(r["al"]) >> a) & 1) | (((int(r["ar"]) >> a) & 1) << 1)
-        store[f"a{a}"] = pair_str(c)
-        store[f"a{a}^"] = pair_str(ab)
+        nib = (int(r["state"][a // 8]) >> (4 * (a % 8))) & 15
+        store[f"a{a}"] = pair_str(nib & 3)
+        store[f"a{a}^"] = pair_str(nib >> 2)
     status = RUN_STATUS_NAMES[int(r["status"])]
     stuck = None
     if status == "stuck":
