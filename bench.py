@@ -213,10 +213,10 @@ def run_ours(args, rank, world, local):
     def step(ev0=None, ev1=None):
         if ev0 is not None:
             ev0.record(stream)
-        ctx.eval_traces(d_rec, N, N_CALLS, N_ARRAYS, FUEL, d_res, d_bnd, stream=s)
+        # trace_eval with the counter reduction fused into the kernel epilogue
+        ctx.eval_traces_counted(d_rec, N, N_CALLS, N_ARRAYS, FUEL, d_res, d_cnt, d_bnd, stream=s)
         if ev1 is not None:
             ev1.record(stream)
-        ctx.reduce_counters(d_res, N, d_cnt, s)
         if world > 1:
             with torch.cuda.stream(stream):
                 dist.all_reduce(d_cnt[:10])  # exact: integer sums

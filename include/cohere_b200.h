@@ -165,6 +165,11 @@ static inline size_t coh_records_elems(uint64_t n_traces, uint32_t n_calls) {
 int coh_eval_traces(coh_ctx* ctx, const coh_trace_batch* batch, coh_trace_result* d_results,
                     uint32_t* d_boundary, void* stream);
 
+/* coh_eval_traces + the counter reduction below fused into the same kernel (zeroes
+ * d_counters first): the form the multi-GPU step uses before its allreduce. */
+int coh_eval_traces_counted(coh_ctx* ctx, const coh_trace_batch* batch, coh_trace_result* d_results,
+                            uint32_t* d_boundary, uint64_t* d_counters, void* stream);
+
 /* Same, from HOST buffers (records/results/boundary in host memory, ideally pinned):
  * chunked H2D -> kernel -> D2H pipelined over two streams inside the call; returns
  * after the results are on the host.  batch->records is a host pointer here. */

@@ -110,6 +110,7 @@ def lib():
             "coh_gen_records_host": (i, [u64, u64, u64, u32, u32, u32, vp]),
             "coh_eval_traces": (i, [vp, C.POINTER(_Batch), vp, vp, vp]),
             "coh_eval_traces_host": (i, [vp, C.POINTER(_Batch), vp, vp]),
+            "coh_eval_traces_counted": (i, [vp, C.POINTER(_Batch), vp, vp, vp, vp]),
             "coh_reduce_counters": (i, [vp, vp, u64, vp, vp]),
             "coh_launch_count": (u64, [vp]),
             "coh_host_alloc": (vp, [C.c_size_t]),
@@ -227,6 +228,16 @@ class Context:
         self._check(
             self._L.coh_eval_traces(self._h, C.byref(b), _ptr(d_results), _ptr(d_boundary), _ptr(stream)),
             "coh_eval_traces",
+        )
+
+    def eval_traces_counted(self, d_records, n_traces, n_calls, n_arrays, fuel, d_results, d_counters, d_boundary=None,
+                            array_bytes=None, stream=0):
+        """coh_eval_traces with the COH_N_COUNTERS reduction fused into the kernel."""
+        b = self._batch(d_records, n_traces, n_calls, n_arrays, fuel, array_bytes)
+        self._check(
+            self._L.coh_eval_traces_counted(self._h, C.byref(b), _ptr(d_results), _ptr(d_boundary), _ptr(d_counters),
+                                            _ptr(stream)),
+            "coh_eval_traces_counted",
         )
 
     def eval_traces_host(self, records: np.ndarray, n_traces, n_calls, n_arrays, fuel=10000, array_bytes=None,

@@ -154,13 +154,19 @@ void build_call_table(CallTable* t) {
       const coh_call_outcome o = simulate_block(type, s, 1 << 30);
       uint32_t lo, hi;
       if (o.status != COH_RUN_DONE) {
-        lo = kSlowAddend;
-        hi = 0;
+        lo = 0;
+        hi = kSlowAddend;
       } else {
-        lo = ((uint32_t)o.steps + (uint32_t)(((int)o.viol_after - (int)o.viol_before) * 256)) & 0xFFFFu;
-        hi = (uint32_t)((((int)o.state_after - (int)s) << kStateShift) + ((int)o.transfers << kCountShift)) & 0xFFFFu;
+        lo = (uint32_t)((((int)o.state_after - (int)s) << kStateShift) + ((int)o.transfers << kCountShift)) & 0xFFFFu;
+        hi = ((uint32_t)o.steps + (uint32_t)(((int)o.viol_after - (int)o.viol_before) * 256)) & 0xFFFFu;
       }
       t->lut[lut_slot(type, s)] = lo | (hi << 16);
+      for (uint32_t rem = 0; rem < 8; ++rem) {
+        const coh_call_outcome q = simulate_block(type, s, rem == 7 ? (1 << 30) : (int)rem);
+        t->slow[slow_index(type, s, rem)] =
+            (uint32_t)q.status | ((uint32_t)q.steps << 2) | ((uint32_t)q.transfers << 5) |
+            ((uint32_t)q.state_after << 7) | ((uint32_t)q.stuck_effect << 11) | ((uint32_t)q.stuck_flags << 14);
+      }
     }
   }
 }

@@ -15,10 +15,11 @@ struct coh_ctx {
   int device = 0;
   std::string err;
   uint32_t* d_lut = nullptr;
-  uint64_t* d_prog = nullptr;
+  uint32_t* d_slow = nullptr;
   uint64_t* d_bytes = nullptr;
   int sms = 148;
-  int blocks_per_sm = 1;
+  int blocks_per_sm = 1;       // narrow (u16) trace_eval
+  int blocks_per_sm_wide = 1;  // wide (u32) trace_eval
   uint64_t launches = 0;
   // host-buffer pipeline
   cudaStream_t hs[2] = {nullptr, nullptr};
@@ -70,7 +71,7 @@ int bytes_mode(coh_ctx* ctx, const coh_trace_batch* b, bool* uniform, uint64_t* 
 
 int eval_device(coh_ctx* ctx, const coh_trace_batch* b, const uint16_t* d_records,
                 uint64_t n_traces, coh_trace_result* d_results, uint32_t* d_boundary,
-                cudaStream_t s) {
+                cudaStream_t s, uint64_t* d_counters = nullptr) {
   bool uniform;
   uint64_t ub;
   int rc = bytes_mode(ctx, b, &uniform, &ub);
@@ -91,12 +92,14 @@ int eval_device(coh_ctx* ctx, const coh_trace_batch* b, const uint16_t* d_record
   L.bytes_uniform = ub;
   L.d_array_bytes = ctx->d_bytes;
   L.d_lut = ctx->d_lut;
-  L.d_prog = ctx->d_prog;
+  L.d_slow = ctx->d_slow;
   L.results = d_results;
   L.boundary = d_boundary;
+  L.counters = d_counters;
   // persistent grid, equal rounds per block
   const uint64_t need = (n_traces + 127) / 128;
-  const uint64_t cap = (uint64_t)ctx->sms * (uint64_t)std::max(1, ctx->blocks_per_sm);
+  const int bps = cohb::trace_eval_wide(b->n_calls) ? ctx->blocks_per_sm_wide : ctx->blocks_per_sm;
+  const uint64_t cap = (uint64_t)ctx->sms * (uint64_t)std::max(1, bps);
   const uint64_t rounds = (need + cap - 1) / cap;
   L.grid = (int)((need + rounds - 1) / rounds);
   std::string err;
@@ -130,15 +133,16 @@ int coh_ctx_create(int device, coh_ctx** out) {
   int rc = COH_OK;
   do {
     if ((e = cudaMalloc(&ctx->d_lut, sizeof table.lut)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&ctx->d_prog, sizeof table.prog)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&ctx->d_slow, sizeof table.slow)) != cudaSuccess) break;
     if ((e = cudaMalloc(&ctx->d_bytes, sizeof(uint64_t) * COH_MAX_ARRAYS)) != cudaSuccess) break;
     if ((e = cudaMemcpy(ctx->d_lut, table.lut, sizeof table.lut, cudaMemcpyHostToDevice)) != cudaSuccess) break;
-    if ((e = cudaMemcpy(ctx->d_prog, table.prog, sizeof table.prog, cudaMemcpyHostToDevice)) != cudaSuccess) break;
+    if ((e = cudaMemcpy(ctx->d_slow, table.slow, sizeof table.slow, cudaMemcpyHostToDevice)) != cudaSuccess) break;
     if ((e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess) break;
     cohb::trace_eval_set_smem_attr();
     int tpb = 0;
     std::string err;
-    rc = cohb::trace_eval_occupancy(&ctx->blocks_per_sm, &tpb, COH_MAX_ARRAYS, &err);
+    rc = cohb::trace_eval_occupancy(&ctx->blocks_per_sm, &tpb, 256, &err);
+    if (rc == COH_OK) rc = cohb::trace_eval_occupancy(&ctx->blocks_per_sm_wide, &tpb, 4096, &err);
   } while (0);
   if (e != cudaSuccess || rc != COH_OK) {
     coh_ctx_destroy(ctx);
@@ -151,7 +155,7 @@ int coh_ctx_create(int device, coh_ctx** out) {
 void coh_ctx_destroy(coh_ctx* ctx) {
   if (!ctx) return;
   cudaFree(ctx->d_lut);
-  cudaFree(ctx->d_prog);
+  cudaFree(ctx->d_slow);
   cudaFree(ctx->d_bytes);
   for (int k = 0; k < 2; ++k) {
     cudaFree(ctx->d_rec[k]);
@@ -211,6 +215,20 @@ int coh_eval_traces(coh_ctx* ctx, const coh_trace_batch* batch, coh_trace_result
   if (batch->n_traces && !d_results) return arg_fail(ctx, "d_results is NULL");
   return eval_device(ctx, batch, batch->records, batch->n_traces, d_results, d_boundary,
                      static_cast<cudaStream_t>(stream));
+}
+
+int coh_eval_traces_counted(coh_ctx* ctx, const coh_trace_batch* batch, coh_trace_result* d_results,
+                            uint32_t* d_boundary, uint64_t* d_counters, void* stream) {
+  int rc = validate(ctx, batch);
+  if (rc) return rc;
+  if (batch->n_traces && !d_results) return arg_fail(ctx, "d_results is NULL");
+  if (!d_counters) return arg_fail(ctx, "d_counters is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (batch->n_traces == 0) {
+    COH_CUDA(ctx, cudaMemsetAsync(d_counters, 0, sizeof(uint64_t) * COH_N_COUNTERS, s));
+    return COH_OK;
+  }
+  return eval_device(ctx, batch, batch->records, batch->n_traces, d_results, d_boundary, s, d_counters);
 }
 
 int coh_eval_traces_host(coh_ctx* ctx, const coh_trace_batch* batch, coh_trace_result* h_results,

@@ -49,10 +49,13 @@ int launch_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32
   return COH_OK;
 }
 
-// Counters (include/cohere_b200.h, COH_N_COUNTERS).  Warp shuffle reduce, one atomic
-// per warp per counter.
-__global__ void k_reduce_counters(const coh_trace_result* __restrict__ r, uint64_t n,
-                                  unsigned long long* __restrict__ out) {
+// Counters (include/cohere_b200.h, COH_N_COUNTERS): grid-stride accumulation, warp
+// shuffle + shared-memory block reduction, then one atomic per counter per block (a
+// per-warp atomic made this kernel contention-bound).
+constexpr int kRedThreads = 256;
+__global__ void __launch_bounds__(kRedThreads) k_reduce_counters(const coh_trace_result* __restrict__ r,
+                                                                 uint64_t n, unsigned long long* __restrict__ out) {
+  __shared__ uint64_t part[kRedThreads / 32][COH_N_COUNTERS];
   uint64_t c[COH_N_COUNTERS] = {0};
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -70,12 +73,20 @@ __global__ void k_reduce_counters(const coh_trace_result* __restrict__ r, uint64
     c[8] += q3.x;
     c[9] += 1;
   }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int k = 0; k < COH_N_COUNTERS; ++k) {
     uint64_t v = c[k];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out + k, (unsigned long long)v);
+    if (lane == 0) part[warp][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < COH_N_COUNTERS) {
+    uint64_t v = 0;
+#pragma unroll
+    for (int w = 0; w < kRedThreads / 32; ++w) v += part[w][threadIdx.x];
+    if (v) atomicAdd(out + threadIdx.x, (unsigned long long)v);
   }
 }
 
@@ -87,9 +98,9 @@ int launch_reduce_counters(const coh_trace_result* d_results, uint64_t n_traces,
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    uint64_t blocks = (n_traces + 255) / 256;
-    if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
-    k_reduce_counters<<<(unsigned)blocks, 256, 0, s>>>(
+    uint64_t blocks = (n_traces + kRedThreads - 1) / kRedThreads;
+    if (blocks > (uint64_t)sms * 4) blocks = (uint64_t)sms * 4;
+    k_reduce_counters<<<(unsigned)blocks, kRedThreads, 0, s>>>(
         d_results, n_traces, reinterpret_cast<unsigned long long*>(d_counters));
     e = cudaGetLastError();
   }

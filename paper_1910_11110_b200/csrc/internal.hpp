@@ -27,15 +27,27 @@ constexpr uint32_t kStateShift = 2;
 constexpr uint32_t kCountShift = 6;
 
 // LUT entry (uint32), stored at slot = type*16 + (state ^ (type & 15)) (bank swizzle):
-//   lo16 : accumulator addend = steps + viol_delta * 256   (mod 2^16)
-//          or kSlowAddend for a (type, state) that gets stuck / is malformed
-//   hi16 : signed delta of the state word = ((ns - s) << kStateShift) + (tr << kCountShift)
+//   lo16 : signed delta of the state word = ((ns - s) << kStateShift) + (tr << kCountShift)
+//          (0 for slow entries, so the speculative store rewrites the old word)
+//   hi16 : signed accumulator addend = steps + viol_delta * 256, or kSlowAddend for a
+//          (type, state) that gets stuck / is malformed
 constexpr uint32_t kSlowAddend = 0x8000u;
 constexpr uint32_t lut_slot(uint32_t type, uint32_t state) { return type * 16u + (state ^ (type & 15u)); }
 
+// Slow-outcome table: the exact block outcome for (type, state, remaining fuel r), r
+// clamped to [0, 7] (a block takes at most 6 steps, so r >= 7 means "unlimited"):
+//   bits 0-1 status, 2-4 steps, 5-6 transfers, 7-10 state after, 11-13 stuck effect,
+//   14-17 stuck flags (site | key kind << 1 | actual << 2)
+constexpr int kSlowEntries = kLutEntries * 8;
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+constexpr uint32_t slow_index(uint32_t type, uint32_t state, uint32_t rem) { return (type * 16u + state) * 8u + rem; }
+
 struct CallTable {
   uint32_t lut[kLutEntries];
-  uint64_t prog[kCallTypes];   // 8 micro-ops per type, byte k = op k
+  uint32_t slow[kSlowEntries];
+  uint64_t prog[kCallTypes];   // 8 micro-ops per type, byte k = op k (host/ABI listing)
 };
 
 // Builds the table by running the restated rules (calltable.cpp).
@@ -56,14 +68,17 @@ struct TraceLaunch {
   uint64_t bytes_uniform;
   const uint64_t* d_array_bytes;   // device, n_arrays (used when !uniform_bytes)
   const uint32_t* d_lut;
-  const uint64_t* d_prog;
+  const uint32_t* d_slow;
   coh_trace_result* results;
   uint32_t* boundary;
+  uint64_t* counters;  // optional fused counter reduction (device, COH_N_COUNTERS)
   int grid;
 };
 int launch_trace_eval(const TraceLaunch& p, void* stream, std::string* err);
 void trace_eval_set_smem_attr();
-int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t n_arrays, std::string* err);
+// u16 store words keep the per-array 10-bit transfer counter exact up to 511 calls
+inline bool trace_eval_wide(uint32_t n_calls) { return n_calls > 511u; }
+int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t n_calls, std::string* err);
 int launch_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
                        uint32_t n_arrays, uint32_t adv_per1024, uint16_t* d_records, void* stream,
                        std::string* err);

@@ -4,21 +4,26 @@
 // shared fuel + abstraction_correct (modes.hpp:79-90).
 //
 // Layout:
-//   * per-thread store: one u32 word per array in shared memory, column-interleaved
-//     s_st[a][tid] (bank = tid mod 32: conflict-free whatever arrays a warp touches);
-//     bits 2-5 = state nibble (cl, cr, al, ar), bits 6-31 = per-array transfer count.
+//   * per-thread store: one word per array in shared memory (u16, or u32 for traces
+//     longer than 511 calls), bank-interleaved so a warp's lanes never conflict whatever
+//     arrays they touch; bits 2-5 = state nibble (cl, cr, al, ar), bits 6+ = per-array
+//     transfer count.
 //   * call table (calltable.cpp): 64 call types x 16 states of u32, XOR-swizzled
 //     (slot = type*16 + (state ^ (type & 15))) so the common (type, state) pairs of a
-//     warp land in distinct banks; lo16 = accumulator addend, hi16 = signed delta of
-//     the state word.
+//     warp land in distinct banks; lo16 = signed delta of the store word, hi16 = signed
+//     accumulator addend.
 //   * records: call-major interleaved, 128-bit streaming loads of 8 calls, a ring of
 //     4 loads (32 calls) in flight per thread.
-//   * accumulator: bits 0-7 steps since the last flush (flushed every 32 calls),
-//     bits 8-15 number of arrays whose abstraction is currently violated (boundary_ok
-//     <=> zero), bit 15 poisoned by slow entries (stuck / defect).
-//   * slow calls (stuck, fuel, malformed) replay the call's micro-ops exactly
-//     (slow_call) after leaving the unrolled loop; they yield StuckInfo + partial state.
+//   * accumulator (clean 32-bit): bits 0-7 steps since the last flush (every 32 calls),
+//     bits 8-14 number of arrays whose abstraction is currently violated (boundary_ok
+//     <=> acc < 0x100), bit 15 set by slow entries (stuck / defect).
+//   * slow calls (stuck, fuel, malformed) leave the unrolled loop; the call is
+//     re-derived from a sentinel in the boundary shift register and its exact outcome
+//     (StuckInfo, partial state and steps) read from a host-compiled table indexed by
+//     (type, state, remaining fuel).
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 #include "internal.hpp"
 
@@ -26,16 +31,12 @@ namespace cohb {
 
 constexpr int kNT = 128;  // traces (threads) per block
 
-// One static shared block so every access is [register + compile-time symbol offset]:
-//   words [0, 1024)            call table (4 KB)
-//   words [1024, 1024 + 64*NT) per-trace stores, s_st[a][tid] (32 KB)
-//   then 64 x u64              per-array sizes (non-uniform bytes only)
-constexpr int kStOff = kLutEntries;
-__shared__ __align__(16) uint32_t s_mem[kLutEntries + COH_MAX_ARRAYS * kNT + 2 * COH_MAX_ARRAYS];
-#define s_lut (s_mem)
-#define s_st (s_mem + kStOff)
-#define s_bytes (reinterpret_cast<uint64_t*>(s_mem + kStOff + COH_MAX_ARRAYS * kNT))
-
+// Per-trace store word: u16 (kNarrow, 128 B per trace, n_calls <= 511 so the 10-bit
+// per-array transfer counter cannot overflow) or u32 (wide, 256 B per trace).
+// Narrow slots are lane-interleaved so that a warp's 32 lanes always hit 32 distinct
+// banks whatever arrays they touch:
+//   u16 index = a*kNT + (warp>>1)*64 + 2*lane + (warp&1)  ->  bank = lane.
+// Shared block (per instantiation): [call table 4 KB][stores][64 x u64 array sizes].
 struct KParams {
   const uint4* rec;
   uint64_t n_traces;
@@ -46,104 +47,55 @@ struct KParams {
   uint64_t bytes_uniform;
   const uint64_t* array_bytes;
   const uint32_t* lut;
-  const uint64_t* prog;
+  const uint32_t* slow;
   coh_trace_result* res;
   uint32_t* bnd;
+  unsigned long long* counters;  // optional fused COH_N_COUNTERS reduction (zeroed by the launcher)
 };
 
-struct SlowOut {
-  uint32_t status, word, steps, effect, flags;
-};
-
-// Exact replay of one block's micro-ops from the state word `old_word` with `rem` fuel
-// left (semantics.hpp:253-287: Done before fuel; Stuck consumes no step, store kept).
-__device__ __noinline__ void slow_call(uint64_t prog, uint32_t old_word, int rem, SlowOut* o) {
-  uint32_t s = (old_word >> kStateShift) & 15u;
-  uint32_t steps = 0, tr = 0, status = COH_RUN_DONE, eff_out = 0, flags = 0;
-  for (int k = 0; k < 8;) {
-    const uint32_t op = (uint32_t)(prog >> (8 * k)) & 0xFFu;
-    if (op == OP_END) break;
-    if (op == OP_DEFECT) { status = COH_RUN_DEFECT; break; }  // construction defect first
-    if ((int)steps >= rem) { status = COH_RUN_FUEL_EXHAUSTED; break; }
-    const uint32_t kop = op & 3u;
-    if (kop == OP_IF_VALID || kop == OP_IF_GVALID) {
-      const uint32_t taken = kop == OP_IF_VALID ? (s >> 2) & 1u : (s >> 3) & 1u;
-      ++steps;
-      k += taken ? 3 : 1;
-      continue;
-    }
-    const uint32_t eff = (op >> 2) & 7u, site = (op >> 5) & 1u, abs_t = (op >> 6) & 1u;
-    const uint32_t sh = abs_t ? 2u : 0u;
-    const uint32_t before = (s >> sh) & 3u;
-    uint32_t q = site ? (((before & 1u) << 1) | (before >> 1)) : before;  // swapped(before)
-    int after;
-    switch (eff) {
-      case COH_PUSH: after = (q & 1u) ? 3 : -1; break;   // (V,X) -> (V,V)
-      case COH_PULL: after = (q & 2u) ? 3 : -1; break;   // (X,V) -> (V,V)
-      case COH_READ: after = (q & 1u) ? (int)q : -1; break;
-      case COH_WRITE: after = 1; break;                  // (X,Y) -> (V,I)
-      default: after = (int)q; break;
-    }
-    if (after < 0) {
-      status = COH_RUN_STUCK;
-      eff_out = eff;
-      flags = site | (abs_t << 1) | (before << 2);
-      break;
-    }
-    q = (uint32_t)after;
-    if (site) q = ((q & 1u) << 1) | (q >> 1);
-    s = (s & ~(3u << sh)) | (q << sh);
-    ++steps;
-    if (!abs_t && (eff == COH_PUSH || eff == COH_PULL)) ++tr;
-    ++k;
-  }
-  o->status = status;
-  o->word = (old_word & ~(15u << kStateShift)) + (tr << kCountShift) + (s << kStateShift);
-  o->steps = steps;
-  o->effect = eff_out;
-  o->flags = flags;
-}
-
-__device__ __forceinline__ uint32_t lds(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ void sts(uint32_t a, uint32_t v) {
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-
-// bnd = 2*bnd + (acc & 0xFF00 != 0): the carry of (x + 0xFFFFFFFF) is (x != 0).
+// bnd = 2*bnd + (acc >= 0x100): the accumulator is clean (steps | viol << 8), so the
+// carry of acc + 0xFFFFFF00 is exactly "some array's abstraction is violated".
 __device__ __forceinline__ uint32_t shift_in_violation(uint32_t bnd, uint32_t acc) {
   uint32_t out;
-  asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, 0xFFFFFFFF;\n\taddc.u32 %0, %2, %2;\n\t}"
+  asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, 0xFFFFFF00;\n\taddc.u32 %0, %2, %2;\n\t}"
       : "=r"(out)
-      : "r"(acc & 0xFF00u), "r"(bnd));
+      : "r"(acc), "r"(bnd));
   return out;
 }
 
 // FLAGS: kFuel = fuel may run out (fuel < 6 x n_calls), kBytes = non-uniform array
-// sizes, kArr = n_arrays < 64 (range-check array ids).
-enum : int { kFuel = 1, kBytes = 2, kArr = 4 };
+// sizes, kArr = n_arrays < 64 (range-check array ids), kWide = u32 store words.
+enum : int { kFuel = 1, kBytes = 2, kArr = 4, kWide = 8 };
 
 template <int FLAGS>
-__global__ void __launch_bounds__(kNT) k_trace_eval(const KParams p) {
+__global__ void __launch_bounds__(kNT, (FLAGS & kWide) ? 6 : 10) k_trace_eval(const KParams p) {
   constexpr bool CHECK_FUEL = FLAGS & kFuel;
   constexpr bool UNIFORM = !(FLAGS & kBytes);
   constexpr bool CHECK_ARR = FLAGS & kArr;
+  constexpr bool WIDE = FLAGS & kWide;
+  using Word = typename std::conditional<WIDE, uint32_t, uint16_t>::type;
+  constexpr uint32_t kStride = sizeof(Word) * kNT;  // bytes between arrays of one column
+  constexpr int kStWords = COH_MAX_ARRAYS * kNT * (int)sizeof(Word) / 4;
+  __shared__ __align__(16) uint32_t s_mem[kLutEntries + kStWords + 2 * COH_MAX_ARRAYS];
+  __shared__ unsigned long long s_cnt[COH_N_COUNTERS];
+  uint32_t* const s_lut = s_mem;
+  char* const s_stb = reinterpret_cast<char*>(s_mem + kLutEntries);
+  uint64_t* const s_bytes = reinterpret_cast<uint64_t*>(s_mem + kLutEntries + kStWords);
+
   const int tid = threadIdx.x;
   for (int i = tid; i < kLutEntries; i += kNT) s_lut[i] = p.lut[i];
   if (!UNIFORM)
     for (int i = tid; i < COH_MAX_ARRAYS; i += kNT)
       s_bytes[i] = i < (int)p.n_arrays ? p.array_bytes[i] : 0ull;
   constexpr uint32_t kInit = COH_STATE_INITIAL << kStateShift;
-#pragma unroll 8
-  for (int a = 0; a < COH_MAX_ARRAYS; ++a) s_st[a * kNT + tid] = kInit;
+  constexpr uint32_t kInitWord = WIDE ? kInit : (kInit | (kInit << 16));
+  for (int i = tid; i < kStWords; i += kNT) s_mem[kLutEntries + i] = kInitWord;
+  if (tid < COH_N_COUNTERS) s_cnt[tid] = 0ull;
   __syncthreads();  // the only block barrier: afterwards each thread owns its column
 
-  const uint32_t col = (uint32_t)__cvta_generic_to_shared(s_st) + 4u * tid;
-  const uint32_t lut = (uint32_t)__cvta_generic_to_shared(s_lut);
-  char* const stc = reinterpret_cast<char*>(s_st) + 4 * tid;  // this thread's column
+  const uint32_t warp = tid >> 5, lane = tid & 31;
+  const uint32_t thread_off = WIDE ? 4u * tid : (warp >> 1) * 128u + 4u * lane + 2u * (warp & 1u);
+  char* const stc = s_stb + thread_off;  // this thread's column: stc + a * kStride
   const uint64_t n = p.n_traces;
   const uint32_t n_calls = p.n_calls, n_arrays = p.n_arrays;
   const uint32_t n_chunks = (n_calls + 7u) / 8u;
@@ -170,15 +122,15 @@ __global__ void __launch_bounds__(kNT) k_trace_eval(const KParams p) {
 #define COH_CALL(R)                                                                         \
   {                                                                                         \
     const uint32_t r_ = (R);                                                                \
-    uint32_t* sp_ = reinterpret_cast<uint32_t*>(stc + (r_ & 63u) * 512u); /* s_st[a][tid] */ \
+    Word* sp_ = reinterpret_cast<Word*>(stc + (r_ & 63u) * kStride);   /* store[a][tid] */ \
     const uint32_t old_ = *sp_;                                                             \
     const uint32_t e_ = *reinterpret_cast<const uint32_t*>(                                 \
         reinterpret_cast<const char*>(s_lut) + ((r_ & 0xFC0u) | (((r_ >> 4) ^ old_) & 0x3Cu))); \
-    acc += e_;                                                                              \
+    acc += (uint32_t)((int32_t)e_ >> 16);                                                   \
     bool stop_ = false;                                                                     \
     if (CHECK_FUEL) stop_ |= (int)(acc & 0xFFu) > fuel_left;                                \
     if (CHECK_ARR) stop_ |= (r_ & 63u) >= n_arrays;                                         \
-    if (!stop_) *sp_ = old_ + (uint32_t)((int32_t)e_ >> 16); /* slow entries: +0 */         \
+    if (!stop_) *sp_ = (Word)(old_ + (WIDE ? (uint32_t)(int32_t)(int16_t)e_ : e_));         \
     if (__builtin_expect(stop_ || (acc & 0x8000u) != 0u, 0)) goto slow_path;               \
     bnd = shift_in_violation(bnd, acc);                                                     \
   }
@@ -245,16 +197,28 @@ __global__ void __launch_bounds__(kNT) k_trace_eval(const KParams p) {
     const uint32_t w4[4] = {chunk.x, chunk.y, chunk.z, chunk.w};
     const uint32_t r = (w4[(i & 7u) >> 1] >> (16u * (i & 1u))) & 0xFFFFu;
     const uint32_t a = r & 63u;
-    const uint32_t old = lds(col + (a << 9));  // untouched: the fast path did not store
-    const uint32_t e = lds(lut + ((r & 0xFC0u) | (((r >> 4) ^ old) & 0x3Cu)));
-    acc -= e;  // undo the accumulate (low 16 bits exact)
-    SlowOut so;
-    if (CHECK_ARR && a >= n_arrays) {
-      so = SlowOut{COH_RUN_DEFECT, old, 0u, 0u, 0u};
-    } else {
-      slow_call(p.prog[(r >> 6) & 63u], old, p.fuel - (int)steps - (int)(acc & 0xFFu), &so);
-    }
-    sts(col + (a << 9), so.word);
+    Word* const sp = reinterpret_cast<Word*>(stc + a * kStride);
+    const uint32_t old = *sp;  // untouched: the fast path did not store
+    const uint32_t e = *reinterpret_cast<const uint32_t*>(
+        reinterpret_cast<const char*>(s_lut) + ((r & 0xFC0u) | (((r >> 4) ^ old) & 0x3Cu)));
+    acc -= (uint32_t)((int32_t)e >> 16);  // undo the accumulate
+    // exact outcome from the host-compiled slow table (type, state, remaining fuel)
+    const int rem_i = p.fuel - (int)steps - (int)(acc & 0xFFu);
+    const uint32_t rem = rem_i <= 0 ? 0u : (rem_i >= 7 ? 7u : (uint32_t)rem_i);
+    const uint32_t s0 = (old >> kStateShift) & 15u;
+    const uint32_t info = (CHECK_ARR && a >= n_arrays)
+                              ? (uint32_t)COH_RUN_DEFECT | (s0 << 7)
+                              : __ldg(p.slow + slow_index((r >> 6) & 63u, s0, rem));
+    struct {
+      uint32_t status, word, steps, effect, flags;
+    } so;
+    so.status = info & 3u;
+    so.steps = (info >> 2) & 7u;
+    so.word = (old & ~(15u << kStateShift)) + (((info >> 5) & 3u) << kCountShift) +
+              (((info >> 7) & 15u) << kStateShift);
+    so.effect = (info >> 11) & 7u;
+    so.flags = (info >> 14) & 15u;
+    *sp = (Word)so.word;
     steps += (acc & 0xFFu) + so.steps;
     status = so.status;
     stuck_call = i;
@@ -277,8 +241,9 @@ __global__ void __launch_bounds__(kNT) k_trace_eval(const KParams p) {
 #pragma unroll
     for (int a = 0; a < COH_MAX_ARRAYS; ++a) {
       if (a < (int)n_arrays) {
-        const uint32_t w = lds(col + (a << 9));
-        sts(col + (a << 9), kInit);  // reset for this thread's next trace
+        Word* const wp = reinterpret_cast<Word*>(stc + a * kStride);
+        const uint32_t w = *wp;
+        *wp = (Word)kInit;  // reset for this thread's next trace
         const int sh = 4 * (a & 7) - (int)kStateShift;
         sw[a >> 3] |= (sh >= 0 ? (w << sh) : (w >> -sh)) & (15u << (4 * (a & 7)));
         transfers += w >> kCountShift;
@@ -292,7 +257,24 @@ __global__ void __launch_bounds__(kNT) k_trace_eval(const KParams p) {
     __stcs(out + 2, make_uint4((uint32_t)tbytes, (uint32_t)(tbytes >> 32), steps, transfers));
     __stcs(out + 3, make_uint4(calls_done, viol_blocks, stuck_call,
                                status | (stuck_arr << 8) | (stuck_eff << 16) | (stuck_flags << 24)));
+    if (p.counters) {  // fused counter reduction: warp redux, one shared atomic per warp
+      const uint32_t m = __activemask();
+      const bool leader = (lane == (uint32_t)(__ffs(m) - 1));
+      uint32_t v[9] = {status == COH_RUN_STUCK, status == COH_RUN_FUEL_EXHAUSTED, viol_blocks != 0u,
+                       status == COH_RUN_DEFECT, steps, transfers, viol_blocks, calls_done, 1u};
+      const int slot[9] = {0, 1, 2, 3, 4, 5, 7, 8, 9};
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        v[k] = __reduce_add_sync(m, v[k]);
+        if (leader && v[k]) atomicAdd(&s_cnt[slot[k]], (unsigned long long)v[k]);
+      }
+      if (tbytes) atomicAdd(&s_cnt[6], (unsigned long long)tbytes);
+    }
   }
+  }
+  if (p.counters) {
+    __syncthreads();
+    if (tid < COH_N_COUNTERS && s_cnt[tid]) atomicAdd(p.counters + tid, s_cnt[tid]);
   }
 }
 
@@ -307,9 +289,11 @@ static int launch_one(const TraceLaunch& L, const KParams& kp, cudaStream_t s, s
   return COH_OK;
 }
 
-int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t, std::string* err) {
+int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t n_calls, std::string* err) {
   int b = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trace_eval<0>, kNT, 0);
+  cudaError_t e = trace_eval_wide(n_calls)
+                      ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trace_eval<kWide>, kNT, 0)
+                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trace_eval<0>, kNT, 0);
   if (e != cudaSuccess) {
     *err = std::string("occupancy: ") + cudaGetErrorString(e);
     return COH_E_CUDA;
@@ -331,22 +315,29 @@ int launch_trace_eval(const TraceLaunch& L, void* stream, std::string* err) {
   kp.bytes_uniform = L.bytes_uniform;
   kp.array_bytes = L.d_array_bytes;
   kp.lut = L.d_lut;
-  kp.prog = L.d_prog;
+  kp.slow = L.d_slow;
   kp.res = L.results;
   kp.bnd = L.boundary;
+  kp.counters = reinterpret_cast<unsigned long long*>(L.counters);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int f = (L.check_fuel ? kFuel : 0) | (L.uniform_bytes ? 0 : kBytes) |
-                (L.n_arrays < COH_MAX_ARRAYS ? kArr : 0);
-  switch (f) {
-    case 0: return launch_one<0>(L, kp, s, err);
-    case 1: return launch_one<1>(L, kp, s, err);
-    case 2: return launch_one<2>(L, kp, s, err);
-    case 3: return launch_one<3>(L, kp, s, err);
-    case 4: return launch_one<4>(L, kp, s, err);
-    case 5: return launch_one<5>(L, kp, s, err);
-    case 6: return launch_one<6>(L, kp, s, err);
-    default: return launch_one<7>(L, kp, s, err);
+  if (L.counters) {
+    cudaError_t e = cudaMemsetAsync(L.counters, 0, sizeof(uint64_t) * COH_N_COUNTERS, s);
+    if (e != cudaSuccess) {
+      *err = std::string("counter memset: ") + cudaGetErrorString(e);
+      return COH_E_CUDA;
+    }
   }
+  const int f = (L.check_fuel ? kFuel : 0) | (L.uniform_bytes ? 0 : kBytes) |
+                (L.n_arrays < COH_MAX_ARRAYS ? kArr : 0) | (trace_eval_wide(L.n_calls) ? kWide : 0);
+  switch (f) {
+#define COH_CASE(F) \
+  case F: return launch_one<F>(L, kp, s, err);
+    COH_CASE(0) COH_CASE(1) COH_CASE(2) COH_CASE(3) COH_CASE(4) COH_CASE(5) COH_CASE(6) COH_CASE(7)
+    COH_CASE(8) COH_CASE(9) COH_CASE(10) COH_CASE(11) COH_CASE(12) COH_CASE(13) COH_CASE(14)
+    COH_CASE(15)
+#undef COH_CASE
+  }
+  return COH_E_ARG;
 }
 
 void trace_eval_set_smem_attr() {}

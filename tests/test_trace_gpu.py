@@ -112,6 +112,28 @@ def test_kernel_vs_oracle(ctx, cfg):
     assert np.array_equal(bnd, want_b)
 
 
+@pytest.mark.parametrize("cfg", [CONFIGS[1], CONFIGS[2], CONFIGS[8], CONFIGS[3]], ids=["adv", "fuel", "bytes", "wide"])
+def test_fused_counters_equal_sum_of_results(ctx, cfg):
+    seed, nt, nc, na, adv, fuel, ab = cfg
+    recs = coh.gen_records_host(seed, 0, nt, nc, na, adv)
+    d_rec = torch.from_numpy(recs.view(np.int16).copy()).cuda()
+    d_res = torch.empty(nt * 64, dtype=torch.uint8, device="cuda")
+    d_cnt = torch.full((16,), 7, dtype=torch.int64, device="cuda")
+    ctx.eval_traces_counted(d_rec, nt, nc, na, fuel, d_res, d_cnt, None, array_bytes=ab,
+                            stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    res = d_res.cpu().numpy().view(coh.RESULT_DTYPE)
+    cnt = d_cnt.cpu().numpy().view(np.uint64)[:10]
+    want, _ = o.orc_eval(recs, nt, nc, na, fuel, ab)
+    assert same(res, want)
+    st = want["status"]
+    exp = [(st == 1).sum(), (st == 2).sum(), (want["violations"] > 0).sum(), (st == 3).sum(),
+           want["steps"].astype(np.uint64).sum(), want["transfers"].astype(np.uint64).sum(),
+           want["transfer_bytes"].sum(), want["violations"].astype(np.uint64).sum(),
+           want["calls_done"].astype(np.uint64).sum(), nt]
+    assert [int(x) for x in cnt] == [int(x) for x in exp]
+
+
 def test_defect_records(ctx):
     recs = np.zeros(coh.records_elems(2, 8), dtype=np.uint16)
     recs[0:8] = [0, 0, 3 << 6, 0, 0, 0, 0, 0]
@@ -149,10 +171,12 @@ def test_full_size_c2_properties(ctx):
     ctx.gen_records(seed, 0, N, nc, na, adv, d_rec, s)
     d_res = torch.empty(N * 64, dtype=torch.uint8, device="cuda")
     d_bnd = torch.empty(coh.boundary_words(nc) * N, dtype=torch.int32, device="cuda")
-    ctx.eval_traces(d_rec, N, nc, na, 10000, d_res, d_bnd, stream=s)
     d_cnt = torch.zeros(16, dtype=torch.int64, device="cuda")
-    ctx.reduce_counters(d_res, N, d_cnt, s)
+    ctx.eval_traces_counted(d_rec, N, nc, na, 10000, d_res, d_cnt, d_bnd, stream=s)
+    d_cnt2 = torch.zeros(16, dtype=torch.int64, device="cuda")
+    ctx.reduce_counters(d_res, N, d_cnt2, s)
     torch.cuda.synchronize()
+    assert torch.equal(d_cnt[:10], d_cnt2[:10])  # fused == separate reduction
     res = d_res.cpu().numpy().view(coh.RESULT_DTYPE)
     bnd = d_bnd.cpu().numpy().view(np.uint32)
     cnt = d_cnt.cpu().numpy().view(np.uint64)[:10]
