@@ -163,16 +163,27 @@ def cpu_sample(seconds, threads, trace0=0):
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return  # rank 0 alone runs the reference arm
+    import paper_1910_11110_b200 as coh
+
     threads = os.cpu_count() or 1
-    # per-step sample sized so warmup + steps finish within ~2 minutes
-    per_step = max(0.2, min(5.0, 120.0 / max(1, args.steps + args.warmup)))
-    for w in range(args.warmup):
-        cpu_sample(per_step, threads, trace0=w * 4096)
-    t_calls, t_sec, last = 0, 0.0, None
-    for k in range(args.steps):
-        last = cpu_sample(per_step, threads, trace0=(1 << 30) + k * 65536)
-        t_calls += last["calls"]
-        t_sec += last["seconds"]
+    kind, fn = cpu_eval_fn()
+    cores = threads if kind == "reference" else 1
+    # one calibration, then every step evaluates a fixed-size sample of fresh trace ids,
+    # sized so warmup + steps finish within ~2 minutes
+    per_step = max(0.05, min(5.0, 110.0 / max(1, args.steps + args.warmup)))
+    cal = cpu_sample(min(per_step, 1.0), threads, trace0=1 << 40)
+    n_step = max(cores, int(cal["traces"] * per_step / max(cal["seconds"], 1e-3)))
+    t_calls, t_sec = 0, 0.0
+    for k in range(args.warmup + args.steps):
+        recs = coh.gen_records_host(SEED, (1 << 30) + k * n_step, n_step, N_CALLS, N_ARRAYS, ADV)
+        t0 = time.perf_counter()
+        res, _ = fn(recs, n_step, cores)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            t_calls += evaluated_calls(res)
+            t_sec += dt
+    last = {"cores": cores, "kind": kind,
+            "sample": f"{n_step} traces of the same workload per step (fresh trace ids per step)"}
     value = t_calls / t_sec
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "calls/s", "n_gpus": world,
