@@ -193,6 +193,56 @@ uint64_t coh_launch_count(const coh_ctx* ctx);
 void* coh_host_alloc(size_t bytes);
 void coh_host_free(void* p);
 
+/* ==== element-granular path (overlapping sub-array views) ========
+ * One element program = one buffer of n_cells cells, up to COH_MAX_VIEWS views (absolute
+ * inclusive ranges, program.hpp:31-46), and a sequence of component calls, each one
+ * declared mode on one view plus a body of up to two element range effects
+ * (`w x[i]` / `r x[i]` for every i in [lo, hi], view-relative, program.hpp:94-101).
+ * Before running, every call's modes are closed over view overlaps exactly as
+ * rewrite_program / infer_overlap_closure do (overlap.hpp:182-242).
+ * Store layout on the device: two bit planes per buffer, L (local valid) and R (remote
+ * valid), bit i of word i/32; initial_store puts every cell at (V,I): L = 1, R = 0.   */
+#define COH_MAX_VIEWS 16
+typedef struct coh_elem_op {
+  uint8_t effect;   /* COH_READ or COH_WRITE */
+  uint8_t site;     /* COH_LOCAL / COH_REMOTE */
+  uint16_t pad;
+  uint32_t lo, hi;  /* view-relative, inclusive */
+} coh_elem_op;
+typedef struct coh_elem_call {
+  uint32_t view;      /* declared view index */
+  uint8_t kind;       /* COH_R / COH_W / COH_RW */
+  uint8_t site;
+  uint8_t n_body;     /* 0..2 */
+  uint8_t pad;
+  coh_elem_op body[2];
+} coh_elem_call;
+typedef struct coh_elem_program {
+  uint32_t n_cells;
+  uint32_t n_views;
+  const uint32_t* view_lo;   /* absolute, inclusive */
+  const uint32_t* view_hi;
+  uint32_t n_calls;
+  int32_t fuel;
+  const coh_elem_call* calls;
+} coh_elem_program;
+/* Per-program outcome.  stuck key: element b[stuck_index] (key kind concrete) or the
+ * abstract key of view stuck_index (key kind abstract).  Transfers are the executed
+ * concrete whole-view syncs; their transfer ranges are the maximal runs of changed
+ * cells of each sync's delta (semantics.hpp:125-128, 155-166). */
+typedef struct coh_elem_result {
+  uint8_t status, stuck_effect, stuck_flags, pad;  /* stuck_flags as coh_trace_result */
+  uint32_t stuck_call;
+  uint32_t stuck_index;
+  uint32_t calls_done;
+  uint32_t violations;
+  uint32_t transfers;
+  uint64_t steps;
+  uint64_t transfer_cells;   /* sum of run lengths ("minimal" transfer, in cells)    */
+  uint64_t n_runs;
+  uint64_t vpu_cells;        /* VectorPU-faithful: whole view range per sync */
+} coh_elem_result;
+
 #ifdef __cplusplus
 }
 #endif

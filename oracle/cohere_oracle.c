@@ -226,3 +226,183 @@ int orc_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t 
       }
   return 0;
 }
+
+/* ===================================================================================
+ * Element-granular programs (restatement, bit planes):
+ *   overlap closure     infer_overlap_closure, overlap.hpp:182-230 (one declared mode
+ *                       per call: W/RW on x appends RW@site on every overlapping view in
+ *                       declaration order; overlaps() overlap.hpp:17-20)
+ *   translation         translate_mode/translate_block, modes.hpp:31-59 (whole-view sync
+ *                       of the concrete range, then the abstract key)
+ *   whole-view sync     semantics.hpp:155-166: atomic over [lo,hi] ascending, first
+ *                       failing cell is the stuck key, delta = changed cells
+ *   element effects     program.hpp:94-101 + apply_effect_at, one step per cell
+ *   boundary check      abstraction_correct, modes.hpp:79-90 (every view, every cell)
+ */
+#include <stdlib.h>
+
+static int bit_get(const uint8_t* p, uint32_t i) { return p[i]; }
+
+typedef struct {
+  uint8_t* L;
+  uint8_t* R;
+  uint8_t abs[COH_MAX_VIEWS];
+  int64_t steps;
+  int64_t fuel;
+  coh_elem_result* out;
+  uint32_t* runs;
+  uint64_t runs_cap;
+  int overflow;
+} orc_elem_state;
+
+/* one step budget check: 1 = ok to step, 0 = fuel exhausted */
+static int fuel_ok(orc_elem_state* st) { return st->steps < st->fuel; }
+
+static void set_stuck(orc_elem_state* st, int eff, int site, int abs_key, uint32_t index, int actual) {
+  st->out->status = COH_RUN_STUCK;
+  st->out->stuck_effect = (uint8_t)eff;
+  st->out->stuck_flags = (uint8_t)(site | (abs_key << 1) | (actual << 2));
+  st->out->stuck_index = index;
+}
+
+/* returns 0 to continue, 1 when the run stops (stuck / fuel) */
+static int abstract_effect(orc_elem_state* st, uint32_t v, int eff, int site) {
+  if (!fuel_ok(st)) { st->out->status = COH_RUN_FUEL_EXHAUSTED; return 1; }
+  const int after = orc_apply_cell(eff, site, st->abs[v]);
+  if (after < 0) { set_stuck(st, eff, site, 1, v, st->abs[v]); return 1; }
+  st->abs[v] = (uint8_t)after;
+  st->steps++;
+  return 0;
+}
+
+static int whole_view_sync(orc_elem_state* st, uint32_t lo, uint32_t hi, int eff, int site) {
+  if (!fuel_ok(st)) { st->out->status = COH_RUN_FUEL_EXHAUSTED; return 1; }
+  /* unify every cell first (atomic: a failure leaves the store untouched) */
+  for (uint32_t i = lo; i <= hi; ++i) {
+    const int pair = bit_get(st->L, i) | (bit_get(st->R, i) << 1);
+    if (orc_apply_cell(eff, site, pair) < 0) { set_stuck(st, eff, site, 0, i, pair); return 1; }
+  }
+  int64_t run_lo = -1;
+  for (uint32_t i = lo; i <= hi + 1; ++i) {
+    int changed = 0;
+    if (i <= hi) {
+      const int pair = bit_get(st->L, i) | (bit_get(st->R, i) << 1);
+      const int after = orc_apply_cell(eff, site, pair);
+      changed = after != pair;
+      st->L[i] = (uint8_t)(after & 1);
+      st->R[i] = (uint8_t)((after >> 1) & 1);
+    }
+    if (changed && run_lo < 0) run_lo = i;
+    if (!changed && run_lo >= 0) {
+      if (st->out->n_runs < st->runs_cap) {
+        if (st->runs) {
+          st->runs[2 * st->out->n_runs] = (uint32_t)run_lo;
+          st->runs[2 * st->out->n_runs + 1] = i - 1;
+        }
+      } else {
+        st->overflow = 1;
+      }
+      st->out->n_runs++;
+      st->out->transfer_cells += (uint64_t)(i - run_lo);
+      run_lo = -1;
+    }
+  }
+  st->out->transfers++;
+  st->out->vpu_cells += (uint64_t)(hi - lo + 1);
+  st->steps++;
+  return 0;
+}
+
+static int element_range(orc_elem_state* st, uint32_t lo, uint32_t hi, int eff, int site) {
+  for (uint32_t i = lo; i <= hi; ++i) {
+    if (!fuel_ok(st)) { st->out->status = COH_RUN_FUEL_EXHAUSTED; return 1; }
+    const int pair = bit_get(st->L, i) | (bit_get(st->R, i) << 1);
+    const int after = orc_apply_cell(eff, site, pair);
+    if (after < 0) { set_stuck(st, eff, site, 0, i, pair); return 1; }
+    st->L[i] = (uint8_t)(after & 1);
+    st->R[i] = (uint8_t)((after >> 1) & 1);
+    st->steps++;
+  }
+  return 0;
+}
+
+/* translate_mode (modes.hpp:31-50) executed directly */
+static int run_mode(orc_elem_state* st, const coh_elem_program* P, uint32_t v, int kind, int site) {
+  const int sync = site == COH_REMOTE ? COH_PUSH : COH_PULL;
+  if (kind == COH_R || kind == COH_RW) {
+    if (!fuel_ok(st)) { st->out->status = COH_RUN_FUEL_EXHAUSTED; return 1; }
+    const int flag = site == COH_REMOTE ? (st->abs[v] >> 1) & 1 : st->abs[v] & 1;
+    st->steps++; /* the if step */
+    if (!flag) {
+      if (whole_view_sync(st, P->view_lo[v], P->view_hi[v], sync, COH_LOCAL)) return 1;
+      if (abstract_effect(st, v, sync, COH_LOCAL)) return 1;
+    }
+  }
+  if (kind == COH_W || kind == COH_RW)
+    if (abstract_effect(st, v, COH_WRITE, site)) return 1;
+  return 0;
+}
+
+int orc_elem_run(const coh_elem_program* P, coh_elem_result* out, uint32_t* plane_l, uint32_t* plane_r,
+                 uint8_t* view_abs, uint32_t* boundary, uint32_t* runs, uint64_t runs_cap) {
+  if (P->n_views > COH_MAX_VIEWS) return -1;
+  for (uint32_t v = 0; v < P->n_views; ++v)
+    if (P->view_lo[v] > P->view_hi[v] || P->view_hi[v] >= P->n_cells) return -1;
+  orc_elem_state st;
+  memset(&st, 0, sizeof st);
+  memset(out, 0, sizeof *out);
+  st.L = (uint8_t*)malloc(P->n_cells);
+  st.R = (uint8_t*)malloc(P->n_cells);
+  memset(st.L, 1, P->n_cells); /* initial_store: (V,I) */
+  memset(st.R, 0, P->n_cells);
+  for (uint32_t v = 0; v < P->n_views; ++v) st.abs[v] = 1;
+  st.fuel = P->fuel;
+  st.out = out;
+  st.runs = runs;
+  st.runs_cap = runs_cap;
+  const uint32_t n_words = (P->n_calls + 31) / 32;
+  if (boundary) memset(boundary, 0, 4u * n_words);
+  int rc = 0;
+  uint32_t c;
+  for (c = 0; c < P->n_calls; ++c) {
+    const coh_elem_call* call = &P->calls[c];
+    const uint32_t x = call->view;
+    if (x >= P->n_views) { rc = -1; break; }
+    /* closure: declared mode, then shadow RW on overlapping views (declaration order) */
+    if (run_mode(&st, P, x, call->kind, call->site)) break;
+    int stopped = 0;
+    if (call->kind != COH_R)
+      for (uint32_t y = 0; y < P->n_views && !stopped; ++y)
+        if (y != x && P->view_lo[x] <= P->view_hi[y] && P->view_lo[y] <= P->view_hi[x])
+          stopped = run_mode(&st, P, y, COH_RW, call->site);
+    if (stopped) break;
+    for (int k = 0; k < call->n_body && !stopped; ++k) {
+      const coh_elem_op* op = &call->body[k];
+      stopped = element_range(&st, P->view_lo[x] + op->lo, P->view_lo[x] + op->hi, op->effect, op->site);
+    }
+    if (stopped) break;
+    int ok = 1;
+    for (uint32_t v = 0; v < P->n_views && ok; ++v)
+      for (uint32_t i = P->view_lo[v]; i <= P->view_hi[v]; ++i) {
+        const int pair = st.L[i] | (st.R[i] << 1);
+        if (!orc_leq(st.abs[v], pair)) { ok = 0; break; }
+      }
+    out->calls_done++;
+    if (!ok) out->violations++;
+    if (ok && boundary) boundary[c / 32] |= 1u << (c % 32);
+  }
+  if (out->status != COH_RUN_DONE) out->stuck_call = c;
+  out->steps = (uint64_t)st.steps;
+  const uint32_t n_pw = (P->n_cells + 31) / 32;
+  memset(plane_l, 0, 4u * n_pw);
+  memset(plane_r, 0, 4u * n_pw);
+  for (uint32_t i = 0; i < P->n_cells; ++i) {
+    if (st.L[i]) plane_l[i / 32] |= 1u << (i % 32);
+    if (st.R[i]) plane_r[i / 32] |= 1u << (i % 32);
+  }
+  for (uint32_t v = 0; v < P->n_views; ++v) view_abs[v] = st.abs[v];
+  free(st.L);
+  free(st.R);
+  if (rc) return rc;
+  return st.overflow ? -3 : 0;
+}

@@ -13,6 +13,8 @@
 //           shipped; transfers / transfer_bytes are reported as 0.
 //
 // Output uses the product's result POD (include/cohere_b200.h) so tests compare fields.
+#include <pthread.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
@@ -254,6 +256,151 @@ int ref_selfcheck(const uint16_t* records, uint64_t n_total, uint32_t n_calls, u
     if (std::memcmp(&r0, &r1, sizeof r0) != 0 || b0 != b1) ++bad;
   }
   return bad;
+}
+
+// ---------------------------------------------------------------------------------
+// Element-granular programs (one buffer "b", views "v0".."vK"): the reference's own
+// Declarations / DeclBlock / rewrite_program (overlap closure, overlap.hpp:234-242) /
+// translate_block / run(Full) / abstraction_correct, block by block.  Transfer ranges
+// are the maximal runs of each whole-view sync step's delta (changed cells, ascending,
+// semantics.hpp:125-128, 155-166).  Returns 0, -1 on a construction error, -2 on an
+// OverlapInferenceError, -3 when runs_cap is too small.
+static int ref_elem_run_impl(const coh_elem_program* P, coh_elem_result* out, uint32_t* plane_l, uint32_t* plane_r,
+                             uint8_t* view_abs, uint32_t* boundary, uint32_t* runs, uint64_t runs_cap) {
+  try {
+    AnnotatedProgram p;
+    p.decls.add_buffer({"b", (int)P->n_cells, {}});
+    for (uint32_t v = 0; v < P->n_views; ++v)
+      p.decls.add_view({"v" + std::to_string(v), "b", (int)P->view_lo[v], (int)P->view_hi[v], {}});
+    for (uint32_t c = 0; c < P->n_calls; ++c) {
+      const coh_elem_call& call = P->calls[c];
+      const std::string x = "v" + std::to_string(call.view);
+      AccessMode m;
+      m.kind = static_cast<AccessMode::Kind>(call.kind);
+      m.site = call.site ? Site::Remote : Site::Local;
+      m.view = x;
+      std::vector<Stmt> body;
+      for (int k = 0; k < call.n_body; ++k) {
+        const coh_elem_op& op = call.body[k];
+        for (uint32_t i = op.lo; i <= op.hi; ++i)
+          body.push_back(Stmt::effect(static_cast<EffectKind>(op.effect), p.decls.element_target(x, (int)i),
+                                      op.site ? Site::Remote : Site::Local));
+      }
+      p.blocks.emplace_back(std::vector<AccessMode>{m}, Stmt::seq(body));
+    }
+    AnnotatedProgram q = rewrite_program(p, build_registry(p.decls));
+    std::memset(out, 0, sizeof *out);
+    Store store = initial_store(q.decls);
+    Schedule schedule;
+    int64_t steps = 0;
+    RunStatus status = RunStatus::Done;
+    std::optional<StuckInfo> stuck;
+    const uint32_t n_words = (P->n_calls + 31) / 32;
+    if (boundary) std::memset(boundary, 0, 4u * n_words);
+    uint32_t c = 0;
+    for (; c < q.blocks.size(); ++c) {
+      RunResult rr = run(translate_block(q.blocks[c], q.decls), std::move(store), (int)(P->fuel - steps),
+                         schedule, TraceMode::Full);
+      store = std::move(rr.store);
+      steps += rr.steps;
+      status = rr.status;
+      schedule.pos = rr.schedule_consumed;
+      for (const auto& ts : rr.trace) {
+        if (ts.head.op() != Stmt::Op::Effect) continue;
+        const auto& n = ts.head.node();
+        if (n.target.kind != Target::Kind::WholeView) continue;
+        out->transfers++;
+        out->vpu_cells += (uint64_t)(n.target.hi - n.target.lo + 1);
+        int64_t run_lo = -2, run_hi = -2;
+        auto flush = [&] {
+          if (run_lo < 0) return 0;
+          if (out->n_runs >= runs_cap) return -3;
+          if (runs) {
+            runs[2 * out->n_runs] = (uint32_t)run_lo;
+            runs[2 * out->n_runs + 1] = (uint32_t)run_hi;
+          }
+          out->n_runs++;
+          out->transfer_cells += (uint64_t)(run_hi - run_lo + 1);
+          return 0;
+        };
+        for (const auto& [key, pair] : ts.delta) {
+          (void)pair;
+          if (key.index == run_hi + 1) {
+            run_hi = key.index;
+          } else {
+            if (flush()) return -3;
+            run_lo = run_hi = key.index;
+          }
+        }
+        if (flush()) return -3;
+      }
+      if (rr.status != RunStatus::Done) {
+        stuck = rr.stuck;
+        break;
+      }
+      const bool ok = abstraction_correct(store, q.decls);
+      if (!ok) out->violations++;
+      if (ok && boundary) boundary[c / 32] |= 1u << (c % 32);
+      out->calls_done++;
+    }
+    out->status = (uint8_t)status;
+    out->steps = (uint64_t)steps;
+    if (status != RunStatus::Done) {
+      out->stuck_call = c;
+      if (stuck) {
+        out->stuck_effect = (uint8_t)stuck->effect;
+        const bool abs_key = stuck->key.kind == VarKey::Kind::Abstract;
+        out->stuck_flags = (uint8_t)((stuck->site == Site::Remote ? 1u : 0u) | (abs_key ? 2u : 0u) |
+                                     (pair_bits(stuck->actual) << 2));
+        out->stuck_index = abs_key ? (uint32_t)std::stoi(stuck->key.name.substr(1)) : (uint32_t)stuck->key.index;
+      }
+    }
+    const uint32_t n_pw = (P->n_cells + 31) / 32;
+    std::memset(plane_l, 0, 4u * n_pw);
+    std::memset(plane_r, 0, 4u * n_pw);
+    for (uint32_t i = 0; i < P->n_cells; ++i) {
+      const uint32_t b = pair_bits(store.at(VarKey::element("b", (int)i)));
+      if (b & 1u) plane_l[i / 32] |= 1u << (i % 32);
+      if (b & 2u) plane_r[i / 32] |= 1u << (i % 32);
+    }
+    for (uint32_t v = 0; v < P->n_views; ++v)
+      view_abs[v] = (uint8_t)pair_bits(store.at(VarKey::abstract("v" + std::to_string(v))));
+    return 0;
+  } catch (const OverlapInferenceError&) {
+    return -2;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// The reference builds element bodies as right-nested Stmt chains and normalises /
+// destroys them recursively, so large views need a deep stack: run on a pthread with
+// a 4 GiB stack (virtual; only touched pages are committed).
+struct ElemArgs {
+  const coh_elem_program* P;
+  coh_elem_result* out;
+  uint32_t *plane_l, *plane_r;
+  uint8_t* view_abs;
+  uint32_t *boundary, *runs;
+  uint64_t runs_cap;
+  int rc;
+};
+static void* elem_thread(void* a) {
+  ElemArgs* e = static_cast<ElemArgs*>(a);
+  e->rc = ref_elem_run_impl(e->P, e->out, e->plane_l, e->plane_r, e->view_abs, e->boundary, e->runs, e->runs_cap);
+  return nullptr;
+}
+int ref_elem_run(const coh_elem_program* P, coh_elem_result* out, uint32_t* plane_l, uint32_t* plane_r,
+                 uint8_t* view_abs, uint32_t* boundary, uint32_t* runs, uint64_t runs_cap) {
+  ElemArgs a{P, out, plane_l, plane_r, view_abs, boundary, runs, runs_cap, -1};
+  pthread_attr_t attr;
+  pthread_attr_init(&attr);
+  pthread_attr_setstacksize(&attr, (size_t)4 << 30);
+  pthread_t th;
+  if (pthread_create(&th, &attr, elem_thread, &a) != 0) return -4;
+  pthread_join(th, nullptr);
+  pthread_attr_destroy(&attr);
+  return a.rc;
 }
 
 }  // extern "C"
