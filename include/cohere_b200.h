@@ -243,6 +243,36 @@ typedef struct coh_elem_result {
   uint64_t vpu_cells;        /* VectorPU-faithful: whole view range per sync */
 } coh_elem_result;
 
+typedef struct coh_elem_stats {
+  double device_ms;        /* init + all stages, CUDA events on the evaluation stream     */
+  uint64_t alg_bytes;      /* algorithmic bytes: sync 3m/8 + 8 per run,
+                              read m/8, write m/4, view check m/8 or m/4                  */
+  uint64_t launches;
+  uint64_t tiles;
+  uint32_t stages;
+  uint32_t pad;
+} coh_elem_stats;
+
+/* Evaluate n element programs (one buffer each) on the device; host inputs and outputs.
+ * Replaces, per program, rewrite_program + run_annotated over views (overlap.hpp:234,
+ * modes.hpp:105) with element bodies, and extracts the transfer ranges of every
+ * whole-view sync.  Optional outputs (NULL to skip):
+ *   planes_out    [n][2][plane_words] final L and R planes (bit i of word i/32)
+ *   view_abs_out  [n][COH_MAX_VIEWS] final abstract pair of every view (bit0 L, bit1 R)
+ *   boundary_out  [n][boundary_words] boundary_ok bit per completed call
+ *   runs_out      [n][runs_cap][2] transfer ranges (first, last cell), ascending per sync
+ * Returns COH_E_CONSTRUCTION for malformed programs (program.hpp:57-110 analogues). */
+int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32_t n_progs,
+                  coh_elem_result* results, uint32_t* planes_out, uint32_t plane_words,
+                  uint8_t* view_abs_out, uint32_t* boundary_out, uint32_t boundary_words,
+                  uint32_t* runs_out, uint64_t runs_cap, coh_elem_stats* stats);
+
+/* Synthetic element program (views + calls) for program id `prog_id`; see DESIGN.md §3b.
+ * view_lo/view_hi: n_views entries; calls: n_calls entries. */
+int coh_elem_gen(uint64_t seed, uint64_t prog_id, uint32_t n_cells, uint32_t n_views,
+                 uint32_t n_calls, uint32_t adv_per1024, uint32_t* view_lo, uint32_t* view_hi,
+                 coh_elem_call* calls);
+
 #ifdef __cplusplus
 }
 #endif

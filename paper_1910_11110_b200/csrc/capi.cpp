@@ -11,24 +11,6 @@
 #include "gen_common.h"
 #include "internal.hpp"
 
-struct coh_ctx {
-  int device = 0;
-  std::string err;
-  uint32_t* d_lut = nullptr;
-  uint32_t* d_slow = nullptr;
-  uint64_t* d_bytes = nullptr;
-  int sms = 148;
-  int blocks_per_sm = 1;       // narrow (u16) trace_eval
-  int blocks_per_sm_wide = 1;  // wide (u32) trace_eval
-  uint64_t launches = 0;
-  // host-buffer pipeline
-  cudaStream_t hs[2] = {nullptr, nullptr};
-  uint16_t* d_rec[2] = {nullptr, nullptr};
-  coh_trace_result* d_res[2] = {nullptr, nullptr};
-  uint32_t* d_bnd[2] = {nullptr, nullptr};
-  size_t rec_cap = 0, res_cap = 0, bnd_cap = 0;  // bytes per buffer
-};
-
 namespace {
 
 int cuda_fail(coh_ctx* ctx, cudaError_t e, const char* what) {

@@ -1,0 +1,362 @@
+// Element-granular path, device side: validity bit planes (L = local valid, R = remote
+// valid; bit i of word i/32) for many buffers, executed stage by stage (op k of every
+// buffer in stage k).  Per stage:
+//   pass1  one CTA per 64 Ki-cell tile: SYNC -> first zero of the source plane
+//          (stuck cell) + zero-run starts/ends/zeros of the destination; READ -> first
+//          zero; WRITE -> applied directly (cannot fail); CHECK -> per-view
+//          all-ones / all-zero flags (abstraction_correct, modes.hpp:79-90)
+//   decide one thread per buffer: stuck (whole-view sync is atomic, semantics.hpp:
+//          155-166: nothing is written when any cell fails), run offsets (exclusive
+//          scan over the op's tiles), boundary bit
+//   apply  SYNC tiles that passed: write the transfer ranges (maximal runs of cells the
+//          sync changes, ascending) and set the destination plane
+// Words move as 128-bit loads (8 consecutive words per thread), warp/block reductions
+// via shuffles; every kernel is HBM-streaming.
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "elem.hpp"
+#include "internal.hpp"
+
+namespace cohb {
+
+constexpr int kET = 256;                   // threads per tile CTA
+constexpr int kWPT = kElemTileWords / kET; // 8 words per thread
+static_assert(kWPT == 8, "8 words per thread");
+
+
+__device__ __forceinline__ uint32_t word_mask(uint32_t w, uint32_t lo, uint32_t hi) {
+  const uint32_t wl = lo >> 5, wh = hi >> 5;
+  if (w < wl || w > wh) return 0u;
+  uint32_t m = 0xFFFFFFFFu;
+  if (w == wl) m &= 0xFFFFFFFFu << (lo & 31u);
+  if (w == wh) m &= 0xFFFFFFFFu >> (31u - (hi & 31u));
+  return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  T s = 0;
+#pragma unroll
+  for (int k = 0; k < kET / 32; ++k) s += red[k];
+  return s;
+}
+
+__device__ __forceinline__ uint32_t block_or(uint32_t v, uint32_t* red) {
+  v = __reduce_or_sync(0xffffffffu, v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kET / 32; ++k) s |= red[k];
+  return s;
+}
+
+__device__ __forceinline__ uint32_t block_min(uint32_t v, uint32_t* red) {
+  v = __reduce_min_sync(0xffffffffu, v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  uint32_t s = 0xFFFFFFFFu;
+#pragma unroll
+  for (int k = 0; k < kET / 32; ++k) s = min(s, red[k]);
+  return s;
+}
+
+// Exclusive block scan of per-thread counts; returns this thread's prefix.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) red[warp] = x;
+  __syncthreads();
+  uint32_t base = 0;
+  for (int k = 0; k < warp; ++k) base += red[k];
+  return base + x - v;
+}
+
+__device__ __forceinline__ void load8(const uint32_t* p, uint32_t (&w)[kWPT]) {
+  const uint4 a = __ldcg(reinterpret_cast<const uint4*>(p));
+  const uint4 b = __ldcg(reinterpret_cast<const uint4*>(p) + 1);
+  w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+  w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+}
+__device__ __forceinline__ void store8(uint32_t* p, const uint32_t (&w)[kWPT]) {
+  reinterpret_cast<uint4*>(p)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  reinterpret_cast<uint4*>(p)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
+// Zero-run starts / ends of z (zeros of the destination inside the range) for this
+// thread's 8 words, given the neighbouring bits.
+__device__ __forceinline__ void run_edges(const uint32_t (&z)[kWPT], uint32_t prev_top, uint32_t next_bot,
+                                          uint32_t (&st)[kWPT], uint32_t (&en)[kWPT]) {
+#pragma unroll
+  for (int k = 0; k < kWPT; ++k) {
+    const uint32_t pt = k ? (z[k - 1] >> 31) : prev_top;
+    const uint32_t nb = k < kWPT - 1 ? (z[k + 1] & 1u) : next_bot;
+    st[k] = z[k] & ~((z[k] << 1) | pt);
+    en[k] = z[k] & ~((z[k] >> 1) | (nb << 31));
+  }
+}
+
+__global__ void __launch_bounds__(kET) k_elem_pass1(const ElemDev d) {
+  __shared__ uint32_t red[kET / 32];
+  __shared__ uint32_t s_first[kET], s_last[kET];
+  const ElemTile tile = d.tiles[blockIdx.x];
+  const uint32_t b = tile.b;
+  if (d.st[b].dead) return;
+  const ElemOp op = d.ops[b];
+  uint32_t* Lp = d.planes + (size_t)b * 2u * d.W;
+  uint32_t* Rp = Lp + d.W;
+  const uint32_t base = (tile.w0 / kElemTileWords) * kElemTileWords + threadIdx.x * kWPT;
+  const int tloc = (int)(blockIdx.x);  // index of this tile within the stage
+  if (op.type == EOP_CHECK) {
+    const uint32_t lo = d.view_lo[b * COH_MAX_VIEWS + tile.view], hi = d.view_hi[b * COH_MAX_VIEWS + tile.view];
+    const uint32_t a = (op.lo >> (2 * tile.view)) & 3u;  // abstract pair of the view
+    uint32_t l[kWPT], r[kWPT];
+    uint32_t f = 0;
+    if (a != 2u) load8(Lp + base, l);   // (I,V) needs only R
+    if (a != 1u) load8(Rp + base, r);   // (V,I) needs only L
+#pragma unroll
+    for (int k = 0; k < kWPT; ++k) {
+      const uint32_t m = word_mask(base + k, lo, hi);
+      if (a != 2u && (~l[k] & m)) f |= 1u;
+      if (a != 1u && (~r[k] & m)) f |= 2u;
+      if (a == 0u && ((l[k] | r[k]) & m)) f |= 4u;
+    }
+    f = block_or(f, red);
+    if (threadIdx.x == 0 && f) atomicOr(&d.sc[b].view_flags[tile.view], f);
+    return;
+  }
+  const uint32_t lo = op.lo, hi = op.hi;
+  uint32_t m[kWPT];
+#pragma unroll
+  for (int k = 0; k < kWPT; ++k) m[k] = word_mask(base + k, lo, hi);
+  if (op.type == EOP_WRITE) {  // set plane op.plane, clear the other (w x[i] @site)
+    uint32_t* sp = op.plane ? Rp : Lp;
+    uint32_t* cp = op.plane ? Lp : Rp;
+    uint32_t s[kWPT], c[kWPT];
+    load8(sp + base, s);
+    load8(cp + base, c);
+#pragma unroll
+    for (int k = 0; k < kWPT; ++k) {
+      s[k] |= m[k];
+      c[k] &= ~m[k];
+    }
+    store8(sp + base, s);
+    store8(cp + base, c);
+    return;
+  }
+  // SYNC / READ: first zero of the required (source) plane
+  const uint32_t* src = op.plane ? Rp : Lp;
+  uint32_t v[kWPT];
+  load8(src + base, v);
+  uint32_t fz = kNoCell;
+#pragma unroll
+  for (int k = kWPT - 1; k >= 0; --k) {
+    const uint32_t z = ~v[k] & m[k];
+    if (z) fz = (base + k) * 32u + (__ffs(z) - 1);
+  }
+  fz = block_min(fz, red);
+  if (threadIdx.x == 0 && fz != kNoCell) atomicMin(&d.sc[b].first_zero, fz);
+  if (op.type != EOP_SYNC) return;
+  // destination zero runs: counts for the offsets, and the tile's edge bits
+  const uint32_t* dst = op.plane ? Lp : Rp;
+  uint32_t z[kWPT], sts[kWPT], ens[kWPT];
+  load8(dst + base, v);
+#pragma unroll
+  for (int k = 0; k < kWPT; ++k) z[k] = ~v[k] & m[k];
+  s_first[threadIdx.x] = z[0];
+  s_last[threadIdx.x] = z[kWPT - 1];
+  const uint32_t tstart = (tile.w0 / kElemTileWords) * kElemTileWords;
+  uint32_t edge_prev = 0, edge_next = 0;
+  if (threadIdx.x == 0 && tstart > 0) {
+    const uint32_t w = tstart - 1;
+    edge_prev = (~dst[w] & word_mask(w, lo, hi)) >> 31;
+  }
+  __shared__ uint32_t s_next;
+  if (threadIdx.x == kET - 1) {
+    if (tstart + kElemTileWords < d.W) {
+      const uint32_t w = tstart + kElemTileWords;
+      edge_next = ~dst[w] & word_mask(w, lo, hi) & 1u;
+    }
+    s_next = edge_next;
+  }
+  __syncthreads();
+  const uint32_t pt = threadIdx.x ? (s_last[threadIdx.x - 1] >> 31) : edge_prev;
+  const uint32_t nb = threadIdx.x < kET - 1 ? (s_first[threadIdx.x + 1] & 1u) : edge_next;
+  run_edges(z, pt, nb, sts, ens);
+  uint32_t ns = 0, ne = 0, nz = 0;
+#pragma unroll
+  for (int k = 0; k < kWPT; ++k) {
+    ns += __popc(sts[k]);
+    ne += __popc(ens[k]);
+    nz += __popc(z[k]);
+  }
+  ns = block_sum(ns, red);
+  ne = block_sum(ne, red);
+  nz = block_sum(nz, red);
+  if (threadIdx.x == 0) {
+    d.tcnt[4 * tloc + 0] = ns;
+    d.tcnt[4 * tloc + 1] = ne;
+    d.tcnt[4 * tloc + 2] = nz;
+    d.tcnt[4 * tloc + 3] = edge_prev | (s_next << 1);
+  }
+}
+
+__global__ void k_elem_decide(const ElemDev d) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= d.n_progs) return;
+  const ElemOp op = d.ops[b];
+  ElemState& st = d.st[b];
+  ElemScratch& sc = d.sc[b];
+  if (op.type != EOP_NONE && !st.dead) {
+    if (op.type == EOP_SYNC || op.type == EOP_READ) {
+      const uint32_t fz = sc.first_zero;
+      if (fz != kNoCell) {
+        const uint32_t* Lp = d.planes + (size_t)b * 2u * d.W;
+        const uint32_t* Rp = Lp + d.W;
+        st.dead = 1;
+        st.stuck_op = d.stage;
+        st.stuck_cell = fz;
+        st.stuck_pair = ((Lp[fz >> 5] >> (fz & 31u)) & 1u) | (((Rp[fz >> 5] >> (fz & 31u)) & 1u) << 1);
+      } else if (op.type == EOP_SYNC) {
+        const uint32_t t0 = op.tile0;  // stage-local tile index
+        const uint32_t n_t = ((op.hi >> 5) / kElemTileWords) - ((op.lo >> 5) / kElemTileWords) + 1;
+        unsigned long long bs = st.n_runs, be = st.n_runs, zeros = 0;
+        for (uint32_t k = 0; k < n_t; ++k) {
+          const uint32_t* c = d.tcnt + 4 * (t0 + k);
+          d.tbase[2 * (t0 + k)] = bs;
+          d.tbase[2 * (t0 + k) + 1] = be;
+          bs += c[0];
+          be += c[1];
+          zeros += c[2];
+        }
+        st.n_runs = bs;
+        st.transfers += 1;
+        st.transfer_cells += zeros;
+      }
+    } else if (op.type == EOP_CHECK) {
+      bool ok = true;
+      for (uint32_t v = 0; v < op.plane; ++v) {
+        const uint32_t a = (op.lo >> (2 * v)) & 3u, f = sc.view_flags[v];
+        // leq(a, cell) for every cell of the view (Appendix B of SURVEY):
+        // (V,I): L all 1; (I,V): R all 1; (V,V): both; (I,I): L|R all 0
+        const bool okv = a == 1u ? !(f & 1u) : a == 2u ? !(f & 2u) : a == 3u ? !(f & 3u) : !(f & 4u);
+        ok = ok && okv;
+      }
+      st.calls_done += 1;
+      if (!ok) st.violations += 1;
+      else if (d.boundary) d.boundary[(size_t)b * d.bwords + op.call / 32] |= 1u << (op.call % 32);
+    }
+  }
+  sc.first_zero = kNoCell;
+  for (int v = 0; v < COH_MAX_VIEWS; ++v) sc.view_flags[v] = 0;
+}
+
+__global__ void __launch_bounds__(kET) k_elem_apply(const ElemDev d) {
+  __shared__ uint32_t red[kET / 32];
+  __shared__ uint32_t s_first[kET], s_last[kET];
+  const ElemTile tile = d.tiles[blockIdx.x];
+  const uint32_t b = tile.b;
+  const ElemOp op = d.ops[b];
+  if (op.type != EOP_SYNC || d.st[b].dead) return;
+  uint32_t* Lp = d.planes + (size_t)b * 2u * d.W;
+  uint32_t* Rp = Lp + d.W;
+  uint32_t* dst = op.plane ? Lp : Rp;
+  const uint32_t base = (tile.w0 / kElemTileWords) * kElemTileWords + threadIdx.x * kWPT;
+  const int tloc = (int)blockIdx.x;
+  uint32_t v[kWPT], m[kWPT], z[kWPT], sts[kWPT], ens[kWPT];
+  load8(dst + base, v);
+#pragma unroll
+  for (int k = 0; k < kWPT; ++k) {
+    m[k] = word_mask(base + k, op.lo, op.hi);
+    z[k] = ~v[k] & m[k];
+  }
+  s_first[threadIdx.x] = z[0];
+  s_last[threadIdx.x] = z[kWPT - 1];
+  __syncthreads();
+  const uint32_t edges = d.tcnt[4 * tloc + 3];
+  const uint32_t pt = threadIdx.x ? (s_last[threadIdx.x - 1] >> 31) : (edges & 1u);
+  const uint32_t nb = threadIdx.x < kET - 1 ? (s_first[threadIdx.x + 1] & 1u) : (edges >> 1);
+  run_edges(z, pt, nb, sts, ens);
+  if (d.runs_cap) {
+    uint32_t ns = 0, ne = 0;
+#pragma unroll
+    for (int k = 0; k < kWPT; ++k) {
+      ns += __popc(sts[k]);
+      ne += __popc(ens[k]);
+    }
+    unsigned long long os = d.tbase[2 * tloc] + block_excl_scan(ns, red);
+    unsigned long long oe = d.tbase[2 * tloc + 1] + block_excl_scan(ne, red);
+    const size_t arena = (size_t)b * d.runs_cap;
+#pragma unroll
+    for (int k = 0; k < kWPT; ++k) {
+      for (uint32_t x = sts[k]; x; x &= x - 1, ++os)
+        if (os < d.runs_cap) d.runs_lo[arena + os] = (base + k) * 32u + (__ffs(x) - 1);
+      for (uint32_t x = ens[k]; x; x &= x - 1, ++oe)
+        if (oe < d.runs_cap) d.runs_hi[arena + oe] = (base + k) * 32u + (__ffs(x) - 1);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kWPT; ++k) v[k] |= m[k];
+  store8(dst + base, v);
+}
+
+int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, bool has_sync, void* stream, std::string* err) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n_tiles) k_elem_pass1<<<n_tiles, kET, 0, s>>>(d);
+  k_elem_decide<<<(d.n_progs + 127) / 128, 128, 0, s>>>(d);
+  if (has_sync && n_tiles) k_elem_apply<<<n_tiles, kET, 0, s>>>(d);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("element stage launch: ") + cudaGetErrorString(e);
+    return COH_E_CUDA;
+  }
+  return COH_OK;
+}
+
+// Initial store: every cell (V,I) -> L = 1 on [0, n_cells), R = 0.
+__global__ void k_elem_init(uint32_t* planes, uint32_t W, const uint32_t* n_cells, uint32_t n_progs) {
+  const uint64_t total = (uint64_t)n_progs * 2u * W;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = (uint32_t)(i / (2u * W));
+    const uint32_t r = (uint32_t)(i - (uint64_t)b * 2u * W);
+    uint32_t v = 0;
+    if (r < W) {
+      const uint32_t n = n_cells[b], w = r;
+      v = (w + 1) * 32u <= n ? 0xFFFFFFFFu : (w * 32u < n ? (0xFFFFFFFFu >> (32u - (n - w * 32u))) : 0u);
+    }
+    planes[i] = v;
+  }
+}
+
+int launch_elem_init(uint32_t* planes, uint32_t W, const uint32_t* n_cells, uint32_t n_progs, void* stream,
+                     std::string* err) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  k_elem_init<<<148 * 8, 256, 0, s>>>(planes, W, n_cells, n_progs);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("element init launch: ") + cudaGetErrorString(e);
+    return COH_E_CUDA;
+  }
+  return COH_OK;
+}
+
+}  // namespace cohb

@@ -1,0 +1,494 @@
+// Element-granular path, host side: program generator, overlap closure, and the compiler
+// that turns each program into a per-buffer list of device ops plus a host-known step
+// timeline.  Everything that depends only on abstract keys runs here (the abstract pairs
+// of views evolve independently of concrete cells, which can only stop a run by getting
+// stuck); every concrete cell operation runs on the device.
+//
+//   overlap closure   infer_overlap_closure, overlap.hpp:182-230 (+ overlaps :17-20)
+//   translation       translate_mode / translate_block, modes.hpp:31-59
+//   stepping / fuel   run, semantics.hpp:253-287 (Done before fuel; If = one step;
+//                     an element range op = one step per cell)
+//   abstract effects  effect_signature / apply_signature, validity.hpp:79-120 (swap rule
+//                     semantics.hpp:109-130)
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "elem.hpp"
+#include "gen_common.h"
+#include "internal.hpp"
+
+namespace cohb {
+namespace {
+
+int apply_pair(uint32_t eff, uint32_t site, uint32_t p) {
+  uint32_t q = site ? (((p & 1u) << 1) | (p >> 1)) : p;
+  int r;
+  switch (eff) {
+    case COH_PUSH: r = (q & 1u) ? 3 : -1; break;
+    case COH_PULL: r = (q & 2u) ? 3 : -1; break;
+    case COH_READ: r = (q & 1u) ? (int)q : -1; break;
+    case COH_WRITE: r = 1; break;
+    default: r = (int)q; break;
+  }
+  if (r < 0) return -1;
+  return site ? (int)((((uint32_t)r & 1u) << 1) | ((uint32_t)r >> 1)) : r;
+}
+
+bool overlaps(const coh_elem_program& P, uint32_t x, uint32_t y) {
+  return x != y && P.view_lo[x] <= P.view_hi[y] && P.view_lo[y] <= P.view_hi[x];
+}
+
+struct Mode {
+  uint32_t view, kind, site;
+};
+
+// infer_overlap_closure for a block with one declared mode: W/RW on x adds RW@site on
+// every overlapping view, appended in view-declaration order (overlap.hpp:212-228); an R
+// infers nothing.  (With a single declared mode no cross-site conflict can arise.)
+std::vector<Mode> closure(const coh_elem_program& P, const coh_elem_call& c) {
+  std::vector<Mode> m{{c.view, c.kind, c.site}};
+  if (c.kind == COH_R) return m;
+  for (uint32_t y = 0; y < P.n_views; ++y)
+    if (overlaps(P, c.view, y)) m.push_back({y, (uint32_t)COH_RW, c.site});
+  return m;
+}
+
+}  // namespace
+
+int elem_compile(const coh_elem_program* progs, uint32_t n, ElemPlan* plan, std::string* err) {
+  plan->n_progs = n;
+  plan->tl.assign(n, {});
+  uint32_t max_cells = 1;
+  std::vector<std::vector<ElemOp>> per(n);
+  uint64_t alg = 0;
+  for (uint32_t b = 0; b < n; ++b) {
+    const coh_elem_program& P = progs[b];
+    if (P.n_cells == 0 || P.n_views > COH_MAX_VIEWS) {
+      *err = "element program " + std::to_string(b) + ": n_cells must be >= 1 and n_views <= 16";
+      return COH_E_CONSTRUCTION;
+    }
+    for (uint32_t v = 0; v < P.n_views; ++v)
+      if (P.view_lo[v] > P.view_hi[v] || P.view_hi[v] >= P.n_cells) {
+        *err = "view v" + std::to_string(v) + " range does not fit its buffer";  // program.hpp:65-68
+        return COH_E_CONSTRUCTION;
+      }
+    max_cells = std::max(max_cells, P.n_cells);
+    ElemPlan::Timeline& T = plan->tl[b];
+    std::vector<ElemOp>& ops = per[b];
+    uint32_t abs[COH_MAX_VIEWS];
+    for (uint32_t v = 0; v < P.n_views; ++v) abs[v] = 1;  // initial_store: (V,I)
+    uint64_t steps = 0;
+    const uint64_t fuel = P.fuel < 0 ? 0 : (uint64_t)P.fuel;
+    bool stop = false;
+    auto fuel_out = [&](uint32_t c) {
+      if (steps < fuel) return false;
+      T.term_status = COH_RUN_FUEL_EXHAUSTED;
+      T.term_call = c;
+      stop = true;
+      return true;
+    };
+    auto emit = [&](uint8_t type, uint8_t plane, uint32_t c, uint32_t lo, uint32_t hi) {
+      ops.push_back(ElemOp{type, plane, (uint16_t)c, lo, hi, 0});
+      T.steps_before.push_back(steps);
+      uint32_t packed = 0;
+      for (uint32_t v = 0; v < P.n_views; ++v) packed |= abs[v] << (2 * v);
+      T.abs_before.push_back(packed);
+    };
+    for (uint32_t c = 0; c < P.n_calls && !stop; ++c) {
+      const coh_elem_call& call = P.calls[c];
+      if (call.view >= P.n_views || call.kind > COH_RW || call.n_body > 2) {
+        *err = "call " + std::to_string(c) + " of program " + std::to_string(b) + " is malformed";
+        return COH_E_CONSTRUCTION;
+      }
+      for (const Mode& m : closure(P, call)) {
+        const uint32_t v = m.view, lo = P.view_lo[v], hi = P.view_hi[v];
+        if (m.kind == COH_R || m.kind == COH_RW) {
+          if (fuel_out(c)) break;
+          steps++;  // if (valid(v^)) / if (gvalid(v^))
+          const bool valid = m.site ? (abs[v] >> 1) & 1u : abs[v] & 1u;
+          if (!valid) {
+            // concrete whole-view sync, Local site (ast.hpp:144): pull needs R, sets L;
+            // push needs L, sets R
+            const uint32_t sync = m.site ? COH_PUSH : COH_PULL;
+            if (fuel_out(c)) break;
+            emit(EOP_SYNC, sync == COH_PULL ? 1 : 0, c, lo, hi);
+            const uint64_t mcells = (uint64_t)(hi - lo + 1);
+            alg += 3 * ((mcells + 7) / 8);  // read src + read dst + write dst (+ 8 B per run at run time)
+            steps++;
+            if (fuel_out(c)) break;
+            const int after = apply_pair(sync, COH_LOCAL, abs[v]);
+            if (after < 0) {
+              T.term_status = COH_RUN_STUCK;
+              T.term_call = c;
+              T.term_effect = (uint8_t)sync;
+              T.term_flags = (uint8_t)(0u | (1u << 1) | (abs[v] << 2));
+              T.term_index = v;
+              stop = true;
+              break;
+            }
+            abs[v] = (uint32_t)after;
+            steps++;
+          }
+        }
+        if (m.kind == COH_W || m.kind == COH_RW) {
+          if (fuel_out(c)) break;
+          abs[v] = (uint32_t)apply_pair(COH_WRITE, m.site, abs[v]);  // w v^ never fails
+          steps++;
+        }
+      }
+      if (stop) break;
+      for (uint32_t k = 0; k < call.n_body && !stop; ++k) {
+        const coh_elem_op& op = call.body[k];
+        const uint32_t vlo = P.view_lo[call.view], len = P.view_hi[call.view] - vlo + 1;
+        if (op.lo > op.hi || op.hi >= len || (op.effect != COH_READ && op.effect != COH_WRITE)) {
+          *err = "body op of call " + std::to_string(c) + " is malformed";
+          return COH_E_CONSTRUCTION;
+        }
+        uint64_t m = (uint64_t)(op.hi - op.lo + 1);
+        if (fuel_out(c)) break;
+        const uint64_t avail = fuel - steps;
+        const bool trunc = avail < m;
+        if (trunc) m = avail;
+        const uint32_t lo = vlo + op.lo, hi = lo + (uint32_t)m - 1;
+        // the plane a read needs / a write sets: local site -> L, remote -> R
+        emit(op.effect == COH_READ ? EOP_READ : EOP_WRITE, op.site ? 1 : 0, c, lo, hi);
+        alg += (op.effect == COH_READ ? 1 : 2) * ((m + 7) / 8);
+        steps += m;
+        if (trunc) {
+          T.term_status = COH_RUN_FUEL_EXHAUSTED;
+          T.term_call = c;
+          stop = true;
+        }
+      }
+      if (stop) break;
+      // abstraction_correct after the completed block: pack every view's abstract pair
+      uint32_t packed = 0;
+      for (uint32_t v = 0; v < P.n_views; ++v) {
+        packed |= abs[v] << (2 * v);
+        const uint64_t mv = (uint64_t)(P.view_hi[v] - P.view_lo[v] + 1);
+        alg += ((abs[v] == 1u || abs[v] == 2u) ? 1 : 2) * ((mv + 7) / 8);
+      }
+      emit(EOP_CHECK, (uint8_t)P.n_views, c, packed, 0);
+      T.calls_checked++;
+    }
+    T.n_ops = (uint32_t)ops.size();
+    T.steps_total = steps;
+    T.abs_final = 0;
+    for (uint32_t v = 0; v < P.n_views; ++v) T.abs_final |= abs[v] << (2 * v);
+  }
+  // stages: op k of every program runs in stage k
+  uint32_t n_stages = 0;
+  for (auto& v : per) n_stages = std::max(n_stages, (uint32_t)v.size());
+  plan->n_stages = n_stages;
+  plan->max_words = ((max_cells + 31) / 32 + 3) & ~3u;
+  plan->ops.assign((size_t)n_stages * n, ElemOp{EOP_NONE, 0, 0, 0, 0, 0});
+  plan->tiles.clear();
+  plan->stage_tile0.assign(n_stages + 1, 0);
+  plan->stage_has_sync.assign(n_stages, 0);
+  for (uint32_t s = 0; s < n_stages; ++s) {
+    plan->stage_tile0[s] = (uint32_t)plan->tiles.size();
+    for (uint32_t b = 0; b < n; ++b) {
+      if (s >= per[b].size()) continue;
+      ElemOp op = per[b][s];
+      op.tile0 = (uint32_t)plan->tiles.size() - plan->stage_tile0[s];  // stage-local
+      auto add_range = [&](uint32_t lo, uint32_t hi, uint16_t view) {
+        const uint32_t w_lo = lo / 32, w_hi = hi / 32;
+        uint16_t idx = 0;
+        for (uint32_t t0 = (w_lo / kElemTileWords) * kElemTileWords; t0 <= w_hi; t0 += kElemTileWords) {
+          const uint32_t a = std::max(t0, w_lo), z = std::min(t0 + kElemTileWords - 1, w_hi);
+          plan->tiles.push_back(ElemTile{b, a, z, view, idx++});
+        }
+      };
+      if (op.type == EOP_CHECK) {
+        for (uint32_t v = 0; v < progs[b].n_views; ++v) add_range(progs[b].view_lo[v], progs[b].view_hi[v], (uint16_t)v);
+      } else {
+        add_range(op.lo, op.hi, 0);
+      }
+      if (op.type == EOP_SYNC) plan->stage_has_sync[s] = 1;
+      plan->ops[(size_t)s * n + b] = op;
+    }
+  }
+  plan->stage_tile0[n_stages] = (uint32_t)plan->tiles.size();
+  plan->alg_bytes = alg;
+  return COH_OK;
+}
+
+}  // namespace cohb
+
+// ---- generator ------------------------------------------------------------------------
+// Views follow the acceptance pattern lo ~ U[0,n), hi = lo + U[0, n-lo)
+// (tests/acceptance.cpp:235-236).  Calls: view ~ U[0,V), kind ~ U{R,W,RW}, site ~ U{L,R};
+// adversarial with probability adv_per1024/1024, else the canonical body:
+//   R: r x[0..len-1]@S   W: w x[0..len-1]@S   RW: r x[0..len-1]@S; w x[a..b]@S
+// adversarial variants: 1 empty, 2 r x[a..b]@O, 3 w x[a..b]@S (partial write),
+//   4 w x[a..b]@O, 5 r x[0..len-1]@S; w x[a..b]@O
+extern "C" int coh_elem_gen(uint64_t seed, uint64_t prog_id, uint32_t n_cells, uint32_t n_views,
+                            uint32_t n_calls, uint32_t adv_per1024, uint32_t* view_lo, uint32_t* view_hi,
+                            coh_elem_call* calls) {
+  if (n_cells == 0 || n_views == 0 || n_views > COH_MAX_VIEWS) return COH_E_ARG;
+  uint64_t k = 0;
+  auto h = [&]() { return coh_splitmix64(seed ^ (prog_id << 24) ^ (k++)); };
+  for (uint32_t v = 0; v < n_views; ++v) {
+    const uint32_t lo = (uint32_t)(h() % n_cells);
+    view_lo[v] = lo;
+    view_hi[v] = lo + (uint32_t)(h() % (uint64_t)(n_cells - lo));
+  }
+  for (uint32_t c = 0; c < n_calls; ++c) {
+    const uint64_t x = h();
+    coh_elem_call& cl = calls[c];
+    std::memset(&cl, 0, sizeof cl);
+    cl.view = (uint32_t)(x % n_views);
+    cl.kind = (uint8_t)((x >> 8) % 3);
+    cl.site = (uint8_t)((x >> 10) & 1);
+    const bool adv = ((x >> 16) & 1023u) < adv_per1024;
+    const uint32_t variant = adv ? 1u + (uint32_t)((x >> 26) % 5) : 0u;
+    const uint32_t len = view_hi[cl.view] - view_lo[cl.view] + 1;
+    const uint32_t a = (uint32_t)(h() % len);
+    const uint32_t b = a + (uint32_t)(h() % (uint64_t)(len - a));
+    const uint8_t S = cl.site, O = (uint8_t)(cl.site ^ 1);
+    auto op = [&](uint8_t eff, uint8_t site, uint32_t lo, uint32_t hi) {
+      coh_elem_op& o = cl.body[cl.n_body++];
+      o.effect = eff;
+      o.site = site;
+      o.lo = lo;
+      o.hi = hi;
+    };
+    switch (variant) {
+      case 0:
+        if (cl.kind == COH_R) op(COH_READ, S, 0, len - 1);
+        else if (cl.kind == COH_W) op(COH_WRITE, S, 0, len - 1);
+        else { op(COH_READ, S, 0, len - 1); op(COH_WRITE, S, a, b); }
+        break;
+      case 1: break;
+      case 2: op(COH_READ, O, a, b); break;
+      case 3: op(COH_WRITE, S, a, b); break;
+      case 4: op(COH_WRITE, O, a, b); break;
+      default: op(COH_READ, S, 0, len - 1); op(COH_WRITE, O, a, b); break;
+    }
+  }
+  return COH_OK;
+}
+
+// ---- C ABI: compile, execute stage by stage, finalise ----------------------------------
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() { cudaFree(p); }
+  template <typename T>
+  T* as() { return static_cast<T*>(p); }
+};
+
+}  // namespace
+
+extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32_t n,
+                             coh_elem_result* results, uint32_t* planes_out, uint32_t plane_words,
+                             uint8_t* view_abs_out, uint32_t* boundary_out, uint32_t boundary_words,
+                             uint32_t* runs_out, uint64_t runs_cap, coh_elem_stats* stats) {
+  using namespace cohb;
+  if (!ctx) return COH_E_ARG;
+  if (n && (!progs || !results)) {
+    ctx->err = "progs/results is NULL";
+    return COH_E_ARG;
+  }
+  if (n == 0) return COH_OK;
+  ElemPlan plan;
+  std::string err;
+  int rc = elem_compile(progs, n, &plan, &err);
+  if (rc) {
+    ctx->err = err;
+    return rc;
+  }
+  const uint32_t W = ((plan.max_words + kElemTileWords - 1) / kElemTileWords) * kElemTileWords;
+  uint32_t bwords = 1;
+  for (uint32_t b = 0; b < n; ++b) bwords = std::max(bwords, (progs[b].n_calls + 31) / 32);
+  if (planes_out) {  // plane_words must hold every program's cells
+    uint32_t need = 0;
+    for (uint32_t b = 0; b < n; ++b) need = std::max(need, (progs[b].n_cells + 31) / 32);
+    if (plane_words < need) {
+      ctx->err = "plane_words too small";
+      return COH_E_ARG;
+    }
+  }
+  if (boundary_out && boundary_words < bwords) {
+    ctx->err = "boundary_words too small";
+    return COH_E_ARG;
+  }
+  uint32_t max_tiles = 1;
+  for (uint32_t s = 0; s < plan.n_stages; ++s)
+    max_tiles = std::max(max_tiles, plan.stage_tile0[s + 1] - plan.stage_tile0[s]);
+
+  DevBuf planes, ops, tiles, st, sc, tcnt, tbase, vlo, vhi, ncell, bnd, rlo, rhi;
+  auto alloc = [&](DevBuf& d, size_t bytes) { return cudaMalloc(&d.p, std::max<size_t>(bytes, 16)); };
+#define COH_E(x)                                                  \
+  do {                                                            \
+    cudaError_t e_ = (x);                                         \
+    if (e_ != cudaSuccess) {                                      \
+      ctx->err = std::string(#x) + ": " + cudaGetErrorString(e_); \
+      return COH_E_CUDA;                                          \
+    }                                                             \
+  } while (0)
+  COH_E(alloc(planes, (size_t)n * 2 * W * 4));
+  COH_E(alloc(ops, plan.ops.size() * sizeof(ElemOp)));
+  COH_E(alloc(tiles, plan.tiles.size() * sizeof(ElemTile)));
+  COH_E(alloc(st, (size_t)n * sizeof(ElemState)));
+  COH_E(alloc(sc, (size_t)n * sizeof(ElemScratch)));
+  COH_E(alloc(tcnt, (size_t)max_tiles * 4 * 4));
+  COH_E(alloc(tbase, (size_t)max_tiles * 2 * 8));
+  COH_E(alloc(vlo, (size_t)n * COH_MAX_VIEWS * 4));
+  COH_E(alloc(vhi, (size_t)n * COH_MAX_VIEWS * 4));
+  COH_E(alloc(ncell, (size_t)n * 4));
+  COH_E(alloc(bnd, (size_t)n * bwords * 4));
+  if (runs_cap) {
+    COH_E(alloc(rlo, (size_t)n * runs_cap * 4));
+    COH_E(alloc(rhi, (size_t)n * runs_cap * 4));
+  }
+  std::vector<uint32_t> h_vlo((size_t)n * COH_MAX_VIEWS, 0), h_vhi((size_t)n * COH_MAX_VIEWS, 0), h_nc(n);
+  for (uint32_t b = 0; b < n; ++b) {
+    h_nc[b] = progs[b].n_cells;
+    for (uint32_t v = 0; v < progs[b].n_views; ++v) {
+      h_vlo[(size_t)b * COH_MAX_VIEWS + v] = progs[b].view_lo[v];
+      h_vhi[(size_t)b * COH_MAX_VIEWS + v] = progs[b].view_hi[v];
+    }
+  }
+  std::vector<ElemScratch> h_sc(n);
+  for (auto& x : h_sc) {
+    x.first_zero = kNoCell;
+    for (auto& f : x.view_flags) f = 0;
+  }
+  if (!ctx->hs[0]) COH_E(cudaStreamCreateWithFlags(&ctx->hs[0], cudaStreamNonBlocking));
+  cudaStream_t s = ctx->hs[0];
+  COH_E(cudaMemcpyAsync(ops.p, plan.ops.data(), plan.ops.size() * sizeof(ElemOp), cudaMemcpyHostToDevice, s));
+  if (!plan.tiles.empty())
+    COH_E(cudaMemcpyAsync(tiles.p, plan.tiles.data(), plan.tiles.size() * sizeof(ElemTile), cudaMemcpyHostToDevice, s));
+  COH_E(cudaMemcpyAsync(vlo.p, h_vlo.data(), h_vlo.size() * 4, cudaMemcpyHostToDevice, s));
+  COH_E(cudaMemcpyAsync(vhi.p, h_vhi.data(), h_vhi.size() * 4, cudaMemcpyHostToDevice, s));
+  COH_E(cudaMemcpyAsync(ncell.p, h_nc.data(), h_nc.size() * 4, cudaMemcpyHostToDevice, s));
+  COH_E(cudaMemcpyAsync(sc.p, h_sc.data(), h_sc.size() * sizeof(ElemScratch), cudaMemcpyHostToDevice, s));
+  COH_E(cudaMemsetAsync(st.p, 0, (size_t)n * sizeof(ElemState), s));
+  COH_E(cudaMemsetAsync(bnd.p, 0, (size_t)n * bwords * 4, s));
+  cudaEvent_t e0, e1;
+  COH_E(cudaEventCreate(&e0));
+  COH_E(cudaEventCreate(&e1));
+  COH_E(cudaEventRecord(e0, s));
+  rc = launch_elem_init(planes.as<uint32_t>(), W, ncell.as<uint32_t>(), n, s, &err);
+  uint64_t launches = 1;
+  for (uint32_t stg = 0; stg < plan.n_stages && rc == COH_OK; ++stg) {
+    ElemDev d;
+    d.planes = planes.as<uint32_t>();
+    d.W = W;
+    d.ops = ops.as<ElemOp>() + (size_t)stg * n;
+    d.tiles = tiles.as<ElemTile>() + plan.stage_tile0[stg];
+    d.st = st.as<ElemState>();
+    d.sc = sc.as<ElemScratch>();
+    d.tcnt = tcnt.as<uint32_t>();
+    d.tbase = tbase.as<unsigned long long>();
+    d.view_lo = vlo.as<uint32_t>();
+    d.view_hi = vhi.as<uint32_t>();
+    d.boundary = bnd.as<uint32_t>();
+    d.bwords = bwords;
+    d.runs_lo = rlo.as<uint32_t>();
+    d.runs_hi = rhi.as<uint32_t>();
+    d.runs_cap = runs_cap;
+    d.n_progs = n;
+    d.stage = stg;
+    const uint32_t nt = plan.stage_tile0[stg + 1] - plan.stage_tile0[stg];
+    rc = launch_elem_stage(d, nt, plan.stage_has_sync[stg] != 0, s, &err);
+    launches += (nt ? 1 : 0) + 1 + ((plan.stage_has_sync[stg] && nt) ? 1 : 0);
+  }
+  COH_E(cudaEventRecord(e1, s));
+  if (rc) {
+    ctx->err = err;
+    cudaStreamSynchronize(s);
+    return rc;
+  }
+  std::vector<ElemState> h_st(n);
+  COH_E(cudaMemcpyAsync(h_st.data(), st.p, (size_t)n * sizeof(ElemState), cudaMemcpyDeviceToHost, s));
+  std::vector<uint32_t> h_bnd;
+  if (boundary_out) {
+    h_bnd.resize((size_t)n * bwords);
+    COH_E(cudaMemcpyAsync(h_bnd.data(), bnd.p, h_bnd.size() * 4, cudaMemcpyDeviceToHost, s));
+  }
+  if (planes_out)
+    COH_E(cudaMemcpy2DAsync(planes_out, (size_t)plane_words * 4, planes.p, (size_t)W * 4,
+                            (size_t)std::min(plane_words, W) * 4, (size_t)2 * n, cudaMemcpyDeviceToHost, s));
+  std::vector<uint32_t> h_rlo, h_rhi;
+  if (runs_out && runs_cap) {
+    h_rlo.resize((size_t)n * runs_cap);
+    h_rhi.resize((size_t)n * runs_cap);
+    COH_E(cudaMemcpyAsync(h_rlo.data(), rlo.p, h_rlo.size() * 4, cudaMemcpyDeviceToHost, s));
+    COH_E(cudaMemcpyAsync(h_rhi.data(), rhi.p, h_rhi.size() * 4, cudaMemcpyDeviceToHost, s));
+  }
+  COH_E(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ctx->launches += launches;
+
+  uint64_t alg = plan.alg_bytes;
+  for (uint32_t b = 0; b < n; ++b) {
+    const ElemPlan::Timeline& T = plan.tl[b];
+    const ElemState& S = h_st[b];
+    coh_elem_result& r = results[b];
+    std::memset(&r, 0, sizeof r);
+    r.calls_done = S.calls_done;
+    r.violations = S.violations;
+    r.transfers = S.transfers;
+    r.transfer_cells = S.transfer_cells;
+    r.n_runs = S.n_runs;
+    alg += 8 * S.n_runs;
+    uint32_t abs_final = T.abs_final;
+    uint32_t executed_ops = T.n_ops;
+    if (S.dead) {
+      const ElemOp& op = plan.ops[(size_t)S.stuck_op * n + b];
+      executed_ops = S.stuck_op;
+      r.status = COH_RUN_STUCK;
+      r.stuck_call = op.call;
+      r.stuck_index = S.stuck_cell;
+      const uint32_t site = op.type == EOP_READ ? op.plane : 0u;
+      r.stuck_effect = (uint8_t)(op.type == EOP_READ ? COH_READ : (op.plane ? COH_PULL : COH_PUSH));
+      r.stuck_flags = (uint8_t)(site | (S.stuck_pair << 2));
+      r.steps = T.steps_before[S.stuck_op] + (op.type == EOP_READ ? (uint64_t)(S.stuck_cell - op.lo) : 0u);
+      abs_final = T.abs_before[S.stuck_op];
+    } else {
+      r.status = T.term_status;
+      r.steps = T.steps_total;
+      if (T.term_status != COH_RUN_DONE) {
+        r.stuck_call = T.term_call;
+        r.stuck_effect = T.term_effect;
+        r.stuck_flags = T.term_flags;
+        r.stuck_index = T.term_index;
+      }
+    }
+    // VectorPU-faithful transfer size: the whole view range of every executed sync
+    for (uint32_t k = 0; k < executed_ops; ++k) {
+      const ElemOp& op = plan.ops[(size_t)k * n + b];
+      if (op.type == EOP_SYNC) r.vpu_cells += (uint64_t)(op.hi - op.lo + 1);
+    }
+    if (view_abs_out)
+      for (uint32_t v = 0; v < COH_MAX_VIEWS; ++v)
+        view_abs_out[(size_t)b * COH_MAX_VIEWS + v] = v < progs[b].n_views ? (uint8_t)((abs_final >> (2 * v)) & 3u) : 0;
+    if (boundary_out)
+      for (uint32_t w = 0; w < boundary_words; ++w)
+        boundary_out[(size_t)b * boundary_words + w] = w < bwords ? h_bnd[(size_t)b * bwords + w] : 0u;
+    if (runs_out && runs_cap) {
+      const uint64_t m = std::min<uint64_t>(S.n_runs, runs_cap);
+      for (uint64_t k = 0; k < m; ++k) {
+        runs_out[((size_t)b * runs_cap + k) * 2] = h_rlo[(size_t)b * runs_cap + k];
+        runs_out[((size_t)b * runs_cap + k) * 2 + 1] = h_rhi[(size_t)b * runs_cap + k];
+      }
+    }
+  }
+  if (stats) {
+    stats->device_ms = ms;
+    stats->alg_bytes = alg;
+    stats->launches = launches;
+    stats->tiles = plan.tiles.size();
+    stats->stages = plan.n_stages;
+    stats->pad = 0;
+  }
+  return COH_OK;
+#undef COH_E
+}

@@ -1,6 +1,8 @@
 // Internal declarations shared by the host runtime (.cpp) and the CUDA sources (.cu).
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdint>
 #include <string>
 
@@ -86,3 +88,22 @@ int launch_reduce_counters(const coh_trace_result* d_results, uint64_t n_traces,
                            uint64_t* d_counters, void* stream, std::string* err);
 
 }  // namespace cohb
+
+// The context behind the opaque coh_ctx handle (capi.cpp, elem_host.cpp).
+struct coh_ctx {
+  int device = 0;
+  std::string err;
+  uint32_t* d_lut = nullptr;
+  uint32_t* d_slow = nullptr;
+  uint64_t* d_bytes = nullptr;
+  int sms = 148;
+  int blocks_per_sm = 1;       // narrow (u16) trace_eval
+  int blocks_per_sm_wide = 1;  // wide (u32) trace_eval
+  uint64_t launches = 0;
+  // host-buffer pipeline
+  cudaStream_t hs[2] = {nullptr, nullptr};
+  uint16_t* d_rec[2] = {nullptr, nullptr};
+  coh_trace_result* d_res[2] = {nullptr, nullptr};
+  uint32_t* d_bnd[2] = {nullptr, nullptr};
+  size_t rec_cap = 0, res_cap = 0, bnd_cap = 0;  // bytes per buffer
+};

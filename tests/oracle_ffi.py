@@ -106,3 +106,30 @@ def orc_gen(seed, trace0, n_traces, n_calls, n_arrays, adv):
     out = np.zeros(records_elems(n_traces, n_calls), dtype=np.uint16)
     oracle().orc_gen_records(seed, trace0, n_traces, n_calls, n_arrays, adv, out.ctypes.data)
     return out
+
+
+# ---- element programs -------------------------------------------------------------------
+def _elem_fn(lib, name):
+    f = getattr(lib, name)
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p] * 7 + [C.c_uint64]
+    return f
+
+
+def elem_run(which, program, runs_cap=4096):
+    """Run one element program on the C oracle ('orc') or the reference ('ref')."""
+    from paper_1910_11110_b200.elem import ElemResult
+
+    lib_, name = (oracle(), "orc_elem_run") if which == "orc" else (reference(), "ref_elem_run")
+    f = _elem_fn(lib_, name)
+    st = program.struct()
+    r = ElemResult()
+    pw = (program.n_cells + 31) // 32
+    L = np.zeros(pw, np.uint32)
+    R = np.zeros(pw, np.uint32)
+    va = np.zeros(16, np.uint8)
+    b = np.zeros(max(1, (program.n_calls + 31) // 32), np.uint32)
+    runs = np.zeros((max(1, runs_cap), 2), np.uint32)
+    rc = f(C.addressof(st), C.addressof(r), L.ctypes.data, R.ctypes.data, va.ctypes.data, b.ctypes.data,
+           runs.ctypes.data, runs_cap)
+    return rc, r, L, R, va, b, runs[: min(r.n_runs, runs_cap)]

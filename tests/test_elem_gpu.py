@@ -1,0 +1,77 @@
+"""GPU parity tests of the element-granular path (bit planes, whole-view syncs with
+transfer-range extraction, element range effects, per-view boundary checks): bit-exact
+against the reference's golden fixtures, the C oracle at up to 2^24 cells, and batch
+invariance."""
+import numpy as np
+import pytest
+
+import oracle_ffi as o
+from paper_1910_11110_b200.elem import Program, elem_eval
+from test_elem_oracle import golden_programs
+
+pytestmark = pytest.mark.gpu
+
+
+def compare(out, i, want, key, runs_cap=4096):
+    r = out["results"][i]
+    assert np.array_equal(np.array(r.as_tuple(), np.uint64), want["result"]), (key, r.as_tuple(), want["result"])
+    pw = want["planes"].shape[1]
+    assert np.array_equal(out["planes"][i][:, :pw], want["planes"]), key
+    nv = len(want["view_abs"])
+    assert np.array_equal(out["view_abs"][i][:nv], want["view_abs"]), key
+    bw = len(want["boundary"])
+    assert np.array_equal(out["boundary"][i][:bw], want["boundary"]), key
+    m = min(int(r.n_runs), runs_cap)
+    assert np.array_equal(out["runs"][i][:m], want["runs"][:m]), key
+
+
+def test_golden_batch(ctx):
+    items = list(golden_programs())
+    out = elem_eval(ctx, [p for _, _, p, _ in items])
+    for i, (key, params, p, want) in enumerate(items):
+        compare(out, i, want, key)
+
+
+def test_golden_one_by_one(ctx):
+    for key, params, p, want in list(golden_programs())[:12]:
+        compare(elem_eval(ctx, [p]), 0, want, key)
+
+
+def oracle_want(p, runs_cap=1 << 16):
+    rc, r, L, R, va, b, runs = o.elem_run("orc", p, runs_cap)
+    assert rc in (0, -3)
+    return {"result": np.array(r.as_tuple(), np.uint64), "planes": np.stack([L, R]), "view_abs": va,
+            "boundary": b, "runs": runs}
+
+
+@pytest.mark.parametrize("n_cells,n_progs,adv", [(1 << 16, 16, 64), (1 << 20, 8, 128), ((1 << 20) + 37, 4, 1024),
+                                                 (1 << 24, 2, 64)])
+def test_vs_oracle_large(ctx, n_cells, n_progs, adv):
+    progs = [Program.generate(5, i, n_cells, 8, 12, adv) for i in range(n_progs)]
+    out = elem_eval(ctx, progs, runs_cap=1 << 16)
+    for i, p in enumerate(progs):
+        compare(out, i, oracle_want(p), f"n={n_cells} prog={i}", runs_cap=1 << 16)
+
+
+def test_fuel_limited_vs_oracle(ctx):
+    progs = [Program.generate(6, i, 5000, 6, 10, 300, fuel=f) for i, f in enumerate([0, 1, 2, 3, 50, 777, 4999, 30000])]
+    out = elem_eval(ctx, progs)
+    for i, p in enumerate(progs):
+        compare(out, i, oracle_want(p), f"fuel prog {i}")
+
+
+def test_runs_capacity_overflow_counts_everything(ctx):
+    p = Program.generate(8, 3, 1 << 16, 8, 16, 1024)
+    full = elem_eval(ctx, [p], runs_cap=1 << 16)
+    small = elem_eval(ctx, [p], runs_cap=4)
+    assert small["results"][0].n_runs == full["results"][0].n_runs
+    assert np.array_equal(small["runs"][0][:4], full["runs"][0][:4])
+
+
+def test_malformed_program_is_construction_error(ctx):
+    import paper_1910_11110_b200 as coh
+
+    bad = Program(100, [10], [200], [(0, 0, 0, [])])  # view outside its buffer
+    with pytest.raises(coh.CohError) as e:
+        elem_eval(ctx, [bad])
+    assert e.value.code == 1
