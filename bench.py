@@ -39,6 +39,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=3.0, help="wall seconds of the CPU baseline sample")
+    ap.add_argument("--bitmap-buffers", type=int, default=256, help="C3 buffers per GPU (0 = skip)")
+    ap.add_argument("--bitmap-log2-cells", type=int, default=24)
+    ap.add_argument("--bitmap-calls", type=int, default=8)
     return ap.parse_args()
 
 
@@ -198,6 +201,46 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- bitmaps (C3)
+def run_bitmap(args, ctx, rank, world):
+    """BASELINE config 3 per GPU: B buffers x 2^24 cells, 8 overlapping views each, K calls
+    per buffer through the element path (overlap closure, whole-view syncs + transfer-range
+    extraction, element range bodies, per-view boundary checks).  Algorithmic bytes per
+    SURVEY §8(d); device time by CUDA events inside coh_elem_eval; max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1910_11110_b200.elem import Program, elem_eval
+
+    B, n, K = args.bitmap_buffers, 1 << args.bitmap_log2_cells, args.bitmap_calls
+    progs = [Program.generate(3, rank * B + b, n, 8, K, 64) for b in range(B)]
+    elem_eval(ctx, progs[: max(1, B // 8)], want_planes=False, runs_cap=0)  # warm
+    best = None
+    for _ in range(3):
+        out = elem_eval(ctx, progs, want_planes=False, runs_cap=0)
+        st = out["stats"]
+        if best is None or st.device_ms < best[0]:
+            best = (st.device_ms, st.alg_bytes, st.stages, st.launches)
+    ms, alg, stages, launches = best
+    if world > 1:
+        t = torch.tensor([ms, float(alg)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t[0:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:2])
+        ms, alg = float(t[0].item()), int(t[1].item())
+    peak, src = peaks()
+    gbs = alg / (ms / 1e3) / 1e9
+    res = out["results"]
+    return {"metric": "bitmap GB/s (algorithmic bytes / device time)", "value": gbs, "unit": "GB/s",
+            "frac": gbs / peak, "peak": peak, "peak_source": src, "device_ms": ms, "alg_bytes": alg,
+            "stages": stages, "launches": launches,
+            "config": {"workload": "C3: element-granular bit planes, overlapping views", "buffers_per_gpu": B,
+                       "cells": n, "views": 8, "calls": K, "adv_per1024": 64,
+                       "l2": "1 GiB of planes per GPU > L2, no flush"},
+            "outcomes": {"stuck": sum(1 for i in range(B) if res[i].status == 1),
+                         "transfers": sum(res[i].transfers for i in range(B)),
+                         "runs": sum(res[i].n_runs for i in range(B))}}
+
+
 # ---------------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local):
     import torch
@@ -307,6 +350,7 @@ def run_ours(args, rank, world, local):
                "ms_per_step": 1e3 * dt / args.e2e_steps}
         for p in (p_rec, p_res, p_bnd):
             L.coh_host_free(p)
+    bitmap = run_bitmap(args, ctx, rank, world) if args.bitmap_buffers > 0 else None
     clocks.stop()
 
     cpu = None
@@ -330,6 +374,7 @@ def run_ours(args, rank, world, local):
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms": k_ms,
                          "note": "INT/LSU-issue bound in practice; see profiles/ for pipe utilisation"},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "gpu_launches": launches,
+            "bitmap": bitmap,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -219,60 +219,92 @@ __global__ void __launch_bounds__(kET) k_elem_pass1(const ElemDev d) {
   }
 }
 
-__global__ void k_elem_decide(const ElemDev d) {
-  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per buffer: stuck detection, run-offset scan over the op's tiles (32 tiles
+// per warp step, shuffle scan), boundary bit, scratch reset.
+constexpr int kDecideWarps = 4;
+__global__ void __launch_bounds__(32 * kDecideWarps) k_elem_decide(const ElemDev d) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t b = blockIdx.x * kDecideWarps + (threadIdx.x >> 5);
   if (b >= d.n_progs) return;
   const ElemOp op = d.ops[b];
-  ElemState& st = d.st[b];
-  ElemScratch& sc = d.sc[b];
-  if (op.type != EOP_NONE && !st.dead) {
+  ElemState* __restrict__ st = d.st + b;
+  ElemScratch* __restrict__ sc = d.sc + b;
+  const uint32_t dead = st->dead;
+  __syncwarp();
+  if (op.type != EOP_NONE && !dead) {
     if (op.type == EOP_SYNC || op.type == EOP_READ) {
-      const uint32_t fz = sc.first_zero;
+      const uint32_t fz = sc->first_zero;
       if (fz != kNoCell) {
-        const uint32_t* Lp = d.planes + (size_t)b * 2u * d.W;
-        const uint32_t* Rp = Lp + d.W;
-        st.dead = 1;
-        st.stuck_op = d.stage;
-        st.stuck_cell = fz;
-        st.stuck_pair = ((Lp[fz >> 5] >> (fz & 31u)) & 1u) | (((Rp[fz >> 5] >> (fz & 31u)) & 1u) << 1);
+        if (lane == 0) {
+          const uint32_t* Lp = d.planes + (size_t)b * 2u * d.W;
+          const uint32_t* Rp = Lp + d.W;
+          st->dead = 1;
+          st->stuck_op = d.stage;
+          st->stuck_cell = fz;
+          st->stuck_pair = ((Lp[fz >> 5] >> (fz & 31u)) & 1u) | (((Rp[fz >> 5] >> (fz & 31u)) & 1u) << 1);
+        }
       } else if (op.type == EOP_SYNC) {
         const uint32_t t0 = op.tile0;  // stage-local tile index
         const uint32_t n_t = ((op.hi >> 5) / kElemTileWords) - ((op.lo >> 5) / kElemTileWords) + 1;
-        unsigned long long bs = st.n_runs, be = st.n_runs, zeros = 0;
-        for (uint32_t k = 0; k < n_t; ++k) {
-          const uint32_t* c = d.tcnt + 4 * (t0 + k);
-          d.tbase[2 * (t0 + k)] = bs;
-          d.tbase[2 * (t0 + k) + 1] = be;
-          bs += c[0];
-          be += c[1];
-          zeros += c[2];
+        const unsigned long long run0 = st->n_runs;
+        unsigned long long cs = 0, ce = 0, zeros = 0;
+        for (uint32_t k0 = 0; k0 < n_t; k0 += 32) {
+          const uint32_t k = k0 + lane;
+          uint32_t ns = 0, ne = 0, nz = 0;
+          if (k < n_t) {
+            const uint4 c = *reinterpret_cast<const uint4*>(d.tcnt + 4 * (t0 + k));
+            ns = c.x;
+            ne = c.y;
+            nz = c.z;
+          }
+          uint32_t xs = ns, xe = ne;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t ys = __shfl_up_sync(0xffffffffu, xs, o), ye = __shfl_up_sync(0xffffffffu, xe, o);
+            if (lane >= (uint32_t)o) {
+              xs += ys;
+              xe += ye;
+            }
+          }
+          if (k < n_t) {
+            d.tbase[2 * (t0 + k)] = run0 + cs + xs - ns;
+            d.tbase[2 * (t0 + k) + 1] = run0 + ce + xe - ne;
+          }
+          cs += __shfl_sync(0xffffffffu, xs, 31);
+          ce += __shfl_sync(0xffffffffu, xe, 31);
+          zeros += __reduce_add_sync(0xffffffffu, nz);
         }
-        st.n_runs = bs;
-        st.transfers += 1;
-        st.transfer_cells += zeros;
+        if (lane == 0) {
+          st->n_runs = run0 + cs;
+          st->transfers += 1;
+          st->transfer_cells += zeros;
+        }
       }
     } else if (op.type == EOP_CHECK) {
-      bool ok = true;
-      for (uint32_t v = 0; v < op.plane; ++v) {
-        const uint32_t a = (op.lo >> (2 * v)) & 3u, f = sc.view_flags[v];
-        // leq(a, cell) for every cell of the view (Appendix B of SURVEY):
+      bool okv = true;
+      if (lane < op.plane) {
+        const uint32_t a = (op.lo >> (2 * lane)) & 3u, f = sc->view_flags[lane];
+        // leq(a, cell) for every cell of the view:
         // (V,I): L all 1; (I,V): R all 1; (V,V): both; (I,I): L|R all 0
-        const bool okv = a == 1u ? !(f & 1u) : a == 2u ? !(f & 2u) : a == 3u ? !(f & 3u) : !(f & 4u);
-        ok = ok && okv;
+        okv = a == 1u ? !(f & 1u) : a == 2u ? !(f & 2u) : a == 3u ? !(f & 3u) : !(f & 4u);
       }
-      st.calls_done += 1;
-      if (!ok) st.violations += 1;
-      else if (d.boundary) d.boundary[(size_t)b * d.bwords + op.call / 32] |= 1u << (op.call % 32);
+      const bool ok = __all_sync(0xffffffffu, okv);
+      if (lane == 0) {
+        st->calls_done += 1;
+        if (!ok) st->violations += 1;
+        else if (d.boundary) d.boundary[(size_t)b * d.bwords + op.call / 32] |= 1u << (op.call % 32);
+      }
     }
   }
-  sc.first_zero = kNoCell;
-  for (int v = 0; v < COH_MAX_VIEWS; ++v) sc.view_flags[v] = 0;
+  if (lane == 0) sc->first_zero = kNoCell;
+  if (lane < COH_MAX_VIEWS) sc->view_flags[lane] = 0;
 }
 
 __global__ void __launch_bounds__(kET) k_elem_apply(const ElemDev d) {
   __shared__ uint32_t red[kET / 32];
   __shared__ uint32_t s_first[kET], s_last[kET];
-  const ElemTile tile = d.tiles[blockIdx.x];
+  const int tloc = (int)d.sync_tiles[blockIdx.x];  // stage-local tile index of a SYNC op
+  const ElemTile tile = d.tiles[tloc];
   const uint32_t b = tile.b;
   const ElemOp op = d.ops[b];
   if (op.type != EOP_SYNC || d.st[b].dead) return;
@@ -280,7 +312,6 @@ __global__ void __launch_bounds__(kET) k_elem_apply(const ElemDev d) {
   uint32_t* Rp = Lp + d.W;
   uint32_t* dst = op.plane ? Lp : Rp;
   const uint32_t base = (tile.w0 / kElemTileWords) * kElemTileWords + threadIdx.x * kWPT;
-  const int tloc = (int)blockIdx.x;
   uint32_t v[kWPT], m[kWPT], z[kWPT], sts[kWPT], ens[kWPT];
   load8(dst + base, v);
 #pragma unroll
@@ -318,11 +349,11 @@ __global__ void __launch_bounds__(kET) k_elem_apply(const ElemDev d) {
   store8(dst + base, v);
 }
 
-int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, bool has_sync, void* stream, std::string* err) {
+int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, uint32_t n_sync_tiles, void* stream, std::string* err) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n_tiles) k_elem_pass1<<<n_tiles, kET, 0, s>>>(d);
-  k_elem_decide<<<(d.n_progs + 127) / 128, 128, 0, s>>>(d);
-  if (has_sync && n_tiles) k_elem_apply<<<n_tiles, kET, 0, s>>>(d);
+  k_elem_decide<<<(d.n_progs + kDecideWarps - 1) / kDecideWarps, 32 * kDecideWarps, 0, s>>>(d);
+  if (n_sync_tiles) k_elem_apply<<<n_sync_tiles, kET, 0, s>>>(d);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("element stage launch: ") + cudaGetErrorString(e);

@@ -63,6 +63,8 @@ struct ElemPlan {
   std::vector<ElemTile> tiles;       // all stages concatenated
   std::vector<uint32_t> stage_tile0; // n_stages + 1 offsets into tiles
   std::vector<uint8_t> stage_has_sync;
+  std::vector<uint32_t> sync_tiles;        // stage-local tile indices of SYNC ops, by stage
+  std::vector<uint32_t> stage_sync0;       // n_stages + 1 offsets into sync_tiles
   // host timeline, per program
   struct Timeline {
     std::vector<uint64_t> steps_before;   // per stage (device op) of this program
@@ -88,6 +90,7 @@ struct ElemDev {
   uint32_t W;                  // words per plane (multiple of kElemTileWords)
   const ElemOp* ops;           // this stage, [b]
   const ElemTile* tiles;       // this stage
+  const uint32_t* sync_tiles;  // this stage: tile indices the apply pass visits
   ElemState* st;
   ElemScratch* sc;
   uint32_t* tcnt;              // per tile of this stage: starts, ends, zeros, edge bits
@@ -102,7 +105,7 @@ struct ElemDev {
   uint32_t n_progs;
   uint32_t stage;
 };
-int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, bool has_sync, void* stream, std::string* err);
+int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, uint32_t n_sync_tiles, void* stream, std::string* err);
 int launch_elem_init(uint32_t* planes, uint32_t W, const uint32_t* n_cells, uint32_t n_progs, void* stream,
                      std::string* err);
 

@@ -186,8 +186,11 @@ int elem_compile(const coh_elem_program* progs, uint32_t n, ElemPlan* plan, std:
   plan->tiles.clear();
   plan->stage_tile0.assign(n_stages + 1, 0);
   plan->stage_has_sync.assign(n_stages, 0);
+  plan->sync_tiles.clear();
+  plan->stage_sync0.assign(n_stages + 1, 0);
   for (uint32_t s = 0; s < n_stages; ++s) {
     plan->stage_tile0[s] = (uint32_t)plan->tiles.size();
+    plan->stage_sync0[s] = (uint32_t)plan->sync_tiles.size();
     for (uint32_t b = 0; b < n; ++b) {
       if (s >= per[b].size()) continue;
       ElemOp op = per[b][s];
@@ -205,11 +208,16 @@ int elem_compile(const coh_elem_program* progs, uint32_t n, ElemPlan* plan, std:
       } else {
         add_range(op.lo, op.hi, 0);
       }
-      if (op.type == EOP_SYNC) plan->stage_has_sync[s] = 1;
+      if (op.type == EOP_SYNC) {
+        plan->stage_has_sync[s] = 1;
+        for (uint32_t k = op.tile0; k < (uint32_t)plan->tiles.size() - plan->stage_tile0[s]; ++k)
+          plan->sync_tiles.push_back(k);
+      }
       plan->ops[(size_t)s * n + b] = op;
     }
   }
   plan->stage_tile0[n_stages] = (uint32_t)plan->tiles.size();
+  plan->stage_sync0[n_stages] = (uint32_t)plan->sync_tiles.size();
   plan->alg_bytes = alg;
   return COH_OK;
 }
@@ -319,7 +327,7 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
   for (uint32_t s = 0; s < plan.n_stages; ++s)
     max_tiles = std::max(max_tiles, plan.stage_tile0[s + 1] - plan.stage_tile0[s]);
 
-  DevBuf planes, ops, tiles, st, sc, tcnt, tbase, vlo, vhi, ncell, bnd, rlo, rhi;
+  DevBuf planes, ops, tiles, stiles, st, sc, tcnt, tbase, vlo, vhi, ncell, bnd, rlo, rhi;
   auto alloc = [&](DevBuf& d, size_t bytes) { return cudaMalloc(&d.p, std::max<size_t>(bytes, 16)); };
 #define COH_E(x)                                                  \
   do {                                                            \
@@ -332,6 +340,7 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
   COH_E(alloc(planes, (size_t)n * 2 * W * 4));
   COH_E(alloc(ops, plan.ops.size() * sizeof(ElemOp)));
   COH_E(alloc(tiles, plan.tiles.size() * sizeof(ElemTile)));
+  COH_E(alloc(stiles, plan.sync_tiles.size() * 4));
   COH_E(alloc(st, (size_t)n * sizeof(ElemState)));
   COH_E(alloc(sc, (size_t)n * sizeof(ElemScratch)));
   COH_E(alloc(tcnt, (size_t)max_tiles * 4 * 4));
@@ -362,6 +371,8 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
   COH_E(cudaMemcpyAsync(ops.p, plan.ops.data(), plan.ops.size() * sizeof(ElemOp), cudaMemcpyHostToDevice, s));
   if (!plan.tiles.empty())
     COH_E(cudaMemcpyAsync(tiles.p, plan.tiles.data(), plan.tiles.size() * sizeof(ElemTile), cudaMemcpyHostToDevice, s));
+  if (!plan.sync_tiles.empty())
+    COH_E(cudaMemcpyAsync(stiles.p, plan.sync_tiles.data(), plan.sync_tiles.size() * 4, cudaMemcpyHostToDevice, s));
   COH_E(cudaMemcpyAsync(vlo.p, h_vlo.data(), h_vlo.size() * 4, cudaMemcpyHostToDevice, s));
   COH_E(cudaMemcpyAsync(vhi.p, h_vhi.data(), h_vhi.size() * 4, cudaMemcpyHostToDevice, s));
   COH_E(cudaMemcpyAsync(ncell.p, h_nc.data(), h_nc.size() * 4, cudaMemcpyHostToDevice, s));
@@ -380,6 +391,7 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
     d.W = W;
     d.ops = ops.as<ElemOp>() + (size_t)stg * n;
     d.tiles = tiles.as<ElemTile>() + plan.stage_tile0[stg];
+    d.sync_tiles = stiles.as<uint32_t>() + plan.stage_sync0[stg];
     d.st = st.as<ElemState>();
     d.sc = sc.as<ElemScratch>();
     d.tcnt = tcnt.as<uint32_t>();
@@ -394,8 +406,9 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
     d.n_progs = n;
     d.stage = stg;
     const uint32_t nt = plan.stage_tile0[stg + 1] - plan.stage_tile0[stg];
-    rc = launch_elem_stage(d, nt, plan.stage_has_sync[stg] != 0, s, &err);
-    launches += (nt ? 1 : 0) + 1 + ((plan.stage_has_sync[stg] && nt) ? 1 : 0);
+    const uint32_t ns = plan.stage_sync0[stg + 1] - plan.stage_sync0[stg];
+    rc = launch_elem_stage(d, nt, ns, s, &err);
+    launches += (nt ? 1 : 0) + 1 + (ns ? 1 : 0);
   }
   COH_E(cudaEventRecord(e1, s));
   if (rc) {

@@ -1,0 +1,42 @@
+"""C3 measurement: B buffers x 2^k cells, 8 overlapping views each, K component calls per
+buffer (overlap closure, whole-view syncs with transfer-range extraction, element range
+bodies, per-view boundary checks).  Prints algorithmic GB/s over the device time."""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_1910_11110_b200 as coh  # noqa: E402
+from paper_1910_11110_b200.elem import Program, elem_eval  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--buffers", type=int, default=256)
+ap.add_argument("--log2-cells", type=int, default=24)
+ap.add_argument("--views", type=int, default=8)
+ap.add_argument("--calls", type=int, default=8)
+ap.add_argument("--adv", type=int, default=64)
+ap.add_argument("--reps", type=int, default=3)
+a = ap.parse_args()
+ctx = coh.Context(0)
+t0 = time.time()
+progs = [Program.generate(3, b, 1 << a.log2_cells, a.views, a.calls, a.adv) for b in range(a.buffers)]
+gen_s = time.time() - t0
+best = None
+for r in range(a.reps):
+    out = elem_eval(ctx, progs, want_planes=False, runs_cap=0)
+    st = out["stats"]
+    gbs = st.alg_bytes / (st.device_ms / 1e3) / 1e9
+    if best is None or gbs > best["gbs"]:
+        best = {"gbs": gbs, "device_ms": st.device_ms, "alg_bytes": st.alg_bytes, "stages": st.stages,
+                "launches": st.launches, "tiles": st.tiles}
+res = out["results"]
+summary = {"buffers": a.buffers, "cells": 1 << a.log2_cells, "views": a.views, "calls": a.calls, "adv": a.adv,
+           "gen_s": gen_s, **best, "frac_of_6497": best["gbs"] / 6497.1,
+           "status": [sum(1 for i in range(a.buffers) if res[i].status == s) for s in range(4)],
+           "transfers": sum(res[i].transfers for i in range(a.buffers)),
+           "runs": sum(res[i].n_runs for i in range(a.buffers))}
+print(json.dumps(summary))
