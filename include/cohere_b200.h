@@ -273,6 +273,51 @@ int coh_elem_gen(uint64_t seed, uint64_t prog_id, uint32_t n_cells, uint32_t n_v
                  uint32_t n_calls, uint32_t adv_per1024, uint32_t* view_lo, uint32_t* view_hi,
                  coh_elem_call* calls);
 
+/* ==== coherent container runtime (config C5) ======================
+ * VectorPU's coherence control on the calculus: each vector is one
+ * whole-array variable with pinned host + device copies and its calculus state (concrete
+ * and abstract pairs, starting at (V,I)/(V,I), program.hpp:174-184).  A component call
+ * executes the translated block (modes.hpp:31-59): guards on the abstract flags issue
+ * cudaMemcpyAsync (push = H2D for a GPU component, pull = D2H for a CPU component) on the
+ * runtime stream, then the component runs, then its body effects.  Stuck steps return
+ * COH_E_DEFECT (StuckInfo text in coh_last_error).  The bytes moved equal the
+ * evaluator's prediction for the same call sequence (transfers x vector bytes).       */
+typedef struct coh_rt coh_rt;
+typedef struct coh_rt_arg {
+  uint32_t vec;
+  uint32_t kind;       /* COH_R / COH_W / COH_RW */
+} coh_rt_arg;
+/* GPU components receive the runtime stream and must launch on it; CPU components get
+ * NULL and run after the stream drained. */
+typedef void (*coh_rt_fn)(void* user, void* stream);
+typedef struct coh_rt_stats {
+  uint64_t h2d_bytes, d2h_bytes;
+  uint64_t h2d_copies, d2h_copies;
+  uint64_t calls, syncs_elided, stuck_calls;
+} coh_rt_stats;
+int coh_rt_create(coh_ctx* ctx, coh_rt** out);
+void coh_rt_destroy(coh_rt* rt);
+int coh_rt_vector(coh_rt* rt, size_t bytes, uint32_t* id);
+void* coh_rt_host_ptr(coh_rt* rt, uint32_t id);
+void* coh_rt_device_ptr(coh_rt* rt, uint32_t id);
+void* coh_rt_stream(coh_rt* rt);
+int coh_rt_state(coh_rt* rt, uint32_t id, uint8_t* nibble);  /* cl | cr<<1 | al<<2 | ar<<3 */
+int coh_rt_call(coh_rt* rt, uint32_t site, const coh_rt_arg* args, uint32_t n_args, coh_rt_fn fn, void* user);
+int coh_rt_sync(coh_rt* rt);
+int coh_rt_get_stats(const coh_rt* rt, coh_rt_stats* out);
+/* Built-in trivial components over float vectors: W -> x = 1, RW -> x = 0.5x + 1,
+ * R -> checksum.  user points to a coh_rt_touch. */
+typedef struct coh_rt_touch {
+  coh_rt* rt;
+  uint32_t n;
+  uint32_t vec[8];
+  uint32_t kind[8];
+  uint64_t bytes[8];
+  double checksum;
+} coh_rt_touch;
+void coh_rt_touch_cpu(void* user, void* stream);
+void coh_rt_touch_gpu(void* user, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -268,7 +268,11 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kWide) ? 6 : 10) k_trace_eval(co
         v[k] = __reduce_add_sync(m, v[k]);
         if (leader && v[k]) atomicAdd(&s_cnt[slot[k]], (unsigned long long)v[k]);
       }
-      if (tbytes) atomicAdd(&s_cnt[6], (unsigned long long)tbytes);
+      if (UNIFORM) {  // bytes = transfers x size: one multiply by the leader
+        if (leader && v[5]) atomicAdd(&s_cnt[6], (unsigned long long)v[5] * p.bytes_uniform);
+      } else if (tbytes) {  // non-uniform sizes: per-lane shared atomic
+        atomicAdd(&s_cnt[6], (unsigned long long)tbytes);
+      }
     }
   }
   }

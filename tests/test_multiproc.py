@@ -1,0 +1,75 @@
+"""World-size-2 gloo tests of the multi-GPU host logic (config C4): trace-id sharding,
+per-rank evaluation, and the counter allreduce.  The per-rank evaluator here is the CPU
+oracle (no GPU in this container); on the GPU box the same host code drives trace_eval."""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle_ffi as o
+import paper_1910_11110_b200 as coh
+from paper_1910_11110_b200 import shard
+
+N_PER, NC, NA, ADV, SEED = 300, 96, 16, 40, 4
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    t0, n = shard.shard_range(rank, world, N_PER)
+    recs = coh.gen_records_host(SEED, t0, n, NC, NA, ADV)
+    res, bnd = o.orc_eval(recs, n, NC, NA)
+    cnt = torch.from_numpy(shard.counters_from_results(res).view(np.int64).copy())
+    shard.allreduce_counters(cnt)
+    # strong-scaling split of the same job also sums to the same counters
+    f0, fn = shard.split_range(rank, world, world * N_PER)
+    recs2 = coh.gen_records_host(SEED, f0, fn, NC, NA, ADV)
+    res2, _ = o.orc_eval(recs2, fn, NC, NA)
+    cnt2 = torch.from_numpy(shard.counters_from_results(res2).view(np.int64).copy())
+    shard.allreduce_counters(cnt2)
+    np.save(os.path.join(outdir, f"res{rank}.npy"), res.view(np.uint8))
+    if rank == 0:
+        np.save(os.path.join(outdir, "cnt.npy"), cnt.numpy())
+        np.save(os.path.join(outdir, "cnt2.npy"), cnt2.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_counters_equal_single_process(world):
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(world, _free_port(), d), nprocs=world, join=True)
+        total = world * N_PER
+        recs = coh.gen_records_host(SEED, 0, total, NC, NA, ADV)
+        res, _ = o.orc_eval(recs, total, NC, NA)
+        want = shard.counters_from_results(res).view(np.int64)
+        assert np.array_equal(np.load(os.path.join(d, "cnt.npy")), want)
+        assert np.array_equal(np.load(os.path.join(d, "cnt2.npy")), want)
+        # per-trace results of the shards are the same bytes as the unsharded run
+        got = np.concatenate([np.load(os.path.join(d, f"res{r}.npy")) for r in range(world)])
+        assert np.array_equal(got, res.view(np.uint8))
+
+
+def test_split_range_partitions():
+    for world in (1, 2, 3, 8):
+        for total in (0, 1, 7, 1000, 1 << 20):
+            spans = [shard.split_range(r, world, total) for r in range(world)]
+            assert sum(n for _, n in spans) == total
+            pos = 0
+            for first, n in spans:
+                assert first == pos
+                pos += n
