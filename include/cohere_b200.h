@@ -189,6 +189,10 @@ int coh_reduce_counters(coh_ctx* ctx, const coh_trace_result* d_results, uint64_
 /* Kernels launched by this ctx since creation (the bench's gpu_launches claim). */
 uint64_t coh_launch_count(const coh_ctx* ctx);
 
+/* Best-of-reps pinned cudaMemcpyAsync bandwidth (GB/s) in each direction: the host-device
+ * link roofline of the container path (config C5). */
+int coh_measure_link(coh_ctx* ctx, size_t bytes, int reps, double* h2d_gbs, double* d2h_gbs);
+
 /* Pinned host memory for the host-buffer entry points. */
 void* coh_host_alloc(size_t bytes);
 void coh_host_free(void* p);

@@ -115,6 +115,7 @@ def lib():
             "coh_launch_count": (u64, [vp]),
             "coh_host_alloc": (vp, [C.c_size_t]),
             "coh_host_free": (None, [vp]),
+            "coh_measure_link": (i, [vp, C.c_size_t, i, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -255,6 +256,11 @@ class Context:
             "coh_eval_traces_host",
         )
         return results, boundary
+
+    def measure_link(self, nbytes: int, reps: int = 3) -> tuple[float, float]:
+        h2d, d2h = C.c_double(), C.c_double()
+        self._check(self._L.coh_measure_link(self._h, nbytes, reps, C.byref(h2d), C.byref(d2h)), "coh_measure_link")
+        return h2d.value, d2h.value
 
     def reduce_counters(self, d_results, n_traces, d_counters, stream=0):
         self._check(self._L.coh_reduce_counters(self._h, _ptr(d_results), n_traces, _ptr(d_counters), _ptr(stream)),

@@ -264,6 +264,42 @@ int coh_eval_traces_host(coh_ctx* ctx, const coh_trace_batch* batch, coh_trace_r
   return COH_OK;
 }
 
+int coh_measure_link(coh_ctx* ctx, size_t bytes, int reps, double* h2d_gbs, double* d2h_gbs) {
+  if (!ctx || !h2d_gbs || !d2h_gbs || bytes == 0) return COH_E_ARG;
+  void *h = nullptr, *d = nullptr;
+  COH_CUDA(ctx, cudaHostAlloc(&h, bytes, cudaHostAllocDefault));
+  if (cudaMalloc(&d, bytes) != cudaSuccess) {
+    cudaFreeHost(h);
+    ctx->err = "coh_measure_link: device allocation";
+    return COH_E_CUDA;
+  }
+  cudaStream_t s;
+  cudaEvent_t e0, e1;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double best[2] = {0, 0};
+  for (int dir = 0; dir < 2; ++dir)
+    for (int r = 0; r < std::max(1, reps); ++r) {
+      cudaEventRecord(e0, s);
+      if (dir == 0) cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s);
+      else cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s);
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      best[dir] = std::max(best[dir], (double)bytes / (ms / 1e3) / 1e9);
+    }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(s);
+  cudaFree(d);
+  cudaFreeHost(h);
+  *h2d_gbs = best[0];
+  *d2h_gbs = best[1];
+  return COH_OK;
+}
+
 int coh_reduce_counters(coh_ctx* ctx, const coh_trace_result* d_results, uint64_t n_traces,
                         uint64_t* d_counters, void* stream) {
   if (!ctx) return COH_E_ARG;
