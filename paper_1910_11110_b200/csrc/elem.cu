@@ -114,55 +114,85 @@ __device__ __forceinline__ void run_edges(const uint32_t (&z)[kWPT], uint32_t pr
   }
 }
 
-__global__ void __launch_bounds__(kET) k_elem_pass1(const ElemDev d) {
+// A tile is "full" when every word of its aligned 2048-word block lies strictly inside
+// the op range: then every mask is all-ones and the per-word mask work disappears
+// (uniform per CTA, so no divergence).
+__device__ __forceinline__ bool tile_full(uint32_t tstart, uint32_t lo, uint32_t hi) {
+  return tstart * 32u >= lo && (tstart + kElemTileWords) * 32u - 1u <= hi;
+}
+
+__device__ __forceinline__ void masks8(uint32_t base, uint32_t lo, uint32_t hi, bool full, uint32_t (&m)[kWPT]) {
+#pragma unroll
+  for (int k = 0; k < kWPT; ++k) m[k] = full ? 0xFFFFFFFFu : word_mask(base + k, lo, hi);
+}
+
+__device__ __forceinline__ void store8_const(uint32_t* p, uint32_t v) {
+  const uint4 q = make_uint4(v, v, v, v);
+  __stcg(reinterpret_cast<uint4*>(p), q);
+  __stcg(reinterpret_cast<uint4*>(p) + 1, q);
+}
+
+__global__ void __launch_bounds__(kET, 8) k_elem_pass1(const ElemDev d) {
   __shared__ uint32_t red[kET / 32];
   __shared__ uint32_t s_first[kET], s_last[kET];
+  __shared__ uint32_t s_next;
   const ElemTile tile = d.tiles[blockIdx.x];
   const uint32_t b = tile.b;
-  if (d.st[b].dead) return;
-  const ElemOp op = d.ops[b];
   uint32_t* Lp = d.planes + (size_t)b * 2u * d.W;
   uint32_t* Rp = Lp + d.W;
-  const uint32_t base = (tile.w0 / kElemTileWords) * kElemTileWords + threadIdx.x * kWPT;
+  const uint32_t tstart = tile.tstart;
+  const uint32_t base = tstart + threadIdx.x * kWPT;
   const int tloc = (int)(blockIdx.x);  // index of this tile within the stage
+  const uint32_t lane = threadIdx.x & 31;
+  struct {
+    uint8_t type, plane;
+  } op{tile.type, tile.plane};
   if (op.type == EOP_CHECK) {
-    const uint32_t lo = d.view_lo[b * COH_MAX_VIEWS + tile.view], hi = d.view_hi[b * COH_MAX_VIEWS + tile.view];
-    const uint32_t a = (op.lo >> (2 * tile.view)) & 3u;  // abstract pair of the view
-    uint32_t l[kWPT], r[kWPT];
-    uint32_t f = 0;
+    // abstraction_correct for one view over this tile: which of "some L=0", "some R=0",
+    // "some L|R=1" occur.  Violations are rare: warp OR, atomic only when non-zero.
+    // (Loads are issued before the dead-flag check: reads are harmless.)
+    const uint32_t lo = tile.lo, hi = tile.hi, a = tile.apair;
+    uint32_t l[kWPT], r[kWPT], m[kWPT];
     if (a != 2u) load8(Lp + base, l);   // (I,V) needs only R
     if (a != 1u) load8(Rp + base, r);   // (V,I) needs only L
+    masks8(base, lo, hi, tile_full(tstart, lo, hi), m);
+    uint32_t f = 0;
 #pragma unroll
     for (int k = 0; k < kWPT; ++k) {
-      const uint32_t m = word_mask(base + k, lo, hi);
-      if (a != 2u && (~l[k] & m)) f |= 1u;
-      if (a != 1u && (~r[k] & m)) f |= 2u;
-      if (a == 0u && ((l[k] | r[k]) & m)) f |= 4u;
+      if (a != 2u && (~l[k] & m[k])) f |= 1u;
+      if (a != 1u && (~r[k] & m[k])) f |= 2u;
+      if (a == 0u && ((l[k] | r[k]) & m[k])) f |= 4u;
     }
-    f = block_or(f, red);
-    if (threadIdx.x == 0 && f) atomicOr(&d.sc[b].view_flags[tile.view], f);
+    f = __reduce_or_sync(0xffffffffu, f);
+    if (lane == 0 && f && !d.st[b].dead) atomicOr(&d.sc[b].view_flags[tile.view], f);
     return;
   }
-  const uint32_t lo = op.lo, hi = op.hi;
+  const uint32_t lo = tile.lo, hi = tile.hi;
+  const bool full = tile_full(tstart, lo, hi);
   uint32_t m[kWPT];
-#pragma unroll
-  for (int k = 0; k < kWPT; ++k) m[k] = word_mask(base + k, lo, hi);
+  masks8(base, lo, hi, full, m);
   if (op.type == EOP_WRITE) {  // set plane op.plane, clear the other (w x[i] @site)
     uint32_t* sp = op.plane ? Rp : Lp;
     uint32_t* cp = op.plane ? Lp : Rp;
-    uint32_t s[kWPT], c[kWPT];
-    load8(sp + base, s);
-    load8(cp + base, c);
+    if (d.st[b].dead) return;  // writes are guarded by the (device-side) stuck flag
+    if (full) {                // interior tile: pure stores, m/4 bytes
+      store8_const(sp + base, 0xFFFFFFFFu);
+      store8_const(cp + base, 0u);
+      return;
+    }
+    uint32_t sv[kWPT], cv[kWPT];
+    load8(sp + base, sv);
+    load8(cp + base, cv);
 #pragma unroll
     for (int k = 0; k < kWPT; ++k) {
-      s[k] |= m[k];
-      c[k] &= ~m[k];
+      sv[k] |= m[k];
+      cv[k] &= ~m[k];
     }
-    store8(sp + base, s);
-    store8(cp + base, c);
+    store8(sp + base, sv);
+    store8(cp + base, cv);
     return;
   }
-  // SYNC / READ: first zero of the required (source) plane
+  // SYNC / READ: first zero of the required (source) plane; rare -> warp min + atomic
   const uint32_t* src = op.plane ? Rp : Lp;
   uint32_t v[kWPT];
   load8(src + base, v);
@@ -172,8 +202,8 @@ __global__ void __launch_bounds__(kET) k_elem_pass1(const ElemDev d) {
     const uint32_t z = ~v[k] & m[k];
     if (z) fz = (base + k) * 32u + (__ffs(z) - 1);
   }
-  fz = block_min(fz, red);
-  if (threadIdx.x == 0 && fz != kNoCell) atomicMin(&d.sc[b].first_zero, fz);
+  fz = __reduce_min_sync(0xffffffffu, fz);
+  if (lane == 0 && fz != kNoCell) atomicMin(&d.sc[b].first_zero, fz);  // ignored if dead
   if (op.type != EOP_SYNC) return;
   // destination zero runs: counts for the offsets, and the tile's edge bits
   const uint32_t* dst = op.plane ? Lp : Rp;
@@ -183,14 +213,13 @@ __global__ void __launch_bounds__(kET) k_elem_pass1(const ElemDev d) {
   for (int k = 0; k < kWPT; ++k) z[k] = ~v[k] & m[k];
   s_first[threadIdx.x] = z[0];
   s_last[threadIdx.x] = z[kWPT - 1];
-  const uint32_t tstart = (tile.w0 / kElemTileWords) * kElemTileWords;
-  uint32_t edge_prev = 0, edge_next = 0;
+  uint32_t edge_prev = 0;
   if (threadIdx.x == 0 && tstart > 0) {
     const uint32_t w = tstart - 1;
     edge_prev = (~dst[w] & word_mask(w, lo, hi)) >> 31;
   }
-  __shared__ uint32_t s_next;
   if (threadIdx.x == kET - 1) {
+    uint32_t edge_next = 0;
     if (tstart + kElemTileWords < d.W) {
       const uint32_t w = tstart + kElemTileWords;
       edge_next = ~dst[w] & word_mask(w, lo, hi) & 1u;
@@ -199,7 +228,7 @@ __global__ void __launch_bounds__(kET) k_elem_pass1(const ElemDev d) {
   }
   __syncthreads();
   const uint32_t pt = threadIdx.x ? (s_last[threadIdx.x - 1] >> 31) : edge_prev;
-  const uint32_t nb = threadIdx.x < kET - 1 ? (s_first[threadIdx.x + 1] & 1u) : edge_next;
+  const uint32_t nb = threadIdx.x < kET - 1 ? (s_first[threadIdx.x + 1] & 1u) : s_next;
   run_edges(z, pt, nb, sts, ens);
   uint32_t ns = 0, ne = 0, nz = 0;
 #pragma unroll
@@ -211,12 +240,8 @@ __global__ void __launch_bounds__(kET) k_elem_pass1(const ElemDev d) {
   ns = block_sum(ns, red);
   ne = block_sum(ne, red);
   nz = block_sum(nz, red);
-  if (threadIdx.x == 0) {
-    d.tcnt[4 * tloc + 0] = ns;
-    d.tcnt[4 * tloc + 1] = ne;
-    d.tcnt[4 * tloc + 2] = nz;
-    d.tcnt[4 * tloc + 3] = edge_prev | (s_next << 1);
-  }
+  if (threadIdx.x == 0)
+    *reinterpret_cast<uint4*>(d.tcnt + 4 * tloc) = make_uint4(ns, ne, nz, edge_prev | (s_next << 1));
 }
 
 // One warp per buffer: stuck detection, run-offset scan over the op's tiles (32 tiles
@@ -248,31 +273,34 @@ __global__ void __launch_bounds__(32 * kDecideWarps) k_elem_decide(const ElemDev
         const uint32_t n_t = ((op.hi >> 5) / kElemTileWords) - ((op.lo >> 5) / kElemTileWords) + 1;
         const unsigned long long run0 = st->n_runs;
         unsigned long long cs = 0, ce = 0, zeros = 0;
-        for (uint32_t k0 = 0; k0 < n_t; k0 += 32) {
-          const uint32_t k = k0 + lane;
-          uint32_t ns = 0, ne = 0, nz = 0;
-          if (k < n_t) {
-            const uint4 c = *reinterpret_cast<const uint4*>(d.tcnt + 4 * (t0 + k));
-            ns = c.x;
-            ne = c.y;
-            nz = c.z;
-          }
-          uint32_t xs = ns, xe = ne;
+        for (uint32_t k0 = 0; k0 < n_t; k0 += 32 * 8) {
+          uint4 c[8];  // issue every load of the batch before the dependent scan
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t ys = __shfl_up_sync(0xffffffffu, xs, o), ye = __shfl_up_sync(0xffffffffu, xe, o);
-            if (lane >= (uint32_t)o) {
-              xs += ys;
-              xe += ye;
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t k = k0 + 32u * j + lane;
+            c[j] = k < n_t ? __ldg(reinterpret_cast<const uint4*>(d.tcnt) + (t0 + k)) : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t k = k0 + 32u * j + lane;
+            const uint32_t ns = c[j].x, ne = c[j].y;
+            uint32_t xs = ns, xe = ne;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t ys = __shfl_up_sync(0xffffffffu, xs, o), ye = __shfl_up_sync(0xffffffffu, xe, o);
+              if (lane >= (uint32_t)o) {
+                xs += ys;
+                xe += ye;
+              }
             }
+            if (k < n_t) {
+              d.tbase[2 * (t0 + k)] = run0 + cs + xs - ns;
+              d.tbase[2 * (t0 + k) + 1] = run0 + ce + xe - ne;
+            }
+            cs += __shfl_sync(0xffffffffu, xs, 31);
+            ce += __shfl_sync(0xffffffffu, xe, 31);
+            zeros += __reduce_add_sync(0xffffffffu, c[j].z);
           }
-          if (k < n_t) {
-            d.tbase[2 * (t0 + k)] = run0 + cs + xs - ns;
-            d.tbase[2 * (t0 + k) + 1] = run0 + ce + xe - ne;
-          }
-          cs += __shfl_sync(0xffffffffu, xs, 31);
-          ce += __shfl_sync(0xffffffffu, xe, 31);
-          zeros += __reduce_add_sync(0xffffffffu, nz);
         }
         if (lane == 0) {
           st->n_runs = run0 + cs;
@@ -300,60 +328,113 @@ __global__ void __launch_bounds__(32 * kDecideWarps) k_elem_decide(const ElemDev
   if (lane < COH_MAX_VIEWS) sc->view_flags[lane] = 0;
 }
 
-__global__ void __launch_bounds__(kET) k_elem_apply(const ElemDev d) {
-  __shared__ uint32_t red[kET / 32];
-  __shared__ uint32_t s_first[kET], s_last[kET];
-  const int tloc = (int)d.sync_tiles[blockIdx.x];  // stage-local tile index of a SYNC op
-  const ElemTile tile = d.tiles[tloc];
-  const uint32_t b = tile.b;
-  const ElemOp op = d.ops[b];
-  if (op.type != EOP_SYNC || d.st[b].dead) return;
-  uint32_t* Lp = d.planes + (size_t)b * 2u * d.W;
-  uint32_t* Rp = Lp + d.W;
-  uint32_t* dst = op.plane ? Lp : Rp;
-  const uint32_t base = (tile.w0 / kElemTileWords) * kElemTileWords + threadIdx.x * kWPT;
-  uint32_t v[kWPT], m[kWPT], z[kWPT], sts[kWPT], ens[kWPT];
-  load8(dst + base, v);
+// Warp-per-tile over this stage's SYNC tiles (self-contained descriptors): each warp loads
+// its descriptor, then the two device-side inputs together (stuck flag, run counts).
+// Tiles without run edges (almost all) are a coalesced read-modify-write or, when the
+// tile lies inside the range, a pure store of ones; edge tiles emit their transfer runs
+// with a warp scan (lane l owns words [64 l, 64 l + 63] of the tile).
+constexpr int kApplyWarps = 8;
+constexpr int kWPL = kElemTileWords / 32;  // 64 words per lane
+__global__ void __launch_bounds__(32 * kApplyWarps) k_elem_apply(const ElemDev d, uint32_t n_sync_tiles) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t gw = blockIdx.x * kApplyWarps + (threadIdx.x >> 5), nw = gridDim.x * kApplyWarps;
+  for (uint32_t it = gw; it < n_sync_tiles; it += nw) {
+    const ElemTile tile = d.sync_desc[it];
+    const uint32_t b = tile.b, tloc = tile.tloc;
+    const uint32_t dead = d.st[b].dead;
+    const uint4 cnt = *reinterpret_cast<const uint4*>(d.tcnt + 4 * tloc);
+    if (dead) continue;  // warp-uniform
+    uint32_t* Lp = d.planes + (size_t)b * 2u * d.W;
+    uint32_t* dst = tile.plane ? Lp : Lp + d.W;
+    const uint32_t tstart = tile.tstart;
+    const bool full = tile_full(tstart, tile.lo, tile.hi);
+    uint4* dst4 = reinterpret_cast<uint4*>(dst + tstart);
+    if (!(d.runs_cap && (cnt.x | cnt.y))) {
+      // no runs to emit: dst |= mask over the tile, 512 contiguous bytes per instruction
+      if (full) {
 #pragma unroll
-  for (int k = 0; k < kWPT; ++k) {
-    m[k] = word_mask(base + k, op.lo, op.hi);
-    z[k] = ~v[k] & m[k];
-  }
-  s_first[threadIdx.x] = z[0];
-  s_last[threadIdx.x] = z[kWPT - 1];
-  __syncthreads();
-  const uint32_t edges = d.tcnt[4 * tloc + 3];
-  const uint32_t pt = threadIdx.x ? (s_last[threadIdx.x - 1] >> 31) : (edges & 1u);
-  const uint32_t nb = threadIdx.x < kET - 1 ? (s_first[threadIdx.x + 1] & 1u) : (edges >> 1);
-  run_edges(z, pt, nb, sts, ens);
-  if (d.runs_cap) {
-    uint32_t ns = 0, ne = 0;
-#pragma unroll
-    for (int k = 0; k < kWPT; ++k) {
-      ns += __popc(sts[k]);
-      ne += __popc(ens[k]);
+        for (int j = 0; j < kElemTileWords / 128; ++j)
+          __stcg(dst4 + lane + 32 * j, make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu));
+      } else {
+        for (int j = 0; j < kElemTileWords / 128; ++j) {
+          const uint32_t w = tstart + 4u * (lane + 32u * j);
+          uint4 q = __ldcg(dst4 + lane + 32 * j);
+          q.x |= word_mask(w, tile.lo, tile.hi);
+          q.y |= word_mask(w + 1, tile.lo, tile.hi);
+          q.z |= word_mask(w + 2, tile.lo, tile.hi);
+          q.w |= word_mask(w + 3, tile.lo, tile.hi);
+          __stcg(dst4 + lane + 32 * j, q);
+        }
+      }
+      continue;
     }
-    unsigned long long os = d.tbase[2 * tloc] + block_excl_scan(ns, red);
-    unsigned long long oe = d.tbase[2 * tloc + 1] + block_excl_scan(ne, red);
+    // edge tile: lane-contiguous words, run starts/ends, warp-scanned offsets
+    const uint32_t base = tstart + lane * kWPL;
+    unsigned long long os = d.tbase[2 * tloc], oe = d.tbase[2 * tloc + 1];
+    uint32_t carry_prev = cnt.w & 1u;  // top zero-bit of the word before the tile
     const size_t arena = (size_t)b * d.runs_cap;
-#pragma unroll
-    for (int k = 0; k < kWPT; ++k) {
-      for (uint32_t x = sts[k]; x; x &= x - 1, ++os)
-        if (os < d.runs_cap) d.runs_lo[arena + os] = (base + k) * 32u + (__ffs(x) - 1);
-      for (uint32_t x = ens[k]; x; x &= x - 1, ++oe)
-        if (oe < d.runs_cap) d.runs_hi[arena + oe] = (base + k) * 32u + (__ffs(x) - 1);
+    // pass A: counts per lane (for the exclusive scan)
+    uint32_t ns = 0, ne = 0;
+    uint32_t first_z = 0, last_z = 0;
+    for (int k = 0; k < kWPL; ++k) {
+      const uint32_t z = ~dst[base + k] & word_mask(base + k, tile.lo, tile.hi);
+      if (k == 0) first_z = z;
+      if (k == kWPL - 1) last_z = z;
+      (void)z;
     }
-  }
+    const uint32_t prev_last = __shfl_up_sync(0xffffffffu, last_z, 1);  // all lanes shuffle
+    const uint32_t prev_top = lane ? (prev_last >> 31) : carry_prev;
+    const uint32_t next_first = __shfl_down_sync(0xffffffffu, first_z, 1);
+    const uint32_t next_bot = lane < 31 ? (next_first & 1u) : (cnt.w >> 1);
+    {
+      uint32_t pz = prev_top;
+      for (int k = 0; k < kWPL; ++k) {
+        const uint32_t z = ~dst[base + k] & word_mask(base + k, tile.lo, tile.hi);
+        const uint32_t zn = k < kWPL - 1 ? (~dst[base + k + 1] & word_mask(base + k + 1, tile.lo, tile.hi)) & 1u : next_bot;
+        ns += __popc(z & ~((z << 1) | pz));
+        ne += __popc(z & ~((z >> 1) | (zn << 31)));
+        pz = z >> 31;
+      }
+    }
+    uint32_t xs = ns, xe = ne;
 #pragma unroll
-  for (int k = 0; k < kWPT; ++k) v[k] |= m[k];
-  store8(dst + base, v);
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t ys = __shfl_up_sync(0xffffffffu, xs, o), ye = __shfl_up_sync(0xffffffffu, xe, o);
+      if (lane >= (uint32_t)o) {
+        xs += ys;
+        xe += ye;
+      }
+    }
+    os += xs - ns;
+    oe += xe - ne;
+    __syncwarp();
+    // pass B: emit, then set the destination bits
+    uint32_t pz = prev_top;
+    for (int k = 0; k < kWPL; ++k) {
+      const uint32_t m = word_mask(base + k, tile.lo, tile.hi);
+      const uint32_t v = dst[base + k];
+      const uint32_t z = ~v & m;
+      const uint32_t zn = k < kWPL - 1 ? (~dst[base + k + 1] & word_mask(base + k + 1, tile.lo, tile.hi)) & 1u : next_bot;
+      const uint32_t st = z & ~((z << 1) | pz), en = z & ~((z >> 1) | (zn << 31));
+      for (uint32_t x = st; x; x &= x - 1, ++os)
+        if (os < d.runs_cap) d.runs_lo[arena + os] = (base + k) * 32u + (__ffs(x) - 1);
+      for (uint32_t x = en; x; x &= x - 1, ++oe)
+        if (oe < d.runs_cap) d.runs_hi[arena + oe] = (base + k) * 32u + (__ffs(x) - 1);
+      pz = z >> 31;
+    }
+    __syncwarp();  // every lane has read its neighbour words before any is overwritten
+    for (int k = 0; k < kWPL; ++k) dst[base + k] |= word_mask(base + k, tile.lo, tile.hi);
+  }
 }
 
 int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, uint32_t n_sync_tiles, void* stream, std::string* err) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n_tiles) k_elem_pass1<<<n_tiles, kET, 0, s>>>(d);
   k_elem_decide<<<(d.n_progs + kDecideWarps - 1) / kDecideWarps, 32 * kDecideWarps, 0, s>>>(d);
-  if (n_sync_tiles) k_elem_apply<<<n_sync_tiles, kET, 0, s>>>(d);
+  if (n_sync_tiles) {
+    const uint32_t blocks = (n_sync_tiles + kApplyWarps - 1) / kApplyWarps;
+    k_elem_apply<<<blocks < 148u * 16u ? blocks : 148u * 16u, 32 * kApplyWarps, 0, s>>>(d, n_sync_tiles);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("element stage launch: ") + cudaGetErrorString(e);
@@ -362,19 +443,25 @@ int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, uint32_t n_sync_tiles,
   return COH_OK;
 }
 
-// Initial store: every cell (V,I) -> L = 1 on [0, n_cells), R = 0.
+// Initial store: every cell (V,I) -> L = 1 on [0, n_cells), R = 0 (program.hpp:174-184).
+// 128-bit stores, one 4-word group per thread iteration.
 __global__ void k_elem_init(uint32_t* planes, uint32_t W, const uint32_t* n_cells, uint32_t n_progs) {
-  const uint64_t total = (uint64_t)n_progs * 2u * W;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+  const uint64_t total4 = (uint64_t)n_progs * 2u * W / 4u;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total4;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t b = (uint32_t)(i / (2u * W));
-    const uint32_t r = (uint32_t)(i - (uint64_t)b * 2u * W);
-    uint32_t v = 0;
+    const uint64_t w0 = i * 4u;
+    const uint32_t b = (uint32_t)(w0 / (2u * W));
+    const uint32_t r = (uint32_t)(w0 - (uint64_t)b * 2u * W);
+    uint32_t q[4] = {0u, 0u, 0u, 0u};
     if (r < W) {
-      const uint32_t n = n_cells[b], w = r;
-      v = (w + 1) * 32u <= n ? 0xFFFFFFFFu : (w * 32u < n ? (0xFFFFFFFFu >> (32u - (n - w * 32u))) : 0u);
+      const uint32_t n = n_cells[b];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t w = r + k;
+        q[k] = (w + 1) * 32u <= n ? 0xFFFFFFFFu : (w * 32u < n ? (0xFFFFFFFFu >> (32u - (n - w * 32u))) : 0u);
+      }
     }
-    planes[i] = v;
+    __stcg(reinterpret_cast<uint4*>(planes) + i, make_uint4(q[0], q[1], q[2], q[3]));
   }
 }
 

@@ -21,15 +21,19 @@ struct ElemOp {
 };
 static_assert(sizeof(ElemOp) == 16, "ElemOp is 16 bytes");
 
-// One CTA's work item: words [w0, w1] (inclusive) of buffer b for that buffer's op in the
-// stage; for CHECK ops `view` names the view whose range the tile covers.
+// One CTA's work item, self-contained so a CTA can start its data loads without a chain
+// of dependent descriptor loads: the 2048-word aligned block `tstart` of buffer b, the
+// cell range [lo, hi] it applies to (op range, or the view range for CHECK), the op
+// type / plane / view / the view's abstract pair, and the stage-local tile index.
 struct ElemTile {
   uint32_t b;
-  uint32_t w0, w1;
-  uint16_t view;
-  uint16_t idx;      // tile index within the op (run-offset scan order)
+  uint32_t tstart;
+  uint32_t lo, hi;
+  uint8_t type, plane, view, apair;
+  uint32_t tloc;
+  uint32_t pad[2];
 };
-static_assert(sizeof(ElemTile) == 16, "ElemTile is 16 bytes");
+static_assert(sizeof(ElemTile) == 32, "ElemTile is 32 bytes");
 
 constexpr uint32_t kElemTileWords = 2048;      // 64 Ki cells per plane per CTA
 constexpr uint32_t kNoCell = 0xFFFFFFFFu;
@@ -63,7 +67,7 @@ struct ElemPlan {
   std::vector<ElemTile> tiles;       // all stages concatenated
   std::vector<uint32_t> stage_tile0; // n_stages + 1 offsets into tiles
   std::vector<uint8_t> stage_has_sync;
-  std::vector<uint32_t> sync_tiles;        // stage-local tile indices of SYNC ops, by stage
+  std::vector<ElemTile> sync_tiles;        // copies of the SYNC ops' tiles, by stage
   std::vector<uint32_t> stage_sync0;       // n_stages + 1 offsets into sync_tiles
   // host timeline, per program
   struct Timeline {
@@ -90,7 +94,7 @@ struct ElemDev {
   uint32_t W;                  // words per plane (multiple of kElemTileWords)
   const ElemOp* ops;           // this stage, [b]
   const ElemTile* tiles;       // this stage
-  const uint32_t* sync_tiles;  // this stage: tile indices the apply pass visits
+  const ElemTile* sync_desc;   // this stage: descriptors of the SYNC tiles (apply pass)
   ElemState* st;
   ElemScratch* sc;
   uint32_t* tcnt;              // per tile of this stage: starts, ends, zeros, edge bits

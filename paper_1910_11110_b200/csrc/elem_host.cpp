@@ -195,29 +195,40 @@ int elem_compile(const coh_elem_program* progs, uint32_t n, ElemPlan* plan, std:
       if (s >= per[b].size()) continue;
       ElemOp op = per[b][s];
       op.tile0 = (uint32_t)plan->tiles.size() - plan->stage_tile0[s];  // stage-local
-      auto add_range = [&](uint32_t lo, uint32_t hi, uint16_t view) {
+      auto add_range = [&](uint32_t lo, uint32_t hi, uint32_t view, uint32_t apair) {
         const uint32_t w_lo = lo / 32, w_hi = hi / 32;
-        uint16_t idx = 0;
         for (uint32_t t0 = (w_lo / kElemTileWords) * kElemTileWords; t0 <= w_hi; t0 += kElemTileWords) {
-          const uint32_t a = std::max(t0, w_lo), z = std::min(t0 + kElemTileWords - 1, w_hi);
-          plan->tiles.push_back(ElemTile{b, a, z, view, idx++});
+          ElemTile t{};
+          t.b = b;
+          t.tstart = t0;
+          t.lo = lo;
+          t.hi = hi;
+          t.type = op.type;
+          t.plane = op.plane;
+          t.view = (uint8_t)view;
+          t.apair = (uint8_t)apair;
+          t.tloc = (uint32_t)plan->tiles.size() - plan->stage_tile0[s];
+          plan->tiles.push_back(t);
         }
       };
       if (op.type == EOP_CHECK) {
-        for (uint32_t v = 0; v < progs[b].n_views; ++v) add_range(progs[b].view_lo[v], progs[b].view_hi[v], (uint16_t)v);
+        for (uint32_t v = 0; v < progs[b].n_views; ++v)
+          add_range(progs[b].view_lo[v], progs[b].view_hi[v], v, (op.lo >> (2 * v)) & 3u);
       } else {
-        add_range(op.lo, op.hi, 0);
+        add_range(op.lo, op.hi, 0, 0);
       }
       if (op.type == EOP_SYNC) {
         plan->stage_has_sync[s] = 1;
         for (uint32_t k = op.tile0; k < (uint32_t)plan->tiles.size() - plan->stage_tile0[s]; ++k)
-          plan->sync_tiles.push_back(k);
+          plan->sync_tiles.push_back(plan->tiles[plan->stage_tile0[s] + k]);
       }
       plan->ops[(size_t)s * n + b] = op;
     }
   }
   plan->stage_tile0[n_stages] = (uint32_t)plan->tiles.size();
   plan->stage_sync0[n_stages] = (uint32_t)plan->sync_tiles.size();
+  // initial_store writes both planes of every cell (L = 1, R = 0)
+  for (uint32_t b = 0; b < n; ++b) alg += 2 * (((uint64_t)progs[b].n_cells + 7) / 8);
   plan->alg_bytes = alg;
   return COH_OK;
 }
@@ -340,7 +351,7 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
   COH_E(alloc(planes, (size_t)n * 2 * W * 4));
   COH_E(alloc(ops, plan.ops.size() * sizeof(ElemOp)));
   COH_E(alloc(tiles, plan.tiles.size() * sizeof(ElemTile)));
-  COH_E(alloc(stiles, plan.sync_tiles.size() * 4));
+  COH_E(alloc(stiles, plan.sync_tiles.size() * sizeof(ElemTile)));
   COH_E(alloc(st, (size_t)n * sizeof(ElemState)));
   COH_E(alloc(sc, (size_t)n * sizeof(ElemScratch)));
   COH_E(alloc(tcnt, (size_t)max_tiles * 4 * 4));
@@ -372,7 +383,8 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
   if (!plan.tiles.empty())
     COH_E(cudaMemcpyAsync(tiles.p, plan.tiles.data(), plan.tiles.size() * sizeof(ElemTile), cudaMemcpyHostToDevice, s));
   if (!plan.sync_tiles.empty())
-    COH_E(cudaMemcpyAsync(stiles.p, plan.sync_tiles.data(), plan.sync_tiles.size() * 4, cudaMemcpyHostToDevice, s));
+    COH_E(cudaMemcpyAsync(stiles.p, plan.sync_tiles.data(), plan.sync_tiles.size() * sizeof(ElemTile),
+                          cudaMemcpyHostToDevice, s));
   COH_E(cudaMemcpyAsync(vlo.p, h_vlo.data(), h_vlo.size() * 4, cudaMemcpyHostToDevice, s));
   COH_E(cudaMemcpyAsync(vhi.p, h_vhi.data(), h_vhi.size() * 4, cudaMemcpyHostToDevice, s));
   COH_E(cudaMemcpyAsync(ncell.p, h_nc.data(), h_nc.size() * 4, cudaMemcpyHostToDevice, s));
@@ -382,33 +394,53 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
   cudaEvent_t e0, e1;
   COH_E(cudaEventCreate(&e0));
   COH_E(cudaEventCreate(&e1));
+  // The whole stage sequence (init + 2-3 kernels per stage) is static once compiled:
+  // capture it into a CUDA graph so the per-stage launch gaps disappear.
+  uint64_t launches = 0;
+  auto enqueue = [&]() -> int {
+    launches = 1;
+    int r = launch_elem_init(planes.as<uint32_t>(), W, ncell.as<uint32_t>(), n, s, &err);
+    for (uint32_t stg = 0; stg < plan.n_stages && r == COH_OK; ++stg) {
+      ElemDev d;
+      d.planes = planes.as<uint32_t>();
+      d.W = W;
+      d.ops = ops.as<ElemOp>() + (size_t)stg * n;
+      d.tiles = tiles.as<ElemTile>() + plan.stage_tile0[stg];
+      d.sync_desc = stiles.as<ElemTile>() + plan.stage_sync0[stg];
+      d.st = st.as<ElemState>();
+      d.sc = sc.as<ElemScratch>();
+      d.tcnt = tcnt.as<uint32_t>();
+      d.tbase = tbase.as<unsigned long long>();
+      d.view_lo = vlo.as<uint32_t>();
+      d.view_hi = vhi.as<uint32_t>();
+      d.boundary = bnd.as<uint32_t>();
+      d.bwords = bwords;
+      d.runs_lo = rlo.as<uint32_t>();
+      d.runs_hi = rhi.as<uint32_t>();
+      d.runs_cap = runs_cap;
+      d.n_progs = n;
+      d.stage = stg;
+      const uint32_t nt = plan.stage_tile0[stg + 1] - plan.stage_tile0[stg];
+      const uint32_t ns = plan.stage_sync0[stg + 1] - plan.stage_sync0[stg];
+      r = launch_elem_stage(d, nt, ns, s, &err);
+      launches += (nt ? 1 : 0) + 1 + (ns ? 1 : 0);
+    }
+    return r;
+  };
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool graphed = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (graphed) {
+    rc = enqueue();
+    graphed = cudaStreamEndCapture(s, &graph) == cudaSuccess && rc == COH_OK &&
+              cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    cudaGetLastError();
+  }
   COH_E(cudaEventRecord(e0, s));
-  rc = launch_elem_init(planes.as<uint32_t>(), W, ncell.as<uint32_t>(), n, s, &err);
-  uint64_t launches = 1;
-  for (uint32_t stg = 0; stg < plan.n_stages && rc == COH_OK; ++stg) {
-    ElemDev d;
-    d.planes = planes.as<uint32_t>();
-    d.W = W;
-    d.ops = ops.as<ElemOp>() + (size_t)stg * n;
-    d.tiles = tiles.as<ElemTile>() + plan.stage_tile0[stg];
-    d.sync_tiles = stiles.as<uint32_t>() + plan.stage_sync0[stg];
-    d.st = st.as<ElemState>();
-    d.sc = sc.as<ElemScratch>();
-    d.tcnt = tcnt.as<uint32_t>();
-    d.tbase = tbase.as<unsigned long long>();
-    d.view_lo = vlo.as<uint32_t>();
-    d.view_hi = vhi.as<uint32_t>();
-    d.boundary = bnd.as<uint32_t>();
-    d.bwords = bwords;
-    d.runs_lo = rlo.as<uint32_t>();
-    d.runs_hi = rhi.as<uint32_t>();
-    d.runs_cap = runs_cap;
-    d.n_progs = n;
-    d.stage = stg;
-    const uint32_t nt = plan.stage_tile0[stg + 1] - plan.stage_tile0[stg];
-    const uint32_t ns = plan.stage_sync0[stg + 1] - plan.stage_sync0[stg];
-    rc = launch_elem_stage(d, nt, ns, s, &err);
-    launches += (nt ? 1 : 0) + 1 + (ns ? 1 : 0);
+  if (graphed) {
+    COH_E(cudaGraphLaunch(exec, s));
+  } else {
+    rc = enqueue();  // capture unavailable: plain stream launches
   }
   COH_E(cudaEventRecord(e1, s));
   if (rc) {
@@ -434,6 +466,8 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
     COH_E(cudaMemcpyAsync(h_rhi.data(), rhi.p, h_rhi.size() * 4, cudaMemcpyDeviceToHost, s));
   }
   COH_E(cudaStreamSynchronize(s));
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
