@@ -251,14 +251,17 @@ __global__ void __launch_bounds__(32 * kDecideWarps) k_elem_decide(const ElemDev
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t b = blockIdx.x * kDecideWarps + (threadIdx.x >> 5);
   if (b >= d.n_progs) return;
+  // every independent input in flight together: op, stuck flag, first zero, view flags
   const ElemOp op = d.ops[b];
   ElemState* __restrict__ st = d.st + b;
   ElemScratch* __restrict__ sc = d.sc + b;
   const uint32_t dead = st->dead;
+  const uint32_t fz0 = sc->first_zero;
+  const uint32_t vf = lane < COH_MAX_VIEWS ? sc->view_flags[lane] : 0u;
   __syncwarp();
   if (op.type != EOP_NONE && !dead) {
     if (op.type == EOP_SYNC || op.type == EOP_READ) {
-      const uint32_t fz = sc->first_zero;
+      const uint32_t fz = fz0;
       if (fz != kNoCell) {
         if (lane == 0) {
           const uint32_t* Lp = d.planes + (size_t)b * 2u * d.W;
@@ -311,7 +314,7 @@ __global__ void __launch_bounds__(32 * kDecideWarps) k_elem_decide(const ElemDev
     } else if (op.type == EOP_CHECK) {
       bool okv = true;
       if (lane < op.plane) {
-        const uint32_t a = (op.lo >> (2 * lane)) & 3u, f = sc->view_flags[lane];
+        const uint32_t a = (op.lo >> (2 * lane)) & 3u, f = vf;
         // leq(a, cell) for every cell of the view:
         // (V,I): L all 1; (I,V): R all 1; (V,V): both; (I,I): L|R all 0
         okv = a == 1u ? !(f & 1u) : a == 2u ? !(f & 2u) : a == 3u ? !(f & 3u) : !(f & 4u);
@@ -335,7 +338,7 @@ __global__ void __launch_bounds__(32 * kDecideWarps) k_elem_decide(const ElemDev
 // with a warp scan (lane l owns words [64 l, 64 l + 63] of the tile).
 constexpr int kApplyWarps = 8;
 constexpr int kWPL = kElemTileWords / 32;  // 64 words per lane
-__global__ void __launch_bounds__(32 * kApplyWarps) k_elem_apply(const ElemDev d, uint32_t n_sync_tiles) {
+__global__ void __launch_bounds__(32 * kApplyWarps, 2) k_elem_apply(const ElemDev d, uint32_t n_sync_tiles) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t gw = blockIdx.x * kApplyWarps + (threadIdx.x >> 5), nw = gridDim.x * kApplyWarps;
   for (uint32_t it = gw; it < n_sync_tiles; it += nw) {
@@ -368,33 +371,34 @@ __global__ void __launch_bounds__(32 * kApplyWarps) k_elem_apply(const ElemDev d
       }
       continue;
     }
-    // edge tile: lane-contiguous words, run starts/ends, warp-scanned offsets
+    // edge tile: lane l owns words [64 l, 64 l + 63], loaded once into registers
     const uint32_t base = tstart + lane * kWPL;
-    unsigned long long os = d.tbase[2 * tloc], oe = d.tbase[2 * tloc + 1];
-    uint32_t carry_prev = cnt.w & 1u;  // top zero-bit of the word before the tile
-    const size_t arena = (size_t)b * d.runs_cap;
-    // pass A: counts per lane (for the exclusive scan)
-    uint32_t ns = 0, ne = 0;
-    uint32_t first_z = 0, last_z = 0;
-    for (int k = 0; k < kWPL; ++k) {
-      const uint32_t z = ~dst[base + k] & word_mask(base + k, tile.lo, tile.hi);
-      if (k == 0) first_z = z;
-      if (k == kWPL - 1) last_z = z;
-      (void)z;
-    }
-    const uint32_t prev_last = __shfl_up_sync(0xffffffffu, last_z, 1);  // all lanes shuffle
-    const uint32_t prev_top = lane ? (prev_last >> 31) : carry_prev;
-    const uint32_t next_first = __shfl_down_sync(0xffffffffu, first_z, 1);
-    const uint32_t next_bot = lane < 31 ? (next_first & 1u) : (cnt.w >> 1);
+    uint32_t z[kWPL];
     {
-      uint32_t pz = prev_top;
-      for (int k = 0; k < kWPL; ++k) {
-        const uint32_t z = ~dst[base + k] & word_mask(base + k, tile.lo, tile.hi);
-        const uint32_t zn = k < kWPL - 1 ? (~dst[base + k + 1] & word_mask(base + k + 1, tile.lo, tile.hi)) & 1u : next_bot;
-        ns += __popc(z & ~((z << 1) | pz));
-        ne += __popc(z & ~((z >> 1) | (zn << 31)));
-        pz = z >> 31;
+      const uint4* p4 = reinterpret_cast<const uint4*>(dst + base);
+#pragma unroll
+      for (int q = 0; q < kWPL / 4; ++q) {
+        const uint4 v = __ldcg(p4 + q);
+        z[4 * q] = ~v.x;
+        z[4 * q + 1] = ~v.y;
+        z[4 * q + 2] = ~v.z;
+        z[4 * q + 3] = ~v.w;
       }
+    }
+    const bool lane_full = tile_full(tstart, tile.lo, tile.hi);
+#pragma unroll
+    for (int k = 0; k < kWPL; ++k) z[k] &= lane_full ? 0xFFFFFFFFu : word_mask(base + k, tile.lo, tile.hi);
+    const uint32_t prev_last = __shfl_up_sync(0xffffffffu, z[kWPL - 1], 1);  // all lanes shuffle
+    const uint32_t next_first = __shfl_down_sync(0xffffffffu, z[0], 1);
+    const uint32_t prev_top = lane ? (prev_last >> 31) : (cnt.w & 1u);
+    const uint32_t next_bot = lane < 31 ? (next_first & 1u) : (cnt.w >> 1);
+    uint32_t ns = 0, ne = 0;
+#pragma unroll
+    for (int k = 0; k < kWPL; ++k) {
+      const uint32_t pz = k ? (z[k - 1] >> 31) : prev_top;
+      const uint32_t zn = k < kWPL - 1 ? (z[k + 1] & 1u) : next_bot;
+      ns += __popc(z[k] & ~((z[k] << 1) | pz));
+      ne += __popc(z[k] & ~((z[k] >> 1) | (zn << 31)));
     }
     uint32_t xs = ns, xe = ne;
 #pragma unroll
@@ -405,25 +409,34 @@ __global__ void __launch_bounds__(32 * kApplyWarps) k_elem_apply(const ElemDev d
         xe += ye;
       }
     }
-    os += xs - ns;
-    oe += xe - ne;
-    __syncwarp();
-    // pass B: emit, then set the destination bits
-    uint32_t pz = prev_top;
+    unsigned long long os = d.tbase[2 * tloc] + (xs - ns), oe = d.tbase[2 * tloc + 1] + (xe - ne);
+    const size_t arena = (size_t)b * d.runs_cap;
+#pragma unroll
     for (int k = 0; k < kWPL; ++k) {
-      const uint32_t m = word_mask(base + k, tile.lo, tile.hi);
-      const uint32_t v = dst[base + k];
-      const uint32_t z = ~v & m;
-      const uint32_t zn = k < kWPL - 1 ? (~dst[base + k + 1] & word_mask(base + k + 1, tile.lo, tile.hi)) & 1u : next_bot;
-      const uint32_t st = z & ~((z << 1) | pz), en = z & ~((z >> 1) | (zn << 31));
+      const uint32_t pz = k ? (z[k - 1] >> 31) : prev_top;
+      const uint32_t zn = k < kWPL - 1 ? (z[k + 1] & 1u) : next_bot;
+      const uint32_t st = z[k] & ~((z[k] << 1) | pz), en = z[k] & ~((z[k] >> 1) | (zn << 31));
       for (uint32_t x = st; x; x &= x - 1, ++os)
         if (os < d.runs_cap) d.runs_lo[arena + os] = (base + k) * 32u + (__ffs(x) - 1);
       for (uint32_t x = en; x; x &= x - 1, ++oe)
         if (oe < d.runs_cap) d.runs_hi[arena + oe] = (base + k) * 32u + (__ffs(x) - 1);
-      pz = z >> 31;
     }
-    __syncwarp();  // every lane has read its neighbour words before any is overwritten
-    for (int k = 0; k < kWPL; ++k) dst[base + k] |= word_mask(base + k, tile.lo, tile.hi);
+    // dst |= mask: the zero bits inside the range become ones
+    {
+      uint4* p4 = reinterpret_cast<uint4*>(dst + base);
+#pragma unroll
+      for (int q = 0; q < kWPL / 4; ++q) {
+        // reconstruct: new = old | mask = ~(z_old & ~mask) ... old = ~(z_unmasked); simpler:
+        // old bits outside the range are unchanged, bits inside become 1
+        const uint32_t w0 = base + 4 * q;
+        uint4 v = __ldcg(p4 + q);
+        v.x |= lane_full ? 0xFFFFFFFFu : word_mask(w0, tile.lo, tile.hi);
+        v.y |= lane_full ? 0xFFFFFFFFu : word_mask(w0 + 1, tile.lo, tile.hi);
+        v.z |= lane_full ? 0xFFFFFFFFu : word_mask(w0 + 2, tile.lo, tile.hi);
+        v.w |= lane_full ? 0xFFFFFFFFu : word_mask(w0 + 3, tile.lo, tile.hi);
+        __stcg(p4 + q, v);
+      }
+    }
   }
 }
 
