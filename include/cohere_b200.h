@@ -322,6 +322,43 @@ typedef struct coh_rt_touch {
 void coh_rt_touch_cpu(void* user, void* stream);
 void coh_rt_touch_gpu(void* user, void* stream);
 
+/* ==== general block programs and schedule sweeps ================
+ * Programs in the full calculus (scalars + one buffer with overlapping views, several
+ * modes per block, element bodies, opaque/validity if and while), generated natively by
+ * a restatement of the test kit's gen_well_declared (testkit.hpp:364-447, mt19937_64
+ * draw order) and closed over overlaps (overlap.hpp:182-230).  coh_sweep runs every
+ * schedule of length <= max_decisions exactly as all_schedules_run (testkit.hpp:465-517)
+ * does — run_annotated per prefix, a run that exhausted its prefix branches into the two
+ * one-longer prefixes — with every run a GPU thread (one frontier level per launch). */
+typedef struct coh_gen_limits {   /* GenLimits, testkit.hpp:279-287 (same order/defaults) */
+  uint32_t max_blocks, max_body_depth, max_vars, max_buffer_len, max_loop_unroll;
+  uint32_t allow_arrays, allow_overlaps, pad;
+} coh_gen_limits;
+/* The generated program in the reference's canonical pretty() form (pretty.hpp:120-139).
+ * Returns COH_OK / COH_E_OVERLAP_CONFLICT, or -(needed size) if cap is too small. */
+int coh_gen_program_text(uint64_t seed, const coh_gen_limits* limits, char* buf, size_t cap);
+typedef struct coh_sweep_leaf {
+  uint64_t seed;
+  uint32_t schedule;          /* answers, bit k = k-th opaque decision                    */
+  uint8_t sched_len;
+  uint8_t status;             /* COH_RUN_*                                                */
+  uint8_t blocks_done;        /* boundary_ok.size()                                       */
+  uint8_t boundary_ok;        /* bit b = boundary_ok[b]                                    */
+  uint32_t steps;
+  uint8_t consumed, overflowed;
+  uint8_t stuck_key;          /* key index (s_i = i, s_i^ = S+i, v_j^ = 2S+j, b0[c] = 2S+V+c) */
+  uint8_t stuck_info;         /* effect | site << 3 | abstract key << 4 | actual << 5       */
+  uint64_t store;             /* 2 bits per key: bit0 local V, bit1 remote V               */
+} coh_sweep_leaf;
+typedef struct coh_sweep_stats {
+  uint64_t programs, runs, done, stuck, fuel_exhausted, runs_with_violation, nodes, conflicts;
+  double device_ms;
+  uint64_t launches;
+} coh_sweep_stats;
+int coh_sweep(coh_ctx* ctx, uint64_t seed0, uint32_t n_seeds, const coh_gen_limits* limits,
+              uint32_t max_decisions, int32_t fuel, coh_sweep_leaf* leaves, uint64_t leaves_cap,
+              coh_sweep_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -403,4 +403,111 @@ int ref_elem_run(const coh_elem_program* P, coh_elem_result* out, uint32_t* plan
   return a.rc;
 }
 
+// ---------------------------------------------------------------------------------
+// General programs: the reference's own gen_well_declared / run_annotated / sweep.
+int ref_gen_program_text(uint64_t seed, char* buf, size_t cap) {
+  const std::string t = pretty(gen_well_declared(seed, GenLimits()));
+  if (!buf || cap <= t.size()) return -(int)t.size() - 1;
+  std::memcpy(buf, t.c_str(), t.size() + 1);
+  return 0;
+}
+
+static int key_index(const Declarations& d, const VarKey& k) {
+  const int S = (int)d.scalars().size(), V = (int)d.views().size();
+  auto find = [](const auto& vec, const std::string& n) {
+    for (size_t i = 0; i < vec.size(); ++i)
+      if (vec[i].name == n) return (int)i;
+    return -1;
+  };
+  switch (k.kind) {
+    case VarKey::Kind::Scalar: return find(d.scalars(), k.name);
+    case VarKey::Kind::Element: return 2 * S + V + k.index;
+    case VarKey::Kind::Abstract: {
+      const int s = find(d.scalars(), k.name);
+      return s >= 0 ? S + s : 2 * S + find(d.views(), k.name);
+    }
+  }
+  return -1;
+}
+
+static uint64_t store_bits(const Store& st, const Declarations& d) {
+  uint64_t out = 0;
+  for (const auto& [k, pr] : st) out |= (uint64_t)pair_bits(pr) << (2 * key_index(d, k));
+  return out;
+}
+
+static void sweep_node(const AnnotatedProgram& p, uint64_t seed, std::vector<bool>& prefix, int max_dec, int fuel,
+                       std::vector<coh_sweep_leaf>& out) {
+  AnnotatedRun r = run_annotated(p, fuel, Schedule(prefix));
+  const bool exhausted = r.schedule_consumed >= prefix.size() && r.schedule_overflowed;
+  if (exhausted && (int)prefix.size() < max_dec) {
+    for (bool bit : {true, false}) {
+      prefix.push_back(bit);
+      sweep_node(p, seed, prefix, max_dec, fuel, out);
+      prefix.pop_back();
+    }
+    return;
+  }
+  coh_sweep_leaf lf;
+  std::memset(&lf, 0, sizeof lf);
+  lf.seed = seed;
+  for (size_t i = 0; i < prefix.size(); ++i) lf.schedule |= (prefix[i] ? 1u : 0u) << i;
+  lf.sched_len = (uint8_t)prefix.size();
+  lf.status = (uint8_t)r.status;
+  lf.blocks_done = (uint8_t)r.boundary_ok.size();
+  for (size_t b = 0; b < r.boundary_ok.size(); ++b) lf.boundary_ok |= (r.boundary_ok[b] ? 1u : 0u) << b;
+  lf.steps = (uint32_t)r.steps;
+  lf.consumed = (uint8_t)r.schedule_consumed;
+  lf.overflowed = r.schedule_overflowed ? 1 : 0;
+  if (r.stuck) {
+    lf.stuck_key = (uint8_t)key_index(p.decls, r.stuck->key);
+    lf.stuck_info = (uint8_t)((uint32_t)r.stuck->effect | ((r.stuck->site == Site::Remote ? 1u : 0u) << 3) |
+                              ((r.stuck->key.kind == VarKey::Kind::Abstract ? 1u : 0u) << 4) |
+                              (pair_bits(r.stuck->actual) << 5));
+  }
+  lf.store = store_bits(r.store, p.decls);
+  out.push_back(lf);
+}
+
+// Leaves of all_schedules_run over seeds [seed0, seed0+n) (testkit.hpp:465-517 order).
+// Returns the number of leaves (may exceed cap) or -1.
+int64_t ref_sweep_leaves(uint64_t seed0, uint32_t n, uint32_t max_dec, int32_t fuel, coh_sweep_leaf* leaves,
+                         uint64_t cap) {
+  std::vector<coh_sweep_leaf> all;
+  try {
+    for (uint32_t k = 0; k < n; ++k) {
+      AnnotatedProgram p = gen_well_declared(seed0 + k, GenLimits());
+      std::vector<bool> prefix;
+      sweep_node(p, seed0 + k, prefix, (int)max_dec, fuel, all);
+    }
+  } catch (...) {
+    return -1;
+  }
+  for (uint64_t i = 0; i < all.size() && i < cap; ++i) leaves[i] = all[i];
+  return (int64_t)all.size();
+}
+
+// The acceptance gate's own aggregate (tests/acceptance.cpp:77-105): runs, outcomes,
+// boundary and oracle agreement via all_schedules_run(with_oracle = true).
+int ref_sweep_stats(uint64_t seed0, uint32_t n, uint32_t max_dec, int32_t fuel, uint64_t* out6) {
+  uint64_t runs = 0, done = 0, stuck = 0, fuelx = 0, bad_bnd = 0, oracle_bad = 0;
+  for (uint32_t k = 0; k < n; ++k) {
+    AnnotatedProgram p = gen_well_declared(seed0 + k, GenLimits());
+    ScheduleSweep sw = all_schedules_run(p, (int)max_dec, fuel, true);
+    runs += sw.runs;
+    done += sw.outcomes[RunStatus::Done];
+    stuck += sw.outcomes[RunStatus::Stuck];
+    fuelx += sw.outcomes[RunStatus::FuelExhausted];
+    bad_bnd += sw.all_boundaries_ok ? 0 : 1;
+    oracle_bad += sw.oracle_agreed ? 0 : 1;
+  }
+  out6[0] = runs;
+  out6[1] = done;
+  out6[2] = stuck;
+  out6[3] = fuelx;
+  out6[4] = bad_bnd;
+  out6[5] = oracle_bad;
+  return 0;
+}
+
 }  // extern "C"

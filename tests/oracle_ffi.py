@@ -133,3 +133,35 @@ def elem_run(which, program, runs_cap=4096):
     rc = f(C.addressof(st), C.addressof(r), L.ctypes.data, R.ctypes.data, va.ctypes.data, b.ctypes.data,
            runs.ctypes.data, runs_cap)
     return rc, r, L, R, va, b, runs[: min(r.n_runs, runs_cap)]
+
+
+# ---- general programs / sweeps ----------------------------------------------------------
+def ref_program_text(seed):
+    L = reference()
+    L.ref_gen_program_text.restype = C.c_int
+    L.ref_gen_program_text.argtypes = [C.c_uint64, C.c_char_p, C.c_size_t]
+    buf = C.create_string_buffer(1 << 16)
+    assert L.ref_gen_program_text(seed, buf, len(buf)) == 0
+    return buf.value.decode()
+
+
+def ref_sweep_leaves(seed0, n, max_dec=6, fuel=10000, cap=1 << 20):
+    from paper_1910_11110_b200.sweep import LEAF_DTYPE
+
+    L = reference()
+    L.ref_sweep_leaves.restype = C.c_int64
+    L.ref_sweep_leaves.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_int32, C.c_void_p, C.c_uint64]
+    out = np.zeros(cap, LEAF_DTYPE)
+    got = L.ref_sweep_leaves(seed0, n, max_dec, fuel, out.ctypes.data, cap)
+    assert 0 <= got <= cap
+    return out[:got]
+
+
+def ref_sweep_stats(seed0, n, max_dec=6, fuel=10000):
+    L = reference()
+    L.ref_sweep_stats.restype = C.c_int
+    L.ref_sweep_stats.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_int32, C.c_void_p]
+    out = np.zeros(6, np.uint64)
+    L.ref_sweep_stats(seed0, n, max_dec, fuel, out.ctypes.data)
+    return dict(zip(["runs", "done", "stuck", "fuel_exhausted", "bad_boundary_programs", "oracle_disagreements"],
+                    (int(x) for x in out)))
