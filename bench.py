@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--bitmap-calls", type=int, default=8)
     ap.add_argument("--container-log2-floats", type=int, default=28, help="C5 vector size (0 = skip)")
     ap.add_argument("--container-calls", type=int, default=64)
+    ap.add_argument("--sweep-seeds", type=int, default=100000, help="acceptance-sweep seeds (0 = skip)")
     return ap.parse_args()
 
 
@@ -278,6 +279,23 @@ def run_container(args, ctx):
     return out
 
 
+def run_sweep(args, ctx):
+    """the acceptance corpus (gen_well_declared programs) swept over
+    every schedule of <= 6 opaque decisions, one GPU thread per run; the reference does
+    the same sweep single-threaded (criterion 4: 10000 seeds = 85335 runs in ~4.5 s)."""
+    from paper_1910_11110_b200.sweep import sweep
+
+    t0 = time.perf_counter()
+    _, st = sweep(ctx, 0, args.sweep_seeds, 6, 10000)
+    wall = time.perf_counter() - t0
+    return {"metric": "acceptance-sweep runs/s", "seeds": args.sweep_seeds, "runs": st["runs"],
+            "done": st["done"], "stuck": st["stuck"], "fuel_exhausted": st["fuel_exhausted"],
+            "runs_with_violation": st["runs_with_violation"], "device_ms": st["device_ms"],
+            "device_runs_per_s": st["nodes"] / (st["device_ms"] / 1e3) if st["device_ms"] else None,
+            "wall_s": wall, "wall_runs_per_s": st["runs"] / wall,
+            "note": "wall includes host program generation, bytecode compile and frontier management"}
+
+
 def coh_lib():
     import paper_1910_11110_b200 as coh
 
@@ -396,6 +414,7 @@ def run_ours(args, rank, world, local):
             L.coh_host_free(p)
     bitmap = run_bitmap(args, ctx, rank, world) if args.bitmap_buffers > 0 else None
     clocks.stop()
+    sweep_info = run_sweep(args, ctx) if (args.sweep_seeds > 0 and rank == 0) else None
     container = None
     if args.container_log2_floats > 0 and rank == 0:
         try:
@@ -424,7 +443,7 @@ def run_ours(args, rank, world, local):
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms": k_ms,
                          "note": "INT/LSU-issue bound in practice; see profiles/ for pipe utilisation"},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "gpu_launches": launches,
-            "bitmap": bitmap, "container": container,
+            "bitmap": bitmap, "container": container, "sweep": sweep_info,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
