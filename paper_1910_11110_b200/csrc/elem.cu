@@ -164,34 +164,13 @@ __global__ void __launch_bounds__(kET, 8) k_elem_pass1(const ElemDev d) {
       if (a == 0u && ((l[k] | r[k]) & m[k])) f |= 4u;
     }
     f = __reduce_or_sync(0xffffffffu, f);
-    if (lane == 0 && f && !d.st[b].dead) atomicOr(&d.sc[b].view_flags[tile.view], f);
+    if (lane == 0 && f && !d.st[b].dead) atomicOr(&d.sc[b * kSlots + tile.slot].view_flags[tile.view], f);
     return;
   }
   const uint32_t lo = tile.lo, hi = tile.hi;
   const bool full = tile_full(tstart, lo, hi);
   uint32_t m[kWPT];
   masks8(base, lo, hi, full, m);
-  if (op.type == EOP_WRITE) {  // set plane op.plane, clear the other (w x[i] @site)
-    uint32_t* sp = op.plane ? Rp : Lp;
-    uint32_t* cp = op.plane ? Lp : Rp;
-    if (d.st[b].dead) return;  // writes are guarded by the (device-side) stuck flag
-    if (full) {                // interior tile: pure stores, m/4 bytes
-      store8_const(sp + base, 0xFFFFFFFFu);
-      store8_const(cp + base, 0u);
-      return;
-    }
-    uint32_t sv[kWPT], cv[kWPT];
-    load8(sp + base, sv);
-    load8(cp + base, cv);
-#pragma unroll
-    for (int k = 0; k < kWPT; ++k) {
-      sv[k] |= m[k];
-      cv[k] &= ~m[k];
-    }
-    store8(sp + base, sv);
-    store8(cp + base, cv);
-    return;
-  }
   // SYNC / READ: first zero of the required (source) plane; rare -> warp min + atomic
   const uint32_t* src = op.plane ? Rp : Lp;
   uint32_t v[kWPT];
@@ -203,7 +182,7 @@ __global__ void __launch_bounds__(kET, 8) k_elem_pass1(const ElemDev d) {
     if (z) fz = (base + k) * 32u + (__ffs(z) - 1);
   }
   fz = __reduce_min_sync(0xffffffffu, fz);
-  if (lane == 0 && fz != kNoCell) atomicMin(&d.sc[b].first_zero, fz);  // ignored if dead
+  if (lane == 0 && fz != kNoCell) atomicMin(&d.sc[b * kSlots + tile.slot].first_zero, fz);  // ignored if dead
   if (op.type != EOP_SYNC) return;
   // destination zero runs: counts for the offsets, and the tile's edge bits
   const uint32_t* dst = op.plane ? Lp : Rp;
@@ -244,33 +223,38 @@ __global__ void __launch_bounds__(kET, 8) k_elem_pass1(const ElemDev d) {
     *reinterpret_cast<uint4*>(d.tcnt + 4 * tloc) = make_uint4(ns, ne, nz, edge_prev | (s_next << 1));
 }
 
-// One warp per buffer: stuck detection, run-offset scan over the op's tiles (32 tiles
-// per warp step, shuffle scan), boundary bit, scratch reset.
+// One warp per buffer: walks the buffer's ops of this stage in program order — stuck
+// detection (the first stuck op stops the buffer; a whole-view sync is atomic), run-offset
+// scan over a SYNC's tiles (shuffle scan, loads issued in batches), boundary bits — and
+// resets the scratch.
 constexpr int kDecideWarps = 4;
 __global__ void __launch_bounds__(32 * kDecideWarps) k_elem_decide(const ElemDev d) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t b = blockIdx.x * kDecideWarps + (threadIdx.x >> 5);
   if (b >= d.n_progs) return;
-  // every independent input in flight together: op, stuck flag, first zero, view flags
-  const ElemOp op = d.ops[b];
   ElemState* __restrict__ st = d.st + b;
-  ElemScratch* __restrict__ sc = d.sc + b;
-  const uint32_t dead = st->dead;
-  const uint32_t fz0 = sc->first_zero;
-  const uint32_t vf = lane < COH_MAX_VIEWS ? sc->view_flags[lane] : 0u;
-  __syncwarp();
-  if (op.type != EOP_NONE && !dead) {
+  uint32_t dead = st->dead;
+  for (uint32_t slot = 0; slot < kSlots; ++slot) {
+    const ElemOp op = d.ops[b * kSlots + slot];
+    if (op.type == EOP_NONE) break;
+    ElemScratch* __restrict__ sc = d.sc + b * kSlots + slot;
+    const uint32_t fz0 = sc->first_zero;
+    const uint32_t vf = lane < COH_MAX_VIEWS ? sc->view_flags[lane] : 0u;
+    __syncwarp();
+    if (lane == 0) sc->first_zero = kNoCell;
+    if (lane < COH_MAX_VIEWS) sc->view_flags[lane] = 0;
+    if (dead) continue;  // keep resetting the scratch of the remaining slots
     if (op.type == EOP_SYNC || op.type == EOP_READ) {
-      const uint32_t fz = fz0;
-      if (fz != kNoCell) {
+      if (fz0 != kNoCell) {
         if (lane == 0) {
           const uint32_t* Lp = d.planes + (size_t)b * 2u * d.W;
           const uint32_t* Rp = Lp + d.W;
           st->dead = 1;
-          st->stuck_op = d.stage;
-          st->stuck_cell = fz;
-          st->stuck_pair = ((Lp[fz >> 5] >> (fz & 31u)) & 1u) | (((Rp[fz >> 5] >> (fz & 31u)) & 1u) << 1);
+          st->stuck_op = d.stage * kSlots + slot;
+          st->stuck_cell = fz0;
+          st->stuck_pair = ((Lp[fz0 >> 5] >> (fz0 & 31u)) & 1u) | (((Rp[fz0 >> 5] >> (fz0 & 31u)) & 1u) << 1);
         }
+        dead = 1;
       } else if (op.type == EOP_SYNC) {
         const uint32_t t0 = op.tile0;  // stage-local tile index
         const uint32_t n_t = ((op.hi >> 5) / kElemTileWords) - ((op.lo >> 5) / kElemTileWords) + 1;
@@ -326,9 +310,8 @@ __global__ void __launch_bounds__(32 * kDecideWarps) k_elem_decide(const ElemDev
         else if (d.boundary) d.boundary[(size_t)b * d.bwords + op.call / 32] |= 1u << (op.call % 32);
       }
     }
+    __syncwarp();
   }
-  if (lane == 0) sc->first_zero = kNoCell;
-  if (lane < COH_MAX_VIEWS) sc->view_flags[lane] = 0;
 }
 
 // Warp-per-tile over this stage's SYNC tiles (self-contained descriptors): each warp loads
@@ -345,9 +328,33 @@ __global__ void __launch_bounds__(32 * kApplyWarps, 2) k_elem_apply(const ElemDe
     const ElemTile tile = d.sync_desc[it];
     const uint32_t b = tile.b, tloc = tile.tloc;
     const uint32_t dead = d.st[b].dead;
-    const uint4 cnt = *reinterpret_cast<const uint4*>(d.tcnt + 4 * tloc);
-    if (dead) continue;  // warp-uniform
+    const uint4 cnt = tile.type == EOP_SYNC ? *reinterpret_cast<const uint4*>(d.tcnt + 4 * tloc) : make_uint4(0u, 0u, 0u, 0u);
+    if (dead) continue;  // warp-uniform (also set by an earlier op of this stage)
     uint32_t* Lp = d.planes + (size_t)b * 2u * d.W;
+    if (tile.type == EOP_WRITE) {  // w x[i] @site over the range: set one plane, clear the other
+      uint4* sp4 = reinterpret_cast<uint4*>((tile.plane ? Lp + d.W : Lp) + tile.tstart);
+      uint4* cp4 = reinterpret_cast<uint4*>((tile.plane ? Lp : Lp + d.W) + tile.tstart);
+      if (tile_full(tile.tstart, tile.lo, tile.hi)) {
+#pragma unroll
+        for (int j = 0; j < kElemTileWords / 128; ++j) {
+          __stcg(sp4 + lane + 32 * j, make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu));
+          __stcg(cp4 + lane + 32 * j, make_uint4(0u, 0u, 0u, 0u));
+        }
+      } else {
+        for (int j = 0; j < kElemTileWords / 128; ++j) {
+          const uint32_t w = tile.tstart + 4u * (lane + 32u * j);
+          const uint32_t m0 = word_mask(w, tile.lo, tile.hi), m1 = word_mask(w + 1, tile.lo, tile.hi),
+                         m2 = word_mask(w + 2, tile.lo, tile.hi), m3 = word_mask(w + 3, tile.lo, tile.hi);
+          if ((m0 | m1 | m2 | m3) == 0u) continue;
+          uint4 a = __ldcg(sp4 + lane + 32 * j), c = __ldcg(cp4 + lane + 32 * j);
+          a.x |= m0; a.y |= m1; a.z |= m2; a.w |= m3;
+          c.x &= ~m0; c.y &= ~m1; c.z &= ~m2; c.w &= ~m3;
+          __stcg(sp4 + lane + 32 * j, a);
+          __stcg(cp4 + lane + 32 * j, c);
+        }
+      }
+      continue;
+    }
     uint32_t* dst = tile.plane ? Lp : Lp + d.W;
     const uint32_t tstart = tile.tstart;
     const bool full = tile_full(tstart, tile.lo, tile.hi);
@@ -443,7 +450,8 @@ __global__ void __launch_bounds__(32 * kApplyWarps, 2) k_elem_apply(const ElemDe
 int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, uint32_t n_sync_tiles, void* stream, std::string* err) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n_tiles) k_elem_pass1<<<n_tiles, kET, 0, s>>>(d);
-  k_elem_decide<<<(d.n_progs + kDecideWarps - 1) / kDecideWarps, 32 * kDecideWarps, 0, s>>>(d);
+  if (n_tiles)  // a stage with only WRITE ops has nothing to decide (writes cannot get stuck)
+    k_elem_decide<<<(d.n_progs + kDecideWarps - 1) / kDecideWarps, 32 * kDecideWarps, 0, s>>>(d);
   if (n_sync_tiles) {
     const uint32_t blocks = (n_sync_tiles + kApplyWarps - 1) / kApplyWarps;
     k_elem_apply<<<blocks < 148u * 16u ? blocks : 148u * 16u, 32 * kApplyWarps, 0, s>>>(d, n_sync_tiles);

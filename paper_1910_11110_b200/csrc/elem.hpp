@@ -9,6 +9,12 @@
 
 namespace cohb {
 
+// A stage holds, per buffer, up to kSlots consecutive ops: read-only ops (READ, CHECK)
+// followed by at most one writing op (SYNC or WRITE) as the last.  pass1 evaluates every
+// read against the stage-start state, decide walks the slots in program order (the first
+// stuck op stops the buffer), apply performs the write.
+constexpr uint32_t kSlots = 4;
+
 // One device op of one buffer in one stage (16 B).
 enum : uint8_t { EOP_NONE = 0, EOP_SYNC = 1, EOP_READ = 2, EOP_WRITE = 3, EOP_CHECK = 4 };
 struct ElemOp {
@@ -30,8 +36,9 @@ struct ElemTile {
   uint32_t tstart;
   uint32_t lo, hi;
   uint8_t type, plane, view, apair;
-  uint32_t tloc;
-  uint32_t pad[2];
+  uint32_t tloc;     // stage-local index in the pass1 tile list (tcnt / tbase slot)
+  uint32_t slot;     // op slot of the buffer in this stage
+  uint32_t pad;
 };
 static_assert(sizeof(ElemTile) == 32, "ElemTile is 32 bytes");
 
@@ -41,7 +48,7 @@ constexpr uint32_t kNoCell = 0xFFFFFFFFu;
 // Device-side per-buffer state.
 struct ElemState {
   uint32_t dead;          // stopped by a device-detected stuck
-  uint32_t stuck_op;      // stage index
+  uint32_t stuck_op;      // stage * kSlots + slot
   uint32_t stuck_cell;
   uint32_t stuck_pair;    // bit0 L, bit1 R at stuck_cell
   uint32_t calls_done;
@@ -52,7 +59,7 @@ struct ElemState {
   unsigned long long n_runs;      // run starts emitted (== ends)
 };
 
-// Per-stage scratch, per buffer.
+// Per-stage scratch, per buffer and op slot ([b * kSlots + slot]).
 struct ElemScratch {
   uint32_t first_zero;    // atomicMin over the op range (SYNC source / READ plane)
   uint32_t view_flags[COH_MAX_VIEWS];   // CHECK: bit0 some L=0, bit1 some R=0, bit2 some L|R=1
@@ -63,16 +70,17 @@ struct ElemPlan {
   uint32_t n_progs = 0;
   uint32_t max_words = 0;            // words per plane per buffer (multiple of 4)
   uint32_t n_stages = 0;
-  std::vector<ElemOp> ops;           // [stage][prog]
+  std::vector<ElemOp> ops;           // [stage][prog][slot]
   std::vector<ElemTile> tiles;       // all stages concatenated
   std::vector<uint32_t> stage_tile0; // n_stages + 1 offsets into tiles
   std::vector<uint8_t> stage_has_sync;
-  std::vector<ElemTile> sync_tiles;        // copies of the SYNC ops' tiles, by stage
+  std::vector<ElemTile> sync_tiles;        // apply-pass tiles (SYNC and WRITE ops), by stage
   std::vector<uint32_t> stage_sync0;       // n_stages + 1 offsets into sync_tiles
   // host timeline, per program
   struct Timeline {
     std::vector<uint64_t> steps_before;   // per stage (device op) of this program
     std::vector<uint32_t> abs_before;     // abstract pairs (2 b/view) before each device op
+    std::vector<uint32_t> op_pos;         // stage * kSlots + slot of each device op
     uint32_t abs_final = 0;
     uint32_t n_ops = 0;
     uint64_t steps_total = 0;             // steps when the host-known sequence ends
@@ -92,7 +100,7 @@ int elem_compile(const coh_elem_program* progs, uint32_t n, ElemPlan* plan, std:
 struct ElemDev {
   uint32_t* planes;            // [b][2][W]
   uint32_t W;                  // words per plane (multiple of kElemTileWords)
-  const ElemOp* ops;           // this stage, [b]
+  const ElemOp* ops;           // this stage, [b][slot]
   const ElemTile* tiles;       // this stage
   const ElemTile* sync_desc;   // this stage: descriptors of the SYNC tiles (apply pass)
   ElemState* st;

@@ -177,12 +177,27 @@ int elem_compile(const coh_elem_program* progs, uint32_t n, ElemPlan* plan, std:
     T.abs_final = 0;
     for (uint32_t v = 0; v < P.n_views; ++v) T.abs_final |= abs[v] << (2 * v);
   }
-  // stages: op k of every program runs in stage k
+  // stages: per buffer, runs of read-only ops closed by at most one writing op
+  std::vector<std::vector<std::vector<ElemOp>>> st_ops(n);  // [b][stage] -> ops in order
+  for (uint32_t b = 0; b < n; ++b) {
+    std::vector<ElemOp> cur;
+    plan->tl[b].op_pos.clear();
+    for (const ElemOp& op : per[b]) {
+      const bool writes = op.type == EOP_SYNC || op.type == EOP_WRITE;
+      cur.push_back(op);
+      plan->tl[b].op_pos.push_back((uint32_t)st_ops[b].size() * kSlots + (uint32_t)cur.size() - 1);
+      if (writes || cur.size() == kSlots) {
+        st_ops[b].push_back(cur);
+        cur.clear();
+      }
+    }
+    if (!cur.empty()) st_ops[b].push_back(cur);
+  }
   uint32_t n_stages = 0;
-  for (auto& v : per) n_stages = std::max(n_stages, (uint32_t)v.size());
+  for (auto& v : st_ops) n_stages = std::max(n_stages, (uint32_t)v.size());
   plan->n_stages = n_stages;
   plan->max_words = ((max_cells + 31) / 32 + 3) & ~3u;
-  plan->ops.assign((size_t)n_stages * n, ElemOp{EOP_NONE, 0, 0, 0, 0, 0});
+  plan->ops.assign((size_t)n_stages * n * kSlots, ElemOp{EOP_NONE, 0, 0, 0, 0, 0});
   plan->tiles.clear();
   plan->stage_tile0.assign(n_stages + 1, 0);
   plan->stage_has_sync.assign(n_stages, 0);
@@ -192,37 +207,43 @@ int elem_compile(const coh_elem_program* progs, uint32_t n, ElemPlan* plan, std:
     plan->stage_tile0[s] = (uint32_t)plan->tiles.size();
     plan->stage_sync0[s] = (uint32_t)plan->sync_tiles.size();
     for (uint32_t b = 0; b < n; ++b) {
-      if (s >= per[b].size()) continue;
-      ElemOp op = per[b][s];
-      op.tile0 = (uint32_t)plan->tiles.size() - plan->stage_tile0[s];  // stage-local
-      auto add_range = [&](uint32_t lo, uint32_t hi, uint32_t view, uint32_t apair) {
-        const uint32_t w_lo = lo / 32, w_hi = hi / 32;
-        for (uint32_t t0 = (w_lo / kElemTileWords) * kElemTileWords; t0 <= w_hi; t0 += kElemTileWords) {
-          ElemTile t{};
-          t.b = b;
-          t.tstart = t0;
-          t.lo = lo;
-          t.hi = hi;
-          t.type = op.type;
-          t.plane = op.plane;
-          t.view = (uint8_t)view;
-          t.apair = (uint8_t)apair;
-          t.tloc = (uint32_t)plan->tiles.size() - plan->stage_tile0[s];
-          plan->tiles.push_back(t);
+      if (s >= st_ops[b].size()) continue;
+      for (uint32_t slot = 0; slot < st_ops[b][s].size(); ++slot) {
+        ElemOp op = st_ops[b][s][slot];
+        op.tile0 = (uint32_t)plan->tiles.size() - plan->stage_tile0[s];  // stage-local (pass1 list)
+        auto make_tiles = [&](uint32_t lo, uint32_t hi, uint32_t view, uint32_t apair, std::vector<ElemTile>& dst,
+                              bool pass1) {
+          const uint32_t w_lo = lo / 32, w_hi = hi / 32;
+          for (uint32_t t0 = (w_lo / kElemTileWords) * kElemTileWords; t0 <= w_hi; t0 += kElemTileWords) {
+            ElemTile t{};
+            t.b = b;
+            t.tstart = t0;
+            t.lo = lo;
+            t.hi = hi;
+            t.type = op.type;
+            t.plane = op.plane;
+            t.view = (uint8_t)view;
+            t.apair = (uint8_t)apair;
+            t.tloc = pass1 ? (uint32_t)plan->tiles.size() - plan->stage_tile0[s] : 0u;
+            t.slot = slot;
+            dst.push_back(t);
+          }
+        };
+        if (op.type == EOP_CHECK) {
+          for (uint32_t v = 0; v < progs[b].n_views; ++v)
+            make_tiles(progs[b].view_lo[v], progs[b].view_hi[v], v, (op.lo >> (2 * v)) & 3u, plan->tiles, true);
+        } else if (op.type == EOP_WRITE) {
+          make_tiles(op.lo, op.hi, 0, 0, plan->sync_tiles, false);  // apply pass only
+        } else {
+          const size_t first = plan->tiles.size();
+          make_tiles(op.lo, op.hi, 0, 0, plan->tiles, true);
+          if (op.type == EOP_SYNC) {
+            plan->stage_has_sync[s] = 1;
+            for (size_t k = first; k < plan->tiles.size(); ++k) plan->sync_tiles.push_back(plan->tiles[k]);
+          }
         }
-      };
-      if (op.type == EOP_CHECK) {
-        for (uint32_t v = 0; v < progs[b].n_views; ++v)
-          add_range(progs[b].view_lo[v], progs[b].view_hi[v], v, (op.lo >> (2 * v)) & 3u);
-      } else {
-        add_range(op.lo, op.hi, 0, 0);
+        plan->ops[((size_t)s * n + b) * kSlots + slot] = op;
       }
-      if (op.type == EOP_SYNC) {
-        plan->stage_has_sync[s] = 1;
-        for (uint32_t k = op.tile0; k < (uint32_t)plan->tiles.size() - plan->stage_tile0[s]; ++k)
-          plan->sync_tiles.push_back(plan->tiles[plan->stage_tile0[s] + k]);
-      }
-      plan->ops[(size_t)s * n + b] = op;
     }
   }
   plan->stage_tile0[n_stages] = (uint32_t)plan->tiles.size();
@@ -353,7 +374,7 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
   COH_E(alloc(tiles, plan.tiles.size() * sizeof(ElemTile)));
   COH_E(alloc(stiles, plan.sync_tiles.size() * sizeof(ElemTile)));
   COH_E(alloc(st, (size_t)n * sizeof(ElemState)));
-  COH_E(alloc(sc, (size_t)n * sizeof(ElemScratch)));
+  COH_E(alloc(sc, (size_t)n * kSlots * sizeof(ElemScratch)));
   COH_E(alloc(tcnt, (size_t)max_tiles * 4 * 4));
   COH_E(alloc(tbase, (size_t)max_tiles * 2 * 8));
   COH_E(alloc(vlo, (size_t)n * COH_MAX_VIEWS * 4));
@@ -372,7 +393,7 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
       h_vhi[(size_t)b * COH_MAX_VIEWS + v] = progs[b].view_hi[v];
     }
   }
-  std::vector<ElemScratch> h_sc(n);
+  std::vector<ElemScratch> h_sc((size_t)n * kSlots);
   for (auto& x : h_sc) {
     x.first_zero = kNoCell;
     for (auto& f : x.view_flags) f = 0;
@@ -404,7 +425,7 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
       ElemDev d;
       d.planes = planes.as<uint32_t>();
       d.W = W;
-      d.ops = ops.as<ElemOp>() + (size_t)stg * n;
+      d.ops = ops.as<ElemOp>() + (size_t)stg * n * kSlots;
       d.tiles = tiles.as<ElemTile>() + plan.stage_tile0[stg];
       d.sync_desc = stiles.as<ElemTile>() + plan.stage_sync0[stg];
       d.st = st.as<ElemState>();
@@ -423,7 +444,7 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
       const uint32_t nt = plan.stage_tile0[stg + 1] - plan.stage_tile0[stg];
       const uint32_t ns = plan.stage_sync0[stg + 1] - plan.stage_sync0[stg];
       r = launch_elem_stage(d, nt, ns, s, &err);
-      launches += (nt ? 1 : 0) + 1 + (ns ? 1 : 0);
+      launches += (nt ? 2 : 0) + (ns ? 1 : 0);
     }
     return r;
   };
@@ -489,16 +510,19 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
     uint32_t abs_final = T.abs_final;
     uint32_t executed_ops = T.n_ops;
     if (S.dead) {
-      const ElemOp& op = plan.ops[(size_t)S.stuck_op * n + b];
-      executed_ops = S.stuck_op;
+      const uint32_t stage = S.stuck_op / kSlots, slot = S.stuck_op % kSlots;
+      const ElemOp& op = plan.ops[((size_t)stage * n + b) * kSlots + slot];
+      uint32_t k = 0;
+      while (k < T.op_pos.size() && T.op_pos[k] != S.stuck_op) ++k;
+      executed_ops = k;
       r.status = COH_RUN_STUCK;
       r.stuck_call = op.call;
       r.stuck_index = S.stuck_cell;
       const uint32_t site = op.type == EOP_READ ? op.plane : 0u;
       r.stuck_effect = (uint8_t)(op.type == EOP_READ ? COH_READ : (op.plane ? COH_PULL : COH_PUSH));
       r.stuck_flags = (uint8_t)(site | (S.stuck_pair << 2));
-      r.steps = T.steps_before[S.stuck_op] + (op.type == EOP_READ ? (uint64_t)(S.stuck_cell - op.lo) : 0u);
-      abs_final = T.abs_before[S.stuck_op];
+      r.steps = T.steps_before[k] + (op.type == EOP_READ ? (uint64_t)(S.stuck_cell - op.lo) : 0u);
+      abs_final = T.abs_before[k];
     } else {
       r.status = T.term_status;
       r.steps = T.steps_total;
@@ -511,7 +535,8 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
     }
     // VectorPU-faithful transfer size: the whole view range of every executed sync
     for (uint32_t k = 0; k < executed_ops; ++k) {
-      const ElemOp& op = plan.ops[(size_t)k * n + b];
+      const uint32_t pos = T.op_pos[k];
+      const ElemOp& op = plan.ops[((size_t)(pos / kSlots) * n + b) * kSlots + pos % kSlots];
       if (op.type == EOP_SYNC) r.vpu_cells += (uint64_t)(op.hi - op.lo + 1);
     }
     if (view_abs_out)
