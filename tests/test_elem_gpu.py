@@ -75,3 +75,18 @@ def test_malformed_program_is_construction_error(ctx):
     with pytest.raises(coh.CohError) as e:
         elem_eval(ctx, [bad])
     assert e.value.code == 1
+
+
+def test_reference_sample_element_gpu(ctx):
+    # proj/samples/element_gpu.coh + proj/tests/golden/element_gpu.run.txt:
+    #   buffer b[10]; view x = b[0:9]; GRW(x) { gw x[3]; }
+    #   -> done, 5 steps, b[3] (I,V), every other cell (V,V), x^ (I,V)
+    p = Program(10, [0], [9], [(0, 2, 1, [(3, 1, 3, 3)])])
+    out = elem_eval(ctx, [p])
+    r = out["results"][0]
+    assert r.status == 0 and r.steps == 5 and r.transfers == 1
+    L, R = out["planes"][0][0][0], out["planes"][0][1][0]
+    cells = [("V" if (L >> i) & 1 else "I") + ("V" if (R >> i) & 1 else "I") for i in range(10)]
+    assert cells == ["VV"] * 3 + ["IV"] + ["VV"] * 6
+    assert out["view_abs"][0][0] == 2  # (I,V)
+    assert list(map(list, out["runs"][0][:1])) == [[0, 9]]  # the push copies the whole view once
