@@ -157,11 +157,22 @@ __global__ void __launch_bounds__(kET, 8) k_elem_pass1(const ElemDev d) {
     if (a != 1u) load8(Rp + base, r);   // (V,I) needs only L
     masks8(base, lo, hi, tile_full(tstart, lo, hi), m);
     uint32_t f = 0;
+    if (tile_full(tstart, lo, hi)) {  // interior tile: AND / OR reductions, no per-word masks
+      uint32_t al = 0xFFFFFFFFu, ar = 0xFFFFFFFFu, o = 0u;
 #pragma unroll
-    for (int k = 0; k < kWPT; ++k) {
-      if (a != 2u && (~l[k] & m[k])) f |= 1u;
-      if (a != 1u && (~r[k] & m[k])) f |= 2u;
-      if (a == 0u && ((l[k] | r[k]) & m[k])) f |= 4u;
+      for (int k = 0; k < kWPT; ++k) {
+        if (a != 2u) al &= l[k];
+        if (a != 1u) ar &= r[k];
+        if (a == 0u) o |= l[k] | r[k];
+      }
+      f = (a != 2u && al != 0xFFFFFFFFu ? 1u : 0u) | (a != 1u && ar != 0xFFFFFFFFu ? 2u : 0u) | (o ? 4u : 0u);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kWPT; ++k) {
+        if (a != 2u && (~l[k] & m[k])) f |= 1u;
+        if (a != 1u && (~r[k] & m[k])) f |= 2u;
+        if (a == 0u && ((l[k] | r[k]) & m[k])) f |= 4u;
+      }
     }
     f = __reduce_or_sync(0xffffffffu, f);
     if (lane == 0 && f && !d.st[b].dead) atomicOr(&d.sc[b * kSlots + tile.slot].view_flags[tile.view], f);
@@ -176,10 +187,15 @@ __global__ void __launch_bounds__(kET, 8) k_elem_pass1(const ElemDev d) {
   uint32_t v[kWPT];
   load8(src + base, v);
   uint32_t fz = kNoCell;
+  uint32_t all = 0xFFFFFFFFu;
 #pragma unroll
-  for (int k = kWPT - 1; k >= 0; --k) {
-    const uint32_t z = ~v[k] & m[k];
-    if (z) fz = (base + k) * 32u + (__ffs(z) - 1);
+  for (int k = 0; k < kWPT; ++k) all &= v[k] | ~m[k];
+  if (all != 0xFFFFFFFFu) {  // some required bit is 0 here: locate the first one
+#pragma unroll
+    for (int k = kWPT - 1; k >= 0; --k) {
+      const uint32_t z = ~v[k] & m[k];
+      if (z) fz = (base + k) * 32u + (__ffs(z) - 1);
+    }
   }
   fz = __reduce_min_sync(0xffffffffu, fz);
   if (lane == 0 && fz != kNoCell) atomicMin(&d.sc[b * kSlots + tile.slot].first_zero, fz);  // ignored if dead
@@ -208,13 +224,28 @@ __global__ void __launch_bounds__(kET, 8) k_elem_pass1(const ElemDev d) {
   __syncthreads();
   const uint32_t pt = threadIdx.x ? (s_last[threadIdx.x - 1] >> 31) : edge_prev;
   const uint32_t nb = threadIdx.x < kET - 1 ? (s_first[threadIdx.x + 1] & 1u) : s_next;
-  run_edges(z, pt, nb, sts, ens);
   uint32_t ns = 0, ne = 0, nz = 0;
+  uint32_t zor = 0u, zand = 0xFFFFFFFFu;
 #pragma unroll
   for (int k = 0; k < kWPT; ++k) {
-    ns += __popc(sts[k]);
-    ne += __popc(ens[k]);
-    nz += __popc(z[k]);
+    zor |= z[k];
+    zand &= z[k];
+  }
+  if (zor == 0u) {
+    // destination already valid on these 8 words: no changed cells, no run edges
+  } else if (zand == 0xFFFFFFFFu) {
+    // all 256 cells change: a run can only start at the first bit / end at the last
+    nz = 32u * kWPT;
+    ns = pt ? 0u : 1u;
+    ne = nb ? 0u : 1u;
+  } else {
+    run_edges(z, pt, nb, sts, ens);
+#pragma unroll
+    for (int k = 0; k < kWPT; ++k) {
+      ns += __popc(sts[k]);
+      ne += __popc(ens[k]);
+      nz += __popc(z[k]);
+    }
   }
   ns = block_sum(ns, red);
   ne = block_sum(ne, red);
@@ -321,7 +352,7 @@ __global__ void __launch_bounds__(32 * kDecideWarps) k_elem_decide(const ElemDev
 // with a warp scan (lane l owns words [64 l, 64 l + 63] of the tile).
 constexpr int kApplyWarps = 8;
 constexpr int kWPL = kElemTileWords / 32;  // 64 words per lane
-__global__ void __launch_bounds__(32 * kApplyWarps, 2) k_elem_apply(const ElemDev d, uint32_t n_sync_tiles) {
+__global__ void __launch_bounds__(32 * kApplyWarps, 4) k_elem_apply(const ElemDev d, uint32_t n_sync_tiles) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t gw = blockIdx.x * kApplyWarps + (threadIdx.x >> 5), nw = gridDim.x * kApplyWarps;
   for (uint32_t it = gw; it < n_sync_tiles; it += nw) {
