@@ -296,6 +296,38 @@ def run_sweep(args, ctx):
             "note": "wall includes host program generation, bytecode compile and frontier management"}
 
 
+def run_c1(ctx):
+    """BASELINE config 1: one trace of 1000 random calls on one array (seed 0, default
+    mix), the latency case: device time of one trace_eval launch (CUDA events, best of
+    20) vs the reference's run_annotated on the same records (host, best of 5)."""
+    import torch
+
+    import paper_1910_11110_b200 as coh
+
+    recs = coh.gen_records_host(0, 0, 1, 1000, 1, ADV)
+    s = torch.cuda.current_stream().cuda_stream
+    d_rec = torch.from_numpy(recs.view(np.int16).copy()).cuda()
+    d_res = torch.empty(64, dtype=torch.uint8, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = None
+    for _ in range(20):
+        e0.record()
+        ctx.eval_traces(d_rec, 1, 1000, 1, FUEL, d_res, None, stream=s)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) * 1e3
+        best = t if best is None else min(best, t)
+    kind, fn = cpu_eval_fn()
+    ref = None
+    for _ in range(5):
+        t0 = time.perf_counter()
+        fn(recs, 1, 1)
+        t = (time.perf_counter() - t0) * 1e6
+        ref = t if ref is None else min(ref, t)
+    return {"metric": "C1 latency: one trace of 1000 calls on one array", "gpu_us": best, "cpu_us": ref,
+            "cpu_kind": kind, "note": "a single dependent chain: one GPU thread vs one CPU thread"}
+
+
 def coh_lib():
     import paper_1910_11110_b200 as coh
 
@@ -415,6 +447,7 @@ def run_ours(args, rank, world, local):
     bitmap = run_bitmap(args, ctx, rank, world) if args.bitmap_buffers > 0 else None
     clocks.stop()
     sweep_info = run_sweep(args, ctx) if (args.sweep_seeds > 0 and rank == 0) else None
+    c1 = run_c1(ctx) if rank == 0 else None
     container = None
     if args.container_log2_floats > 0 and rank == 0:
         try:
@@ -443,7 +476,7 @@ def run_ours(args, rank, world, local):
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms": k_ms,
                          "note": "INT/LSU-issue bound in practice; see profiles/ for pipe utilisation"},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "gpu_launches": launches,
-            "bitmap": bitmap, "container": container, "sweep": sweep_info,
+            "bitmap": bitmap, "container": container, "sweep": sweep_info, "c1": c1,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
