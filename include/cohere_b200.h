@@ -47,22 +47,27 @@ enum { COH_KEY_CONCRETE = 0, COH_KEY_ABSTRACT = 1 }; /* VarKey::Kind Scalar / Ab
 /* ---- whole-array component-call records ------------------------------------------
  * One uint16 per component call (one DeclBlock with a single AccessMode on one array,
  * program.hpp:212-235), SURVEY §8(d):
- *   bits 0-5  array id            (the scalar "a<id>" of the reference harness)
- *   bits 6-7  mode kind R/W/RW    (3 is malformed -> COH_RUN_DEFECT)
- *   bit  8    site (0 CPU/Local, 1 GPU/Remote)
- *   bits 9-11 body variant        (0 = canonical well-declared body, 1..7 adversarial;
- *                                  see DESIGN.md §3 / coh_body_variant_ops)
- *   bits 12-15 zero
+ *   bits 0-1   reserved (zero; ignored)
+ *   bits 2-7   call type = mode kind R/W/RW (bits 2-3; 3 is malformed -> COH_RUN_DEFECT)
+ *              | site << 2 (bit 4: 0 CPU/Local, 1 GPU/Remote)
+ *              | body variant << 3 (bits 5-7: 0 = canonical well-declared body, 1..7
+ *                adversarial; see DESIGN.md §3 / coh_calltable_program)
+ *   bits 8-13  array id (the scalar "a<id>" of the reference harness; an id >= n_arrays
+ *              is a missing key -> COH_RUN_DEFECT)
+ *   bits 14-15 reserved (zero; ignored)
+ * The two fields sit in separate bytes so the device turns a record into a store-slot
+ * address and a call-table address with one masked logic op each.
  * Device layout, "call-major interleaved": rec(t, i) = records[((i/8)*n_traces + t)*8 + i%8]
  * so one 128-bit load brings 8 calls of one trace and a warp's loads are contiguous.
  * Padding records (i >= n_calls) are ignored.
  */
-#define COH_REC_ARRAY(r) ((r) & 63u)
-#define COH_REC_KIND(r) (((r) >> 6) & 3u)
-#define COH_REC_SITE(r) (((r) >> 8) & 1u)
-#define COH_REC_VARIANT(r) (((r) >> 9) & 7u)
+#define COH_REC_TYPE(r) (((r) >> 2) & 63u)
+#define COH_REC_ARRAY(r) (((r) >> 8) & 63u)
+#define COH_REC_KIND(r) (((r) >> 2) & 3u)
+#define COH_REC_SITE(r) (((r) >> 4) & 1u)
+#define COH_REC_VARIANT(r) (((r) >> 5) & 7u)
 #define COH_MAKE_REC(arr, kind, site, var) \
-  ((uint16_t)(((arr) & 63u) | (((kind) & 3u) << 6) | (((site) & 1u) << 8) | (((var) & 7u) << 9)))
+  ((uint16_t)((((arr) & 63u) << 8) | (((kind) & 3u) << 2) | (((site) & 1u) << 4) | (((var) & 7u) << 5)))
 #define COH_MAX_ARRAYS 64
 #define COH_N_VARIANTS 8
 
@@ -120,7 +125,7 @@ const char* coh_version(void);
  * Replaces translate_mode / translate_block (modes.hpp:31-59) + effect_signature /
  * apply_signature (validity.hpp:79-120) + the swap rule of apply_effect_at
  * (semantics.hpp:109-130), compiled into a (call type x 16 states) table.
- * call type = record bits 6..11 (kind | site<<2 | variant<<3), 64 types.
+ * call type = record bits 2..7 (kind | site<<2 | variant<<3), 64 types.
  * coh_calltable_describe fills, for one (type, state), what the reference run of that
  * block from that store produces.  Returns COH_OK or COH_E_ARG. */
 typedef struct coh_call_outcome {

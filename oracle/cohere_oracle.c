@@ -130,7 +130,7 @@ static void run_block(const orc_stmt* s, int n, int* conc, int* abst, int fuel, 
 /* One block from a state nibble (cl, cr, al, ar): the call-table KAT. */
 int orc_call_outcome(uint32_t call_type, uint32_t state, coh_call_outcome* out) {
   orc_stmt s[8];
-  const int n = translate_call((uint16_t)(call_type << 6), s);
+  const int n = translate_call((uint16_t)(call_type << 2), s); /* COH_REC_TYPE */
   int conc = (int)(state & 3u), abst = (int)(state >> 2);
   orc_block_out o;
   memset(out, 0, sizeof *out);

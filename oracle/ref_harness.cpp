@@ -220,7 +220,7 @@ int ref_call_outcome(uint32_t call_type, uint32_t state, coh_call_outcome* o) {
   Store s = initial_store(d);
   s.put(VarKey::scalar("a0"), bits_pair(state & 3u));
   s.put(VarKey::abstract("a0"), bits_pair(state >> 2));
-  const uint16_t rec = (uint16_t)(call_type << 6);
+  const uint16_t rec = (uint16_t)(call_type << 2);  // array 0, COH_REC_TYPE = call_type
   DeclBlock b = make_block(d, rec);
   auto viol = [&](const Store& st) { return abstraction_correct(st, d) ? 0 : 1; };
   o->viol_before = (uint8_t)viol(s);

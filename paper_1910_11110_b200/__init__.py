@@ -19,6 +19,8 @@ from ._ffi import (  # noqa: F401
     gen_records_host,
     lib,
     lib_path,
+    make_record,
+    record_fields,
     records_elems,
     boundary_words,
 )
@@ -40,6 +42,8 @@ __all__ = [
     "calltable_describe",
     "calltable_program",
     "gen_records_host",
+    "make_record",
+    "record_fields",
     "records_elems",
     "boundary_words",
     "annotated_run",

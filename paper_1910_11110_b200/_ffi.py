@@ -125,6 +125,18 @@ def lib():
     return _lib
 
 
+def make_record(array: int, kind: int, site: int, variant: int) -> int:
+    """One whole-array call record (include/cohere_b200.h COH_MAKE_REC): call type in
+    bits 2-7 (kind | site << 2 | variant << 3), array id in bits 8-13."""
+    return ((array & 63) << 8) | ((kind & 3) << 2) | ((site & 1) << 4) | ((variant & 7) << 5)
+
+
+def record_fields(recs: np.ndarray) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
+    """(array, kind, site, variant) of packed records."""
+    r = recs.astype(np.uint32)
+    return (r >> 8) & 63, (r >> 2) & 3, (r >> 4) & 1, (r >> 5) & 7
+
+
 def records_elems(n_traces: int, n_calls: int) -> int:
     return ((n_calls + 7) // 8) * n_traces * 8
 

@@ -149,7 +149,7 @@ class Runtime:
         each (vector, mode) argument becomes one canonical-body call record (a
         multi-argument block is split into single-mode blocks; for canonical bodies the
         copies are identical)."""
-        recs = [a | (k << 6) | (s << 8) for s, args in self.log for a, k in args]
+        recs = [_ffi.make_record(a, k, s, 0) for s, args in self.log for a, k in args]
         n = len(recs)
         out = np.zeros(_ffi.records_elems(1, n), np.uint16)
         out[:n] = recs  # one trace: record i at [(i/8)*1 + 0]*8 + i%8 == i

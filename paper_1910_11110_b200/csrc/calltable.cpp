@@ -150,17 +150,19 @@ void build_call_table(CallTable* t) {
     uint64_t prog = 0;
     for (int k = 0; k < 8; ++k) prog |= (uint64_t)ops[k] << (8 * k);
     t->prog[type] = prog;
+    t->lut[kStates * 64u + type] = kPoisonSlot | (kSlowAddend << 16);  // poison row
     for (uint32_t s = 0; s < (uint32_t)kStates; ++s) {
       const coh_call_outcome o = simulate_block(type, s, 1 << 30);
       uint32_t lo, hi;
       if (o.status != COH_RUN_DONE) {
-        lo = 0;
+        lo = slot_word(s);
         hi = kSlowAddend;
       } else {
-        lo = (uint32_t)((((int)o.state_after - (int)s) << kStateShift) + ((int)o.transfers << kCountShift)) & 0xFFFFu;
-        hi = ((uint32_t)o.steps + (uint32_t)(((int)o.viol_after - (int)o.viol_before) * 256)) & 0xFFFFu;
+        lo = slot_word(o.state_after);
+        hi = ((uint32_t)o.steps + ((uint32_t)o.transfers << kAccXferShift) +
+              (uint32_t)(((int)o.viol_after - (int)o.viol_before + 1) * (1 << kAccViolShift))) & 0xFFFFu;
       }
-      t->lut[lut_slot(type, s)] = lo | (hi << 16);
+      t->lut[lut_word(type, s)] = lo | (hi << 16);
       for (uint32_t rem = 0; rem < 8; ++rem) {
         const coh_call_outcome q = simulate_block(type, s, rem == 7 ? (1 << 30) : (int)rem);
         t->slow[slow_index(type, s, rem)] =

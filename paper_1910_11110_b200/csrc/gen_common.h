@@ -24,5 +24,5 @@ COH_HD uint16_t coh_gen_record(uint64_t seed, uint64_t trace_id, uint32_t call_i
   const uint32_t site = (uint32_t)((h >> 48) & 1ull);
   const uint32_t adv = ((uint32_t)((h >> 49) & 0x3FFull)) < adv_per1024;
   const uint32_t var = adv ? 1u + (uint32_t)((((h >> 59) & 0x1Full) * 7ull) >> 5) : 0u;
-  return (uint16_t)(arr | (kind << 6) | (site << 8) | (var << 9));
+  return (uint16_t)((arr << 8) | (kind << 2) | (site << 4) | (var << 5));
 }

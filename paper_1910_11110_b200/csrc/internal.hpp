@@ -8,6 +8,12 @@
 
 #include "cohere_b200.h"
 
+#if defined(__CUDACC__)
+#define COH_HDC __host__ __device__ constexpr
+#else
+#define COH_HDC constexpr
+#endif
+
 namespace cohb {
 
 // ---- micro-op encoding of one translated block (see coh_calltable_program) ----------
@@ -18,33 +24,42 @@ constexpr uint8_t op_effect(uint32_t eff, uint32_t site, uint32_t abstract_targe
 // A malformed record (mode kind 3) compiles to this single op.
 constexpr uint8_t OP_DEFECT = 0x80;
 
-constexpr int kCallTypes = 64;   // record bits 6..11
+constexpr int kCallTypes = 64;   // record bits 2..7
 constexpr int kStates = 16;      // state nibble
-constexpr int kLutEntries = kCallTypes * kStates;
 
-// State word in shared memory (one u32 per array per trace):
-//   bits kStateShift..+3 : state nibble (bit0 cl, bit1 cr, bit2 al, bit3 ar)
-//   bits kCountShift..31 : executed concrete push/pull on this array (transfers)
-constexpr uint32_t kStateShift = 2;
-constexpr uint32_t kCountShift = 6;
+// Store slot in shared memory (one u16 per array per trace), "clean" so that it can be
+// XORed straight into a table address:
+//   bits 2-5  state nibble (bit0 cl, bit1 cr, bit2 al, bit3 ar) -- the bank-swizzle copy
+//   bits 8-11 state nibble again                                  -- the table row
+//   bit  12   poison row: an array id >= n_arrays (a missing key, program.hpp:147-151)
+// Transfers, steps and violations are not per-array state: they accumulate in a register.
+COH_HDC uint32_t slot_word(uint32_t state) { return (state << 8) | (state << 2); }
+constexpr uint32_t kPoisonSlot = 0x1000u;
 
-// LUT entry (uint32), stored at slot = type*16 + (state ^ (type & 15)) (bank swizzle):
-//   lo16 : signed delta of the state word = ((ns - s) << kStateShift) + (tr << kCountShift)
-//          (0 for slow entries, so the speculative store rewrites the old word)
-//   hi16 : signed accumulator addend = steps + viol_delta * 256, or kSlowAddend for a
-//          (type, state) that gets stuck / is malformed
+// Call table (u32 entries), addressed by byte offset (type << 2) ^ slot, i.e. word
+// state*64 + (type ^ state): rows of 64 words per state (bank = (type ^ state) & 31, so
+// the common (type, state) pairs of a warp spread over the banks), plus row 16 for the
+// poison slot (word 1024 + type).
+//   lo16 : the slot word after the call (stored as is)
+//   hi16 : accumulator addend = steps + (transfers << 7) + ((viol_delta + 1) << 13), always
+//          in [0, 0x7FFF] (the +1 is a per-call bias the device subtracts at each flush), or
+//          kSlowAddend (the entry is negative) for a (type, state) that gets stuck / is
+//          malformed / reads a poison slot
+constexpr int kLutRows = kStates + 1;
+constexpr int kLutEntries = kLutRows * kCallTypes;
 constexpr uint32_t kSlowAddend = 0x8000u;
-constexpr uint32_t lut_slot(uint32_t type, uint32_t state) { return type * 16u + (state ^ (type & 15u)); }
+COH_HDC uint32_t lut_word(uint32_t type, uint32_t state) { return state * 64u + (type ^ state); }
+constexpr uint32_t kAccSteps = 0x7Fu;   // accumulator bits 0-6: steps since the last flush
+constexpr uint32_t kAccXferShift = 7;   // bits 7-12: transfers since the last flush
+constexpr uint32_t kAccViolShift = 13;  // bits 13-19: arrays whose abstraction is violated
+constexpr uint32_t kAccKeep = ~((1u << kAccViolShift) - 1u);
 
 // Slow-outcome table: the exact block outcome for (type, state, remaining fuel r), r
 // clamped to [0, 7] (a block takes at most 6 steps, so r >= 7 means "unlimited"):
 //   bits 0-1 status, 2-4 steps, 5-6 transfers, 7-10 state after, 11-13 stuck effect,
 //   14-17 stuck flags (site | key kind << 1 | actual << 2)
-constexpr int kSlowEntries = kLutEntries * 8;
-#if defined(__CUDACC__)
-__host__ __device__
-#endif
-constexpr uint32_t slow_index(uint32_t type, uint32_t state, uint32_t rem) { return (type * 16u + state) * 8u + rem; }
+constexpr int kSlowEntries = kCallTypes * kStates * 8;
+COH_HDC uint32_t slow_index(uint32_t type, uint32_t state, uint32_t rem) { return (type * 16u + state) * 8u + rem; }
 
 struct CallTable {
   uint32_t lut[kLutEntries];
@@ -78,9 +93,7 @@ struct TraceLaunch {
 };
 int launch_trace_eval(const TraceLaunch& p, void* stream, std::string* err);
 void trace_eval_set_smem_attr();
-// u16 store words keep the per-array 10-bit transfer counter exact up to 511 calls
-inline bool trace_eval_wide(uint32_t n_calls) { return n_calls > 511u; }
-int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t n_calls, std::string* err);
+int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, std::string* err);
 int launch_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
                        uint32_t n_arrays, uint32_t adv_per1024, uint16_t* d_records, void* stream,
                        std::string* err);
@@ -97,8 +110,7 @@ struct coh_ctx {
   uint32_t* d_slow = nullptr;
   uint64_t* d_bytes = nullptr;
   int sms = 148;
-  int blocks_per_sm = 1;       // narrow (u16) trace_eval
-  int blocks_per_sm_wide = 1;  // wide (u32) trace_eval
+  int blocks_per_sm = 1;       // trace_eval residency
   uint64_t launches = 0;
   // host-buffer pipeline
   cudaStream_t hs[2] = {nullptr, nullptr};

@@ -4,39 +4,51 @@
 // shared fuel + abstraction_correct (modes.hpp:79-90).
 //
 // Layout:
-//   * per-thread store: one word per array in shared memory (u16, or u32 for traces
-//     longer than 511 calls), bank-interleaved so a warp's lanes never conflict whatever
-//     arrays they touch; bits 2-5 = state nibble (cl, cr, al, ar), bits 6+ = per-array
-//     transfer count.
-//   * call table (calltable.cpp): 64 call types x 16 states of u32, XOR-swizzled
-//     (slot = type*16 + (state ^ (type & 15))) so the common (type, state) pairs of a
-//     warp land in distinct banks; lo16 = signed delta of the store word, hi16 = signed
-//     accumulator addend.
-//   * records: call-major interleaved, 128-bit streaming loads of 8 calls, a ring of
-//     4 loads (32 calls) in flight per thread.
-//   * accumulator (clean 32-bit): bits 0-7 steps since the last flush (every 32 calls),
-//     bits 8-14 number of arrays whose abstraction is currently violated (boundary_ok
-//     <=> acc < 0x100), bit 15 set by slow entries (stuck / defect).
-//   * slow calls (stuck, fuel, malformed) leave the unrolled loop; the call is
-//     re-derived from a sentinel in the boundary shift register and its exact outcome
-//     (StuckInfo, partial state and steps) read from a host-compiled table indexed by
-//     (type, state, remaining fuel).
+//   * per-thread store: one clean u16 slot per array in shared memory (internal.hpp
+//     slot_word: state nibble at bits 2-5 and 8-11), lane-interleaved so a warp's lanes
+//     never conflict whatever arrays they touch:
+//       byte offset = a*256 + (warp>>1)*128 + 4*lane + 2*(warp&1)   ->  bank = lane.
+//     Slots of arrays >= n_arrays hold the poison word (a missing key).
+//   * call table: 17 rows x 64 u32, addressed by (record & 0xFC) ^ slot (internal.hpp
+//     lut_word); lo16 = the slot word after the call, hi16 = signed accumulator addend.
+//   * records: the record's array byte (bits 8-13) is the slot offset, its type byte
+//     (bits 2-7) XOR the slot is the table offset: per call one masked logic op each,
+//     plus one IMAD.HI per pair to bring the odd call down.  128-bit streaming loads of
+//     8 calls, a ring of 4 loads (32 calls) in flight, continued across traces.
+//   * accumulator (32-bit register): bits 0-6 steps and 7-12 transfers since the last
+//     flush (every 16 calls), 13-19 number of arrays whose abstraction is violated
+//     (boundary_ok <=> acc < 0x2000); a slow entry (stuck / defect / poison) adds -32768,
+//     so "acc < 0" is the stop predicate.  Once it is set the accumulator, the store and
+//     the boundary shift register freeze (predicated updates), and the branch to the slow
+//     path is taken once per 8 calls.
+//   * slow calls: the call index is recovered from a sentinel in the boundary shift
+//     register and its exact outcome (StuckInfo, partial state and steps) read from a
+//     host-compiled table indexed by (type, state, remaining fuel) — no interpreter on the
+//     device.
 #include <cuda_runtime.h>
-
-#include <type_traits>
 
 #include "internal.hpp"
 
 namespace cohb {
 
 constexpr int kNT = 128;  // traces (threads) per block
+constexpr uint32_t kStoreBytes = COH_MAX_ARRAYS * kNT * 2u;
 
-// Per-trace store word: u16 (kNarrow, 128 B per trace, n_calls <= 511 so the 10-bit
-// per-array transfer counter cannot overflow) or u32 (wide, 256 B per trace).
-// Narrow slots are lane-interleaved so that a warp's 32 lanes always hit 32 distinct
-// banks whatever arrays they touch:
-//   u16 index = a*kNT + (warp>>1)*64 + 2*lane + (warp&1)  ->  bank = lane.
-// Shared block (per instantiation): [call table 4 KB][stores][64 x u64 array sizes].
+// The block's shared memory, one struct so the hot loop can address the table and the
+// store with [reg + immediate].  A CTA launched without a cluster is rank 0 of its own
+// cluster, so its shared::cta window addresses are plain offsets; the first static
+// variable sits after the 1 KB system-reserved area (checked at kernel entry).
+struct __align__(16) TraceSmem {
+  uint32_t lut[kLutEntries];
+  uint16_t store[kStoreBytes / 2];
+  unsigned long long cnt[COH_N_COUNTERS];
+  uint64_t bytes[COH_MAX_ARRAYS];
+};
+constexpr uint32_t kSmemBase = 0x400u;
+constexpr uint32_t kLutAddr = kSmemBase;
+constexpr uint32_t kStoreAddr = kSmemBase + kLutEntries * 4u;
+static_assert(kStoreAddr % 16u == 0u, "store alignment");
+
 struct KParams {
   const uint4* rec;
   uint64_t n_traces;
@@ -53,61 +65,143 @@ struct KParams {
   unsigned long long* counters;  // optional fused COH_N_COUNTERS reduction (zeroed by the launcher)
 };
 
-// bnd = 2*bnd + (acc >= 0x100): the accumulator is clean (steps | viol << 8), so the
-// carry of acc + 0xFFFFFF00 is exactly "some array's abstraction is violated".
+// bnd = 2*bnd + (acc >= 0x2000): with the accumulator clean (steps | transfers << 7 |
+// violated << 13), the carry of acc + 0xFFFFE000 is exactly "some array's abstraction is
+// violated" (abstraction_correct is false).
 __device__ __forceinline__ uint32_t shift_in_violation(uint32_t bnd, uint32_t acc) {
   uint32_t out;
-  asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, 0xFFFFFF00;\n\taddc.u32 %0, %2, %2;\n\t}"
+  asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, 0xFFFFE000;\n\taddc.u32 %0, %2, %2;\n\t}"
       : "=r"(out)
       : "r"(acc), "r"(bnd));
   return out;
 }
 
+// acc + (e >> 16, signed) on the FMA pipe: hi32(e * 2^16) + acc.
+__device__ __forceinline__ uint32_t acc_add(uint32_t acc, uint32_t e) {
+  uint32_t out;
+  asm("mad.hi.s32 %0, %1, 65536, %2;" : "=r"(out) : "r"(e), "r"(acc));
+  return out;
+}
+
+// Violation threshold after call c (0..15) of a 16-call flush window: every call adds a
+// bias of 1 << 13 (the table's violation delta is stored +1 so no addend is negative),
+// so "some array violated" <=> acc >= (c + 2) << 13.  Returned as the u32 addend whose
+// carry-out is that test.
+__host__ __device__ constexpr uint32_t viol_threshold_addend(int c) { return (uint32_t)(0x100000000ull - ((uint64_t)(c + 2) << 13)); }
+
+// Eight calls (one 128-bit record chunk) in one asm block, so the stop predicate stays
+// a predicate: per call one masked OR (slot address), LDS, one masked XOR (table
+// address), LDS, a sticky sign test of the entry (slow entries are negative), then the
+// predicated accumulate / store / boundary shift.  The run is live at chunk entry (the
+// caller branches out after every chunk).  HALF = which half of the 16-call flush
+// window the chunk is.  Returns the stop flag.
+#define COH_PTX_CALL(W, T)                             \
+  "{\n\t"                                              \
+  "and.b32 so, " W ", 0x3F00;\n\t"                    \
+  "or.b32 so, so, %4;\n\t"                            \
+  "ld.shared.u16 sv, [so+%5];\n\t"                    \
+  "and.b32 ix, " W ", 0xFC;\n\t"                      \
+  "xor.b32 ix, ix, sv;\n\t"                           \
+  "ld.shared.u32 ev, [ix+%6];\n\t"                    \
+  "setp.lt.or.s32 p, ev, 0, p;\n\t"                   \
+  COH_PTX_ACC                                          \
+  "st.shared.u16 [so+%5], ev;\n\t"                    \
+  "add.cc.u32 cy, %0, " T ";\n\t"                     \
+  "addc.u32 %1, %1, %1;\n\t"                          \
+  "SKIP:\n\t}\n\t"
+#define COH_PTX_PAIR(R, T0, T1)        \
+  COH_PTX_CALL(R, T0)                  \
+  "mul.hi.u32 th, " R ", 65536;\n\t"  \
+  COH_PTX_CALL("th", T1)
+#define COH_PTX_CHUNK                                                                       \
+  "{\n\t.reg .u32 so, sv, ix, ev, cy, th, an;\n\t.reg .pred p;\n\t"                     \
+  "setp.ne.u32 p, 0, 0;\n\t"                                                               \
+  COH_PTX_PAIR("%7", "%11", "%12") COH_PTX_PAIR("%8", "%13", "%14")                         \
+  COH_PTX_PAIR("%9", "%15", "%16") COH_PTX_PAIR("%10", "%17", "%18")                        \
+  "selp.u32 %2, 1, 0, p;\n\t}"
+#define COH_PTX_OPERANDS(H)                                                                         \
+  : "+r"(acc), "+r"(bnd), "=r"(stop)                                                                \
+  : "r"(fuel_left), "r"(toff), "n"(kStoreAddr), "n"(kLutAddr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), \
+    "n"(viol_threshold_addend(8 * H + 0)), "n"(viol_threshold_addend(8 * H + 1)),                    \
+    "n"(viol_threshold_addend(8 * H + 2)), "n"(viol_threshold_addend(8 * H + 3)),                    \
+    "n"(viol_threshold_addend(8 * H + 4)), "n"(viol_threshold_addend(8 * H + 5)),                    \
+    "n"(viol_threshold_addend(8 * H + 6)), "n"(viol_threshold_addend(8 * H + 7))                     \
+  : "memory"
+
+template <bool FUEL, int H>
+__device__ __forceinline__ uint32_t run_chunk(const uint4 v, uint32_t toff, uint32_t& acc, uint32_t& bnd,
+                                              int fuel_left) {
+  uint32_t stop;
+  if (FUEL) {  // the call's steps must fit the remaining fuel, else it is the slow call
+#define COH_PTX_ACC                                 \
+  "mul.hi.s32 cy, ev, 65536;\n\t"                   \
+  "add.s32 an, %0, cy;\n\t"                         \
+  "and.b32 cy, an, 0x7F;\n\t"                       \
+  "setp.gt.or.s32 p, cy, %3, p;\n\t"                \
+  "@p bra SKIP;\n\t"                                \
+  "mov.u32 %0, an;\n\t"
+    asm volatile(COH_PTX_CHUNK COH_PTX_OPERANDS(H));
+#undef COH_PTX_ACC
+  } else {
+#define COH_PTX_ACC "@p bra SKIP;\n\tmul.hi.s32 cy, ev, 65536;\n\tadd.s32 %0, %0, cy;\n\t"
+    asm volatile(COH_PTX_CHUNK COH_PTX_OPERANDS(H));
+#undef COH_PTX_ACC
+  }
+  return stop;
+}
+
 // FLAGS: kFuel = fuel may run out (fuel < 6 x n_calls), kBytes = non-uniform array
-// sizes, kArr = n_arrays < 64 (range-check array ids), kWide = u32 store words.
-enum : int { kFuel = 1, kBytes = 2, kArr = 4, kWide = 8 };
+// sizes (per-call byte accumulation), kRing = n_calls % 32 == 0 (the record ring runs on
+// into the next trace).
+enum : int { kFuel = 1, kBytes = 2, kRing = 4 };
 
 template <int FLAGS>
-__global__ void __launch_bounds__(kNT, (FLAGS & kWide) ? 6 : 10) k_trace_eval(const KParams p) {
+__global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
   constexpr bool CHECK_FUEL = FLAGS & kFuel;
   constexpr bool UNIFORM = !(FLAGS & kBytes);
-  constexpr bool CHECK_ARR = FLAGS & kArr;
-  constexpr bool WIDE = FLAGS & kWide;
-  using Word = typename std::conditional<WIDE, uint32_t, uint16_t>::type;
-  constexpr uint32_t kStride = sizeof(Word) * kNT;  // bytes between arrays of one column
-  constexpr int kStWords = COH_MAX_ARRAYS * kNT * (int)sizeof(Word) / 4;
-  __shared__ __align__(16) uint32_t s_mem[kLutEntries + kStWords + 2 * COH_MAX_ARRAYS];
-  __shared__ unsigned long long s_cnt[COH_N_COUNTERS];
-  uint32_t* const s_lut = s_mem;
-  char* const s_stb = reinterpret_cast<char*>(s_mem + kLutEntries);
-  uint64_t* const s_bytes = reinterpret_cast<uint64_t*>(s_mem + kLutEntries + kStWords);
+  constexpr bool RING = FLAGS & kRing;
+  __shared__ TraceSmem sm;
+  uint32_t* const s_lut = sm.lut;
+  uint16_t* const s_store = sm.store;
+  uint64_t* const s_bytes = sm.bytes;
+  unsigned long long* const s_cnt = sm.cnt;
+  char* const stb = reinterpret_cast<char*>(s_store);
+  const char* const lutb = reinterpret_cast<const char*>(s_lut);
+  if ((uint32_t)__cvta_generic_to_shared(&sm) != kSmemBase) __trap();  // layout assumption
 
   const int tid = threadIdx.x;
+  const uint32_t n_arrays = p.n_arrays;
   for (int i = tid; i < kLutEntries; i += kNT) s_lut[i] = p.lut[i];
   if (!UNIFORM)
-    for (int i = tid; i < COH_MAX_ARRAYS; i += kNT)
-      s_bytes[i] = i < (int)p.n_arrays ? p.array_bytes[i] : 0ull;
-  constexpr uint32_t kInit = COH_STATE_INITIAL << kStateShift;
-  constexpr uint32_t kInitWord = WIDE ? kInit : (kInit | (kInit << 16));
-  for (int i = tid; i < kStWords; i += kNT) s_mem[kLutEntries + i] = kInitWord;
+    for (int i = tid; i < COH_MAX_ARRAYS; i += kNT) s_bytes[i] = i < (int)n_arrays ? p.array_bytes[i] : 0ull;
+  constexpr uint32_t kInit = slot_word(COH_STATE_INITIAL);
+  // slots are array-major (64 x 256 B): u32 word i covers array i / 64
+  for (int i = tid; i < (int)(kStoreBytes / 4); i += kNT) {
+    const uint32_t w = (uint32_t)(i >> 6) < n_arrays ? kInit : kPoisonSlot;
+    reinterpret_cast<uint32_t*>(s_store)[i] = w | (w << 16);
+  }
   if (tid < COH_N_COUNTERS) s_cnt[tid] = 0ull;
   __syncthreads();  // the only block barrier: afterwards each thread owns its column
 
   const uint32_t warp = tid >> 5, lane = tid & 31;
-  const uint32_t thread_off = WIDE ? 4u * tid : (warp >> 1) * 128u + 4u * lane + 2u * (warp & 1u);
-  char* const stc = s_stb + thread_off;  // this thread's column: stc + a * kStride
+  const uint32_t toff = (warp >> 1) * 128u + 4u * lane + 2u * (warp & 1u);  // < 256
   const uint64_t n = p.n_traces;
-  const uint32_t n_calls = p.n_calls, n_arrays = p.n_arrays;
+  const uint32_t n_calls = p.n_calls;
   const uint32_t n_chunks = (n_calls + 7u) / 8u;
   const uint32_t n_groups = n_calls / 32u;
   const uint32_t n_words = (n_calls + 31u) / 32u;
   const uint64_t stride = (uint64_t)gridDim.x * kNT;
 
+  uint4 ring[4];
+  bool ring_ok = false;  // ring already holds chunks 0..3 of this thread's next trace
+
   for (uint64_t base = (uint64_t)blockIdx.x * kNT; base < n; base += stride) {
     const uint64_t t = base + tid;
     if (t >= n) continue;
     const uint4* rp = p.rec + t;
-    uint32_t acc = 0, steps = 0, viol_blocks = 0;
+    const uint64_t t_next = t + stride;
+    uint32_t acc = 0, steps = 0, xfers = 0, viol_blocks = 0;
+    uint64_t tbytes = 0;
     // bnd: shift register of boundary-VIOLATION bits of the current 32-call group,
     // seeded with a sentinel 1: after k calls the sentinel sits at bit k (call 0's bit
     // at k-1); the stored boundary_ok word is its reversed complement.
@@ -115,116 +209,130 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kWide) ? 6 : 10) k_trace_eval(co
     uint32_t status = COH_RUN_DONE, stuck_call = 0, stuck_arr = 0, stuck_eff = 0, stuck_flags = 0;
     uint32_t calls_done = n_calls;
     int fuel_left = p.fuel;
+    bool stop = false;
 
-    // One call; R = 16-bit record (bits above 15 may hold garbage).  Nothing per call
-    // site survives into the slow path (it re-derives the call from the sentinel), so
-    // the fast path carries no bookkeeping moves.
-#define COH_CALL(R)                                                                         \
-  {                                                                                         \
-    const uint32_t r_ = (R);                                                                \
-    Word* sp_ = reinterpret_cast<Word*>(stc + (r_ & 63u) * kStride);   /* store[a][tid] */ \
-    const uint32_t old_ = *sp_;                                                             \
-    const uint32_t e_ = *reinterpret_cast<const uint32_t*>(                                 \
-        reinterpret_cast<const char*>(s_lut) + ((r_ & 0xFC0u) | (((r_ >> 4) ^ old_) & 0x3Cu))); \
-    acc += (uint32_t)((int32_t)e_ >> 16);                                                   \
-    bool stop_ = false;                                                                     \
-    if (CHECK_FUEL) stop_ |= (int)(acc & 0xFFu) > fuel_left;                                \
-    if (CHECK_ARR) stop_ |= (r_ & 63u) >= n_arrays;                                         \
-    if (!stop_) *sp_ = (Word)(old_ + (WIDE ? (uint32_t)(int32_t)(int16_t)e_ : e_));         \
-    if (__builtin_expect(stop_ || (acc & 0x8000u) != 0u, 0)) goto slow_path;               \
-    bnd = shift_in_violation(bnd, acc);                                                     \
+    // One call.  T = the record in bits 0-15 (bits 16+ may hold the next record).  The
+    // updates after the table lookup are predicated on !stop, so after a slow entry the
+    // store, the accumulator and the sentinel keep the state just before that call.
+#define COH_CALL(T, C)                                                                    \
+  {                                                                                       \
+    const uint32_t t_ = (T);                                                              \
+    const uint32_t so_ = (t_ & 0x3F00u) | toff;                                           \
+    const uint32_t s_ = *reinterpret_cast<const uint16_t*>(stb + so_);                    \
+    const uint32_t e_ = *reinterpret_cast<const uint32_t*>(lutb + ((t_ & 0xFCu) ^ s_));   \
+    const uint32_t an_ = acc + (uint32_t)((int32_t)e_ >> 16);                             \
+    stop |= (int32_t)e_ < 0;                                                              \
+    if (CHECK_FUEL) stop |= (int)(an_ & kAccSteps) > fuel_left;                           \
+    if (!stop) {                                                                          \
+      acc = an_;                                                                          \
+      *reinterpret_cast<uint16_t*>(stb + so_) = (uint16_t)e_;                             \
+      bnd = 2u * bnd + (acc + viol_threshold_addend(C) < acc ? 1u : 0u);                  \
+      if (!UNIFORM) tbytes += (uint64_t)((e_ >> 23) & 3u) * s_bytes[(t_ >> 8) & 63u];      \
+    }                                                                                     \
   }
-#define COH_CHUNK(W)            \
-  COH_CALL((W).x)               \
-  COH_CALL((W).x >> 16)         \
-  COH_CALL((W).y)               \
-  COH_CALL((W).y >> 16)         \
-  COH_CALL((W).z)               \
-  COH_CALL((W).z >> 16)         \
-  COH_CALL((W).w)               \
-  COH_CALL((W).w >> 16)
+#define COH_PAIR(W, C) \
+  COH_CALL(W, C)       \
+  COH_CALL(__umulhi((W), 0x10000u), (C) + 1)
+#define COH_CHUNK(V, H)                                                                   \
+  if (UNIFORM) {                                                                          \
+    stop = run_chunk<CHECK_FUEL, H>((V), toff, acc, bnd, fuel_left);                      \
+  } else {                                                                                \
+    COH_PAIR((V).x, 8 * H) COH_PAIR((V).y, 8 * H + 2) COH_PAIR((V).z, 8 * H + 4)           \
+    COH_PAIR((V).w, 8 * H + 6)                                                            \
+  }                                                                                       \
+  if (__builtin_expect(stop, 0)) goto slow_path;
+#define COH_FLUSH                                 \
+  steps += acc & kAccSteps;                       \
+  xfers += (acc >> kAccXferShift) & 0x3Fu;        \
+  acc = (acc & kAccKeep) - (16u << kAccViolShift); \
+  if (CHECK_FUEL) fuel_left = p.fuel - (int)steps;
 
     {
-      uint4 ring[4];  // fully (re)initialised per trace so nothing stays live across traces
+      if (!ring_ok) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        ring[j] = (uint32_t)j < n_chunks ? __ldcs(rp + (uint64_t)j * n) : make_uint4(0u, 0u, 0u, 0u);
+        for (int j = 0; j < 4; ++j)
+          ring[j] = (uint32_t)j < n_chunks ? __ldcs(rp + (uint64_t)j * n) : make_uint4(0u, 0u, 0u, 0u);
+      }
+      ring_ok = false;
       for (uint32_t g = 0; g < n_groups; ++g) {
         i0 = g * 32u;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint4 cur = ring[j];
-          const uint32_t cn = 4u * (g + 1u) + (uint32_t)j;
-          if (cn < n_chunks) ring[j] = __ldcs(rp + (uint64_t)cn * n);
-          COH_CHUNK(cur)
-        }
+#define COH_STEP(J)                                                                       \
+  {                                                                                       \
+    const uint4 cur = ring[J];                                                            \
+    const uint32_t cn = 4u * (g + 1u) + (uint32_t)(J);                                    \
+    if (cn < n_chunks) {                                                                  \
+      ring[J] = __ldcs(rp + (uint64_t)cn * n);                                            \
+    } else if (RING && t_next < n) { /* last group: chunk J of the next trace */          \
+      ring[J] = __ldcs(rp + stride + (uint64_t)(J) * n);                                  \
+    }                                                                                     \
+    COH_CHUNK(cur, ((J) & 1))                                                             \
+    if ((J) & 1) { COH_FLUSH }                                                            \
+  }
+        COH_STEP(0) COH_STEP(1) COH_STEP(2) COH_STEP(3)
+#undef COH_STEP
         // 32 calls done: the sentinel was shifted out, call 0's violation bit is bit 31
         bnd = ~__brev(bnd);
         if (p.bnd) p.bnd[(uint64_t)g * n + t] = bnd;
         viol_blocks += 32u - __popc(bnd);
         bnd = 1u;
-        steps += acc & 0xFFu;
-        acc &= 0xFF00u;
-        if (CHECK_FUEL) fuel_left = p.fuel - (int)steps;
       }
-      const uint32_t tail = n_calls - n_groups * 32u;
-      if (tail) {
-        i0 = n_groups * 32u;
+      if (RING) ring_ok = true;
+      if (!RING) {
+        const uint32_t tail = n_calls - n_groups * 32u;
+        if (tail) {
+          i0 = n_groups * 32u;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t w4[4] = {ring[j].x, ring[j].y, ring[j].z, ring[j].w};
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t w4[4] = {ring[j].x, ring[j].y, ring[j].z, ring[j].w};
 #pragma unroll
-          for (int h = 0; h < 8; ++h) {
-            if (8u * j + h < tail) COH_CALL(w4[h >> 1] >> (16 * (h & 1)))
+            for (int h = 0; h < 8; ++h) {
+              if (8u * j + h < tail) COH_CALL(h & 1 ? (w4[h >> 1] >> 16) : w4[h >> 1], 8 * (j & 1) + h)
+            }
+            if (stop) goto slow_path;
+            if (j & 1) { COH_FLUSH }
           }
+          const uint32_t word = (~__brev(bnd ^ (1u << tail))) >> (32u - tail);
+          viol_blocks += tail - __popc(word);
+          if (p.bnd) p.bnd[(uint64_t)n_groups * n + t] = word;
         }
-        const uint32_t word = (~__brev(bnd ^ (1u << tail))) >> (32u - tail);
-        viol_blocks += tail - __popc(word);
-        steps += acc & 0xFFu;
-        acc &= 0xFF00u;
-        if (p.bnd) p.bnd[(uint64_t)n_groups * n + t] = word;
       }
       goto finished;
     }
+#undef COH_FLUSH
 #undef COH_CHUNK
+#undef COH_PAIR
 #undef COH_CALL
 
   slow_path : {
-    // which call: k calls of this group completed (sentinel position)
+    ring_ok = false;
+    // which call: k calls of this 32-group completed (sentinel position)
     const uint32_t k = 31u - __clz(bnd);
     const uint32_t i = i0 + k;
     const uint4 chunk = __ldcs(rp + (uint64_t)(i / 8u) * n);
     const uint32_t w4[4] = {chunk.x, chunk.y, chunk.z, chunk.w};
     const uint32_t r = (w4[(i & 7u) >> 1] >> (16u * (i & 1u))) & 0xFFFFu;
-    const uint32_t a = r & 63u;
-    Word* const sp = reinterpret_cast<Word*>(stc + a * kStride);
-    const uint32_t old = *sp;  // untouched: the fast path did not store
-    const uint32_t e = *reinterpret_cast<const uint32_t*>(
-        reinterpret_cast<const char*>(s_lut) + ((r & 0xFC0u) | (((r >> 4) ^ old) & 0x3Cu)));
-    acc -= (uint32_t)((int32_t)e >> 16);  // undo the accumulate
+    const uint32_t a = (r >> 8) & 63u, type = (r >> 2) & 63u;
+    uint16_t* const sp = reinterpret_cast<uint16_t*>(stb + ((r & 0x3F00u) | toff));
+    const uint32_t s = *sp;  // untouched: the store froze before this call
+    // the accumulator froze before this call too (its bias does not reach bits 0-12)
+    steps += acc & kAccSteps;
+    xfers += (acc >> kAccXferShift) & 0x3Fu;
     // exact outcome from the host-compiled slow table (type, state, remaining fuel)
-    const int rem_i = p.fuel - (int)steps - (int)(acc & 0xFFu);
+    const int rem_i = p.fuel - (int)steps;
     const uint32_t rem = rem_i <= 0 ? 0u : (rem_i >= 7 ? 7u : (uint32_t)rem_i);
-    const uint32_t s0 = (old >> kStateShift) & 15u;
-    const uint32_t info = (CHECK_ARR && a >= n_arrays)
-                              ? (uint32_t)COH_RUN_DEFECT | (s0 << 7)
-                              : __ldg(p.slow + slow_index((r >> 6) & 63u, s0, rem));
-    struct {
-      uint32_t status, word, steps, effect, flags;
-    } so;
-    so.status = info & 3u;
-    so.steps = (info >> 2) & 7u;
-    so.word = (old & ~(15u << kStateShift)) + (((info >> 5) & 3u) << kCountShift) +
-              (((info >> 7) & 15u) << kStateShift);
-    so.effect = (info >> 11) & 7u;
-    so.flags = (info >> 14) & 15u;
-    *sp = (Word)so.word;
-    steps += (acc & 0xFFu) + so.steps;
-    status = so.status;
+    const uint32_t s0 = (s >> 8) & 15u;
+    const bool missing = s == kPoisonSlot;  // array id >= n_arrays
+    const uint32_t info = missing ? (uint32_t)COH_RUN_DEFECT : __ldg(p.slow + slow_index(type, s0, rem));
+    const uint32_t so_steps = (info >> 2) & 7u, so_xf = (info >> 5) & 3u;
+    if (!missing) *sp = (uint16_t)slot_word((info >> 7) & 15u);
+    steps += so_steps;
+    xfers += so_xf;
+    if (!UNIFORM && !missing) tbytes += (uint64_t)so_xf * s_bytes[a];
+    status = info & 3u;
     stuck_call = i;
     stuck_arr = a;
-    stuck_eff = so.effect;
-    stuck_flags = so.flags;
+    stuck_eff = (info >> 11) & 7u;
+    stuck_flags = (info >> 14) & 15u;
     calls_done = i;
     const uint32_t word = k ? ((~__brev(bnd ^ (1u << k))) >> (32u - k)) : 0u;
     viol_blocks += k - __popc(word);
@@ -236,32 +344,28 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kWide) ? 6 : 10) k_trace_eval(co
   }
   finished : {
     uint32_t sw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    uint32_t transfers = 0;
-    uint64_t tbytes = 0;
 #pragma unroll
     for (int a = 0; a < COH_MAX_ARRAYS; ++a) {
       if (a < (int)n_arrays) {
-        Word* const wp = reinterpret_cast<Word*>(stc + a * kStride);
+        uint16_t* const wp = reinterpret_cast<uint16_t*>(stb + a * 256 + toff);
         const uint32_t w = *wp;
-        *wp = (Word)kInit;  // reset for this thread's next trace
-        const int sh = 4 * (a & 7) - (int)kStateShift;
+        *wp = (uint16_t)kInit;  // reset for this thread's next trace
+        const int sh = 4 * (a & 7) - 2;
         sw[a >> 3] |= (sh >= 0 ? (w << sh) : (w >> -sh)) & (15u << (4 * (a & 7)));
-        transfers += w >> kCountShift;
-        if (!UNIFORM) tbytes += (uint64_t)(w >> kCountShift) * s_bytes[a];
       }
     }
-    if (UNIFORM) tbytes = (uint64_t)transfers * p.bytes_uniform;
+    const uint64_t tb = UNIFORM ? (uint64_t)xfers * p.bytes_uniform : tbytes;
     uint4* out = reinterpret_cast<uint4*>(p.res + t);
     __stcs(out + 0, make_uint4(sw[0], sw[1], sw[2], sw[3]));
     __stcs(out + 1, make_uint4(sw[4], sw[5], sw[6], sw[7]));
-    __stcs(out + 2, make_uint4((uint32_t)tbytes, (uint32_t)(tbytes >> 32), steps, transfers));
+    __stcs(out + 2, make_uint4((uint32_t)tb, (uint32_t)(tb >> 32), steps, xfers));
     __stcs(out + 3, make_uint4(calls_done, viol_blocks, stuck_call,
                                status | (stuck_arr << 8) | (stuck_eff << 16) | (stuck_flags << 24)));
     if (p.counters) {  // fused counter reduction: warp redux, one shared atomic per warp
       const uint32_t m = __activemask();
       const bool leader = (lane == (uint32_t)(__ffs(m) - 1));
       uint32_t v[9] = {status == COH_RUN_STUCK, status == COH_RUN_FUEL_EXHAUSTED, viol_blocks != 0u,
-                       status == COH_RUN_DEFECT, steps, transfers, viol_blocks, calls_done, 1u};
+                       status == COH_RUN_DEFECT, steps, xfers, viol_blocks, calls_done, 1u};
       const int slot[9] = {0, 1, 2, 3, 4, 5, 7, 8, 9};
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
@@ -270,8 +374,8 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kWide) ? 6 : 10) k_trace_eval(co
       }
       if (UNIFORM) {  // bytes = transfers x size: one multiply by the leader
         if (leader && v[5]) atomicAdd(&s_cnt[6], (unsigned long long)v[5] * p.bytes_uniform);
-      } else if (tbytes) {  // non-uniform sizes: per-lane shared atomic
-        atomicAdd(&s_cnt[6], (unsigned long long)tbytes);
+      } else if (tb) {  // non-uniform sizes: per-lane shared atomic
+        atomicAdd(&s_cnt[6], (unsigned long long)tb);
       }
     }
   }
@@ -293,11 +397,9 @@ static int launch_one(const TraceLaunch& L, const KParams& kp, cudaStream_t s, s
   return COH_OK;
 }
 
-int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t n_calls, std::string* err) {
+int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, std::string* err) {
   int b = 0;
-  cudaError_t e = trace_eval_wide(n_calls)
-                      ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trace_eval<kWide>, kNT, 0)
-                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trace_eval<0>, kNT, 0);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trace_eval<kRing>, kNT, 0);
   if (e != cudaSuccess) {
     *err = std::string("occupancy: ") + cudaGetErrorString(e);
     return COH_E_CUDA;
@@ -332,13 +434,11 @@ int launch_trace_eval(const TraceLaunch& L, void* stream, std::string* err) {
     }
   }
   const int f = (L.check_fuel ? kFuel : 0) | (L.uniform_bytes ? 0 : kBytes) |
-                (L.n_arrays < COH_MAX_ARRAYS ? kArr : 0) | (trace_eval_wide(L.n_calls) ? kWide : 0);
+                (L.n_calls % 32u == 0u && L.n_calls >= 32u ? kRing : 0);
   switch (f) {
 #define COH_CASE(F) \
   case F: return launch_one<F>(L, kp, s, err);
     COH_CASE(0) COH_CASE(1) COH_CASE(2) COH_CASE(3) COH_CASE(4) COH_CASE(5) COH_CASE(6) COH_CASE(7)
-    COH_CASE(8) COH_CASE(9) COH_CASE(10) COH_CASE(11) COH_CASE(12) COH_CASE(13) COH_CASE(14)
-    COH_CASE(15)
 #undef COH_CASE
   }
   return COH_E_ARG;

@@ -84,9 +84,10 @@ def test_calltable_program_renders_reference_translation():
 
 def test_host_generator_distribution():
     recs = coh.gen_records_host(1, 0, 4096, 256, 64, 1)
-    arr = recs & 63
-    kind = (recs >> 6) & 3
-    var = (recs >> 9) & 7
+    arr = (recs >> 8) & 63
+    kind = (recs >> 2) & 3
+    var = (recs >> 5) & 7
+    assert not (recs & 0xC003).any()  # reserved bits
     assert np.bincount(arr, minlength=64).min() > 0.8 * recs.size / 64
     assert set(np.unique(kind)) == {0, 1, 2}
     frac_adv = (var != 0).mean()

@@ -136,8 +136,8 @@ def test_fused_counters_equal_sum_of_results(ctx, cfg):
 
 def test_defect_records(ctx):
     recs = np.zeros(coh.records_elems(2, 8), dtype=np.uint16)
-    recs[0:8] = [0, 0, 3 << 6, 0, 0, 0, 0, 0]
-    recs[8:16] = [0, 1, 2, 5, 0, 0, 0, 0]
+    recs[0:8] = [0, 0, coh.make_record(0, 3, 0, 0), 0, 0, 0, 0, 0]
+    recs[8:16] = [coh.make_record(a, 0, 0, 0) for a in (0, 1, 2, 5, 0, 0, 0, 0)]
     res, bnd = dev_eval(ctx, recs, 2, 8, 4, 10000)
     want, want_b = o.orc_eval(recs, 2, 8, 4)
     assert same(res, want) and np.array_equal(bnd, want_b)
