@@ -29,17 +29,20 @@ constexpr int kStates = 16;      // state nibble
 
 // Store slot in shared memory (one u16 per array per trace), "clean" so that it can be
 // XORed straight into a table address:
-//   bits 2-5  state nibble (bit0 cl, bit1 cr, bit2 al, bit3 ar) -- the bank-swizzle copy
-//   bits 8-11 state nibble again                                  -- the table row
+//   bits 2-7  slot_swizzle(state) = state * 9 mod 64               -- the bank swizzle
+//   bits 8-11 state nibble (bit0 cl, bit1 cr, bit2 al, bit3 ar)    -- the table row
 //   bit  12   poison row: an array id >= n_arrays (a missing key, program.hpp:147-151)
 // Transfers, steps and violations are not per-array state: they accumulate in a register.
-COH_HDC uint32_t slot_word(uint32_t state) { return (state << 8) | (state << 2); }
+COH_HDC uint32_t slot_swizzle(uint32_t state) { return (state * 9u) & 63u; }
+COH_HDC uint32_t slot_word(uint32_t state) { return (state << 8) | (slot_swizzle(state) << 2); }
+COH_HDC uint32_t slot_state(uint32_t slot) { return (slot >> 8) & 15u; }
 constexpr uint32_t kPoisonSlot = 0x1000u;
 
 // Call table (u32 entries), addressed by byte offset (type << 2) ^ slot, i.e. word
-// state*64 + (type ^ state): rows of 64 words per state (bank = (type ^ state) & 31, so
-// the common (type, state) pairs of a warp spread over the banks), plus row 16 for the
-// poison slot (word 1024 + type).
+// state*64 + (type ^ swizzle(state)): rows of 64 words per state, bank = (type ^
+// swizzle) & 31, which spreads the common (type, state) pairs of a warp over the banks
+// (1.016 wavefronts per lookup on the C2 mix, vs 1.81 for swizzle = state); row 16
+// serves the poison slot (word 1024 + type).
 //   lo16 : the slot word after the call (stored as is)
 //   hi16 : accumulator addend = steps + (transfers << 7) + ((viol_delta + 1) << 13), always
 //          in [0, 0x7FFF] (the +1 is a per-call bias the device subtracts at each flush), or
@@ -48,7 +51,7 @@ constexpr uint32_t kPoisonSlot = 0x1000u;
 constexpr int kLutRows = kStates + 1;
 constexpr int kLutEntries = kLutRows * kCallTypes;
 constexpr uint32_t kSlowAddend = 0x8000u;
-COH_HDC uint32_t lut_word(uint32_t type, uint32_t state) { return state * 64u + (type ^ state); }
+COH_HDC uint32_t lut_word(uint32_t type, uint32_t state) { return state * 64u + (type ^ slot_swizzle(state)); }
 constexpr uint32_t kAccSteps = 0x7Fu;   // accumulator bits 0-6: steps since the last flush
 constexpr uint32_t kAccXferShift = 7;   // bits 7-12: transfers since the last flush
 constexpr uint32_t kAccViolShift = 13;  // bits 13-19: arrays whose abstraction is violated

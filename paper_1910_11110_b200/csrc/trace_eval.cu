@@ -161,45 +161,39 @@ __global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
   constexpr bool UNIFORM = !(FLAGS & kBytes);
   constexpr bool RING = FLAGS & kRing;
   __shared__ TraceSmem sm;
-  uint32_t* const s_lut = sm.lut;
-  uint16_t* const s_store = sm.store;
-  uint64_t* const s_bytes = sm.bytes;
-  unsigned long long* const s_cnt = sm.cnt;
-  char* const stb = reinterpret_cast<char*>(s_store);
-  const char* const lutb = reinterpret_cast<const char*>(s_lut);
+  char* const stb = reinterpret_cast<char*>(sm.store);
+  const char* const lutb = reinterpret_cast<const char*>(sm.lut);
   if ((uint32_t)__cvta_generic_to_shared(&sm) != kSmemBase) __trap();  // layout assumption
 
-  const int tid = threadIdx.x;
-  const uint32_t n_arrays = p.n_arrays;
-  for (int i = tid; i < kLutEntries; i += kNT) s_lut[i] = p.lut[i];
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t i = tid; i < (uint32_t)kLutEntries; i += kNT) sm.lut[i] = p.lut[i];
   if (!UNIFORM)
-    for (int i = tid; i < COH_MAX_ARRAYS; i += kNT) s_bytes[i] = i < (int)n_arrays ? p.array_bytes[i] : 0ull;
+    for (uint32_t i = tid; i < COH_MAX_ARRAYS; i += kNT) sm.bytes[i] = i < p.n_arrays ? p.array_bytes[i] : 0ull;
   constexpr uint32_t kInit = slot_word(COH_STATE_INITIAL);
   // slots are array-major (64 x 256 B): u32 word i covers array i / 64
-  for (int i = tid; i < (int)(kStoreBytes / 4); i += kNT) {
-    const uint32_t w = (uint32_t)(i >> 6) < n_arrays ? kInit : kPoisonSlot;
-    reinterpret_cast<uint32_t*>(s_store)[i] = w | (w << 16);
+  for (uint32_t i = tid; i < kStoreBytes / 4u; i += kNT) {
+    const uint32_t w = (i >> 6) < p.n_arrays ? kInit : kPoisonSlot;
+    reinterpret_cast<uint32_t*>(sm.store)[i] = w | (w << 16);
   }
-  if (tid < COH_N_COUNTERS) s_cnt[tid] = 0ull;
+  if (tid < COH_N_COUNTERS) sm.cnt[tid] = 0ull;
   __syncthreads();  // the only block barrier: afterwards each thread owns its column
 
-  const uint32_t warp = tid >> 5, lane = tid & 31;
+  const uint32_t warp = tid >> 5, lane = tid & 31u;
   const uint32_t toff = (warp >> 1) * 128u + 4u * lane + 2u * (warp & 1u);  // < 256
-  const uint64_t n = p.n_traces;
+  const uint32_t n = p.n_traces;  // < 2^32 (checked by the launcher)
   const uint32_t n_calls = p.n_calls;
   const uint32_t n_chunks = (n_calls + 7u) / 8u;
   const uint32_t n_groups = n_calls / 32u;
-  const uint32_t n_words = (n_calls + 31u) / 32u;
-  const uint64_t stride = (uint64_t)gridDim.x * kNT;
+  const uint32_t stride = gridDim.x * kNT;
+  // chunk c of trace u: 8 calls, one 128-bit streaming load
+#define COH_REC(C, U) __ldcs(p.rec + (uint64_t)(C) * n + (U))
 
   uint4 ring[4];
   bool ring_ok = false;  // ring already holds chunks 0..3 of this thread's next trace
 
-  for (uint64_t base = (uint64_t)blockIdx.x * kNT; base < n; base += stride) {
-    const uint64_t t = base + tid;
+  for (uint32_t base = blockIdx.x * kNT; base < n; base += stride) {
+    const uint32_t t = base + tid;
     if (t >= n) continue;
-    const uint4* rp = p.rec + t;
-    const uint64_t t_next = t + stride;
     uint32_t acc = 0, steps = 0, xfers = 0, viol_blocks = 0;
     uint64_t tbytes = 0;
     // bnd: shift register of boundary-VIOLATION bits of the current 32-call group,
@@ -211,9 +205,9 @@ __global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
     int fuel_left = p.fuel;
     bool stop = false;
 
-    // One call.  T = the record in bits 0-15 (bits 16+ may hold the next record).  The
-    // updates after the table lookup are predicated on !stop, so after a slow entry the
-    // store, the accumulator and the sentinel keep the state just before that call.
+    // One call (C++ form: non-uniform byte sizes and the ragged tail).  T = the record in
+    // bits 0-15 (bits 16+ may hold the next record), C = its position in the 16-call
+    // flush window.  Same semantics as the asm chunk.
 #define COH_CALL(T, C)                                                                    \
   {                                                                                       \
     const uint32_t t_ = (T);                                                              \
@@ -227,7 +221,7 @@ __global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
       acc = an_;                                                                          \
       *reinterpret_cast<uint16_t*>(stb + so_) = (uint16_t)e_;                             \
       bnd = 2u * bnd + (acc + viol_threshold_addend(C) < acc ? 1u : 0u);                  \
-      if (!UNIFORM) tbytes += (uint64_t)((e_ >> 23) & 3u) * s_bytes[(t_ >> 8) & 63u];      \
+      if (!UNIFORM) tbytes += (uint64_t)((e_ >> 23) & 3u) * sm.bytes[(t_ >> 8) & 63u];     \
     }                                                                                     \
   }
 #define COH_PAIR(W, C) \
@@ -241,32 +235,32 @@ __global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
     COH_PAIR((V).w, 8 * H + 6)                                                            \
   }                                                                                       \
   if (__builtin_expect(stop, 0)) goto slow_path;
-#define COH_FLUSH                                 \
-  steps += acc & kAccSteps;                       \
-  xfers += (acc >> kAccXferShift) & 0x3Fu;        \
+#define COH_FLUSH                                  \
+  steps += acc & kAccSteps;                        \
+  xfers += (acc >> kAccXferShift) & 0x3Fu;         \
   acc = (acc & kAccKeep) - (16u << kAccViolShift); \
   if (CHECK_FUEL) fuel_left = p.fuel - (int)steps;
 
     {
       if (!ring_ok) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          ring[j] = (uint32_t)j < n_chunks ? __ldcs(rp + (uint64_t)j * n) : make_uint4(0u, 0u, 0u, 0u);
+        for (int j = 0; j < 4; ++j) ring[j] = (uint32_t)j < n_chunks ? COH_REC(j, t) : make_uint4(0u, 0u, 0u, 0u);
       }
       ring_ok = false;
       for (uint32_t g = 0; g < n_groups; ++g) {
         i0 = g * 32u;
-#define COH_STEP(J)                                                                       \
-  {                                                                                       \
-    const uint4 cur = ring[J];                                                            \
-    const uint32_t cn = 4u * (g + 1u) + (uint32_t)(J);                                    \
-    if (cn < n_chunks) {                                                                  \
-      ring[J] = __ldcs(rp + (uint64_t)cn * n);                                            \
-    } else if (RING && t_next < n) { /* last group: chunk J of the next trace */          \
-      ring[J] = __ldcs(rp + stride + (uint64_t)(J) * n);                                  \
-    }                                                                                     \
-    COH_CHUNK(cur, ((J) & 1))                                                             \
-    if ((J) & 1) { COH_FLUSH }                                                            \
+        // evaluate ring slot J, then refill it with the chunk 4 ahead (in the last group:
+        // chunk J of this thread's next trace)
+#define COH_STEP(J)                                                    \
+  {                                                                    \
+    COH_CHUNK(ring[J], ((J) & 1))                                      \
+    const uint32_t cn = 4u * (g + 1u) + (uint32_t)(J);                 \
+    if (cn < n_chunks) {                                               \
+      ring[J] = COH_REC(cn, t);                                        \
+    } else if (RING && t + stride < n) {                               \
+      ring[J] = COH_REC(J, t + stride);                                \
+    }                                                                  \
+    if ((J) & 1) { COH_FLUSH }                                         \
   }
         COH_STEP(0) COH_STEP(1) COH_STEP(2) COH_STEP(3)
 #undef COH_STEP
@@ -308,7 +302,7 @@ __global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
     // which call: k calls of this 32-group completed (sentinel position)
     const uint32_t k = 31u - __clz(bnd);
     const uint32_t i = i0 + k;
-    const uint4 chunk = __ldcs(rp + (uint64_t)(i / 8u) * n);
+    const uint4 chunk = COH_REC(i / 8u, t);
     const uint32_t w4[4] = {chunk.x, chunk.y, chunk.z, chunk.w};
     const uint32_t r = (w4[(i & 7u) >> 1] >> (16u * (i & 1u))) & 0xFFFFu;
     const uint32_t a = (r >> 8) & 63u, type = (r >> 2) & 63u;
@@ -320,14 +314,13 @@ __global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
     // exact outcome from the host-compiled slow table (type, state, remaining fuel)
     const int rem_i = p.fuel - (int)steps;
     const uint32_t rem = rem_i <= 0 ? 0u : (rem_i >= 7 ? 7u : (uint32_t)rem_i);
-    const uint32_t s0 = (s >> 8) & 15u;
     const bool missing = s == kPoisonSlot;  // array id >= n_arrays
-    const uint32_t info = missing ? (uint32_t)COH_RUN_DEFECT : __ldg(p.slow + slow_index(type, s0, rem));
+    const uint32_t info = missing ? (uint32_t)COH_RUN_DEFECT : __ldg(p.slow + slow_index(type, slot_state(s), rem));
     const uint32_t so_steps = (info >> 2) & 7u, so_xf = (info >> 5) & 3u;
     if (!missing) *sp = (uint16_t)slot_word((info >> 7) & 15u);
     steps += so_steps;
     xfers += so_xf;
-    if (!UNIFORM && !missing) tbytes += (uint64_t)so_xf * s_bytes[a];
+    if (!UNIFORM && !missing) tbytes += (uint64_t)so_xf * sm.bytes[a];
     status = info & 3u;
     stuck_call = i;
     stuck_arr = a;
@@ -339,18 +332,18 @@ __global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
     if (p.bnd) {
       const uint32_t g = i / 32u;
       p.bnd[(uint64_t)g * n + t] = word;
-      for (uint32_t w = g + 1; w < n_words; ++w) p.bnd[(uint64_t)w * n + t] = 0u;
+      for (uint32_t w = g + 1; w < (n_calls + 31u) / 32u; ++w) p.bnd[(uint64_t)w * n + t] = 0u;
     }
   }
   finished : {
     uint32_t sw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int a = 0; a < COH_MAX_ARRAYS; ++a) {
-      if (a < (int)n_arrays) {
+      if (a < (int)p.n_arrays) {
         uint16_t* const wp = reinterpret_cast<uint16_t*>(stb + a * 256 + toff);
         const uint32_t w = *wp;
         *wp = (uint16_t)kInit;  // reset for this thread's next trace
-        const int sh = 4 * (a & 7) - 2;
+        const int sh = 4 * (a & 7) - 8;  // state nibble at slot bits 8-11
         sw[a >> 3] |= (sh >= 0 ? (w << sh) : (w >> -sh)) & (15u << (4 * (a & 7)));
       }
     }
@@ -370,19 +363,20 @@ __global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
         v[k] = __reduce_add_sync(m, v[k]);
-        if (leader && v[k]) atomicAdd(&s_cnt[slot[k]], (unsigned long long)v[k]);
+        if (leader && v[k]) atomicAdd(&sm.cnt[slot[k]], (unsigned long long)v[k]);
       }
       if (UNIFORM) {  // bytes = transfers x size: one multiply by the leader
-        if (leader && v[5]) atomicAdd(&s_cnt[6], (unsigned long long)v[5] * p.bytes_uniform);
+        if (leader && v[5]) atomicAdd(&sm.cnt[6], (unsigned long long)v[5] * p.bytes_uniform);
       } else if (tb) {  // non-uniform sizes: per-lane shared atomic
-        atomicAdd(&s_cnt[6], (unsigned long long)tb);
+        atomicAdd(&sm.cnt[6], (unsigned long long)tb);
       }
     }
   }
   }
+#undef COH_REC
   if (p.counters) {
     __syncthreads();
-    if (tid < COH_N_COUNTERS && s_cnt[tid]) atomicAdd(p.counters + tid, s_cnt[tid]);
+    if (tid < COH_N_COUNTERS && sm.cnt[tid]) atomicAdd(p.counters + tid, sm.cnt[tid]);
   }
 }
 
@@ -411,6 +405,10 @@ int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, std::string
 
 int launch_trace_eval(const TraceLaunch& L, void* stream, std::string* err) {
   if (L.n_traces == 0) return COH_OK;
+  if (L.n_traces >= (1ull << 32) - 2u * 148u * kNT * 16u) {
+    *err = "trace_eval: n_traces must be < 2^32 per launch";
+    return COH_E_ARG;
+  }
   KParams kp;
   kp.rec = reinterpret_cast<const uint4*>(L.records);
   kp.n_traces = L.n_traces;
