@@ -78,12 +78,7 @@ int eval_device(coh_ctx* ctx, const coh_trace_batch* b, const uint16_t* d_record
   L.results = d_results;
   L.boundary = d_boundary;
   L.counters = d_counters;
-  // persistent grid, equal rounds per block
-  const uint64_t need = (n_traces + 127) / 128;
-  const int bps = ctx->blocks_per_sm;
-  const uint64_t cap = (uint64_t)ctx->sms * (uint64_t)std::max(1, bps);
-  const uint64_t rounds = (need + cap - 1) / cap;
-  L.grid = (int)((need + rounds - 1) / rounds);
+  L.sms = ctx->sms;  // the launcher sizes a persistent grid for the chosen variant
   std::string err;
   rc = cohb::launch_trace_eval(L, s, &err);
   if (rc) {
@@ -123,7 +118,7 @@ int coh_ctx_create(int device, coh_ctx** out) {
     cohb::trace_eval_set_smem_attr();
     int tpb = 0;
     std::string err;
-    rc = cohb::trace_eval_occupancy(&ctx->blocks_per_sm, &tpb, &err);
+    rc = cohb::trace_eval_occupancy(&ctx->blocks_per_sm, &tpb, 256, &err);
   } while (0);
   if (e != cudaSuccess || rc != COH_OK) {
     coh_ctx_destroy(ctx);

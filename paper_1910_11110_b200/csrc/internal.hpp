@@ -92,11 +92,11 @@ struct TraceLaunch {
   coh_trace_result* results;
   uint32_t* boundary;
   uint64_t* counters;  // optional fused counter reduction (device, COH_N_COUNTERS)
-  int grid;
+  int sms;  // SM count (persistent grid)
 };
 int launch_trace_eval(const TraceLaunch& p, void* stream, std::string* err);
 void trace_eval_set_smem_attr();
-int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, std::string* err);
+int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t n_calls, std::string* err);
 int launch_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
                        uint32_t n_arrays, uint32_t adv_per1024, uint16_t* d_records, void* stream,
                        std::string* err);

@@ -27,6 +27,8 @@
 //     device.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "internal.hpp"
 
 namespace cohb {
@@ -150,16 +152,25 @@ __device__ __forceinline__ uint32_t run_chunk(const uint4 v, uint32_t toff, uint
   return stop;
 }
 
+// 0, computed from x so that the scheduler cannot hoist or sink what depends on it
+// (ptxas would otherwise move the ring loads next to their first use).
+__device__ __forceinline__ uint32_t pin_zero(uint32_t x) {
+  uint32_t z;
+  asm volatile("prmt.b32 %0, %1, 0, 0x4444;" : "=r"(z) : "r"(x));
+  return z;
+}
+
 // FLAGS: kFuel = fuel may run out (fuel < 6 x n_calls), kBytes = non-uniform array
 // sizes (per-call byte accumulation), kRing = n_calls % 32 == 0 (the record ring runs on
 // into the next trace).
-enum : int { kFuel = 1, kBytes = 2, kRing = 4 };
+enum : int { kFuel = 1, kBytes = 2, kRing = 4, kDouble = 8 };
 
 template <int FLAGS>
-__global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
+__global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? 8 : 10) k_trace_eval(const KParams p) {
   constexpr bool CHECK_FUEL = FLAGS & kFuel;
   constexpr bool UNIFORM = !(FLAGS & kBytes);
   constexpr bool RING = FLAGS & kRing;
+  constexpr bool DOUBLE = FLAGS & kDouble;  // n_calls % 64 == 0: two register rings
   __shared__ TraceSmem sm;
   char* const stb = reinterpret_cast<char*>(sm.store);
   const char* const lutb = reinterpret_cast<const char*>(sm.lut);
@@ -189,6 +200,10 @@ __global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
 #define COH_REC(C, U) __ldcs(p.rec + (uint64_t)(C) * n + (U))
 
   uint4 ring[4];
+  uint4 B[4];  // second ring of the DOUBLE variant
+  if (DOUBLE)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) B[j] = make_uint4(0u, 0u, 0u, 0u);
   bool ring_ok = false;  // ring already holds chunks 0..3 of this thread's next trace
 
   for (uint32_t base = blockIdx.x * kNT; base < n; base += stride) {
@@ -247,29 +262,64 @@ __global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
         for (int j = 0; j < 4; ++j) ring[j] = (uint32_t)j < n_chunks ? COH_REC(j, t) : make_uint4(0u, 0u, 0u, 0u);
       }
       ring_ok = false;
-      for (uint32_t g = 0; g < n_groups; ++g) {
-        i0 = g * 32u;
-        // evaluate ring slot J, then refill it with the chunk 4 ahead (in the last group:
-        // chunk J of this thread's next trace)
-#define COH_STEP(J)                                                    \
-  {                                                                    \
-    COH_CHUNK(ring[J], ((J) & 1))                                      \
-    const uint32_t cn = 4u * (g + 1u) + (uint32_t)(J);                 \
-    if (cn < n_chunks) {                                               \
-      ring[J] = COH_REC(cn, t);                                        \
-    } else if (RING && t + stride < n) {                               \
-      ring[J] = COH_REC(J, t + stride);                                \
-    }                                                                  \
-    if ((J) & 1) { COH_FLUSH }                                         \
+#define COH_GROUP_END(G)                                                          \
+  /* 32 calls done: the sentinel was shifted out, call 0's violation bit is 31 */ \
+  bnd = ~__brev(bnd);                                                             \
+  if (p.bnd) p.bnd[(uint64_t)(G) * n + t] = bnd;                                  \
+  viol_blocks += 32u - __popc(bnd);                                               \
+  bnd = 1u;
+      if (DOUBLE) {
+        // Two register rings, A = even groups, B = odd groups.  A group's four loads are
+        // issued together right after its predecessor's first chunk, so every first use
+        // (which waits for all outstanding loads: they share one scoreboard) has three
+        // chunks of lead.  n_groups is even; after the last pair A holds chunks 0..3 of
+        // this thread's next trace (RING).
+        uint4* const A = ring;
+        for (uint32_t g = 0; g < n_groups; g += 2u) {
+          i0 = g * 32u;
+          COH_CHUNK(A[0], 0)
+          {
+            const uint32_t tz = t + pin_zero(bnd);  // keeps the loads after chunk 0
+#pragma unroll
+            for (int j = 0; j < 4; ++j) B[j] = COH_REC(4u * (g + 1u) + (uint32_t)j, tz);
+          }
+          COH_CHUNK(A[1], 1) COH_FLUSH
+          COH_CHUNK(A[2], 0)
+          COH_CHUNK(A[3], 1) COH_FLUSH
+          COH_GROUP_END(g)
+          i0 += 32u;
+          COH_CHUNK(B[0], 0)
+          {
+            const bool last = g + 2u >= n_groups;
+            const bool nx = RING && last && t + stride < n;
+            const uint32_t tz = (nx ? t + stride : t) + pin_zero(bnd);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) A[j] = COH_REC(last ? (uint32_t)j : 4u * (g + 2u) + (uint32_t)j, tz);
+          }
+          COH_CHUNK(B[1], 1) COH_FLUSH
+          COH_CHUNK(B[2], 0)
+          COH_CHUNK(B[3], 1) COH_FLUSH
+          COH_GROUP_END(g + 1u)
+        }
+      } else {
+        for (uint32_t g = 0; g < n_groups; ++g) {
+          i0 = g * 32u;
+          // evaluate ring slot J, then refill it with the chunk 4 ahead (in the last
+          // group: chunk J of this thread's next trace)
+#define COH_STEP(J)                                                                   \
+  {                                                                                   \
+    COH_CHUNK(ring[J], ((J) & 1))                                                     \
+    const uint32_t cn = 4u * (g + 1u) + (uint32_t)(J);                                \
+    const bool nx_ = RING && cn >= n_chunks && t + stride < n;                        \
+    ring[J] = COH_REC(cn < n_chunks ? cn : (uint32_t)(J), nx_ ? t + stride : t);      \
+    if ((J) & 1) { COH_FLUSH }                                                        \
   }
-        COH_STEP(0) COH_STEP(1) COH_STEP(2) COH_STEP(3)
+          COH_STEP(0) COH_STEP(1) COH_STEP(2) COH_STEP(3)
 #undef COH_STEP
-        // 32 calls done: the sentinel was shifted out, call 0's violation bit is bit 31
-        bnd = ~__brev(bnd);
-        if (p.bnd) p.bnd[(uint64_t)g * n + t] = bnd;
-        viol_blocks += 32u - __popc(bnd);
-        bnd = 1u;
+          COH_GROUP_END(g)
+        }
       }
+#undef COH_GROUP_END
       if (RING) ring_ok = true;
       if (!RING) {
         const uint32_t tail = n_calls - n_groups * 32u;
@@ -299,6 +349,14 @@ __global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
 
   slow_path : {
     ring_ok = false;
+    uint32_t keep = 0;  // 0; ties the rings to this path (see below)
+    if (DOUBLE) {
+      // The rings are live on this path too, so the scheduler cannot sink their loads
+      // past the slow-path branches (which would leave them no lead before first use).
+#pragma unroll
+      for (int j = 0; j < 4; ++j) keep ^= ring[j].x ^ ring[j].y ^ ring[j].z ^ ring[j].w ^ B[j].x ^ B[j].y ^ B[j].z ^ B[j].w;
+      keep = pin_zero(keep);
+    }
     // which call: k calls of this 32-group completed (sentinel position)
     const uint32_t k = 31u - __clz(bnd);
     const uint32_t i = i0 + k;
@@ -325,7 +383,7 @@ __global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
     stuck_call = i;
     stuck_arr = a;
     stuck_eff = (info >> 11) & 7u;
-    stuck_flags = (info >> 14) & 15u;
+    stuck_flags = ((info >> 14) & 15u) | keep;
     calls_done = i;
     const uint32_t word = k ? ((~__brev(bnd ^ (1u << k))) >> (32u - k)) : 0u;
     viol_blocks += k - __popc(word);
@@ -380,9 +438,28 @@ __global__ void __launch_bounds__(kNT, 10) k_trace_eval(const KParams p) {
   }
 }
 
+static bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && *v && *v != '0';
+}
+
 template <int F>
 static int launch_one(const TraceLaunch& L, const KParams& kp, cudaStream_t s, std::string* err) {
-  k_trace_eval<F><<<L.grid, kNT, 0, s>>>(kp);
+  static int occ = 0;  // resident blocks per SM of this variant
+  if (!occ) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trace_eval<F>, kNT, 0);
+    if (e != cudaSuccess || occ < 1) {
+      *err = std::string("trace_eval occupancy: ") + cudaGetErrorString(e);
+      occ = 0;
+      return COH_E_CUDA;
+    }
+  }
+  // persistent grid: every block runs the same number of rounds
+  const uint64_t need = (L.n_traces + kNT - 1) / kNT;
+  const uint64_t cap = (uint64_t)L.sms * (uint64_t)occ;
+  const uint64_t rounds = (need + cap - 1) / cap;
+  const int grid = (int)((need + rounds - 1) / rounds);
+  k_trace_eval<F><<<grid, kNT, 0, s>>>(kp);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("trace_eval launch: ") + cudaGetErrorString(e);
@@ -391,9 +468,11 @@ static int launch_one(const TraceLaunch& L, const KParams& kp, cudaStream_t s, s
   return COH_OK;
 }
 
-int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, std::string* err) {
+int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t n_calls, std::string* err) {
   int b = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trace_eval<kRing>, kNT, 0);
+  const bool dbl = n_calls % 64u == 0u && n_calls >= 64u && !getenv_flag("COH_TE_SINGLE");
+  cudaError_t e = dbl ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trace_eval<kRing | kDouble>, kNT, 0)
+                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_trace_eval<kRing>, kNT, 0);
   if (e != cudaSuccess) {
     *err = std::string("occupancy: ") + cudaGetErrorString(e);
     return COH_E_CUDA;
@@ -432,11 +511,13 @@ int launch_trace_eval(const TraceLaunch& L, void* stream, std::string* err) {
     }
   }
   const int f = (L.check_fuel ? kFuel : 0) | (L.uniform_bytes ? 0 : kBytes) |
-                (L.n_calls % 32u == 0u && L.n_calls >= 32u ? kRing : 0);
+                (L.n_calls % 32u == 0u && L.n_calls >= 32u ? kRing : 0) |
+                (L.n_calls % 64u == 0u && L.n_calls >= 64u && !getenv_flag("COH_TE_SINGLE") ? kDouble : 0);
   switch (f) {
 #define COH_CASE(F) \
   case F: return launch_one<F>(L, kp, s, err);
     COH_CASE(0) COH_CASE(1) COH_CASE(2) COH_CASE(3) COH_CASE(4) COH_CASE(5) COH_CASE(6) COH_CASE(7)
+    COH_CASE(12) COH_CASE(13) COH_CASE(14) COH_CASE(15)
 #undef COH_CASE
   }
   return COH_E_ARG;
