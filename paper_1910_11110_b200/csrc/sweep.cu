@@ -36,6 +36,7 @@ __global__ void k_sweep_run(const uint32_t* __restrict__ code, const SweepMeta* 
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_items) return;
   const SweepItem it = items[i];
+  const unsigned long long sbits = (unsigned long long)it.bits | ((unsigned long long)it.pad << 32);
   const SweepMeta m = meta[it.prog];
   const uint32_t* prog = code + m.code_off;
   unsigned long long store = 0x5555555555555555ull;  // initial_store: every key (V,I)
@@ -70,7 +71,7 @@ __global__ void k_sweep_run(const uint32_t* __restrict__ code, const SweepMeta* 
       const uint32_t ck = (ins >> 4) & 3u, key = (ins >> 8) & 0xFFu;
       uint32_t bit;
       if (ck == 2u) {
-        if (cursor < it.len) bit = (it.bits >> cursor++) & 1u;
+        if (cursor < it.len) bit = (uint32_t)(sbits >> cursor++) & 1u;
         else { overflow = 1; bit = 0; }
       } else {
         bit = (uint32_t)(store >> (2 * key + ck)) & 1u;  // valid: local flag, gvalid: remote

@@ -34,9 +34,9 @@ struct SweepMeta {
 };
 struct SweepItem {
   uint32_t prog;
-  uint32_t bits;   // schedule answers, bit k = k-th
-  uint32_t len;
-  uint32_t pad;
+  uint32_t bits;   // schedule answers, bit k = k-th (answers 0..31)
+  uint32_t len;    // <= 64
+  uint32_t pad;    // answers 32..63
 };
 struct SweepOut {
   uint32_t status_consumed;  // bits 0-1 status, 2-9 consumed, 10 overflowed, 11-15 blocks done,
