@@ -366,21 +366,22 @@ int coh_sweep(coh_ctx* ctx, uint64_t seed0, uint32_t n_seeds, const coh_gen_limi
 
 /* ---- DSL front end and CLI reporting ----------------------
  * The reference command line (tools/cohere_main.cpp:80-230) over program text.
- * command: "check" | "run" | "infer" | "translate" (cmd_check / cmd_run / cmd_infer /
- * cmd_translate); opts mirror its flags (--raw, --json, --no-overlap, --fuel,
- * --schedule).  Writes what the CLI prints to stdout / stderr (NUL-terminated) and its
+ * command: "check" | "run" | "trace" | "infer" | "translate" (cmd_check / cmd_run /
+ * cmd_infer / cmd_translate); opts mirror its flags (--raw, --json, --no-overlap, --fuel,
+ * --schedule, --trace).  Writes what the CLI prints to stdout / stderr (NUL-terminated) and its
  * exit code (0 ok, 1 diagnostics / overlap conflict, 2 usage / parse / construction
  * error, 3 stuck, 4 fuel exhausted).  Parsing (parse.hpp), overlap closure (overlap.hpp),
  * the static checker (checker.hpp) and the printers (pretty.hpp) are host passes; "run"
  * executes the translated program on the GPU (the general block interpreter of
- * coh_sweep: at most 32 store keys, schedules of at most 64 answers).  "trace" (per-step
- * listing) is not produced by the device interpreter (exit 2).  ctx may be NULL except
- * for "run".  Returns COH_OK (the CLI outcome is in *exit_code), a negative value
+ * coh_sweep: at most 32 store keys, schedules of at most 64 answers), which records one
+ * (instruction, rule, store) entry per step for "trace" / --trace (at most 4M steps).
+ * ctx may be NULL except for "run" / "trace".  Returns COH_OK (the CLI outcome is in *exit_code), a negative value
  * -(needed bytes) when out/err were too small (the texts are truncated), or COH_E_*. */
 typedef struct coh_cli_opts {
   int raw, json, no_overlap;
   int32_t fuel;              /* --fuel (default 10000; must be >= 1)  */
   const char* schedule;      /* --schedule "0101" or NULL             */
+  int trace;                 /* run --trace                           */
 } coh_cli_opts;
 int coh_cli(coh_ctx* ctx, const char* command, const char* src, const coh_cli_opts* opts,
             char* out, size_t out_cap, char* err, size_t err_cap, int* exit_code);

@@ -5,7 +5,7 @@
 // program text (the reference CLI itself needs CLI11 and nlohmann/json, which are not in
 // this image: SURVEY §8(c)).  Built into oracle/_ref/libcohere_ref.so with ref_harness.cpp.
 //
-// ref_cli(command, src, raw, no_overlap, fuel, schedule, out, out_cap, err, err_cap, &exit)
+// ref_cli(command, src, raw, no_overlap, fuel, schedule, trace, out, out_cap, err, err_cap, &exit)
 // follows cmd_check / cmd_run / cmd_infer / cmd_translate and the exception-to-exit-code
 // mapping of main() (tools/cohere_main.cpp:80-274), text output only.
 #include <cstring>
@@ -29,7 +29,22 @@ std::string diag_line(const std::string& rule, const std::string& view, SourcePo
   return std::to_string(pos.line) + ":" + std::to_string(pos.col) + ": " + rule + " [" + view + "] " + msg + "\n";
 }
 
-int report(const RunResult& r, bool schedule_given, std::ostringstream& out, std::ostringstream& err) {
+int report(const RunResult& r, bool schedule_given, bool trace, std::ostringstream& out, std::ostringstream& err) {
+  if (trace) {
+    int idx = 0;
+    for (const auto& step : r.trace) {
+      std::ostringstream line;
+      line << ++idx << " " << name_of(step.rule);
+      while (line.str().size() < 16) line << " ";
+      line << to_string(step.head);
+      const char* sep = " => ";
+      for (const auto& [key, pair] : step.delta) {
+        line << sep << to_string(key) << "=" << to_string(pair);
+        sep = " ";
+      }
+      out << line.str() << "\n";
+    }
+  }
   out << "outcome: " << name_of(r.status) << "\n";
   out << "steps: " << r.steps << "\n";
   if (r.stuck) out << "stuck at: " << r.stuck->describe() << "\n";
@@ -44,7 +59,7 @@ int report(const RunResult& r, bool schedule_given, std::ostringstream& out, std
 }
 
 int command(const std::string& cmd, const std::string& src, bool raw, bool no_overlap, int fuel,
-            const std::string& schedule, std::ostringstream& out, std::ostringstream& err) {
+            const std::string& schedule, bool trace, std::ostringstream& out, std::ostringstream& err) {
   if (cmd == "check") {
     if (raw) {
       RawProgram p = parse_raw(src);
@@ -60,11 +75,13 @@ int command(const std::string& cmd, const std::string& src, bool raw, bool no_ov
     for (const auto& n : check_notes(p)) out << "note: " << diag_line(n.rule, n.view, n.pos, n.message);
     return diags.empty() ? 0 : 1;
   }
-  if (cmd == "run") {
+  if (cmd == "run" || cmd == "trace") {
+    trace = trace || cmd == "trace";
+    const TraceMode mode = trace ? TraceMode::Full : TraceMode::None;
     Schedule sched = Schedule::from_string(schedule);
     if (raw) {
       RawProgram p = parse_raw(src);
-      return report(run(p, fuel, sched, TraceMode::None), !schedule.empty(), out, err);
+      return report(run(p, fuel, sched, mode), !schedule.empty(), trace, out, err);
     }
     AnnotatedProgram p = parse_program(src);
     OverlapRegistry reg = no_overlap ? OverlapRegistry() : build_registry(p.decls);
@@ -74,8 +91,8 @@ int command(const std::string& cmd, const std::string& src, bool raw, bool no_ov
       for (const auto& d : diags) err << diag_line(d.rule, d.view, d.pos, d.message);
       return 1;
     }
-    return report(run(translate_program(p), initial_store(p.decls), fuel, sched, TraceMode::None), !schedule.empty(),
-                  out, err);
+    return report(run(translate_program(p), initial_store(p.decls), fuel, sched, mode), !schedule.empty(), trace, out,
+                  err);
   }
   if (cmd == "infer" || cmd == "translate") {
     if (raw) throw std::runtime_error(cmd + " needs an annotated program");
@@ -95,11 +112,11 @@ int command(const std::string& cmd, const std::string& src, bool raw, bool no_ov
 }  // namespace
 
 extern "C" int ref_cli(const char* cmd, const char* src, int raw, int no_overlap, int fuel, const char* schedule,
-                       char* out, size_t out_cap, char* err, size_t err_cap, int* exit_code) {
+                       int trace, char* out, size_t out_cap, char* err, size_t err_cap, int* exit_code) {
   std::ostringstream o, e;
   int code;
   try {
-    code = command(cmd, src, raw != 0, no_overlap != 0, fuel, schedule ? schedule : "", o, e);
+    code = command(cmd, src, raw != 0, no_overlap != 0, fuel, schedule ? schedule : "", trace != 0, o, e);
   } catch (const ParseError& x) {
     e << "error: " << x.what() << "\n";
     code = 2;

@@ -16,7 +16,7 @@ from ._ffi import CohError, lib
 
 class _Opts(C.Structure):
     _fields_ = [("raw", C.c_int), ("json", C.c_int), ("no_overlap", C.c_int), ("fuel", C.c_int32),
-                ("schedule", C.c_char_p)]
+                ("schedule", C.c_char_p), ("trace", C.c_int)]
 
 
 def _register(L):
@@ -30,9 +30,9 @@ _register(lib())
 
 
 def run_cli(command: str, src: str, ctx=None, raw: bool = False, json: bool = False, no_overlap: bool = False,
-            fuel: int = 10000, schedule: str | None = None) -> tuple[str, str, int]:
+            fuel: int = 10000, schedule: str | None = None, trace: bool = False) -> tuple[str, str, int]:
     """(stdout, stderr, exit code) of the reference CLI's `command` on program text `src`."""
-    o = _Opts(int(raw), int(json), int(no_overlap), fuel, schedule.encode() if schedule else None)
+    o = _Opts(int(raw), int(json), int(no_overlap), fuel, schedule.encode() if schedule else None, int(trace))
     cap = 1 << 16
     while True:
         out, err, code = C.create_string_buffer(cap), C.create_string_buffer(cap), C.c_int(0)
@@ -58,6 +58,8 @@ def main(argv: list[str] | None = None) -> int:
         if run_flags:
             s.add_argument("--fuel", type=int, default=10000)
             s.add_argument("--schedule", default="")
+        if name == "run":
+            s.add_argument("--trace", action="store_true")
     a = p.parse_args(argv)
     try:
         src = open(a.file, encoding="utf-8").read()
@@ -69,7 +71,7 @@ def main(argv: list[str] | None = None) -> int:
         from ._ffi import Context
         ctx = Context(0)
     out, err, code = run_cli(a.cmd, src, ctx, a.raw, a.json, a.no_overlap, getattr(a, "fuel", 10000),
-                             getattr(a, "schedule", "") or None)
+                             getattr(a, "schedule", "") or None, getattr(a, "trace", False))
     sys.stdout.write(out)
     sys.stderr.write(err)
     return code

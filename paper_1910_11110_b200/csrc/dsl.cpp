@@ -870,6 +870,13 @@ KeyMap key_map(const Decls& d) {  // initial_store (program.hpp:174-184): every 
 struct Emit {
   const KeyMap& km;
   std::vector<uint32_t> code;
+  std::vector<std::string> head;  // per instruction: to_string of the statement it starts
+  void note(const Stmt& s) {
+    std::string h;
+    one_line(List{s}, h);
+    head.resize(code.size() + 1);
+    head[code.size()] = h;
+  }
   uint32_t key(const Target& t) const {
     switch (t.kind) {
       case 0: return km.scalar.at(t.name);
@@ -879,6 +886,7 @@ struct Emit {
   }
   void list(const List& l) {
     for (const auto& s : l) {
+      note(s);
       if (s.op == 0) {
         if (s.t.kind == 3) {
           const uint32_t base = km.buf_base.at(s.t.buffer);
@@ -924,7 +932,7 @@ struct DevBuf {
 };
 
 int device_run(coh_ctx* ctx, const std::vector<uint32_t>& code, uint32_t n_keys, int32_t fuel, uint64_t bits,
-               uint32_t len, RunOut* r, std::string* err) {
+               uint32_t len, RunOut* r, std::string* err, std::vector<SweepTrace>* trace = nullptr) {
   if (!ctx) {
     *err = "run needs a device context";
     return COH_E_ARG;
@@ -933,7 +941,7 @@ int device_run(coh_ctx* ctx, const std::vector<uint32_t>& code, uint32_t n_keys,
     *err = "cudaSetDevice failed";
     return COH_E_CUDA;
   }
-  DevBuf d_code, d_meta, d_checks, d_item, d_out;
+  DevBuf d_code, d_meta, d_checks, d_item, d_out, d_trace;
   SweepMeta meta{0, n_keys, 0, 0};
   SweepItem item{0, (uint32_t)bits, len, (uint32_t)(bits >> 32)};
   SweepOut out{};
@@ -952,11 +960,16 @@ int device_run(coh_ctx* ctx, const std::vector<uint32_t>& code, uint32_t n_keys,
   COH_D(cudaMemcpy(d_code.p, code.data(), code.size() * 4, cudaMemcpyHostToDevice));
   COH_D(cudaMemcpy(d_meta.p, &meta, sizeof meta, cudaMemcpyHostToDevice));
   COH_D(cudaMemcpy(d_item.p, &item, sizeof item, cudaMemcpyHostToDevice));
+  if (trace) COH_D(cudaMalloc(&d_trace.p, (size_t)fuel * sizeof(SweepTrace)));
   const int rc = launch_sweep_run(static_cast<uint32_t*>(d_code.p), static_cast<SweepMeta*>(d_meta.p),
                                   static_cast<uint16_t*>(d_checks.p), static_cast<SweepItem*>(d_item.p), 1u, fuel,
-                                  static_cast<SweepOut*>(d_out.p), s, err);
+                                  static_cast<SweepOut*>(d_out.p), s, err, static_cast<SweepTrace*>(d_trace.p));
   if (rc) return rc;
   COH_D(cudaMemcpy(&out, d_out.p, sizeof out, cudaMemcpyDeviceToHost));
+  if (trace) {
+    trace->resize(out.steps);
+    if (out.steps) COH_D(cudaMemcpy(trace->data(), d_trace.p, out.steps * sizeof(SweepTrace), cudaMemcpyDeviceToHost));
+  }
 #undef COH_D
   ctx->launches++;
   r->status = out.status_consumed & 3u;
@@ -986,6 +999,40 @@ struct Cli {
 };
 
 // report_run (tools/cohere_main.cpp:96-158), text and JSON
+std::string store_record(const KeyMap& km, uint32_t k, uint32_t bits) {
+  return "{\"key\":" + jstr(key_str(km.keys[k])) + ",\"local\":" + jstr((bits & 1u) ? "V" : "I") +
+         ",\"remote\":" + jstr((bits & 2u) ? "V" : "I") + "}";
+}
+
+// the --trace listing (tools/cohere_main.cpp:97-120): step, rule, head, changed keys in
+// application order (a whole-view sync changes its cells ascending = key order)
+void report_trace(const KeyMap& km, const std::vector<std::string>& head, const std::vector<SweepTrace>& tr,
+                  const coh_cli_opts& o, Cli& c) {
+  static const char* rule[] = {"effect", "remote-effect", "while-true", "while-false", "if-true", "if-false"};
+  unsigned long long before = 0;
+  for (uint32_t k = 0; k < km.keys.size(); ++k) before |= 1ull << (2 * k);  // initial_store: (V,I)
+  for (size_t i = 0; i < tr.size(); ++i) {
+    const unsigned long long after = tr[i].store;
+    std::string delta;
+    for (uint32_t k = 0; k < km.keys.size(); ++k) {
+      const uint32_t a = (uint32_t)(after >> (2 * k)) & 3u;
+      if (a == ((uint32_t)(before >> (2 * k)) & 3u)) continue;
+      if (o.json) delta += (delta.empty() ? "" : ",") + store_record(km, k, a);
+      else delta += (delta.empty() ? " => " : " ") + key_str(km.keys[k]) + "=" + pair_str(a);
+    }
+    const std::string& h = head[tr[i].pc];
+    if (o.json) {
+      c.out += "{\"delta\":[" + delta + "],\"head\":" + jstr(h) + ",\"rule\":" + jstr(rule[tr[i].rule]) +
+               ",\"step\":" + std::to_string(i + 1) + "}\n";
+    } else {
+      std::string line = std::to_string(i + 1) + " " + rule[tr[i].rule];
+      if (line.size() < 16) line.append(16 - line.size(), ' ');
+      c.out += line + h + delta + "\n";
+    }
+    before = after;
+  }
+}
+
 void report(const KeyMap& km, const RunOut& r, const coh_cli_opts& o, bool schedule_given, Cli& c) {
   static const char* st[] = {"done", "stuck", "fuel-exhausted", "defect"};
   if (o.json) {
@@ -1012,8 +1059,7 @@ void report(const KeyMap& km, const RunOut& r, const coh_cli_opts& o, bool sched
   for (uint32_t k : order) {
     const uint32_t bits = (uint32_t)(r.store >> (2 * k)) & 3u;
     if (o.json)
-      c.out += "{\"key\":" + jstr(key_str(km.keys[k])) + ",\"local\":" + jstr((bits & 1u) ? "V" : "I") +
-               ",\"remote\":" + jstr((bits & 2u) ? "V" : "I") + "}\n";
+      c.out += store_record(km, k, bits) + "\n";
     else
       c.out += key_str(km.keys[k]) + " " + pair_str(bits) + "\n";
   }
@@ -1058,11 +1104,7 @@ int cli(coh_ctx* ctx, const std::string& cmd, const std::string& src, const coh_
     return COH_OK;
   }
   if (cmd == "run" || cmd == "trace") {
-    if (cmd == "trace") {
-      c.err += "error: step traces are not produced by the device interpreter\n";
-      c.exit = 2;
-      return COH_OK;
-    }
+    const bool tracing = cmd == "trace" || o.trace;
     for (char ch : schedule)
       if (ch != '0' && ch != '1') throw ConstructionError("schedule must be a string of 0s and 1s");
     if (schedule.size() > 64) throw ConstructionError("schedules longer than 64 answers are not supported");
@@ -1094,16 +1136,26 @@ int cli(coh_ctx* ctx, const std::string& cmd, const std::string& src, const coh_
       *fatal = "program has " + std::to_string(km.keys.size()) + " store keys; the device interpreter holds 32";
       return COH_E_CONSTRUCTION;
     }
-    Emit e{km, {}};
+    Emit e{km, {}, {}};
     e.list(prog);
     e.code.push_back(BC_END);
     if (e.code.size() > 65535) {
       *fatal = "program exceeds 64K interpreter instructions";
       return COH_E_CONSTRUCTION;
     }
+    if (tracing && o.fuel > (1 << 22)) {
+      *fatal = "--trace records at most 4M steps (lower --fuel)";
+      return COH_E_ARG;
+    }
     RunOut r{};
-    const int rc = device_run(ctx, e.code, (uint32_t)km.keys.size(), o.fuel, bits, (uint32_t)schedule.size(), &r, fatal);
+    std::vector<SweepTrace> tr;
+    const int rc = device_run(ctx, e.code, (uint32_t)km.keys.size(), o.fuel, bits, (uint32_t)schedule.size(), &r, fatal,
+                              tracing ? &tr : nullptr);
     if (rc) return rc;
+    if (tracing) {
+      e.head.resize(e.code.size());
+      report_trace(km, e.head, tr, o, c);
+    }
     report(km, r, o, !schedule.empty(), c);
     return COH_OK;
   }
@@ -1156,7 +1208,7 @@ extern "C" int coh_cli(coh_ctx* ctx, const char* command, const char* src, const
                        size_t out_cap, char* err, size_t err_cap, int* exit_code) {
   using namespace cohb::dsl;
   if (!command || !src || !exit_code) return COH_E_ARG;
-  coh_cli_opts o = opts ? *opts : coh_cli_opts{0, 0, 0, 10000, nullptr};
+  coh_cli_opts o = opts ? *opts : coh_cli_opts{0, 0, 0, 10000, nullptr, 0};
   Cli c;
   std::string fatal;
   int rc = COH_OK;

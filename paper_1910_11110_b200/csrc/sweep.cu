@@ -32,10 +32,12 @@ __device__ __forceinline__ bool leq_d(uint32_t a, uint32_t c) {
 
 __global__ void k_sweep_run(const uint32_t* __restrict__ code, const SweepMeta* __restrict__ meta,
                             const uint16_t* __restrict__ checks, const SweepItem* __restrict__ items,
-                            uint32_t n_items, int32_t fuel, SweepOut* __restrict__ out) {
+                            uint32_t n_items, int32_t fuel, SweepOut* __restrict__ out,
+                            SweepTrace* __restrict__ trace) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_items) return;
   const SweepItem it = items[i];
+  if (i != 0) trace = nullptr;
   const unsigned long long sbits = (unsigned long long)it.bits | ((unsigned long long)it.pad << 32);
   const SweepMeta m = meta[it.prog];
   const uint32_t* prog = code + m.code_off;
@@ -76,6 +78,7 @@ __global__ void k_sweep_run(const uint32_t* __restrict__ code, const SweepMeta* 
       } else {
         bit = (uint32_t)(store >> (2 * key + ck)) & 1u;  // valid: local flag, gvalid: remote
       }
+      if (trace) trace[steps] = SweepTrace{pc, (op == BC_WHILE ? 2u : 4u) + (bit ? 0u : 1u), store};
       ++steps;
       pc = bit ? pc + 1 : (ins >> 16);
       continue;
@@ -111,6 +114,7 @@ __global__ void k_sweep_run(const uint32_t* __restrict__ code, const SweepMeta* 
         store = (store & ~(3ull << (2 * k))) | ((unsigned long long)apply_pair_d(eff, site, before) << (2 * k));
       }
     }
+    if (trace) trace[steps] = SweepTrace{pc, site, store};
     ++steps;
     ++pc;
   }
@@ -126,10 +130,11 @@ __global__ void k_sweep_run(const uint32_t* __restrict__ code, const SweepMeta* 
 }  // namespace
 
 int launch_sweep_run(const uint32_t* code, const SweepMeta* meta, const uint16_t* checks, const SweepItem* items,
-                     uint32_t n_items, int32_t fuel, SweepOut* out, void* stream, std::string* err) {
+                     uint32_t n_items, int32_t fuel, SweepOut* out, void* stream, std::string* err,
+                     SweepTrace* trace) {
   if (!n_items) return COH_OK;
   k_sweep_run<<<(n_items + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(code, meta, checks, items,
-                                                                                   n_items, fuel, out);
+                                                                                   n_items, fuel, out, trace);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("sweep launch: ") + cudaGetErrorString(e);

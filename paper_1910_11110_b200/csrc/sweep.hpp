@@ -46,7 +46,16 @@ struct SweepOut {
   uint32_t stuck;            // effect | site << 3 | key kind (abstract) << 4 | actual << 5
   uint32_t pad;
 };
+// One record per reduction step of item 0 (the CLI's --trace): the instruction that fired,
+// the rule (0 effect, 1 remote-effect, 2 while-true, 3 while-false, 4 if-true, 5 if-false,
+// semantics.hpp:76-79) and the store after the step.
+struct SweepTrace {
+  uint32_t pc;
+  uint32_t rule;
+  unsigned long long store;
+};
 int launch_sweep_run(const uint32_t* code, const SweepMeta* meta, const uint16_t* checks, const SweepItem* items,
-                     uint32_t n_items, int32_t fuel, SweepOut* out, void* stream, std::string* err);
+                     uint32_t n_items, int32_t fuel, SweepOut* out, void* stream, std::string* err,
+                     SweepTrace* trace = nullptr);
 
 }  // namespace cohb

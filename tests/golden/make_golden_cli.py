@@ -5,9 +5,9 @@ build container (where /root/reference exists):
     make -C oracle && python tests/golden/make_golden_cli.py
 
 Output (committed): cli.json.gz, one record per case
-  {cmd, src, raw, no_overlap, fuel, schedule, out, err, exit}
+  {cmd, src, raw, no_overlap, fuel, schedule, trace, out, err, exit}
 Corpus:
-  * the reference's samples/*.coh under every command and flag combination (their
+  * the reference's samples/*.coh under every command and flag combination, traces included (their
     outputs include the reference's own tests/golden/*.txt, checked here);
   * gen_well_declared programs (coh_gen_program_text, text-identical to the reference
     generator) under run (several schedules and fuels), infer, translate, check;
@@ -37,16 +37,16 @@ REF_GOLDEN = "/root/reference/proj/tests/golden"
 def ref_fn():
     R = o.reference()
     R.ref_cli.restype = C.c_int
-    R.ref_cli.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_char_p, C.c_size_t,
-                          C.c_char_p, C.c_size_t, C.POINTER(C.c_int)]
+    R.ref_cli.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int, C.c_char_p,
+                          C.c_size_t, C.c_char_p, C.c_size_t, C.POINTER(C.c_int)]
 
-    def call(cmd, src, raw=0, no_overlap=0, fuel=10000, schedule=""):
-        cap = 1 << 18
+    def call(cmd, src, raw=0, no_overlap=0, fuel=10000, schedule="", trace=0):
+        cap = 1 << 20
         out, err, code = C.create_string_buffer(cap), C.create_string_buffer(cap), C.c_int()
-        rc = R.ref_cli(cmd.encode(), src.encode(), raw, no_overlap, fuel, schedule.encode(), out, cap, err, cap,
+        rc = R.ref_cli(cmd.encode(), src.encode(), raw, no_overlap, fuel, schedule.encode(), trace, out, cap, err, cap,
                        C.byref(code))
         assert rc == 0
-        return dict(cmd=cmd, src=src, raw=raw, no_overlap=no_overlap, fuel=fuel, schedule=schedule,
+        return dict(cmd=cmd, src=src, raw=raw, no_overlap=no_overlap, fuel=fuel, schedule=schedule, trace=trace,
                     out=out.value.decode(), err=err.value.decode(), exit=code.value)
     return call
 
@@ -144,6 +144,9 @@ def main():
                     cases.append(ref(cmd, src, raw, no))
         for sched in ("0", "1", "0101"):
             cases.append(ref("run", src, 0, 0, 10000, sched))
+        for raw in (0, 1):
+            cases.append(ref("trace", src, raw))
+            cases.append(ref("run", src, raw, 0, 4, "1", 1))
         for fuel in (1, 2, 3, 5):
             cases.append(ref("run", src, 0, 0, fuel))
     for g in sorted(glob.glob(os.path.join(REF_GOLDEN, "*.txt"))):
@@ -162,13 +165,15 @@ def main():
             cases.append(ref("run", src, 0, 0, 10000, sched))
         cases.append(ref("run", src, 0, 0, rng.randrange(1, 12), "1" * rng.randrange(0, 4)))
         cases.append(ref("run", src, 0, 1))
+        if seed % 4 == 0:
+            cases.append(ref("trace", src, 0, 0, 10000, "".join(rng.choice("01") for _ in range(6))))
         for cmd in ("check", "infer", "translate"):
             cases.append(ref(cmd, src))
         m = mutate(src, rng)
         cases.append(ref("check", m))
         cases.append(ref("run", m, 0, 0, 10000, "01"))
         r = raw_of(src, rng)
-        cases.append(ref("run", r, 1, 0, 10000, "10"))
+        cases.append(ref("run", r, 1, 0, 10000, "10", seed % 5 == 0))
         cases.append(ref("check", r, 1))
     # 4. edge cases
     for cmd, src in EDGE:
@@ -176,6 +181,7 @@ def main():
             cases.append(ref(cmd, src, 0, no))
     for cmd, src in RAW_EDGE:
         cases.append(ref(cmd, src, 1, 0, 10000, "110"))
+        cases.append(ref(cmd, src, 1, 0, 10000, "110", 1))
     cases.append(ref("run", "scalar x\nR(x) { r x; }\n", 0, 0, 10000, "012"))  # bad schedule
     with gzip.open(os.path.join(HERE, "cli.json.gz"), "wt") as f:
         json.dump(cases, f)

@@ -22,7 +22,7 @@ CASES = json.load(gzip.open(os.path.join(HERE, "golden", "cli.json.gz"), "rt"))
 
 def got(c, ctx=None):
     return run_cli(c["cmd"], c["src"], ctx, raw=bool(c["raw"]), no_overlap=bool(c["no_overlap"]), fuel=c["fuel"],
-                   schedule=c["schedule"] or None)
+                   schedule=c["schedule"] or None, trace=bool(c.get("trace", 0)))
 
 
 def want(c):
@@ -30,7 +30,7 @@ def want(c):
 
 
 def test_host_commands_match_reference():
-    host = [c for c in CASES if c["cmd"] != "run"]
+    host = [c for c in CASES if c["cmd"] not in ("run", "trace")]
     assert len(host) > 2000
     for c in host:
         assert got(c) == want(c), (c["cmd"], c["src"])
@@ -38,7 +38,7 @@ def test_host_commands_match_reference():
 
 def test_run_rejections_before_execution():
     # diagnostics (exit 1), parse / construction / schedule errors (exit 2) never reach the device
-    rej = [c for c in CASES if c["cmd"] == "run" and c["exit"] in (1, 2)]
+    rej = [c for c in CASES if c["cmd"] in ("run", "trace") and c["exit"] in (1, 2)]
     assert len(rej) > 200
     for c in rej:
         assert got(c) == want(c), c["src"]
@@ -103,8 +103,8 @@ def test_live_reference_fresh_programs():
 
 @pytest.mark.gpu
 def test_run_on_gpu_matches_reference(ctx):
-    runs = [c for c in CASES if c["cmd"] == "run"]
-    assert len(runs) > 2500
+    runs = [c for c in CASES if c["cmd"] in ("run", "trace")]
+    assert len(runs) > 2500 and sum(1 for c in runs if c["cmd"] == "trace" or c["trace"]) > 150
     n_exec = 0
     for c in runs:
         assert got(c, ctx) == want(c), (c["src"], c["schedule"], c["fuel"], c["raw"])
