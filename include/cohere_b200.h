@@ -386,6 +386,32 @@ typedef struct coh_cli_opts {
 int coh_cli(coh_ctx* ctx, const char* command, const char* src, const coh_cli_opts* opts,
             char* out, size_t out_cap, char* err, size_t err_cap, int* exit_code);
 
+/* ---- batched overlap registry and mode closure -----------------
+ * OverlapRegistry (overlap.hpp:33-175) and infer_overlap_closure (overlap.hpp:177-230)
+ * for many views and many blocks at once.  A view: its buffer id, inclusive absolute
+ * range, and name_rank = the position of its name in std::string order (the reference's
+ * query results and `needed` map are name-sorted; the rank decides which view an
+ * OverlapInferenceError names); its declaration order is its index.  A mode: var = view
+ * index (flags bit0 set) or scalar id, kind COH_R/W/RW, site, flags bit1 = shadow.
+ * All pointers are device memory; calls are stream-ordered. */
+typedef struct coh_view { uint32_t buffer; int32_t lo, hi; uint32_t name_rank; } coh_view;
+typedef struct coh_mode { uint32_t var; uint8_t kind, site, flags, pad; } coh_mode;
+typedef struct coh_registry coh_registry;
+/* build_registry (overlap.hpp:232-239) for n_views views (ranges must fit their buffers) */
+int coh_registry_build(coh_ctx* ctx, const coh_view* d_views, uint32_t n_views, coh_registry** out, void* stream);
+void coh_registry_destroy(coh_registry* r);
+/* query(view) (overlap.hpp:86-108) for each probe view: up to hits_stride hits written
+ * name-sorted at d_hits[q * hits_stride], the total count in d_hit_count[q]. */
+int coh_registry_query(coh_ctx* ctx, const coh_registry* r, const uint32_t* d_probes, uint32_t n_probes,
+                       uint32_t* d_hits, uint32_t hits_stride, uint32_t* d_hit_count, void* stream);
+/* infer_overlap_closure for each block b (modes d_modes[d_block_off[b] .. d_block_off[b+1])):
+ * the closed list at d_out[b * out_stride], its length in d_out_count[b], d_status[b] = -1,
+ * or d_status[b] = y for OverlapInferenceError(y), or -2 when the block exceeds the
+ * per-block limits (64 declared modes, 64 inferred views, out_stride). */
+int coh_overlap_closure(coh_ctx* ctx, const coh_registry* r, const coh_mode* d_modes, const uint32_t* d_block_off,
+                        uint32_t n_blocks, coh_mode* d_out, uint32_t out_stride, uint32_t* d_out_count,
+                        int32_t* d_status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,6 +54,10 @@ def reference():
         L.ref_call_outcome.argtypes = [u32, u32, C.POINTER(_Outcome)]
         L.ref_selfcheck.restype = C.c_int
         L.ref_selfcheck.argtypes = [vp, u64, u32, u32, i32]
+        L.ref_overlap_closure.restype = C.c_int
+        L.ref_overlap_closure.argtypes = [vp, u32, u32, vp, vp, u32, vp, u32, vp, vp]
+        L.ref_registry_query.restype = C.c_int
+        L.ref_registry_query.argtypes = [vp, u32, vp, u32, vp, u32, vp, C.c_int]
         _ref = L
     return _ref
 
