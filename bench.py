@@ -10,6 +10,7 @@ One step = one pass of the hot path over one batch: trace_eval over this rank's 
 Prints ONE JSON line on rank 0.  See DESIGN.md §6 for every field.
 """
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -45,6 +46,8 @@ def parse():
     ap.add_argument("--container-log2-floats", type=int, default=28, help="C5 vector size (0 = skip)")
     ap.add_argument("--container-calls", type=int, default=64)
     ap.add_argument("--sweep-seeds", type=int, default=100000, help="acceptance-sweep seeds (0 = skip)")
+    ap.add_argument("--overlap-views", type=int, default=1 << 20, help="overlap registry views (0 = skip)")
+    ap.add_argument("--overlap-blocks", type=int, default=1 << 20)
     return ap.parse_args()
 
 
@@ -296,6 +299,72 @@ def run_sweep(args, ctx):
             "note": "wall includes host program generation, bytecode compile and frontier management"}
 
 
+def run_overlap(args, ctx):
+    """the batched overlap registry + closure.  1M views over 4096
+    buffers of 2^20 cells (lengths up to 2^12), 1M blocks of 1-4 view modes; registry
+    build (CUB sort + max-hi tree) and closure timed with CUDA events on the stream; the
+    reference's build_registry + infer_overlap_closure timed on the host for a sample."""
+    import torch
+
+    from paper_1910_11110_b200.overlap import Registry, gen_workload_fast
+
+    nv, nb = args.overlap_views, args.overlap_blocks
+    views, modes, off = gen_workload_fast(11, 4096, 1 << 20, nv, nb, 4, 1 << 12)
+    s = torch.cuda.current_stream()
+    d_views = torch.from_numpy(views.view(np.uint8).copy()).cuda()
+    d_modes = torch.from_numpy(modes.view(np.uint8).copy()).cuda()
+    d_off = torch.from_numpy(off.view(np.int32).copy()).cuda()
+    stride = 64
+    d_out = torch.empty(nb * stride * 8, dtype=torch.uint8, device="cuda")
+    d_cnt = torch.empty(nb, dtype=torch.int32, device="cuda")
+    d_st = torch.empty(nb, dtype=torch.int32, device="cuda")
+    L = coh_lib()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    best_b = best_c = None
+    for _ in range(5):
+        h = ctypes.c_void_p()
+        e[0].record()
+        rc = L.coh_registry_build(ctx._h, d_views.data_ptr(), nv, ctypes.byref(h), s.cuda_stream)
+        e[1].record()
+        assert rc == 0
+        e[2].record()
+        rc = L.coh_overlap_closure(ctx._h, h, d_modes.data_ptr(), d_off.data_ptr(), nb, d_out.data_ptr(), stride,
+                                   d_cnt.data_ptr(), d_st.data_ptr(), s.cuda_stream)
+        e[3].record()
+        torch.cuda.synchronize()
+        assert rc == 0
+        L.coh_registry_destroy(h)
+        tb, tc = e[0].elapsed_time(e[1]), e[2].elapsed_time(e[3])
+        best_b = tb if best_b is None else min(best_b, tb)
+        best_c = tc if best_c is None else min(best_c, tc)
+    st = d_st.cpu().numpy()
+    cnt = d_cnt.cpu().numpy()
+    out = {"metric": "overlap closure blocks/s", "views": nv, "blocks": nb, "modes": int(len(modes)),
+           "registry_build_ms": best_b, "closure_ms": best_c, "blocks_per_s": nb / (best_c / 1e3),
+           "closed": int((st == -1).sum()), "conflicts": int((st >= 0).sum()), "over_limit": int((st == -2).sum()),
+           "inferred_modes": int((cnt[st == -1] - np.diff(off)[st == -1]).sum())}
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle_ffi as o
+        if o.have_ref():
+            R = o.reference()
+            sample = min(nb, 20000)
+            o_cnt = np.zeros(sample, np.uint32)
+            o_st = np.zeros(sample, np.int32)
+            o_out = np.zeros(sample * stride * 8, np.uint8)
+            t0 = time.perf_counter()
+            R.ref_overlap_closure(views.ctypes.data, nv, 0, modes.ctypes.data, off.ctypes.data, sample,
+                                  o_out.ctypes.data, stride, o_cnt.ctypes.data, o_st.ctypes.data)
+            t = time.perf_counter() - t0
+            agree = bool(np.array_equal(o_st, st[:sample]))
+            out["cpu_reference"] = {"blocks_per_s": sample / t, "sample_blocks": sample, "cores": 1,
+                                    "wall_s": t, "status_agree": agree,
+                                    "note": "includes the reference's build_registry of all views (std::multimap)"}
+    except Exception as ex:  # the reference .so is test infrastructure; its absence is not fatal here
+        out["cpu_reference"] = {"error": f"{type(ex).__name__}: {ex}"}
+    return out
+
+
 def run_c1(ctx):
     """BASELINE config 1: one trace of 1000 random calls on one array (seed 0, default
     mix), the latency case: device time of one trace_eval launch (CUDA events, best of
@@ -448,6 +517,7 @@ def run_ours(args, rank, world, local):
     clocks.stop()
     sweep_info = run_sweep(args, ctx) if (args.sweep_seeds > 0 and rank == 0) else None
     c1 = run_c1(ctx) if rank == 0 else None
+    overlap = run_overlap(args, ctx) if (args.overlap_views > 0 and rank == 0) else None
     container = None
     if args.container_log2_floats > 0 and rank == 0:
         try:
@@ -476,7 +546,7 @@ def run_ours(args, rank, world, local):
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms": k_ms,
                          "note": "INT/LSU-issue bound in practice; see profiles/ for pipe utilisation"},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "gpu_launches": launches,
-            "bitmap": bitmap, "container": container, "sweep": sweep_info, "c1": c1,
+            "bitmap": bitmap, "container": container, "sweep": sweep_info, "c1": c1, "overlap": overlap,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -119,3 +119,36 @@ def gen_workload(seed: int, n_buffers: int, buf_len: int, n_views: int, n_blocks
             modes.append((int(rng.integers(0, n_scalars)), int(rng.integers(0, 3)), int(rng.integers(0, 2)), 0, 0))
         off.append(len(modes))
     return views, np.array(modes, MODE_DTYPE), np.array(off, np.uint32)
+
+
+def gen_workload_fast(seed: int, n_buffers: int, buf_len: int, n_views: int, n_blocks: int, modes_per_block: int,
+                      max_view_len: int, p_same_site: float = 0.9):
+    """Vectorised generator for large batches (the bench): each block declares k in
+    [1, modes_per_block] distinct views of one buffer (consecutive in that buffer's view
+    list from a random start), random kinds, mostly one site."""
+    rng = np.random.default_rng(seed)
+    views = np.zeros(n_views, VIEW_DTYPE)
+    buf = np.sort(rng.integers(0, n_buffers, n_views)).astype(np.uint32)
+    views["buffer"] = buf
+    views["lo"] = rng.integers(0, buf_len, n_views)
+    views["hi"] = np.minimum(views["lo"] + rng.integers(0, max_view_len, n_views), buf_len - 1)
+    views["name_rank"] = rng.permutation(n_views)
+    start = np.searchsorted(buf, np.arange(n_buffers)).astype(np.int64)
+    count = np.bincount(buf, minlength=n_buffers).astype(np.int64)
+    nonempty = np.nonzero(count)[0]
+    b = nonempty[rng.integers(0, len(nonempty), n_blocks)]
+    k = np.minimum(rng.integers(1, modes_per_block + 1, n_blocks), count[b])
+    off = np.zeros(n_blocks + 1, np.uint32)
+    off[1:] = np.cumsum(k)
+    blk = np.repeat(np.arange(n_blocks), k)
+    j = np.arange(off[-1]) - np.repeat(off[:-1].astype(np.int64), k)
+    r0 = rng.integers(0, 1 << 30, n_blocks)
+    cb = count[b][blk]
+    modes = np.zeros(int(off[-1]), MODE_DTYPE)
+    modes["var"] = start[b][blk] + (r0[blk] + j) % cb
+    modes["kind"] = rng.integers(0, 3, len(modes))
+    site0 = rng.integers(0, 2, n_blocks)[blk]
+    flip = rng.random(len(modes)) >= p_same_site
+    modes["site"] = np.where(flip, 1 - site0, site0)
+    modes["flags"] = FLAG_VIEW
+    return views, modes, off
