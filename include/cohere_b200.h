@@ -412,6 +412,35 @@ int coh_overlap_closure(coh_ctx* ctx, const coh_registry* r, const coh_mode* d_m
                         uint32_t n_blocks, coh_mode* d_out, uint32_t out_stride, uint32_t* d_out_count,
                         int32_t* d_status, void* stream);
 
+/* ---- bit-plane primitives ---------------------------------------
+ * A plane is a run of 32-bit words in device memory (d_words 16-byte aligned); cell i of
+ * the plane starting at word `word_off` is bit i%32 of word word_off + i/32.  A range is
+ * the cells [lo, hi] (inclusive; lo > hi = empty) of one plane.  Batched over ranges, one
+ * persistent launch per call, stream-ordered.  Semantics:
+ *   range_set / range_clear  bits [lo, hi] := 1 / 0 (element writes w x[i] on a range;
+ *                            ranges may share edge words)
+ *   first_zero               d_first[k] = the first cell of range k whose bit is 0 (the
+ *                            stuck cell of a whole-view sync, semantics.hpp:155-166), or
+ *                            0xFFFFFFFF
+ *   extract_zero_runs        maximal runs of 0 bits in each range, ascending (the transfer
+ *                            ranges of a whole-view sync): run j of range k is
+ *                            [d_run_start[g], d_run_end[g]] with g = d_run_off[k] + j;
+ *                            d_run_off has n + 1 entries (its last = the total; runs beyond
+ *                            `cap` are counted but not written)
+ *   view_check               d_ok[k] = abstraction_correct of one view (modes.hpp:84-88)
+ *                            with abstract pair d_abs_pair[k] (bit0 local V, bit1 remote V)
+ *                            against planes L (local valid) and R (remote valid) */
+typedef struct coh_bitmap_range { uint64_t word_off; uint32_t lo, hi; } coh_bitmap_range;
+int coh_bitmap_range_set(coh_ctx* ctx, uint32_t* d_words, const coh_bitmap_range* d_ranges, uint32_t n, void* stream);
+int coh_bitmap_range_clear(coh_ctx* ctx, uint32_t* d_words, const coh_bitmap_range* d_ranges, uint32_t n, void* stream);
+int coh_bitmap_first_zero(coh_ctx* ctx, const uint32_t* d_words, const coh_bitmap_range* d_ranges, uint32_t n,
+                          uint32_t* d_first, void* stream);
+int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_words, const coh_bitmap_range* d_ranges, uint32_t n,
+                                 uint32_t* d_run_start, uint32_t* d_run_end, uint64_t cap, uint64_t* d_run_off,
+                                 void* stream);
+int coh_bitmap_view_check(coh_ctx* ctx, const uint32_t* d_L, const uint32_t* d_R, const coh_bitmap_range* d_ranges,
+                          const uint8_t* d_abs_pair, uint32_t n, uint8_t* d_ok, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,94 @@
+"""Bit-plane primitives against a numpy restatement of Appendix B
+(bit i of word i/32; whole-view sync stuck cell = first 0 ascending; transfer ranges =
+maximal 0-runs ascending; view check = leq of the abstract pair against every cell):
+random planes, ragged ranges sharing edge words, empty ranges, several planes per call,
+ranges up to 2^24 cells.  Bit-exact."""
+import numpy as np
+import pytest
+
+from paper_1910_11110_b200.bitmap import RANGE_DTYPE
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def bits_of(words: np.ndarray) -> np.ndarray:
+    return np.unpackbits(words.view(np.uint8), bitorder="little")
+
+
+def words_of(bits: np.ndarray) -> np.ndarray:
+    return np.packbits(bits.astype(np.uint8), bitorder="little").view(np.uint32)
+
+
+def random_planes(rng, n_planes, n_cells, density):
+    n_words = n_cells // 32
+    bits = (rng.random(n_planes * n_cells) < density).astype(np.uint8)
+    # runs: flip long stretches so runs of every length occur
+    for _ in range(n_planes * 4):
+        a = int(rng.integers(0, n_planes * n_cells))
+        bits[a: a + int(rng.integers(1, 5000))] = rng.integers(0, 2)
+    return bits, n_words
+
+
+def random_ranges(rng, n_planes, n_cells, n_words, k):
+    r = np.zeros(k, RANGE_DTYPE)
+    p = rng.integers(0, n_planes, k)
+    lo = rng.integers(0, n_cells, k)
+    hi = np.minimum(lo + rng.integers(0, n_cells, k) // rng.integers(1, 64, k), n_cells - 1)
+    r["word_off"], r["lo"], r["hi"] = p * n_words, lo, hi
+    r["lo"][:3] = [0, 5, 9]
+    r["hi"][:3] = [n_cells - 1, 4, 9]  # whole plane, empty, single cell
+    return r
+
+
+def cells(r, n_cells):
+    base = int(r["word_off"]) * 32
+    return base + int(r["lo"]), base + int(r["hi"])
+
+
+@pytest.mark.parametrize("n_cells,n_planes,k", [(1 << 12, 5, 200), (1 << 16, 3, 400), (1 << 24, 2, 40)])
+def test_first_zero_runs_view_check(ctx, n_cells, n_planes, k):
+    from paper_1910_11110_b200.bitmap import first_zero, view_check, zero_runs
+    rng = np.random.default_rng(n_cells + k)
+    bits, n_words = random_planes(rng, n_planes, n_cells, 0.97)
+    rbits, _ = random_planes(rng, n_planes, n_cells, 0.5)
+    L = torch.from_numpy(words_of(bits).view(np.int32).copy()).cuda()
+    R = torch.from_numpy(words_of(rbits).view(np.int32).copy()).cuda()
+    ranges = random_ranges(rng, n_planes, n_cells, n_words, k)
+    fz = first_zero(ctx, L, ranges)
+    off, st, en = zero_runs(ctx, L, ranges, cap=1 << 22)
+    ab = rng.integers(0, 4, k).astype(np.uint8)
+    ok = view_check(ctx, L, R, ranges, ab)
+    for j, r in enumerate(ranges):
+        a, b = cells(r, n_cells)
+        seg = bits[a: b + 1] if b >= a else bits[:0]
+        z = np.nonzero(seg == 0)[0]
+        assert fz[j] == (int(r["lo"]) + int(z[0]) if len(z) else 0xFFFFFFFF), j
+        # maximal zero runs, ascending, plane-relative cell indices
+        d = np.diff(np.concatenate([[1], seg, [1]]).astype(np.int8))
+        ws, we = np.nonzero(d == -1)[0], np.nonzero(d == 1)[0] - 1
+        o0, o1 = int(off[j]), int(off[j + 1])
+        assert o1 - o0 == len(ws), j
+        assert np.array_equal(st[o0:o1], ws + int(r["lo"])) and np.array_equal(en[o0:o1], we + int(r["lo"])), j
+        rseg = rbits[a: b + 1] if b >= a else rbits[:0]
+        want = {1: bool(seg.all()), 2: bool(rseg.all()), 3: bool(seg.all() and rseg.all()),
+                0: not bool((seg | rseg).any())}[int(ab[j])]
+        assert ok[j] == want, (j, ab[j])
+
+
+def test_range_set_clear(ctx):
+    from paper_1910_11110_b200.bitmap import range_set
+    rng = np.random.default_rng(5)
+    n_cells, n_planes = 1 << 18, 4
+    bits, n_words = random_planes(rng, n_planes, n_cells, 0.5)
+    dev = torch.from_numpy(words_of(bits).view(np.int32).copy()).cuda()
+    want = bits.copy()
+    for value in (True, False, True):
+        ranges = random_ranges(rng, n_planes, n_cells, n_words, 300)
+        range_set(ctx, dev, ranges, value)
+        for r in ranges:
+            a, b = cells(r, n_cells)
+            if b >= a:
+                want[a: b + 1] = 1 if value else 0
+        torch.cuda.synchronize()
+        assert np.array_equal(bits_of(dev.cpu().numpy().view(np.uint32)), want)
