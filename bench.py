@@ -247,6 +247,81 @@ def run_bitmap(args, ctx, rank, world):
                          "runs": sum(res[i].n_runs for i in range(B))}}
 
 
+def run_bitmap_primitives(args, ctx):
+    """SURVEY §8(b) item 2 primitives on C3-sized planes: 256 planes x 2^24 cells (512 MiB
+    per plane array, > L2), one range per plane covering a random 60-100% of it.  Each
+    primitive timed with CUDA events on the stream (best of 5); algorithmic bytes per
+    SURVEY §8(d): set/clear m/8 written, first zero m/8 read, view check 2 x m/8 read,
+    zero runs 2 x m/8 read (count + write passes) + 8 B per run."""
+    import torch
+
+    from paper_1910_11110_b200.bitmap import RANGE_DTYPE
+
+    P, n = args.bitmap_buffers, 1 << args.bitmap_log2_cells
+    words = n // 32
+    rng = np.random.default_rng(3)
+    L = torch.full((P * words,), -1, dtype=torch.int32, device="cuda")
+    Rp = torch.zeros(P * words, dtype=torch.int32, device="cuda")
+    ranges = np.zeros(P, RANGE_DTYPE)
+    ranges["word_off"] = np.arange(P) * words
+    ranges["lo"] = rng.integers(0, n // 5, P)
+    ranges["hi"] = n - 1 - rng.integers(0, n // 5, P)
+    m = int((ranges["hi"].astype(np.int64) - ranges["lo"] + 1).sum())
+    d_r = torch.from_numpy(ranges.view(np.uint8).copy()).cuda()
+    # fragment R: a sparse pattern of set cells (zero runs of ~2^12 cells)
+    frag = np.zeros(P, RANGE_DTYPE)
+    frag_r = []
+    for k in range(P):
+        for c in rng.integers(0, n - 64, 64):
+            frag_r.append((k * words, int(c), int(c) + int(rng.integers(0, 64))))
+    frag = np.array(frag_r, RANGE_DTYPE)
+    d_f = torch.from_numpy(frag.view(np.uint8).copy()).cuda()
+    Lb = coh_lib()
+    s = torch.cuda.current_stream().cuda_stream
+    assert Lb.coh_bitmap_range_set(ctx._h, Rp.data_ptr(), d_f.data_ptr(), len(frag), s) == 0
+    first = torch.empty(P, dtype=torch.int32, device="cuda")
+    ok = torch.empty(P, dtype=torch.uint8, device="cuda")
+    ab = torch.ones(P, dtype=torch.uint8, device="cuda")
+    cap = 1 << 22
+    rs = torch.empty(cap, dtype=torch.int32, device="cuda")
+    re_ = torch.empty(cap, dtype=torch.int32, device="cuda")
+    roff = torch.empty(P + 1, dtype=torch.int64, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed(fn):
+        best = None
+        for _ in range(6):
+            e0.record()
+            rc = fn()
+            e1.record()
+            torch.cuda.synchronize()
+            assert rc == 0
+            t = e0.elapsed_time(e1)
+            best = t if best is None else min(best, t)
+        return best
+
+    peak, src = peaks()
+    out = {"metric": "bit-plane primitives GB/s (algorithmic bytes / device time)", "planes": P, "cells": n,
+           "cells_in_ranges": m, "peak": peak, "peak_source": src}
+    t = timed(lambda: Lb.coh_bitmap_first_zero(ctx._h, L.data_ptr(), d_r.data_ptr(), P, first.data_ptr(), s))
+    out["first_zero"] = {"ms": t, "gbs": m / 8 / (t / 1e3) / 1e9}
+    t = timed(lambda: Lb.coh_bitmap_view_check(ctx._h, L.data_ptr(), Rp.data_ptr(), d_r.data_ptr(), ab.data_ptr(), P,
+                                               ok.data_ptr(), s))
+    out["view_check"] = {"ms": t, "gbs": 2 * m / 8 / (t / 1e3) / 1e9}
+    t = timed(lambda: Lb.coh_bitmap_extract_zero_runs(ctx._h, Rp.data_ptr(), d_r.data_ptr(), P, rs.data_ptr(),
+                                                      re_.data_ptr(), cap, roff.data_ptr(), s))
+    runs = int(roff[-1].item())
+    out["zero_runs"] = {"ms": t, "runs": runs, "gbs": (2 * m / 8 + 8 * runs) / (t / 1e3) / 1e9,
+                        "note": "includes the tile-count read-back that sizes the scan"}
+    t = timed(lambda: Lb.coh_bitmap_range_set(ctx._h, L.data_ptr(), d_r.data_ptr(), P, s))
+    out["range_set"] = {"ms": t, "gbs": m / 8 / (t / 1e3) / 1e9}
+    t = timed(lambda: Lb.coh_bitmap_range_clear(ctx._h, L.data_ptr(), d_r.data_ptr(), P, s))
+    out["range_clear"] = {"ms": t, "gbs": m / 8 / (t / 1e3) / 1e9}
+    for k in ("first_zero", "view_check", "zero_runs", "range_set", "range_clear"):
+        out[k]["frac"] = out[k]["gbs"] / peak
+    return out
+
+
 # ------------------------------------------------------------- container (C5)
 def run_container(args, ctx):
     """BASELINE config 5: 4 vectors x 2^28 float32 (1 GiB each), a seeded chain of
@@ -524,6 +599,8 @@ def run_ours(args, rank, world, local):
         for p in (p_rec, p_res, p_bnd):
             L.coh_host_free(p)
     bitmap = run_bitmap(args, ctx, rank, world) if args.bitmap_buffers > 0 else None
+    if bitmap is not None and rank == 0:
+        bitmap["primitives"] = run_bitmap_primitives(args, ctx)
     clocks.stop()
     sweep_info = run_sweep(args, ctx) if (args.sweep_seeds > 0 and rank == 0) else None
     c1 = run_c1(ctx) if rank == 0 else None

@@ -76,15 +76,6 @@ __device__ __forceinline__ TileGeom geom(const Tiles& T, uint64_t tile) {
   return g;
 }
 
-__global__ void k_tile_counts(const coh_bitmap_range* r, uint32_t n, uint64_t* tiles) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    const uint64_t q0 = (r[i].word_off + (r[i].lo >> 5)) >> 2, q1 = (r[i].word_off + (r[i].hi >> 5)) >> 2;
-    tiles[i] = r[i].lo <= r[i].hi ? (q1 - q0 + kTileQuads) / kTileQuads : 0;
-  }
-  if (i == n) tiles[n] = 0;
-}
-
 template <bool SET>
 __global__ void __launch_bounds__(kBT) k_range_set(uint32_t* words, Tiles T) {
   const uint64_t n_tiles = T.prefix[T.n];
@@ -326,16 +317,50 @@ struct Scratch {
 
 int grid_for(coh_ctx* ctx) { return ctx->sms * 8; }
 
-// Tile prefix for the ranges: tiles[n + 1] (exclusive scan of per-range tile counts).
+// Tile prefix for the ranges: prefix[n + 1] (exclusive scan of per-range tile counts), one
+// single-block launch (a running carry over chunks of 1024 ranges).
+__global__ void __launch_bounds__(1024) k_tile_prefix(const coh_bitmap_range* r, uint32_t n, uint64_t* prefix) {
+  __shared__ uint64_t warp_sum[32];
+  __shared__ uint64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t base = 0; base <= n; base += 1024) {
+    const uint32_t i = base + threadIdx.x;
+    uint64_t v = 0;
+    if (i < n) {
+      const uint64_t q0 = (r[i].word_off + (r[i].lo >> 5)) >> 2, q1 = (r[i].word_off + (r[i].hi >> 5)) >> 2;
+      v = r[i].lo <= r[i].hi ? (q1 - q0 + kTileQuads) / kTileQuads : 0;
+    }
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) warp_sum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t w = warp_sum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+        if (lane >= (uint32_t)o) w += y;
+      }
+      warp_sum[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const uint64_t excl = carry + (warp ? warp_sum[warp - 1] : 0) + x - v;
+    if (i <= n) prefix[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_sum[31];
+    __syncthreads();
+  }
+}
+
 int tile_prefix(coh_ctx* ctx, const coh_bitmap_range* d_r, uint32_t n, uint64_t* d_prefix, cudaStream_t s) {
-  k_tile_counts<<<(n + 1 + 255) / 256, 256, 0, s>>>(d_r, n, d_prefix);
-  size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, d_prefix, d_prefix, (int)n + 1, s);
-  Scratch t;
-  t.s = s;
-  if (cudaMallocAsync(&t.p, tmp, s) != cudaSuccess) return COH_E_CUDA;
-  cub::DeviceScan::ExclusiveSum(t.p, tmp, d_prefix, d_prefix, (int)n + 1, s);
-  ctx->launches += 2;
+  k_tile_prefix<<<1, 1024, 0, s>>>(d_r, n, d_prefix);
+  ctx->launches += 1;
   return cudaGetLastError() == cudaSuccess ? COH_OK : COH_E_CUDA;
 }
 
