@@ -115,6 +115,12 @@ int coh_ctx_create(int device, coh_ctx** out) {
     if ((e = cudaMemcpy(ctx->d_lut, table.lut, sizeof table.lut, cudaMemcpyHostToDevice)) != cudaSuccess) break;
     if ((e = cudaMemcpy(ctx->d_slow, table.slow, sizeof table.slow, cudaMemcpyHostToDevice)) != cudaSuccess) break;
     if ((e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess) break;
+    {  // stream-ordered scratch (cudaMallocAsync) stays in the pool instead of being unmapped at every sync
+      cudaMemPool_t pool;
+      uint64_t keep = ~0ull;
+      if ((e = cudaDeviceGetDefaultMemPool(&pool, device)) != cudaSuccess) break;
+      if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess) break;
+    }
     cohb::trace_eval_set_smem_attr();
     int tpb = 0;
     std::string err;
