@@ -75,25 +75,74 @@ __device__ __forceinline__ void warp_chunk(uint64_t Q, uint64_t& f0, uint64_t& f
 }
 
 // Walks this lane's quads of the warp chunk (lane + 32 j), kU steps per iteration so the
-// loads of several steps are in flight.  body(r, R, qa) for each valid quad.
+// loads of several steps are in flight.  body(r, R, qa, interior) for each valid quad;
+// interior = neither the first nor the last quad of its range, i.e. all four words lie
+// wholly inside [lo, hi] (the fast path: no masks).
 template <class Body>
 __device__ __forceinline__ void walk(const Flat& F, uint64_t f0, uint64_t f1, Body&& body) {
   const uint32_t lane = threadIdx.x & 31;
   if (f0 >= f1) return;
   uint32_t r = find_range(F, f0 + lane < f1 ? f0 + lane : f1 - 1);
-  uint64_t next = F.qp[r + 1];
+  uint64_t qbeg = F.qp[r], qend = F.qp[r + 1];
+  coh_bitmap_range R = F.r[r];
+  uint64_t qa0 = qa_first(R) - qbeg;
   for (uint64_t base = f0; base < f1; base += 32ull * kU) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const uint64_t f = base + 32ull * u + lane;
       if (f >= f1) break;
-      while (f >= next) {  // monotone advance (empty ranges skipped)
-        ++r;
-        next = F.qp[r + 1];
+      if (f >= qend) {  // monotone advance (empty ranges skipped)
+        do {
+          ++r;
+          qbeg = qend;
+          qend = F.qp[r + 1];
+        } while (f >= qend);
+        R = F.r[r];
+        qa0 = qa_first(R) - qbeg;
       }
-      const coh_bitmap_range R = F.r[r];
-      body(r, R, qa_first(R) + (f - F.qp[r]));
+      body(r, R, qa0 + f, f != qbeg && f + 1 != qend);
     }
+  }
+}
+
+// walk() for reading kernels: the kU quads of an iteration are located and their 16-byte
+// words (from NP planes) loaded first, then processed, so all kU x NP loads are in flight
+// together.  body(r, qa, interior, v[NP]); edge quads re-read their range record (L1 hit).
+template <int NP, class Body>
+__device__ __forceinline__ void walk_pf(const Flat& F, uint64_t f0, uint64_t f1, const uint32_t* const (&planes)[NP],
+                                        Body&& body) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (f0 >= f1) return;
+  uint32_t r = find_range(F, f0 + lane < f1 ? f0 + lane : f1 - 1);
+  uint64_t qbeg = F.qp[r], qend = F.qp[r + 1];
+  uint64_t qa0 = qa_first(F.r[r]) - qbeg;
+  for (uint64_t base = f0; base < f1; base += 32ull * kU) {
+    uint32_t rr[kU];
+    uint64_t qa[kU];
+    bool in[kU], ok[kU];
+    uint4 v[kU][NP];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t f = base + 32ull * u + lane;
+      ok[u] = f < f1;
+      if (ok[u] && f >= qend) {
+        do {
+          ++r;
+          qbeg = qend;
+          qend = F.qp[r + 1];
+        } while (f >= qend);
+        qa0 = qa_first(F.r[r]) - qbeg;
+      }
+      rr[u] = r;
+      qa[u] = qa0 + f;
+      in[u] = f != qbeg && f + 1 != qend;
+#pragma unroll
+      for (int p = 0; p < NP; ++p)
+        v[u][p] = ok[u] ? __ldcs(reinterpret_cast<const uint4*>(planes[p]) + qa[u]) : make_uint4(~0u, ~0u, ~0u, ~0u);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (ok[u]) body(rr[u], qa[u], in[u], v[u]);
   }
 }
 
@@ -136,7 +185,12 @@ template <bool SET>
 __global__ void __launch_bounds__(kBT) k_range_set(uint32_t* words, Flat F) {
   uint64_t f0, f1, wid;
   warp_chunk(F.qp[F.n], f0, f1, wid);
-  walk(F, f0, f1, [&](uint32_t, const coh_bitmap_range& R, uint64_t qa) {
+  walk(F, f0, f1, [&](uint32_t, const coh_bitmap_range& R, uint64_t qa, bool interior) {
+    if (interior) {
+      const uint32_t v = SET ? 0xFFFFFFFFu : 0u;
+      __stcs(reinterpret_cast<uint4*>(words) + qa, make_uint4(v, v, v, v));
+      return;
+    }
     uint32_t m[4];
     bool full = true;
 #pragma unroll
@@ -196,8 +250,11 @@ __global__ void __launch_bounds__(kBT) k_first_zero(const uint32_t* words, Flat 
   warp_chunk(F.qp[F.n], f0, f1, wid);
   Acc<0> acc;
   acc.out = first;
-  walk(F, f0, f1, [&](uint32_t r, const coh_bitmap_range& R, uint64_t qa) {
-    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(words) + qa);
+  const uint32_t* const planes[1] = {words};
+  walk_pf<1>(F, f0, f1, planes, [&](uint32_t r, uint64_t qa, bool interior, const uint4 (&vv)[1]) {
+    const uint4 v = vv[0];
+    if (interior && (v.x & v.y & v.z & v.w) == 0xFFFFFFFFu) return;  // no zero: nothing to record
+    const coh_bitmap_range R = F.r[r];
     const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
     uint32_t best = kNone;
 #pragma unroll
@@ -216,8 +273,16 @@ __global__ void __launch_bounds__(kBT) k_view_flags(const uint32_t* L, const uin
   warp_chunk(F.qp[F.n], f0, f1, wid);
   Acc<1> acc;
   acc.out = flags;
-  walk(F, f0, f1, [&](uint32_t r, const coh_bitmap_range& R, uint64_t qa) {
-    const uint4 a = __ldcs(reinterpret_cast<const uint4*>(L) + qa), b = __ldcs(reinterpret_cast<const uint4*>(Rp) + qa);
+  const uint32_t* const planes[2] = {L, Rp};
+  walk_pf<2>(F, f0, f1, planes, [&](uint32_t r, uint64_t qa, bool interior, const uint4 (&v)[2]) {
+    const uint4 a = v[0], b = v[1];
+    if (interior) {  // whole words: AND / OR folds
+      const uint32_t land = a.x & a.y & a.z & a.w, rand_ = b.x & b.y & b.z & b.w;
+      const uint32_t lor = a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w;
+      acc.add(r, (~land ? 1u : 0u) | (~rand_ ? 2u : 0u) | (lor ? 4u : 0u));
+      return;
+    }
+    const coh_bitmap_range R = F.r[r];
     const uint32_t la[4] = {a.x, a.y, a.z, a.w}, ra[4] = {b.x, b.y, b.z, b.w};
     uint32_t f = 0;  // bit0 some L == 0, bit1 some R == 0, bit2 some L | R == 1
 #pragma unroll
@@ -238,19 +303,24 @@ __global__ void k_view_finish(const uint32_t* flags, const uint8_t* abs_pair, ui
   ok[i] = a == 1u ? L1 : a == 2u ? R1 : a == 3u ? (L1 && R1) : none;
 }
 
-// Run starts / ends of one quad: a start is a 0 cell whose predecessor (in the range) is
-// not 0, an end a 0 cell whose successor is not 0.
-__device__ __forceinline__ void quad_runs(const uint32_t* words, const coh_bitmap_range& R, uint64_t qa,
-                                          uint32_t st[4], uint32_t en[4]) {
-  const uint4 v = __ldcs(reinterpret_cast<const uint4*>(words) + qa);
-  const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-  const uint64_t wr0 = qa * 4 - R.word_off;  // plane-relative word of w4[0] (may wrap: masks are 0)
-  const uint32_t mp = cell_mask(wr0 - 1, R.lo, R.hi), mn = cell_mask(wr0 + 4, R.lo, R.hi);
-  const uint32_t zp = mp ? (~__ldg(words + qa * 4 - 1) & mp) : 0u;
-  const uint32_t zn = mn ? (~__ldg(words + qa * 4 + 4) & mn) : 0u;
-  uint32_t z[4];
+// Run starts / ends of one quad, given the plane words just before and after it: a start
+// is a 0 cell whose predecessor (in the range) is not 0, an end a 0 cell whose successor is
+// not 0.  Interior quads (neither first nor last of their range) need no masks.
+__device__ __forceinline__ void runs_of(const coh_bitmap_range* Rp, uint64_t qa, bool interior, const uint4 v,
+                                        uint32_t pw, uint32_t nw, uint32_t st[4], uint32_t en[4]) {
+  uint32_t z[4], zp, zn;
+  if (interior) {
+    z[0] = ~v.x, z[1] = ~v.y, z[2] = ~v.z, z[3] = ~v.w;
+    zp = ~pw, zn = ~nw;
+  } else {
+    const coh_bitmap_range R = *Rp;
+    const uint64_t wr0 = qa * 4 - R.word_off;  // plane-relative word of v.x (may wrap: masks are 0)
+    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-  for (int k = 0; k < 4; ++k) z[k] = ~w4[k] & cell_mask(wr0 + k, R.lo, R.hi);
+    for (int k = 0; k < 4; ++k) z[k] = ~w4[k] & cell_mask(wr0 + k, R.lo, R.hi);
+    zp = ~pw & cell_mask(wr0 - 1, R.lo, R.hi);
+    zn = ~nw & cell_mask(wr0 + 4, R.lo, R.hi);
+  }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const uint32_t prev = k ? z[k - 1] : zp, next = k < 3 ? z[k + 1] : zn;
@@ -259,88 +329,116 @@ __device__ __forceinline__ void quad_runs(const uint32_t* words, const coh_bitma
   }
 }
 
-// Per warp chunk: run starts and run ends (a run may start in one chunk and end in a later
-// one, so the two counts differ).
-__global__ void __launch_bounds__(kBT) k_runs_count(const uint32_t* words, Flat F, uint64_t* chunk_starts,
-                                                    uint64_t* chunk_ends) {
-  uint64_t f0, f1, wid;
-  warp_chunk(F.qp[F.n], f0, f1, wid);
-  uint32_t cs = 0, ce = 0;
-  walk(F, f0, f1, [&](uint32_t, const coh_bitmap_range& R, uint64_t qa) {
-    uint32_t st[4], en[4];
-    quad_runs(words, R, qa, st, en);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      cs += __popc(st[k]);
-      ce += __popc(en[k]);
-    }
-  });
-  cs = __reduce_add_sync(0xFFFFFFFFu, cs);
-  ce = __reduce_add_sync(0xFFFFFFFFu, ce);
-  if ((threadIdx.x & 31) == 0) {
-    chunk_starts[wid] = cs;
-    chunk_ends[wid] = ce;
-  }
-}
-
-__global__ void __launch_bounds__(kBT) k_runs_write(const uint32_t* words, Flat F, const uint64_t* chunk_off,
-                                                    const uint64_t* chunk_end_off, uint32_t* run_start,
-                                                    uint32_t* run_end, uint64_t cap, uint64_t* run_off) {
+// Both run passes.  WRITE = false: per warp chunk, the number of run starts and ends
+// (a run may start in one chunk and end in a later one).  WRITE = true: every start / end
+// at its global ascending position (chunk prefix + warp scan per step), and run_off for
+// the ranges whose first quad is here.  Neighbour words come from the adjacent lanes by
+// shuffle; only the chunk / iteration edges load them.
+template <bool WRITE>
+__global__ void __launch_bounds__(kBT, 4) k_runs(const uint32_t* words, Flat F, uint64_t* chunk_s, uint64_t* chunk_e,
+                                              uint32_t* run_start, uint32_t* run_end, uint64_t cap, uint64_t* run_off) {
   uint64_t f0, f1, wid;
   warp_chunk(F.qp[F.n], f0, f1, wid);
   const uint32_t lane = threadIdx.x & 31;
-  if (f0 >= f1) return;
-  uint64_t gs = chunk_off[wid], ge = chunk_end_off[wid];  // starts / ends before this warp step
+  if (f0 >= f1) {
+    if (!WRITE && lane == 0) chunk_s[wid] = chunk_e[wid] = 0;
+    return;
+  }
+  uint64_t gs = WRITE ? chunk_s[wid] : 0, ge = WRITE ? chunk_e[wid] : 0;
+  uint32_t cs = 0, ce = 0;
   uint32_t r = find_range(F, f0 + lane < f1 ? f0 + lane : f1 - 1);
-  uint64_t next = F.qp[r + 1];
-  for (uint64_t step = f0; step < f1; step += 32) {  // one warp step per iteration
-    const uint64_t f = step + lane;
-    const bool on = f < f1;
-    uint32_t st[4] = {0, 0, 0, 0}, en[4] = {0, 0, 0, 0};
-    coh_bitmap_range R{};
-    uint64_t qa = 0;
-    if (on) {
-      while (f >= next) {
-        ++r;
-        next = F.qp[r + 1];
-      }
-      R = F.r[r];
-      qa = qa_first(R) + (f - F.qp[r]);
-      quad_runs(words, R, qa, st, en);
-    }
-    const uint32_t ns = __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
-    const uint32_t ne = __popc(en[0]) + __popc(en[1]) + __popc(en[2]) + __popc(en[3]);
-    uint32_t ps = ns, pe = ne;  // inclusive warp scans
+  uint64_t qbeg = F.qp[r], qend = F.qp[r + 1];
+  uint64_t qa0 = qa_first(F.r[r]) - qbeg;
+  uint32_t carry = 0;
+  bool carry_ok = false;
+  for (uint64_t base = f0; base < f1; base += 32ull * kU) {
+    uint32_t rr[kU];
+    uint64_t qa[kU], ff[kU], qb[kU], qe[kU];
+    bool ok[kU];
+    uint4 v[kU];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, ps, o), b = __shfl_up_sync(0xFFFFFFFFu, pe, o);
-      if (lane >= (uint32_t)o) {
-        ps += a;
-        pe += b;
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t f = base + 32ull * u + lane;
+      ok[u] = f < f1;
+      if (ok[u] && f >= qend) {
+        do {
+          ++r;
+          qbeg = qend;
+          qend = F.qp[r + 1];
+        } while (f >= qend);
+        qa0 = qa_first(F.r[r]) - qbeg;
       }
+      rr[u] = r, qa[u] = qa0 + f, ff[u] = f, qb[u] = qbeg, qe[u] = qend;
+      v[u] = ok[u] ? __ldcs(reinterpret_cast<const uint4*>(words) + qa[u]) : make_uint4(~0u, ~0u, ~0u, ~0u);
     }
-    uint64_t s = gs + ps - ns, e = ge + pe - ne;
-    if (on && f == F.qp[r])  // the first quad of range r (and of the empty ranges just before it)
-      for (int64_t q = r; q >= 0 && F.qp[q] == f; --q) run_off[q] = s;
-    if (on) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint64_t cell0 = (qa * 4 + k - R.word_off) * 32;
-        uint32_t a = st[k], b = en[k];
-        while (a) {
-          if (s < cap) run_start[s] = (uint32_t)(cell0 + __ffs(a) - 1);
-          ++s;
-          a &= a - 1;
-        }
-        while (b) {
-          if (e < cap) run_end[e] = (uint32_t)(cell0 + __ffs(b) - 1);
-          ++e;
-          b &= b - 1;
+    for (int u = 0; u < kU; ++u) {
+      uint32_t pw = __shfl_up_sync(0xFFFFFFFFu, v[u].w, 1);
+      uint32_t nw = __shfl_down_sync(0xFFFFFFFFu, v[u].x, 1);
+      const uint32_t pw0 = u ? __shfl_sync(0xFFFFFFFFu, v[u ? u - 1 : 0].w, 31) : carry;
+      const uint32_t nw31 = u < kU - 1 ? __shfl_sync(0xFFFFFFFFu, v[u < kU - 1 ? u + 1 : 0].x, 0) : 0u;
+      if (lane == 0) pw = pw0;
+      if (lane == 31) nw = nw31;
+      const uint64_t f = ff[u];
+      const bool in = ok[u] && f != qb[u] && f + 1 != qe[u];
+      if (ok[u]) {  // neighbours the shuffles could not supply (same range only; else masked)
+        if (lane == 0 && u == 0 && !carry_ok && f != qb[u]) pw = __ldg(words + qa[u] * 4 - 1);
+        if (((lane == 31 && u == kU - 1) || f + 1 >= f1) && f + 1 != qe[u]) nw = __ldg(words + qa[u] * 4 + 4);
+      }
+      uint32_t st[4] = {0, 0, 0, 0}, en[4] = {0, 0, 0, 0};
+      if (ok[u] && !(in && (v[u].x & v[u].y & v[u].z & v[u].w) == 0xFFFFFFFFu))
+        runs_of(F.r + rr[u], qa[u], in, v[u], pw, nw, st, en);
+      const uint32_t ns = __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
+      const uint32_t ne = __popc(en[0]) + __popc(en[1]) + __popc(en[2]) + __popc(en[3]);
+      if (!WRITE) {
+        cs += ns, ce += ne;
+        continue;
+      }
+      const bool first_q = ok[u] && f == qb[u];
+      if (!__any_sync(0xFFFFFFFFu, ns || ne || first_q)) continue;  // nothing to place in this step
+      uint32_t ps = ns, pe = ne;  // inclusive warp scans
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, ps, o), b = __shfl_up_sync(0xFFFFFFFFu, pe, o);
+        if (lane >= (uint32_t)o) {
+          ps += a;
+          pe += b;
         }
       }
+      uint64_t s = gs + ps - ns, e = ge + pe - ne;
+      if (first_q)  // the first quad of range r (and of the empty ranges just before it)
+        for (int64_t q = rr[u]; q >= 0 && F.qp[q] == f; --q) run_off[q] = s;
+      if (ns | ne) {
+        const uint64_t wbase = qa[u] * 4 - F.r[rr[u]].word_off;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t cell0 = (wbase + k) * 32;
+          uint32_t a = st[k], b = en[k];
+          while (a) {
+            if (s < cap) run_start[s] = (uint32_t)(cell0 + __ffs(a) - 1);
+            ++s;
+            a &= a - 1;
+          }
+          while (b) {
+            if (e < cap) run_end[e] = (uint32_t)(cell0 + __ffs(b) - 1);
+            ++e;
+            b &= b - 1;
+          }
+        }
+      }
+      gs += __shfl_sync(0xFFFFFFFFu, ps, 31);
+      ge += __shfl_sync(0xFFFFFFFFu, pe, 31);
     }
-    gs += __shfl_sync(0xFFFFFFFFu, ps, 31);
-    ge += __shfl_sync(0xFFFFFFFFu, pe, 31);
+    carry = __shfl_sync(0xFFFFFFFFu, v[kU - 1].w, 31);
+    carry_ok = true;
+  }
+  if (!WRITE) {
+    cs = __reduce_add_sync(0xFFFFFFFFu, cs);
+    ce = __reduce_add_sync(0xFFFFFFFFu, ce);
+    if (lane == 0) {
+      chunk_s[wid] = cs;
+      chunk_e[wid] = ce;
+    }
   }
 }
 
@@ -455,7 +553,7 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   uint64_t* chunk_e = chunk + n_chunks + 1;
   if ((e = cudaMemsetAsync(chunk, 0, sizeof(uint64_t) * 2 * (n_chunks + 1), s)) != cudaSuccess)
     return fail(ctx, "zero_runs init", e);
-  k_runs_count<<<grid_for(ctx), kBT, 0, s>>>(d_words, F, chunk, chunk_e);
+  k_runs<false><<<grid_for(ctx), kBT, 0, s>>>(d_words, F, chunk, chunk_e, nullptr, nullptr, 0, nullptr);
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, chunk, chunk, (int)(n_chunks + 1), s);
   Scratch sc;
@@ -463,7 +561,7 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   if ((e = cudaMallocAsync(&sc.p, tmp, s)) != cudaSuccess) return fail(ctx, "zero_runs scan scratch", e);
   cub::DeviceScan::ExclusiveSum(sc.p, tmp, chunk, chunk, (int)(n_chunks + 1), s);
   cub::DeviceScan::ExclusiveSum(sc.p, tmp, chunk_e, chunk_e, (int)(n_chunks + 1), s);
-  k_runs_write<<<grid_for(ctx), kBT, 0, s>>>(d_words, F, chunk, chunk_e, d_run_start, d_run_end, cap, d_run_off);
+  k_runs<true><<<grid_for(ctx), kBT, 0, s>>>(d_words, F, chunk, chunk_e, d_run_start, d_run_end, cap, d_run_off);
   k_run_off_tail<<<(n + 1 + 255) / 256, 256, 0, s>>>(F.qp, chunk, n_chunks, n, d_run_off);
   ctx->launches += 5;
   return check(ctx, "zero_runs");
