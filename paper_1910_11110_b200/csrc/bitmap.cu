@@ -17,10 +17,10 @@
 // 512-byte access), four steps in flight; a lane finds its range once by binary search and
 // then only advances.  Per-range results (first zero, view flags) accumulate in registers
 // and are flushed with one atomic when the range changes (warp-reduced when the whole warp
-// agrees), so the loop has no barriers and stays HBM-bound.  Zero runs: a count pass per
-// warp chunk, a CUB scan over chunks, and a write pass that places each run start / end at
-// its global ascending position (the k-th start and the k-th end are the same run: runs
-// never cross ranges).
+// agrees), so the loop has no barriers and stays HBM-bound.  Zero runs: one pass with a
+// decoupled look-back over warp chunks (count -> publish -> prefix from the predecessors ->
+// re-walk the chunk from L2 and place each start / end at its global ascending position;
+// the k-th start and the k-th end are the same run: runs never cross ranges).
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
@@ -44,6 +44,11 @@ struct Flat {
 
 __device__ __forceinline__ uint64_t qa_first(const coh_bitmap_range& R) { return (R.word_off + (R.lo >> 5)) >> 2; }
 __device__ __forceinline__ uint64_t qa_last(const coh_bitmap_range& R) { return (R.word_off + (R.hi >> 5)) >> 2; }
+// The flat space gives every range whole 128-byte lines (8 quads): a warp step of 32 quads
+// then writes / reads exactly four full lines, so no L2 sector is ever half-written by two
+// different steps (which costs a DRAM read-fill).  The padding quads are never touched.
+__device__ __forceinline__ uint64_t qa_base(const coh_bitmap_range& R) { return qa_first(R) & ~7ull; }
+__device__ __forceinline__ uint64_t qa_end(const coh_bitmap_range& R) { return qa_last(R) | 7ull; }
 
 // Mask of the cells of plane-relative word w inside [lo, hi].
 __device__ __forceinline__ uint32_t cell_mask(uint64_t w, uint32_t lo, uint32_t hi) {
@@ -85,7 +90,7 @@ __device__ __forceinline__ void walk(const Flat& F, uint64_t f0, uint64_t f1, Bo
   uint32_t r = find_range(F, f0 + lane < f1 ? f0 + lane : f1 - 1);
   uint64_t qbeg = F.qp[r], qend = F.qp[r + 1];
   coh_bitmap_range R = F.r[r];
-  uint64_t qa0 = qa_first(R) - qbeg;
+  uint64_t qa0 = qa_base(R) - qbeg, qtf = qa_first(R), qtl = qa_last(R);
   for (uint64_t base = f0; base < f1; base += 32ull * kU) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -98,9 +103,10 @@ __device__ __forceinline__ void walk(const Flat& F, uint64_t f0, uint64_t f1, Bo
           qend = F.qp[r + 1];
         } while (f >= qend);
         R = F.r[r];
-        qa0 = qa_first(R) - qbeg;
+        qa0 = qa_base(R) - qbeg, qtf = qa_first(R), qtl = qa_last(R);
       }
-      body(r, R, qa0 + f, f != qbeg && f + 1 != qend);
+      const uint64_t qa = qa0 + f;
+      if (qa >= qtf && qa <= qtl) body(r, R, qa, qa != qtf && qa != qtl);
     }
   }
 }
@@ -115,7 +121,8 @@ __device__ __forceinline__ void walk_pf(const Flat& F, uint64_t f0, uint64_t f1,
   if (f0 >= f1) return;
   uint32_t r = find_range(F, f0 + lane < f1 ? f0 + lane : f1 - 1);
   uint64_t qbeg = F.qp[r], qend = F.qp[r + 1];
-  uint64_t qa0 = qa_first(F.r[r]) - qbeg;
+  coh_bitmap_range R0 = F.r[r];
+  uint64_t qa0 = qa_base(R0) - qbeg, qtf = qa_first(R0), qtl = qa_last(R0);
   for (uint64_t base = f0; base < f1; base += 32ull * kU) {
     uint32_t rr[kU];
     uint64_t qa[kU];
@@ -124,18 +131,20 @@ __device__ __forceinline__ void walk_pf(const Flat& F, uint64_t f0, uint64_t f1,
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const uint64_t f = base + 32ull * u + lane;
-      ok[u] = f < f1;
-      if (ok[u] && f >= qend) {
+      bool live = f < f1;
+      if (live && f >= qend) {
         do {
           ++r;
           qbeg = qend;
           qend = F.qp[r + 1];
         } while (f >= qend);
-        qa0 = qa_first(F.r[r]) - qbeg;
+        const coh_bitmap_range R = F.r[r];
+        qa0 = qa_base(R) - qbeg, qtf = qa_first(R), qtl = qa_last(R);
       }
       rr[u] = r;
       qa[u] = qa0 + f;
-      in[u] = f != qbeg && f + 1 != qend;
+      ok[u] = live && qa[u] >= qtf && qa[u] <= qtl;
+      in[u] = qa[u] != qtf && qa[u] != qtl;
 #pragma unroll
       for (int p = 0; p < NP; ++p)
         v[u][p] = ok[u] ? __ldcs(reinterpret_cast<const uint4*>(planes[p]) + qa[u]) : make_uint4(~0u, ~0u, ~0u, ~0u);
@@ -155,7 +164,7 @@ __global__ void __launch_bounds__(1024) k_quad_prefix(const coh_bitmap_range* r,
   for (uint32_t base = 0; base <= n; base += 1024) {
     const uint32_t i = base + threadIdx.x;
     uint64_t v = 0;
-    if (i < n && r[i].lo <= r[i].hi) v = qa_last(r[i]) - qa_first(r[i]) + 1;
+    if (i < n && r[i].lo <= r[i].hi) v = qa_end(r[i]) - qa_base(r[i]) + 1;
     uint64_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -188,7 +197,7 @@ __global__ void __launch_bounds__(kBT) k_range_set(uint32_t* words, Flat F) {
   walk(F, f0, f1, [&](uint32_t, const coh_bitmap_range& R, uint64_t qa, bool interior) {
     if (interior) {
       const uint32_t v = SET ? 0xFFFFFFFFu : 0u;
-      __stcs(reinterpret_cast<uint4*>(words) + qa, make_uint4(v, v, v, v));
+      reinterpret_cast<uint4*>(words)[qa] = make_uint4(v, v, v, v);
       return;
     }
     uint32_t m[4];
@@ -200,7 +209,7 @@ __global__ void __launch_bounds__(kBT) k_range_set(uint32_t* words, Flat F) {
     }
     if (full) {
       const uint32_t v = SET ? 0xFFFFFFFFu : 0u;
-      __stcs(reinterpret_cast<uint4*>(words) + qa, make_uint4(v, v, v, v));
+      reinterpret_cast<uint4*>(words)[qa] = make_uint4(v, v, v, v);
       return;
     }
 #pragma unroll
@@ -310,6 +319,12 @@ __device__ __forceinline__ void runs_of(const coh_bitmap_range* Rp, uint64_t qa,
                                         uint32_t pw, uint32_t nw, uint32_t st[4], uint32_t en[4]) {
   uint32_t z[4], zp, zn;
   if (interior) {
+    if ((v.x | v.y | v.z | v.w) == 0u) {  // all 0: a start iff the cell before is set, an end iff the one after
+      st[0] = pw >> 31;
+      en[3] = (nw & 1u) << 31;
+      st[1] = st[2] = st[3] = en[0] = en[1] = en[2] = 0u;
+      return;
+    }
     z[0] = ~v.x, z[1] = ~v.y, z[2] = ~v.z, z[3] = ~v.w;
     zp = ~pw, zn = ~nw;
   } else {
@@ -329,47 +344,42 @@ __device__ __forceinline__ void runs_of(const coh_bitmap_range* Rp, uint64_t qa,
   }
 }
 
-// Both run passes.  WRITE = false: per warp chunk, the number of run starts and ends
-// (a run may start in one chunk and end in a later one).  WRITE = true: every start / end
-// at its global ascending position (chunk prefix + warp scan per step), and run_off for
-// the ranges whose first quad is here.  Neighbour words come from the adjacent lanes by
-// shuffle; only the chunk / iteration edges load them.
-template <bool WRITE>
-__global__ void __launch_bounds__(kBT, 4) k_runs(const uint32_t* words, Flat F, uint64_t* chunk_s, uint64_t* chunk_e,
-                                              uint32_t* run_start, uint32_t* run_end, uint64_t cap, uint64_t* run_off) {
-  uint64_t f0, f1, wid;
-  warp_chunk(F.qp[F.n], f0, f1, wid);
+// Walks the warp chunk [f0, f1) in steps of 32 quads (kU steps' loads in flight) and calls
+// visit(u, ok, f, r, qa, qbeg, st, en) warp-synchronously for every step (all lanes, ok =
+// the lane has a quad).  Neighbour words come from the adjacent lanes by shuffle; only the
+// chunk / iteration edges load them.
+template <class Visit>
+__device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F, uint64_t f0, uint64_t f1,
+                                           Visit&& visit) {
   const uint32_t lane = threadIdx.x & 31;
-  if (f0 >= f1) {
-    if (!WRITE && lane == 0) chunk_s[wid] = chunk_e[wid] = 0;
-    return;
-  }
-  uint64_t gs = WRITE ? chunk_s[wid] : 0, ge = WRITE ? chunk_e[wid] : 0;
-  uint32_t cs = 0, ce = 0;
   uint32_t r = find_range(F, f0 + lane < f1 ? f0 + lane : f1 - 1);
   uint64_t qbeg = F.qp[r], qend = F.qp[r + 1];
-  uint64_t qa0 = qa_first(F.r[r]) - qbeg;
+  coh_bitmap_range R0 = F.r[r];
+  uint64_t qa0 = qa_base(R0) - qbeg, qtf = qa_first(R0), qtl = qa_last(R0);
   uint32_t carry = 0;
   bool carry_ok = false;
   for (uint64_t base = f0; base < f1; base += 32ull * kU) {
     uint32_t rr[kU];
-    uint64_t qa[kU], ff[kU], qb[kU], qe[kU];
-    bool ok[kU];
+    uint64_t qa[kU], tf[kU], tl[kU];
+    bool ok[kU], at_start[kU];
     uint4 v[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const uint64_t f = base + 32ull * u + lane;
-      ok[u] = f < f1;
-      if (ok[u] && f >= qend) {
+      const bool live = f < f1;
+      if (live && f >= qend) {
         do {
           ++r;
           qbeg = qend;
           qend = F.qp[r + 1];
         } while (f >= qend);
-        qa0 = qa_first(F.r[r]) - qbeg;
+        const coh_bitmap_range R = F.r[r];
+        qa0 = qa_base(R) - qbeg, qtf = qa_first(R), qtl = qa_last(R);
       }
-      rr[u] = r, qa[u] = qa0 + f, ff[u] = f, qb[u] = qbeg, qe[u] = qend;
-      v[u] = ok[u] ? __ldcs(reinterpret_cast<const uint4*>(words) + qa[u]) : make_uint4(~0u, ~0u, ~0u, ~0u);
+      rr[u] = r, qa[u] = qa0 + f, tf[u] = qtf, tl[u] = qtl;
+      ok[u] = live && qa[u] >= qtf && qa[u] <= qtl;
+      at_start[u] = live && f == qbeg;
+      v[u] = ok[u] ? __ldcg(reinterpret_cast<const uint4*>(words) + qa[u]) : make_uint4(~0u, ~0u, ~0u, ~0u);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -379,73 +389,150 @@ __global__ void __launch_bounds__(kBT, 4) k_runs(const uint32_t* words, Flat F, 
       const uint32_t nw31 = u < kU - 1 ? __shfl_sync(0xFFFFFFFFu, v[u < kU - 1 ? u + 1 : 0].x, 0) : 0u;
       if (lane == 0) pw = pw0;
       if (lane == 31) nw = nw31;
-      const uint64_t f = ff[u];
-      const bool in = ok[u] && f != qb[u] && f + 1 != qe[u];
-      if (ok[u]) {  // neighbours the shuffles could not supply (same range only; else masked)
-        if (lane == 0 && u == 0 && !carry_ok && f != qb[u]) pw = __ldg(words + qa[u] * 4 - 1);
-        if (((lane == 31 && u == kU - 1) || f + 1 >= f1) && f + 1 != qe[u]) nw = __ldg(words + qa[u] * 4 + 4);
+      const uint64_t f = base + 32ull * u + lane;
+      const bool in = ok[u] && qa[u] != tf[u] && qa[u] != tl[u];
+      if (ok[u]) {  // neighbours the shuffles could not supply (inside the range only; else masked)
+        if (lane == 0 && u == 0 && !carry_ok && qa[u] != tf[u]) pw = __ldg(words + qa[u] * 4 - 1);
+        if (((lane == 31 && u == kU - 1) || f + 1 >= f1) && qa[u] != tl[u]) nw = __ldg(words + qa[u] * 4 + 4);
       }
       uint32_t st[4] = {0, 0, 0, 0}, en[4] = {0, 0, 0, 0};
       if (ok[u] && !(in && (v[u].x & v[u].y & v[u].z & v[u].w) == 0xFFFFFFFFu))
         runs_of(F.r + rr[u], qa[u], in, v[u], pw, nw, st, en);
-      const uint32_t ns = __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
-      const uint32_t ne = __popc(en[0]) + __popc(en[1]) + __popc(en[2]) + __popc(en[3]);
-      if (!WRITE) {
-        cs += ns, ce += ne;
-        continue;
-      }
-      const bool first_q = ok[u] && f == qb[u];
-      if (!__any_sync(0xFFFFFFFFu, ns || ne || first_q)) continue;  // nothing to place in this step
-      uint32_t ps = ns, pe = ne;  // inclusive warp scans
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, ps, o), b = __shfl_up_sync(0xFFFFFFFFu, pe, o);
-        if (lane >= (uint32_t)o) {
-          ps += a;
-          pe += b;
-        }
-      }
-      uint64_t s = gs + ps - ns, e = ge + pe - ne;
-      if (first_q)  // the first quad of range r (and of the empty ranges just before it)
-        for (int64_t q = rr[u]; q >= 0 && F.qp[q] == f; --q) run_off[q] = s;
-      if (ns | ne) {
-        const uint64_t wbase = qa[u] * 4 - F.r[rr[u]].word_off;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint64_t cell0 = (wbase + k) * 32;
-          uint32_t a = st[k], b = en[k];
-          while (a) {
-            if (s < cap) run_start[s] = (uint32_t)(cell0 + __ffs(a) - 1);
-            ++s;
-            a &= a - 1;
-          }
-          while (b) {
-            if (e < cap) run_end[e] = (uint32_t)(cell0 + __ffs(b) - 1);
-            ++e;
-            b &= b - 1;
-          }
-        }
-      }
-      gs += __shfl_sync(0xFFFFFFFFu, ps, 31);
-      ge += __shfl_sync(0xFFFFFFFFu, pe, 31);
+      visit(ok[u], f, rr[u], qa[u], at_start[u], st, en);
     }
     carry = __shfl_sync(0xFFFFFFFFu, v[kU - 1].w, 31);
     carry_ok = true;
   }
-  if (!WRITE) {
-    cs = __reduce_add_sync(0xFFFFFFFFu, cs);
-    ce = __reduce_add_sync(0xFFFFFFFFu, ce);
-    if (lane == 0) {
-      chunk_s[wid] = cs;
-      chunk_e[wid] = ce;
+}
+
+// Single-pass run extraction (decoupled look-back): warps take chunks in ticket order,
+// count their starts / ends (the DRAM read), publish the aggregates, look back over the
+// predecessors' published values for the exclusive prefix, publish the inclusive prefix,
+// then re-walk the chunk (now an L2 read) placing every start / end at its global
+// ascending position.  status words: value << 2 | flag (0 none, 1 aggregate, 2 prefix).
+constexpr uint64_t kFlagAgg = 1, kFlagPre = 2;
+
+__device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+constexpr uint64_t kMaxChunks = 65536;  // status slots; chunks grow past 65536 x 32 quads
+
+__global__ void __launch_bounds__(kBT, 4) k_runs_1p(const uint32_t* words, Flat F, uint32_t* ticket, uint64_t* stat_s,
+                                                    uint64_t* stat_e, uint64_t* totals, uint32_t* run_start,
+                                                    uint32_t* run_end, uint64_t cap, uint64_t* run_off) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t Q = F.qp[F.n];
+  // small chunks taken in ticket order, so each chunk's second walk finds it in L2 / L1
+  const uint64_t per = ((Q + kMaxChunks - 1) / kMaxChunks + 31) & ~31ull;
+  const uint64_t per_c = per > 1024 ? per : 1024;
+  const uint64_t chunks = (Q + per_c - 1) / per_c;
+  for (;;) {
+  uint32_t c = 0;
+  if (lane == 0) c = atomicAdd(ticket, 1u);
+  c = __shfl_sync(0xFFFFFFFFu, c, 0);
+  if (c >= chunks) return;
+  const uint64_t f0 = (uint64_t)c * per_c, f1 = f0 + per_c < Q ? f0 + per_c : Q;
+  // pass A: aggregates
+  uint32_t cs = 0, ce = 0;
+  if (f0 < f1)
+    chunk_runs(words, F, f0, f1, [&](bool, uint64_t, uint32_t, uint64_t, bool, const uint32_t* st, const uint32_t* en) {
+      cs += __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
+      ce += __popc(en[0]) + __popc(en[1]) + __popc(en[2]) + __popc(en[3]);
+    });
+  const uint64_t agg_s = __reduce_add_sync(0xFFFFFFFFu, cs), agg_e = __reduce_add_sync(0xFFFFFFFFu, ce);
+  // publish the aggregates (chunk 0: its prefix), then a warp-parallel look-back: 32
+  // predecessors per window, summed up to the nearest one holding an inclusive prefix
+  if (lane == 0) {
+    const uint64_t flag = c == 0 ? kFlagPre : kFlagAgg;
+    st_status(stat_s + c, (agg_s << 2) | flag);
+    st_status(stat_e + c, (agg_e << 2) | flag);
+  }
+  uint64_t ex_s = 0, ex_e = 0;
+  if (c > 0) {
+    for (int which = 0; which < 2; ++which) {
+      const uint64_t* stat = which ? stat_e : stat_s;
+      uint64_t ex = 0;
+      for (int64_t top = (int64_t)c - 1; top >= 0; top -= 32) {
+        const int64_t j = top - (int64_t)lane;
+        uint64_t a = j >= 0 ? 0 : (uint64_t)kFlagPre;  // before chunk 0: an empty prefix
+        if (j >= 0) {
+          do {
+            a = ld_status(stat + j);
+          } while ((a & 3) == 0);
+        }
+        const uint32_t pre = __ballot_sync(0xFFFFFFFFu, (a & 3) == kFlagPre);
+        const uint32_t upto = pre ? (uint32_t)(__ffs(pre) - 1) : 31u;  // nearest prefix in the window
+        uint64_t x = lane <= upto ? (a >> 2) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+        ex += x;
+        if (pre) break;
+      }
+      if (which) ex_e = ex;
+      else ex_s = ex;
     }
+    if (lane == 0) {
+      st_status(stat_s + c, ((ex_s + agg_s) << 2) | kFlagPre);
+      st_status(stat_e + c, ((ex_e + agg_e) << 2) | kFlagPre);
+    }
+  }
+  if (lane == 0 && c == chunks - 1) {
+    totals[0] = ex_s + agg_s;
+    totals[1] = ex_e + agg_e;
+  }
+  uint64_t gs = ex_s, ge = ex_e;
+  // pass B: place the starts and ends
+  chunk_runs(words, F, f0, f1,
+             [&](bool ok, uint64_t f, uint32_t r, uint64_t qa, bool at_start, const uint32_t* st, const uint32_t* en) {
+               const uint32_t ns = __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
+               const uint32_t ne = __popc(en[0]) + __popc(en[1]) + __popc(en[2]) + __popc(en[3]);
+               const bool first_q = at_start;  // the range's first flat quad (padding or not)
+               if (!__any_sync(0xFFFFFFFFu, ns || ne || first_q)) return;  // nothing to place in this step
+               uint32_t ps = ns, pe = ne;  // inclusive warp scans
+#pragma unroll
+               for (int o = 1; o < 32; o <<= 1) {
+                 const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, ps, o), b = __shfl_up_sync(0xFFFFFFFFu, pe, o);
+                 if (lane >= (uint32_t)o) {
+                   ps += a;
+                   pe += b;
+                 }
+               }
+               uint64_t s = gs + ps - ns, e = ge + pe - ne;
+               if (first_q)  // the first quad of range r (and of the empty ranges just before it)
+                 for (int64_t q = r; q >= 0 && F.qp[q] == f; --q) run_off[q] = s;
+               if (ns | ne) {
+                 const uint64_t wbase = qa * 4 - F.r[r].word_off;
+#pragma unroll
+                 for (int k = 0; k < 4; ++k) {
+                   const uint64_t cell0 = (wbase + k) * 32;
+                   uint32_t a = st[k], b = en[k];
+                   while (a) {
+                     if (s < cap) run_start[s] = (uint32_t)(cell0 + __ffs(a) - 1);
+                     ++s;
+                     a &= a - 1;
+                   }
+                   while (b) {
+                     if (e < cap) run_end[e] = (uint32_t)(cell0 + __ffs(b) - 1);
+                     ++e;
+                     b &= b - 1;
+                   }
+                 }
+               }
+               gs += __shfl_sync(0xFFFFFFFFu, ps, 31);
+               ge += __shfl_sync(0xFFFFFFFFu, pe, 31);
+             });
   }
 }
 
-__global__ void k_run_off_tail(const uint64_t* qp, const uint64_t* chunk_off, uint64_t n_chunks, uint32_t n,
-                               uint64_t* run_off) {
+__global__ void k_run_off_tail(const uint64_t* qp, const uint64_t* totals, uint32_t n, uint64_t* run_off) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i <= n && qp[i] >= qp[n]) run_off[i] = chunk_off[n_chunks];  // ranges starting at the end: the total
+  if (i <= n && qp[i] >= qp[n]) run_off[i] = totals[0];  // ranges starting at the end: the total
 }
 
 struct Scratch {
@@ -544,25 +631,20 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   if (!n) return COH_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   COH_BM_FLAT(ctx, d_ranges, n, s)
-  const uint64_t n_chunks = (uint64_t)grid_for(ctx) * (kBT / 32);
+  const uint64_t n_chunks = kMaxChunks;
   Scratch co;
   co.s = s;
-  cudaError_t e = cudaMallocAsync(&co.p, sizeof(uint64_t) * 2 * (n_chunks + 1), s);
+  const size_t bytes = sizeof(uint64_t) * (2 * n_chunks + 2) + 16;
+  cudaError_t e = cudaMallocAsync(&co.p, bytes, s);
   if (e != cudaSuccess) return fail(ctx, "zero_runs scratch", e);
-  uint64_t* chunk = static_cast<uint64_t*>(co.p);
-  uint64_t* chunk_e = chunk + n_chunks + 1;
-  if ((e = cudaMemsetAsync(chunk, 0, sizeof(uint64_t) * 2 * (n_chunks + 1), s)) != cudaSuccess)
-    return fail(ctx, "zero_runs init", e);
-  k_runs<false><<<grid_for(ctx), kBT, 0, s>>>(d_words, F, chunk, chunk_e, nullptr, nullptr, 0, nullptr);
-  size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, chunk, chunk, (int)(n_chunks + 1), s);
-  Scratch sc;
-  sc.s = s;
-  if ((e = cudaMallocAsync(&sc.p, tmp, s)) != cudaSuccess) return fail(ctx, "zero_runs scan scratch", e);
-  cub::DeviceScan::ExclusiveSum(sc.p, tmp, chunk, chunk, (int)(n_chunks + 1), s);
-  cub::DeviceScan::ExclusiveSum(sc.p, tmp, chunk_e, chunk_e, (int)(n_chunks + 1), s);
-  k_runs<true><<<grid_for(ctx), kBT, 0, s>>>(d_words, F, chunk, chunk_e, d_run_start, d_run_end, cap, d_run_off);
-  k_run_off_tail<<<(n + 1 + 255) / 256, 256, 0, s>>>(F.qp, chunk, n_chunks, n, d_run_off);
-  ctx->launches += 5;
+  if ((e = cudaMemsetAsync(co.p, 0, bytes, s)) != cudaSuccess) return fail(ctx, "zero_runs init", e);
+  uint64_t* stat_s = static_cast<uint64_t*>(co.p);
+  uint64_t* stat_e = stat_s + n_chunks;
+  uint64_t* totals = stat_e + n_chunks;
+  uint32_t* ticket = reinterpret_cast<uint32_t*>(totals + 2);
+  k_runs_1p<<<grid_for(ctx), kBT, 0, s>>>(d_words, F, ticket, stat_s, stat_e, totals, d_run_start, d_run_end, cap,
+                                          d_run_off);
+  k_run_off_tail<<<(n + 1 + 255) / 256, 256, 0, s>>>(F.qp, totals, n, d_run_off);
+  ctx->launches += 2;
   return check(ctx, "zero_runs");
 }
