@@ -17,10 +17,10 @@
 // 512-byte access), four steps in flight; a lane finds its range once by binary search and
 // then only advances.  Per-range results (first zero, view flags) accumulate in registers
 // and are flushed with one atomic when the range changes (warp-reduced when the whole warp
-// agrees), so the loop has no barriers and stays HBM-bound.  Zero runs: one pass with a
-// decoupled look-back over warp chunks (count -> publish -> prefix from the predecessors ->
-// re-walk the chunk from L2 and place each start / end at its global ascending position;
-// the k-th start and the k-th end are the same run: runs never cross ranges).
+// agrees), so the loop has no barriers and stays HBM-bound.  Zero runs: a count pass over
+// warp chunks, a CUB scan of the counts, and a write pass placing each start / end at its
+// global ascending position (the k-th start and the k-th end are the same run: runs never
+// cross ranges).
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
@@ -405,95 +405,40 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
   }
 }
 
-// Single-pass run extraction (decoupled look-back): warps take chunks in ticket order,
-// count their starts / ends (the DRAM read), publish the aggregates, look back over the
-// predecessors' published values for the exclusive prefix, publish the inclusive prefix,
-// then re-walk the chunk (now an L2 read) placing every start / end at its global
-// ascending position.  status words: value << 2 | flag (0 none, 1 aggregate, 2 prefix).
-constexpr uint64_t kFlagAgg = 1, kFlagPre = 2;
-
-__device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-constexpr uint64_t kMaxChunks = 65536;  // status slots; chunks grow past 65536 x 32 quads
-
-__global__ void __launch_bounds__(kBT, 4) k_runs_1p(const uint32_t* words, Flat F, uint32_t* ticket, uint64_t* stat_s,
-                                                    uint64_t* stat_e, uint64_t* totals, uint32_t* run_start,
-                                                    uint32_t* run_end, uint64_t cap, uint64_t* run_off) {
+// Run extraction in two passes over warp chunks: count (starts and ends separately: a run
+// may start in one chunk and end in a later one), an exclusive scan of the chunk counts,
+// then the write walk placing every start / end at its global ascending position (chunk
+// prefix + warp scan per step), plus run_off for the ranges whose first quad is in the
+// chunk.  (A single-pass decoupled look-back over ticketed chunks was measured slower on
+// B200: the first wave's look-backs walk back over thousands of aggregates.)
+template <bool WRITE>
+__global__ void __launch_bounds__(kBT, 4) k_runs(const uint32_t* words, Flat F, uint64_t* chunk_s, uint64_t* chunk_e,
+                                                 uint32_t* run_start, uint32_t* run_end, uint64_t cap,
+                                                 uint64_t* run_off) {
+  uint64_t f0, f1, wid;
+  warp_chunk(F.qp[F.n], f0, f1, wid);
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t Q = F.qp[F.n];
-  // small chunks taken in ticket order, so each chunk's second walk finds it in L2 / L1
-  const uint64_t per = ((Q + kMaxChunks - 1) / kMaxChunks + 31) & ~31ull;
-  const uint64_t per_c = per > 1024 ? per : 1024;
-  const uint64_t chunks = (Q + per_c - 1) / per_c;
-  for (;;) {
-  uint32_t c = 0;
-  if (lane == 0) c = atomicAdd(ticket, 1u);
-  c = __shfl_sync(0xFFFFFFFFu, c, 0);
-  if (c >= chunks) return;
-  const uint64_t f0 = (uint64_t)c * per_c, f1 = f0 + per_c < Q ? f0 + per_c : Q;
-  // pass A: aggregates
-  uint32_t cs = 0, ce = 0;
-  if (f0 < f1)
+  if (f0 >= f1) return;
+  if (!WRITE) {
+    uint32_t cs = 0, ce = 0;
     chunk_runs(words, F, f0, f1, [&](bool, uint64_t, uint32_t, uint64_t, bool, const uint32_t* st, const uint32_t* en) {
       cs += __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
       ce += __popc(en[0]) + __popc(en[1]) + __popc(en[2]) + __popc(en[3]);
     });
-  const uint64_t agg_s = __reduce_add_sync(0xFFFFFFFFu, cs), agg_e = __reduce_add_sync(0xFFFFFFFFu, ce);
-  // publish the aggregates (chunk 0: its prefix), then a warp-parallel look-back: 32
-  // predecessors per window, summed up to the nearest one holding an inclusive prefix
-  if (lane == 0) {
-    const uint64_t flag = c == 0 ? kFlagPre : kFlagAgg;
-    st_status(stat_s + c, (agg_s << 2) | flag);
-    st_status(stat_e + c, (agg_e << 2) | flag);
-  }
-  uint64_t ex_s = 0, ex_e = 0;
-  if (c > 0) {
-    for (int which = 0; which < 2; ++which) {
-      const uint64_t* stat = which ? stat_e : stat_s;
-      uint64_t ex = 0;
-      for (int64_t top = (int64_t)c - 1; top >= 0; top -= 32) {
-        const int64_t j = top - (int64_t)lane;
-        uint64_t a = j >= 0 ? 0 : (uint64_t)kFlagPre;  // before chunk 0: an empty prefix
-        if (j >= 0) {
-          do {
-            a = ld_status(stat + j);
-          } while ((a & 3) == 0);
-        }
-        const uint32_t pre = __ballot_sync(0xFFFFFFFFu, (a & 3) == kFlagPre);
-        const uint32_t upto = pre ? (uint32_t)(__ffs(pre) - 1) : 31u;  // nearest prefix in the window
-        uint64_t x = lane <= upto ? (a >> 2) : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
-        ex += x;
-        if (pre) break;
-      }
-      if (which) ex_e = ex;
-      else ex_s = ex;
-    }
+    cs = __reduce_add_sync(0xFFFFFFFFu, cs);
+    ce = __reduce_add_sync(0xFFFFFFFFu, ce);
     if (lane == 0) {
-      st_status(stat_s + c, ((ex_s + agg_s) << 2) | kFlagPre);
-      st_status(stat_e + c, ((ex_e + agg_e) << 2) | kFlagPre);
+      chunk_s[wid] = cs;
+      chunk_e[wid] = ce;
     }
+    return;
   }
-  if (lane == 0 && c == chunks - 1) {
-    totals[0] = ex_s + agg_s;
-    totals[1] = ex_e + agg_e;
-  }
-  uint64_t gs = ex_s, ge = ex_e;
-  // pass B: place the starts and ends
+  uint64_t gs = chunk_s[wid], ge = chunk_e[wid];
   chunk_runs(words, F, f0, f1,
              [&](bool ok, uint64_t f, uint32_t r, uint64_t qa, bool at_start, const uint32_t* st, const uint32_t* en) {
                const uint32_t ns = __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
                const uint32_t ne = __popc(en[0]) + __popc(en[1]) + __popc(en[2]) + __popc(en[3]);
-               const bool first_q = at_start;  // the range's first flat quad (padding or not)
-               if (!__any_sync(0xFFFFFFFFu, ns || ne || first_q)) return;  // nothing to place in this step
+               if (!__any_sync(0xFFFFFFFFu, ns || ne || at_start)) return;  // nothing to place in this step
                uint32_t ps = ns, pe = ne;  // inclusive warp scans
 #pragma unroll
                for (int o = 1; o < 32; o <<= 1) {
@@ -504,7 +449,7 @@ __global__ void __launch_bounds__(kBT, 4) k_runs_1p(const uint32_t* words, Flat 
                  }
                }
                uint64_t s = gs + ps - ns, e = ge + pe - ne;
-               if (first_q)  // the first quad of range r (and of the empty ranges just before it)
+               if (at_start)  // the first flat quad of range r (and of the empty ranges just before it)
                  for (int64_t q = r; q >= 0 && F.qp[q] == f; --q) run_off[q] = s;
                if (ns | ne) {
                  const uint64_t wbase = qa * 4 - F.r[r].word_off;
@@ -527,7 +472,6 @@ __global__ void __launch_bounds__(kBT, 4) k_runs_1p(const uint32_t* words, Flat 
                gs += __shfl_sync(0xFFFFFFFFu, ps, 31);
                ge += __shfl_sync(0xFFFFFFFFu, pe, 31);
              });
-  }
 }
 
 __global__ void k_run_off_tail(const uint64_t* qp, const uint64_t* totals, uint32_t n, uint64_t* run_off) {
@@ -631,20 +575,26 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   if (!n) return COH_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   COH_BM_FLAT(ctx, d_ranges, n, s)
-  const uint64_t n_chunks = kMaxChunks;
+  const uint64_t n_chunks = (uint64_t)grid_for(ctx) * (kBT / 32);
   Scratch co;
   co.s = s;
-  const size_t bytes = sizeof(uint64_t) * (2 * n_chunks + 2) + 16;
-  cudaError_t e = cudaMallocAsync(&co.p, bytes, s);
+  cudaError_t e = cudaMallocAsync(&co.p, sizeof(uint64_t) * 2 * (n_chunks + 1), s);
   if (e != cudaSuccess) return fail(ctx, "zero_runs scratch", e);
-  if ((e = cudaMemsetAsync(co.p, 0, bytes, s)) != cudaSuccess) return fail(ctx, "zero_runs init", e);
-  uint64_t* stat_s = static_cast<uint64_t*>(co.p);
-  uint64_t* stat_e = stat_s + n_chunks;
-  uint64_t* totals = stat_e + n_chunks;
-  uint32_t* ticket = reinterpret_cast<uint32_t*>(totals + 2);
-  k_runs_1p<<<grid_for(ctx), kBT, 0, s>>>(d_words, F, ticket, stat_s, stat_e, totals, d_run_start, d_run_end, cap,
-                                          d_run_off);
+  uint64_t* chunk = static_cast<uint64_t*>(co.p);
+  uint64_t* chunk_e = chunk + n_chunks + 1;
+  if ((e = cudaMemsetAsync(chunk, 0, sizeof(uint64_t) * 2 * (n_chunks + 1), s)) != cudaSuccess)
+    return fail(ctx, "zero_runs init", e);
+  k_runs<false><<<grid_for(ctx), kBT, 0, s>>>(d_words, F, chunk, chunk_e, nullptr, nullptr, 0, nullptr);
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, chunk, chunk, (int)(n_chunks + 1), s);
+  Scratch sc;
+  sc.s = s;
+  if ((e = cudaMallocAsync(&sc.p, tmp, s)) != cudaSuccess) return fail(ctx, "zero_runs scan scratch", e);
+  cub::DeviceScan::ExclusiveSum(sc.p, tmp, chunk, chunk, (int)(n_chunks + 1), s);
+  cub::DeviceScan::ExclusiveSum(sc.p, tmp, chunk_e, chunk_e, (int)(n_chunks + 1), s);
+  k_runs<true><<<grid_for(ctx), kBT, 0, s>>>(d_words, F, chunk, chunk_e, d_run_start, d_run_end, cap, d_run_off);
+  uint64_t* totals = chunk + n_chunks;  // exclusive scan: entry n_chunks holds the total
   k_run_off_tail<<<(n + 1 + 255) / 256, 256, 0, s>>>(F.qp, totals, n, d_run_off);
-  ctx->launches += 2;
+  ctx->launches += 6;
   return check(ctx, "zero_runs");
 }
