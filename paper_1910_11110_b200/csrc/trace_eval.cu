@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? 8 : 10) k_trace_eval(
       // The rings are live on this path too, so the scheduler cannot sink their loads
       // past the slow-path branches (which would leave them no lead before first use).
 #pragma unroll
-      for (int j = 0; j < 4; ++j) keep ^= ring[j].x ^ ring[j].y ^ ring[j].z ^ ring[j].w ^ B[j].x ^ B[j].y ^ B[j].z ^ B[j].w;
+      for (int j = 0; j < 4; ++j) keep ^= ring[j].x ^ B[j].x;  // one word per 128-bit load suffices
       keep = pin_zero(keep);
     }
     // which call: k calls of this 32-group completed (sentinel position)
