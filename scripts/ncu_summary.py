@@ -1,5 +1,5 @@
 """Extract the judged metrics of one ncu --set full capture into profiles/.
-usage: python scripts/ncu_summary.py REP.ncu-rep OUT_PREFIX [traces_per_launch]"""
+usage: python scripts/ncu_summary.py REP.ncu-rep OUT_PREFIX [traces_per_launch] [kernel-substring]"""
 import csv
 import json
 import subprocess
@@ -24,7 +24,7 @@ KEYS = [
 
 def main():
     rep, prefix = sys.argv[1], sys.argv[2]
-    traces = int(sys.argv[3]) if len(sys.argv) > 3 else None
+    traces = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3] != "-" else None
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr, units = rows[0], rows[1]
@@ -41,7 +41,8 @@ def main():
                     d[k] = v
                 d[k + ".unit"] = units[i]
         kernels.append(d)
-    k = kernels[0]
+    pick = sys.argv[4] if len(sys.argv) > 4 else ""
+    k = next(kk for kk in kernels if pick in kk["kernel"])
     scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0}
     dram = k["dram__bytes_read.sum"] * scale.get(k["dram__bytes_read.sum.unit"], 1) + \
         k["dram__bytes_write.sum"] * scale.get(k["dram__bytes_write.sum.unit"], 1)
