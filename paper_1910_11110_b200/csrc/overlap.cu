@@ -283,6 +283,7 @@ __global__ void k_closure(RegDev r, const coh_mode* modes, const uint32_t* off, 
 
 struct coh_registry {
   int device = 0;
+  cudaStream_t stream = nullptr;  // the build stream; the memory is stream-ordered
   uint32_t n = 0, P = 1;
   void* mem = nullptr;  // one allocation: keys, lo, hi, view, tree, views copy
   cohb::RegDev dev{};
@@ -315,7 +316,8 @@ extern "C" int coh_registry_build(coh_ctx* ctx, const coh_view* d_views, uint32_
   cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
                                   (uint32_t*)nullptr, (int)n, 0, 64, s);
   const size_t total = o_tmp + tmp_bytes;
-  cudaError_t e = cudaMalloc(&r->mem, total);
+  r->stream = s;
+  cudaError_t e = cudaMallocAsync(&r->mem, total, s);
   if (e != cudaSuccess) {
     delete r;
     return fail(ctx, "registry alloc", e);
@@ -340,7 +342,7 @@ extern "C" int coh_registry_build(coh_ctx* ctx, const coh_view* d_views, uint32_
   for (uint32_t first = P >> 1; first >= 1; first >>= 1)
     k_build_tree_level<<<(first + 255) / 256, 256, 0, s>>>(first, first, tree);
   if ((e = cudaGetLastError()) != cudaSuccess) {
-    cudaFree(r->mem);
+    cudaFreeAsync(r->mem, s);
     delete r;
     return fail(ctx, "registry build", e);
   }
@@ -352,7 +354,7 @@ extern "C" int coh_registry_build(coh_ctx* ctx, const coh_view* d_views, uint32_
 
 extern "C" void coh_registry_destroy(coh_registry* r) {
   if (!r) return;
-  cudaFree(r->mem);
+  cudaFreeAsync(r->mem, r->stream);
   delete r;
 }
 
