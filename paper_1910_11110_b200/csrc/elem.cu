@@ -26,6 +26,13 @@ constexpr int kWPT = kElemTileWords / kET; // 8 words per thread
 static_assert(kWPT == 8, "8 words per thread");
 
 
+// Programmatic dependent launch: a stage kernel may be scheduled while its predecessor
+// drains; it reads only host-built descriptors before waiting for the predecessor's
+// results (griddepcontrol.wait = cudaGridDependencySynchronize) and lets its own successor
+// launch early.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 __device__ __forceinline__ uint32_t word_mask(uint32_t w, uint32_t lo, uint32_t hi) {
   const uint32_t wl = lo >> 5, wh = hi >> 5;
   if (w < wl || w > wh) return 0u;
@@ -137,6 +144,8 @@ __global__ void __launch_bounds__(kET, 8) k_elem_pass1(const ElemDev d) {
   __shared__ uint32_t s_first[kET], s_last[kET];
   __shared__ uint32_t s_next;
   const ElemTile tile = d.tiles[blockIdx.x];
+  griddep_wait();
+  griddep_launch();
   const uint32_t b = tile.b;
   uint32_t* Lp = d.planes + (size_t)b * 2u * d.W;
   uint32_t* Rp = Lp + d.W;
@@ -262,6 +271,8 @@ constexpr int kDecideWarps = 4;
 __global__ void __launch_bounds__(32 * kDecideWarps) k_elem_decide(const ElemDev d) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t b = blockIdx.x * kDecideWarps + (threadIdx.x >> 5);
+  griddep_wait();
+  griddep_launch();
   if (b >= d.n_progs) return;
   ElemState* __restrict__ st = d.st + b;
   uint32_t dead = st->dead;
@@ -355,6 +366,8 @@ constexpr int kWPL = kElemTileWords / 32;  // 64 words per lane
 __global__ void __launch_bounds__(32 * kApplyWarps, 4) k_elem_apply(const ElemDev d, uint32_t n_sync_tiles) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t gw = blockIdx.x * kApplyWarps + (threadIdx.x >> 5), nw = gridDim.x * kApplyWarps;
+  griddep_wait();
+  griddep_launch();
   for (uint32_t it = gw; it < n_sync_tiles; it += nw) {
     const ElemTile tile = d.sync_desc[it];
     const uint32_t b = tile.b, tloc = tile.tloc;
@@ -478,16 +491,32 @@ __global__ void __launch_bounds__(32 * kApplyWarps, 4) k_elem_apply(const ElemDe
   }
 }
 
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), uint32_t grid, uint32_t block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, uint32_t n_sync_tiles, void* stream, std::string* err) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (n_tiles) k_elem_pass1<<<n_tiles, kET, 0, s>>>(d);
-  if (n_tiles)  // a stage with only WRITE ops has nothing to decide (writes cannot get stuck)
-    k_elem_decide<<<(d.n_progs + kDecideWarps - 1) / kDecideWarps, 32 * kDecideWarps, 0, s>>>(d);
-  if (n_sync_tiles) {
+  cudaError_t e = cudaSuccess;
+  if (n_tiles && e == cudaSuccess) e = launch_pdl(k_elem_pass1, n_tiles, kET, s, d);
+  if (n_tiles && e == cudaSuccess)  // a stage with only WRITE ops has nothing to decide (writes cannot get stuck)
+    e = launch_pdl(k_elem_decide, (d.n_progs + kDecideWarps - 1) / kDecideWarps, 32 * kDecideWarps, s, d);
+  if (n_sync_tiles && e == cudaSuccess) {
     const uint32_t blocks = (n_sync_tiles + kApplyWarps - 1) / kApplyWarps;
-    k_elem_apply<<<blocks < 148u * 16u ? blocks : 148u * 16u, 32 * kApplyWarps, 0, s>>>(d, n_sync_tiles);
+    e = launch_pdl(k_elem_apply, blocks < 148u * 16u ? blocks : 148u * 16u, 32 * kApplyWarps, s, d, n_sync_tiles);
   }
-  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("element stage launch: ") + cudaGetErrorString(e);
     return COH_E_CUDA;
