@@ -363,6 +363,16 @@ typedef struct coh_sweep_stats {
 int coh_sweep(coh_ctx* ctx, uint64_t seed0, uint32_t n_seeds, const coh_gen_limits* limits,
               uint32_t max_decisions, int32_t fuel, coh_sweep_leaf* leaves, uint64_t leaves_cap,
               coh_sweep_stats* stats);
+/* Acceptance criterion 1 (tests/acceptance.cpp:107-138): every straight-line raw program of
+ * length <= max_len (<= 8) over the ten effect forms on one scalar (enumerate_raw_programs,
+ * testkit.hpp:241-268, in its order), run on the GPU block interpreter from initial_store;
+ * outcome counts and the number of programs that ever leave a key (I,I). statuses[i]
+ * (optional) = COH_RUN_* of program i. */
+typedef struct coh_enum_stats {
+  uint64_t programs, done, stuck, fuel_exhausted, unsafe, steps;
+} coh_enum_stats;
+int coh_enum_straight_line(coh_ctx* ctx, uint32_t max_len, int32_t fuel, coh_enum_stats* stats, uint8_t* statuses,
+                           uint64_t statuses_cap);
 
 /* ---- DSL front end and CLI reporting ----------------------
  * The reference command line (tools/cohere_main.cpp:80-230) over program text.

@@ -135,3 +135,27 @@ extern "C" int ref_cli(const char* cmd, const char* src, int raw, int no_overlap
   *exit_code = code;
   return (o.str().size() >= out_cap || e.str().size() >= err_cap) ? -1 : 0;
 }
+
+// Acceptance criterion 1 (tests/acceptance.cpp:107-138) through the reference itself:
+// enumerate_raw_programs + run from initial_store, one status per program (RunStatus
+// ordinals), and whether any step left a key (I,I) (checked after every step of a traced run).
+extern "C" int ref_enum_straight_line(int max_len, int fuel, unsigned char* statuses, long cap, long* unsafe_programs) {
+  EnumLimits limits;
+  limits.max_len = max_len;
+  std::vector<Stmt> programs = enumerate_raw_programs(limits);
+  Declarations d;
+  d.add_scalar({"x", {}});
+  const Store s0 = initial_store(d);
+  long unsafe = 0;
+  for (size_t i = 0; i < programs.size(); ++i) {
+    RunResult r = run(programs[i], s0, fuel, Schedule(), TraceMode::Full);
+    Store s = s0;
+    bool bad = is_unsafe(s);
+    for (const auto& step : r.trace)
+      for (const auto& [key, pair] : step.delta) bad = bad || pair == kBothInvalid;
+    unsafe += bad ? 1 : 0;
+    if ((long)i < cap) statuses[i] = (unsigned char)r.status;
+  }
+  *unsafe_programs = unsafe;
+  return (int)programs.size();
+}

@@ -44,7 +44,7 @@ __global__ void k_sweep_run(const uint32_t* __restrict__ code, const SweepMeta* 
   unsigned long long store = 0x5555555555555555ull;  // initial_store: every key (V,I)
   if (m.n_keys < 32) store &= (1ull << (2 * m.n_keys)) - 1ull;
   uint32_t pc = 0, steps = 0, cursor = 0, overflow = 0, bnd = 0, blocks = 0, status = COH_RUN_DONE;
-  uint32_t stuck_key = 0, stuck = 0;
+  uint32_t stuck_key = 0, stuck = 0, unsafe = 0;  // unsafe: some step left a key (I,I) (is_unsafe)
   for (;;) {
     const uint32_t ins = prog[pc];
     const uint32_t op = ins & 15u;
@@ -95,6 +95,7 @@ __global__ void k_sweep_run(const uint32_t* __restrict__ code, const SweepMeta* 
         break;
       }
       store = (store & ~(3ull << (2 * key))) | ((unsigned long long)after << (2 * key));
+      unsafe |= after == 0;
     } else {  // BC_WHOLE: atomic over the cells, ascending
       const uint32_t lo = (ins >> 8) & 0xFFu, hi = (ins >> 16) & 0xFFu;
       bool fail = false;
@@ -111,7 +112,9 @@ __global__ void k_sweep_run(const uint32_t* __restrict__ code, const SweepMeta* 
       if (fail) break;
       for (uint32_t k = lo; k <= hi; ++k) {
         const uint32_t before = (uint32_t)(store >> (2 * k)) & 3u;
-        store = (store & ~(3ull << (2 * k))) | ((unsigned long long)apply_pair_d(eff, site, before) << (2 * k));
+        const uint32_t after = (uint32_t)apply_pair_d(eff, site, before);
+        store = (store & ~(3ull << (2 * k))) | ((unsigned long long)after << (2 * k));
+        unsafe |= after == 0;
       }
     }
     if (trace) trace[steps] = SweepTrace{pc, site, store};
@@ -123,7 +126,7 @@ __global__ void k_sweep_run(const uint32_t* __restrict__ code, const SweepMeta* 
   o.steps = steps;
   o.store = store;
   o.stuck = stuck;
-  o.pad = 0;
+  o.pad = unsafe;
   out[i] = o;
 }
 

@@ -44,7 +44,7 @@ struct SweepOut {
   uint32_t steps;
   unsigned long long store;  // 2 bits per key (bit0 local, bit1 remote)
   uint32_t stuck;            // effect | site << 3 | key kind (abstract) << 4 | actual << 5
-  uint32_t pad;
+  uint32_t pad;              // 1 when some step left a key (I,I) (is_unsafe, program.hpp:166-172)
 };
 // One record per reduction step of item 0 (the CLI's --trace): the instruction that fired,
 // the rule (0 effect, 1 remote-effect, 2 while-true, 3 while-false, 4 if-true, 5 if-false,

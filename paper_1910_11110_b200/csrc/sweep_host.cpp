@@ -580,3 +580,82 @@ extern "C" int coh_sweep(coh_ctx* ctx, uint64_t seed0, uint32_t n_seeds, const c
   return COH_OK;
 #undef COH_S
 }
+
+// ---- acceptance criterion 1 (tests/acceptance.cpp:107-138) ---------------------------
+// enumerate_raw_programs (testkit.hpp:241-268): every straight-line program of length
+// <= max_len over the ten effect forms (push, pull, r, w, noop x local, remote) on one
+// scalar, run from initial_store on the GPU block interpreter; counts of outcomes and of
+// programs that ever reach an unsafe (I,I) key.
+extern "C" int coh_enum_straight_line(coh_ctx* ctx, uint32_t max_len, int32_t fuel, coh_enum_stats* stats,
+                                      uint8_t* statuses, uint64_t statuses_cap) {
+  using namespace cohb;
+  if (!ctx || !stats || max_len > 8) return COH_E_ARG;
+  std::vector<uint32_t> code;
+  std::vector<SweepMeta> meta;
+  std::vector<uint32_t> prog;  // current program: form indices
+  // breadth-first by length, forms in the reference's order (kind-major, then site)
+  std::vector<std::vector<uint32_t>> frontier = {{}};
+  auto emit = [&](const std::vector<uint32_t>& p) {
+    meta.push_back(SweepMeta{(uint32_t)code.size(), 2u, 0u, 0u});  // keys: x = 0, x^ = 1
+    for (uint32_t f : p) code.push_back(BC_EFF | ((f / 2) << 4) | ((f % 2) << 7) | (0u << 8));
+    code.push_back(BC_END);
+  };
+  emit({});
+  for (uint32_t len = 1; len <= max_len; ++len) {
+    std::vector<std::vector<uint32_t>> next;
+    for (const auto& pre : frontier)
+      for (uint32_t f = 0; f < 10; ++f) {
+        std::vector<uint32_t> p = pre;
+        p.push_back(f);
+        emit(p);
+        next.push_back(std::move(p));
+      }
+    frontier.swap(next);
+  }
+  const uint32_t n = (uint32_t)meta.size();
+  std::vector<SweepItem> items(n);
+  for (uint32_t i = 0; i < n; ++i) items[i] = SweepItem{i, 0, 0, 0};
+  DevMem d_code, d_meta, d_checks, d_items, d_out;
+  cudaStream_t s = nullptr;
+#define COH_S(x)                                                  \
+  do {                                                            \
+    cudaError_t e_ = (x);                                         \
+    if (e_ != cudaSuccess) {                                      \
+      ctx->err = std::string(#x) + ": " + cudaGetErrorString(e_); \
+      return COH_E_CUDA;                                          \
+    }                                                             \
+  } while (0)
+  COH_S(cudaMalloc(&d_code.p, code.size() * 4));
+  COH_S(cudaMalloc(&d_meta.p, meta.size() * sizeof(SweepMeta)));
+  COH_S(cudaMalloc(&d_checks.p, 16));
+  COH_S(cudaMalloc(&d_items.p, items.size() * sizeof(SweepItem)));
+  COH_S(cudaMalloc(&d_out.p, items.size() * sizeof(SweepOut)));
+  COH_S(cudaMemcpy(d_code.p, code.data(), code.size() * 4, cudaMemcpyHostToDevice));
+  COH_S(cudaMemcpy(d_meta.p, meta.data(), meta.size() * sizeof(SweepMeta), cudaMemcpyHostToDevice));
+  COH_S(cudaMemcpy(d_items.p, items.data(), items.size() * sizeof(SweepItem), cudaMemcpyHostToDevice));
+  std::string err;
+  int rc = launch_sweep_run(static_cast<uint32_t*>(d_code.p), static_cast<SweepMeta*>(d_meta.p),
+                            static_cast<uint16_t*>(d_checks.p), static_cast<SweepItem*>(d_items.p), n, fuel,
+                            static_cast<SweepOut*>(d_out.p), s, &err);
+  if (rc) {
+    ctx->err = err;
+    return rc;
+  }
+  std::vector<SweepOut> out(n);
+  COH_S(cudaMemcpy(out.data(), d_out.p, n * sizeof(SweepOut), cudaMemcpyDeviceToHost));
+#undef COH_S
+  ctx->launches++;
+  coh_enum_stats st{};
+  st.programs = n;
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t status = out[i].status_consumed & 3u;
+    if (status == COH_RUN_DONE) st.done++;
+    else if (status == COH_RUN_STUCK) st.stuck++;
+    else st.fuel_exhausted++;
+    st.unsafe += out[i].pad ? 1 : 0;
+    st.steps += out[i].steps;
+    if (statuses && i < statuses_cap) statuses[i] = (uint8_t)status;
+  }
+  *stats = st;
+  return COH_OK;
+}

@@ -34,8 +34,15 @@ class _Stats(C.Structure):
                 ("conflicts", C.c_uint64), ("device_ms", C.c_double), ("launches", C.c_uint64)]
 
 
+class EnumStats(C.Structure):
+    _fields_ = [("programs", C.c_uint64), ("done", C.c_uint64), ("stuck", C.c_uint64), ("fuel_exhausted", C.c_uint64),
+                ("unsafe", C.c_uint64), ("steps", C.c_uint64)]
+
+
 def _register(L):
     vp = C.c_void_p
+    L.coh_enum_straight_line.restype = C.c_int
+    L.coh_enum_straight_line.argtypes = [vp, C.c_uint32, C.c_int32, vp, vp, C.c_uint64]
     L.coh_gen_program_text.restype = C.c_int
     L.coh_gen_program_text.argtypes = [C.c_uint64, vp, C.c_char_p, C.c_size_t]
     L.coh_sweep.restype = C.c_int
@@ -64,3 +71,14 @@ def sweep(ctx, seed0: int, n_seeds: int, max_decisions: int = 6, fuel: int = 100
     ctx._check(rc, "coh_sweep")
     stats = {k: getattr(st, k) for k, _ in st._fields_}
     return leaves[: min(leaves_cap, stats["runs"])], stats
+
+
+def enum_straight_line(ctx, max_len: int = 4, fuel: int = 16):
+    """Acceptance criterion 1 on the GPU: (stats dict, per-program RunStatus array) for every
+    straight-line program of length <= max_len over the ten effect forms on one scalar."""
+    st = EnumStats()
+    n = sum(10 ** k for k in range(max_len + 1))
+    statuses = np.zeros(n, np.uint8)
+    rc = lib().coh_enum_straight_line(ctx._h, max_len, fuel, C.addressof(st), statuses.ctypes.data, n)
+    ctx._check(rc, "coh_enum_straight_line")
+    return {k: int(getattr(st, k)) for k, _ in st._fields_}, statuses

@@ -75,3 +75,14 @@ def test_gpu_sweep_other_limits_vs_live_reference(ctx):
         _same_leaves(got, o.ref_sweep_leaves(5000, 200, fuel=fuel))
     got, _ = sweep(ctx, 0, 200, 3, 10000, leaves_cap=1 << 16)
     _same_leaves(got, o.ref_sweep_leaves(0, 200, max_dec=3))
+
+
+@pytest.mark.gpu
+def test_acceptance_criterion_1_enumeration(ctx):
+    # tests/acceptance.cpp:107-138: 11111 straight-line programs -> 4565 done / 6546 stuck,
+    # no fully-invalid state; per-program statuses equal the reference's (tests/golden/enum4.npy)
+    from paper_1910_11110_b200.sweep import enum_straight_line
+    st, statuses = enum_straight_line(ctx, 4, 16)
+    assert (st["programs"], st["done"], st["stuck"], st["fuel_exhausted"], st["unsafe"]) == (11111, 4565, 6546, 0, 0)
+    want = np.load(os.path.join(os.path.dirname(__file__), "golden", "enum4.npy"))
+    assert np.array_equal(statuses, want)
