@@ -303,6 +303,8 @@ typedef struct coh_rt_stats {
   uint64_t h2d_bytes, d2h_bytes;
   uint64_t h2d_copies, d2h_copies;
   uint64_t calls, syncs_elided, stuck_calls;
+  double copy_ms;  /* device time of the copies (CUDA events around each cudaMemcpyAsync; counted
+                      once the runtime has synchronised past them: CPU calls, coh_rt_sync) */
 } coh_rt_stats;
 int coh_rt_create(coh_ctx* ctx, coh_rt** out);
 void coh_rt_destroy(coh_rt* rt);

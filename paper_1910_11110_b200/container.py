@@ -28,7 +28,7 @@ class _Arg(C.Structure):
 class _Stats(C.Structure):
     _fields_ = [("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("h2d_copies", C.c_uint64),
                 ("d2h_copies", C.c_uint64), ("calls", C.c_uint64), ("syncs_elided", C.c_uint64),
-                ("stuck_calls", C.c_uint64)]
+                ("stuck_calls", C.c_uint64), ("copy_ms", C.c_double)]
 
 
 class _Touch(C.Structure):
@@ -142,7 +142,7 @@ class Runtime:
     def stats(self) -> dict:
         st = _Stats()
         lib().coh_rt_get_stats(self._h, C.addressof(st))
-        return {k: int(getattr(st, k)) for k, _ in st._fields_}
+        return {k: (float if k == "copy_ms" else int)(getattr(st, k)) for k, _ in st._fields_}
 
     def records(self) -> np.ndarray:
         """The executed calls as one whole-array trace (include/cohere_b200.h records):

@@ -63,7 +63,32 @@ struct coh_rt {
   std::vector<RtVector> vec;
   cudaStream_t stream = nullptr;
   coh_rt_stats stats{};
+  std::vector<cudaEvent_t> ev_free;                           // event pool
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_open;  // copies not yet harvested
 };
+
+namespace {
+cudaEvent_t take_event(coh_rt* rt) {
+  if (!rt->ev_free.empty()) {
+    cudaEvent_t e = rt->ev_free.back();
+    rt->ev_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+// After a stream synchronisation every recorded copy has completed: add their durations.
+void harvest(coh_rt* rt) {
+  for (auto& pr : rt->ev_open) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) rt->stats.copy_ms += ms;
+    rt->ev_free.push_back(pr.first);
+    rt->ev_free.push_back(pr.second);
+  }
+  rt->ev_open.clear();
+}
+}  // namespace
 
 extern "C" {
 
@@ -83,6 +108,8 @@ int coh_rt_create(coh_ctx* ctx, coh_rt** out) {
 void coh_rt_destroy(coh_rt* rt) {
   if (!rt) return;
   cudaStreamSynchronize(rt->stream);
+  harvest(rt);
+  for (cudaEvent_t e : rt->ev_free) cudaEventDestroy(e);
   for (auto& v : rt->vec) {
     cudaFreeHost(v.host);
     cudaFree(v.dev);
@@ -152,9 +179,13 @@ int coh_rt_call(coh_rt* rt, uint32_t site, const coh_rt_arg* args, uint32_t n_ar
         const int a = apply_pair(sync, COH_LOCAL, v.abst);
         if (a < 0) return stuck(sync, COH_LOCAL, args[i].vec, true, v.abst);
         // the transfer: upload for a GPU component (push), download for a CPU one (pull)
+        const cudaEvent_t e0 = take_event(rt), e1 = take_event(rt);
+        cudaEventRecord(e0, rt->stream);
         cudaError_t e = sync == COH_PUSH
                             ? cudaMemcpyAsync(v.dev, v.host, v.bytes, cudaMemcpyHostToDevice, rt->stream)
                             : cudaMemcpyAsync(v.host, v.dev, v.bytes, cudaMemcpyDeviceToHost, rt->stream);
+        cudaEventRecord(e1, rt->stream);
+        rt->ev_open.emplace_back(e0, e1);
         if (e != cudaSuccess) {
           rt->ctx->err = std::string("coh_rt_call copy: ") + cudaGetErrorString(e);
           return COH_E_CUDA;
@@ -189,6 +220,7 @@ int coh_rt_call(coh_rt* rt, uint32_t site, const coh_rt_arg* args, uint32_t n_ar
         rt->ctx->err = std::string("coh_rt_call sync: ") + cudaGetErrorString(e);
         return COH_E_CUDA;
       }
+      harvest(rt);
       fn(user, nullptr);
     }
   }
@@ -207,6 +239,7 @@ int coh_rt_sync(coh_rt* rt) {
     rt->ctx->err = std::string("coh_rt_sync: ") + cudaGetErrorString(e);
     return COH_E_CUDA;
   }
+  harvest(rt);
   return COH_OK;
 }
 

@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests/test_elem_gpu.py tests/test_container.py -x -q -m gpu > gpurun_out/pytest_gpu_elem.txt 2>&1
-timeout 300 python scripts/bench_elem.py --reps 5 > gpurun_out/bench_elem_pdl.json 2>&1
+timeout 600 python -m pytest tests/test_container.py -x -q -m gpu > gpurun_out/pytest_gpu_ct.txt 2>&1
+timeout 600 python bench.py --steps 20 --no-cpu-baseline --bitmap-buffers 0 --sweep-seeds 0 --overlap-views 0 --e2e-steps 0 > gpurun_out/bench_ct.json 2> gpurun_out/bench_ct.err
