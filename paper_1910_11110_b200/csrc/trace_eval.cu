@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? 8 : 10) k_trace_eval(
     uint32_t calls_done = n_calls;
     int fuel_left = p.fuel;
     bool stop = false;
+    uint4 stuck_chunk;
 
     // One call (C++ form: non-uniform byte sizes and the ragged tail).  T = the record in
     // bits 0-15 (bits 16+ may hold the next record), C = its position in the 16-call
@@ -249,7 +250,10 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? 8 : 10) k_trace_eval(
     COH_PAIR((V).x, 8 * H) COH_PAIR((V).y, 8 * H + 2) COH_PAIR((V).z, 8 * H + 4)           \
     COH_PAIR((V).w, 8 * H + 6)                                                            \
   }                                                                                       \
-  if (__builtin_expect(stop, 0)) goto slow_path;
+  if (__builtin_expect(stop, 0)) {                                                         \
+    stuck_chunk = (V); /* the stuck call's chunk, still in registers */                    \
+    goto slow_path;                                                                       \
+  }
 #define COH_FLUSH                                  \
   steps += acc & kAccSteps;                        \
   xfers += (acc >> kAccXferShift) & 0x3Fu;         \
@@ -332,7 +336,10 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? 8 : 10) k_trace_eval(
             for (int h = 0; h < 8; ++h) {
               if (8u * j + h < tail) COH_CALL(h & 1 ? (w4[h >> 1] >> 16) : w4[h >> 1], 8 * (j & 1) + h)
             }
-            if (stop) goto slow_path;
+            if (stop) {
+              stuck_chunk = ring[j];
+              goto slow_path;
+            }
             if (j & 1) { COH_FLUSH }
           }
           const uint32_t word = (~__brev(bnd ^ (1u << tail))) >> (32u - tail);
@@ -360,9 +367,10 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? 8 : 10) k_trace_eval(
     // which call: k calls of this 32-group completed (sentinel position)
     const uint32_t k = 31u - __clz(bnd);
     const uint32_t i = i0 + k;
-    const uint4 chunk = COH_REC(i / 8u, t);
-    const uint32_t w4[4] = {chunk.x, chunk.y, chunk.z, chunk.w};
-    const uint32_t r = (w4[(i & 7u) >> 1] >> (16u * (i & 1u))) & 0xFFFFu;
+    const uint4 chunk = stuck_chunk;
+    const uint32_t q = i & 7u;  // the call within its chunk (selects, no local array)
+    const uint32_t wsel = (q & 4u) ? ((q & 2u) ? chunk.w : chunk.z) : ((q & 2u) ? chunk.y : chunk.x);
+    const uint32_t r = (wsel >> (16u * (q & 1u))) & 0xFFFFu;
     const uint32_t a = (r >> 8) & 63u, type = (r >> 2) & 63u;
     uint16_t* const sp = reinterpret_cast<uint16_t*>(stb + ((r & 0x3F00u) | toff));
     const uint32_t s = *sp;  // untouched: the store froze before this call
