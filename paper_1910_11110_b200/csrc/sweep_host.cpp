@@ -13,6 +13,7 @@
 #include <map>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.hpp"
@@ -460,22 +461,49 @@ extern "C" int coh_sweep(coh_ctx* ctx, uint64_t seed0, uint32_t n_seeds, const c
   std::vector<SweepMeta> meta;
   std::vector<uint64_t> seeds;
   std::vector<uint32_t> nS, nV;
-  for (uint32_t k = 0; k < n_seeds; ++k) {
-    SweepProgram sp;
-    if (sweep_compile(seed0 + k, L, &sp, nullptr) != COH_OK) {
-      st.conflicts++;  // OverlapInferenceError: the reference generator would throw
-      continue;
-    }
-    if (sp.n_keys > 32 || sp.code.size() > 65535) {
-      ctx->err = "program " + std::to_string(seed0 + k) + " exceeds the 32-key / 64K-instruction interpreter";
+  // program generation + bytecode compile on all host threads (seed slices), then
+  // concatenated in seed order
+  const uint32_t n_th = std::max(1u, std::min<uint32_t>(std::thread::hardware_concurrency(), (n_seeds + 255) / 256));
+  std::vector<std::vector<SweepProgram>> part(n_th);
+  std::vector<std::vector<uint64_t>> part_seed(n_th);
+  std::vector<uint64_t> part_conflicts(n_th, 0);
+  std::vector<int> part_err(n_th, 0);
+  {
+    std::vector<std::thread> pool;
+    for (uint32_t th = 0; th < n_th; ++th)
+      pool.emplace_back([&, th] {
+        const uint32_t k0 = (uint32_t)((uint64_t)n_seeds * th / n_th), k1 = (uint32_t)((uint64_t)n_seeds * (th + 1) / n_th);
+        for (uint32_t k = k0; k < k1; ++k) {
+          SweepProgram sp;
+          if (sweep_compile(seed0 + k, L, &sp, nullptr) != COH_OK) {
+            part_conflicts[th]++;  // OverlapInferenceError: the reference generator would throw
+            continue;
+          }
+          if (sp.n_keys > 32 || sp.code.size() > 65535) {
+            part_err[th] = (int)(k - k0) + 1;
+            return;
+          }
+          part[th].push_back(std::move(sp));
+          part_seed[th].push_back(seed0 + k);
+        }
+      });
+    for (auto& t : pool) t.join();
+  }
+  for (uint32_t th = 0; th < n_th; ++th) {
+    if (part_err[th]) {
+      ctx->err = "a generated program exceeds the 32-key / 64K-instruction interpreter";
       return COH_E_CONSTRUCTION;
     }
-    meta.push_back(SweepMeta{(uint32_t)code.size(), sp.n_keys, (uint32_t)checks.size(), (uint32_t)sp.checks.size()});
-    code.insert(code.end(), sp.code.begin(), sp.code.end());
-    checks.insert(checks.end(), sp.checks.begin(), sp.checks.end());
-    seeds.push_back(seed0 + k);
-    nS.push_back(sp.n_scalars);
-    nV.push_back(sp.n_views);
+    st.conflicts += part_conflicts[th];
+    for (size_t j = 0; j < part[th].size(); ++j) {
+      const SweepProgram& sp = part[th][j];
+      meta.push_back(SweepMeta{(uint32_t)code.size(), sp.n_keys, (uint32_t)checks.size(), (uint32_t)sp.checks.size()});
+      code.insert(code.end(), sp.code.begin(), sp.code.end());
+      checks.insert(checks.end(), sp.checks.begin(), sp.checks.end());
+      seeds.push_back(part_seed[th][j]);
+      nS.push_back(sp.n_scalars);
+      nV.push_back(sp.n_views);
+    }
   }
   st.programs = meta.size();
   DevMem d_code, d_meta, d_checks, d_items, d_out;
