@@ -100,6 +100,13 @@ __global__ void k_build_tree_level(uint32_t first, uint32_t count, int32_t* tree
     tree[node] = max(tree[2 * node], tree[2 * node + 1]);
   }
 }
+// The top levels (nodes < first) in one block: level by level with block barriers.
+__global__ void __launch_bounds__(1024) k_build_tree_top(uint32_t first, int32_t* tree) {
+  for (uint32_t f = first; f >= 1; f >>= 1) {
+    for (uint32_t i = threadIdx.x; i < f; i += blockDim.x) tree[f + i] = max(tree[2 * (f + i)], tree[2 * (f + i) + 1]);
+    __syncthreads();
+  }
+}
 __global__ void k_make_keys(const coh_view* views, uint32_t n, uint64_t* key, uint32_t* idx) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
@@ -339,14 +346,15 @@ extern "C" int coh_registry_build(coh_ctx* ctx, const coh_view* d_views, uint32_
     k_gather<<<(n_views + 255) / 256, 256, 0, s>>>(views, view, n_views, lo, hi);
   }
   k_build_tree_leaves<<<(P + 255) / 256, 256, 0, s>>>(n_views, P, hi, tree);
-  for (uint32_t first = P >> 1; first >= 1; first >>= 1)
-    k_build_tree_level<<<(first + 255) / 256, 256, 0, s>>>(first, first, tree);
+  uint32_t first = P >> 1;
+  for (; first > 1024; first >>= 1) k_build_tree_level<<<(first + 255) / 256, 256, 0, s>>>(first, first, tree);
+  if (first >= 1) k_build_tree_top<<<1, 1024, 0, s>>>(first, tree);
   if ((e = cudaGetLastError()) != cudaSuccess) {
     cudaFreeAsync(r->mem, s);
     delete r;
     return fail(ctx, "registry build", e);
   }
-  ctx->launches += (n_views ? 3 : 1) + (uint64_t)(31 - __builtin_clz(P));  // + the CUB sort
+  ctx->launches += (n_views ? 4 : 2) + (uint64_t)(P > 2048 ? 31 - __builtin_clz(P / 2048) : 0);  // + the CUB sort
   r->dev = RegDev{n_views, P, key, lo, hi, view, tree, views};
   *out = r;
   return COH_OK;
