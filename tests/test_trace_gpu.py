@@ -207,3 +207,33 @@ def test_full_size_c2_properties(ctx):
         ctx.eval_traces(r, shard, nc, na, 10000, o_res, None, stream=s)
         torch.cuda.synchronize()
         assert torch.equal(o_res, d_res[k * shard * 64:(k + 1) * shard * 64]), k
+
+
+def test_full_size_c2_every_trace_vs_oracle(ctx):
+    """BASELINE config 2 at full size, every one of the 1M traces (256M calls) against the C
+    oracle (run on all host cores in trace-id slices): results and boundary bits bit-exact."""
+    import concurrent.futures as cf
+
+    N, nc, na, adv, seed = 1 << 20, 256, 64, 1, 1
+    s = torch.cuda.current_stream().cuda_stream
+    d_rec = torch.empty(coh.records_elems(N, nc), dtype=torch.int16, device="cuda")
+    ctx.gen_records(seed, 0, N, nc, na, adv, d_rec, s)
+    d_res = torch.empty(N * 64, dtype=torch.uint8, device="cuda")
+    d_bnd = torch.empty(coh.boundary_words(nc) * N, dtype=torch.int32, device="cuda")
+    ctx.eval_traces(d_rec, N, nc, na, 10000, d_res, d_bnd, stream=s)
+    torch.cuda.synchronize()
+    recs = d_rec.cpu().numpy().view(np.uint16)
+    res = d_res.cpu().numpy().view(coh.RESULT_DTYPE)
+    bnd = d_bnd.cpu().numpy().view(np.uint32).reshape(coh.boundary_words(nc), N)
+    k = max(1, min(32, os.cpu_count() or 1))
+    cuts = [N * i // k for i in range(k + 1)]
+
+    def check(i):
+        a, b = cuts[i], cuts[i + 1]
+        w, wb = o.orc_eval(recs, N, nc, na, 10000, t_begin=a, t_end=b)
+        ok = np.array_equal(res[a:b].view(np.uint8), w.view(np.uint8))
+        okb = np.array_equal(bnd[:, a:b], wb.reshape(coh.boundary_words(nc), b - a))
+        return ok and okb
+
+    with cf.ThreadPoolExecutor(k) as ex:
+        assert all(ex.map(check, range(k)))
