@@ -7,7 +7,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "lib", "libcohere_b200.so")
+lib_path = os.environ.get("COH_B200_LIB") or os.path.join(_HERE, "lib", "libcohere_b200.so")
 
 COH_OK, COH_E_CONSTRUCTION, COH_E_DEFECT, COH_E_OVERLAP_CONFLICT, COH_E_CUDA, COH_E_NCCL, COH_E_ARG = range(7)
 _ERR_NAMES = {

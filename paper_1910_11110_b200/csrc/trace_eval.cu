@@ -7,14 +7,16 @@
 //   * per-thread store: one clean u16 slot per array in shared memory (internal.hpp
 //     slot_word: state nibble at bits 2-5 and 8-11), lane-interleaved so a warp's lanes
 //     never conflict whatever arrays they touch:
-//       byte offset = a*256 + (warp>>1)*128 + 4*lane + 2*(warp&1)   ->  bank = lane.
+//       byte offset = (warp>>2)*16K + a*256 + ((warp>>1)&1)*128 + 4*lane + 2*(warp&1)
+//       ->  bank = lane (each 128 threads of a 256-thread block own a 16 KB region).
 //     Slots of arrays >= n_arrays hold the poison word (a missing key).
 //   * call table: 17 rows x 64 u32, addressed by (record & 0xFC) ^ slot (internal.hpp
 //     lut_word); lo16 = the slot word after the call, hi16 = signed accumulator addend.
 //   * records: the record's array byte (bits 8-13) is the slot offset, its type byte
 //     (bits 2-7) XOR the slot is the table offset: per call one masked logic op each,
 //     plus one IMAD.HI per pair to bring the odd call down.  128-bit streaming loads of
-//     8 calls, a ring of 4 loads (32 calls) in flight, continued across traces.
+//     8 calls, two register rings of 4 loads (32 calls each) alternating, continued
+//     across traces; addresses advance by byte increments.
 //   * accumulator (32-bit register): bits 0-6 steps and 7-12 transfers since the last
 //     flush (every 16 calls), 13-19 number of arrays whose abstraction is violated
 //     (boundary_ok <=> acc < 0x2000); a slow entry (stuck / defect / poison) adds -32768,
@@ -33,7 +35,17 @@
 
 namespace cohb {
 
-constexpr int kNT = 128;  // traces (threads) per block
+#ifndef COH_TE_NT
+#define COH_TE_NT 256
+#endif
+#ifndef COH_TE_MINB_DOUBLE
+#define COH_TE_MINB_DOUBLE 4
+#endif
+#ifndef COH_TE_MINB
+#define COH_TE_MINB 5
+#endif
+constexpr int kNT = COH_TE_NT;  // traces (threads) per block
+static_assert(kNT % 128 == 0 && kNT <= 512, "store regions hold 128 threads each");
 constexpr uint32_t kStoreBytes = COH_MAX_ARRAYS * kNT * 2u;
 
 // The block's shared memory, one struct so the hot loop can address the table and the
@@ -166,7 +178,7 @@ __device__ __forceinline__ uint32_t pin_zero(uint32_t x) {
 enum : int { kFuel = 1, kBytes = 2, kRing = 4, kDouble = 8 };
 
 template <int FLAGS>
-__global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? 8 : 10) k_trace_eval(const KParams p) {
+__global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : COH_TE_MINB) k_trace_eval(const KParams p) {
   constexpr bool CHECK_FUEL = FLAGS & kFuel;
   constexpr bool UNIFORM = !(FLAGS & kBytes);
   constexpr bool RING = FLAGS & kRing;
@@ -181,16 +193,18 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? 8 : 10) k_trace_eval(
   if (!UNIFORM)
     for (uint32_t i = tid; i < COH_MAX_ARRAYS; i += kNT) sm.bytes[i] = i < p.n_arrays ? p.array_bytes[i] : 0ull;
   constexpr uint32_t kInit = slot_word(COH_STATE_INITIAL);
-  // slots are array-major (64 x 256 B): u32 word i covers array i / 64
+  // slots are array-major (64 x 256 B per region): u32 word i covers array (i / 64) % 64
   for (uint32_t i = tid; i < kStoreBytes / 4u; i += kNT) {
-    const uint32_t w = (i >> 6) < p.n_arrays ? kInit : kPoisonSlot;
+    const uint32_t w = ((i >> 6) & 63u) < p.n_arrays ? kInit : kPoisonSlot;
     reinterpret_cast<uint32_t*>(sm.store)[i] = w | (w << 16);
   }
   if (tid < COH_N_COUNTERS) sm.cnt[tid] = 0ull;
   __syncthreads();  // the only block barrier: afterwards each thread owns its column
 
   const uint32_t warp = tid >> 5, lane = tid & 31u;
-  const uint32_t toff = (warp >> 1) * 128u + 4u * lane + 2u * (warp & 1u);  // < 256
+  // this thread's u16 column: 128 threads share a 16 KB region (64 array rows of 256 B);
+  // region r sits at r << 14, so (record & 0x3F00) | toff addresses the slot
+  const uint32_t toff = ((warp >> 2) << 14) | ((warp >> 1) & 1u) * 128u + 4u * lane + 2u * (warp & 1u);
   const uint32_t n = p.n_traces;  // < 2^32 (checked by the launcher)
   const uint32_t n_calls = p.n_calls;
   const uint32_t n_chunks = (n_calls + 7u) / 8u;
@@ -278,15 +292,26 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? 8 : 10) k_trace_eval(
         // (which waits for all outstanding loads: they share one scoreboard) has three
         // chunks of lead.  n_groups is even; after the last pair A holds chunks 0..3 of
         // this thread's next trace (RING).
+        // Addresses advance by byte increments (one 64-bit add per load, no wide
+        // multiply).
         uint4* const A = ring;
+        const uint64_t nb = 16ull * n;  // bytes between chunk rows
+        const char* gp = reinterpret_cast<const char*>(p.rec + t) + 4u * nb;  // chunk 4(g+1) of trace t
+#define COH_LOAD4(R, Q)                                                                 \
+  {                                                                                     \
+    const char* q_ = (Q);                                                               \
+    R[0] = __ldcs(reinterpret_cast<const uint4*>(q_));                                  \
+    q_ += nb;                                                                           \
+    R[1] = __ldcs(reinterpret_cast<const uint4*>(q_));                                  \
+    q_ += nb;                                                                           \
+    R[2] = __ldcs(reinterpret_cast<const uint4*>(q_));                                  \
+    q_ += nb;                                                                           \
+    R[3] = __ldcs(reinterpret_cast<const uint4*>(q_));                                  \
+  }
         for (uint32_t g = 0; g < n_groups; g += 2u) {
           i0 = g * 32u;
           COH_CHUNK(A[0], 0)
-          {
-            const uint32_t tz = t + pin_zero(bnd);  // keeps the loads after chunk 0
-#pragma unroll
-            for (int j = 0; j < 4; ++j) B[j] = COH_REC(4u * (g + 1u) + (uint32_t)j, tz);
-          }
+          COH_LOAD4(B, gp + pin_zero(bnd))  // pin: keeps the loads after chunk 0
           COH_CHUNK(A[1], 1) COH_FLUSH
           COH_CHUNK(A[2], 0)
           COH_CHUNK(A[3], 1) COH_FLUSH
@@ -296,15 +321,16 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? 8 : 10) k_trace_eval(
           {
             const bool last = g + 2u >= n_groups;
             const bool nx = RING && last && t + stride < n;
-            const uint32_t tz = (nx ? t + stride : t) + pin_zero(bnd);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) A[j] = COH_REC(last ? (uint32_t)j : 4u * (g + 2u) + (uint32_t)j, tz);
+            COH_LOAD4(A, (last ? reinterpret_cast<const char*>(p.rec + (nx ? t + stride : t)) : gp + 4u * nb) +
+                             pin_zero(bnd))
+            gp += 8u * nb;
           }
           COH_CHUNK(B[1], 1) COH_FLUSH
           COH_CHUNK(B[2], 0)
           COH_CHUNK(B[3], 1) COH_FLUSH
           COH_GROUP_END(g + 1u)
         }
+#undef COH_LOAD4
       } else {
         for (uint32_t g = 0; g < n_groups; ++g) {
           i0 = g * 32u;
