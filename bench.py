@@ -312,7 +312,7 @@ def run_bitmap_primitives(args, ctx):
                                                       re_.data_ptr(), cap, roff.data_ptr(), s))
     runs = int(roff[-1].item())
     out["zero_runs"] = {"ms": t, "runs": runs, "gbs": (m / 8 + 8 * runs) / (t / 1e3) / 1e9,
-                        "note": "count + write passes (the plane is read twice); bytes counted once per SURVEY 8(d)"}
+                        "note": "collect pass reads the plane once; chunks with > 256 runs re-walk it in the place pass"}
     t = timed(lambda: Lb.coh_bitmap_range_set(ctx._h, L.data_ptr(), d_r.data_ptr(), P, s))
     out["range_set"] = {"ms": t, "gbs": m / 8 / (t / 1e3) / 1e9}
     t = timed(lambda: Lb.coh_bitmap_range_clear(ctx._h, L.data_ptr(), d_r.data_ptr(), P, s))

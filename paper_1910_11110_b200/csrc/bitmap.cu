@@ -17,13 +17,11 @@
 // 512-byte access), four steps in flight; a lane finds its range once by binary search and
 // then only advances.  Per-range results (first zero, view flags) accumulate in registers
 // and are flushed with one atomic when the range changes (warp-reduced when the whole warp
-// agrees), so the loop has no barriers and stays HBM-bound.  Zero runs: a count pass over
-// warp chunks, a CUB scan of the counts, and a write pass placing each start / end at its
-// global ascending position (the k-th start and the k-th end are the same run: runs never
-// cross ranges).
+// agrees), so the loop has no barriers and stays HBM-bound.  Zero runs: a collect pass over
+// warp chunks (counts + staged runs), a scan of the chunk counts, and a place pass putting
+// each start / end at its global ascending position (the k-th start and the k-th end are
+// the same run: runs never cross ranges).
 #include <cuda_runtime.h>
-
-#include <cub/cub.cuh>
 
 #include <string>
 
@@ -359,11 +357,41 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
   uint32_t carry = 0;
   bool carry_ok = false;
   for (uint64_t base = f0; base < f1; base += 32ull * kU) {
-    uint32_t rr[kU];
-    uint64_t qa[kU], tf[kU], tl[kU];
-    bool ok[kU], at_start[kU];
-    uint4 v[kU];
+    // Fast iteration (warp-uniform): all 32 x kU quads are interior quads of one range
+    // (then every lane is in the same range, see the monotone advance below), so no
+    // per-quad range tracking, masks or edge loads.
+    if (__all_sync(0xFFFFFFFFu, base + 32ull * kU <= f1 && base + 32ull * kU <= qend && qa0 + base > qtf &&
+                                    qa0 + base + 32ull * kU - 1 < qtl)) {
+      const uint64_t qb = qa0 + base + lane;
+      uint4 v[kU];
 #pragma unroll
+      for (int u = 0; u < kU; ++u) v[u] = __ldcg(reinterpret_cast<const uint4*>(words) + qb + 32ull * u);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t a4 = v[u].x & v[u].y & v[u].z & v[u].w;
+        if (__all_sync(0xFFFFFFFFu, a4 == 0xFFFFFFFFu)) continue;
+        const bool z4 = (v[u].x | v[u].y | v[u].z | v[u].w) == 0u;
+        uint32_t pw = __shfl_up_sync(0xFFFFFFFFu, v[u].w, 1);
+        uint32_t nw = __shfl_down_sync(0xFFFFFFFFu, v[u].x, 1);
+        const uint32_t pw0 = u ? __shfl_sync(0xFFFFFFFFu, v[u ? u - 1 : 0].w, 31) : carry;
+        const uint32_t nw31 = u < kU - 1 ? __shfl_sync(0xFFFFFFFFu, v[u < kU - 1 ? u + 1 : 0].x, 0) : 0u;
+        const uint64_t qa = qb + 32ull * u;
+        if (lane == 0) pw = (u == 0 && !carry_ok) ? __ldg(words + qa * 4 - 1) : pw0;
+        if (lane == 31) nw = u == kU - 1 ? __ldg(words + qa * 4 + 4) : nw31;
+        if (__all_sync(0xFFFFFFFFu, z4) &&
+            !__any_sync(0xFFFFFFFFu, (lane == 0 && (pw >> 31)) || (lane == 31 && (nw & 1u))))
+          continue;  // one zero run continues through the step
+        uint32_t st[4] = {0, 0, 0, 0}, en[4] = {0, 0, 0, 0};
+        if (a4 != 0xFFFFFFFFu) runs_of(F.r + r, qa, true, v[u], pw, nw, st, en);
+        visit(true, base + 32ull * u + lane, r, qa, false, st, en);
+      }
+      carry = __shfl_sync(0xFFFFFFFFu, v[kU - 1].w, 31);
+      carry_ok = true;
+      continue;
+    }
+    // General iteration (range edges, chunk ends): one quad per lane at a time, with
+    // per-lane range tracking and masks; edge neighbours are loaded, not shuffled.
+#pragma unroll 1
     for (int u = 0; u < kU; ++u) {
       const uint64_t f = base + 32ull * u + lane;
       const bool live = f < f1;
@@ -376,107 +404,227 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
         const coh_bitmap_range R = F.r[r];
         qa0 = qa_base(R) - qbeg, qtf = qa_first(R), qtl = qa_last(R);
       }
-      rr[u] = r, qa[u] = qa0 + f, tf[u] = qtf, tl[u] = qtl;
-      ok[u] = live && qa[u] >= qtf && qa[u] <= qtl;
-      at_start[u] = live && f == qbeg;
-      v[u] = ok[u] ? __ldcg(reinterpret_cast<const uint4*>(words) + qa[u]) : make_uint4(~0u, ~0u, ~0u, ~0u);
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      uint32_t pw = __shfl_up_sync(0xFFFFFFFFu, v[u].w, 1);
-      uint32_t nw = __shfl_down_sync(0xFFFFFFFFu, v[u].x, 1);
-      const uint32_t pw0 = u ? __shfl_sync(0xFFFFFFFFu, v[u ? u - 1 : 0].w, 31) : carry;
-      const uint32_t nw31 = u < kU - 1 ? __shfl_sync(0xFFFFFFFFu, v[u < kU - 1 ? u + 1 : 0].x, 0) : 0u;
-      if (lane == 0) pw = pw0;
-      if (lane == 31) nw = nw31;
-      const uint64_t f = base + 32ull * u + lane;
-      const bool in = ok[u] && qa[u] != tf[u] && qa[u] != tl[u];
-      if (ok[u]) {  // neighbours the shuffles could not supply (inside the range only; else masked)
-        if (lane == 0 && u == 0 && !carry_ok && qa[u] != tf[u]) pw = __ldg(words + qa[u] * 4 - 1);
-        if (((lane == 31 && u == kU - 1) || f + 1 >= f1) && qa[u] != tl[u]) nw = __ldg(words + qa[u] * 4 + 4);
+      const uint64_t qa = qa0 + f;
+      const bool ok = live && qa >= qtf && qa <= qtl;
+      const bool first = qa == qtf, last = qa == qtl, in = ok && !first && !last;
+      const uint4 v = ok ? __ldcg(reinterpret_cast<const uint4*>(words) + qa) : make_uint4(~0u, ~0u, ~0u, ~0u);
+      uint32_t pw = __shfl_up_sync(0xFFFFFFFFu, v.w, 1);
+      uint32_t nw = __shfl_down_sync(0xFFFFFFFFu, v.x, 1);
+      if (lane == 0) pw = carry;
+      if (ok) {  // neighbours the shuffles could not supply (inside the range only; else masked)
+        if (lane == 0 && !carry_ok && !first) pw = __ldg(words + qa * 4 - 1);
+        if ((lane == 31 || f + 1 >= f1) && !last) nw = __ldg(words + qa * 4 + 4);
       }
       uint32_t st[4] = {0, 0, 0, 0}, en[4] = {0, 0, 0, 0};
-      if (ok[u] && !(in && (v[u].x & v[u].y & v[u].z & v[u].w) == 0xFFFFFFFFu))
-        runs_of(F.r + rr[u], qa[u], in, v[u], pw, nw, st, en);
-      visit(ok[u], f, rr[u], qa[u], at_start[u], st, en);
+      if (ok && !(in && (v.x & v.y & v.z & v.w) == 0xFFFFFFFFu)) runs_of(F.r + r, qa, in, v, pw, nw, st, en);
+      visit(ok, f, r, qa, live && f == qbeg, st, en);
+      carry = __shfl_sync(0xFFFFFFFFu, v.w, 31);
+      carry_ok = true;
     }
-    carry = __shfl_sync(0xFFFFFFFFu, v[kU - 1].w, 31);
-    carry_ok = true;
   }
 }
 
-// Run extraction in two passes over warp chunks: count (starts and ends separately: a run
-// may start in one chunk and end in a later one), an exclusive scan of the chunk counts,
-// then the write walk placing every start / end at its global ascending position (chunk
-// prefix + warp scan per step), plus run_off for the ranges whose first quad is in the
-// chunk.  (A single-pass decoupled look-back over ticketed chunks was measured slower on
-// B200: the first wave's look-backs walk back over thousands of aggregates.)
-template <bool WRITE>
-__global__ void __launch_bounds__(kBT, 4) k_runs(const uint32_t* words, Flat F, uint64_t* chunk_s, uint64_t* chunk_e,
-                                                 uint32_t* run_start, uint32_t* run_end, uint64_t cap,
-                                                 uint64_t* run_off) {
+// Run extraction.  Collect: each warp walks its chunk once, counting run starts and ends
+// (separately: a run may start in one chunk and end in a later one) and staging the first
+// kRunCap of each, chunk-local and ascending, in scratch, plus the chunk-local start count
+// at the first quad of every range that begins in the chunk.  An exclusive scan of the
+// chunk counts gives every chunk its global offsets.  Place: each warp copies its staged
+// runs to their global positions; only a chunk with more than kRunCap runs walks its
+// quads again.  Sparse planes (the usual sync destination) are therefore read once.  (A
+// single-pass decoupled look-back over ticketed chunks was measured slower on B200: the
+// first wave's look-backs walk back over thousands of aggregates.)
+constexpr uint32_t kRunCap = 256;
+
+// Places the starts / ends of one warp step at chunk-relative (STAGE) or global positions
+// s.., e.. (warp-synchronous; s and e advance by the warp's totals).
+template <bool STAGE>
+__device__ __forceinline__ void place_step(const Flat& F, uint64_t f, uint32_t r, uint64_t qa, bool at_start,
+                                           const uint32_t* st, const uint32_t* en, uint64_t& gs, uint64_t& ge,
+                                           uint32_t* out_s, uint32_t* out_e, uint64_t cap, uint32_t* off_local) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t ns = __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
+  const uint32_t ne = __popc(en[0]) + __popc(en[1]) + __popc(en[2]) + __popc(en[3]);
+  if (!__any_sync(0xFFFFFFFFu, ns || ne || (STAGE && at_start))) return;  // nothing to place in this step
+  uint32_t ps = ns, pe = ne;  // inclusive warp scans
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, ps, o), b = __shfl_up_sync(0xFFFFFFFFu, pe, o);
+    if (lane >= (uint32_t)o) {
+      ps += a;
+      pe += b;
+    }
+  }
+  uint64_t s = gs + ps - ns, e = ge + pe - ne;
+  if (STAGE && at_start)  // the first flat quad of range r (and of the empty ranges just before it)
+    for (int64_t q = r; q >= 0 && F.qp[q] == f; --q) off_local[q] = (uint32_t)s;
+  if (ns | ne) {
+    const uint64_t wbase = qa * 4 - F.r[r].word_off;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t cell0 = (wbase + k) * 32;
+      uint32_t a = st[k], b = en[k];
+      while (a) {
+        if (s < cap) out_s[s] = (uint32_t)(cell0 + __ffs(a) - 1);
+        ++s;
+        a &= a - 1;
+      }
+      while (b) {
+        if (e < cap) out_e[e] = (uint32_t)(cell0 + __ffs(b) - 1);
+        ++e;
+        b &= b - 1;
+      }
+    }
+  }
+  gs += __shfl_sync(0xFFFFFFFFu, ps, 31);
+  ge += __shfl_sync(0xFFFFFFFFu, pe, 31);
+}
+
+// In-place exclusive scans of the chunk start and end counts (n1 = n_chunks + 1 entries
+// each, the last one 0 before and the total after) by one block of NT threads, each
+// summing a stretch of consecutive entries: a few thousand entries.
+template <uint32_t NT>
+__device__ void block_scan_counts(uint64_t* a, uint64_t* b, uint64_t n1) {
+  __shared__ uint64_t wsum[2][NT / 32];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t per = (n1 + NT - 1) / NT, i0 = threadIdx.x * per, i1 = min(i0 + per, n1);
+  uint64_t sa = 0, sb = 0;
+  for (uint64_t i = i0; i < i1; ++i) {
+    sa += __ldcg(a + i);
+    sb += __ldcg(b + i);
+  }
+  uint64_t xa = sa, xb = sb;  // inclusive warp scans
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t ya = __shfl_up_sync(0xFFFFFFFFu, xa, o), yb = __shfl_up_sync(0xFFFFFFFFu, xb, o);
+    if (lane >= (uint32_t)o) {
+      xa += ya;
+      xb += yb;
+    }
+  }
+  if (lane == 31) {
+    wsum[0][warp] = xa;
+    wsum[1][warp] = xb;
+  }
+  __syncthreads();
+  if (warp < 2) {
+    uint64_t w = lane < NT / 32 ? wsum[warp][lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+      if (lane >= (uint32_t)o) w += y;
+    }
+    if (lane < NT / 32) wsum[warp][lane] = w;
+  }
+  __syncthreads();
+  uint64_t ca = (warp ? wsum[0][warp - 1] : 0) + xa - sa, cb = (warp ? wsum[1][warp - 1] : 0) + xb - sb;
+  for (uint64_t i = i0; i < i1; ++i) {
+    const uint64_t va = __ldcg(a + i), vb = __ldcg(b + i);
+    a[i] = ca;
+    b[i] = cb;
+    ca += va;
+    cb += vb;
+  }
+}
+
+// Collect pass.  Per warp chunk: start / end counts (chunk_s, chunk_e) and staged runs;
+// per block: its totals (block_s, block_e).  The last block to finish (ticket) turns the
+// block totals into exclusive scans, so the place pass finds every chunk's global offset
+// as its block's offset plus the counts of the block's earlier warps.
+// counts layout: chunk_s, chunk_e (n_chunks each), block_s, block_e (n_blocks + 1 each),
+// ticket; all zeroed.
+struct RunCounts {
+  uint64_t *chunk_s, *chunk_e, *block_s, *block_e;
+  unsigned int* ticket;
+};
+
+__global__ void __launch_bounds__(kBT, 4) k_runs_collect(const uint32_t* words, Flat F, RunCounts C, uint32_t* stage,
+                                                         uint32_t* off_local) {
+  __shared__ uint64_t ws[2][kBT / 32];
+  __shared__ bool last;
   uint64_t f0, f1, wid;
   warp_chunk(F.qp[F.n], f0, f1, wid);
-  const uint32_t lane = threadIdx.x & 31;
-  if (f0 >= f1) return;
-  if (!WRITE) {
-    uint32_t cs = 0, ce = 0;
-    chunk_runs(words, F, f0, f1, [&](bool, uint64_t, uint32_t, uint64_t, bool, const uint32_t* st, const uint32_t* en) {
-      cs += __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
-      ce += __popc(en[0]) + __popc(en[1]) + __popc(en[2]) + __popc(en[3]);
-    });
-    cs = __reduce_add_sync(0xFFFFFFFFu, cs);
-    ce = __reduce_add_sync(0xFFFFFFFFu, ce);
-    if (lane == 0) {
-      chunk_s[wid] = cs;
-      chunk_e[wid] = ce;
-    }
-    return;
+  uint64_t ls = 0, le = 0;
+  if (f0 < f1) {
+    uint32_t* const ss = stage + wid * (2 * kRunCap);
+    chunk_runs(words, F, f0, f1,
+               [&](bool, uint64_t f, uint32_t r, uint64_t qa, bool at_start, const uint32_t* st, const uint32_t* en) {
+                 place_step<true>(F, f, r, qa, at_start, st, en, ls, le, ss, ss + kRunCap, kRunCap, off_local);
+               });
   }
-  uint64_t gs = chunk_s[wid], ge = chunk_e[wid];
-  chunk_runs(words, F, f0, f1,
-             [&](bool ok, uint64_t f, uint32_t r, uint64_t qa, bool at_start, const uint32_t* st, const uint32_t* en) {
-               const uint32_t ns = __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
-               const uint32_t ne = __popc(en[0]) + __popc(en[1]) + __popc(en[2]) + __popc(en[3]);
-               if (!__any_sync(0xFFFFFFFFu, ns || ne || at_start)) return;  // nothing to place in this step
-               uint32_t ps = ns, pe = ne;  // inclusive warp scans
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    C.chunk_s[wid] = ls;
+    C.chunk_e[wid] = le;
+    ws[0][warp] = ls;
+    ws[1][warp] = le;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t bs = 0, be = 0;
 #pragma unroll
-               for (int o = 1; o < 32; o <<= 1) {
-                 const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, ps, o), b = __shfl_up_sync(0xFFFFFFFFu, pe, o);
-                 if (lane >= (uint32_t)o) {
-                   ps += a;
-                   pe += b;
-                 }
-               }
-               uint64_t s = gs + ps - ns, e = ge + pe - ne;
-               if (at_start)  // the first flat quad of range r (and of the empty ranges just before it)
-                 for (int64_t q = r; q >= 0 && F.qp[q] == f; --q) run_off[q] = s;
-               if (ns | ne) {
-                 const uint64_t wbase = qa * 4 - F.r[r].word_off;
-#pragma unroll
-                 for (int k = 0; k < 4; ++k) {
-                   const uint64_t cell0 = (wbase + k) * 32;
-                   uint32_t a = st[k], b = en[k];
-                   while (a) {
-                     if (s < cap) run_start[s] = (uint32_t)(cell0 + __ffs(a) - 1);
-                     ++s;
-                     a &= a - 1;
-                   }
-                   while (b) {
-                     if (e < cap) run_end[e] = (uint32_t)(cell0 + __ffs(b) - 1);
-                     ++e;
-                     b &= b - 1;
-                   }
-                 }
-               }
-               gs += __shfl_sync(0xFFFFFFFFu, ps, 31);
-               ge += __shfl_sync(0xFFFFFFFFu, pe, 31);
-             });
+    for (int w = 0; w < (int)(kBT / 32); ++w) {
+      bs += ws[0][w];
+      be += ws[1][w];
+    }
+    C.block_s[blockIdx.x] = bs;
+    C.block_e[blockIdx.x] = be;
+    __threadfence();
+    last = atomicAdd(C.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    block_scan_counts<kBT>(C.block_s, C.block_e, (uint64_t)gridDim.x + 1);
+  }
 }
 
-__global__ void k_run_off_tail(const uint64_t* qp, const uint64_t* totals, uint32_t n, uint64_t* run_off) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i <= n && qp[i] >= qp[n]) run_off[i] = totals[0];  // ranges starting at the end: the total
+// global start / end offsets of warp chunk wid
+__device__ __forceinline__ void chunk_offsets(const RunCounts& C, uint64_t wid, uint64_t& gs, uint64_t& ge) {
+  const uint64_t blk = wid / (kBT / 32);
+  gs = __ldcg(C.block_s + blk);
+  ge = __ldcg(C.block_e + blk);
+  for (uint64_t w = blk * (kBT / 32); w < wid; ++w) {
+    gs += __ldcg(C.chunk_s + w);
+    ge += __ldcg(C.chunk_e + w);
+  }
+}
+
+// Place pass, plus run_off[i] = global index of range i's first run: its chunk's offset +
+// the chunk-local count staged by the collect pass; ranges starting at the end get the
+// total.
+__global__ void __launch_bounds__(kBT, 4) k_runs_place(const uint32_t* words, Flat F, RunCounts C,
+                                                       const uint32_t* stage, const uint32_t* off_local,
+                                                       uint32_t* run_start, uint32_t* run_end, uint64_t cap,
+                                                       uint64_t* run_off) {
+  const uint64_t Q = F.qp[F.n], n_chunks = (uint64_t)gridDim.x * (kBT / 32);
+  const uint64_t cper = (((Q + n_chunks - 1) / n_chunks) + 31) & ~31ull;  // as warp_chunk
+  for (uint64_t i = (uint64_t)blockIdx.x * kBT + threadIdx.x; i <= F.n; i += (uint64_t)gridDim.x * kBT) {
+    const uint64_t f = F.qp[i];
+    uint64_t gs = C.block_s[gridDim.x], ge;
+    if (f < Q) {
+      chunk_offsets(C, f / cper, gs, ge);
+      gs += off_local[i];
+    }
+    run_off[i] = gs;
+  }
+  uint64_t f0, f1, wid;
+  warp_chunk(Q, f0, f1, wid);
+  if (f0 >= f1) return;
+  uint64_t gs, ge;
+  chunk_offsets(C, wid, gs, ge);
+  const uint64_t cs = C.chunk_s[wid], ce = C.chunk_e[wid];
+  if (cs <= kRunCap && ce <= kRunCap) {
+    const uint32_t* const ss = stage + wid * (2 * kRunCap);
+    for (uint32_t i = threadIdx.x & 31; i < cs; i += 32)
+      if (gs + i < cap) run_start[gs + i] = ss[i];
+    for (uint32_t i = threadIdx.x & 31; i < ce; i += 32)
+      if (ge + i < cap) run_end[ge + i] = ss[kRunCap + i];
+    return;
+  }
+  chunk_runs(words, F, f0, f1,
+             [&](bool, uint64_t f, uint32_t r, uint64_t qa, bool at_start, const uint32_t* st, const uint32_t* en) {
+               place_step<false>(F, f, r, qa, at_start, st, en, gs, ge, run_start, run_end, cap, nullptr);
+             });
 }
 
 struct Scratch {
@@ -575,26 +723,30 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   if (!n) return COH_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   COH_BM_FLAT(ctx, d_ranges, n, s)
-  const uint64_t n_chunks = (uint64_t)grid_for(ctx) * (kBT / 32);
+  // one wave of the collect pass (the place pass reuses its warp -> chunk mapping)
+  int occ = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_runs_collect, kBT, 0);
+  if (e != cudaSuccess) return fail(ctx, "zero_runs occupancy", e);
+  const int grid = ctx->sms * (occ > 0 ? occ : 1);
+  const uint64_t n_chunks = (uint64_t)grid * (kBT / 32);
+  // scratch: run counts (see RunCounts), staged runs, chunk-local range offsets
+  const size_t counts_b = sizeof(uint64_t) * (2 * n_chunks + 2 * ((size_t)grid + 1) + 1);
+  const size_t stage_b = sizeof(uint32_t) * 2 * kRunCap * n_chunks;
   Scratch co;
   co.s = s;
-  cudaError_t e = cudaMallocAsync(&co.p, sizeof(uint64_t) * 2 * (n_chunks + 1), s);
+  e = cudaMallocAsync(&co.p, counts_b + stage_b + sizeof(uint32_t) * ((size_t)n + 1), s);
   if (e != cudaSuccess) return fail(ctx, "zero_runs scratch", e);
-  uint64_t* chunk = static_cast<uint64_t*>(co.p);
-  uint64_t* chunk_e = chunk + n_chunks + 1;
-  if ((e = cudaMemsetAsync(chunk, 0, sizeof(uint64_t) * 2 * (n_chunks + 1), s)) != cudaSuccess)
-    return fail(ctx, "zero_runs init", e);
-  k_runs<false><<<grid_for(ctx), kBT, 0, s>>>(d_words, F, chunk, chunk_e, nullptr, nullptr, 0, nullptr);
-  size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, chunk, chunk, (int)(n_chunks + 1), s);
-  Scratch sc;
-  sc.s = s;
-  if ((e = cudaMallocAsync(&sc.p, tmp, s)) != cudaSuccess) return fail(ctx, "zero_runs scan scratch", e);
-  cub::DeviceScan::ExclusiveSum(sc.p, tmp, chunk, chunk, (int)(n_chunks + 1), s);
-  cub::DeviceScan::ExclusiveSum(sc.p, tmp, chunk_e, chunk_e, (int)(n_chunks + 1), s);
-  k_runs<true><<<grid_for(ctx), kBT, 0, s>>>(d_words, F, chunk, chunk_e, d_run_start, d_run_end, cap, d_run_off);
-  uint64_t* totals = chunk + n_chunks;  // exclusive scan: entry n_chunks holds the total
-  k_run_off_tail<<<(n + 1 + 255) / 256, 256, 0, s>>>(F.qp, totals, n, d_run_off);
-  ctx->launches += 6;
+  RunCounts C;
+  C.chunk_s = static_cast<uint64_t*>(co.p);
+  C.chunk_e = C.chunk_s + n_chunks;
+  C.block_s = C.chunk_e + n_chunks;
+  C.block_e = C.block_s + grid + 1;
+  C.ticket = reinterpret_cast<unsigned int*>(C.block_e + grid + 1);
+  uint32_t* stage = reinterpret_cast<uint32_t*>(static_cast<char*>(co.p) + counts_b);
+  uint32_t* off_local = stage + 2 * kRunCap * n_chunks;
+  if ((e = cudaMemsetAsync(co.p, 0, counts_b, s)) != cudaSuccess) return fail(ctx, "zero_runs init", e);
+  k_runs_collect<<<grid, kBT, 0, s>>>(d_words, F, C, stage, off_local);
+  k_runs_place<<<grid, kBT, 0, s>>>(d_words, F, C, stage, off_local, d_run_start, d_run_end, cap, d_run_off);
+  ctx->launches += 2;
   return check(ctx, "zero_runs");
 }

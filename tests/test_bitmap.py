@@ -92,3 +92,50 @@ def test_range_set_clear(ctx):
                 want[a: b + 1] = 1 if value else 0
         torch.cuda.synchronize()
         assert np.array_equal(bits_of(dev.cpu().numpy().view(np.uint32)), want)
+
+
+def ref_runs(bits, ranges, n_cells):
+    off, st, en = [0], [], []
+    for r in ranges:
+        a, b = cells(r, n_cells)
+        seg = bits[a: b + 1] if b >= a else bits[:0]
+        d = np.diff(np.concatenate([[1], seg, [1]]).astype(np.int8))
+        st.append(np.nonzero(d == -1)[0] + int(r["lo"]))
+        en.append(np.nonzero(d == 1)[0] - 1 + int(r["lo"]))
+        off.append(off[-1] + len(st[-1]))
+    return np.array(off, np.uint64), np.concatenate(st).astype(np.uint32), np.concatenate(en).astype(np.uint32)
+
+
+@pytest.mark.parametrize("pattern", ["sparse", "dense", "mixed"])
+def test_zero_runs_staging(ctx, pattern):
+    """Zero runs on 2^22-cell planes whose chunks hold few runs (staged once and copied),
+    many runs (over the per-chunk staging capacity: the chunk is walked again) or both,
+    with whole-plane, ragged and empty ranges; plus output truncated at `cap`."""
+    from paper_1910_11110_b200.bitmap import zero_runs
+    rng = np.random.default_rng({"sparse": 1, "dense": 2, "mixed": 3}[pattern])
+    n_cells, n_planes = 1 << 22, 4
+    n = n_planes * n_cells
+    if pattern == "sparse":
+        bits = (rng.random(n) < 0.99995).astype(np.uint8)
+    elif pattern == "dense":
+        bits = (rng.random(n) < 0.5).astype(np.uint8)
+    else:  # dense and sparse stretches alternate
+        bits = np.ones(n, np.uint8)
+        for a in range(0, n, 1 << 18):
+            if rng.random() < 0.5:
+                bits[a: a + (1 << 18)] = rng.random(1 << 18) < 0.4
+            else:
+                bits[a: a + (1 << 18)] = rng.random(1 << 18) < 0.9999
+    ranges = random_ranges(rng, n_planes, n_cells, n_cells // 32, 24)
+    ranges["word_off"][:n_planes] = np.arange(n_planes) * (n_cells // 32)
+    ranges["lo"][:n_planes], ranges["hi"][:n_planes] = 0, n_cells - 1
+    ranges["lo"][n_planes], ranges["hi"][n_planes] = 7, 3  # empty
+    dev = torch.from_numpy(words_of(bits).view(np.int32).copy()).cuda()
+    want_off, want_st, want_en = ref_runs(bits, ranges, n_cells)
+    off, st, en = zero_runs(ctx, dev, ranges, cap=len(want_st) + 5)
+    assert np.array_equal(off, want_off)
+    assert np.array_equal(st, want_st) and np.array_equal(en, want_en)
+    cap = max(1, len(want_st) // 3)
+    off, st, en = zero_runs(ctx, dev, ranges, cap=cap)
+    assert np.array_equal(off, want_off)
+    assert np.array_equal(st, want_st[:cap]) and np.array_equal(en, want_en[:cap])
