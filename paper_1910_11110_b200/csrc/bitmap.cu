@@ -77,6 +77,16 @@ __device__ __forceinline__ void warp_chunk(uint64_t Q, uint64_t& f0, uint64_t& f
   f1 = f0 + per < Q ? f0 + per : Q;
 }
 
+// True (warp-uniform) when the iteration's 32 x kU quads [base, base + 32 kU) are all
+// interior quads of the lanes' current range: then every lane is in that one range (a
+// lane's range only advances, and the iteration lies inside it), and the walkers skip
+// per-quad range tracking (its 64-bit compares dominate the instruction count).
+__device__ __forceinline__ bool interior_iteration(uint64_t base, uint64_t f1, uint64_t qend, uint64_t qa0,
+                                                   uint64_t qtf, uint64_t qtl) {
+  const uint64_t e = base + 32ull * kU;
+  return __all_sync(0xFFFFFFFFu, e <= f1 && e <= qend && qa0 + base > qtf && qa0 + e - 1 < qtl);
+}
+
 // Walks this lane's quads of the warp chunk (lane + 32 j), kU steps per iteration so the
 // loads of several steps are in flight.  body(r, R, qa, interior) for each valid quad;
 // interior = neither the first nor the last quad of its range, i.e. all four words lie
@@ -90,6 +100,11 @@ __device__ __forceinline__ void walk(const Flat& F, uint64_t f0, uint64_t f1, Bo
   coh_bitmap_range R = F.r[r];
   uint64_t qa0 = qa_base(R) - qbeg, qtf = qa_first(R), qtl = qa_last(R);
   for (uint64_t base = f0; base < f1; base += 32ull * kU) {
+    if (interior_iteration(base, f1, qend, qa0, qtf, qtl)) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) body(r, R, qa0 + base + 32ull * u + lane, true);
+      continue;
+    }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const uint64_t f = base + 32ull * u + lane;
@@ -122,10 +137,20 @@ __device__ __forceinline__ void walk_pf(const Flat& F, uint64_t f0, uint64_t f1,
   coh_bitmap_range R0 = F.r[r];
   uint64_t qa0 = qa_base(R0) - qbeg, qtf = qa_first(R0), qtl = qa_last(R0);
   for (uint64_t base = f0; base < f1; base += 32ull * kU) {
+    uint4 v[kU][NP];
+    if (interior_iteration(base, f1, qend, qa0, qtf, qtl)) {
+      const uint64_t qb = qa0 + base + lane;
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+#pragma unroll
+        for (int p = 0; p < NP; ++p) v[u][p] = __ldcs(reinterpret_cast<const uint4*>(planes[p]) + qb + 32ull * u);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) body(r, qb + 32ull * u, true, v[u]);
+      continue;
+    }
     uint32_t rr[kU];
     uint64_t qa[kU];
     bool in[kU], ok[kU];
-    uint4 v[kU][NP];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const uint64_t f = base + 32ull * u + lane;
@@ -360,8 +385,7 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
     // Fast iteration (warp-uniform): all 32 x kU quads are interior quads of one range
     // (then every lane is in the same range, see the monotone advance below), so no
     // per-quad range tracking, masks or edge loads.
-    if (__all_sync(0xFFFFFFFFu, base + 32ull * kU <= f1 && base + 32ull * kU <= qend && qa0 + base > qtf &&
-                                    qa0 + base + 32ull * kU - 1 < qtl)) {
+    if (interior_iteration(base, f1, qend, qa0, qtf, qtl)) {
       const uint64_t qb = qa0 + base + lane;
       uint4 v[kU];
 #pragma unroll
