@@ -19,4 +19,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_el
   -o $OUT/prof_elem_pass1_$TAG -f python scripts/bench_elem.py --reps 1 --buffers 256 > $OUT/ncu_elem_$TAG.txt 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_elem_apply -s 10 -c 1 \
   -o $OUT/prof_elem_apply_$TAG -f python scripts/bench_elem.py --reps 1 --buffers 256 >> $OUT/ncu_elem_$TAG.txt 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_runs_collect -c 1 \
+  -o $OUT/prof_runs_collect_$TAG -f python scripts/bitmap_prims.py > $OUT/ncu_prims_$TAG.txt 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_range_set -s 1 -c 1 \
+  -o $OUT/prof_range_set_$TAG -f python scripts/bitmap_prims.py >> $OUT/ncu_prims_$TAG.txt 2>&1
 echo done
