@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "internal.hpp"
 
@@ -69,7 +70,7 @@ struct KParams {
   uint32_t n_calls;
   uint32_t n_arrays;
   int32_t fuel;
-  uint32_t pad;
+  uint32_t uniform;  // array sizes are all bytes_uniform (else array_bytes)
   uint64_t bytes_uniform;
   const uint64_t* array_bytes;
   const uint32_t* lut;
@@ -472,6 +473,311 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
   }
 }
 
+// ---------------------------------------------------------------------------------
+// k_trace_scan — the latency path for few, long single-array traces (BASELINE C1: one
+// trace of 1000 calls on one array).  One thread per trace is a chain of n_calls
+// dependent table lookups (~50 ns each); here a block evaluates one trace with the calls
+// spread over its threads.  Each call is a function on the 16 states of the array, so the
+// state entering every call is a prefix composition — an associative scan:
+//   1. each thread composes the maps of its kScanCPT consecutive calls (16 start states
+//      stepped through the table in parallel; a start state that reaches a slow entry
+//      — stuck / malformed / missing key — is flagged);
+//   2. a block scan of those maps gives every thread the state entering its first call;
+//   3. each thread re-runs its calls from that state (steps, transfers, boundary bits);
+//      block scans of the steps find the fuel cut-off, a block min the first slow call
+//      (= the stop of run_annotated, modes.hpp:118-121), resolved by the same host-
+//      compiled slow table as the per-thread kernel.
+// Results are field-for-field those of k_trace_eval (tests run both on the same inputs).
+constexpr int kScanNT = 128;   // threads per trace
+constexpr int kScanCPT = 8;    // consecutive calls per thread (one 16-byte record chunk)
+constexpr uint32_t kScanPass = kScanNT * kScanCPT;
+
+// A state map: byte s of the four words = the state reached from start state s (bits
+// 0-3), bit 4 set when a slow entry was reached on the way.  Composition is four PRMT
+// lookups per word (the byte-permute unit indexes 8-byte tables).
+struct StateMap {
+  uint32_t b[4];
+};
+__device__ __forceinline__ StateMap identity_map() { return StateMap{{0x03020100u, 0x07060504u, 0x0B0A0908u, 0x0F0E0D0Cu}}; }
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// m[i_k] for the four index bytes i_k (0..15) of idx
+__device__ __forceinline__ uint32_t lookup4(const StateMap& m, uint32_t idx) {
+  const uint32_t pairs = idx | (idx >> 4);                     // bytes 0 and 2: two indices each
+  const uint32_t sel = prmt(pairs, 0u, 0x0020u) & 0x7777u;     // four 3-bit byte selectors
+  const uint32_t lo = prmt(m.b[0], m.b[1], sel), hi = prmt(m.b[2], m.b[3], sel);
+  const uint32_t upper = prmt(idx << 4, 0u, 0xBA98u);          // 0xFF where index bit 3 is set
+  return (hi & upper) | (lo & ~upper);
+}
+
+__device__ __forceinline__ StateMap compose(const StateMap& a, const StateMap& b) {  // a, then b
+  StateMap c;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) c.b[g] = lookup4(b, a.b[g] & 0x0F0F0F0Fu) | (a.b[g] & 0x10101010u);
+  return c;
+}
+
+__device__ __forceinline__ uint32_t apply_map(const StateMap& m, uint32_t s) {  // byte s
+  const bool up = s & 8u;
+  return prmt(up ? m.b[2] : m.b[0], up ? m.b[3] : m.b[1], s & 7u) & 0xFFu;
+}
+
+__device__ __forceinline__ StateMap shfl_up_map(const StateMap& m, int o) {
+  StateMap r;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) r.b[g] = __shfl_up_sync(0xFFFFFFFFu, m.b[g], o);
+  return r;
+}
+
+// bit s: state s violates its abstraction (!leq(abstract, concrete), modes.hpp:71-75)
+__host__ __device__ constexpr uint32_t violating_mask() {
+  uint32_t m = 0;
+  for (uint32_t s = 0; s < 16; ++s) {
+    const uint32_t a = s >> 2, c = s & 3u;
+    if (!(a == c || (c == 3u && (a == 1u || a == 2u)))) m |= 1u << s;
+  }
+  return m;
+}
+constexpr uint32_t kViolMask = violating_mask();
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red) {  // kScanNT threads; red: kScanNT / 32
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  T t = 0;
+#pragma unroll
+  for (int w = 0; w < kScanNT / 32; ++w) t += red[w];
+  return t;
+}
+
+__device__ __forceinline__ uint32_t rec_of(const uint32_t (&w4)[4], uint32_t k) {  // k compile-time after unrolling
+  return (w4[k >> 1] >> (16u * (k & 1u))) & 0xFFFFu;
+}
+
+#ifdef COH_SCAN_PROFILE
+#define COH_TS(K) \
+  if (threadIdx.x == 0) ts[K] = clock64();
+#else
+#define COH_TS(K)
+#endif
+__global__ void __launch_bounds__(kScanNT) k_trace_scan(const KParams p) {
+#ifdef COH_SCAN_PROFILE
+  long long ts[8];
+  COH_TS(0)
+#endif
+  __shared__ __align__(16) uint32_t lut[kLutEntries];
+  __shared__ StateMap wmap[kScanNT / 32];
+  __shared__ uint32_t wred[kScanNT / 32];
+  __shared__ unsigned long long wred64[kScanNT / 32];
+  __shared__ uint32_t stop_at, s_end, slow_out[5];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t t = blockIdx.x, n = (uint32_t)p.n_traces, nc = p.n_calls;
+  const char* const lutb = reinterpret_cast<const char*>(lut);
+  // the first pass's records and the table: every load in flight at once
+  uint4 ch = tid * kScanCPT < nc ? __ldg(p.rec + (uint64_t)tid * n + t) : make_uint4(0u, 0u, 0u, 0u);
+  {
+    constexpr uint32_t kQ = kLutEntries / 4u, kIt = (kQ + kScanNT - 1) / kScanNT;
+    static_assert(kLutEntries % 4u == 0u, "table in 16-byte pieces");
+    uint4 v[kIt];
+#pragma unroll
+    for (uint32_t j = 0; j < kIt; ++j)
+      if (tid + j * kScanNT < kQ) v[j] = __ldg(reinterpret_cast<const uint4*>(p.lut) + tid + j * kScanNT);
+#pragma unroll
+    for (uint32_t j = 0; j < kIt; ++j)
+      if (tid + j * kScanNT < kQ) reinterpret_cast<uint4*>(lut)[tid + j * kScanNT] = v[j];
+  }
+  __syncthreads();
+  const uint64_t xbytes = p.uniform ? p.bytes_uniform : p.array_bytes[0];
+  uint32_t s_cur = COH_STATE_INITIAL, steps = 0, xfers = 0, viol_blocks = 0, calls_done = nc;
+  uint32_t status = COH_RUN_DONE, stuck_call = 0, stuck_arr = 0, stuck_eff = 0, stuck_flags = 0;
+  bool stopped = false;
+  uint32_t base = 0;
+  for (; base < nc && !stopped; base += kScanPass) {
+    const uint32_t c0 = base + tid * kScanCPT;
+    const uint32_t cnt = c0 < nc ? min((uint32_t)kScanCPT, nc - c0) : 0u;
+    if (base) ch = cnt ? __ldg(p.rec + (uint64_t)(c0 / 8u) * n + t) : make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t w4[4] = {ch.x, ch.y, ch.z, ch.w};
+    COH_TS(1)
+    // 1. this thread's map: the 16 start states stepped through its calls in parallel.
+    //    Slot words (internal.hpp) make the table address one XOR, and an entry's low
+    //    half is the next slot word; slow entries are negative.
+    uint32_t cur[16], sl[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) cur[s] = slot_word((uint32_t)s), sl[s] = 0u;
+    uint32_t miss = 0;
+#pragma unroll
+    for (int k = 0; k < kScanCPT; ++k) {
+      if ((uint32_t)k < cnt) {
+        const uint32_t r = rec_of(w4, k), tw = r & 0xFCu;
+        if (((r >> 8) & 63u) >= p.n_arrays) miss = 0x80000000u;  // missing key
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+          const uint32_t e = *reinterpret_cast<const uint32_t*>(lutb + ((cur[s] ^ tw) & 0xFFFFu));
+          sl[s] |= e;
+          cur[s] = e;
+        }
+      }
+    }
+    StateMap m;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      m.b[g] = 0u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int s = 4 * g + k;
+        m.b[g] |= (((cur[s] >> 8) & 15u) | (((sl[s] | miss) >> 31) << 4)) << (8 * k);
+      }
+    }
+    COH_TS(2)
+    // 2. inclusive block scan of the maps; exclusive = the map before this thread's calls
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const StateMap y = shfl_up_map(m, o);
+      if (lane >= (uint32_t)o) m = compose(y, m);
+    }
+    if (lane == 31) wmap[warp] = m;
+    __syncthreads();
+    StateMap pre = identity_map();
+    for (uint32_t w = 0; w < warp; ++w) pre = compose(pre, wmap[w]);
+    StateMap ex = shfl_up_map(m, 1);
+    ex = lane ? compose(pre, ex) : pre;
+    const uint32_t v_in = apply_map(ex, s_cur);
+    const bool dead = v_in & 0x10u;  // an earlier call of the pass is slow
+    COH_TS(3)
+    // 3. re-run this thread's calls from the entry state: cumulative steps / transfers
+    //    after call k, state before call k, boundary bits
+    uint32_t cs[kScanCPT], cx[kScanCPT], sb[kScanCPT];
+    uint32_t ok_bits = 0, vbits = 0, first_slow = kScanCPT;
+    uint32_t sw = slot_word(v_in & 15u), acc = 0, xacc = 0;
+#pragma unroll
+    for (int k = 0; k < kScanCPT; ++k) {
+      sb[k] = (sw >> 8) & 15u;
+      if ((uint32_t)k < cnt && first_slow == kScanCPT && !dead) {
+        const uint32_t r = rec_of(w4, k);
+        const uint32_t e = *reinterpret_cast<const uint32_t*>(lutb + ((sw ^ (r & 0xFCu)) & 0xFFFFu));
+        if ((int32_t)e < 0 || ((r >> 8) & 63u) >= p.n_arrays) {
+          first_slow = k;
+        } else {
+          acc += (e >> 16) & kAccSteps;
+          xacc += (e >> (16 + kAccXferShift)) & 0x3Fu;
+          sw = e;
+          if ((kViolMask >> ((e >> 8) & 15u)) & 1u) vbits |= 1u << k;
+          else ok_bits |= 1u << k;
+        }
+      }
+      cs[k] = acc;
+      cx[k] = xacc;
+    }
+    COH_TS(4)
+    // fuel: the steps of the pass before this thread's calls (exclusive block scan); a
+    // call is the slow one if its steps overrun the fuel left
+    uint32_t ps = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, ps, o);
+      if (lane >= (uint32_t)o) ps += y;
+    }
+    if (lane == 31) wred[warp] = ps;
+    if (tid == 0) stop_at = 0xFFFFFFFFu;
+    __syncthreads();
+    uint32_t before = ps - acc;
+    for (uint32_t w = 0; w < warp; ++w) before += wred[w];
+    const int fuel_left = p.fuel - (int)steps;
+    uint32_t stop_k = first_slow;
+#pragma unroll
+    for (int k = kScanCPT - 1; k >= 0; --k)
+      if ((uint32_t)k < first_slow && (int)(before + cs[k]) > fuel_left) stop_k = (uint32_t)k;
+    if (stop_k < cnt) atomicMin(&stop_at, c0 + stop_k);
+    if (cnt && c0 + cnt == min(nc, base + kScanPass)) s_end = (sw >> 8) & 15u;
+    __syncthreads();
+    const uint32_t i = stop_at;  // the pass's first slow call, if any
+    const uint32_t keep = i == 0xFFFFFFFFu ? cnt : (i <= c0 ? 0u : min(cnt, i - c0));  // completed calls
+    const uint32_t km = (1u << keep) - 1u;
+    if (p.bnd) {  // boundary words: four threads per 32-call group
+      uint32_t word = (ok_bits & km) << (8u * (tid & 3u));
+      word |= __shfl_xor_sync(0xFFFFFFFFu, word, 1);
+      word |= __shfl_xor_sync(0xFFFFFFFFu, word, 2);
+      if ((tid & 3u) == 0u && c0 < nc) p.bnd[(uint64_t)(c0 / 32u) * n + t] = word;
+    }
+    uint32_t ks = 0, kx = 0, s_slow = 0;  // cs / cx at call keep - 1, state before call keep
+#pragma unroll
+    for (int k = 0; k < kScanCPT; ++k) {
+      if ((uint32_t)k + 1u == keep) ks = cs[k], kx = cx[k];
+      if ((uint32_t)k == keep) s_slow = sb[k];
+    }
+    COH_TS(5)
+    const unsigned long long sums = block_sum<unsigned long long>(
+        (unsigned long long)ks | ((unsigned long long)kx << 20) | ((unsigned long long)__popc(vbits & km) << 40), wred64);
+    steps += (uint32_t)(sums & 0xFFFFFull);
+    xfers += (uint32_t)((sums >> 20) & 0xFFFFFull);
+    viol_blocks += (uint32_t)(sums >> 40);
+    COH_TS(6)
+    if (i == 0xFFFFFFFFu) {
+      s_cur = s_end;
+    } else {  // resolve the slow call from the slow table (as k_trace_eval's slow path)
+      stopped = true;
+      if (i >= c0 && i < c0 + cnt) {  // keep == i - c0 here
+        const uint32_t k = i - c0;
+        const uint32_t wk = (k & 4u) ? ((k & 2u) ? w4[3] : w4[2]) : ((k & 2u) ? w4[1] : w4[0]);
+        const uint32_t r = (wk >> (16u * (k & 1u))) & 0xFFFFu;
+        const uint32_t a = (r >> 8) & 63u, type = (r >> 2) & 63u;
+        const int rem_i = p.fuel - (int)steps;
+        const uint32_t rem = rem_i <= 0 ? 0u : (rem_i >= 7 ? 7u : (uint32_t)rem_i);
+        const bool missing = a >= p.n_arrays;
+        const uint32_t info = missing ? (uint32_t)COH_RUN_DEFECT : __ldg(p.slow + slow_index(type, s_slow, rem));
+        slow_out[0] = missing ? s_slow : (info >> 7) & 15u;
+        slow_out[1] = (info >> 2) & 7u;
+        slow_out[2] = (info >> 5) & 3u;
+        slow_out[3] = info;
+        slow_out[4] = a;
+      }
+      __syncthreads();
+      const uint32_t info = slow_out[3];
+      s_cur = slow_out[0];
+      steps += slow_out[1];
+      xfers += slow_out[2];
+      status = info & 3u;
+      stuck_call = i;
+      stuck_arr = slow_out[4];
+      stuck_eff = (info >> 11) & 7u;
+      stuck_flags = (info >> 14) & 15u;
+      calls_done = i;
+    }
+    __syncthreads();  // the shared scratch is reused by the next pass
+  }
+  if (p.bnd)  // groups after the stop's pass: no completed calls
+    for (uint32_t g = base / 32u + tid; g < (nc + 31u) / 32u; g += kScanNT) p.bnd[(uint64_t)g * n + t] = 0u;
+  if (tid == 0) {
+#ifdef COH_SCAN_PROFILE
+    COH_TS(7)
+    for (int k = 1; k < 8; ++k) reinterpret_cast<long long*>(p.res + t)[k - 1] = ts[k] - ts[k - 1];
+    return;
+#endif
+    const uint64_t tb = (uint64_t)xfers * xbytes;
+    uint4* out = reinterpret_cast<uint4*>(p.res + t);
+    __stcs(out + 0, make_uint4(s_cur, 0u, 0u, 0u));
+    __stcs(out + 1, make_uint4(0u, 0u, 0u, 0u));
+    __stcs(out + 2, make_uint4((uint32_t)tb, (uint32_t)(tb >> 32), steps, xfers));
+    __stcs(out + 3, make_uint4(calls_done, viol_blocks, stuck_call,
+                               status | (stuck_arr << 8) | (stuck_eff << 16) | (stuck_flags << 24)));
+    if (p.counters) {
+      const unsigned long long v[10] = {status == COH_RUN_STUCK, status == COH_RUN_FUEL_EXHAUSTED, viol_blocks != 0u,
+                                        status == COH_RUN_DEFECT, steps, xfers, tb, viol_blocks, calls_done, 1u};
+#pragma unroll
+      for (int k = 0; k < 10; ++k)
+        if (v[k]) atomicAdd(p.counters + k, v[k]);
+    }
+  }
+}
+
 static bool getenv_flag(const char* name) {
   const char* v = getenv(name);
   return v && *v && *v != '0';
@@ -528,7 +834,7 @@ int launch_trace_eval(const TraceLaunch& L, void* stream, std::string* err) {
   kp.n_calls = L.n_calls;
   kp.n_arrays = L.n_arrays;
   kp.fuel = L.fuel;
-  kp.pad = 0;
+  kp.uniform = L.uniform_bytes ? 1u : 0u;
   kp.bytes_uniform = L.bytes_uniform;
   kp.array_bytes = L.d_array_bytes;
   kp.lut = L.d_lut;
@@ -543,6 +849,21 @@ int launch_trace_eval(const TraceLaunch& L, void* stream, std::string* err) {
       *err = std::string("counter memset: ") + cudaGetErrorString(e);
       return COH_E_CUDA;
     }
+  }
+  // Latency path: too few single-array traces to fill the GPU -> a block per trace.
+  // COH_TE_PATH=thread|scan forces one path (tests compare both).
+  const char* path = std::getenv("COH_TE_PATH");
+  bool scan = L.n_arrays == 1u && L.n_calls >= 64u && L.n_traces <= 2ull * (uint64_t)L.sms;
+  if (path && std::strcmp(path, "thread") == 0) scan = false;
+  if (path && std::strcmp(path, "scan") == 0) scan = L.n_arrays == 1u;
+  if (scan) {
+    k_trace_scan<<<(unsigned)L.n_traces, kScanNT, 0, s>>>(kp);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      *err = std::string("trace_scan launch: ") + cudaGetErrorString(e);
+      return COH_E_CUDA;
+    }
+    return COH_OK;
   }
   const int f = (L.check_fuel ? kFuel : 0) | (L.uniform_bytes ? 0 : kBytes) |
                 (L.n_calls % 32u == 0u && L.n_calls >= 32u ? kRing : 0) |
