@@ -521,10 +521,18 @@ def run_ours(args, rank, world, local):
 
     import paper_1910_11110_b200 as coh
 
-    torch.cuda.set_device(local)
+    # one rank per GPU over NCCL.  COH_BENCH_BACKEND=gloo runs the same multi-rank flow
+    # with several ranks sharing GPUs (device = local rank mod device count): a plumbing
+    # check on a one-GPU box, never a scaling number.
+    backend = os.environ.get("COH_BENCH_BACKEND", "nccl")
+    dev = local % torch.cuda.device_count() if backend != "nccl" else local
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    ctx = coh.Context(local)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+    ctx = coh.Context(dev)
     stream = torch.cuda.Stream()
     s = stream.cuda_stream
     from paper_1910_11110_b200 import shard
@@ -549,7 +557,7 @@ def run_ours(args, rank, world, local):
             with torch.cuda.stream(stream):
                 shard.allreduce_counters(d_cnt)  # the only exchange; exact integer sums
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev)
     clocks.start()
     for _ in range(max(3, args.warmup)):
         step()
