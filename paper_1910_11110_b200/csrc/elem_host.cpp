@@ -11,6 +11,7 @@
 //   abstract effects  effect_signature / apply_signature, validity.hpp:79-120 (swap rule
 //                     semantics.hpp:109-130)
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -322,105 +323,91 @@ struct DevBuf {
 
 }  // namespace
 
-extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32_t n,
-                             coh_elem_result* results, uint32_t* planes_out, uint32_t plane_words,
-                             uint8_t* view_abs_out, uint32_t* boundary_out, uint32_t boundary_words,
-                             uint32_t* runs_out, uint64_t runs_cap, coh_elem_stats* stats) {
-  using namespace cohb;
-  if (!ctx) return COH_E_ARG;
-  if (n && (!progs || !results)) {
-    ctx->err = "progs/results is NULL";
-    return COH_E_ARG;
-  }
-  if (n == 0) return COH_OK;
-  ElemPlan plan;
-  std::string err;
-  int rc = elem_compile(progs, n, &plan, &err);
-  if (rc) {
-    ctx->err = err;
-    return rc;
-  }
-  const uint32_t W = ((plan.max_words + kElemTileWords - 1) / kElemTileWords) * kElemTileWords;
-  uint32_t bwords = 1;
-  for (uint32_t b = 0; b < n; ++b) bwords = std::max(bwords, (progs[b].n_calls + 31) / 32);
-  if (planes_out) {  // plane_words must hold every program's cells
-    uint32_t need = 0;
-    for (uint32_t b = 0; b < n; ++b) need = std::max(need, (progs[b].n_cells + 31) / 32);
-    if (plane_words < need) {
-      ctx->err = "plane_words too small";
-      return COH_E_ARG;
-    }
-  }
-  if (boundary_out && boundary_words < bwords) {
-    ctx->err = "boundary_words too small";
-    return COH_E_ARG;
-  }
-  uint32_t max_tiles = 1;
-  for (uint32_t s = 0; s < plan.n_stages; ++s)
-    max_tiles = std::max(max_tiles, plan.stage_tile0[s + 1] - plan.stage_tile0[s]);
-
-  DevBuf planes, ops, tiles, stiles, st, sc, tcnt, tbase, vlo, vhi, ncell, bnd, rlo, rhi;
-  auto alloc = [&](DevBuf& d, size_t bytes) { return cudaMalloc(&d.p, std::max<size_t>(bytes, 16)); };
-#define COH_E(x)                                                  \
-  do {                                                            \
-    cudaError_t e_ = (x);                                         \
-    if (e_ != cudaSuccess) {                                      \
-      ctx->err = std::string(#x) + ": " + cudaGetErrorString(e_); \
-      return COH_E_CUDA;                                          \
-    }                                                             \
+#define COH_E(x)                                            \
+  do {                                                      \
+    cudaError_t e_ = (x);                                   \
+    if (e_ != cudaSuccess) {                                \
+      *err = std::string(#x) + ": " + cudaGetErrorString(e_); \
+      return COH_E_CUDA;                                    \
+    }                                                       \
   } while (0)
-  COH_E(alloc(planes, (size_t)n * 2 * W * 4));
-  COH_E(alloc(ops, plan.ops.size() * sizeof(ElemOp)));
-  COH_E(alloc(tiles, plan.tiles.size() * sizeof(ElemTile)));
-  COH_E(alloc(stiles, plan.sync_tiles.size() * sizeof(ElemTile)));
-  COH_E(alloc(st, (size_t)n * sizeof(ElemState)));
-  COH_E(alloc(sc, (size_t)n * kSlots * sizeof(ElemScratch)));
-  COH_E(alloc(tcnt, (size_t)max_tiles * 4 * 4));
-  COH_E(alloc(tbase, (size_t)max_tiles * 2 * 8));
-  COH_E(alloc(vlo, (size_t)n * COH_MAX_VIEWS * 4));
-  COH_E(alloc(vhi, (size_t)n * COH_MAX_VIEWS * 4));
-  COH_E(alloc(ncell, (size_t)n * 4));
-  COH_E(alloc(bnd, (size_t)n * bwords * 4));
-  if (runs_cap) {
-    COH_E(alloc(rlo, (size_t)n * runs_cap * 4));
-    COH_E(alloc(rhi, (size_t)n * runs_cap * 4));
+
+namespace {
+using namespace cohb;
+
+// One group of programs (buffers) with its own plan, device state and stage chain.  The
+// buffers of different groups are independent, so their stage chains run concurrently on
+// separate streams (branches of one CUDA graph): one chain's per-stage launch, dependency
+// and drain latency is filled by the other's streaming.
+struct ElemGroup {
+  const coh_elem_program* progs = nullptr;
+  uint32_t n = 0, b0 = 0;  // programs [b0, b0 + n) of the batch
+  ElemPlan plan;
+  uint32_t W = 0, bwords = 1;
+  uint64_t runs_cap = 0, launches = 0;
+  DevBuf planes, ops, tiles, stiles, st, sc, tcnt, tbase, vlo, vhi, ncell, bnd, rlo, rhi;
+
+  int compile(std::string* err) {
+    int rc = elem_compile(progs, n, &plan, err);
+    if (rc) return rc;
+    W = ((plan.max_words + kElemTileWords - 1) / kElemTileWords) * kElemTileWords;
+    for (uint32_t b = 0; b < n; ++b) bwords = std::max(bwords, (progs[b].n_calls + 31) / 32);
+    return COH_OK;
   }
-  std::vector<uint32_t> h_vlo((size_t)n * COH_MAX_VIEWS, 0), h_vhi((size_t)n * COH_MAX_VIEWS, 0), h_nc(n);
-  for (uint32_t b = 0; b < n; ++b) {
-    h_nc[b] = progs[b].n_cells;
-    for (uint32_t v = 0; v < progs[b].n_views; ++v) {
-      h_vlo[(size_t)b * COH_MAX_VIEWS + v] = progs[b].view_lo[v];
-      h_vhi[(size_t)b * COH_MAX_VIEWS + v] = progs[b].view_hi[v];
+
+  int prepare(cudaStream_t s, std::string* err) {  // allocations and uploads (outside the graph)
+    uint32_t max_tiles = 1;
+    for (uint32_t g = 0; g < plan.n_stages; ++g)
+      max_tiles = std::max(max_tiles, plan.stage_tile0[g + 1] - plan.stage_tile0[g]);
+    auto alloc = [&](DevBuf& d, size_t bytes) { return cudaMalloc(&d.p, std::max<size_t>(bytes, 16)); };
+    COH_E(alloc(planes, (size_t)n * 2 * W * 4));
+    COH_E(alloc(ops, plan.ops.size() * sizeof(ElemOp)));
+    COH_E(alloc(tiles, plan.tiles.size() * sizeof(ElemTile)));
+    COH_E(alloc(stiles, plan.sync_tiles.size() * sizeof(ElemTile)));
+    COH_E(alloc(st, (size_t)n * sizeof(ElemState)));
+    COH_E(alloc(sc, (size_t)n * kSlots * sizeof(ElemScratch)));
+    COH_E(alloc(tcnt, (size_t)max_tiles * 4 * 4));
+    COH_E(alloc(tbase, (size_t)max_tiles * 2 * 8));
+    COH_E(alloc(vlo, (size_t)n * COH_MAX_VIEWS * 4));
+    COH_E(alloc(vhi, (size_t)n * COH_MAX_VIEWS * 4));
+    COH_E(alloc(ncell, (size_t)n * 4));
+    COH_E(alloc(bnd, (size_t)n * bwords * 4));
+    if (runs_cap) {
+      COH_E(alloc(rlo, (size_t)n * runs_cap * 4));
+      COH_E(alloc(rhi, (size_t)n * runs_cap * 4));
     }
+    std::vector<uint32_t> h_vlo((size_t)n * COH_MAX_VIEWS, 0), h_vhi((size_t)n * COH_MAX_VIEWS, 0), h_nc(n);
+    for (uint32_t b = 0; b < n; ++b) {
+      h_nc[b] = progs[b].n_cells;
+      for (uint32_t v = 0; v < progs[b].n_views; ++v) {
+        h_vlo[(size_t)b * COH_MAX_VIEWS + v] = progs[b].view_lo[v];
+        h_vhi[(size_t)b * COH_MAX_VIEWS + v] = progs[b].view_hi[v];
+      }
+    }
+    std::vector<ElemScratch> h_sc((size_t)n * kSlots);
+    for (auto& x : h_sc) {
+      x.first_zero = kNoCell;
+      for (auto& f : x.view_flags) f = 0;
+    }
+    COH_E(cudaMemcpyAsync(ops.p, plan.ops.data(), plan.ops.size() * sizeof(ElemOp), cudaMemcpyHostToDevice, s));
+    if (!plan.tiles.empty())
+      COH_E(cudaMemcpyAsync(tiles.p, plan.tiles.data(), plan.tiles.size() * sizeof(ElemTile), cudaMemcpyHostToDevice,
+                            s));
+    if (!plan.sync_tiles.empty())
+      COH_E(cudaMemcpyAsync(stiles.p, plan.sync_tiles.data(), plan.sync_tiles.size() * sizeof(ElemTile),
+                            cudaMemcpyHostToDevice, s));
+    COH_E(cudaMemcpyAsync(vlo.p, h_vlo.data(), h_vlo.size() * 4, cudaMemcpyHostToDevice, s));
+    COH_E(cudaMemcpyAsync(vhi.p, h_vhi.data(), h_vhi.size() * 4, cudaMemcpyHostToDevice, s));
+    COH_E(cudaMemcpyAsync(ncell.p, h_nc.data(), h_nc.size() * 4, cudaMemcpyHostToDevice, s));
+    COH_E(cudaMemcpyAsync(sc.p, h_sc.data(), h_sc.size() * sizeof(ElemScratch), cudaMemcpyHostToDevice, s));
+    COH_E(cudaMemsetAsync(st.p, 0, (size_t)n * sizeof(ElemState), s));
+    COH_E(cudaMemsetAsync(bnd.p, 0, (size_t)n * bwords * 4, s));
+    return cudaStreamSynchronize(s) == cudaSuccess ? COH_OK : COH_E_CUDA;  // host vectors die here
   }
-  std::vector<ElemScratch> h_sc((size_t)n * kSlots);
-  for (auto& x : h_sc) {
-    x.first_zero = kNoCell;
-    for (auto& f : x.view_flags) f = 0;
-  }
-  if (!ctx->hs[0]) COH_E(cudaStreamCreateWithFlags(&ctx->hs[0], cudaStreamNonBlocking));
-  cudaStream_t s = ctx->hs[0];
-  COH_E(cudaMemcpyAsync(ops.p, plan.ops.data(), plan.ops.size() * sizeof(ElemOp), cudaMemcpyHostToDevice, s));
-  if (!plan.tiles.empty())
-    COH_E(cudaMemcpyAsync(tiles.p, plan.tiles.data(), plan.tiles.size() * sizeof(ElemTile), cudaMemcpyHostToDevice, s));
-  if (!plan.sync_tiles.empty())
-    COH_E(cudaMemcpyAsync(stiles.p, plan.sync_tiles.data(), plan.sync_tiles.size() * sizeof(ElemTile),
-                          cudaMemcpyHostToDevice, s));
-  COH_E(cudaMemcpyAsync(vlo.p, h_vlo.data(), h_vlo.size() * 4, cudaMemcpyHostToDevice, s));
-  COH_E(cudaMemcpyAsync(vhi.p, h_vhi.data(), h_vhi.size() * 4, cudaMemcpyHostToDevice, s));
-  COH_E(cudaMemcpyAsync(ncell.p, h_nc.data(), h_nc.size() * 4, cudaMemcpyHostToDevice, s));
-  COH_E(cudaMemcpyAsync(sc.p, h_sc.data(), h_sc.size() * sizeof(ElemScratch), cudaMemcpyHostToDevice, s));
-  COH_E(cudaMemsetAsync(st.p, 0, (size_t)n * sizeof(ElemState), s));
-  COH_E(cudaMemsetAsync(bnd.p, 0, (size_t)n * bwords * 4, s));
-  cudaEvent_t e0, e1;
-  COH_E(cudaEventCreate(&e0));
-  COH_E(cudaEventCreate(&e1));
-  // The whole stage sequence (init + 2-3 kernels per stage) is static once compiled:
-  // capture it into a CUDA graph so the per-stage launch gaps disappear.
-  uint64_t launches = 0;
-  auto enqueue = [&]() -> int {
+
+  int enqueue(cudaStream_t s, std::string* err) {  // init + every stage (captured into the graph)
     launches = 1;
-    int r = launch_elem_init(planes.as<uint32_t>(), W, ncell.as<uint32_t>(), n, s, &err);
+    int r = launch_elem_init(planes.as<uint32_t>(), W, ncell.as<uint32_t>(), n, s, err);
     for (uint32_t stg = 0; stg < plan.n_stages && r == COH_OK; ++stg) {
       ElemDev d;
       d.planes = planes.as<uint32_t>();
@@ -443,16 +430,99 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
       d.stage = stg;
       const uint32_t nt = plan.stage_tile0[stg + 1] - plan.stage_tile0[stg];
       const uint32_t ns = plan.stage_sync0[stg + 1] - plan.stage_sync0[stg];
-      r = launch_elem_stage(d, nt, ns, s, &err);
+      r = launch_elem_stage(d, nt, ns, s, err);
       launches += (nt ? 2 : 0) + (ns ? 1 : 0);
     }
     return r;
+  }
+};
+
+}  // namespace
+
+static int elem_eval_impl(coh_ctx* ctx, const coh_elem_program* progs, uint32_t n, coh_elem_result* results,
+                          uint32_t* planes_out, uint32_t plane_words, uint8_t* view_abs_out, uint32_t* boundary_out,
+                          uint32_t boundary_words, uint32_t* runs_out, uint64_t runs_cap, coh_elem_stats* stats,
+                          std::string* err) {
+  std::string& err_s = *err;
+  // concurrent stage chains (one per group of >= 32 buffers, up to kChains)
+  constexpr uint32_t kChains = 4;
+  const char* gv = std::getenv("COH_ELEM_CHAINS");
+  const uint32_t gmax = gv ? std::max(1, std::min((int)kChains, std::atoi(gv))) : kChains;
+  const uint32_t G = std::max(1u, std::min(gmax, n / 32u));
+  std::vector<ElemGroup> grp(G);
+  for (uint32_t g = 0; g < G; ++g) {
+    grp[g].b0 = (uint32_t)((uint64_t)n * g / G);
+    grp[g].n = (uint32_t)((uint64_t)n * (g + 1) / G) - grp[g].b0;
+    grp[g].progs = progs + grp[g].b0;
+    grp[g].runs_cap = runs_cap;
+    int rc = grp[g].compile(err);
+    if (rc) {
+      ctx->err = err_s;
+      return rc;
+    }
+  }
+  if (planes_out) {  // plane_words must hold every program's cells
+    uint32_t need = 0;
+    for (uint32_t b = 0; b < n; ++b) need = std::max(need, (progs[b].n_cells + 31) / 32);
+    if (plane_words < need) {
+      ctx->err = "plane_words too small";
+      return COH_E_ARG;
+    }
+  }
+  uint32_t bwords = 1;
+  for (auto& g : grp) bwords = std::max(bwords, g.bwords);
+  if (boundary_out && boundary_words < bwords) {
+    ctx->err = "boundary_words too small";
+    return COH_E_ARG;
+  }
+  if (!ctx->hs[0] && cudaStreamCreateWithFlags(&ctx->hs[0], cudaStreamNonBlocking) != cudaSuccess) {
+    ctx->err = "stream create";
+    return COH_E_CUDA;
+  }
+  struct Streams {  // the chains' extra streams (branches of the captured graph)
+    cudaStream_t s[kChains] = {};
+    ~Streams() {
+      for (uint32_t k = 1; k < kChains; ++k)
+        if (s[k]) cudaStreamDestroy(s[k]);
+    }
+  } st_;
+  st_.s[0] = ctx->hs[0];
+  for (uint32_t k = 1; k < G; ++k) COH_E(cudaStreamCreateWithFlags(&st_.s[k], cudaStreamNonBlocking));
+  cudaStream_t* strm = st_.s;
+  cudaStream_t s = strm[0];
+  for (auto& g : grp) {
+    const int rc = g.prepare(s, err);
+    if (rc) {
+      ctx->err = err_s.empty() ? std::string("element upload failed") : err_s;
+      return rc;
+    }
+  }
+  cudaEvent_t e0, e1, fork, join[kChains];
+  COH_E(cudaEventCreate(&e0));
+  COH_E(cudaEventCreate(&e1));
+  COH_E(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  for (uint32_t k = 0; k < kChains; ++k) COH_E(cudaEventCreateWithFlags(&join[k], cudaEventDisableTiming));
+  // The stage sequences are static once compiled: capture them into one CUDA graph (the
+  // groups g > 0 fork onto their own streams and join back) so launch gaps disappear.
+  auto enqueue_all = [&]() -> int {
+    COH_E(cudaEventRecord(fork, s));
+    for (uint32_t g = 1; g < G; ++g) COH_E(cudaStreamWaitEvent(strm[g], fork, 0));
+    for (uint32_t g = 0; g < G; ++g) {
+      const int r = grp[g].enqueue(strm[g], err);
+      if (r) return r;
+    }
+    for (uint32_t g = 1; g < G; ++g) {
+      COH_E(cudaEventRecord(join[g], strm[g]));
+      COH_E(cudaStreamWaitEvent(s, join[g], 0));
+    }
+    return COH_OK;
   };
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  int rc = COH_OK;
   bool graphed = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
   if (graphed) {
-    rc = enqueue();
+    rc = enqueue_all();
     graphed = cudaStreamEndCapture(s, &graph) == cudaSuccess && rc == COH_OK &&
               cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
     cudaGetLastError();
@@ -461,30 +531,35 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
   if (graphed) {
     COH_E(cudaGraphLaunch(exec, s));
   } else {
-    rc = enqueue();  // capture unavailable: plain stream launches
+    rc = enqueue_all();  // capture unavailable: plain stream launches
   }
   COH_E(cudaEventRecord(e1, s));
   if (rc) {
-    ctx->err = err;
-    cudaStreamSynchronize(s);
+    ctx->err = err_s;
+    cudaDeviceSynchronize();
     return rc;
   }
-  std::vector<ElemState> h_st(n);
-  COH_E(cudaMemcpyAsync(h_st.data(), st.p, (size_t)n * sizeof(ElemState), cudaMemcpyDeviceToHost, s));
-  std::vector<uint32_t> h_bnd;
-  if (boundary_out) {
-    h_bnd.resize((size_t)n * bwords);
-    COH_E(cudaMemcpyAsync(h_bnd.data(), bnd.p, h_bnd.size() * 4, cudaMemcpyDeviceToHost, s));
-  }
-  if (planes_out)
-    COH_E(cudaMemcpy2DAsync(planes_out, (size_t)plane_words * 4, planes.p, (size_t)W * 4,
-                            (size_t)std::min(plane_words, W) * 4, (size_t)2 * n, cudaMemcpyDeviceToHost, s));
-  std::vector<uint32_t> h_rlo, h_rhi;
-  if (runs_out && runs_cap) {
-    h_rlo.resize((size_t)n * runs_cap);
-    h_rhi.resize((size_t)n * runs_cap);
-    COH_E(cudaMemcpyAsync(h_rlo.data(), rlo.p, h_rlo.size() * 4, cudaMemcpyDeviceToHost, s));
-    COH_E(cudaMemcpyAsync(h_rhi.data(), rhi.p, h_rhi.size() * 4, cudaMemcpyDeviceToHost, s));
+  // downloads, per group
+  std::vector<std::vector<ElemState>> h_st(G);
+  std::vector<std::vector<uint32_t>> h_bnd(G), h_rlo(G), h_rhi(G);
+  for (uint32_t gi = 0; gi < G; ++gi) {
+    ElemGroup& g = grp[gi];
+    h_st[gi].resize(g.n);
+    COH_E(cudaMemcpyAsync(h_st[gi].data(), g.st.p, (size_t)g.n * sizeof(ElemState), cudaMemcpyDeviceToHost, s));
+    if (boundary_out) {
+      h_bnd[gi].resize((size_t)g.n * g.bwords);
+      COH_E(cudaMemcpyAsync(h_bnd[gi].data(), g.bnd.p, h_bnd[gi].size() * 4, cudaMemcpyDeviceToHost, s));
+    }
+    if (planes_out)
+      COH_E(cudaMemcpy2DAsync(planes_out + (size_t)g.b0 * 2 * plane_words, (size_t)plane_words * 4, g.planes.p,
+                              (size_t)g.W * 4, (size_t)std::min(plane_words, g.W) * 4, (size_t)2 * g.n,
+                              cudaMemcpyDeviceToHost, s));
+    if (runs_out && runs_cap) {
+      h_rlo[gi].resize((size_t)g.n * runs_cap);
+      h_rhi[gi].resize((size_t)g.n * runs_cap);
+      COH_E(cudaMemcpyAsync(h_rlo[gi].data(), g.rlo.p, h_rlo[gi].size() * 4, cudaMemcpyDeviceToHost, s));
+      COH_E(cudaMemcpyAsync(h_rhi[gi].data(), g.rhi.p, h_rhi[gi].size() * 4, cudaMemcpyDeviceToHost, s));
+    }
   }
   COH_E(cudaStreamSynchronize(s));
   if (exec) cudaGraphExecDestroy(exec);
@@ -493,74 +568,103 @@ extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  ctx->launches += launches;
-
-  uint64_t alg = plan.alg_bytes;
-  for (uint32_t b = 0; b < n; ++b) {
-    const ElemPlan::Timeline& T = plan.tl[b];
-    const ElemState& S = h_st[b];
-    coh_elem_result& r = results[b];
-    std::memset(&r, 0, sizeof r);
-    r.calls_done = S.calls_done;
-    r.violations = S.violations;
-    r.transfers = S.transfers;
-    r.transfer_cells = S.transfer_cells;
-    r.n_runs = S.n_runs;
-    alg += 8 * S.n_runs;
-    uint32_t abs_final = T.abs_final;
-    uint32_t executed_ops = T.n_ops;
-    if (S.dead) {
-      const uint32_t stage = S.stuck_op / kSlots, slot = S.stuck_op % kSlots;
-      const ElemOp& op = plan.ops[((size_t)stage * n + b) * kSlots + slot];
-      uint32_t k = 0;
-      while (k < T.op_pos.size() && T.op_pos[k] != S.stuck_op) ++k;
-      executed_ops = k;
-      r.status = COH_RUN_STUCK;
-      r.stuck_call = op.call;
-      r.stuck_index = S.stuck_cell;
-      const uint32_t site = op.type == EOP_READ ? op.plane : 0u;
-      r.stuck_effect = (uint8_t)(op.type == EOP_READ ? COH_READ : (op.plane ? COH_PULL : COH_PUSH));
-      r.stuck_flags = (uint8_t)(site | (S.stuck_pair << 2));
-      r.steps = T.steps_before[k] + (op.type == EOP_READ ? (uint64_t)(S.stuck_cell - op.lo) : 0u);
-      abs_final = T.abs_before[k];
-    } else {
-      r.status = T.term_status;
-      r.steps = T.steps_total;
-      if (T.term_status != COH_RUN_DONE) {
-        r.stuck_call = T.term_call;
-        r.stuck_effect = T.term_effect;
-        r.stuck_flags = T.term_flags;
-        r.stuck_index = T.term_index;
+  cudaEventDestroy(fork);
+  for (uint32_t k = 0; k < kChains; ++k) cudaEventDestroy(join[k]);
+  uint64_t launches = 0, alg = 0, n_tiles = 0;
+  uint32_t stages = 0;
+  for (uint32_t gi = 0; gi < G; ++gi) {
+    ElemGroup& g = grp[gi];
+    launches += g.launches;
+    alg += g.plan.alg_bytes;
+    n_tiles += g.plan.tiles.size();
+    stages = std::max(stages, g.plan.n_stages);
+    const uint32_t n_g = g.n;
+    for (uint32_t bl = 0; bl < n_g; ++bl) {
+      const uint32_t b = g.b0 + bl;  // batch index
+      const ElemPlan::Timeline& T = g.plan.tl[bl];
+      const ElemState& S = h_st[gi][bl];
+      coh_elem_result& r = results[b];
+      std::memset(&r, 0, sizeof r);
+      r.calls_done = S.calls_done;
+      r.violations = S.violations;
+      r.transfers = S.transfers;
+      r.transfer_cells = S.transfer_cells;
+      r.n_runs = S.n_runs;
+      alg += 8 * S.n_runs;
+      uint32_t abs_final = T.abs_final;
+      uint32_t executed_ops = T.n_ops;
+      if (S.dead) {
+        const uint32_t stage = S.stuck_op / kSlots, slot = S.stuck_op % kSlots;
+        const ElemOp& op = g.plan.ops[((size_t)stage * n_g + bl) * kSlots + slot];
+        uint32_t k = 0;
+        while (k < T.op_pos.size() && T.op_pos[k] != S.stuck_op) ++k;
+        executed_ops = k;
+        r.status = COH_RUN_STUCK;
+        r.stuck_call = op.call;
+        r.stuck_index = S.stuck_cell;
+        const uint32_t site = op.type == EOP_READ ? op.plane : 0u;
+        r.stuck_effect = (uint8_t)(op.type == EOP_READ ? COH_READ : (op.plane ? COH_PULL : COH_PUSH));
+        r.stuck_flags = (uint8_t)(site | (S.stuck_pair << 2));
+        r.steps = T.steps_before[k] + (op.type == EOP_READ ? (uint64_t)(S.stuck_cell - op.lo) : 0u);
+        abs_final = T.abs_before[k];
+      } else {
+        r.status = T.term_status;
+        r.steps = T.steps_total;
+        if (T.term_status != COH_RUN_DONE) {
+          r.stuck_call = T.term_call;
+          r.stuck_effect = T.term_effect;
+          r.stuck_flags = T.term_flags;
+          r.stuck_index = T.term_index;
+        }
       }
-    }
-    // VectorPU-faithful transfer size: the whole view range of every executed sync
-    for (uint32_t k = 0; k < executed_ops; ++k) {
-      const uint32_t pos = T.op_pos[k];
-      const ElemOp& op = plan.ops[((size_t)(pos / kSlots) * n + b) * kSlots + pos % kSlots];
-      if (op.type == EOP_SYNC) r.vpu_cells += (uint64_t)(op.hi - op.lo + 1);
-    }
-    if (view_abs_out)
-      for (uint32_t v = 0; v < COH_MAX_VIEWS; ++v)
-        view_abs_out[(size_t)b * COH_MAX_VIEWS + v] = v < progs[b].n_views ? (uint8_t)((abs_final >> (2 * v)) & 3u) : 0;
-    if (boundary_out)
-      for (uint32_t w = 0; w < boundary_words; ++w)
-        boundary_out[(size_t)b * boundary_words + w] = w < bwords ? h_bnd[(size_t)b * bwords + w] : 0u;
-    if (runs_out && runs_cap) {
-      const uint64_t m = std::min<uint64_t>(S.n_runs, runs_cap);
-      for (uint64_t k = 0; k < m; ++k) {
-        runs_out[((size_t)b * runs_cap + k) * 2] = h_rlo[(size_t)b * runs_cap + k];
-        runs_out[((size_t)b * runs_cap + k) * 2 + 1] = h_rhi[(size_t)b * runs_cap + k];
+      // VectorPU-faithful transfer size: the whole view range of every executed sync
+      for (uint32_t k = 0; k < executed_ops; ++k) {
+        const uint32_t pos = T.op_pos[k];
+        const ElemOp& op = g.plan.ops[((size_t)(pos / kSlots) * n_g + bl) * kSlots + pos % kSlots];
+        if (op.type == EOP_SYNC) r.vpu_cells += (uint64_t)(op.hi - op.lo + 1);
+      }
+      if (view_abs_out)
+        for (uint32_t v = 0; v < COH_MAX_VIEWS; ++v)
+          view_abs_out[(size_t)b * COH_MAX_VIEWS + v] =
+              v < progs[b].n_views ? (uint8_t)((abs_final >> (2 * v)) & 3u) : 0;
+      if (boundary_out)
+        for (uint32_t w = 0; w < boundary_words; ++w)
+          boundary_out[(size_t)b * boundary_words + w] = w < g.bwords ? h_bnd[gi][(size_t)bl * g.bwords + w] : 0u;
+      if (runs_out && runs_cap) {
+        const uint64_t m = std::min<uint64_t>(S.n_runs, runs_cap);
+        for (uint64_t k = 0; k < m; ++k) {
+          runs_out[((size_t)b * runs_cap + k) * 2] = h_rlo[gi][(size_t)bl * runs_cap + k];
+          runs_out[((size_t)b * runs_cap + k) * 2 + 1] = h_rhi[gi][(size_t)bl * runs_cap + k];
+        }
       }
     }
   }
+  ctx->launches += launches;
   if (stats) {
     stats->device_ms = ms;
     stats->alg_bytes = alg;
     stats->launches = launches;
-    stats->tiles = plan.tiles.size();
-    stats->stages = plan.n_stages;
+    stats->tiles = n_tiles;
+    stats->stages = stages;
     stats->pad = 0;
   }
   return COH_OK;
+}
 #undef COH_E
+
+extern "C" int coh_elem_eval(coh_ctx* ctx, const coh_elem_program* progs, uint32_t n,
+                             coh_elem_result* results, uint32_t* planes_out, uint32_t plane_words,
+                             uint8_t* view_abs_out, uint32_t* boundary_out, uint32_t boundary_words,
+                             uint32_t* runs_out, uint64_t runs_cap, coh_elem_stats* stats) {
+  if (!ctx) return COH_E_ARG;
+  if (n && (!progs || !results)) {
+    ctx->err = "progs/results is NULL";
+    return COH_E_ARG;
+  }
+  if (n == 0) return COH_OK;
+  std::string err;
+  const int rc = elem_eval_impl(ctx, progs, n, results, planes_out, plane_words, view_abs_out, boundary_out,
+                                boundary_words, runs_out, runs_cap, stats, &err);
+  if (rc && !err.empty()) ctx->err = err;
+  return rc;
 }

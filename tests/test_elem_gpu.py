@@ -90,3 +90,17 @@ def test_reference_sample_element_gpu(ctx):
     assert cells == ["VV"] * 3 + ["IV"] + ["VV"] * 6
     assert out["view_abs"][0][0] == 2  # (I,V)
     assert list(map(list, out["runs"][0][:1])) == [[0, 9]]  # the push copies the whole view once
+
+
+def test_two_chain_batch_vs_oracle(ctx):
+    """A batch of >= 64 programs runs as two concurrent stage chains (each half its own
+    plan, with different stage counts): every output still equals the oracle's, and the
+    reference goldens repeated past the threshold still match."""
+    progs = [Program.generate(9, i, (1 << 14) + 97 * i, 8, 6 + (i % 11), 64 + 8 * (i % 5)) for i in range(96)]
+    out = elem_eval(ctx, progs, runs_cap=1 << 14)
+    for i, p in enumerate(progs):
+        compare(out, i, oracle_want(p, 1 << 14), f"prog {i}", runs_cap=1 << 14)
+    items = list(golden_programs()) * 2
+    out = elem_eval(ctx, [p for _, _, p, _ in items])
+    for i, (key, params, p, want) in enumerate(items):
+        compare(out, i, want, key)
