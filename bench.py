@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--sweep-seeds", type=int, default=100000, help="acceptance-sweep seeds (0 = skip)")
     ap.add_argument("--overlap-views", type=int, default=1 << 20, help="overlap registry views (0 = skip)")
     ap.add_argument("--overlap-blocks", type=int, default=1 << 20)
+    ap.add_argument("--c4-traces", type=int, default=1 << 26, help="C4 total traces, split over the ranks (0 = skip)")
     return ap.parse_args()
 
 
@@ -456,6 +457,55 @@ def run_overlap(args, ctx):
     return out
 
 
+def run_c4(args, ctx, rank, world):
+    """BASELINE config 4: 64M traces (C2 format) split over the ranks as contiguous id
+    ranges (strong scaling), each shard generated on its own device; device time of the
+    evaluation (max over ranks), the NCCL allreduce of the counters, and an order-free
+    checksum of every per-trace result (sum over ranks), equal for any rank count."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1910_11110_b200 as coh
+    from paper_1910_11110_b200 import shard
+
+    total = args.c4_traces
+    first, cnt = shard.split_range(rank, world, total)
+    s = torch.cuda.current_stream()
+    d_rec = torch.empty(coh.records_elems(cnt, N_CALLS), dtype=torch.int16, device="cuda")
+    d_res = torch.empty(cnt * 64, dtype=torch.uint8, device="cuda")
+    d_cnt = torch.zeros(16, dtype=torch.int64, device="cuda")
+    ctx.gen_records(SEED, first, cnt, N_CALLS, N_ARRAYS, ADV, d_rec, s.cuda_stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = None
+    for _ in range(3):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0.record(s)
+        ctx.eval_traces_counted(d_rec, cnt, N_CALLS, N_ARRAYS, FUEL, d_res, d_cnt, None, stream=s.cuda_stream)
+        e1.record(s)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    chk = shard.results_checksum(d_res)
+    t = torch.tensor([best], dtype=torch.float64, device="cuda")
+    c = torch.tensor([chk - (1 << 64) if chk >= 1 << 63 else chk], dtype=torch.int64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        shard.allreduce_counters(d_cnt)
+        dist.all_reduce(c)
+    counters = d_cnt.cpu().numpy().view(np.uint64)[:10]
+    ms = float(t.item())
+    calls = int(counters[8] + counters[0] + counters[1] + counters[3])
+    del d_rec, d_res
+    torch.cuda.empty_cache()
+    return {"metric": "C4: 64M traces split over the ranks (strong scaling), calls/s", "traces": total,
+            "traces_per_rank": cnt, "value": calls / (ms / 1e3), "unit": "calls/s", "ms": ms, "scaling": "strong",
+            "checksum": f"{int(c.item()) & ((1 << 64) - 1):016x}",
+            "counters": {n: int(v) for n, v in zip(coh.COUNTER_NAMES, counters)},
+            "note": "device time of one evaluation (best of 3, max over ranks); records generated on each device"}
+
+
 def run_c1(ctx):
     """BASELINE config 1: one trace of 1000 random calls on one array (seed 0, default
     mix), the latency case.  gpu_us: the evaluation as a CUDA graph replayed between two
@@ -638,6 +688,7 @@ def run_ours(args, rank, world, local):
     clocks.stop()
     sweep_info = run_sweep(args, ctx) if (args.sweep_seeds > 0 and rank == 0) else None
     c1 = run_c1(ctx) if rank == 0 else None
+    c4 = run_c4(args, ctx, rank, world) if args.c4_traces > 0 else None
     overlap = run_overlap(args, ctx) if (args.overlap_views > 0 and rank == 0) else None
     container = None
     if args.container_log2_floats > 0 and rank == 0:
@@ -667,7 +718,7 @@ def run_ours(args, rank, world, local):
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms": k_ms,
                          "note": "INT/LSU-issue bound in practice; see profiles/ for pipe utilisation"},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "gpu_launches": launches,
-            "bitmap": bitmap, "container": container, "sweep": sweep_info, "c1": c1, "overlap": overlap,
+            "bitmap": bitmap, "container": container, "sweep": sweep_info, "c1": c1, "c4": c4, "overlap": overlap,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -190,7 +190,32 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
   if ((uint32_t)__cvta_generic_to_shared(&sm) != kSmemBase) __trap();  // layout assumption
 
   const uint32_t tid = threadIdx.x;
-  for (uint32_t i = tid; i < (uint32_t)kLutEntries; i += kNT) sm.lut[i] = p.lut[i];
+  const uint32_t n = p.n_traces;  // < 2^32 (checked by the launcher)
+  const uint32_t n_calls = p.n_calls;
+  const uint32_t n_chunks = (n_calls + 7u) / 8u;
+  // chunk c of trace u: 8 calls, one 128-bit streaming load
+#define COH_REC(C, U) __ldcs(p.rec + (uint64_t)(C) * n + (U))
+  // The first trace's record loads and the table loads go out before the block's set-up,
+  // so their latency overlaps it (the launch's fixed cost).
+  uint4 ring[4];
+  bool ring_ok = false;  // ring already holds chunks 0..3 of this thread's next trace
+  if (blockIdx.x * kNT + tid < n) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      ring[j] = (uint32_t)j < n_chunks ? COH_REC(j, blockIdx.x * kNT + tid) : make_uint4(0u, 0u, 0u, 0u);
+    ring_ok = true;
+  }
+  {
+    constexpr uint32_t kQ = kLutEntries / 4u, kIt = (kQ + kNT - 1) / kNT;
+    static_assert(kLutEntries % 4u == 0u, "table in 16-byte pieces");
+    uint4 v[kIt];
+#pragma unroll
+    for (uint32_t j = 0; j < kIt; ++j)
+      if (tid + j * kNT < kQ) v[j] = __ldg(reinterpret_cast<const uint4*>(p.lut) + tid + j * kNT);
+#pragma unroll
+    for (uint32_t j = 0; j < kIt; ++j)
+      if (tid + j * kNT < kQ) reinterpret_cast<uint4*>(sm.lut)[tid + j * kNT] = v[j];
+  }
   if (!UNIFORM)
     for (uint32_t i = tid; i < COH_MAX_ARRAYS; i += kNT) sm.bytes[i] = i < p.n_arrays ? p.array_bytes[i] : 0ull;
   constexpr uint32_t kInit = slot_word(COH_STATE_INITIAL);
@@ -206,20 +231,13 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
   // this thread's u16 column: 128 threads share a 16 KB region (64 array rows of 256 B);
   // region r sits at r << 14, so (record & 0x3F00) | toff addresses the slot
   const uint32_t toff = ((warp >> 2) << 14) | ((warp >> 1) & 1u) * 128u + 4u * lane + 2u * (warp & 1u);
-  const uint32_t n = p.n_traces;  // < 2^32 (checked by the launcher)
-  const uint32_t n_calls = p.n_calls;
-  const uint32_t n_chunks = (n_calls + 7u) / 8u;
   const uint32_t n_groups = n_calls / 32u;
   const uint32_t stride = gridDim.x * kNT;
-  // chunk c of trace u: 8 calls, one 128-bit streaming load
-#define COH_REC(C, U) __ldcs(p.rec + (uint64_t)(C) * n + (U))
 
-  uint4 ring[4];
   uint4 B[4];  // second ring of the DOUBLE variant
   if (DOUBLE)
 #pragma unroll
     for (int j = 0; j < 4; ++j) B[j] = make_uint4(0u, 0u, 0u, 0u);
-  bool ring_ok = false;  // ring already holds chunks 0..3 of this thread's next trace
 
   for (uint32_t base = blockIdx.x * kNT; base < n; base += stride) {
     const uint32_t t = base + tid;

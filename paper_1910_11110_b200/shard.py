@@ -52,3 +52,23 @@ def allreduce_counters(counters, group=None):
 
     dist.all_reduce(counters[:N_COUNTERS], op=dist.ReduceOp.SUM, group=group)
     return counters
+
+
+_MIX = (0x9E3779B97F4A7C15, 0xC2B2AE3D27D4EB4F, 0x165667B19E3779F9, 0x27D4EB2F165667C5,
+        0x94D049BB133111EB, 0xBF58476D1CE4E5B9, 0x2545F4914F6CDD1D, 0x5851F42D4C957F2D)
+
+
+def results_checksum(d_results) -> int:
+    """Order-free 64-bit checksum of a batch of coh_trace_result records on the device
+    (a torch uint8 tensor): a 64-bit mix of each 64-byte record, summed with wraparound
+    over the records.  Shards of any size and count add up (mod 2^64) to the value of
+    the whole batch, so per-trace equality between G = 1 and G = 8 is
+    one integer compare."""
+    import torch
+
+    x = d_results.view(torch.int64).view(-1, 8)
+    h = torch.zeros(x.shape[0], dtype=torch.int64, device=x.device)
+    for k, mul in enumerate(_MIX):
+        h ^= x[:, k] * (mul - (1 << 64) if mul >= 1 << 63 else mul)
+        h = h * 0x5851F42D4C957F2D + k
+    return int(h.sum().item()) & ((1 << 64) - 1)

@@ -73,3 +73,20 @@ def test_split_range_partitions():
             for first, n in spans:
                 assert first == pos
                 pos += n
+
+
+def test_results_checksum_adds_over_shards():
+    """The C4 cross-G check: the checksum of a batch equals the (mod 2^64) sum of the
+    checksums of any contiguous split of it, and changes when one record does."""
+    import torch
+
+    from paper_1910_11110_b200 import shard
+    rng = np.random.default_rng(4)
+    res = torch.from_numpy(rng.integers(0, 256, 64 * 1000, dtype=np.uint8))
+    whole = shard.results_checksum(res)
+    for world in (1, 2, 3, 8):
+        parts = [shard.split_range(r, world, 1000) for r in range(world)]
+        total = sum(shard.results_checksum(res[64 * f:64 * (f + c)]) for f, c in parts) & ((1 << 64) - 1)
+        assert total == whole
+    res[64 * 517 + 9] ^= 1
+    assert shard.results_checksum(res) != whole

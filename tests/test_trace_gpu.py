@@ -237,3 +237,43 @@ def test_full_size_c2_every_trace_vs_oracle(ctx):
 
     with cf.ThreadPoolExecutor(k) as ex:
         assert all(ex.map(check, range(k)))
+
+
+def test_c4_full_size_shards(ctx):
+    """BASELINE config 4 at full size on one device: 64M traces evaluated as one batch and
+    as 8 contiguous shards (each generated on the device from its id range) give the same
+    per-trace results (order-free checksum of every record) and counters; a sample of the
+    ids = 0 (mod 64) matches the oracle; fused counters equal the separate reduction."""
+    from paper_1910_11110_b200 import shard
+    N, nc, na, adv, seed, G = 1 << 26, 256, 64, 1, 1, 8
+    s = torch.cuda.current_stream().cuda_stream
+    d_rec = torch.empty(coh.records_elems(N, nc), dtype=torch.int16, device="cuda")
+    ctx.gen_records(seed, 0, N, nc, na, adv, d_rec, s)
+    d_res = torch.empty(N * 64, dtype=torch.uint8, device="cuda")
+    d_cnt = torch.zeros(16, dtype=torch.int64, device="cuda")
+    ctx.eval_traces_counted(d_rec, N, nc, na, 10000, d_res, d_cnt, None, stream=s)
+    d_cnt2 = torch.zeros(16, dtype=torch.int64, device="cuda")
+    ctx.reduce_counters(d_res, N, d_cnt2, s)
+    torch.cuda.synchronize()
+    assert torch.equal(d_cnt[:10], d_cnt2[:10])
+    whole = shard.results_checksum(d_res)
+    for t in range(0, N, N // 997 // 64 * 64)[:400]:  # ids = 0 mod 64 across the range
+        w, _ = o.orc_eval(coh.gen_records_host(seed, t, 1, nc, na, adv), 1, nc, na, 10000)
+        assert same(d_res[t * 64:(t + 1) * 64].cpu().numpy().view(coh.RESULT_DTYPE), w), t
+    del d_rec
+    total, cnt_sum = 0, np.zeros(10, np.uint64)
+    for g in range(G):
+        first, cnt = shard.split_range(g, G, N)
+        d_r = torch.empty(coh.records_elems(cnt, nc), dtype=torch.int16, device="cuda")
+        ctx.gen_records(seed, first, cnt, nc, na, adv, d_r, s)
+        d_o = torch.empty(cnt * 64, dtype=torch.uint8, device="cuda")
+        d_c = torch.zeros(16, dtype=torch.int64, device="cuda")
+        ctx.eval_traces_counted(d_r, cnt, nc, na, 10000, d_o, d_c, None, stream=s)
+        torch.cuda.synchronize()
+        assert torch.equal(d_o, d_res[first * 64:(first + cnt) * 64])
+        total = (total + shard.results_checksum(d_o)) & ((1 << 64) - 1)
+        cnt_sum += d_c.cpu().numpy().view(np.uint64)[:10]
+        del d_r, d_o
+    assert total == whole
+    assert np.array_equal(cnt_sum, d_cnt.cpu().numpy().view(np.uint64)[:10])
+    torch.cuda.empty_cache()
