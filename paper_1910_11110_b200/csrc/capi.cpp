@@ -79,8 +79,18 @@ int eval_device(coh_ctx* ctx, const coh_trace_batch* b, const uint16_t* d_record
   L.boundary = d_boundary;
   L.counters = d_counters;
   L.sms = ctx->sms;  // the launcher sizes a persistent grid for the chosen variant
+  // the work-distribution ticket of long launches (more than five rounds of traces per
+  // thread): stream-ordered from the pool, private to this launch (launches of one
+  // context on different streams may run concurrently)
+  unsigned int* ticket = nullptr;
+  if (n_traces > 5ull * 1024ull * (uint64_t)ctx->sms) {
+    COH_CUDA(ctx, cudaMallocAsync(reinterpret_cast<void**>(&ticket), sizeof(unsigned int), s));
+    COH_CUDA(ctx, cudaMemsetAsync(ticket, 0, sizeof(unsigned int), s));
+  }
+  L.ticket = ticket;
   std::string err;
   rc = cohb::launch_trace_eval(L, s, &err);
+  if (ticket) cudaFreeAsync(ticket, s);
   if (rc) {
     ctx->err = err;
     return rc;

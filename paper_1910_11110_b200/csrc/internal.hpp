@@ -93,6 +93,7 @@ struct TraceLaunch {
   uint32_t* boundary;
   uint64_t* counters;  // optional fused counter reduction (device, COH_N_COUNTERS)
   int sms;  // SM count (persistent grid)
+  unsigned int* ticket;  // device, zeroed, private to this launch (dynamic trace batches)
 };
 int launch_trace_eval(const TraceLaunch& p, void* stream, std::string* err);
 void trace_eval_set_smem_attr();

@@ -11,7 +11,8 @@ import paper_1910_11110_b200 as coh  # noqa: E402
 
 ctx = coh.Context(0)
 s = torch.cuda.current_stream().cuda_stream
-nc, na, adv = 256, 64, 1
+nc, na = 256, 64
+adv = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 N = 1 << 24
 d_rec = torch.empty(coh.records_elems(N, nc), dtype=torch.int16, device="cuda")
 d_res = torch.empty(N * 64, dtype=torch.uint8, device="cuda")
