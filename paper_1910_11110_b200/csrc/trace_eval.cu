@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
 #ifdef COH_TE_TIMELINE  // per block: entry, after set-up, exit (debug builds only)
   __syncthreads();
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl2));
-  if (tid == 0) {
+  if (tid == 0 && p.bnd) {
     unsigned long long* tl = reinterpret_cast<unsigned long long*>(p.bnd) + 3 * blockIdx.x;
     tl[0] = tl0, tl[1] = tl1, tl[2] = tl2;
   }
