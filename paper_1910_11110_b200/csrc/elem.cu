@@ -366,10 +366,13 @@ constexpr int kWPL = kElemTileWords / 32;  // 64 words per lane
 __global__ void __launch_bounds__(32 * kApplyWarps, 4) k_elem_apply(const ElemDev d, uint32_t n_sync_tiles) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t gw = blockIdx.x * kApplyWarps + (threadIdx.x >> 5), nw = gridDim.x * kApplyWarps;
+  // descriptors are host-built: the first one loads while the predecessor drains
+  ElemTile next = gw < n_sync_tiles ? d.sync_desc[gw] : ElemTile{};
   griddep_wait();
   griddep_launch();
   for (uint32_t it = gw; it < n_sync_tiles; it += nw) {
-    const ElemTile tile = d.sync_desc[it];
+    const ElemTile tile = next;
+    if (it + nw < n_sync_tiles) next = d.sync_desc[it + nw];
     const uint32_t b = tile.b, tloc = tile.tloc;
     const uint32_t dead = d.st[b].dead;
     const uint4 cnt = tile.type == EOP_SYNC ? *reinterpret_cast<const uint4*>(d.tcnt + 4 * tloc) : make_uint4(0u, 0u, 0u, 0u);
