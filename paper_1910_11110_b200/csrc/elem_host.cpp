@@ -445,7 +445,7 @@ static int elem_eval_impl(coh_ctx* ctx, const coh_elem_program* progs, uint32_t 
                           std::string* err) {
   std::string& err_s = *err;
   // concurrent stage chains (one per group of >= 32 buffers, up to kChains)
-  constexpr uint32_t kChains = 4;
+  constexpr uint32_t kChains = 6;
   const char* gv = std::getenv("COH_ELEM_CHAINS");
   const uint32_t gmax = gv ? std::max(1, std::min((int)kChains, std::atoi(gv))) : kChains;
   const uint32_t G = std::max(1u, std::min(gmax, n / 32u));
