@@ -394,17 +394,20 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
       for (int u = 0; u < kU; ++u) {
         const uint32_t a4 = v[u].x & v[u].y & v[u].z & v[u].w;
         if (__all_sync(0xFFFFFFFFu, a4 == 0xFFFFFFFFu)) continue;
-        const bool z4 = (v[u].x | v[u].y | v[u].z | v[u].w) == 0u;
+        // the words just before and after the step (warp-uniform; the iteration lies
+        // inside the range, so both exist)
+        const uint64_t q0 = qa0 + base + 32ull * u;  // lane 0's quad
+        const uint32_t pw0 = u ? __shfl_sync(0xFFFFFFFFu, v[u ? u - 1 : 0].w, 31)
+                               : (carry_ok ? carry : __ldg(words + q0 * 4 - 1));
+        const uint32_t nw31 = u < kU - 1 ? __shfl_sync(0xFFFFFFFFu, v[u < kU - 1 ? u + 1 : 0].x, 0)
+                                         : __ldg(words + (q0 + 32) * 4);
+        if (__all_sync(0xFFFFFFFFu, (v[u].x | v[u].y | v[u].z | v[u].w) == 0u) && !((pw0 >> 31) | (nw31 & 1u)))
+          continue;  // one zero run continues through the step
         uint32_t pw = __shfl_up_sync(0xFFFFFFFFu, v[u].w, 1);
         uint32_t nw = __shfl_down_sync(0xFFFFFFFFu, v[u].x, 1);
-        const uint32_t pw0 = u ? __shfl_sync(0xFFFFFFFFu, v[u ? u - 1 : 0].w, 31) : carry;
-        const uint32_t nw31 = u < kU - 1 ? __shfl_sync(0xFFFFFFFFu, v[u < kU - 1 ? u + 1 : 0].x, 0) : 0u;
         const uint64_t qa = qb + 32ull * u;
-        if (lane == 0) pw = (u == 0 && !carry_ok) ? __ldg(words + qa * 4 - 1) : pw0;
-        if (lane == 31) nw = u == kU - 1 ? __ldg(words + qa * 4 + 4) : nw31;
-        if (__all_sync(0xFFFFFFFFu, z4) &&
-            !__any_sync(0xFFFFFFFFu, (lane == 0 && (pw >> 31)) || (lane == 31 && (nw & 1u))))
-          continue;  // one zero run continues through the step
+        if (lane == 0) pw = pw0;
+        if (lane == 31) nw = nw31;
         uint32_t st[4] = {0, 0, 0, 0}, en[4] = {0, 0, 0, 0};
         if (a4 != 0xFFFFFFFFu) runs_of(F.r + r, qa, true, v[u], pw, nw, st, en);
         visit(true, base + 32ull * u + lane, r, qa, false, st, en);
