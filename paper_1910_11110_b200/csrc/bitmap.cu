@@ -213,8 +213,52 @@ __global__ void __launch_bounds__(1024) k_quad_prefix(const coh_bitmap_range* r,
   }
 }
 
+// Up to kFusedRanges ranges, every block scans the range list itself into shared memory
+// (F.qp == nullptr on entry) instead of a separate single-block prefix launch.
+constexpr uint32_t kFusedRanges = 1023;
+__device__ __forceinline__ void shared_prefix(Flat& F, uint64_t* s_qp) {
+  if (F.qp) return;
+  __shared__ uint64_t wsum[kBT / 32];
+  constexpr uint32_t kPer = (kFusedRanges + 1) / kBT;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint64_t v[kPer], sum = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < kPer; ++j) {
+    const uint32_t i = tid * kPer + j;
+    v[j] = 0;
+    if (i < F.n) {
+      const coh_bitmap_range R = F.r[i];
+      if (R.lo <= R.hi) v[j] = qa_end(R) - qa_base(R) + 1;
+    }
+    sum += v[j];
+  }
+  uint64_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= (uint32_t)o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  uint64_t e = x - sum;
+  for (uint32_t w = 0; w < warp; ++w) e += wsum[w];
+#pragma unroll
+  for (uint32_t j = 0; j < kPer; ++j) {
+    const uint32_t i = tid * kPer + j;
+    if (i <= F.n) s_qp[i] = e;
+    e += v[j];
+  }
+  __syncthreads();
+  F.qp = s_qp;
+}
+#define COH_BM_PROLOGUE               \
+  __shared__ uint64_t s_qp_[kFusedRanges + 1]; \
+  Flat F = Fg;                        \
+  shared_prefix(F, s_qp_);
+
 template <bool SET>
-__global__ void __launch_bounds__(kBT) k_range_set(uint32_t* words, Flat F) {
+__global__ void __launch_bounds__(kBT) k_range_set(uint32_t* words, Flat Fg) {
+  COH_BM_PROLOGUE
   uint64_t f0, f1, wid;
   warp_chunk(F.qp[F.n], f0, f1, wid);
   walk(F, f0, f1, [&](uint32_t, const coh_bitmap_range& R, uint64_t qa, bool interior) {
@@ -277,7 +321,8 @@ struct Acc {
   }
 };
 
-__global__ void __launch_bounds__(kBT) k_first_zero(const uint32_t* words, Flat F, uint32_t* first) {
+__global__ void __launch_bounds__(kBT) k_first_zero(const uint32_t* words, Flat Fg, uint32_t* first) {
+  COH_BM_PROLOGUE
   uint64_t f0, f1, wid;
   warp_chunk(F.qp[F.n], f0, f1, wid);
   Acc<0> acc;
@@ -300,7 +345,8 @@ __global__ void __launch_bounds__(kBT) k_first_zero(const uint32_t* words, Flat 
   acc.finish();
 }
 
-__global__ void __launch_bounds__(kBT) k_view_flags(const uint32_t* L, const uint32_t* Rp, Flat F, uint32_t* flags) {
+__global__ void __launch_bounds__(kBT) k_view_flags(const uint32_t* L, const uint32_t* Rp, Flat Fg, uint32_t* flags) {
+  COH_BM_PROLOGUE
   uint64_t f0, f1, wid;
   warp_chunk(F.qp[F.n], f0, f1, wid);
   Acc<1> acc;
@@ -564,8 +610,9 @@ struct RunCounts {
   unsigned int* ticket;
 };
 
-__global__ void __launch_bounds__(kBT, 4) k_runs_collect(const uint32_t* words, Flat F, RunCounts C, uint32_t* stage,
+__global__ void __launch_bounds__(kBT, 4) k_runs_collect(const uint32_t* words, Flat Fg, RunCounts C, uint32_t* stage,
                                                          uint32_t* off_local) {
+  COH_BM_PROLOGUE
   __shared__ uint64_t ws[2][kBT / 32];
   __shared__ bool last;
   uint64_t f0, f1, wid;
@@ -619,10 +666,11 @@ __device__ __forceinline__ void chunk_offsets(const RunCounts& C, uint64_t wid, 
 // Place pass, plus run_off[i] = global index of range i's first run: its chunk's offset +
 // the chunk-local count staged by the collect pass; ranges starting at the end get the
 // total.
-__global__ void __launch_bounds__(kBT, 4) k_runs_place(const uint32_t* words, Flat F, RunCounts C,
+__global__ void __launch_bounds__(kBT, 4) k_runs_place(const uint32_t* words, Flat Fg, RunCounts C,
                                                        const uint32_t* stage, const uint32_t* off_local,
                                                        uint32_t* run_start, uint32_t* run_end, uint64_t cap,
                                                        uint64_t* run_off) {
+  COH_BM_PROLOGUE
   const uint64_t Q = F.qp[F.n], n_chunks = (uint64_t)gridDim.x * (kBT / 32);
   const uint64_t cper = (((Q + n_chunks - 1) / n_chunks) + 31) & ~31ull;  // as warp_chunk
   for (uint64_t i = (uint64_t)blockIdx.x * kBT + threadIdx.x; i <= F.n; i += (uint64_t)gridDim.x * kBT) {
@@ -680,15 +728,15 @@ int check(coh_ctx* ctx, const char* what) {
 using namespace cohb;
 
 // flat quad prefix of the ranges, in stream-ordered scratch
-#define COH_BM_FLAT(ctx, d_r, n, s)                                                           \
-  Scratch pre_;                                                                             \
-  pre_.s = s;                                                                               \
-  {                                                                                         \
-    const cudaError_t e_ = cudaMallocAsync(&pre_.p, sizeof(uint64_t) * ((size_t)n + 1), s); \
-    if (e_ != cudaSuccess) return fail(ctx, "bitmap scratch", e_);                         \
-  }                                                                                         \
-  k_quad_prefix<<<1, 1024, 0, s>>>(d_r, n, static_cast<uint64_t*>(pre_.p));                 \
-  ctx->launches++;                                                                          \
+#define COH_BM_FLAT(ctx, d_r, n, s)                                                             \
+  Scratch pre_;                                                                               \
+  pre_.s = s;                                                                                 \
+  if (n > kFusedRanges) { /* else each block scans the ranges itself (shared_prefix) */        \
+    const cudaError_t e_ = cudaMallocAsync(&pre_.p, sizeof(uint64_t) * ((size_t)n + 1), s);   \
+    if (e_ != cudaSuccess) return fail(ctx, "bitmap scratch", e_);                           \
+    k_quad_prefix<<<1, 1024, 0, s>>>(d_r, n, static_cast<uint64_t*>(pre_.p));                 \
+    ctx->launches++;                                                                          \
+  }                                                                                           \
   const Flat F{d_r, static_cast<uint64_t*>(pre_.p), n};
 
 static int range_fill(coh_ctx* ctx, uint32_t* d_words, const coh_bitmap_range* d_r, uint32_t n, bool set, void* stream) {

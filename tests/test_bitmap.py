@@ -46,7 +46,7 @@ def cells(r, n_cells):
     return base + int(r["lo"]), base + int(r["hi"])
 
 
-@pytest.mark.parametrize("n_cells,n_planes,k", [(1 << 12, 5, 200), (1 << 16, 3, 400), (1 << 24, 2, 40)])
+@pytest.mark.parametrize("n_cells,n_planes,k", [(1 << 12, 5, 200), (1 << 16, 3, 400), (1 << 24, 2, 40), (1 << 14, 4, 3000)])
 def test_first_zero_runs_view_check(ctx, n_cells, n_planes, k):
     from paper_1910_11110_b200.bitmap import first_zero, view_check, zero_runs
     rng = np.random.default_rng(n_cells + k)
@@ -76,15 +76,16 @@ def test_first_zero_runs_view_check(ctx, n_cells, n_planes, k):
         assert ok[j] == want, (j, ab[j])
 
 
-def test_range_set_clear(ctx):
+@pytest.mark.parametrize("k", [300, 2500])  # range prefix in each block / a separate scan
+def test_range_set_clear(ctx, k):
     from paper_1910_11110_b200.bitmap import range_set
-    rng = np.random.default_rng(5)
+    rng = np.random.default_rng(5 + k)
     n_cells, n_planes = 1 << 18, 4
     bits, n_words = random_planes(rng, n_planes, n_cells, 0.5)
     dev = torch.from_numpy(words_of(bits).view(np.int32).copy()).cuda()
     want = bits.copy()
     for value in (True, False, True):
-        ranges = random_ranges(rng, n_planes, n_cells, n_words, 300)
+        ranges = random_ranges(rng, n_planes, n_cells, n_words, k)
         range_set(ctx, dev, ranges, value)
         for r in ranges:
             a, b = cells(r, n_cells)
