@@ -552,69 +552,17 @@ __device__ __forceinline__ void place_step(const Flat& F, uint64_t f, uint32_t r
   ge += __shfl_sync(0xFFFFFFFFu, pe, 31);
 }
 
-// In-place exclusive scans of the chunk start and end counts (n1 = n_chunks + 1 entries
-// each, the last one 0 before and the total after) by one block of NT threads, each
-// summing a stretch of consecutive entries: a few thousand entries.
-template <uint32_t NT>
-__device__ void block_scan_counts(uint64_t* a, uint64_t* b, uint64_t n1) {
-  __shared__ uint64_t wsum[2][NT / 32];
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t per = (n1 + NT - 1) / NT, i0 = threadIdx.x * per, i1 = min(i0 + per, n1);
-  uint64_t sa = 0, sb = 0;
-  for (uint64_t i = i0; i < i1; ++i) {
-    sa += __ldcg(a + i);
-    sb += __ldcg(b + i);
-  }
-  uint64_t xa = sa, xb = sb;  // inclusive warp scans
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t ya = __shfl_up_sync(0xFFFFFFFFu, xa, o), yb = __shfl_up_sync(0xFFFFFFFFu, xb, o);
-    if (lane >= (uint32_t)o) {
-      xa += ya;
-      xb += yb;
-    }
-  }
-  if (lane == 31) {
-    wsum[0][warp] = xa;
-    wsum[1][warp] = xb;
-  }
-  __syncthreads();
-  if (warp < 2) {
-    uint64_t w = lane < NT / 32 ? wsum[warp][lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
-      if (lane >= (uint32_t)o) w += y;
-    }
-    if (lane < NT / 32) wsum[warp][lane] = w;
-  }
-  __syncthreads();
-  uint64_t ca = (warp ? wsum[0][warp - 1] : 0) + xa - sa, cb = (warp ? wsum[1][warp - 1] : 0) + xb - sb;
-  for (uint64_t i = i0; i < i1; ++i) {
-    const uint64_t va = __ldcg(a + i), vb = __ldcg(b + i);
-    a[i] = ca;
-    b[i] = cb;
-    ca += va;
-    cb += vb;
-  }
-}
-
 // Collect pass.  Per warp chunk: start / end counts (chunk_s, chunk_e) and staged runs;
-// per block: its totals (block_s, block_e).  The last block to finish (ticket) turns the
-// block totals into exclusive scans, so the place pass finds every chunk's global offset
-// as its block's offset plus the counts of the block's earlier warps.
-// counts layout: chunk_s, chunk_e (n_chunks each), block_s, block_e (n_blocks + 1 each),
-// ticket; all zeroed.
+// per block: its totals (block_s, block_e).  Every place block scans the block totals
+// itself (a few hundred entries), so neither a ticket nor a zeroing memset is needed.
 struct RunCounts {
   uint64_t *chunk_s, *chunk_e, *block_s, *block_e;
-  unsigned int* ticket;
 };
 
 __global__ void __launch_bounds__(kBT, 4) k_runs_collect(const uint32_t* words, Flat Fg, RunCounts C, uint32_t* stage,
                                                          uint32_t* off_local) {
   COH_BM_PROLOGUE
   __shared__ uint64_t ws[2][kBT / 32];
-  __shared__ bool last;
   uint64_t f0, f1, wid;
   warp_chunk(F.qp[F.n], f0, f1, wid);
   uint64_t ls = 0, le = 0;
@@ -642,21 +590,63 @@ __global__ void __launch_bounds__(kBT, 4) k_runs_collect(const uint32_t* words, 
     }
     C.block_s[blockIdx.x] = bs;
     C.block_e[blockIdx.x] = be;
-    __threadfence();
-    last = atomicAdd(C.ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last) {
-    __threadfence();
-    block_scan_counts<kBT>(C.block_s, C.block_e, (uint64_t)gridDim.x + 1);
   }
 }
 
-// global start / end offsets of warp chunk wid
-__device__ __forceinline__ void chunk_offsets(const RunCounts& C, uint64_t wid, uint64_t& gs, uint64_t& ge) {
+// Exclusive scans of a[0..n) and b[0..n) into sa / sb (n + 1 entries, the last = totals),
+// one block of kBT threads, n <= kBT * kPer.
+constexpr uint32_t kMaxCollectBlocks = 2048;
+__device__ void block_scan2(const uint64_t* a, const uint64_t* b, uint32_t n, uint64_t* sa, uint64_t* sb) {
+  constexpr uint32_t kPer = kMaxCollectBlocks / kBT;
+  __shared__ uint64_t wsum[2][kBT / 32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint64_t va[kPer], vb[kPer], xa = 0, xb = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < kPer; ++j) {
+    const uint32_t i = tid * kPer + j;
+    va[j] = i < n ? a[i] : 0;
+    vb[j] = i < n ? b[i] : 0;
+    xa += va[j];
+    xb += vb[j];
+  }
+  const uint64_t ta = xa, tb = xb;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t ya = __shfl_up_sync(0xFFFFFFFFu, xa, o), yb = __shfl_up_sync(0xFFFFFFFFu, xb, o);
+    if (lane >= (uint32_t)o) {
+      xa += ya;
+      xb += yb;
+    }
+  }
+  if (lane == 31) {
+    wsum[0][warp] = xa;
+    wsum[1][warp] = xb;
+  }
+  __syncthreads();
+  uint64_t ea = xa - ta, eb = xb - tb;
+  for (uint32_t w = 0; w < warp; ++w) {
+    ea += wsum[0][w];
+    eb += wsum[1][w];
+  }
+#pragma unroll
+  for (uint32_t j = 0; j < kPer; ++j) {
+    const uint32_t i = tid * kPer + j;
+    if (i <= n) {
+      sa[i] = ea;
+      sb[i] = eb;
+    }
+    ea += va[j];
+    eb += vb[j];
+  }
+  __syncthreads();
+}
+
+// global start / end offsets of warp chunk wid (bs / be: exclusive scans of the block totals)
+__device__ __forceinline__ void chunk_offsets(const RunCounts& C, const uint64_t* bs, const uint64_t* be, uint64_t wid,
+                                              uint64_t& gs, uint64_t& ge) {
   const uint64_t blk = wid / (kBT / 32);
-  gs = __ldcg(C.block_s + blk);
-  ge = __ldcg(C.block_e + blk);
+  gs = bs[blk];
+  ge = be[blk];
   for (uint64_t w = blk * (kBT / 32); w < wid; ++w) {
     gs += __ldcg(C.chunk_s + w);
     ge += __ldcg(C.chunk_e + w);
@@ -671,13 +661,15 @@ __global__ void __launch_bounds__(kBT, 4) k_runs_place(const uint32_t* words, Fl
                                                        uint32_t* run_start, uint32_t* run_end, uint64_t cap,
                                                        uint64_t* run_off) {
   COH_BM_PROLOGUE
+  __shared__ uint64_t bs[kMaxCollectBlocks + 1], be[kMaxCollectBlocks + 1];
+  block_scan2(C.block_s, C.block_e, gridDim.x, bs, be);
   const uint64_t Q = F.qp[F.n], n_chunks = (uint64_t)gridDim.x * (kBT / 32);
   const uint64_t cper = (((Q + n_chunks - 1) / n_chunks) + 31) & ~31ull;  // as warp_chunk
   for (uint64_t i = (uint64_t)blockIdx.x * kBT + threadIdx.x; i <= F.n; i += (uint64_t)gridDim.x * kBT) {
     const uint64_t f = F.qp[i];
-    uint64_t gs = C.block_s[gridDim.x], ge;
+    uint64_t gs = bs[gridDim.x], ge;
     if (f < Q) {
-      chunk_offsets(C, f / cper, gs, ge);
+      chunk_offsets(C, bs, be, f / cper, gs, ge);
       gs += off_local[i];
     }
     run_off[i] = gs;
@@ -686,7 +678,7 @@ __global__ void __launch_bounds__(kBT, 4) k_runs_place(const uint32_t* words, Fl
   warp_chunk(Q, f0, f1, wid);
   if (f0 >= f1) return;
   uint64_t gs, ge;
-  chunk_offsets(C, wid, gs, ge);
+  chunk_offsets(C, bs, be, wid, gs, ge);
   const uint64_t cs = C.chunk_s[wid], ce = C.chunk_e[wid];
   if (cs <= kRunCap && ce <= kRunCap) {
     const uint32_t* const ss = stage + wid * (2 * kRunCap);
@@ -804,8 +796,10 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   if (e != cudaSuccess) return fail(ctx, "zero_runs occupancy", e);
   const int grid = ctx->sms * (occ > 0 ? occ : 1);
   const uint64_t n_chunks = (uint64_t)grid * (kBT / 32);
-  // scratch: run counts (see RunCounts), staged runs, chunk-local range offsets
-  const size_t counts_b = sizeof(uint64_t) * (2 * n_chunks + 2 * ((size_t)grid + 1) + 1);
+  if (grid > (int)kMaxCollectBlocks) return fail(ctx, "zero_runs grid", cudaErrorInvalidConfiguration);
+  // scratch: run counts (see RunCounts, all written by the collect pass), staged runs,
+  // chunk-local range offsets
+  const size_t counts_b = sizeof(uint64_t) * (2 * n_chunks + 2 * (size_t)grid);
   const size_t stage_b = sizeof(uint32_t) * 2 * kRunCap * n_chunks;
   Scratch co;
   co.s = s;
@@ -815,11 +809,9 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   C.chunk_s = static_cast<uint64_t*>(co.p);
   C.chunk_e = C.chunk_s + n_chunks;
   C.block_s = C.chunk_e + n_chunks;
-  C.block_e = C.block_s + grid + 1;
-  C.ticket = reinterpret_cast<unsigned int*>(C.block_e + grid + 1);
+  C.block_e = C.block_s + grid;
   uint32_t* stage = reinterpret_cast<uint32_t*>(static_cast<char*>(co.p) + counts_b);
   uint32_t* off_local = stage + 2 * kRunCap * n_chunks;
-  if ((e = cudaMemsetAsync(co.p, 0, counts_b, s)) != cudaSuccess) return fail(ctx, "zero_runs init", e);
   k_runs_collect<<<grid, kBT, 0, s>>>(d_words, F, C, stage, off_local);
   k_runs_place<<<grid, kBT, 0, s>>>(d_words, F, C, stage, off_local, d_run_start, d_run_end, cap, d_run_off);
   ctx->launches += 2;
