@@ -359,7 +359,52 @@ def run_container(args, ctx):
            "config": {"workload": "C5: 4 x 1 GiB float32 vectors, seeded chain of CPU/GPU components",
                       "vector_bytes": n * 4, "calls": args.container_calls}}
     rt.close()
+    out["views"] = run_container_views(args, ctx)
     return out
+
+
+def run_container_views(args, ctx):
+    """C5 with pvector views: one mother vector of 2^24 float32 cells, 8 overlapping views,
+    a seeded chain of component calls on them (element bodies, closure shadows);
+    every transfer range is one cudaMemcpyAsync.  Bytes and copies must equal the element
+    evaluator's prediction for the same program (and the stuck call, if any)."""
+    from paper_1910_11110_b200 import CohError
+    from paper_1910_11110_b200.container import Runtime
+    from paper_1910_11110_b200.elem import Program, elem_eval
+
+    # element bodies cost one step per cell and the calculus' fuel is an int32: 2^24
+    # cells (64 MiB) x 64 calls stays inside it, so the run completes (status 0 below)
+    n = 1 << min(24, args.container_log2_floats)
+    prog = Program.generate(21, 0, n, 8, args.container_calls, 16, fuel=(1 << 31) - 1)
+    pred = elem_eval(ctx, [prog], want_planes=False, runs_cap=1 << 16)["results"][0]
+    rt = Runtime(ctx)
+    buf = rt.buffer(n, 4)
+    for lo, hi in zip(prog.view_lo, prog.view_hi):
+        buf.view(int(lo), int(hi))
+    stuck_at = None
+    t0 = time.perf_counter()
+    for c in range(prog.n_calls):
+        try:
+            buf.call(prog.calls[c])
+        except CohError:
+            stuck_at = c
+            break
+    rt.sync()
+    dt = time.perf_counter() - t0
+    st = rt.stats()
+    moved = st["h2d_bytes"] + st["d2h_bytes"]
+    copies = st["h2d_copies"] + st["d2h_copies"]
+    rt.close()
+    return {"metric": "view chain: bytes moved == evaluator prediction",
+            "match": moved == 4 * int(pred.transfer_cells) and copies == int(pred.n_runs) and
+            (stuck_at == int(pred.stuck_call) if pred.status == 1 else stuck_at is None),
+            "bytes_moved": moved, "bytes_predicted": 4 * int(pred.transfer_cells), "copies": copies,
+            "runs_predicted": int(pred.n_runs), "calls_done": int(st["calls"]), "stuck_call": stuck_at,
+            "evaluator_status": int(pred.status),
+            "vpu_whole_view_bytes": 4 * int(pred.vpu_cells), "wall_s": dt, "copy_ms": st["copy_ms"],
+            "link_gbs_during_copies": moved / (st["copy_ms"] / 1e3) / 1e9 if st["copy_ms"] else None,
+            "config": {"workload": "C5 views: a 64 MiB float32 mother vector, 8 overlapping views",
+                       "cells": n, "calls": prog.n_calls}}
 
 
 def run_sweep(args, ctx):

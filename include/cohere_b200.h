@@ -329,6 +329,39 @@ typedef struct coh_rt_touch {
 void coh_rt_touch_cpu(void* user, void* stream);
 void coh_rt_touch_gpu(void* user, void* stream);
 
+/* ---- views: VectorPU's pvector<T>(mother, lo, hi) ----------------
+ * A buffer is a mother vector of n_cells elements (pinned host + device copies) whose
+ * validity is element-granular: planes L (CPU valid) and R (GPU valid), bit i of word
+ * i/32, starting at L = 1, R = 0 (program.hpp:174-184).  Views are inclusive cell ranges
+ * of one buffer, in declaration order, each with its abstract pair (starting (V,I)).
+ * coh_rt_call_view runs one component call on the buffer's views exactly as the element
+ * evaluator (coh_elem_eval) runs the same coh_elem_call: the overlap closure (W/RW on
+ * view x adds a same-site RW on every overlapping view, overlap.hpp:182-230), the guards
+ * (a whole-view sync when the abstract flag is not valid at the component's site: stuck
+ * at the first cell whose source bit is 0, otherwise every maximal run of cells whose
+ * destination bit is 0 is copied with one cudaMemcpyAsync, semantics.hpp:155-166), the
+ * abstract writes, then the body ops in order (READ needs the site's bit on its range,
+ * WRITE sets it and clears the other; partial effects persist when a READ gets stuck),
+ * and the component (run only when the block completes).  Copies: pull = D2H before a
+ * CPU component, push = H2D before a GPU component, on the runtime stream.  Stuck returns
+ * COH_E_DEFECT.  Every copy is logged (coh_rt_copy_log) so tests can compare it with the
+ * evaluator's transfer ranges.                                                         */
+typedef struct coh_rt_copy {
+  uint32_t buffer;
+  uint32_t first, last;  /* cells, inclusive */
+  uint32_t h2d;          /* 1 = push (host -> device), 0 = pull */
+} coh_rt_copy;
+int coh_rt_buffer(coh_rt* rt, uint32_t n_cells, uint32_t elem_bytes, uint32_t* id);
+int coh_rt_view(coh_rt* rt, uint32_t buffer, uint32_t lo, uint32_t hi, uint32_t* view_index);
+int coh_rt_call_view(coh_rt* rt, uint32_t buffer, const coh_elem_call* call, coh_rt_fn fn, void* user);
+int coh_rt_view_state(coh_rt* rt, uint32_t buffer, uint32_t view_index, uint8_t* abs_pair);
+/* planes_out: 2 x ceil(n_cells / 32) words (L then R); synchronises the runtime stream */
+int coh_rt_buffer_planes(coh_rt* rt, uint32_t buffer, uint32_t* planes_out);
+void* coh_rt_buffer_host_ptr(coh_rt* rt, uint32_t buffer);
+void* coh_rt_buffer_device_ptr(coh_rt* rt, uint32_t buffer);
+/* copies issued so far, in order: *n = total; up to cap entries are written */
+int coh_rt_copy_log(const coh_rt* rt, coh_rt_copy* out, uint64_t cap, uint64_t* n);
+
 /* ==== general block programs and schedule sweeps ================
  * Programs in the full calculus (scalars + one buffer with overlapping views, several
  * modes per block, element bodies, opaque/validity if and while), generated natively by

@@ -58,7 +58,29 @@ def _register(L):
     L.coh_rt_get_stats.argtypes = [vp, vp]
 
 
+def _register_views(L):
+    vp, u32, u64 = C.c_void_p, C.c_uint32, C.c_uint64
+    L.coh_rt_buffer.restype = C.c_int
+    L.coh_rt_buffer.argtypes = [vp, u32, u32, C.POINTER(u32)]
+    L.coh_rt_view.restype = C.c_int
+    L.coh_rt_view.argtypes = [vp, u32, u32, u32, C.POINTER(u32)]
+    L.coh_rt_call_view.restype = C.c_int
+    L.coh_rt_call_view.argtypes = [vp, u32, vp, vp, vp]
+    L.coh_rt_view_state.restype = C.c_int
+    L.coh_rt_view_state.argtypes = [vp, u32, u32, C.POINTER(C.c_uint8)]
+    L.coh_rt_buffer_planes.restype = C.c_int
+    L.coh_rt_buffer_planes.argtypes = [vp, u32, vp]
+    L.coh_rt_buffer_host_ptr.restype = vp
+    L.coh_rt_buffer_host_ptr.argtypes = [vp, u32]
+    L.coh_rt_buffer_device_ptr.restype = vp
+    L.coh_rt_buffer_device_ptr.argtypes = [vp, u32]
+    L.coh_rt_copy_log.restype = C.c_int
+    L.coh_rt_copy_log.argtypes = [vp, vp, u64, C.POINTER(u64)]
+
+
 _register(lib())
+_register_views(lib())
+COPY_DTYPE = np.dtype([("buffer", "<u4"), ("first", "<u4"), ("last", "<u4"), ("h2d", "<u4")])
 _TOUCH = {0: C.cast(lib().coh_rt_touch_cpu, C.c_void_p).value, 1: C.cast(lib().coh_rt_touch_gpu, C.c_void_p).value}
 
 
@@ -80,6 +102,48 @@ class Vector:
         s = C.c_uint8()
         lib().coh_rt_state(self.rt._h, self.id, C.byref(s))
         return s.value
+
+
+class Buffer:
+    """A mother vector with element-granular validity and views (pvector<T>(mother, lo,
+    hi)): calls are coh_elem_call records on its views, executed with
+    the copies of exactly the cells the element evaluator predicts."""
+
+    def __init__(self, rt, bid, n_cells, elem_bytes):
+        self.rt, self.id, self.n_cells, self.elem_bytes = rt, bid, n_cells, elem_bytes
+        self.views: list[tuple[int, int]] = []
+
+    def view(self, lo: int, hi: int) -> int:
+        vi = C.c_uint32()
+        self.rt.ctx._check(lib().coh_rt_view(self.rt._h, self.id, lo, hi, C.byref(vi)), "coh_rt_view")
+        self.views.append((lo, hi))
+        return vi.value
+
+    def call(self, call, component=None):
+        """One component call (an elem.ElemCall on this buffer's views); component: None
+        (coherence only) or (fn pointer, user pointer).  Raises CohError when stuck."""
+        fn, user = component if component is not None else (None, None)
+        self.rt.ctx._check(lib().coh_rt_call_view(self.rt._h, self.id, C.addressof(call), fn, user), "coh_rt_call_view")
+
+    def view_state(self, v: int) -> int:
+        s = C.c_uint8()
+        lib().coh_rt_view_state(self.rt._h, self.id, v, C.byref(s))
+        return s.value
+
+    def planes(self) -> np.ndarray:
+        w = (self.n_cells + 31) // 32
+        out = np.zeros((2, w), np.uint32)
+        self.rt.ctx._check(lib().coh_rt_buffer_planes(self.rt._h, self.id, out.ctypes.data), "coh_rt_buffer_planes")
+        return out
+
+    @property
+    def host(self) -> np.ndarray:
+        p = lib().coh_rt_buffer_host_ptr(self.rt._h, self.id)
+        return np.ctypeslib.as_array((C.c_uint8 * (self.n_cells * self.elem_bytes)).from_address(p))
+
+    @property
+    def device_ptr(self) -> int:
+        return lib().coh_rt_buffer_device_ptr(self.rt._h, self.id)
 
 
 class Runtime:
@@ -135,6 +199,20 @@ class Runtime:
         rc = lib().coh_rt_call(self._h, s, C.addressof(arr), len(args), fn, user)
         self.ctx._check(rc, "coh_rt_call")
         self.log.append((s, [(v.id, KIND[k]) for v, k in args]))
+
+    def buffer(self, n_cells: int, elem_bytes: int = 4) -> Buffer:
+        bid = C.c_uint32()
+        self.ctx._check(lib().coh_rt_buffer(self._h, n_cells, elem_bytes, C.byref(bid)), "coh_rt_buffer")
+        return Buffer(self, bid.value, n_cells, elem_bytes)
+
+    def copy_log(self) -> np.ndarray:
+        """Every copy issued so far (COPY_DTYPE: buffer, first / last cell, h2d)."""
+        n = C.c_uint64()
+        lib().coh_rt_copy_log(self._h, None, 0, C.byref(n))
+        out = np.zeros(n.value, COPY_DTYPE)
+        if n.value:
+            lib().coh_rt_copy_log(self._h, out.ctypes.data, n.value, C.byref(n))
+        return out
 
     def sync(self):
         self.ctx._check(lib().coh_rt_sync(self._h), "coh_rt_sync")
