@@ -112,3 +112,40 @@ def test_view_data_really_moves(ctx):
         assert buf.view_state(a) == 2 and buf.view_state(b) == 3  # a^ (I,V), b^ (V,V)
     finally:
         rt.close()
+
+
+def test_view_argument_errors_and_stuck_text(ctx):
+    """Construction errors (view outside its buffer, malformed call) and a stuck sync
+    (data valid nowhere the view needs it) come back as the reference's error kinds."""
+    from paper_1910_11110_b200.elem import ElemCall
+    rt = Runtime(ctx)
+    try:
+        buf = rt.buffer(1000, 8)
+        with pytest.raises(CohError):
+            buf.view(10, 1000)  # hi past the buffer (program.hpp:65-68)
+        v = buf.view(0, 99)
+        w = buf.view(50, 149)
+        bad = ElemCall()
+        bad.view, bad.kind, bad.site, bad.n_body = 7, 0, 0, 0  # no such view
+        with pytest.raises(CohError):
+            buf.call(bad)
+        # an adversarial body: R(v) on the CPU (v^ valid there: no sync) whose body reads
+        # on the GPU, where nothing was ever copied -> stuck at v's first cell
+        c = ElemCall()
+        c.view, c.kind, c.site, c.n_body = v, 0, 0, 1
+        c.body[0].effect, c.body[0].site, c.body[0].lo, c.body[0].hi = 2, 1, 0, 99
+        with pytest.raises(CohError) as e:
+            buf.call(c)
+        assert "stuck" in str(e.value) and "cell 0" in str(e.value)
+        assert rt.stats()["stuck_calls"] == 1 and len(rt.copy_log()) == 0
+        # the same block with the read at the mode's site completes, and a GPU read of w
+        # then uploads w's cells
+        c.body[0].site = 0
+        buf.call(c)
+        g = ElemCall()
+        g.view, g.kind, g.site, g.n_body = w, 0, 1, 1
+        g.body[0].effect, g.body[0].site, g.body[0].lo, g.body[0].hi = 2, 1, 0, 99
+        buf.call(g)
+        assert [(int(x["first"]), int(x["last"]), int(x["h2d"])) for x in rt.copy_log()] == [(50, 149, 1)]
+    finally:
+        rt.close()
