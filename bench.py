@@ -313,13 +313,36 @@ def run_bitmap_primitives(args, ctx):
                                                       re_.data_ptr(), cap, roff.data_ptr(), s))
     runs = int(roff[-1].item())
     out["zero_runs"] = {"ms": t, "runs": runs, "gbs": (m / 8 + 8 * runs) / (t / 1e3) / 1e9,
-                        "note": "collect pass reads the plane once; chunks with > 256 runs re-walk it in the place pass"}
+                        "note": "collect pass reads the plane once; chunks with > 1024 runs re-walk it in the place pass"}
     t = timed(lambda: Lb.coh_bitmap_range_set(ctx._h, L.data_ptr(), d_r.data_ptr(), P, s))
     out["range_set"] = {"ms": t, "gbs": m / 8 / (t / 1e3) / 1e9}
     t = timed(lambda: Lb.coh_bitmap_range_clear(ctx._h, L.data_ptr(), d_r.data_ptr(), P, s))
     out["range_clear"] = {"ms": t, "gbs": m / 8 / (t / 1e3) / 1e9}
     for k in ("first_zero", "view_check", "zero_runs", "range_set", "range_clear"):
         out[k]["frac"] = out[k]["gbs"] / peak
+    # run extraction across fragmentation (rho in {0, 2^-16, 2^-8, 1/2} of
+    # cells set in the destination plane, independently per cell): the same planes and
+    # ranges; output-bound at rho = 1/2 (a run every four cells)
+    Pf = P
+    sweep = {}
+    for name, ands in (("0", None), ("2^-16", 16), ("2^-8", 8), ("1/2", 1)):
+        plane = torch.zeros(Pf * words, dtype=torch.int32, device="cuda")
+        if ands:
+            plane.fill_(-1)
+            for _ in range(ands):
+                plane &= torch.randint(-(1 << 31), 1 << 31, (Pf * words,), dtype=torch.int32, device="cuda")
+        mf = int((ranges["hi"][:Pf].astype(np.int64) - ranges["lo"][:Pf] + 1).sum())
+        capf = mf // 3 + 16 if ands == 1 else cap
+        rsf = torch.empty(capf, dtype=torch.int32, device="cuda")
+        ref_ = torch.empty(capf, dtype=torch.int32, device="cuda")
+        t = timed(lambda: Lb.coh_bitmap_extract_zero_runs(ctx._h, plane.data_ptr(), d_r.data_ptr(), Pf, rsf.data_ptr(),
+                                                          ref_.data_ptr(), capf, roff.data_ptr(), s))
+        runs = int(roff[Pf].item())
+        gbs = (mf / 8 + 8 * runs) / (t / 1e3) / 1e9
+        sweep[name] = {"ms": t, "runs": runs, "gbs": gbs, "frac": gbs / peak}
+        del plane, rsf, ref_
+    out["zero_runs_by_fragmentation"] = {"planes": Pf, "cells_in_ranges": mf, "rho": sweep,
+                                         "note": "bytes = m/8 read + 8 per run written (SURVEY 8(d))"}
     return out
 
 

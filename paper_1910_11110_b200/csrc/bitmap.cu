@@ -506,7 +506,49 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
 // quads again.  Sparse planes (the usual sync destination) are therefore read once.  (A
 // single-pass decoupled look-back over ticketed chunks was measured slower on B200: the
 // first wave's look-backs walk back over thousands of aggregates.)
-constexpr uint32_t kRunCap = 256;
+constexpr uint32_t kRunCap = 4096;
+#ifndef COH_DENSE_STEP
+#define COH_DENSE_STEP 64
+#endif
+constexpr uint32_t kDenseStep = COH_DENSE_STEP;  // runs per warp step above which the warp writes cooperatively
+
+// Dense steps: the warp writes the step's T positions [base, base + T) together, 32
+// consecutive positions per store.  Position p belongs to the lane L with S_L <= p <
+// S_L + n_L (S = the exclusive scan of the lanes' counts; found by a binary search over
+// shuffled S) and is the (p - S_L)-th set bit of L's four mask words, at cell cb_L + 32 k
+// + bit.  Positions at or past `cap` are neither computed nor written.
+__device__ __forceinline__ void emit_dense(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3, uint32_t S, uint32_t T,
+                                           uint64_t cb, uint64_t base, uint32_t* out, uint64_t cap) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t lim = base >= cap ? 0 : (T < cap - base ? T : cap - base);  // warp-uniform
+  for (uint32_t k = 0; k * 32 < lim; ++k) {
+    const uint32_t p = k * 32 + lane;
+    uint32_t L = 0;
+#pragma unroll
+    for (uint32_t b = 16; b; b >>= 1)
+      if (__shfl_sync(0xFFFFFFFFu, S, L + b) <= p) L += b;
+    uint32_t rr = p - __shfl_sync(0xFFFFFFFFu, S, L);
+    const uint32_t w0 = __shfl_sync(0xFFFFFFFFu, m0, L), w1 = __shfl_sync(0xFFFFFFFFu, m1, L);
+    const uint32_t w2 = __shfl_sync(0xFFFFFFFFu, m2, L), w3 = __shfl_sync(0xFFFFFFFFu, m3, L);
+    const uint64_t c = __shfl_sync(0xFFFFFFFFu, cb, L);
+    // the word holding the rr-th set bit, then the bit (binary search by popcount)
+    uint32_t w = w0, wi = 0, cnt = __popc(w0);
+    if (rr >= cnt) { rr -= cnt; w = w1; wi = 1; cnt = __popc(w1); }
+    if (wi == 1 && rr >= cnt) { rr -= cnt; w = w2; wi = 2; cnt = __popc(w2); }
+    if (wi == 2 && rr >= cnt) { rr -= cnt; w = w3; wi = 3; }
+    uint32_t pos = 0;
+#pragma unroll
+    for (uint32_t sh = 16; sh; sh >>= 1) {
+      const uint32_t low = __popc(w & ((1u << sh) - 1u));
+      if (rr >= low) {
+        rr -= low;
+        w >>= sh;
+        pos += sh;
+      }
+    }
+    if (p < lim) out[base + p] = (uint32_t)(c + 32u * wi + pos);
+  }
+}
 
 // Places the starts / ends of one warp step at chunk-relative (STAGE) or global positions
 // s.., e.. (warp-synchronous; s and e advance by the warp's totals).
@@ -530,7 +572,12 @@ __device__ __forceinline__ void place_step(const Flat& F, uint64_t f, uint32_t r
   uint64_t s = gs + ps - ns, e = ge + pe - ne;
   if (STAGE && at_start)  // the first flat quad of range r (and of the empty ranges just before it)
     for (int64_t q = r; q >= 0 && F.qp[q] == f; --q) off_local[q] = (uint32_t)s;
-  if (ns | ne) {
+  const uint32_t Ts = __shfl_sync(0xFFFFFFFFu, ps, 31), Te = __shfl_sync(0xFFFFFFFFu, pe, 31);
+  if (Ts + Te > kDenseStep) {  // coalesced cooperative writes
+    const uint64_t cb = (qa * 4 - F.r[r].word_off) * 32;
+    emit_dense(st[0], st[1], st[2], st[3], ps - ns, Ts, cb, gs, out_s, cap);
+    emit_dense(en[0], en[1], en[2], en[3], pe - ne, Te, cb, ge, out_e, cap);
+  } else if (ns | ne) {  // sparse step: each lane writes its few runs
     const uint64_t wbase = qa * 4 - F.r[r].word_off;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -548,8 +595,8 @@ __device__ __forceinline__ void place_step(const Flat& F, uint64_t f, uint32_t r
       }
     }
   }
-  gs += __shfl_sync(0xFFFFFFFFu, ps, 31);
-  ge += __shfl_sync(0xFFFFFFFFu, pe, 31);
+  gs += Ts;
+  ge += Te;
 }
 
 // Collect pass.  Per warp chunk: start / end counts (chunk_s, chunk_e) and staged runs;
