@@ -42,6 +42,8 @@ struct RegDev {
   const uint32_t* view;        // sorted position -> view index
   const int32_t* tree;         // 2P nodes, node 1 = root, max hi (INT_MIN for padding)
   const coh_view* views;       // by view index
+  const uint64_t* hoff;        // optional CSR of every view's hits (n + 1 offsets) ...
+  const uint32_t* hits;        // ... name-rank ordered, probe excluded (nullptr: use the tree)
 };
 
 __device__ __forceinline__ uint32_t lower_bound_key(const uint64_t* key, uint32_t n, uint64_t k) {
@@ -136,6 +138,32 @@ __device__ void query_view(const RegDev& r, uint32_t p, F&& f) {
   });
 }
 
+// Registry build, second half: every view's hits once, as a CSR in name-rank order, so a
+// closure reads a short contiguous list instead of descending the tree per mode.
+__global__ void k_count_hits(RegDev r, uint64_t* cnt) {
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= r.n) return;
+  uint32_t c = 0;
+  query_view(r, v, [&](uint32_t) { ++c; });
+  cnt[v] = c;
+}
+
+__global__ void k_fill_hits(RegDev r, const uint64_t* off, uint32_t* hits) {
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= r.n) return;
+  uint32_t* h = hits + off[v];
+  uint32_t k = 0;
+  query_view(r, v, [&](uint32_t y) {  // insertion by name rank (std::set<std::string> order)
+    const uint32_t ry = r.views[y].name_rank;
+    uint32_t j = k++;
+    while (j > 0 && r.views[h[j - 1]].name_rank > ry) {
+      h[j] = h[j - 1];
+      --j;
+    }
+    h[j] = y;
+  });
+}
+
 __global__ void k_query(RegDev r, const uint32_t* probes, uint32_t n_probes, uint32_t* hits, uint32_t stride,
                         uint32_t* count) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -182,25 +210,37 @@ __global__ void k_closure(RegDev r, const coh_mode* modes, const uint32_t* off, 
     uint32_t hv[kMaxNeeded];
     uint32_t nh = 0;
     bool over = false;
-    query_view(r, m.var, [&](uint32_t y) {
-      if (m.kind == COH_W) {  // skip y with a same-site W (the declared set)
-        for (uint32_t q = m0; q < m1; ++q) {
-          const coh_mode o2 = modes[q];
-          if ((o2.flags & 1u) && o2.var == y && o2.kind == COH_W && o2.site == m.site) return;
+    auto skip = [&](uint32_t y) {  // a W skips y with a same-site W (the declared set)
+      if (m.kind != COH_W) return false;
+      for (uint32_t q = m0; q < m1; ++q) {
+        const coh_mode o2 = modes[q];
+        if ((o2.flags & 1u) && o2.var == y && o2.kind == COH_W && o2.site == m.site) return true;
+      }
+      return false;
+    };
+    if (r.hits) {  // the precomputed, already name-ordered list
+      for (uint64_t i = r.hoff[m.var], e = r.hoff[m.var + 1]; i < e && !over; ++i) {
+        const uint32_t y = r.hits[i];
+        if (skip(y)) continue;
+        if (nh == kMaxNeeded) over = true;
+        else hv[nh++] = y;
+      }
+    } else {
+      query_view(r, m.var, [&](uint32_t y) {
+        if (skip(y)) return;
+        if (nh == kMaxNeeded) {
+          over = true;
+          return;
         }
-      }
-      if (nh == kMaxNeeded) {
-        over = true;
-        return;
-      }
-      const uint32_t ry = r.views[y].name_rank;
-      uint32_t j = nh++;
-      while (j > 0 && r.views[hv[j - 1]].name_rank > ry) {
-        hv[j] = hv[j - 1];
-        --j;
-      }
-      hv[j] = y;
-    });
+        const uint32_t ry = r.views[y].name_rank;
+        uint32_t j = nh++;
+        while (j > 0 && r.views[hv[j - 1]].name_rank > ry) {
+          hv[j] = hv[j - 1];
+          --j;
+        }
+        hv[j] = y;
+      });
+    }
     if (over) {
       st = -2;
       break;
@@ -293,6 +333,7 @@ struct coh_registry {
   cudaStream_t stream = nullptr;  // the build stream; the memory is stream-ordered
   uint32_t n = 0, P = 1;
   void* mem = nullptr;  // one allocation: keys, lo, hi, view, tree, views copy
+  void* csr = nullptr;  // the hits CSR (offsets, then hits), when it fits kMaxCsrHits
   cohb::RegDev dev{};
   std::string err;
 };
@@ -355,13 +396,52 @@ extern "C" int coh_registry_build(coh_ctx* ctx, const coh_view* d_views, uint32_
     return fail(ctx, "registry build", e);
   }
   ctx->launches += (n_views ? 4 : 2) + (uint64_t)(P > 2048 ? 31 - __builtin_clz(P / 2048) : 0);  // + the CUB sort
-  r->dev = RegDev{n_views, P, key, lo, hi, view, tree, views};
+  r->dev = RegDev{n_views, P, key, lo, hi, view, tree, views, nullptr, nullptr};
+  if (n_views) {  // every view's hits, once (closures then read contiguous lists); on any
+                  // failure the registry simply keeps answering from the tree
+    constexpr uint64_t kMaxCsrHits = 1ull << 26;
+    const size_t o_tmp2 = align256(8ull * (n_views + 1));
+    size_t scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n_views + 1, s);
+    void* cmem = nullptr;
+    uint64_t total = ~0ull;
+    if (cudaMallocAsync(&cmem, o_tmp2 + scan_bytes, s) == cudaSuccess) {
+      uint64_t* off = static_cast<uint64_t*>(cmem);
+      cudaMemsetAsync(off + n_views, 0, 8, s);
+      k_count_hits<<<(n_views + 255) / 256, 256, 0, s>>>(r->dev, off);
+      cub::DeviceScan::ExclusiveSum(static_cast<char*>(cmem) + o_tmp2, scan_bytes, off, off, (int)n_views + 1, s);
+      if (cudaMemcpyAsync(&total, off + n_views, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+          cudaStreamSynchronize(s) != cudaSuccess)
+        total = ~0ull;
+      void* csr = nullptr;
+      const size_t o_hits = align256(8ull * (n_views + 1));
+      if (total <= kMaxCsrHits && cudaMallocAsync(&csr, o_hits + 4 * std::max<uint64_t>(total, 1), s) == cudaSuccess) {
+        uint64_t* hoff = static_cast<uint64_t*>(csr);
+        uint32_t* hits = reinterpret_cast<uint32_t*>(static_cast<char*>(csr) + o_hits);
+        cudaMemcpyAsync(hoff, off, 8ull * (n_views + 1), cudaMemcpyDeviceToDevice, s);
+        k_fill_hits<<<(n_views + 255) / 256, 256, 0, s>>>(r->dev, hoff, hits);
+        r->csr = csr;
+        r->dev.hoff = hoff;
+        r->dev.hits = hits;
+        ctx->launches += 1;
+      }
+      cudaFreeAsync(cmem, s);
+      ctx->launches += 2;
+    }
+    if (cudaGetLastError() != cudaSuccess && r->csr) {  // fall back to the tree
+      cudaFreeAsync(r->csr, s);
+      r->csr = nullptr;
+      r->dev.hoff = nullptr;
+      r->dev.hits = nullptr;
+    }
+  }
   *out = r;
   return COH_OK;
 }
 
 extern "C" void coh_registry_destroy(coh_registry* r) {
   if (!r) return;
+  if (r->csr) cudaFreeAsync(r->csr, r->stream);
   cudaFreeAsync(r->mem, r->stream);
   delete r;
 }
