@@ -170,6 +170,13 @@ __global__ void k_query(RegDev r, const uint32_t* probes, uint32_t n_probes, uin
   if (q >= n_probes) return;
   uint32_t c = 0;
   uint32_t* out = hits + (uint64_t)q * stride;
+  if (r.hits) {  // the precomputed list, already name-ordered
+    const uint64_t a = r.hoff[probes[q]], e = r.hoff[probes[q] + 1];
+    for (uint64_t i = a; i < e; ++i, ++c)
+      if (c < stride) out[c] = r.hits[i];
+    count[q] = c;
+    return;
+  }
   query_view(r, probes[q], [&](uint32_t y) {
     // insertion by name rank (the reference returns std::set<std::string> order)
     if (c < stride) {
