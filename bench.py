@@ -116,6 +116,27 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_issue(n_traces, kernel_ms, sm_mhz, sms):
+    """The binding roofline of k_trace_eval (instruction issue: "INT pipe
+    is the expected binder"): warp instructions per launch from the committed ncu capture
+    (scaled to this launch's traces) over the measured kernel time, against the issue peak
+    of one warp instruction per clock per SM sub-partition (4 per SM) at the sampled clock."""
+    p = os.path.join(ROOT, "profiles", "ncu_trace_eval.json")
+    if not os.path.exists(p) or not kernel_ms or not sm_mhz:
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    inst = d.get("metrics", {}).get("smsp__inst_executed.sum")
+    if not inst or not d.get("traces_per_launch"):
+        return None
+    inst = inst * n_traces / d["traces_per_launch"]
+    achieved = inst / (kernel_ms / 1e3)
+    peak = 4.0 * sms * sm_mhz * 1e6
+    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "warp inst/s", "frac": achieved / peak,
+            "inst_per_launch": inst, "source": "profiles/ncu_trace_eval.json smsp__inst_executed.sum, "
+                                              "peak = 4 x SMs x sampled SM clock"}
+
+
 def ncu_traffic():
     """dram bytes per trace_eval launch from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_trace_eval.json")
@@ -771,6 +792,7 @@ def run_ours(args, rank, world, local):
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
+        clk = clocks.summary()
         line = {
             "metric": METRIC, "value": value, "unit": "calls/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -784,8 +806,10 @@ def run_ours(args, rank, world, local):
             "roofline": {"bound": "hbm", "kernel": "k_trace_eval", "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms": k_ms,
-                         "note": "INT/LSU-issue bound in practice; see profiles/ for pipe utilisation"},
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "gpu_launches": launches,
+                         "note": "INT/LSU-issue bound in practice: see `issue` (the binding roofline) and profiles/",
+                         "issue": ncu_issue(N, k_ms, (clk or {}).get("sm_mhz"), torch.cuda.get_device_properties(dev)
+                                            .multi_processor_count)},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
             "bitmap": bitmap, "container": container, "sweep": sweep_info, "c1": c1, "c4": c4, "overlap": overlap,
         }
         print(json.dumps(line), flush=True)
