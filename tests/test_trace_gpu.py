@@ -277,3 +277,34 @@ def test_c4_full_size_shards(ctx):
     assert total == whole
     assert np.array_equal(cnt_sum, d_cnt.cpu().numpy().view(np.uint64)[:10])
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("nc", [100, 96, 64])  # ragged (no ring), single ring, double ring
+def test_dynamic_batches_long_launch(ctx, nc):
+    """Launches long enough for the dynamic warp batches (> 5 rounds per thread): every
+    variant's results equal the same traces evaluated as small static launches (whose
+    parity with the oracle the tests above establish), checked in full by checksum and on
+    a sample against the oracle."""
+    from paper_1910_11110_b200 import shard
+    N, na, adv, seed = 1 << 20, 64, 8, 9
+    s = torch.cuda.current_stream().cuda_stream
+    d_rec = torch.empty(coh.records_elems(N, nc), dtype=torch.int16, device="cuda")
+    ctx.gen_records(seed, 0, N, nc, na, adv, d_rec, s)
+    d_res = torch.empty(N * 64, dtype=torch.uint8, device="cuda")
+    ctx.eval_traces(d_rec, N, nc, na, 10000, d_res, None, stream=s)
+    torch.cuda.synchronize()
+    whole = shard.results_checksum(d_res)
+    parts = 0
+    for g in range(16):  # 64K-trace launches: static striding
+        first, cnt = shard.split_range(g, 16, N)
+        d_r = torch.empty(coh.records_elems(cnt, nc), dtype=torch.int16, device="cuda")
+        ctx.gen_records(seed, first, cnt, nc, na, adv, d_r, s)
+        d_o = torch.empty(cnt * 64, dtype=torch.uint8, device="cuda")
+        ctx.eval_traces(d_r, cnt, nc, na, 10000, d_o, None, stream=s)
+        torch.cuda.synchronize()
+        parts = (parts + shard.results_checksum(d_o)) & ((1 << 64) - 1)
+    assert parts == whole
+    res = d_res.cpu().numpy().view(coh.RESULT_DTYPE)
+    for t in range(0, N, 4099)[:200]:
+        w, _ = o.orc_eval(coh.gen_records_host(seed, t, 1, nc, na, adv), 1, nc, na, 10000)
+        assert same(res[t:t + 1], w), t
