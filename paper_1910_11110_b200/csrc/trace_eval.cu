@@ -464,17 +464,27 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
     }
   }
   finished : {
+    // the final store, nibble-packed, and every slot reset for this thread's next trace
     uint32_t sw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t init;  // kInit in a register (else ptxas rematerialises it before every store)
+    asm volatile("mov.u32 %0, %1;" : "=r"(init) : "n"(kInit));
+#define COH_SLOT_OUT(A)                                                                \
+  {                                                                                    \
+    uint16_t* const wp = reinterpret_cast<uint16_t*>(stb + (A) * 256 + toff);          \
+    const uint32_t w = *wp;                                                            \
+    *wp = (uint16_t)init;                                                              \
+    const int sh = 4 * ((A) & 7) - 8; /* state nibble at slot bits 8-11 */             \
+    sw[(A) >> 3] |= (sh >= 0 ? (w << sh) : (w >> -sh)) & (15u << (4 * ((A) & 7)));    \
+  }
+    if (p.n_arrays == COH_MAX_ARRAYS) {  // all 64 arrays (C2): no per-array predicate
 #pragma unroll
-    for (int a = 0; a < COH_MAX_ARRAYS; ++a) {
-      if (a < (int)p.n_arrays) {
-        uint16_t* const wp = reinterpret_cast<uint16_t*>(stb + a * 256 + toff);
-        const uint32_t w = *wp;
-        *wp = (uint16_t)kInit;  // reset for this thread's next trace
-        const int sh = 4 * (a & 7) - 8;  // state nibble at slot bits 8-11
-        sw[a >> 3] |= (sh >= 0 ? (w << sh) : (w >> -sh)) & (15u << (4 * (a & 7)));
-      }
+      for (int a = 0; a < COH_MAX_ARRAYS; ++a) COH_SLOT_OUT(a)
+    } else {
+#pragma unroll
+      for (int a = 0; a < COH_MAX_ARRAYS; ++a)
+        if (a < (int)p.n_arrays) COH_SLOT_OUT(a)
     }
+#undef COH_SLOT_OUT
     const uint64_t tb = UNIFORM ? (uint64_t)xfers * p.bytes_uniform : tbytes;
     uint4* out = reinterpret_cast<uint4*>(p.res + t);
     __stcs(out + 0, make_uint4(sw[0], sw[1], sw[2], sw[3]));
