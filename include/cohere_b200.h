@@ -282,6 +282,24 @@ int coh_elem_gen(uint64_t seed, uint64_t prog_id, uint32_t n_cells, uint32_t n_v
                  uint32_t n_calls, uint32_t adv_per1024, uint32_t* view_lo, uint32_t* view_hi,
                  coh_elem_call* calls);
 
+/* ---- declarations (Declarations, program.hpp:141-226) ------------------------------
+ * A declarations object: whole-array variables (arrays, with their byte sizes) and
+ * buffers with views, numbered in declaration order; it fills the declaration part of
+ * a trace batch or an element program.  Construction defects (more than 64 arrays or 16
+ * views, a view outside its buffer, an empty buffer) are COH_E_CONSTRUCTION
+ * (ConstructionError).  Pointers it hands out live as long as the object. */
+typedef struct coh_decls coh_decls;
+int coh_decls_create(coh_decls** out);
+void coh_decls_destroy(coh_decls* d);
+const char* coh_decls_error(const coh_decls* d);
+int coh_decls_array(coh_decls* d, uint64_t bytes, uint32_t* id);
+int coh_decls_buffer(coh_decls* d, uint32_t n_cells, uint32_t* id);
+int coh_decls_view(coh_decls* d, uint32_t buffer, uint32_t lo, uint32_t hi, uint32_t* view_index);
+/* n_arrays and array_bytes of *b (records, n_traces, n_calls and fuel are the caller's) */
+int coh_decls_trace_batch(const coh_decls* d, coh_trace_batch* b);
+/* n_cells, n_views, view_lo, view_hi of *p for one buffer (calls and fuel are the caller's) */
+int coh_decls_elem_program(const coh_decls* d, uint32_t buffer, coh_elem_program* p);
+
 /* ==== coherent container runtime (config C5) ======================
  * VectorPU's coherence control on the calculus: each vector is one
  * whole-array variable with pinned host + device copies and its calculus state (concrete

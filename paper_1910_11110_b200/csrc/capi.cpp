@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "gen_common.h"
 #include "internal.hpp"
@@ -319,6 +320,84 @@ int coh_reduce_counters(coh_ctx* ctx, const coh_trace_result* d_results, uint64_
   if (rc) ctx->err = err;
   else if (n_traces) ctx->launches++;
   return rc;
+}
+
+}  // extern "C"
+
+// ---- declarations ----------------------------------------------------------------------
+struct coh_decls {
+  std::vector<uint64_t> bytes;                          // arrays
+  std::vector<uint32_t> cells;                          // buffers
+  std::vector<std::vector<uint32_t>> vlo, vhi;          // views per buffer
+  std::string err;
+};
+
+extern "C" {
+
+int coh_decls_create(coh_decls** out) {
+  if (!out) return COH_E_ARG;
+  *out = new coh_decls();
+  return COH_OK;
+}
+
+void coh_decls_destroy(coh_decls* d) { delete d; }
+
+const char* coh_decls_error(const coh_decls* d) { return d ? d->err.c_str() : "no declarations"; }
+
+int coh_decls_array(coh_decls* d, uint64_t bytes, uint32_t* id) {
+  if (!d || !id) return COH_E_ARG;
+  if (d->bytes.size() >= COH_MAX_ARRAYS) {
+    d->err = "more than 64 whole-array variables";
+    return COH_E_CONSTRUCTION;
+  }
+  *id = (uint32_t)d->bytes.size();
+  d->bytes.push_back(bytes);
+  return COH_OK;
+}
+
+int coh_decls_buffer(coh_decls* d, uint32_t n_cells, uint32_t* id) {
+  if (!d || !id) return COH_E_ARG;
+  if (n_cells == 0) {  // program.hpp:57-63: a buffer has at least one element
+    d->err = "buffer size must be positive";
+    return COH_E_CONSTRUCTION;
+  }
+  *id = (uint32_t)d->cells.size();
+  d->cells.push_back(n_cells);
+  d->vlo.emplace_back();
+  d->vhi.emplace_back();
+  return COH_OK;
+}
+
+int coh_decls_view(coh_decls* d, uint32_t buffer, uint32_t lo, uint32_t hi, uint32_t* view_index) {
+  if (!d || !view_index || buffer >= d->cells.size()) return COH_E_ARG;
+  if (lo > hi || hi >= d->cells[buffer]) {  // program.hpp:65-68
+    d->err = "view range does not fit its buffer";
+    return COH_E_CONSTRUCTION;
+  }
+  if (d->vlo[buffer].size() >= COH_MAX_VIEWS) {
+    d->err = "more than 16 views on one buffer";
+    return COH_E_CONSTRUCTION;
+  }
+  *view_index = (uint32_t)d->vlo[buffer].size();
+  d->vlo[buffer].push_back(lo);
+  d->vhi[buffer].push_back(hi);
+  return COH_OK;
+}
+
+int coh_decls_trace_batch(const coh_decls* d, coh_trace_batch* b) {
+  if (!d || !b || d->bytes.empty()) return COH_E_ARG;
+  b->n_arrays = (uint32_t)d->bytes.size();
+  b->array_bytes = d->bytes.data();
+  return COH_OK;
+}
+
+int coh_decls_elem_program(const coh_decls* d, uint32_t buffer, coh_elem_program* p) {
+  if (!d || !p || buffer >= d->cells.size()) return COH_E_ARG;
+  p->n_cells = d->cells[buffer];
+  p->n_views = (uint32_t)d->vlo[buffer].size();
+  p->view_lo = d->vlo[buffer].data();
+  p->view_hi = d->vhi[buffer].data();
+  return COH_OK;
 }
 
 }  // extern "C"
