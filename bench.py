@@ -266,7 +266,30 @@ def run_bitmap(args, ctx, rank, world):
                        "l2": "1 GiB of planes per GPU > L2, no flush"},
             "outcomes": {"stuck": sum(1 for i in range(B) if res[i].status == 1),
                          "transfers": sum(res[i].transfers for i in range(B)),
-                         "runs": sum(res[i].n_runs for i in range(B))}}
+                         "runs": sum(res[i].n_runs for i in range(B))},
+            "cpu_reference": bitmap_cpu_reference(ctx) if rank == 0 and not args.no_cpu_baseline else None}
+
+
+def bitmap_cpu_reference(ctx):
+    """The reference on the C3 workload's shape, bounded (the reference only at
+    n <= 2^20): one program of 2^20 cells, 8 views, 8 calls, run through the reference's
+    own run_annotated over its std::map store (oracle/_ref, one host thread); its
+    algorithmic bytes (the same count as the GPU line's) over its wall time."""
+    from paper_1910_11110_b200.elem import Program, elem_eval
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle_ffi as o
+        if not o.have_ref():
+            return {"unavailable": "oracle/_ref not built"}
+        p = Program.generate(3, 0, 1 << 20, 8, 8, 64)
+        alg = int(elem_eval(ctx, [p], want_planes=False, runs_cap=0)["stats"].alg_bytes)
+        t0 = time.perf_counter()
+        rc = o.elem_run("ref", p)[0]
+        dt = time.perf_counter() - t0
+        return {"value": alg / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference", "seconds": dt,
+                "rc": int(rc), "sample": "one program of 2^20 cells, 8 views, 8 calls (seed 3, program 0)"}
+    except Exception as ex:  # test infrastructure; its absence is not fatal here
+        return {"error": f"{type(ex).__name__}: {ex}"}
 
 
 def run_bitmap_primitives(args, ctx):
