@@ -541,9 +541,14 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
 //      (= the stop of run_annotated, modes.hpp:118-121), resolved by the same host-
 //      compiled slow table as the per-thread kernel.
 // Results are field-for-field those of k_trace_eval (tests run both on the same inputs).
-constexpr int kScanNT = 128;   // threads per trace
-constexpr int kScanCPT = 8;    // consecutive calls per thread (one 16-byte record chunk)
-constexpr uint32_t kScanPass = kScanNT * kScanCPT;
+#ifndef COH_SCAN_CPT
+#define COH_SCAN_CPT 4
+#endif
+constexpr int kScanCPT = COH_SCAN_CPT;  // consecutive calls per thread (half or all of a 16-byte chunk)
+constexpr int kScanNT = 1024 / kScanCPT;  // threads per trace (1024 calls per pass)
+static_assert(kScanCPT == 4 || kScanCPT == 8, "a thread's calls are half or all of one record chunk");
+constexpr uint32_t kGroupThreads = 32u / kScanCPT;  // threads per 32-call boundary word
+constexpr uint32_t kScanPass = kScanNT * kScanCPT;  // 1024
 
 // A state map: byte s of the four words = the state reached from start state s (bits
 // 0-3), bit 4 set when a slow entry was reached on the way.  Composition is four PRMT
@@ -635,7 +640,14 @@ __global__ void __launch_bounds__(kScanNT) k_trace_scan(const KParams p) {
   const uint32_t t = blockIdx.x, n = (uint32_t)p.n_traces, nc = p.n_calls;
   const char* const lutb = reinterpret_cast<const char*>(lut);
   // the first pass's records and the table: every load in flight at once
-  uint4 ch = tid * kScanCPT < nc ? __ldg(p.rec + (uint64_t)tid * n + t) : make_uint4(0u, 0u, 0u, 0u);
+  // this thread's calls: chunk (c0 / 8), all of it (CPT 8) or its half (c0 / 4) & 1 (CPT 4)
+  auto load_calls = [&](uint32_t c0) {
+    if (c0 >= nc) return make_uint4(0u, 0u, 0u, 0u);
+    if (kScanCPT == 8) return __ldg(p.rec + (uint64_t)(c0 / 8u) * n + t);
+    const uint2 h = __ldg(reinterpret_cast<const uint2*>(p.rec + (uint64_t)(c0 / 8u) * n + t) + ((c0 >> 2) & 1u));
+    return make_uint4(h.x, h.y, 0u, 0u);
+  };
+  uint4 ch = load_calls(tid * kScanCPT);
   {
     constexpr uint32_t kQ = kLutEntries / 4u, kIt = (kQ + kScanNT - 1) / kScanNT;
     static_assert(kLutEntries % 4u == 0u, "table in 16-byte pieces");
@@ -656,7 +668,7 @@ __global__ void __launch_bounds__(kScanNT) k_trace_scan(const KParams p) {
   for (; base < nc && !stopped; base += kScanPass) {
     const uint32_t c0 = base + tid * kScanCPT;
     const uint32_t cnt = c0 < nc ? min((uint32_t)kScanCPT, nc - c0) : 0u;
-    if (base) ch = cnt ? __ldg(p.rec + (uint64_t)(c0 / 8u) * n + t) : make_uint4(0u, 0u, 0u, 0u);
+    if (base) ch = load_calls(c0);
     const uint32_t w4[4] = {ch.x, ch.y, ch.z, ch.w};
     COH_TS(1)
     // 1. this thread's map: the 16 start states stepped through its calls in parallel.
@@ -754,11 +766,11 @@ __global__ void __launch_bounds__(kScanNT) k_trace_scan(const KParams p) {
     const uint32_t i = stop_at;  // the pass's first slow call, if any
     const uint32_t keep = i == 0xFFFFFFFFu ? cnt : (i <= c0 ? 0u : min(cnt, i - c0));  // completed calls
     const uint32_t km = (1u << keep) - 1u;
-    if (p.bnd) {  // boundary words: four threads per 32-call group
-      uint32_t word = (ok_bits & km) << (8u * (tid & 3u));
-      word |= __shfl_xor_sync(0xFFFFFFFFu, word, 1);
-      word |= __shfl_xor_sync(0xFFFFFFFFu, word, 2);
-      if ((tid & 3u) == 0u && c0 < nc) p.bnd[(uint64_t)(c0 / 32u) * n + t] = word;
+    if (p.bnd) {  // boundary words: kGroupThreads threads per 32-call group
+      uint32_t word = (ok_bits & km) << (kScanCPT * (tid & (kGroupThreads - 1u)));
+#pragma unroll
+      for (uint32_t o = 1; o < kGroupThreads; o <<= 1) word |= __shfl_xor_sync(0xFFFFFFFFu, word, o);
+      if ((tid & (kGroupThreads - 1u)) == 0u && c0 < nc) p.bnd[(uint64_t)(c0 / 32u) * n + t] = word;
     }
     uint32_t ks = 0, kx = 0, s_slow = 0;  // cs / cx at call keep - 1, state before call keep
 #pragma unroll
