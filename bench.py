@@ -166,21 +166,24 @@ def evaluated_calls(res):
 
 def cpu_sample(seconds, threads, trace0=0):
     """Time the CPU evaluator on a bounded sample of the same workload (trace ids from
-    trace0), sized to ~`seconds` of wall time on `threads` host threads."""
-    import paper_1910_11110_b200 as coh
+    trace0), sized to ~`seconds` of wall time on `threads` host threads.  The records come
+    from the oracle's own generator (orc_gen_records, the same splitmix64 stream as the
+    device generator), so this leg never loads the product library."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_ffi as orc
 
     kind, fn = cpu_eval_fn()
     cores = threads if kind == "reference" else 1
     n = 64 if kind == "reference" else 2048
     while True:
-        recs = coh.gen_records_host(SEED, trace0, n, N_CALLS, N_ARRAYS, ADV)
+        recs = orc.orc_gen(SEED, trace0, n, N_CALLS, N_ARRAYS, ADV)
         t0 = time.perf_counter()
         res, _ = fn(recs, n, cores)
         dt = time.perf_counter() - t0
         if dt >= 0.25 * seconds or n >= (1 << 22):
             if dt < seconds and n < (1 << 22):
                 n = int(n * seconds / max(dt, 1e-3))
-                recs = coh.gen_records_host(SEED, trace0, n, N_CALLS, N_ARRAYS, ADV)
+                recs = orc.orc_gen(SEED, trace0, n, N_CALLS, N_ARRAYS, ADV)
                 t0 = time.perf_counter()
                 res, _ = fn(recs, n, cores)
                 dt = time.perf_counter() - t0
@@ -191,10 +194,22 @@ def cpu_sample(seconds, threads, trace0=0):
         n *= 4
 
 
+def bench_config(world, traces_per_gpu):
+    """The `config` object of both arms (identical by construction)."""
+    return {"workload": WORKLOAD, "traces_per_gpu": traces_per_gpu, "arrays": N_ARRAYS, "calls": N_CALLS,
+            "adv_per1024": ADV, "fuel": FUEL, "parallelism": f"dp{world} (trace-id shards)",
+            "l2": "inputs larger than L2 (records 512 MiB per GPU), no flush"}
+
+
 def run_reference_arm(args, rank, world):
+    """The reference's own CPU implementation of the path (oracle/_ref: the unmodified
+    reference headers, cohere::run_annotated per trace, on all host threads; the C
+    restatement if the reference did not ship).  Nothing from the product package is
+    imported or loaded here: records come from the oracle's generator."""
     if rank != 0:
         return  # rank 0 alone runs the reference arm
-    import paper_1910_11110_b200 as coh
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_ffi as orc
 
     threads = os.cpu_count() or 1
     kind, fn = cpu_eval_fn()
@@ -206,24 +221,23 @@ def run_reference_arm(args, rank, world):
     n_step = max(cores, int(cal["traces"] * per_step / max(cal["seconds"], 1e-3)))
     t_calls, t_sec = 0, 0.0
     for k in range(args.warmup + args.steps):
-        recs = coh.gen_records_host(SEED, (1 << 30) + k * n_step, n_step, N_CALLS, N_ARRAYS, ADV)
+        recs = orc.orc_gen(SEED, (1 << 30) + k * n_step, n_step, N_CALLS, N_ARRAYS, ADV)
         t0 = time.perf_counter()
         res, _ = fn(recs, n_step, cores)
         dt = time.perf_counter() - t0
         if k >= args.warmup:
             t_calls += evaluated_calls(res)
             t_sec += dt
-    last = {"cores": cores, "kind": kind,
-            "sample": f"{n_step} traces of the same workload per step (fresh trace ids per step)"}
     value = t_calls / t_sec
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "calls/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_sec / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
-        "data": "synthetic (splitmix64 call records, seed 1)",
-        "config": {"workload": WORKLOAD, "arrays": N_ARRAYS, "calls": N_CALLS, "adv_per1024": ADV, "fuel": FUEL},
-        "cpu_baseline": {"value": value, "unit": "calls/s", "cores": last["cores"], "kind": last["kind"],
-                         "sample": f"per step: {last['sample']}; run_annotated on all host threads"},
+        "data": "synthetic (counter-based splitmix64 call records, seed 1)",
+        "config": bench_config(world, args.traces),
+        "cpu_baseline": {"value": value, "unit": "calls/s", "cores": cores, "kind": kind,
+                         "sample": f"per step: {n_step} traces of the same workload (fresh trace ids per step), "
+                                   f"cohere::run_annotated on {cores} host threads"},
         "e2e": {"value": value, "unit": "calls/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -569,7 +583,7 @@ def run_overlap(args, ctx):
     return out
 
 
-def run_c4(args, ctx, rank, world):
+def run_c4(args, ctx, rank, world, allreduce):
     """BASELINE config 4: 64M traces (C2 format) split over the ranks as contiguous id
     ranges (strong scaling), each shard generated on its own device; device time of the
     evaluation (max over ranks), the NCCL allreduce of the counters, and an order-free
@@ -604,7 +618,8 @@ def run_c4(args, ctx, rank, world):
     c = torch.tensor([chk - (1 << 64) if chk >= 1 << 63 else chk], dtype=torch.int64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        shard.allreduce_counters(d_cnt)
+        allreduce(d_cnt)
+        torch.cuda.synchronize()
         dist.all_reduce(c)
     counters = d_cnt.cpu().numpy().view(np.uint64)[:10]
     ms = float(t.item())
@@ -688,6 +703,10 @@ def run_ours(args, rank, world, local):
     # with several ranks sharing GPUs (device = local rank mod device count): a plumbing
     # check on a one-GPU box, never a scaling number.
     backend = os.environ.get("COH_BENCH_BACKEND", "nccl")
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if backend == "nccl" and torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks need {world} GPUs, found {torch.cuda.device_count()}")
     dev = local % torch.cuda.device_count() if backend != "nccl" else local
     torch.cuda.set_device(dev)
     if world > 1:
@@ -699,6 +718,23 @@ def run_ours(args, rank, world, local):
     stream = torch.cuda.Stream()
     s = stream.cuda_stream
     from paper_1910_11110_b200 import shard
+
+    # The data-path exchange (the counter allreduce) goes through the library's own NCCL
+    # communicator (coh_comm_allreduce_counters); torch.distributed only carries the
+    # unique id, the barriers and the max-over-ranks timing.  With COH_BENCH_BACKEND=gloo
+    # (ranks sharing one GPU, a plumbing check) NCCL cannot run and torch/gloo sums instead.
+    comm = None
+    if world > 1 and backend == "nccl":
+        box = [coh.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        comm = coh.Comm.init_rank(ctx, box[0], world, rank)
+
+    def allreduce(d_counters):
+        if comm is not None:
+            comm.allreduce_counters(d_counters, s)
+        else:
+            with torch.cuda.stream(stream):
+                shard.allreduce_counters(d_counters)
 
     trace0, N = shard.shard_range(rank, world, args.traces)  # contiguous trace ids, generated on-device
     with torch.cuda.stream(stream):
@@ -717,8 +753,7 @@ def run_ours(args, rank, world, local):
         if ev1 is not None:
             ev1.record(stream)
         if world > 1:
-            with torch.cuda.stream(stream):
-                shard.allreduce_counters(d_cnt)  # the only exchange; exact integer sums
+            allreduce(d_cnt)  # the only exchange; exact integer sums
 
     clocks = ClockSampler(dev)
     clocks.start()
@@ -801,7 +836,7 @@ def run_ours(args, rank, world, local):
     clocks.stop()
     sweep_info = run_sweep(args, ctx) if (args.sweep_seeds > 0 and rank == 0) else None
     c1 = run_c1(ctx) if rank == 0 else None
-    c4 = run_c4(args, ctx, rank, world) if args.c4_traces > 0 else None
+    c4 = run_c4(args, ctx, rank, world, allreduce) if args.c4_traces > 0 else None
     overlap = run_overlap(args, ctx) if (args.overlap_views > 0 and rank == 0) else None
     container = None
     if args.container_log2_floats > 0 and rank == 0:
@@ -822,9 +857,7 @@ def run_ours(args, rank, world, local):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u16",
             "data": "synthetic (counter-based splitmix64 call records generated in HBM, seed 1)",
-            "config": {"workload": WORKLOAD, "traces_per_gpu": N, "arrays": N_ARRAYS, "calls": N_CALLS,
-                       "adv_per1024": ADV, "fuel": FUEL, "parallelism": f"dp{world} (trace-id shards)",
-                       "l2": "inputs larger than L2 (records 512 MiB per GPU), no flush"},
+            "config": bench_config(world, N),
             "transitions_per_s": float(counters[4]) * args.steps / (ms / 1e3),
             "counters_per_step": {n: int(v) for n, v in zip(coh.COUNTER_NAMES, counters[:10])},
             "roofline": {"bound": "hbm", "kernel": "k_trace_eval", "achieved": achieved, "peak": peak,
@@ -837,14 +870,38 @@ def run_ours(args, rank, world, local):
             "bitmap": bitmap, "container": container, "sweep": sweep_info, "c1": c1, "c4": c4, "overlap": overlap,
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
 
 
+def spawn_ranks(args):
+    """`--gpus N` (N > 1) without a launcher: re-run this script as N ranks under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1) and exit with its
+    status; the driver's own torchrun launch sets WORLD_SIZE and never comes here."""
+    import socket
+
+    if os.environ.get("COH_BENCH_BACKEND", "nccl") == "nccl" and args.impl == "ours":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, found {have}")
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return

@@ -191,6 +191,35 @@ int coh_eval_traces_host(coh_ctx* ctx, const coh_trace_batch* batch,
 int coh_reduce_counters(coh_ctx* ctx, const coh_trace_result* d_results, uint64_t n_traces,
                         uint64_t* d_counters, void* stream);
 
+/* ---- multi-GPU (config C4) ---------------------------------------------
+ * Traces are independent units ("independent runs may execute
+ * concurrently with no shared state"; the reference itself is single-threaded), so device
+ * d owns a contiguous trace-id shard and the ONLY exchange is one NCCL sum-allreduce of
+ * the COH_N_COUNTERS uint64 counters.  New in this build (the reference has no collective).
+ * NCCL is bound at run time (libnccl.so.2); any NCCL failure returns COH_E_NCCL. */
+#define COH_COMM_ID_BYTES 128
+typedef struct coh_comm coh_comm;
+int coh_nccl_version(int* version);
+/* One process per GPU: rank 0 makes the id, every rank receives it out of band. */
+int coh_comm_unique_id(uint8_t id[COH_COMM_ID_BYTES]);
+int coh_comm_init_rank(coh_ctx* ctx, const uint8_t id[COH_COMM_ID_BYTES], int world, int rank,
+                       coh_comm** out);
+/* One process driving n_dev devices (ncclCommInitAll): comms[d] belongs to ctxs[d]. */
+int coh_comm_init_all(coh_ctx* const* ctxs, int n_dev, coh_comm** comms);
+void coh_comm_destroy(coh_comm* comm);
+/* Sum d_counters (device, COH_N_COUNTERS) over all ranks, in place, on `stream`. */
+int coh_comm_allreduce_counters(coh_comm* comm, uint64_t* d_counters, void* stream);
+/* Single-process multi-device step: coh_eval_traces_counted of shards[d] on comms[d]'s
+ * device and streams[d], then one grouped allreduce of every d_counters[d]; afterwards
+ * each d_counters[d] holds the whole job's counters.  d_boundary may be NULL. */
+int coh_eval_traces_multi(coh_comm* const* comms, int n_dev, const coh_trace_batch* shards,
+                          coh_trace_result* const* d_results, uint32_t* const* d_boundary,
+                          uint64_t* const* d_counters, void* const* streams);
+/* Host helpers (no GPU): rank's contiguous share of `total` traces (sizes differ by at
+ * most one), and the counter vector of a host result batch (what the kernel computes). */
+int coh_shard_split(uint32_t rank, uint32_t world, uint64_t total, uint64_t* first, uint64_t* count);
+int coh_counters_host(const coh_trace_result* results, uint64_t n_traces, uint64_t* counters);
+
 /* Kernels launched by this ctx since creation (the bench's gpu_launches claim). */
 uint64_t coh_launch_count(const coh_ctx* ctx);
 
@@ -212,6 +241,7 @@ void coh_host_free(void* p);
  * Store layout on the device: two bit planes per buffer, L (local valid) and R (remote
  * valid), bit i of word i/32; initial_store puts every cell at (V,I): L = 1, R = 0.   */
 #define COH_MAX_VIEWS 16
+#define COH_ELEM_MAX_CALLS 65535 /* calls per element program (larger: COH_E_CONSTRUCTION) */
 typedef struct coh_elem_op {
   uint8_t effect;   /* COH_READ or COH_WRITE */
   uint8_t site;     /* COH_LOCAL / COH_REMOTE */

@@ -13,7 +13,13 @@ from ._ffi import (  # noqa: F401
     COUNTER_NAMES,
     RESULT_DTYPE,
     CohError,
+    Comm,
     Context,
+    comm_unique_id,
+    counters_host,
+    eval_traces_multi,
+    nccl_version,
+    shard_split,
     calltable_describe,
     calltable_program,
     gen_records_host,
@@ -37,6 +43,12 @@ from .reference_api import (  # noqa: F401
 __all__ = [
     "Context",
     "CohError",
+    "Comm",
+    "comm_unique_id",
+    "counters_host",
+    "eval_traces_multi",
+    "nccl_version",
+    "shard_split",
     "RESULT_DTYPE",
     "COUNTER_NAMES",
     "calltable_describe",

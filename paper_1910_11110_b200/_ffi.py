@@ -116,6 +116,16 @@ def lib():
             "coh_host_alloc": (vp, [C.c_size_t]),
             "coh_host_free": (None, [vp]),
             "coh_measure_link": (i, [vp, C.c_size_t, i, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+            "coh_nccl_version": (i, [C.POINTER(i)]),
+            "coh_comm_unique_id": (i, [vp]),
+            "coh_comm_init_rank": (i, [vp, vp, i, i, C.POINTER(vp)]),
+            "coh_comm_init_all": (i, [C.POINTER(vp), i, C.POINTER(vp)]),
+            "coh_comm_destroy": (None, [vp]),
+            "coh_comm_allreduce_counters": (i, [vp, vp, vp]),
+            "coh_eval_traces_multi": (i, [C.POINTER(vp), i, vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                          C.POINTER(vp)]),
+            "coh_shard_split": (i, [u32, u32, u64, C.POINTER(u64), C.POINTER(u64)]),
+            "coh_counters_host": (i, [vp, u64, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -277,3 +287,85 @@ class Context:
     def reduce_counters(self, d_results, n_traces, d_counters, stream=0):
         self._check(self._L.coh_reduce_counters(self._h, _ptr(d_results), n_traces, _ptr(d_counters), _ptr(stream)),
                     "coh_reduce_counters")
+
+
+# ---- multi-GPU (include/cohere_b200.h "multi-GPU") --------------------------------------
+COMM_ID_BYTES = 128
+
+
+def shard_split(rank: int, world: int, total: int) -> tuple[int, int]:
+    """(first trace id, count) of a rank's contiguous share of `total` traces (C ABI)."""
+    f, n = C.c_uint64(), C.c_uint64()
+    rc = lib().coh_shard_split(rank, world, total, C.byref(f), C.byref(n))
+    if rc:
+        raise CohError(rc, "coh_shard_split")
+    return f.value, n.value
+
+
+def counters_host(results: np.ndarray) -> np.ndarray:
+    """The COH_N_COUNTERS vector of a host batch of coh_trace_result records (C ABI)."""
+    r = np.ascontiguousarray(results)
+    out = np.zeros(N_COUNTERS, np.uint64)
+    rc = lib().coh_counters_host(r.ctypes.data if len(r) else None, len(r), out.ctypes.data)
+    if rc:
+        raise CohError(rc, "coh_counters_host")
+    return out
+
+
+def nccl_version() -> int | None:
+    v = C.c_int()
+    return v.value if lib().coh_nccl_version(C.byref(v)) == 0 else None
+
+
+def comm_unique_id() -> bytes:
+    buf = (C.c_uint8 * COMM_ID_BYTES)()
+    rc = lib().coh_comm_unique_id(buf)
+    if rc:
+        raise CohError(rc, "coh_comm_unique_id (NCCL unavailable?)")
+    return bytes(buf)
+
+
+class Comm:
+    """An NCCL communicator bound to one Context (coh_comm): the counter allreduce of the
+    multi-GPU trace path."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx, self._h, self._L = ctx, handle, lib()
+
+    @classmethod
+    def init_rank(cls, ctx: Context, unique_id: bytes, world: int, rank: int) -> "Comm":
+        h = C.c_void_p()
+        idb = (C.c_uint8 * COMM_ID_BYTES).from_buffer_copy(unique_id)
+        ctx._check(lib().coh_comm_init_rank(ctx._h, idb, world, rank, C.byref(h)), "coh_comm_init_rank")
+        return cls(ctx, h)
+
+    @classmethod
+    def init_all(cls, ctxs: list) -> list:
+        n = len(ctxs)
+        hs = (C.c_void_p * n)(*[c._h.value for c in ctxs])
+        out = (C.c_void_p * n)()
+        ctxs[0]._check(lib().coh_comm_init_all(hs, n, out), "coh_comm_init_all")
+        return [cls(c, C.c_void_p(out[d])) for d, c in enumerate(ctxs)]
+
+    def allreduce_counters(self, d_counters, stream=0):
+        self.ctx._check(self._L.coh_comm_allreduce_counters(self._h, _ptr(d_counters), _ptr(stream)),
+                        "coh_comm_allreduce_counters")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.coh_comm_destroy(self._h)
+            self._h = None
+
+
+def eval_traces_multi(comms: list, shards: list, d_results: list, d_counters: list, streams: list,
+                      d_boundary: list | None = None):
+    """coh_eval_traces_multi: shards[d] = (d_records, n_traces, n_calls, n_arrays, fuel)."""
+    n = len(comms)
+    batches = (_Batch * n)()
+    for d, (rec, nt, nc, na, fuel) in enumerate(shards):
+        batches[d] = Context._batch(rec, nt, nc, na, fuel, None)
+    arr = lambda xs: (C.c_void_p * n)(*[_ptr(x) for x in xs])  # noqa: E731
+    rc = lib().coh_eval_traces_multi((C.c_void_p * n)(*[c._h.value for c in comms]), n, batches, arr(d_results),
+                                     arr(d_boundary) if d_boundary is not None else None, arr(d_counters),
+                                     arr(streams))
+    comms[0].ctx._check(rc, "coh_eval_traces_multi")

@@ -60,9 +60,14 @@ int eval_device(coh_ctx* ctx, const coh_trace_batch* b, const uint16_t* d_record
   int rc = bytes_mode(ctx, b, &uniform, &ub);
   if (rc) return rc;
   if (n_traces == 0) return COH_OK;
-  if (!uniform)
-    COH_CUDA(ctx, cudaMemcpyAsync(ctx->d_bytes, b->array_bytes, sizeof(uint64_t) * b->n_arrays,
+  // non-uniform sizes: a stream-ordered copy private to this launch (launches of one
+  // context on different streams may run concurrently, so no per-context buffer)
+  uint64_t* d_bytes = nullptr;
+  if (!uniform) {
+    COH_CUDA(ctx, cudaMallocAsync(reinterpret_cast<void**>(&d_bytes), sizeof(uint64_t) * COH_MAX_ARRAYS, s));
+    COH_CUDA(ctx, cudaMemcpyAsync(d_bytes, b->array_bytes, sizeof(uint64_t) * b->n_arrays,
                                   cudaMemcpyHostToDevice, s));
+  }
   cohb::TraceLaunch L;
   L.records = d_records;
   L.n_traces = n_traces;
@@ -73,7 +78,7 @@ int eval_device(coh_ctx* ctx, const coh_trace_batch* b, const uint16_t* d_record
   L.check_fuel = (int64_t)b->fuel < 6 * (int64_t)b->n_calls;
   L.uniform_bytes = uniform;
   L.bytes_uniform = ub;
-  L.d_array_bytes = ctx->d_bytes;
+  L.d_array_bytes = d_bytes;
   L.d_lut = ctx->d_lut;
   L.d_slow = ctx->d_slow;
   L.results = d_results;
@@ -92,6 +97,7 @@ int eval_device(coh_ctx* ctx, const coh_trace_batch* b, const uint16_t* d_record
   std::string err;
   rc = cohb::launch_trace_eval(L, s, &err);
   if (ticket) cudaFreeAsync(ticket, s);
+  if (d_bytes) cudaFreeAsync(d_bytes, s);
   if (rc) {
     ctx->err = err;
     return rc;
@@ -122,7 +128,6 @@ int coh_ctx_create(int device, coh_ctx** out) {
   do {
     if ((e = cudaMalloc(&ctx->d_lut, sizeof table.lut)) != cudaSuccess) break;
     if ((e = cudaMalloc(&ctx->d_slow, sizeof table.slow)) != cudaSuccess) break;
-    if ((e = cudaMalloc(&ctx->d_bytes, sizeof(uint64_t) * COH_MAX_ARRAYS)) != cudaSuccess) break;
     if ((e = cudaMemcpy(ctx->d_lut, table.lut, sizeof table.lut, cudaMemcpyHostToDevice)) != cudaSuccess) break;
     if ((e = cudaMemcpy(ctx->d_slow, table.slow, sizeof table.slow, cudaMemcpyHostToDevice)) != cudaSuccess) break;
     if ((e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess) break;
@@ -132,7 +137,6 @@ int coh_ctx_create(int device, coh_ctx** out) {
       if ((e = cudaDeviceGetDefaultMemPool(&pool, device)) != cudaSuccess) break;
       if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess) break;
     }
-    cohb::trace_eval_set_smem_attr();
     int tpb = 0;
     std::string err;
     rc = cohb::trace_eval_occupancy(&ctx->blocks_per_sm, &tpb, 256, &err);
@@ -149,7 +153,6 @@ void coh_ctx_destroy(coh_ctx* ctx) {
   if (!ctx) return;
   cudaFree(ctx->d_lut);
   cudaFree(ctx->d_slow);
-  cudaFree(ctx->d_bytes);
   for (int k = 0; k < 2; ++k) {
     cudaFree(ctx->d_rec[k]);
     cudaFree(ctx->d_res[k]);

@@ -69,6 +69,10 @@ int elem_compile(const coh_elem_program* progs, uint32_t n, ElemPlan* plan, std:
       *err = "element program " + std::to_string(b) + ": n_cells must be >= 1 and n_views <= 16";
       return COH_E_CONSTRUCTION;
     }
+    if (P.n_calls > COH_ELEM_MAX_CALLS) {  // ElemOp::call and the stuck call index are 16-bit
+      *err = "element program " + std::to_string(b) + ": more than " + std::to_string(COH_ELEM_MAX_CALLS) + " calls";
+      return COH_E_CONSTRUCTION;
+    }
     for (uint32_t v = 0; v < P.n_views; ++v)
       if (P.view_lo[v] > P.view_hi[v] || P.view_hi[v] >= P.n_cells) {
         *err = "view v" + std::to_string(v) + " range does not fit its buffer";  // program.hpp:65-68

@@ -86,7 +86,7 @@ struct TraceLaunch {
   bool check_fuel;
   bool uniform_bytes;
   uint64_t bytes_uniform;
-  const uint64_t* d_array_bytes;   // device, n_arrays (used when !uniform_bytes)
+  const uint64_t* d_array_bytes;   // device, n_arrays, private to the launch (used when !uniform_bytes)
   const uint32_t* d_lut;
   const uint32_t* d_slow;
   coh_trace_result* results;
@@ -96,7 +96,6 @@ struct TraceLaunch {
   unsigned int* ticket;  // device, zeroed, private to this launch (dynamic trace batches)
 };
 int launch_trace_eval(const TraceLaunch& p, void* stream, std::string* err);
-void trace_eval_set_smem_attr();
 int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t n_calls, std::string* err);
 int launch_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
                        uint32_t n_arrays, uint32_t adv_per1024, uint16_t* d_records, void* stream,
@@ -112,7 +111,6 @@ struct coh_ctx {
   std::string err;
   uint32_t* d_lut = nullptr;
   uint32_t* d_slow = nullptr;
-  uint64_t* d_bytes = nullptr;
   int sms = 148;
   int blocks_per_sm = 1;       // trace_eval residency
   uint64_t launches = 0;

@@ -21,6 +21,9 @@ namespace cohb {
 //   BC_END    program done
 enum : uint32_t { BC_EFF = 1, BC_WHOLE = 2, BC_IF = 3, BC_WHILE = 4, BC_JMP = 5, BC_BEND = 6, BC_END = 7 };
 
+// SweepOut packs the completed-block count in 5 bits and boundary_ok in bits 16-23.
+constexpr uint32_t kSweepMaxBlocks = 8;
+
 struct SweepProgram {
   std::vector<uint32_t> code;
   std::vector<uint16_t> checks;  // (abstract key | concrete key << 8) pairs for abstraction_correct

@@ -455,6 +455,10 @@ extern "C" int coh_sweep(coh_ctx* ctx, uint64_t seed0, uint32_t n_seeds, const c
   using namespace cohb;
   if (!ctx || max_decisions > 24) return COH_E_ARG;
   const coh_gen_limits L = limits ? *limits : coh_gen_limits{3, 2, 3, 6, 2, 1, 1, 0};
+  if (L.max_blocks > kSweepMaxBlocks) {  // SweepOut carries 5 block bits and 8 boundary bits
+    ctx->err = "coh_sweep: max_blocks must be <= " + std::to_string(kSweepMaxBlocks);
+    return COH_E_ARG;
+  }
   coh_sweep_stats st{};
   std::vector<uint32_t> code;
   std::vector<uint16_t> checks;

@@ -944,6 +944,5 @@ int launch_trace_eval(const TraceLaunch& L, void* stream, std::string* err) {
   return COH_E_ARG;
 }
 
-void trace_eval_set_smem_attr() {}
 
 }  // namespace cohb

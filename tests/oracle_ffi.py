@@ -10,7 +10,29 @@ import os
 
 import numpy as np
 
-from paper_1910_11110_b200._ffi import RESULT_DTYPE, _Outcome, boundary_words, records_elems
+# The ABI record layouts of include/cohere_b200.h, restated here so that the checker side
+# (tests, the bench's reference arm) never imports or loads the product package.
+RESULT_DTYPE = np.dtype(
+    [("state", "<u4", (8,)), ("transfer_bytes", "<u8"), ("steps", "<u4"), ("transfers", "<u4"),
+     ("calls_done", "<u4"), ("violations", "<u4"), ("stuck_call", "<u4"), ("status", "u1"),
+     ("stuck_array", "u1"), ("stuck_effect", "u1"), ("stuck_flags", "u1")])
+assert RESULT_DTYPE.itemsize == 64
+
+
+class _Outcome(C.Structure):  # coh_call_outcome
+    _fields_ = [(n, C.c_uint8) for n in ("status", "state_after", "steps", "transfers", "viol_before",
+                                          "viol_after", "stuck_effect", "stuck_flags")]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_}
+
+
+def records_elems(n_traces: int, n_calls: int) -> int:
+    return ((n_calls + 7) // 8) * n_traces * 8
+
+
+def boundary_words(n_calls: int) -> int:
+    return (n_calls + 31) // 32
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE_SO = os.path.join(ROOT, "oracle", "_build", "libcohere_oracle.so")

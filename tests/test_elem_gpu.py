@@ -104,3 +104,16 @@ def test_two_chain_batch_vs_oracle(ctx):
     out = elem_eval(ctx, [p for _, _, p, _ in items])
     for i, (key, params, p, want) in enumerate(items):
         compare(out, i, want, key)
+
+
+def test_too_many_calls_is_construction_error(ctx):
+    """ElemOp carries a 16-bit call index: programs over COH_ELEM_MAX_CALLS calls are
+    refused with ConstructionError instead of wrapping the boundary/stuck indices."""
+    from paper_1910_11110_b200.elem import Program, elem_eval
+    from paper_1910_11110_b200 import CohError
+    p = Program.generate(5, 0, 1024, 2, 65536, 0)
+    with pytest.raises(CohError) as e:
+        elem_eval(ctx, [p], want_planes=False)
+    assert e.value.code == 1
+    ok = Program.generate(5, 0, 1024, 2, 65535, 0, fuel=(1 << 31) - 1)
+    elem_eval(ctx, [ok], want_planes=False)

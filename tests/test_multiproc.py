@@ -90,3 +90,54 @@ def test_results_checksum_adds_over_shards():
         assert total == whole
     res[64 * 517 + 9] ^= 1
     assert shard.results_checksum(res) != whole
+
+
+def _worker_cabi(rank, world, port, outdir):
+    """The same step through the product's C ABI host entry points: coh_shard_split for
+    the rank's contiguous trace ids and coh_counters_host for its counter vector (the
+    vector the device kernel computes), summed over the ranks with gloo."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    total = world * N_PER + 3  # ragged: the shards differ by one trace
+    t0, n = coh.shard_split(rank, world, total)
+    assert (t0, n) == shard.split_range(rank, world, total)
+    recs = o.orc_gen(SEED, t0, n, NC, NA, ADV)
+    res, _ = o.orc_eval(recs, n, NC, NA)
+    mine = coh.counters_host(res)
+    assert np.array_equal(mine, shard.counters_from_results(res))
+    cnt = torch.from_numpy(mine.view(np.int64).copy())
+    shard.allreduce_counters(cnt)
+    if rank == 0:
+        np.save(os.path.join(outdir, "cnt.npy"), cnt.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_cabi_sharded_counters_world2():
+    world = 2
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker_cabi, args=(world, _free_port(), d), nprocs=world, join=True)
+        total = world * N_PER + 3
+        res, _ = o.orc_eval(o.orc_gen(SEED, 0, total, NC, NA, ADV), total, NC, NA)
+        assert np.array_equal(np.load(os.path.join(d, "cnt.npy")).view(np.uint64), coh.counters_host(res))
+
+
+def test_cabi_shard_split_and_errors():
+    for world in (1, 2, 3, 8):
+        for total in (0, 1, 7, 1000, 1 << 26):
+            assert [coh.shard_split(r, world, total) for r in range(world)] == \
+                [shard.split_range(r, world, total) for r in range(world)]
+    with pytest.raises(coh.CohError):
+        coh.shard_split(2, 2, 10)
+    with pytest.raises(coh.CohError):
+        coh.shard_split(0, 0, 10)
+    assert np.array_equal(coh.counters_host(np.zeros(0, coh.RESULT_DTYPE)), np.zeros(len(coh.COUNTER_NAMES), np.uint64))
+
+
+def test_nccl_binds_at_run_time():
+    """The library loads without linking NCCL; the communicator entry points bind
+    libnccl.so.2 at run time (a unique id needs no GPU)."""
+    v = coh.nccl_version()
+    assert v is not None and v >= 22000
+    assert len(coh.comm_unique_id()) == 128

@@ -86,3 +86,14 @@ def test_acceptance_criterion_1_enumeration(ctx):
     assert (st["programs"], st["done"], st["stuck"], st["fuel_exhausted"], st["unsafe"]) == (11111, 4565, 6546, 0, 0)
     want = np.load(os.path.join(os.path.dirname(__file__), "golden", "enum4.npy"))
     assert np.array_equal(statuses, want)
+
+
+@pytest.mark.gpu
+def test_sweep_rejects_more_than_8_blocks(ctx):
+    """SweepOut carries boundary_ok for 8 blocks: larger limits are an argument error."""
+    from paper_1910_11110_b200 import CohError
+    from paper_1910_11110_b200.sweep import GenLimits, sweep
+    with pytest.raises(CohError) as e:
+        sweep(ctx, 0, 4, 2, 10000, limits=GenLimits(max_blocks=9))
+    assert e.value.code == 6
+    sweep(ctx, 0, 4, 2, 10000, limits=GenLimits(max_blocks=8))
