@@ -41,7 +41,7 @@ def ref_fn():
                           C.c_size_t, C.c_char_p, C.c_size_t, C.POINTER(C.c_int)]
 
     def call(cmd, src, raw=0, no_overlap=0, fuel=10000, schedule="", trace=0):
-        cap = 1 << 20
+        cap = 1 << 24
         out, err, code = C.create_string_buffer(cap), C.create_string_buffer(cap), C.c_int()
         rc = R.ref_cli(cmd.encode(), src.encode(), raw, no_overlap, fuel, schedule.encode(), trace, out, cap, err, cap,
                        C.byref(code))

@@ -120,3 +120,41 @@ def test_run_json_on_gpu(ctx):
     assert rec[0] == {"outcome": "stuck", "schedule_consumed": 0, "steps": 1,
                       "stuck": {"effect": "r", "have": "(V,I)", "key": "x", "site": "remote"}}
     assert rec[1:] == [{"key": "x", "local": "V", "remote": "I"}, {"key": "x^", "local": "V", "remote": "I"}]
+
+
+WIDE = [
+    # whole-view syncs over tens of thousands of cells, overlap shadows, scalars
+    ("run", "scalar x\nbuffer b[65536]\nview v = b[0:40000]\nview u = b[30000:65535]\nview t = b[100:200]\n"
+            "RW(v) { w v[5]; r v[39999]; }\nGR(u) { gr u[0]; }\nRW(x), R(t) { r t[3]; w x; }\n"
+            "GRW(u) { gw u[7]; }\nR(v) { r v[30001]; }\n", 0, ""),
+    ("run", "buffer b[70000]\nview v = b[0:69999]\nview w = b[12345:12400]\nGRW(w) { gw w[0]; }\nR(v) { r v[12345]; }\n"
+            "RW(v) { w v[12345]; }\nGR(w) { gr w[3]; }\n", 0, ""),
+    # raw: a stuck whole-view sync (the first failing cell, ascending) and fuel cut-offs
+    ("run", "buffer b[100000]\nview v = b[5:99990]\nview u = b[50000:50010]\nw u[3];\ngw u[4];\npush v;\npull v;\n", 1, ""),
+    ("run", "buffer b[4096]\nview v = b[0:4095]\nscalar s\nwhile (opaque) { push v; w s; }\npull v;\n", 1, "1101"),
+    ("trace", "buffer b[300]\nview v = b[0:299]\nview u = b[250:299]\nGRW(u) { gw u[1]; }\nR(v) { r v[251]; }\n", 0, ""),
+    ("trace", "scalar a\nscalar c\nbuffer b[40]\nview v = b[3:39]\nif (opaque) { push v; gw v[2]; pull v; } else { w a; }\n"
+              "while (valid(a)) { gw a; }\nr c;\n", 1, "1"),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not o.have_ref(), reason="oracle/_ref (the compiled reference) not present")
+def test_run_wide_programs_match_live_reference(ctx):
+    """Programs far beyond 32 store keys (buffers up to 100000 cells) run on the bit-plane
+    interpreter and match the reference CLI byte for byte, text and JSON, with and without
+    the step trace, and with a small fuel."""
+    sys.path.insert(0, os.path.join(HERE, "golden"))
+    from make_golden_cli import ref_fn
+    ref = ref_fn()
+    for cmd, src, raw, sched in WIDE:
+        for fuel in (10000, 7):
+            c = ref(cmd, src, raw, 0, fuel, sched)
+            assert got(c, ctx) == want(c), (cmd, src, fuel)
+            if cmd == "run" and len(src) < 200 and "b[4096]" in src:
+                c2 = dict(c, trace=1)
+                r2 = ref(cmd, src, raw, 0, fuel, sched, 1)
+                assert got(c2, ctx) == want(r2), (src, fuel)
+        out, err, code = run_cli(cmd, src, ctx, raw=bool(raw), json=True, schedule=sched or None)
+        assert code == ref(cmd, src, raw, 0, 10000, sched)["exit"]
+        assert all(line.startswith("{") for line in out.splitlines())
