@@ -264,7 +264,36 @@ typedef struct coh_elem_program {
   uint32_t n_calls;
   int32_t fuel;
   const coh_elem_call* calls;
+  /* Pre-fragmented start (rho = 2^-frag_log2; 0 = none): cell i starts
+   * coherent, at (V,V), instead of initial_store's (V,I) iff bit i%32 of
+   * coh_frag_mask(frag_seed, frag_log2, i/32) is set -- as if those cells had already been
+   * synchronised.  Every view stays abstraction-correct ((V,I) <= (V,V), modes.hpp:71-75);
+   * a sync's delta then skips the coherent cells, so its transfer ranges fragment with
+   * density rho.  The prelude takes no steps; the run is run_annotated from that store. */
+  uint64_t frag_seed;
+  uint32_t frag_log2;        /* 0..32 */
+  uint32_t pad;
 } coh_elem_program;
+
+/* Word w of the fragmentation mask: the AND of frag_log2 independent 32-bit draws, so
+ * each cell is set with probability 2^-frag_log2 (draw j = half j%2 of
+ * splitmix64(frag_seed ^ (w << 6) ^ (j >> 1))). */
+static inline uint64_t coh_splitmix64_h(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+static inline uint32_t coh_frag_mask(uint64_t frag_seed, uint32_t frag_log2, uint32_t w) {
+  if (frag_log2 == 0) return 0u;
+  uint32_t m = 0xFFFFFFFFu;
+  for (uint32_t j = 0; j < frag_log2; j += 2) {
+    const uint64_t h = coh_splitmix64_h(frag_seed ^ ((uint64_t)w << 6) ^ (uint64_t)(j >> 1));
+    m &= (uint32_t)h;
+    if (j + 1 < frag_log2) m &= (uint32_t)(h >> 32);
+  }
+  return m;
+}
 /* Per-program outcome.  stuck key: element b[stuck_index] (key kind concrete) or the
  * abstract key of view stuck_index (key kind abstract).  Transfers are the executed
  * concrete whole-view syncs; their transfer ranges are the maximal runs of changed

@@ -355,6 +355,9 @@ int orc_elem_run(const coh_elem_program* P, coh_elem_result* out, uint32_t* plan
   st.R = (uint8_t*)malloc(P->n_cells);
   memset(st.L, 1, P->n_cells); /* initial_store: (V,I) */
   memset(st.R, 0, P->n_cells);
+  if (P->frag_log2 > 32) return -1;
+  for (uint32_t i = 0; i < P->n_cells; ++i) /* pre-fragmented cells start coherent, (V,V) */
+    if ((coh_frag_mask(P->frag_seed, P->frag_log2, i / 32) >> (i % 32)) & 1u) st.R[i] = 1;
   for (uint32_t v = 0; v < P->n_views; ++v) st.abs[v] = 1;
   st.fuel = P->fuel;
   st.out = out;

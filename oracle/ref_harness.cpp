@@ -291,6 +291,9 @@ static int ref_elem_run_impl(const coh_elem_program* P, coh_elem_result* out, ui
     AnnotatedProgram q = rewrite_program(p, build_registry(p.decls));
     std::memset(out, 0, sizeof *out);
     Store store = initial_store(q.decls);
+    for (uint32_t i = 0; i < P->n_cells; ++i)  // pre-fragmented start: these cells coherent
+      if ((coh_frag_mask(P->frag_seed, P->frag_log2, i / 32) >> (i % 32)) & 1u)
+        store.put(VarKey::element("b", (int)i), ValidityPair{Validity::Valid, Validity::Valid});
     Schedule schedule;
     int64_t steps = 0;
     RunStatus status = RunStatus::Done;

@@ -17,6 +17,7 @@
 #include <string>
 
 #include "elem.hpp"
+#include "gen_common.h"
 #include "internal.hpp"
 
 namespace cohb {
@@ -527,32 +528,37 @@ int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, uint32_t n_sync_tiles,
   return COH_OK;
 }
 
-// Initial store: every cell (V,I) -> L = 1 on [0, n_cells), R = 0 (program.hpp:174-184).
-// 128-bit stores, one 4-word group per thread iteration.
-__global__ void k_elem_init(uint32_t* planes, uint32_t W, const uint32_t* n_cells, uint32_t n_progs) {
+// Initial store: every cell (V,I) -> L = 1 on [0, n_cells), R = 0 (program.hpp:174-184),
+// except the pre-fragmented cells (coh_frag_mask), which start coherent: (V,V), R = 1.  pinit[b] =
+// {n_cells, frag_log2, frag_seed lo, frag_seed hi}.  128-bit stores, one 4-word group
+// per thread iteration.
+__global__ void k_elem_init(uint32_t* planes, uint32_t W, const uint4* __restrict__ pinit, uint32_t n_progs) {
   const uint64_t total4 = (uint64_t)n_progs * 2u * W / 4u;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total4;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t w0 = i * 4u;
     const uint32_t b = (uint32_t)(w0 / (2u * W));
     const uint32_t r = (uint32_t)(w0 - (uint64_t)b * 2u * W);
-    uint32_t q[4] = {0u, 0u, 0u, 0u};
-    if (r < W) {
-      const uint32_t n = n_cells[b];
+    const uint32_t rw = r < W ? r : r - W;  // word index within the plane
+    const uint4 pi = pinit[b];
+    const uint32_t n = pi.x;
+    const uint64_t seed = (uint64_t)pi.z | ((uint64_t)pi.w << 32);
+    uint32_t q[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t w = r + k;
-        q[k] = (w + 1) * 32u <= n ? 0xFFFFFFFFu : (w * 32u < n ? (0xFFFFFFFFu >> (32u - (n - w * 32u))) : 0u);
-      }
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t w = rw + k;
+      const uint32_t live = (w + 1) * 32u <= n ? 0xFFFFFFFFu : (w * 32u < n ? (0xFFFFFFFFu >> (32u - (n - w * 32u))) : 0u);
+      const uint32_t frag = (r >= W && live) ? coh_frag_word(seed, pi.y, w) & live : 0u;
+      q[k] = r < W ? live : frag;
     }
     __stcg(reinterpret_cast<uint4*>(planes) + i, make_uint4(q[0], q[1], q[2], q[3]));
   }
 }
 
-int launch_elem_init(uint32_t* planes, uint32_t W, const uint32_t* n_cells, uint32_t n_progs, void* stream,
+int launch_elem_init(uint32_t* planes, uint32_t W, const uint32_t* pinit, uint32_t n_progs, void* stream,
                      std::string* err) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  k_elem_init<<<148 * 8, 256, 0, s>>>(planes, W, n_cells, n_progs);
+  k_elem_init<<<148 * 8, 256, 0, s>>>(planes, W, reinterpret_cast<const uint4*>(pinit), n_progs);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("element init launch: ") + cudaGetErrorString(e);

@@ -118,7 +118,8 @@ struct ElemDev {
   uint32_t stage;
 };
 int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, uint32_t n_sync_tiles, void* stream, std::string* err);
-int launch_elem_init(uint32_t* planes, uint32_t W, const uint32_t* n_cells, uint32_t n_progs, void* stream,
+// pinit: per program {n_cells, frag_log2, frag_seed lo, frag_seed hi} (device)
+int launch_elem_init(uint32_t* planes, uint32_t W, const uint32_t* pinit, uint32_t n_progs, void* stream,
                      std::string* err);
 
 }  // namespace cohb

@@ -69,6 +69,10 @@ int elem_compile(const coh_elem_program* progs, uint32_t n, ElemPlan* plan, std:
       *err = "element program " + std::to_string(b) + ": n_cells must be >= 1 and n_views <= 16";
       return COH_E_CONSTRUCTION;
     }
+    if (P.frag_log2 > 32) {
+      *err = "element program " + std::to_string(b) + ": frag_log2 must be <= 32";
+      return COH_E_CONSTRUCTION;
+    }
     if (P.n_calls > COH_ELEM_MAX_CALLS) {  // ElemOp::call and the stuck call index are 16-bit
       *err = "element program " + std::to_string(b) + ": more than " + std::to_string(COH_ELEM_MAX_CALLS) + " calls";
       return COH_E_CONSTRUCTION;
@@ -374,15 +378,18 @@ struct ElemGroup {
     COH_E(alloc(tbase, (size_t)max_tiles * 2 * 8));
     COH_E(alloc(vlo, (size_t)n * COH_MAX_VIEWS * 4));
     COH_E(alloc(vhi, (size_t)n * COH_MAX_VIEWS * 4));
-    COH_E(alloc(ncell, (size_t)n * 4));
+    COH_E(alloc(ncell, (size_t)n * 16));
     COH_E(alloc(bnd, (size_t)n * bwords * 4));
     if (runs_cap) {
       COH_E(alloc(rlo, (size_t)n * runs_cap * 4));
       COH_E(alloc(rhi, (size_t)n * runs_cap * 4));
     }
-    std::vector<uint32_t> h_vlo((size_t)n * COH_MAX_VIEWS, 0), h_vhi((size_t)n * COH_MAX_VIEWS, 0), h_nc(n);
+    std::vector<uint32_t> h_vlo((size_t)n * COH_MAX_VIEWS, 0), h_vhi((size_t)n * COH_MAX_VIEWS, 0), h_nc(4 * (size_t)n);
     for (uint32_t b = 0; b < n; ++b) {
-      h_nc[b] = progs[b].n_cells;
+      h_nc[4 * b] = progs[b].n_cells;
+      h_nc[4 * b + 1] = progs[b].frag_log2;
+      h_nc[4 * b + 2] = (uint32_t)progs[b].frag_seed;
+      h_nc[4 * b + 3] = (uint32_t)(progs[b].frag_seed >> 32);
       for (uint32_t v = 0; v < progs[b].n_views; ++v) {
         h_vlo[(size_t)b * COH_MAX_VIEWS + v] = progs[b].view_lo[v];
         h_vhi[(size_t)b * COH_MAX_VIEWS + v] = progs[b].view_hi[v];

@@ -26,3 +26,14 @@ COH_HD uint16_t coh_gen_record(uint64_t seed, uint64_t trace_id, uint32_t call_i
   const uint32_t var = adv ? 1u + (uint32_t)((((h >> 59) & 0x1Full) * 7ull) >> 5) : 0u;
   return (uint16_t)((arr << 8) | (kind << 2) | (site << 4) | (var << 5));
 }
+
+// Fragmentation mask of plane word w (include/cohere_b200.h coh_frag_mask, same draws).
+COH_HD uint32_t coh_frag_word(uint64_t frag_seed, uint32_t frag_log2, uint32_t w) {
+  uint32_t m = frag_log2 ? 0xFFFFFFFFu : 0u;
+  for (uint32_t j = 0; j < frag_log2; j += 2) {
+    const uint64_t h = coh_splitmix64(frag_seed ^ ((uint64_t)w << 6) ^ (uint64_t)(j >> 1));
+    m &= (uint32_t)h;
+    if (j + 1 < frag_log2) m &= (uint32_t)(h >> 32);
+  }
+  return m;
+}

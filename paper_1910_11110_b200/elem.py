@@ -24,7 +24,8 @@ class ElemCall(C.Structure):
 
 class ElemProgram(C.Structure):
     _fields_ = [("n_cells", C.c_uint32), ("n_views", C.c_uint32), ("view_lo", C.c_void_p), ("view_hi", C.c_void_p),
-                ("n_calls", C.c_uint32), ("fuel", C.c_int32), ("calls", C.c_void_p)]
+                ("n_calls", C.c_uint32), ("fuel", C.c_int32), ("calls", C.c_void_p), ("frag_seed", C.c_uint64),
+                ("frag_log2", C.c_uint32), ("pad", C.c_uint32)]
 
 
 class ElemResult(C.Structure):
@@ -42,14 +43,18 @@ class ElemStats(C.Structure):
                 ("stages", C.c_uint32), ("pad", C.c_uint32)]
 
 
-assert C.sizeof(ElemCall) == 32 and C.sizeof(ElemResult) == 56 and C.sizeof(ElemProgram) == 40
+assert C.sizeof(ElemCall) == 32 and C.sizeof(ElemResult) == 56 and C.sizeof(ElemProgram) == 56
 
 
 class Program:
     """One buffer `b` of n_cells, views v0..v{k-1} (absolute inclusive ranges) and calls."""
 
-    def __init__(self, n_cells: int, view_lo, view_hi, calls, fuel: int = 10000):
+    def __init__(self, n_cells: int, view_lo, view_hi, calls, fuel: int = 10000, frag_log2: int = 0,
+                 frag_seed: int = 0):
+        """frag_log2 > 0: a pre-fragmented start, 2^-frag_log2 of the cells already
+        coherent at (V,V) (coh_elem_program.frag_*; SURVEY §8(d) C3's rho)."""
         self.n_cells = int(n_cells)
+        self.frag_log2, self.frag_seed = int(frag_log2), int(frag_seed)
         self.view_lo = np.ascontiguousarray(view_lo, dtype=np.uint32)
         self.view_hi = np.ascontiguousarray(view_hi, dtype=np.uint32)
         if isinstance(calls, C.Array):
@@ -68,7 +73,7 @@ class Program:
 
     @classmethod
     def generate(cls, seed: int, prog_id: int, n_cells: int, n_views: int, n_calls: int, adv_per1024: int,
-                 fuel: int = 1 << 30):
+                 fuel: int = 1 << 30, frag_log2: int = 0):
         lo = np.zeros(n_views, np.uint32)
         hi = np.zeros(n_views, np.uint32)
         calls = (ElemCall * max(1, n_calls))()
@@ -76,7 +81,7 @@ class Program:
                                 C.addressof(calls))
         if rc:
             raise CohError(rc, "coh_elem_gen")
-        p = cls(n_cells, lo, hi, calls, fuel)
+        p = cls(n_cells, lo, hi, calls, fuel, frag_log2, (seed * 0x9E3779B97F4A7C15 + prog_id) & ((1 << 64) - 1))
         p.n_calls = n_calls
         return p
 
@@ -90,7 +95,7 @@ class Program:
 
     def struct(self) -> ElemProgram:
         return ElemProgram(self.n_cells, len(self.view_lo), self.view_lo.ctypes.data, self.view_hi.ctypes.data,
-                           self.n_calls, self.fuel, C.addressof(self.calls))
+                           self.n_calls, self.fuel, C.addressof(self.calls), self.frag_seed, self.frag_log2, 0)
 
 
 def program_array(programs):

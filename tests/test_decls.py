@@ -16,7 +16,8 @@ class Batch(C.Structure):  # coh_trace_batch
 
 class Prog(C.Structure):  # coh_elem_program
     _fields_ = [("n_cells", C.c_uint32), ("n_views", C.c_uint32), ("view_lo", C.c_void_p), ("view_hi", C.c_void_p),
-                ("n_calls", C.c_uint32), ("fuel", C.c_int32), ("calls", C.c_void_p)]
+                ("n_calls", C.c_uint32), ("fuel", C.c_int32), ("calls", C.c_void_p), ("frag_seed", C.c_uint64),
+                ("frag_log2", C.c_uint32), ("pad", C.c_uint32)]
 
 
 def _lib():

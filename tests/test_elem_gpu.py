@@ -117,3 +117,35 @@ def test_too_many_calls_is_construction_error(ctx):
     assert e.value.code == 1
     ok = Program.generate(5, 0, 1024, 2, 65535, 0, fuel=(1 << 31) - 1)
     elem_eval(ctx, [ok], want_planes=False)
+
+
+def _want(which, p, runs_cap):
+    rc, r, L, R, va, b, runs = o.elem_run(which, p, runs_cap)
+    assert rc in (0, -3)
+    return {"result": np.array(r.as_tuple(), np.uint64), "planes": np.stack([L, R]), "view_abs": va,
+            "boundary": b, "runs": runs}
+
+
+@pytest.mark.skipif(not o.have_ref(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("n_cells", [1 << 16, 1 << 20])
+def test_vs_live_reference_large(ctx, n_cells):
+    """coh_elem_eval against the reference itself (rewrite_program + run_annotated over its
+    std::map store, oracle/_ref) at 2^16 and 2^20 cells, plain and pre-fragmented starts
+    (rho = 2^-8 and 1/2): results, planes, abstract pairs, boundary bits and every
+    transfer range."""
+    cap = 1 << 20
+    progs = [Program.generate(31, i, n_cells, 8, 8, 64, frag_log2=f) for i, f in enumerate([0, 8, 1])]
+    out = elem_eval(ctx, progs, runs_cap=cap)
+    for i, p in enumerate(progs):
+        compare(out, i, _want("ref", p, cap), f"n={n_cells} prog={i}", runs_cap=cap)
+
+
+@pytest.mark.parametrize("frag_log2", [16, 8, 1])
+def test_fragmented_vs_oracle_2p24(ctx, frag_log2):
+    """The C3 shape with the SURVEY §8(d) fragmentation levels at 2^24 cells, against the
+    C restatement (pinned to the reference above and in the CPU tests)."""
+    cap = 1 << 23
+    progs = [Program.generate(41, i, 1 << 24, 8, 8, 64, frag_log2=frag_log2) for i in range(2)]
+    out = elem_eval(ctx, progs, runs_cap=cap)
+    for i, p in enumerate(progs):
+        compare(out, i, _want("orc", p, cap), f"rho=2^-{frag_log2} prog={i}", runs_cap=cap)

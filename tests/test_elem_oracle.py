@@ -71,3 +71,23 @@ def test_oracle_vs_live_reference_fresh_programs():
         assert a[1].as_tuple() == b[1].as_tuple(), pid
         for x, y in zip(a[2:], b[2:]):
             assert np.array_equal(x, y), pid
+
+
+@pytest.mark.skipif(not o.have_ref(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("frag_log2", [1, 4, 8])
+def test_oracle_vs_live_reference_fragmented(frag_log2):
+    """Pre-fragmented starts (coh_elem_program.frag_*: 2^-frag_log2 of the cells already
+    coherent): the reference run from that store and the oracle agree, and the first
+    syncs' transfer ranges are split by the coherent cells."""
+    runs = 0
+    for pid in range(12):
+        rng = np.random.default_rng(1000 + pid)
+        p = Program.generate(77, pid, int(rng.choice([333, 4096, 1 << 14])), int(rng.integers(1, 9)),
+                             int(rng.integers(2, 9)), int(rng.choice([0, 200])), frag_log2=frag_log2)
+        a, b = o.elem_run("ref", p, 1 << 14), o.elem_run("orc", p, 1 << 14)
+        assert a[0] == b[0] == 0
+        assert a[1].as_tuple() == b[1].as_tuple(), pid
+        for x, y in zip(a[2:], b[2:]):
+            assert np.array_equal(x, y), pid
+        runs += a[1].n_runs
+    assert runs > 12 * (1 if frag_log2 == 8 else 4)
