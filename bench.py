@@ -244,43 +244,61 @@ def run_reference_arm(args, rank, world):
 
 
 # ---------------------------------------------------------------- bitmaps (C3)
+RHOS = (("0", 0), ("2^-16", 16), ("2^-8", 8), ("1/2", 1))
+
+
 def run_bitmap(args, ctx, rank, world):
     """BASELINE config 3 per GPU: B buffers x 2^24 cells, 8 overlapping views each, K calls
     per buffer through the element path (overlap closure, whole-view syncs + transfer-range
-    extraction, element range bodies, per-view boundary checks).  Algorithmic bytes per
-    SURVEY §8(d); device time by CUDA events inside coh_elem_eval; max over ranks."""
+    extraction, element range bodies, per-view boundary checks), at each SURVEY §8(d)
+    pre-fragmentation level rho in {0, 2^-16, 2^-8, 1/2} (that fraction of the cells starts
+    coherent, so the syncs' transfer ranges fragment).  Every transfer range is written on
+    the device (runs_cap from a counting pass; none are copied back inside the timing).
+    Algorithmic bytes per SURVEY §8(d), 8 B per written range; device time by CUDA events
+    inside coh_elem_eval (best of 3); max over ranks."""
     import torch
     import torch.distributed as dist
 
     from paper_1910_11110_b200.elem import Program, elem_eval
 
     B, n, K = args.bitmap_buffers, 1 << args.bitmap_log2_cells, args.bitmap_calls
-    progs = [Program.generate(3, rank * B + b, n, 8, K, 64) for b in range(B)]
-    elem_eval(ctx, progs[: max(1, B // 8)], want_planes=False, runs_cap=0)  # warm
-    best = None
-    for _ in range(3):
-        out = elem_eval(ctx, progs, want_planes=False, runs_cap=0)
-        st = out["stats"]
-        if best is None or st.device_ms < best[0]:
-            best = (st.device_ms, st.alg_bytes, st.stages, st.launches)
-    ms, alg, stages, launches = best
-    if world > 1:
-        t = torch.tensor([ms, float(alg)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t[0:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(t[1:2])
-        ms, alg = float(t[0].item()), int(t[1].item())
     peak, src = peaks()
-    gbs = alg / (ms / 1e3) / 1e9
-    res = out["results"]
-    return {"metric": "bitmap GB/s (algorithmic bytes / device time)", "value": gbs, "unit": "GB/s",
-            "frac": gbs / peak, "peak": peak, "peak_source": src, "device_ms": ms, "alg_bytes": alg,
-            "stages": stages, "launches": launches,
-            "config": {"workload": "C3: element-granular bit planes, overlapping views", "buffers_per_gpu": B,
+    per_rho = {}
+    for name, k in RHOS:
+        progs = [Program.generate(3, rank * B + b, n, 8, K, 64, frag_log2=k) for b in range(B)]
+        t0 = time.perf_counter()
+        count = elem_eval(ctx, progs, want_planes=False, runs_cap=0, download_runs=False)  # counts the ranges
+        wall_ms = 1e3 * (time.perf_counter() - t0)
+        res = count["results"]
+        cap = max(1, max(int(res[i].n_runs) for i in range(B)))
+        best = None
+        for _ in range(3):
+            out = elem_eval(ctx, progs, want_planes=False, runs_cap=cap, download_runs=False)
+            st = out["stats"]
+            if best is None or st.device_ms < best[0]:
+                best = (st.device_ms, st.alg_bytes, st.stages, st.launches)
+        ms, alg, stages, launches = best
+        runs = sum(int(res[i].n_runs) for i in range(B))
+        if world > 1:
+            t = torch.tensor([ms, float(alg), float(runs)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t[0:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(t[1:3])
+            ms, alg, runs = float(t[0].item()), int(t[1].item()), int(t[2].item())
+        gbs = alg / (ms / 1e3) / 1e9
+        per_rho[name] = {"value": gbs, "unit": "GB/s", "frac": gbs / peak, "device_ms": ms, "alg_bytes": alg,
+                         "runs_written": runs, "runs_cap_per_buffer": cap, "stages": stages, "launches": launches,
+                         "host_compile_upload_ms": wall_ms - float(count["stats"].device_ms),
+                         "stuck": sum(1 for i in range(B) if res[i].status == 1),
+                         "transfers": sum(res[i].transfers for i in range(B)),
+                         "transfer_cells": sum(int(res[i].transfer_cells) for i in range(B))}
+        del progs, count, out
+    head = per_rho["2^-16"]
+    return {"metric": "bitmap GB/s (algorithmic bytes / device time), element path C3", "value": head["value"],
+            "unit": "GB/s", "frac": head["frac"], "peak": peak, "peak_source": src, "headline_rho": "2^-16",
+            "rho": per_rho,
+            "config": {"workload": "C3: element-granular bit planes, overlapping views, pre-fragmented", "buffers_per_gpu": B,
                        "cells": n, "views": 8, "calls": K, "adv_per1024": 64,
                        "l2": "1 GiB of planes per GPU > L2, no flush"},
-            "outcomes": {"stuck": sum(1 for i in range(B) if res[i].status == 1),
-                         "transfers": sum(res[i].transfers for i in range(B)),
-                         "runs": sum(res[i].n_runs for i in range(B))},
             "cpu_reference": bitmap_cpu_reference(ctx) if rank == 0 and not args.no_cpu_baseline else None}
 
 
@@ -295,13 +313,13 @@ def bitmap_cpu_reference(ctx):
         import oracle_ffi as o
         if not o.have_ref():
             return {"unavailable": "oracle/_ref not built"}
-        p = Program.generate(3, 0, 1 << 20, 8, 8, 64)
-        alg = int(elem_eval(ctx, [p], want_planes=False, runs_cap=0)["stats"].alg_bytes)
+        p = Program.generate(3, 0, 1 << 20, 8, 8, 64, frag_log2=16)
+        alg = int(elem_eval(ctx, [p], want_planes=False, runs_cap=1 << 20, download_runs=False)["stats"].alg_bytes)
         t0 = time.perf_counter()
         rc = o.elem_run("ref", p)[0]
         dt = time.perf_counter() - t0
         return {"value": alg / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference", "seconds": dt,
-                "rc": int(rc), "sample": "one program of 2^20 cells, 8 views, 8 calls (seed 3, program 0)"}
+                "rc": int(rc), "sample": "one program of 2^20 cells, 8 views, 8 calls, rho 2^-16 (seed 3, program 0)"}
     except Exception as ex:  # test infrastructure; its absence is not fatal here
         return {"error": f"{type(ex).__name__}: {ex}"}
 

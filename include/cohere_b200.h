@@ -275,25 +275,27 @@ typedef struct coh_elem_program {
   uint32_t pad;
 } coh_elem_program;
 
-/* Word w of the fragmentation mask: the AND of frag_log2 independent 32-bit draws, so
- * each cell is set with probability 2^-frag_log2 (draw j = half j%2 of
- * splitmix64(frag_seed ^ (w << 6) ^ (j >> 1))). */
-static inline uint64_t coh_splitmix64_h(uint64_t x) {
-  x += 0x9E3779B97F4A7C15ull;
-  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
-  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-  return x ^ (x >> 31);
-}
+/* Word w of the fragmentation mask: the AND of frag_log2 32-bit draws, so each cell is
+ * set with probability 2^-frag_log2.  Draw 0 is a murmur3 finalizer of the seed and the
+ * word index, draw j+1 a xorshift32 step of draw j. */
 static inline uint32_t coh_frag_mask(uint64_t frag_seed, uint32_t frag_log2, uint32_t w) {
   if (frag_log2 == 0) return 0u;
-  uint32_t m = 0xFFFFFFFFu;
-  for (uint32_t j = 0; j < frag_log2; j += 2) {
-    const uint64_t h = coh_splitmix64_h(frag_seed ^ ((uint64_t)w << 6) ^ (uint64_t)(j >> 1));
-    m &= (uint32_t)h;
-    if (j + 1 < frag_log2) m &= (uint32_t)(h >> 32);
+  uint32_t x = ((uint32_t)frag_seed ^ (w * 0x9E3779B9u)) + (uint32_t)(frag_seed >> 32);
+  x ^= x >> 16;
+  x *= 0x85EBCA6Bu;
+  x ^= x >> 13;
+  x *= 0xC2B2AE35u;
+  x ^= x >> 16;
+  uint32_t m = x;
+  for (uint32_t j = 1; j < frag_log2 && m; ++j) {
+    x ^= x << 13;
+    x ^= x >> 17;
+    x ^= x << 5;
+    m &= x;
   }
   return m;
 }
+
 /* Per-program outcome.  stuck key: element b[stuck_index] (key kind concrete) or the
  * abstract key of view stuck_index (key kind abstract).  Transfers are the executed
  * concrete whole-view syncs; their transfer ranges are the maximal runs of changed

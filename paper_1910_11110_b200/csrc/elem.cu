@@ -19,6 +19,7 @@
 #include "elem.hpp"
 #include "gen_common.h"
 #include "internal.hpp"
+#include "runs_emit.cuh"
 
 namespace cohb {
 
@@ -257,11 +258,30 @@ __global__ void __launch_bounds__(kET, 8) k_elem_pass1(const ElemDev d) {
       nz += __popc(z[k]);
     }
   }
+  const uint32_t my_s = ns, my_e = ne;
   ns = block_sum(ns, red);
   ne = block_sum(ne, red);
   nz = block_sum(nz, red);
   if (threadIdx.x == 0)
     *reinterpret_cast<uint4*>(d.tcnt + 4 * tloc) = make_uint4(ns, ne, nz, edge_prev | (s_next << 1));
+  // Sparse tiles stage their run cells (tile-local order = ascending) so that apply can
+  // write the destination without reading it again (block-uniform condition).
+  if (d.stage_runs && (ns | ne) && ns <= kStageRuns && ne <= kStageRuns) {
+    uint32_t os = block_excl_scan(my_s, red);
+    uint32_t oe = block_excl_scan(my_e, red);
+    uint32_t* const stg = d.stage_runs + (size_t)tloc * 2u * kStageRuns;
+    if (zand == 0xFFFFFFFFu) {  // all 256 cells change: only the first / last cell can be edges
+      if (my_s) stg[os] = base * 32u;
+      if (my_e) stg[kStageRuns + oe] = (base + kWPT) * 32u - 1u;
+    } else if (zor != 0u) {
+      run_edges(z, pt, nb, sts, ens);  // recomputed: keeps them dead across the block sums
+#pragma unroll
+      for (int k = 0; k < kWPT; ++k) {
+        for (uint32_t x = sts[k]; x; x &= x - 1) stg[os++] = (base + k) * 32u + (__ffs(x) - 1);
+        for (uint32_t x = ens[k]; x; x &= x - 1) stg[kStageRuns + oe++] = (base + k) * 32u + (__ffs(x) - 1);
+      }
+    }
+  }
 }
 
 // One warp per buffer: walks the buffer's ops of this stage in program order — stuck
@@ -363,8 +383,9 @@ __global__ void __launch_bounds__(32 * kDecideWarps) k_elem_decide(const ElemDev
 // tile lies inside the range, a pure store of ones; edge tiles emit their transfer runs
 // with a warp scan (lane l owns words [64 l, 64 l + 63] of the tile).
 constexpr int kApplyWarps = 8;
+constexpr int kApplyU = 4;  // warp steps of an edge tile loaded together
 constexpr int kWPL = kElemTileWords / 32;  // 64 words per lane
-__global__ void __launch_bounds__(32 * kApplyWarps, 4) k_elem_apply(const ElemDev d, uint32_t n_sync_tiles) {
+__global__ void __launch_bounds__(32 * kApplyWarps, 3) k_elem_apply(const ElemDev d, uint32_t n_sync_tiles) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t gw = blockIdx.x * kApplyWarps + (threadIdx.x >> 5), nw = gridDim.x * kApplyWarps;
   // descriptors are host-built: the first one loads while the predecessor drains
@@ -426,70 +447,96 @@ __global__ void __launch_bounds__(32 * kApplyWarps, 4) k_elem_apply(const ElemDe
       }
       continue;
     }
-    // edge tile: lane l owns words [64 l, 64 l + 63], loaded once into registers
-    const uint32_t base = tstart + lane * kWPL;
-    uint32_t z[kWPL];
-    {
-      const uint4* p4 = reinterpret_cast<const uint4*>(dst + base);
+    if (full && cnt.x <= kStageRuns && cnt.y <= kStageRuns) {
+      // sparse interior tile: pass1 staged its runs; the destination becomes all ones
+      // without being read again
 #pragma unroll
-      for (int q = 0; q < kWPL / 4; ++q) {
-        const uint4 v = __ldcg(p4 + q);
-        z[4 * q] = ~v.x;
-        z[4 * q + 1] = ~v.y;
-        z[4 * q + 2] = ~v.z;
-        z[4 * q + 3] = ~v.w;
-      }
+      for (int j = 0; j < kElemTileWords / 128; ++j)
+        __stcg(dst4 + lane + 32 * j, make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu));
+      const uint32_t* stg = d.stage_runs + (size_t)tloc * 2u * kStageRuns;
+      const uint64_t gs = d.tbase[2 * tloc], ge = d.tbase[2 * tloc + 1];
+      const size_t arena = (size_t)b * d.runs_cap;
+      for (uint32_t k = lane; k < cnt.x; k += 32)
+        if (gs + k < d.runs_cap) d.runs_lo[arena + gs + k] = __ldcg(stg + k);
+      for (uint32_t k = lane; k < cnt.y; k += 32)
+        if (ge + k < d.runs_cap) d.runs_hi[arena + ge + k] = __ldcg(stg + kStageRuns + k);
+      continue;
     }
-    const bool lane_full = tile_full(tstart, tile.lo, tile.hi);
+    // edge tile: 16 warp steps of 32 quads (lane l on quad l: 512 contiguous bytes), kApplyU
+    // steps loaded together.  Run starts / ends come from each quad and its neighbour words
+    // (adjacent lanes by shuffle; across steps the carried last word; outside the tile the
+    // edge bits pass1 read before anything was written), are placed by a warp scan
+    // (sparse: each lane writes its few; dense: coalesced cooperative stores), and the
+    // destination quad is written back with the range bits set.
+    uint64_t gs = d.tbase[2 * tloc], ge = d.tbase[2 * tloc + 1];
+    uint32_t* const out_s = d.runs_lo + (size_t)b * d.runs_cap;
+    uint32_t* const out_e = d.runs_hi + (size_t)b * d.runs_cap;
+    uint32_t carry = (cnt.w & 1u) << 31;  // z of the cell before the tile, as a word's top bit
+    for (uint32_t s0 = 0; s0 < kElemTileWords / 128; s0 += kApplyU) {
+      uint4 v[kApplyU];
 #pragma unroll
-    for (int k = 0; k < kWPL; ++k) z[k] &= lane_full ? 0xFFFFFFFFu : word_mask(base + k, tile.lo, tile.hi);
-    const uint32_t prev_last = __shfl_up_sync(0xffffffffu, z[kWPL - 1], 1);  // all lanes shuffle
-    const uint32_t next_first = __shfl_down_sync(0xffffffffu, z[0], 1);
-    const uint32_t prev_top = lane ? (prev_last >> 31) : (cnt.w & 1u);
-    const uint32_t next_bot = lane < 31 ? (next_first & 1u) : (cnt.w >> 1);
-    uint32_t ns = 0, ne = 0;
+      for (int u = 0; u < kApplyU; ++u) v[u] = __ldcg(dst4 + 32 * (s0 + u) + lane);
+      // lane 31's successor word for the batch's last step: the next batch's first word, or
+      // the cell after the tile (pass1's edge bit)
+      const uint32_t wn = tstart + 128u * (s0 + kApplyU);
+      const uint32_t z_after = s0 + kApplyU < kElemTileWords / 128
+                                   ? ~__ldcg(dst + wn) & (full ? 0xFFFFFFFFu : word_mask(wn, tile.lo, tile.hi))
+                                   : (cnt.w >> 1) & 1u;
 #pragma unroll
-    for (int k = 0; k < kWPL; ++k) {
-      const uint32_t pz = k ? (z[k - 1] >> 31) : prev_top;
-      const uint32_t zn = k < kWPL - 1 ? (z[k + 1] & 1u) : next_bot;
-      ns += __popc(z[k] & ~((z[k] << 1) | pz));
-      ne += __popc(z[k] & ~((z[k] >> 1) | (zn << 31)));
-    }
-    uint32_t xs = ns, xe = ne;
+      for (int u = 0; u < kApplyU; ++u) {
+        const uint32_t w0 = tstart + 4u * (32u * (s0 + u) + lane);
+        uint32_t m[4], z[4];
+        const uint32_t vv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t ys = __shfl_up_sync(0xffffffffu, xs, o), ye = __shfl_up_sync(0xffffffffu, xe, o);
-      if (lane >= (uint32_t)o) {
-        xs += ys;
-        xe += ye;
-      }
-    }
-    unsigned long long os = d.tbase[2 * tloc] + (xs - ns), oe = d.tbase[2 * tloc + 1] + (xe - ne);
-    const size_t arena = (size_t)b * d.runs_cap;
+        for (int k = 0; k < 4; ++k) {
+          m[k] = full ? 0xFFFFFFFFu : word_mask(w0 + k, tile.lo, tile.hi);
+          z[k] = ~vv[k] & m[k];
+        }
+        uint32_t zp = __shfl_up_sync(0xffffffffu, z[3], 1);
+        uint32_t zn = __shfl_down_sync(0xffffffffu, z[0], 1);
+        // lane 0's first word of the next step (all lanes shuffle; lane 31 uses it)
+        const uint32_t nx = __shfl_sync(0xffffffffu, v[u + 1 < kApplyU ? u + 1 : u].x, 0);
+        if (lane == 0) zp = carry;
+        if (lane == 31)
+          zn = u + 1 < kApplyU ? ~nx & (full ? 0xFFFFFFFFu : word_mask(w0 + 4u, tile.lo, tile.hi)) : z_after;
+        uint32_t st[4], en[4], ns = 0, ne = 0;
 #pragma unroll
-    for (int k = 0; k < kWPL; ++k) {
-      const uint32_t pz = k ? (z[k - 1] >> 31) : prev_top;
-      const uint32_t zn = k < kWPL - 1 ? (z[k + 1] & 1u) : next_bot;
-      const uint32_t st = z[k] & ~((z[k] << 1) | pz), en = z[k] & ~((z[k] >> 1) | (zn << 31));
-      for (uint32_t x = st; x; x &= x - 1, ++os)
-        if (os < d.runs_cap) d.runs_lo[arena + os] = (base + k) * 32u + (__ffs(x) - 1);
-      for (uint32_t x = en; x; x &= x - 1, ++oe)
-        if (oe < d.runs_cap) d.runs_hi[arena + oe] = (base + k) * 32u + (__ffs(x) - 1);
-    }
-    // dst |= mask: the zero bits inside the range become ones
-    {
-      uint4* p4 = reinterpret_cast<uint4*>(dst + base);
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t prev = k ? z[k - 1] : zp, next = k < 3 ? z[k + 1] : zn;
+          st[k] = z[k] & ~((z[k] << 1) | (prev >> 31));
+          en[k] = z[k] & ~((z[k] >> 1) | (next << 31));
+          ns += __popc(st[k]);
+          ne += __popc(en[k]);
+        }
+        if (__any_sync(0xffffffffu, ns | ne)) {
+          uint32_t ps = ns, pe = ne;  // inclusive warp scans
 #pragma unroll
-      for (int q = 0; q < kWPL / 4; ++q) {
-        // reconstruct: new = old | mask = ~(z_old & ~mask) ... old = ~(z_unmasked); simpler:
-        // old bits outside the range are unchanged, bits inside become 1
-        const uint32_t w0 = base + 4 * q;
-        uint4 v = __ldcg(p4 + q);
-        v.x |= lane_full ? 0xFFFFFFFFu : word_mask(w0, tile.lo, tile.hi);
-        v.y |= lane_full ? 0xFFFFFFFFu : word_mask(w0 + 1, tile.lo, tile.hi);
-        v.z |= lane_full ? 0xFFFFFFFFu : word_mask(w0 + 2, tile.lo, tile.hi);
-        v.w |= lane_full ? 0xFFFFFFFFu : word_mask(w0 + 3, tile.lo, tile.hi);
-        __stcg(p4 + q, v);
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, ps, o), y = __shfl_up_sync(0xffffffffu, pe, o);
+            if (lane >= (uint32_t)o) {
+              ps += x;
+              pe += y;
+            }
+          }
+          const uint32_t Ts = __shfl_sync(0xffffffffu, ps, 31), Te = __shfl_sync(0xffffffffu, pe, 31);
+          if (Ts + Te > kDenseStep) {
+            emit_dense(st[0], st[1], st[2], st[3], ps - ns, Ts, (uint64_t)w0 * 32u, gs, out_s, d.runs_cap);
+            emit_dense(en[0], en[1], en[2], en[3], pe - ne, Te, (uint64_t)w0 * 32u, ge, out_e, d.runs_cap);
+          } else if (ns | ne) {
+            uint64_t os = gs + ps - ns, oe = ge + pe - ne;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              for (uint32_t x = st[k]; x; x &= x - 1, ++os)
+                if (os < d.runs_cap) out_s[os] = (w0 + k) * 32u + (__ffs(x) - 1);
+              for (uint32_t x = en[k]; x; x &= x - 1, ++oe)
+                if (oe < d.runs_cap) out_e[oe] = (w0 + k) * 32u + (__ffs(x) - 1);
+            }
+          }
+          gs += Ts;
+          ge += Te;
+        }
+        carry = __shfl_sync(0xffffffffu, z[3], 31);
+        __stcg(dst4 + 32 * (s0 + u) + lane, make_uint4(vv[0] | m[0], vv[1] | m[1], vv[2] | m[2], vv[3] | m[3]));
       }
     }
   }
@@ -532,33 +579,32 @@ int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, uint32_t n_sync_tiles,
 // except the pre-fragmented cells (coh_frag_mask), which start coherent: (V,V), R = 1.  pinit[b] =
 // {n_cells, frag_log2, frag_seed lo, frag_seed hi}.  128-bit stores, one 4-word group
 // per thread iteration.
-__global__ void k_elem_init(uint32_t* planes, uint32_t W, const uint4* __restrict__ pinit, uint32_t n_progs) {
-  const uint64_t total4 = (uint64_t)n_progs * 2u * W / 4u;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total4;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t w0 = i * 4u;
-    const uint32_t b = (uint32_t)(w0 / (2u * W));
-    const uint32_t r = (uint32_t)(w0 - (uint64_t)b * 2u * W);
-    const uint32_t rw = r < W ? r : r - W;  // word index within the plane
-    const uint4 pi = pinit[b];
-    const uint32_t n = pi.x;
-    const uint64_t seed = (uint64_t)pi.z | ((uint64_t)pi.w << 32);
-    uint32_t q[4];
+__global__ void __launch_bounds__(256) k_elem_init(uint32_t* planes, uint32_t W, const uint4* __restrict__ pinit) {
+  const uint32_t b = blockIdx.y;  // one buffer per grid row: no index division
+  const uint4 pi = pinit[b];
+  const uint32_t n = pi.x;
+  const uint64_t seed = (uint64_t)pi.z | ((uint64_t)pi.w << 32);
+  uint4* const L4 = reinterpret_cast<uint4*>(planes + (size_t)b * 2u * W);
+  uint4* const R4 = L4 + W / 4u;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < W / 4u; q += gridDim.x * blockDim.x) {
+    uint32_t l[4], r[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint32_t w = rw + k;
-      const uint32_t live = (w + 1) * 32u <= n ? 0xFFFFFFFFu : (w * 32u < n ? (0xFFFFFFFFu >> (32u - (n - w * 32u))) : 0u);
-      const uint32_t frag = (r >= W && live) ? coh_frag_word(seed, pi.y, w) & live : 0u;
-      q[k] = r < W ? live : frag;
+      const uint32_t w = 4u * q + k;
+      l[k] = (w + 1) * 32u <= n ? 0xFFFFFFFFu : (w * 32u < n ? (0xFFFFFFFFu >> (32u - (n - w * 32u))) : 0u);
+      r[k] = l[k] ? coh_frag_word(seed, pi.y, w) & l[k] : 0u;
     }
-    __stcg(reinterpret_cast<uint4*>(planes) + i, make_uint4(q[0], q[1], q[2], q[3]));
+    __stcg(L4 + q, make_uint4(l[0], l[1], l[2], l[3]));
+    __stcg(R4 + q, make_uint4(r[0], r[1], r[2], r[3]));
   }
 }
 
 int launch_elem_init(uint32_t* planes, uint32_t W, const uint32_t* pinit, uint32_t n_progs, void* stream,
                      std::string* err) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  k_elem_init<<<148 * 8, 256, 0, s>>>(planes, W, reinterpret_cast<const uint4*>(pinit), n_progs);
+  // ~8 quads per thread: enough blocks to fill the GPU for any buffer count
+  const uint32_t per_row = (W / 4u + 256u * 8u - 1u) / (256u * 8u);
+  k_elem_init<<<dim3(per_row, n_progs), 256, 0, s>>>(planes, W, reinterpret_cast<const uint4*>(pinit));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("element init launch: ") + cudaGetErrorString(e);

@@ -43,6 +43,7 @@ struct ElemTile {
 static_assert(sizeof(ElemTile) == 32, "ElemTile is 32 bytes");
 
 constexpr uint32_t kElemTileWords = 2048;      // 64 Ki cells per plane per CTA
+constexpr uint32_t kStageRuns = 256;           // run starts (and ends) a sync tile stages in pass1
 constexpr uint32_t kNoCell = 0xFFFFFFFFu;
 
 // Device-side per-buffer state.
@@ -107,6 +108,7 @@ struct ElemDev {
   ElemScratch* sc;
   uint32_t* tcnt;              // per tile of this stage: starts, ends, zeros, edge bits
   unsigned long long* tbase;   // per tile: run-start offset, run-end offset
+  uint32_t* stage_runs;        // per tile: up to kStageRuns starts, then kStageRuns ends (cells)
   const uint32_t* view_lo;     // [b][16]
   const uint32_t* view_hi;
   uint32_t* boundary;          // [b][bwords]

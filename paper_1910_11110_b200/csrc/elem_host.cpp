@@ -353,7 +353,7 @@ struct ElemGroup {
   ElemPlan plan;
   uint32_t W = 0, bwords = 1;
   uint64_t runs_cap = 0, launches = 0;
-  DevBuf planes, ops, tiles, stiles, st, sc, tcnt, tbase, vlo, vhi, ncell, bnd, rlo, rhi;
+  DevBuf planes, ops, tiles, stiles, st, sc, tcnt, tbase, stage_buf, vlo, vhi, ncell, bnd, rlo, rhi;
 
   int compile(std::string* err) {
     int rc = elem_compile(progs, n, &plan, err);
@@ -376,6 +376,7 @@ struct ElemGroup {
     COH_E(alloc(sc, (size_t)n * kSlots * sizeof(ElemScratch)));
     COH_E(alloc(tcnt, (size_t)max_tiles * 4 * 4));
     COH_E(alloc(tbase, (size_t)max_tiles * 2 * 8));
+    if (runs_cap) COH_E(alloc(stage_buf, (size_t)max_tiles * 2 * kStageRuns * 4));
     COH_E(alloc(vlo, (size_t)n * COH_MAX_VIEWS * 4));
     COH_E(alloc(vhi, (size_t)n * COH_MAX_VIEWS * 4));
     COH_E(alloc(ncell, (size_t)n * 16));
@@ -430,6 +431,7 @@ struct ElemGroup {
       d.sc = sc.as<ElemScratch>();
       d.tcnt = tcnt.as<uint32_t>();
       d.tbase = tbase.as<unsigned long long>();
+      d.stage_runs = stage_buf.as<uint32_t>();
       d.view_lo = vlo.as<uint32_t>();
       d.view_hi = vhi.as<uint32_t>();
       d.boundary = bnd.as<uint32_t>();
@@ -601,7 +603,7 @@ static int elem_eval_impl(coh_ctx* ctx, const coh_elem_program* progs, uint32_t 
       r.transfers = S.transfers;
       r.transfer_cells = S.transfer_cells;
       r.n_runs = S.n_runs;
-      alg += 8 * S.n_runs;
+      alg += 8 * std::min<uint64_t>(S.n_runs, runs_cap);  // ranges actually written (8 B each)
       uint32_t abs_final = T.abs_final;
       uint32_t executed_ops = T.n_ops;
       if (S.dead) {

@@ -27,13 +27,22 @@ COH_HD uint16_t coh_gen_record(uint64_t seed, uint64_t trace_id, uint32_t call_i
   return (uint16_t)((arr << 8) | (kind << 2) | (site << 4) | (var << 5));
 }
 
-// Fragmentation mask of plane word w (include/cohere_b200.h coh_frag_mask, same draws).
+// Fragmentation mask of plane word w (include/cohere_b200.h coh_frag_mask, same draws;
+// once the mask is empty further draws change nothing).
 COH_HD uint32_t coh_frag_word(uint64_t frag_seed, uint32_t frag_log2, uint32_t w) {
-  uint32_t m = frag_log2 ? 0xFFFFFFFFu : 0u;
-  for (uint32_t j = 0; j < frag_log2; j += 2) {
-    const uint64_t h = coh_splitmix64(frag_seed ^ ((uint64_t)w << 6) ^ (uint64_t)(j >> 1));
-    m &= (uint32_t)h;
-    if (j + 1 < frag_log2) m &= (uint32_t)(h >> 32);
+  if (frag_log2 == 0) return 0u;
+  uint32_t x = ((uint32_t)frag_seed ^ (w * 0x9E3779B9u)) + (uint32_t)(frag_seed >> 32);
+  x ^= x >> 16;
+  x *= 0x85EBCA6Bu;
+  x ^= x >> 13;
+  x *= 0xC2B2AE35u;
+  x ^= x >> 16;
+  uint32_t m = x;
+  for (uint32_t j = 1; j < frag_log2 && m; ++j) {
+    x ^= x << 13;
+    x ^= x >> 17;
+    x ^= x << 5;
+    m &= x;
   }
   return m;
 }

@@ -116,8 +116,10 @@ def _register(L):
 _register(lib())
 
 
-def elem_eval(ctx, programs, want_planes=True, runs_cap=4096):
-    """Evaluate element programs on the device.  Returns dict of numpy outputs."""
+def elem_eval(ctx, programs, want_planes=True, runs_cap=4096, download_runs=True):
+    """Evaluate element programs on the device.  Returns dict of numpy outputs.  runs_cap
+    transfer ranges per program are written on the device; download_runs=False leaves
+    them there (the C3 measurement: every range written, none copied to the host)."""
     n = len(programs)
     arr = program_array(programs)
     res = (ElemResult * n)()
@@ -126,10 +128,11 @@ def elem_eval(ctx, programs, want_planes=True, runs_cap=4096):
     planes = np.zeros((n, 2, pw), np.uint32) if want_planes else None
     vabs = np.zeros((n, MAX_VIEWS), np.uint8)
     bnd = np.zeros((n, bw), np.uint32)
-    runs = np.zeros((n, max(1, runs_cap), 2), np.uint32)
+    runs = np.zeros((n, max(1, runs_cap), 2), np.uint32) if download_runs else None
     stats = ElemStats()
     rc = lib().coh_elem_eval(ctx._h, C.addressof(arr), n, C.addressof(res),
                              planes.ctypes.data if want_planes else None, pw, vabs.ctypes.data, bnd.ctypes.data, bw,
-                             runs.ctypes.data if runs_cap else None, runs_cap, C.addressof(stats))
+                             runs.ctypes.data if (runs_cap and download_runs) else None, runs_cap,
+                             C.addressof(stats))
     ctx._check(rc, "coh_elem_eval")
     return {"results": res, "planes": planes, "view_abs": vabs, "boundary": bnd, "runs": runs, "stats": stats}

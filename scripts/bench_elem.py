@@ -20,21 +20,25 @@ ap.add_argument("--views", type=int, default=8)
 ap.add_argument("--calls", type=int, default=8)
 ap.add_argument("--adv", type=int, default=64)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--frag-log2", type=int, default=0, help="pre-fragmentation rho = 2^-k (0 = none)")
 a = ap.parse_args()
 ctx = coh.Context(0)
 t0 = time.time()
-progs = [Program.generate(3, b, 1 << a.log2_cells, a.views, a.calls, a.adv) for b in range(a.buffers)]
+progs = [Program.generate(3, b, 1 << a.log2_cells, a.views, a.calls, a.adv, frag_log2=a.frag_log2)
+         for b in range(a.buffers)]
 gen_s = time.time() - t0
+cnt = elem_eval(ctx, progs, want_planes=False, runs_cap=0, download_runs=False)["results"]
+cap = max(1, max(int(cnt[i].n_runs) for i in range(a.buffers)))  # every transfer range written
 best = None
 for r in range(a.reps):
-    out = elem_eval(ctx, progs, want_planes=False, runs_cap=0)
+    out = elem_eval(ctx, progs, want_planes=False, runs_cap=cap, download_runs=False)
     st = out["stats"]
     gbs = st.alg_bytes / (st.device_ms / 1e3) / 1e9
     if best is None or gbs > best["gbs"]:
         best = {"gbs": gbs, "device_ms": st.device_ms, "alg_bytes": st.alg_bytes, "stages": st.stages,
                 "launches": st.launches, "tiles": st.tiles}
 res = out["results"]
-summary = {"buffers": a.buffers, "cells": 1 << a.log2_cells, "views": a.views, "calls": a.calls, "adv": a.adv,
+summary = {"frag_log2": a.frag_log2, "runs_cap": cap, "buffers": a.buffers, "cells": 1 << a.log2_cells, "views": a.views, "calls": a.calls, "adv": a.adv,
            "gen_s": gen_s, **best, "frac_of_6497": best["gbs"] / 6497.1,
            "status": [sum(1 for i in range(a.buffers) if res[i].status == s) for s in range(4)],
            "transfers": sum(res[i].transfers for i in range(a.buffers)),
