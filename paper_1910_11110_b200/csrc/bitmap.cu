@@ -513,7 +513,8 @@ constexpr uint32_t kRunCap = 4096;
 template <bool STAGE>
 __device__ __forceinline__ void place_step(const Flat& F, uint64_t f, uint32_t r, uint64_t qa, bool at_start,
                                            const uint32_t* st, const uint32_t* en, uint64_t& gs, uint64_t& ge,
-                                           uint32_t* out_s, uint32_t* out_e, uint64_t cap, uint32_t* off_local) {
+                                           uint32_t* out_s, uint32_t* out_e, uint64_t cap, uint32_t* off_local,
+                                           uint32_t* wbuf) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t ns = __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
   const uint32_t ne = __popc(en[0]) + __popc(en[1]) + __popc(en[2]) + __popc(en[3]);
@@ -531,10 +532,10 @@ __device__ __forceinline__ void place_step(const Flat& F, uint64_t f, uint32_t r
   if (STAGE && at_start)  // the first flat quad of range r (and of the empty ranges just before it)
     for (int64_t q = r; q >= 0 && F.qp[q] == f; --q) off_local[q] = (uint32_t)s;
   const uint32_t Ts = __shfl_sync(0xFFFFFFFFu, ps, 31), Te = __shfl_sync(0xFFFFFFFFu, pe, 31);
-  if (Ts + Te > kDenseStep) {  // coalesced cooperative writes
-    const uint64_t cb = (qa * 4 - F.r[r].word_off) * 32;
-    emit_dense(st[0], st[1], st[2], st[3], ps - ns, Ts, cb, gs, out_s, cap);
-    emit_dense(en[0], en[1], en[2], en[3], pe - ne, Te, cb, ge, out_e, cap);
+  if (Ts + Te > kDenseStep) {  // staged in shared memory, written with coalesced stores
+    const uint32_t cb = (uint32_t)((qa * 4 - F.r[r].word_off) * 32);
+    emit_staged(st, ps - ns, Ts, cb, gs, out_s, cap, wbuf);
+    emit_staged(en, pe - ne, Te, cb, ge, out_e, cap, wbuf);
   } else if (ns | ne) {  // sparse step: each lane writes its few runs
     const uint64_t wbase = qa * 4 - F.r[r].word_off;
 #pragma unroll
@@ -564,9 +565,11 @@ struct RunCounts {
   uint64_t *chunk_s, *chunk_e, *block_s, *block_e;
 };
 
-__global__ void __launch_bounds__(kBT, 4) k_runs_collect(const uint32_t* words, Flat Fg, RunCounts C, uint32_t* stage,
+__global__ void __launch_bounds__(kBT, 3) k_runs_collect(const uint32_t* words, Flat Fg, RunCounts C, uint32_t* stage,
                                                          uint32_t* off_local) {
   COH_BM_PROLOGUE
+  extern __shared__ uint32_t runs_smem[];  // kBT / 32 warps x kStageBuf: dense run staging
+  uint32_t* const wbuf = runs_smem + (threadIdx.x >> 5) * kStageBuf;
   __shared__ uint64_t ws[2][kBT / 32];
   uint64_t f0, f1, wid;
   warp_chunk(F.qp[F.n], f0, f1, wid);
@@ -575,7 +578,7 @@ __global__ void __launch_bounds__(kBT, 4) k_runs_collect(const uint32_t* words, 
     uint32_t* const ss = stage + wid * (2 * kRunCap);
     chunk_runs(words, F, f0, f1,
                [&](bool, uint64_t f, uint32_t r, uint64_t qa, bool at_start, const uint32_t* st, const uint32_t* en) {
-                 place_step<true>(F, f, r, qa, at_start, st, en, ls, le, ss, ss + kRunCap, kRunCap, off_local);
+                 place_step<true>(F, f, r, qa, at_start, st, en, ls, le, ss, ss + kRunCap, kRunCap, off_local, wbuf);
                });
   }
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -661,11 +664,13 @@ __device__ __forceinline__ void chunk_offsets(const RunCounts& C, const uint64_t
 // Place pass, plus run_off[i] = global index of range i's first run: its chunk's offset +
 // the chunk-local count staged by the collect pass; ranges starting at the end get the
 // total.
-__global__ void __launch_bounds__(kBT, 4) k_runs_place(const uint32_t* words, Flat Fg, RunCounts C,
+__global__ void __launch_bounds__(kBT, 3) k_runs_place(const uint32_t* words, Flat Fg, RunCounts C,
                                                        const uint32_t* stage, const uint32_t* off_local,
                                                        uint32_t* run_start, uint32_t* run_end, uint64_t cap,
                                                        uint64_t* run_off) {
   COH_BM_PROLOGUE
+  extern __shared__ uint32_t runs_smem[];  // kBT / 32 warps x kStageBuf: dense run staging
+  uint32_t* const wbuf = runs_smem + (threadIdx.x >> 5) * kStageBuf;
   __shared__ uint64_t bs[kMaxCollectBlocks + 1], be[kMaxCollectBlocks + 1];
   block_scan2(C.block_s, C.block_e, gridDim.x, bs, be);
   const uint64_t Q = F.qp[F.n], n_chunks = (uint64_t)gridDim.x * (kBT / 32);
@@ -695,7 +700,7 @@ __global__ void __launch_bounds__(kBT, 4) k_runs_place(const uint32_t* words, Fl
   }
   chunk_runs(words, F, f0, f1,
              [&](bool, uint64_t f, uint32_t r, uint64_t qa, bool at_start, const uint32_t* st, const uint32_t* en) {
-               place_step<false>(F, f, r, qa, at_start, st, en, gs, ge, run_start, run_end, cap, nullptr);
+               place_step<false>(F, f, r, qa, at_start, st, en, gs, ge, run_start, run_end, cap, nullptr, wbuf);
              });
 }
 
@@ -817,8 +822,13 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   C.block_e = C.block_s + grid;
   uint32_t* stage = reinterpret_cast<uint32_t*>(static_cast<char*>(co.p) + counts_b);
   uint32_t* off_local = stage + 2 * kRunCap * n_chunks;
-  k_runs_collect<<<grid, kBT, 0, s>>>(d_words, F, C, stage, off_local);
-  k_runs_place<<<grid, kBT, 0, s>>>(d_words, F, C, stage, off_local, d_run_start, d_run_end, cap, d_run_off);
+  constexpr size_t kRunsSmem = (size_t)(kBT / 32) * kStageBuf * 4u;
+  const bool smem_ok =  // per call: the attribute belongs to the current device
+      cudaFuncSetAttribute(k_runs_collect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRunsSmem) == cudaSuccess &&
+      cudaFuncSetAttribute(k_runs_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRunsSmem) == cudaSuccess;
+  if (!smem_ok) return fail(ctx, "zero runs: shared memory attribute", cudaErrorInvalidValue);
+  k_runs_collect<<<grid, kBT, kRunsSmem, s>>>(d_words, F, C, stage, off_local);
+  k_runs_place<<<grid, kBT, kRunsSmem, s>>>(d_words, F, C, stage, off_local, d_run_start, d_run_end, cap, d_run_off);
   ctx->launches += 2;
   return check(ctx, "zero_runs");
 }

@@ -386,7 +386,9 @@ constexpr int kApplyWarps = 8;
 constexpr int kApplyU = 4;  // warp steps of an edge tile loaded together
 constexpr int kWPL = kElemTileWords / 32;  // 64 words per lane
 __global__ void __launch_bounds__(32 * kApplyWarps, 3) k_elem_apply(const ElemDev d, uint32_t n_sync_tiles) {
+  extern __shared__ uint32_t apply_smem[];  // kApplyWarps x kStageBuf: dense run staging
   const uint32_t lane = threadIdx.x & 31;
+  uint32_t* const wbuf = apply_smem + (threadIdx.x >> 5) * kStageBuf;
   const uint32_t gw = blockIdx.x * kApplyWarps + (threadIdx.x >> 5), nw = gridDim.x * kApplyWarps;
   // descriptors are host-built: the first one loads while the predecessor drains
   ElemTile next = gw < n_sync_tiles ? d.sync_desc[gw] : ElemTile{};
@@ -520,8 +522,8 @@ __global__ void __launch_bounds__(32 * kApplyWarps, 3) k_elem_apply(const ElemDe
           }
           const uint32_t Ts = __shfl_sync(0xffffffffu, ps, 31), Te = __shfl_sync(0xffffffffu, pe, 31);
           if (Ts + Te > kDenseStep) {
-            emit_dense(st[0], st[1], st[2], st[3], ps - ns, Ts, (uint64_t)w0 * 32u, gs, out_s, d.runs_cap);
-            emit_dense(en[0], en[1], en[2], en[3], pe - ne, Te, (uint64_t)w0 * 32u, ge, out_e, d.runs_cap);
+            emit_staged(st, ps - ns, Ts, w0 * 32u, gs, out_s, d.runs_cap, wbuf);
+            emit_staged(en, pe - ne, Te, w0 * 32u, ge, out_e, d.runs_cap, wbuf);
           } else if (ns | ne) {
             uint64_t os = gs + ps - ns, oe = ge + pe - ne;
 #pragma unroll
@@ -543,11 +545,12 @@ __global__ void __launch_bounds__(32 * kApplyWarps, 3) k_elem_apply(const ElemDe
 }
 
 template <typename... KArgs, typename... Args>
-static cudaError_t launch_pdl(void (*kernel)(KArgs...), uint32_t grid, uint32_t block, cudaStream_t s, Args... args) {
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), uint32_t grid, uint32_t block, size_t smem, cudaStream_t s,
+                              Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -560,12 +563,17 @@ static cudaError_t launch_pdl(void (*kernel)(KArgs...), uint32_t grid, uint32_t 
 int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, uint32_t n_sync_tiles, void* stream, std::string* err) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
-  if (n_tiles && e == cudaSuccess) e = launch_pdl(k_elem_pass1, n_tiles, kET, s, d);
+  constexpr size_t kApplySmem = (size_t)kApplyWarps * kStageBuf * 4u;
+  const cudaError_t attr =  // per call: the attribute belongs to the current device
+      cudaFuncSetAttribute(k_elem_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem);
+  if (attr != cudaSuccess) e = attr;
+  if (n_tiles && e == cudaSuccess) e = launch_pdl(k_elem_pass1, n_tiles, kET, 0, s, d);
   if (n_tiles && e == cudaSuccess)  // a stage with only WRITE ops has nothing to decide (writes cannot get stuck)
-    e = launch_pdl(k_elem_decide, (d.n_progs + kDecideWarps - 1) / kDecideWarps, 32 * kDecideWarps, s, d);
+    e = launch_pdl(k_elem_decide, (d.n_progs + kDecideWarps - 1) / kDecideWarps, 32 * kDecideWarps, 0, s, d);
   if (n_sync_tiles && e == cudaSuccess) {
     const uint32_t blocks = (n_sync_tiles + kApplyWarps - 1) / kApplyWarps;
-    e = launch_pdl(k_elem_apply, blocks < 148u * 16u ? blocks : 148u * 16u, 32 * kApplyWarps, s, d, n_sync_tiles);
+    e = launch_pdl(k_elem_apply, blocks < 148u * 16u ? blocks : 148u * 16u, 32 * kApplyWarps, kApplySmem, s, d,
+                   n_sync_tiles);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -587,12 +595,33 @@ __global__ void __launch_bounds__(256) k_elem_init(uint32_t* planes, uint32_t W,
   uint4* const L4 = reinterpret_cast<uint4*>(planes + (size_t)b * 2u * W);
   uint4* const R4 = L4 + W / 4u;
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < W / 4u; q += gridDim.x * blockDim.x) {
-    uint32_t l[4], r[4];
+    uint32_t l[4], r[4] = {0u, 0u, 0u, 0u}, x[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint32_t w = 4u * q + k;
       l[k] = (w + 1) * 32u <= n ? 0xFFFFFFFFu : (w * 32u < n ? (0xFFFFFFFFu >> (32u - (n - w * 32u))) : 0u);
-      r[k] = l[k] ? coh_frag_word(seed, pi.y, w) & l[k] : 0u;
+    }
+    if (pi.y) {  // coh_frag_mask of the four words, their draw chains stepped together
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t v = ((uint32_t)seed ^ ((4u * q + k) * 0x9E3779B9u)) + (uint32_t)(seed >> 32);
+        v ^= v >> 16;
+        v *= 0x85EBCA6Bu;
+        v ^= v >> 13;
+        v *= 0xC2B2AE35u;
+        v ^= v >> 16;
+        x[k] = v;
+        r[k] = v & l[k];
+      }
+      for (uint32_t j = 1; j < pi.y && (r[0] | r[1] | r[2] | r[3]); ++j) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // an emptied mask stays empty: stepping it is harmless
+          x[k] ^= x[k] << 13;
+          x[k] ^= x[k] >> 17;
+          x[k] ^= x[k] << 5;
+          r[k] &= x[k];
+        }
+      }
     }
     __stcg(L4 + q, make_uint4(l[0], l[1], l[2], l[3]));
     __stcg(R4 + q, make_uint4(r[0], r[1], r[2], r[3]));

@@ -51,3 +51,29 @@ __device__ __forceinline__ void emit_dense(uint32_t m0, uint32_t m1, uint32_t m2
 
 
 }  // namespace cohb
+
+namespace cohb {
+
+// Dense warp steps, staged: a step (32 lanes x 4 words = 4096 cells) has at most 2048
+// run starts (or ends).  Every lane writes its own set bits' cells, in ascending order,
+// into the warp's shared-memory buffer at S_lane + rank (independent per lane: no
+// shuffles on the critical path), then the warp copies the step's T cells to out[base ..)
+// with coalesced 128-byte stores.  Buffer index o is stored at o ^ ((o >> 5) & 31): lanes
+// whose offsets are ~32 apart (the dense case) then hit different banks.
+constexpr uint32_t kStageBuf = 2048;  // u32 entries per warp
+__device__ __forceinline__ uint32_t stage_swz(uint32_t o) { return o ^ ((o >> 5) & 31u); }
+
+__device__ __forceinline__ void emit_staged(const uint32_t* m, uint32_t S, uint32_t T, uint32_t cb, uint64_t base,
+                                            uint32_t* out, uint64_t cap, uint32_t* buf) {
+  uint32_t o = S;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    for (uint32_t x = m[k]; x; x &= x - 1) buf[stage_swz(o++)] = cb + 32u * k + (uint32_t)(__ffs(x) - 1);
+  __syncwarp();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t lim = base >= cap ? 0 : (T < cap - base ? T : cap - base);
+  for (uint32_t p = lane; p < lim; p += 32) out[base + p] = buf[stage_swz(p)];
+  __syncwarp();  // the buffer is free again
+}
+
+}  // namespace cohb
