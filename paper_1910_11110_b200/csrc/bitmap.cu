@@ -33,6 +33,7 @@ namespace {
 
 constexpr uint32_t kBT = 256;   // threads per block
 constexpr int kU = 4;           // warp steps in flight
+constexpr int kRU = 8;          // warp steps in flight in the zero-run walker (chunk_runs)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 struct Flat {
@@ -428,17 +429,17 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
   uint64_t qa0 = qa_base(R0) - qbeg, qtf = qa_first(R0), qtl = qa_last(R0);
   uint32_t carry = 0;
   bool carry_ok = false;
-  for (uint64_t base = f0; base < f1; base += 32ull * kU) {
-    // Fast iteration (warp-uniform): all 32 x kU quads are interior quads of one range
+  for (uint64_t base = f0; base < f1; base += 32ull * kRU) {
+    // Fast iteration (warp-uniform): all 32 x kRU quads are interior quads of one range
     // (then every lane is in the same range, see the monotone advance below), so no
     // per-quad range tracking, masks or edge loads.
     if (interior_iteration(base, f1, qend, qa0, qtf, qtl)) {
       const uint64_t qb = qa0 + base + lane;
-      uint4 v[kU];
+      uint4 v[kRU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) v[u] = __ldcg(reinterpret_cast<const uint4*>(words) + qb + 32ull * u);
+      for (int u = 0; u < kRU; ++u) v[u] = __ldcg(reinterpret_cast<const uint4*>(words) + qb + 32ull * u);
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
+      for (int u = 0; u < kRU; ++u) {
         const uint32_t a4 = v[u].x & v[u].y & v[u].z & v[u].w;
         if (__all_sync(0xFFFFFFFFu, a4 == 0xFFFFFFFFu)) continue;
         // the words just before and after the step (warp-uniform; the iteration lies
@@ -446,7 +447,7 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
         const uint64_t q0 = qa0 + base + 32ull * u;  // lane 0's quad
         const uint32_t pw0 = u ? __shfl_sync(0xFFFFFFFFu, v[u ? u - 1 : 0].w, 31)
                                : (carry_ok ? carry : __ldg(words + q0 * 4 - 1));
-        const uint32_t nw31 = u < kU - 1 ? __shfl_sync(0xFFFFFFFFu, v[u < kU - 1 ? u + 1 : 0].x, 0)
+        const uint32_t nw31 = u < kRU - 1 ? __shfl_sync(0xFFFFFFFFu, v[u < kRU - 1 ? u + 1 : 0].x, 0)
                                          : __ldg(words + (q0 + 32) * 4);
         if (__all_sync(0xFFFFFFFFu, (v[u].x | v[u].y | v[u].z | v[u].w) == 0u) && !((pw0 >> 31) | (nw31 & 1u)))
           continue;  // one zero run continues through the step
@@ -459,14 +460,14 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
         if (a4 != 0xFFFFFFFFu) runs_of(F.r + r, qa, true, v[u], pw, nw, st, en);
         visit(true, base + 32ull * u + lane, r, qa, false, st, en);
       }
-      carry = __shfl_sync(0xFFFFFFFFu, v[kU - 1].w, 31);
+      carry = __shfl_sync(0xFFFFFFFFu, v[kRU - 1].w, 31);
       carry_ok = true;
       continue;
     }
     // General iteration (range edges, chunk ends): one quad per lane at a time, with
     // per-lane range tracking and masks; edge neighbours are loaded, not shuffled.
 #pragma unroll 1
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < kRU; ++u) {
       const uint64_t f = base + 32ull * u + lane;
       const bool live = f < f1;
       if (live && f >= qend) {

@@ -65,6 +65,7 @@ __device__ __forceinline__ uint32_t stage_swz(uint32_t o) { return o ^ ((o >> 5)
 
 __device__ __forceinline__ void emit_staged(const uint32_t* m, uint32_t S, uint32_t T, uint32_t cb, uint64_t base,
                                             uint32_t* out, uint64_t cap, uint32_t* buf) {
+  if (base >= cap) return;  // warp-uniform: nothing of this step fits (e.g. a full staging chunk)
   uint32_t o = S;
 #pragma unroll
   for (int k = 0; k < 4; ++k)
