@@ -83,9 +83,10 @@ __device__ __forceinline__ void warp_chunk(uint64_t Q, uint64_t& f0, uint64_t& f
 // interior quads of the lanes' current range: then every lane is in that one range (a
 // lane's range only advances, and the iteration lies inside it), and the walkers skip
 // per-quad range tracking (its 64-bit compares dominate the instruction count).
+template <int U = kU>
 __device__ __forceinline__ bool interior_iteration(uint64_t base, uint64_t f1, uint64_t qend, uint64_t qa0,
                                                    uint64_t qtf, uint64_t qtl) {
-  const uint64_t e = base + 32ull * kU;
+  const uint64_t e = base + 32ull * U;
   return __all_sync(0xFFFFFFFFu, e <= f1 && e <= qend && qa0 + base > qtf && qa0 + e - 1 < qtl);
 }
 
@@ -433,7 +434,7 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
     // Fast iteration (warp-uniform): all 32 x kRU quads are interior quads of one range
     // (then every lane is in the same range, see the monotone advance below), so no
     // per-quad range tracking, masks or edge loads.
-    if (interior_iteration(base, f1, qend, qa0, qtf, qtl)) {
+    if (interior_iteration<kRU>(base, f1, qend, qa0, qtf, qtl)) {
       const uint64_t qb = qa0 + base + lane;
       uint4 v[kRU];
 #pragma unroll
