@@ -6,8 +6,11 @@
 // (modes.hpp:31-59): for every argument in order, the guard on the abstract flag decides
 // whether to copy (`pull x` = cudaMemcpyAsync D2H for a CPU component, `push x` = H2D for
 // a GPU component), then `w x^` for W/RW; then the component runs (CPU: on the calling
-// thread after the stream drains; GPU: launched on the runtime stream); then its body
-// effects (R: `r x`, W: `w x`, RW: both, at the component's site).  A step that cannot
+// thread once its own arguments' copies have landed; GPU: launched on the component
+// stream); then its body effects (R: `r x`, W: `w x`, RW: both, at the component's site).
+// Uploads and downloads run on two side streams; per vector, events on its last device-
+// and host-copy operations order each copy and component after exactly the work on the
+// same vector, so copies of independent vectors overlap each other and the components.  A step that cannot
 // unify (data valid nowhere the component needs it) is the calculus' Stuck and comes back
 // as COH_E_DEFECT with the StuckInfo text in coh_last_error; nothing is copied for it.
 //
@@ -56,6 +59,10 @@ struct RtVector {
   void* host = nullptr;
   void* dev = nullptr;
   uint32_t conc = 1, abst = 1;  // pairs: bit0 local (CPU) valid, bit1 remote (GPU) valid
+  // Stream-ordering state (side streams): the last enqueued operation touching each copy.
+  cudaEvent_t dev_last = nullptr;   // a GPU component, an upload (writes) or a download (reads)
+  cudaEvent_t host_last = nullptr;  // an upload (reads the host copy) or a download (writes it)
+  bool dev_pending = false, host_pending = false, host_written = false;
 };
 
 // A mother vector with element-granular validity (views, pvector<T>): planes L, R in one
@@ -81,7 +88,8 @@ struct coh_rt {
   std::vector<RtVector> vec;
   std::vector<RtBuffer> buf;
   std::vector<coh_rt_copy> log;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;              // GPU components (and the view path)
+  cudaStream_t up = nullptr, down = nullptr;  // side streams: uploads (H2D), downloads (D2H)
   coh_rt_stats stats{};
   std::vector<cudaEvent_t> ev_free;                           // event pool
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_open;  // copies not yet harvested
@@ -116,7 +124,11 @@ int coh_rt_create(coh_ctx* ctx, coh_rt** out) {
   if (!ctx || !out) return COH_E_ARG;
   coh_rt* rt = new coh_rt();
   rt->ctx = ctx;
-  if (cudaStreamCreateWithFlags(&rt->stream, cudaStreamNonBlocking) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&rt->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&rt->up, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&rt->down, cudaStreamNonBlocking) != cudaSuccess) {
+    if (rt->stream) cudaStreamDestroy(rt->stream);
+    if (rt->up) cudaStreamDestroy(rt->up);
     delete rt;
     ctx->err = "coh_rt_create: stream";
     return COH_E_CUDA;
@@ -128,11 +140,15 @@ int coh_rt_create(coh_ctx* ctx, coh_rt** out) {
 void coh_rt_destroy(coh_rt* rt) {
   if (!rt) return;
   cudaStreamSynchronize(rt->stream);
+  cudaStreamSynchronize(rt->up);
+  cudaStreamSynchronize(rt->down);
   harvest(rt);
   for (cudaEvent_t e : rt->ev_free) cudaEventDestroy(e);
   for (auto& v : rt->vec) {
     cudaFreeHost(v.host);
     cudaFree(v.dev);
+    cudaEventDestroy(v.dev_last);
+    cudaEventDestroy(v.host_last);
   }
   for (auto& b : rt->buf) {
     cudaFreeHost(b.host);
@@ -145,6 +161,8 @@ void coh_rt_destroy(coh_rt* rt) {
     cudaFree(b.d_runs);
   }
   cudaStreamDestroy(rt->stream);
+  cudaStreamDestroy(rt->up);
+  cudaStreamDestroy(rt->down);
   delete rt;
 }
 
@@ -161,6 +179,8 @@ int coh_rt_vector(coh_rt* rt, size_t bytes, uint32_t* id) {
     rt->ctx->err = "coh_rt_vector: device allocation of " + std::to_string(bytes) + " bytes";
     return COH_E_CUDA;
   }
+  cudaEventCreateWithFlags(&v.dev_last, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&v.host_last, cudaEventDisableTiming);
   *id = (uint32_t)rt->vec.size();
   rt->vec.push_back(v);
   return COH_OK;
@@ -208,14 +228,22 @@ int coh_rt_call(coh_rt* rt, uint32_t site, const coh_rt_arg* args, uint32_t n_ar
         if (c < 0) return stuck(sync, COH_LOCAL, args[i].vec, false, v.conc);
         const int a = apply_pair(sync, COH_LOCAL, v.abst);
         if (a < 0) return stuck(sync, COH_LOCAL, args[i].vec, true, v.abst);
-        // the transfer: upload for a GPU component (push), download for a CPU one (pull)
+        // the transfer: upload for a GPU component (push), download for a CPU one (pull),
+        // each on its side stream, ordered only after the operations that last touched
+        // this vector's two copies (other vectors' copies and components overlap it)
+        cudaStream_t cs = sync == COH_PUSH ? rt->up : rt->down;
+        if (v.dev_pending) cudaStreamWaitEvent(cs, v.dev_last, 0);
+        if (v.host_pending) cudaStreamWaitEvent(cs, v.host_last, 0);
         const cudaEvent_t e0 = take_event(rt), e1 = take_event(rt);
-        cudaEventRecord(e0, rt->stream);
-        cudaError_t e = sync == COH_PUSH
-                            ? cudaMemcpyAsync(v.dev, v.host, v.bytes, cudaMemcpyHostToDevice, rt->stream)
-                            : cudaMemcpyAsync(v.host, v.dev, v.bytes, cudaMemcpyDeviceToHost, rt->stream);
-        cudaEventRecord(e1, rt->stream);
+        cudaEventRecord(e0, cs);
+        cudaError_t e = sync == COH_PUSH ? cudaMemcpyAsync(v.dev, v.host, v.bytes, cudaMemcpyHostToDevice, cs)
+                                         : cudaMemcpyAsync(v.host, v.dev, v.bytes, cudaMemcpyDeviceToHost, cs);
+        cudaEventRecord(e1, cs);
         rt->ev_open.emplace_back(e0, e1);
+        cudaEventRecord(v.dev_last, cs);
+        cudaEventRecord(v.host_last, cs);
+        v.dev_pending = v.host_pending = true;
+        v.host_written = sync == COH_PULL;
         if (e != cudaSuccess) {
           rt->ctx->err = std::string("coh_rt_call copy: ") + cudaGetErrorString(e);
           return COH_E_CUDA;
@@ -241,18 +269,34 @@ int coh_rt_call(coh_rt* rt, uint32_t site, const coh_rt_arg* args, uint32_t n_ar
     if (args[i].kind != COH_W && apply_pair(COH_READ, site, v.conc) < 0)
       return stuck(COH_READ, site, args[i].vec, false, v.conc);
   }
-  if (fn) {
-    if (site == COH_REMOTE) {
-      fn(user, rt->stream);
-    } else {
-      cudaError_t e = cudaStreamSynchronize(rt->stream);  // copies (and earlier GPU work) land first
-      if (e != cudaSuccess) {
-        rt->ctx->err = std::string("coh_rt_call sync: ") + cudaGetErrorString(e);
-        return COH_E_CUDA;
-      }
-      harvest(rt);
-      fn(user, nullptr);
+  if (site == COH_REMOTE) {
+    // the component stream waits for the last operation on each argument's device copy
+    // (its upload, an earlier component, or a download still reading it)
+    for (uint32_t i = 0; i < n_args; ++i) {
+      RtVector& v = rt->vec[args[i].vec];
+      if (v.dev_pending) cudaStreamWaitEvent(rt->stream, v.dev_last, 0);
     }
+    if (fn) fn(user, rt->stream);
+    for (uint32_t i = 0; i < n_args; ++i) {
+      RtVector& v = rt->vec[args[i].vec];
+      cudaEventRecord(v.dev_last, rt->stream);
+      v.dev_pending = true;
+    }
+  } else if (fn) {
+    // the host thread waits only for its arguments: their downloads (read after write),
+    // and for an argument it writes, an upload still reading the host copy
+    for (uint32_t i = 0; i < n_args; ++i) {
+      RtVector& v = rt->vec[args[i].vec];
+      if (v.host_pending && (v.host_written || args[i].kind != COH_R)) {
+        const cudaError_t e = cudaEventSynchronize(v.host_last);
+        if (e != cudaSuccess) {
+          rt->ctx->err = std::string("coh_rt_call sync: ") + cudaGetErrorString(e);
+          return COH_E_CUDA;
+        }
+        v.host_pending = false;
+      }
+    }
+    fn(user, nullptr);
   }
   for (uint32_t i = 0; i < n_args; ++i) {
     RtVector& v = rt->vec[args[i].vec];
@@ -265,6 +309,9 @@ int coh_rt_call(coh_rt* rt, uint32_t site, const coh_rt_arg* args, uint32_t n_ar
 int coh_rt_sync(coh_rt* rt) {
   if (!rt) return COH_E_ARG;
   cudaError_t e = cudaStreamSynchronize(rt->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(rt->up);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(rt->down);
+  for (auto& v : rt->vec) v.dev_pending = v.host_pending = false;
   if (e != cudaSuccess) {
     rt->ctx->err = std::string("coh_rt_sync: ") + cudaGetErrorString(e);
     return COH_E_CUDA;
