@@ -375,8 +375,9 @@ typedef struct coh_rt_arg {
   uint32_t vec;
   uint32_t kind;       /* COH_R / COH_W / COH_RW */
 } coh_rt_arg;
-/* GPU components receive the runtime stream and must launch on it; CPU components get
- * NULL and run after the stream drained. */
+/* GPU components receive the component stream and must launch on it; CPU components get
+ * NULL and run on the calling thread once their own arguments' copies have landed
+ * (uploads and downloads run on side streams, ordered per vector by events). */
 typedef void (*coh_rt_fn)(void* user, void* stream);
 typedef struct coh_rt_stats {
   uint64_t h2d_bytes, d2h_bytes;
@@ -394,6 +395,11 @@ void* coh_rt_stream(coh_rt* rt);
 int coh_rt_state(coh_rt* rt, uint32_t id, uint8_t* nibble);  /* cl | cr<<1 | al<<2 | ar<<3 */
 int coh_rt_call(coh_rt* rt, uint32_t site, const coh_rt_arg* args, uint32_t n_args, coh_rt_fn fn, void* user);
 int coh_rt_sync(coh_rt* rt);
+/* Asynchronous CPU components (on != 0): a CPU component is enqueued as a stream-ordered
+ * host function (cudaLaunchHostFunc) after its arguments' copies, and coh_rt_call returns
+ * at once, so the copies of later calls overlap it.  Such a component must not call CUDA;
+ * its user data must stay valid and its effects become visible at coh_rt_sync. */
+int coh_rt_set_async(coh_rt* rt, int on);
 int coh_rt_get_stats(const coh_rt* rt, coh_rt_stats* out);
 /* Built-in trivial components over float vectors: W -> x = 1, RW -> x = 0.5x + 1,
  * R -> checksum.  user points to a coh_rt_touch. */

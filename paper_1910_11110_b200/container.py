@@ -56,6 +56,8 @@ def _register(L):
     L.coh_rt_sync.argtypes = [vp]
     L.coh_rt_get_stats.restype = C.c_int
     L.coh_rt_get_stats.argtypes = [vp, vp]
+    L.coh_rt_set_async.restype = C.c_int
+    L.coh_rt_set_async.argtypes = [vp, C.c_int]
 
 
 def _register_views(L):
@@ -154,6 +156,7 @@ class Runtime:
         if rc:
             raise CohError(rc, "coh_rt_create")
         self._h = h
+        self._keep: list = []  # component user data, kept until sync
         self.vectors: list[Vector] = []
         self.log: list[tuple[int, list[tuple[int, int]]]] = []   # (site, [(vec, kind)]) per call
 
@@ -193,7 +196,7 @@ class Runtime:
             for i, (v, k) in enumerate(args):
                 t.vec[i], t.kind[i], t.bytes[i] = v.id, KIND[k], v.nbytes
             fn, user = _TOUCH[s], C.addressof(t)
-            self._keep = t
+            self._keep.append(t)  # stays valid until sync (asynchronous CPU components)
         elif component is not None:
             fn, user = component
         rc = lib().coh_rt_call(self._h, s, C.addressof(arr), len(args), fn, user)
@@ -216,6 +219,12 @@ class Runtime:
 
     def sync(self):
         self.ctx._check(lib().coh_rt_sync(self._h), "coh_rt_sync")
+        self._keep = []
+
+    def set_async(self, on: bool = True):
+        """CPU components as stream-ordered host functions (coh_rt_set_async): calls return
+        at once; host data is final after sync()."""
+        self.ctx._check(lib().coh_rt_set_async(self._h, int(on)), "coh_rt_set_async")
 
     def stats(self) -> dict:
         st = _Stats()

@@ -90,6 +90,8 @@ struct coh_rt {
   std::vector<coh_rt_copy> log;
   cudaStream_t stream = nullptr;              // GPU components (and the view path)
   cudaStream_t up = nullptr, down = nullptr;  // side streams: uploads (H2D), downloads (D2H)
+  cudaStream_t host = nullptr;                // async mode: CPU components as host functions
+  bool async_host = false;
   coh_rt_stats stats{};
   std::vector<cudaEvent_t> ev_free;                           // event pool
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_open;  // copies not yet harvested
@@ -142,6 +144,7 @@ void coh_rt_destroy(coh_rt* rt) {
   cudaStreamSynchronize(rt->stream);
   cudaStreamSynchronize(rt->up);
   cudaStreamSynchronize(rt->down);
+  if (rt->host) cudaStreamSynchronize(rt->host);
   harvest(rt);
   for (cudaEvent_t e : rt->ev_free) cudaEventDestroy(e);
   for (auto& v : rt->vec) {
@@ -163,6 +166,7 @@ void coh_rt_destroy(coh_rt* rt) {
   cudaStreamDestroy(rt->stream);
   cudaStreamDestroy(rt->up);
   cudaStreamDestroy(rt->down);
+  if (rt->host) cudaStreamDestroy(rt->host);
   delete rt;
 }
 
@@ -282,6 +286,38 @@ int coh_rt_call(coh_rt* rt, uint32_t site, const coh_rt_arg* args, uint32_t n_ar
       cudaEventRecord(v.dev_last, rt->stream);
       v.dev_pending = true;
     }
+  } else if (fn && rt->async_host) {
+    // stream-ordered CPU component: the host stream waits for the last operation on each
+    // argument's host copy (its download, an upload still reading it, an earlier CPU
+    // component), then runs the component on the driver's host-function thread
+    for (uint32_t i = 0; i < n_args; ++i) {
+      RtVector& v = rt->vec[args[i].vec];
+      if (v.host_pending) cudaStreamWaitEvent(rt->host, v.host_last, 0);
+    }
+    struct Pack {
+      coh_rt_fn fn;
+      void* user;
+    };
+    Pack* pk = new Pack{fn, user};
+    const cudaError_t e = cudaLaunchHostFunc(
+        rt->host,
+        [](void* p) {
+          Pack* q = static_cast<Pack*>(p);
+          q->fn(q->user, nullptr);
+          delete q;
+        },
+        pk);
+    if (e != cudaSuccess) {
+      delete pk;
+      rt->ctx->err = std::string("coh_rt_call host function: ") + cudaGetErrorString(e);
+      return COH_E_CUDA;
+    }
+    for (uint32_t i = 0; i < n_args; ++i) {
+      RtVector& v = rt->vec[args[i].vec];
+      cudaEventRecord(v.host_last, rt->host);
+      v.host_pending = true;
+      v.host_written = true;
+    }
   } else if (fn) {
     // the host thread waits only for its arguments: their downloads (read after write),
     // and for an argument it writes, an upload still reading the host copy
@@ -311,12 +347,23 @@ int coh_rt_sync(coh_rt* rt) {
   cudaError_t e = cudaStreamSynchronize(rt->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(rt->up);
   if (e == cudaSuccess) e = cudaStreamSynchronize(rt->down);
+  if (e == cudaSuccess && rt->host) e = cudaStreamSynchronize(rt->host);
   for (auto& v : rt->vec) v.dev_pending = v.host_pending = false;
   if (e != cudaSuccess) {
     rt->ctx->err = std::string("coh_rt_sync: ") + cudaGetErrorString(e);
     return COH_E_CUDA;
   }
   harvest(rt);
+  return COH_OK;
+}
+
+int coh_rt_set_async(coh_rt* rt, int on) {
+  if (!rt) return COH_E_ARG;
+  if (on && !rt->host && cudaStreamCreateWithFlags(&rt->host, cudaStreamNonBlocking) != cudaSuccess) {
+    rt->ctx->err = "coh_rt_set_async: stream";
+    return COH_E_CUDA;
+  }
+  rt->async_host = on != 0;
   return COH_OK;
 }
 

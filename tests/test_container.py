@@ -74,3 +74,40 @@ def test_declared_twice_is_construction_error(ctx):
     with pytest.raises(coh.CohError) as e:
         rt.call("cpu", [(x, "R"), (x, "W")])
     assert e.value.code == 1
+
+
+@pytest.mark.parametrize("seed", [3, 11])
+def test_async_host_components_same_data_and_bytes(ctx, seed):
+    """Side streams + stream-ordered CPU components (coh_rt_set_async) reorder nothing the
+    calculus orders: the same chain leaves byte-identical host and device data and moves
+    exactly the same bytes as the synchronous runtime, equal to the evaluator's
+    prediction."""
+    import torch
+
+    from paper_1910_11110_b200.container import Runtime
+
+    outs = []
+    for mode in (False, True):
+        rng = np.random.default_rng(seed)
+        rt = Runtime(ctx)
+        if mode:
+            rt.set_async(True)
+        vecs = [rt.vector(1 << 22) for _ in range(4)]
+        for _ in range(48):
+            k = int(rng.integers(1, 4))
+            idx = rng.choice(4, size=k, replace=False)
+            site = "gpu" if rng.random() < 0.5 else "cpu"
+            rt.call(site, [(vecs[i], ["R", "W", "RW"][int(rng.integers(0, 3))]) for i in idx])
+        for v in vecs:  # bring every vector to the host (CPU reads)
+            rt.call("cpu", [(v, "R")])
+        rt.sync()
+        st = rt.stats()
+        pred = rt.predicted()
+        assert pred["transfer_bytes"] == st["h2d_bytes"] + st["d2h_bytes"]
+        outs.append(([v.host.copy() for v in vecs], st["h2d_bytes"], st["d2h_bytes"]))
+        rt.close()
+    (h0, u0, d0), (h1, u1, d1) = outs
+    assert (u0, d0) == (u1, d1)
+    for a, b in zip(h0, h1):
+        assert np.array_equal(a, b)
+    del torch
