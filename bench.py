@@ -661,7 +661,7 @@ def run_c4(args, ctx, rank, world, allreduce):
         allreduce(d_cnt)
         torch.cuda.synchronize()
         dist.all_reduce(c)
-    counters = d_cnt.cpu().numpy().view(np.uint64)[:10]
+    counters = d_cnt.cpu().numpy().view(np.uint64)[:11]
     ms = float(t.item())
     calls = int(counters[8] + counters[0] + counters[1] + counters[3])
     del d_rec, d_res
@@ -899,7 +899,7 @@ def run_ours(args, rank, world, local):
             "data": "synthetic (counter-based splitmix64 call records generated in HBM, seed 1)",
             "config": bench_config(world, N),
             "transitions_per_s": float(counters[4]) * args.steps / (ms / 1e3),
-            "counters_per_step": {n: int(v) for n, v in zip(coh.COUNTER_NAMES, counters[:10])},
+            "counters_per_step": {n: int(v) for n, v in zip(coh.COUNTER_NAMES, counters[:11])},
             "roofline": {"bound": "hbm", "kernel": "k_trace_eval", "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms": k_ms,

@@ -47,7 +47,10 @@ enum { COH_KEY_CONCRETE = 0, COH_KEY_ABSTRACT = 1 }; /* VarKey::Kind Scalar / Ab
 /* ---- whole-array component-call records ------------------------------------------
  * One uint16 per component call (one DeclBlock with a single AccessMode on one array,
  * program.hpp:212-235), SURVEY §8(d):
- *   bits 0-1   reserved (zero; ignored)
+ *   bit 0      COH_REC_CONT: the call continues the previous call's block (multi-mode
+ *              DeclBlocks, program.hpp:212-235), honoured only in batches flagged
+ *              COH_BATCH_BLOCKS (ignored otherwise)
+ *   bit 1      reserved (zero; ignored)
  *   bits 2-7   call type = mode kind R/W/RW (bits 2-3; 3 is malformed -> COH_RUN_DEFECT)
  *              | site << 2 (bit 4: 0 CPU/Local, 1 GPU/Remote)
  *              | body variant << 3 (bits 5-7: 0 = canonical well-declared body, 1..7
@@ -70,6 +73,7 @@ enum { COH_KEY_CONCRETE = 0, COH_KEY_ABSTRACT = 1 }; /* VarKey::Kind Scalar / Ab
   ((uint16_t)((((arr) & 63u) << 8) | (((kind) & 3u) << 2) | (((site) & 1u) << 4) | (((var) & 7u) << 5)))
 #define COH_MAX_ARRAYS 64
 #define COH_N_VARIANTS 8
+#define COH_REC_CONT 0x1u
 
 /* Per-array 4-bit state nibble: bit0 concrete local valid, bit1 concrete remote valid,
  * bit2 abstract local valid, bit3 abstract remote valid.  initial_store (program.hpp:
@@ -93,8 +97,11 @@ typedef struct coh_trace_result {
   uint8_t stuck_array;      /* StuckInfo::key (array id)                              */
   uint8_t stuck_effect;     /* StuckInfo::effect (COH_PUSH..)                         */
   uint8_t stuck_flags;      /* bit0 StuckInfo::site, bit1 key kind (COH_KEY_*),
-                               bits2-3 StuckInfo::actual (bit2 local V, bit3 remote V)  */
+                               bits2-3 StuckInfo::actual (bit2 local V, bit3 remote V),
+                               bit4 COH_FLAG_UNSAFE: is_unsafe (program.hpp:166-170) of
+                               the final store, some key (I,I) -- unreachable by Property 2 */
 } coh_trace_result;
+#define COH_FLAG_UNSAFE 0x10u
 
 static inline uint32_t coh_result_nibble(const coh_trace_result* r, uint32_t a) {
   return (r->state[a >> 3] >> (4u * (a & 7u))) & 15u;
@@ -106,9 +113,17 @@ typedef struct coh_trace_batch {
   uint32_t n_calls;            /* blocks per trace (>= 1)                              */
   uint32_t n_arrays;           /* 1..64                                                */
   int32_t fuel;                /* shared across blocks, as run_annotated (modes.hpp:110) */
-  uint32_t reserved;
+  uint32_t flags;              /* COH_BATCH_*                                          */
   const uint64_t* array_bytes; /* host, n_arrays entries (NULL => 1 byte each)         */
 } coh_trace_batch;
+
+/* COH_BATCH_BLOCKS: records carry COH_REC_CONT, so a block (one DeclBlock) is a record
+ * without the bit followed by the records with it: its modes in record order (arrays
+ * distinct, else the block is a construction defect), translated as translate_block does
+ * (modes.hpp:53-59): every mode's guard in order, then every record's body in order.
+ * Per-block outputs (calls_done, violations, stuck_call, boundary bits) then count and
+ * index blocks, not records. */
+#define COH_BATCH_BLOCKS 0x1u
 
 /* boundary_ok bitmaps: word-major, boundary[(i/32)*n_traces + t] bit (i%32) is
  * boundary_ok[i] of trace t; bits for calls >= calls_done are 0. */
@@ -184,10 +199,10 @@ int coh_eval_traces_host(coh_ctx* ctx, const coh_trace_batch* batch,
 /* Sum of per-trace counters into COH_N_COUNTERS uint64 (device):
  * [0] traces stuck, [1] traces fuel-exhausted, [2] traces with >=1 boundary violation,
  * [3] defect traces, [4] steps, [5] transfers, [6] transfer_bytes, [7] violating blocks,
- * [8] completed blocks (sum of calls_done), [9] traces.
+ * [8] completed blocks (sum of calls_done), [9] traces, [10] unsafe traces (is_unsafe).
  * Evaluated calls = [8] + [0] + [1] + [3].  This vector is what the multi-GPU path
  * allreduces; integer sums make it exact and order-independent. */
-#define COH_N_COUNTERS 10
+#define COH_N_COUNTERS 11
 int coh_reduce_counters(coh_ctx* ctx, const coh_trace_result* d_results, uint64_t n_traces,
                         uint64_t* d_counters, void* stream);
 

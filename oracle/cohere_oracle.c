@@ -21,6 +21,7 @@
  * tests/test_oracle.py checks this file against every one of them.
  */
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "cohere_b200.h"
@@ -146,12 +147,73 @@ int orc_call_outcome(uint32_t call_type, uint32_t state, coh_call_outcome* out) 
   return 0;
 }
 
-int orc_eval_traces(const uint16_t* records, uint64_t n_total, uint64_t t_begin, uint64_t t_end,
-                    uint32_t n_calls, uint32_t n_arrays, int32_t fuel, const uint64_t* array_bytes,
-                    coh_trace_result* out, uint32_t* boundary) {
+/* One record's statements split as translate_block interleaves them for a multi-mode
+ * block: the mode's guard (ensure_valid + mark_written, modes.hpp:36-48) and its body. */
+static int split_call(uint16_t rec, orc_stmt* guard, int* n_guard, orc_stmt* body) {
+  orc_stmt s[8];
+  const int n = translate_call(rec, s);
+  if (n < 0) return -1;
+  const int kind = (int)COH_REC_KIND(rec);
+  const int g = kind == COH_R ? 3 : kind == COH_W ? 1 : 4;
+  memcpy(guard, s, sizeof(orc_stmt) * (size_t)g);
+  memcpy(body, s + g, sizeof(orc_stmt) * (size_t)(n - g));
+  *n_guard = g;
+  return n - g;
+}
+
+/* run() over a block's statement list, each statement on its own array (the if-guards
+ * skip the two syncs that follow them when the flag is valid). */
+typedef struct {
+  orc_stmt s;
+  int a;
+} orc_astmt;
+
+static void run_multi(const orc_astmt* s, int n, int* conc, int* abst, int fuel, orc_block_out* o, int* stuck_a,
+                      const uint64_t* array_bytes, uint64_t* tbytes) {
+  int k = 0;
+  memset(o, 0, sizeof *o);
+  for (;;) {
+    if (k >= n) { o->status = COH_RUN_DONE; return; }
+    if (o->steps >= fuel) { o->status = COH_RUN_FUEL_EXHAUSTED; return; }
+    const int a = s[k].a;
+    if (s[k].s.kind != 0) {
+      const int flag = s[k].s.kind == 1 ? (abst[a] & 1) : ((abst[a] >> 1) & 1);
+      o->steps++;
+      k += flag ? 3 : 1;
+      continue;
+    }
+    int* cell = s[k].s.abstract_target ? &abst[a] : &conc[a];
+    const int after = orc_apply_cell(s[k].s.eff, s[k].s.site, *cell);
+    if (after < 0) {
+      o->status = COH_RUN_STUCK;
+      o->stuck_eff = s[k].s.eff;
+      o->stuck_flags = s[k].s.site | (s[k].s.abstract_target << 1) | (*cell << 2);
+      *stuck_a = a;
+      return;
+    }
+    *cell = after;
+    o->steps++;
+    if (!s[k].s.abstract_target && (s[k].s.eff == COH_PUSH || s[k].s.eff == COH_PULL)) {
+      o->transfers++;
+      *tbytes += array_bytes ? array_bytes[a] : 1u;
+    }
+    k++;
+  }
+}
+
+/* flags & COH_BATCH_BLOCKS: a record with COH_REC_CONT continues the previous record's
+ * block (a DeclBlock with several modes, program.hpp:212-235): its arrays must be
+ * distinct and declared (else a construction defect at that block), and it runs as
+ * translate_block lays it out (modes.hpp:53-59): all guards in record order, then all
+ * bodies in record order.  Without the flag every record is its own block. */
+int orc_eval_traces_ex(const uint16_t* records, uint64_t n_total, uint64_t t_begin, uint64_t t_end,
+                       uint32_t n_calls, uint32_t n_arrays, int32_t fuel, const uint64_t* array_bytes,
+                       uint32_t flags, coh_trace_result* out, uint32_t* boundary) {
   if (n_arrays < 1 || n_arrays > COH_MAX_ARRAYS || t_end < t_begin) return -1;
   const uint64_t m = t_end - t_begin;
   const uint32_t n_words = (n_calls + 31) / 32;
+  orc_astmt* prog = (orc_astmt*)malloc(sizeof(orc_astmt) * 8u * (n_calls ? n_calls : 1u));
+  if (!prog) return -1;
   for (uint64_t j = 0; j < m; ++j) {
     const uint64_t t = t_begin + j;
     int conc[COH_MAX_ARRAYS], abst[COH_MAX_ARRAYS];
@@ -161,40 +223,77 @@ int orc_eval_traces(const uint16_t* records, uint64_t n_total, uint64_t t_begin,
     if (boundary)
       for (uint32_t w = 0; w < n_words; ++w) boundary[(uint64_t)w * m + j] = 0;
     int steps = 0, status = COH_RUN_DONE;
-    for (uint32_t i = 0; i < n_calls; ++i) {
-      const uint16_t rec = records[((uint64_t)(i / 8) * n_total + t) * 8 + i % 8];
-      const uint32_t a = COH_REC_ARRAY(rec);
-      orc_stmt s[8];
+    uint32_t blk = 0;
+#define ORC_REC(i) records[((uint64_t)((i) / 8) * n_total + t) * 8 + (i) % 8]
+    for (uint32_t b0 = 0; b0 < n_calls; ++blk) {
+      uint32_t b1 = b0 + 1;
+      if (flags & COH_BATCH_BLOCKS)
+        while (b1 < n_calls && (ORC_REC(b1) & COH_REC_CONT)) ++b1;
+      /* DeclBlock construction: every mode declared, well formed, on a distinct array */
+      uint64_t seen = 0;
+      int defect = -1;
+      for (uint32_t i = b0; i < b1 && defect < 0; ++i) {
+        const uint16_t rec = ORC_REC(i);
+        const uint32_t a = COH_REC_ARRAY(rec);
+        if (a >= n_arrays || COH_REC_KIND(rec) == 3 || ((seen >> a) & 1u)) defect = (int)a;
+        seen |= 1ull << a;
+      }
+      if (defect >= 0) {
+        status = COH_RUN_DEFECT;
+        r->stuck_call = blk;
+        r->stuck_array = (uint8_t)defect;
+        break;
+      }
+      int n = 0;
+      orc_stmt g[8], bd[8];
+      for (uint32_t i = b0; i < b1; ++i) { /* guards */
+        int ng = 0;
+        split_call(ORC_REC(i), g, &ng, bd);
+        for (int k = 0; k < ng; ++k) prog[n].s = g[k], prog[n++].a = (int)COH_REC_ARRAY(ORC_REC(i));
+      }
+      for (uint32_t i = b0; i < b1; ++i) { /* bodies */
+        int ng = 0;
+        const int nb = split_call(ORC_REC(i), g, &ng, bd);
+        for (int k = 0; k < nb; ++k) prog[n].s = bd[k], prog[n++].a = (int)COH_REC_ARRAY(ORC_REC(i));
+      }
       orc_block_out o;
-      int dummy_c = 1, dummy_a = 1; /* an unknown array is a construction defect */
-      const int n = a < n_arrays ? translate_call(rec, s) : -1;
-      run_block(s, n, a < n_arrays ? &conc[a] : &dummy_c, a < n_arrays ? &abst[a] : &dummy_a,
-                fuel - steps, &o);
-      steps += o.steps;
+      int stuck_a = (int)COH_REC_ARRAY(ORC_REC(b0)); /* fuel exhaustion: the block's first array */
+      run_multi(prog, n, conc, abst, fuel - steps, &o, &stuck_a, array_bytes, &r->transfer_bytes);
       r->transfers += (uint32_t)o.transfers;
-      if (o.transfers) r->transfer_bytes += (uint64_t)o.transfers * (array_bytes ? array_bytes[a] : 1u);
+      steps += o.steps;
       if (o.status != COH_RUN_DONE) {
         status = o.status;
-        r->stuck_call = i;
-        r->stuck_array = (uint8_t)a;
+        r->stuck_call = blk;
+        r->stuck_array = (uint8_t)stuck_a;
         r->stuck_effect = (uint8_t)o.stuck_eff;
         r->stuck_flags = (uint8_t)o.stuck_flags;
         break;
       }
-      /* abstraction_correct: every array's abstract pair bounds its concrete pair */
       int ok = 1;
       for (uint32_t b = 0; b < n_arrays; ++b)
         if (!orc_leq(abst[b], conc[b])) { ok = 0; break; }
       r->calls_done++;
       if (!ok) r->violations++;
-      if (ok && boundary) boundary[(uint64_t)(i / 32) * m + j] |= 1u << (i % 32);
+      if (ok && boundary) boundary[(uint64_t)(blk / 32) * m + j] |= 1u << (blk % 32);
+      b0 = b1;
     }
+#undef ORC_REC
     r->status = (uint8_t)status;
     r->steps = (uint32_t)steps;
-    for (uint32_t a = 0; a < n_arrays; ++a)
+    for (uint32_t a = 0; a < n_arrays; ++a) {
       r->state[a / 8] |= (uint32_t)(conc[a] | (abst[a] << 2)) << (4 * (a % 8));
+      if (conc[a] == 0 || abst[a] == 0) r->stuck_flags |= COH_FLAG_UNSAFE; /* is_unsafe, program.hpp:166-170 */
+    }
   }
+  free(prog);
   return 0;
+}
+
+int orc_eval_traces(const uint16_t* records, uint64_t n_total, uint64_t t_begin, uint64_t t_end,
+                    uint32_t n_calls, uint32_t n_arrays, int32_t fuel, const uint64_t* array_bytes,
+                    coh_trace_result* out, uint32_t* boundary) {
+  return orc_eval_traces_ex(records, n_total, t_begin, t_end, n_calls, n_arrays, fuel, array_bytes, 0, out,
+                            boundary);
 }
 
 /* Generator restatement (include/cohere_b200.h) for record-checksum parity. */

@@ -97,6 +97,102 @@ void fill_stuck(const std::optional<StuckInfo>& st, coh_trace_result& r) {
                             (pair_bits(st->actual) << 2));
 }
 
+// COH_BATCH_BLOCKS: the reference's own multi-mode DeclBlock for records [b0, b1) --
+// one AccessMode per record, the body the records' bodies in order (translate_block then
+// puts every guard before the body, modes.hpp:53-59).  Returns false when the DeclBlock
+// cannot be built (undeclared / malformed / repeated variable: ConstructionError).
+bool make_multi_block(const Declarations& d, const uint16_t* recs, uint64_t n_total, uint64_t t, uint32_t b0,
+                      uint32_t b1, uint32_t n_arrays, DeclBlock* out, uint32_t* bad_array) {
+  std::vector<AccessMode> modes;
+  std::vector<Stmt> body;
+  uint64_t seen = 0;
+  int repeated = -1;  // the first array named twice (reported as the defect's array)
+  for (uint32_t i = b0; i < b1; ++i) {
+    const uint16_t rec = recs[((uint64_t)(i / 8) * n_total + t) * 8 + i % 8];
+    const uint32_t a = COH_REC_ARRAY(rec), kind = COH_REC_KIND(rec);
+    if (a >= n_arrays || kind > 2) {
+      if (repeated >= 0) break;  // the repeat came first
+      *bad_array = a;
+      return false;
+    }
+    if (((seen >> a) & 1u) && repeated < 0) repeated = (int)a;
+    seen |= 1ull << a;
+    const Site S = COH_REC_SITE(rec) ? Site::Remote : Site::Local;
+    AccessMode m;
+    m.kind = static_cast<AccessMode::Kind>(kind);
+    m.site = S;
+    m.view = array_names()[a];
+    modes.push_back(m);
+    body.push_back(make_body(d, array_names()[a], kind, S, COH_REC_VARIANT(rec)));
+  }
+  try {
+    *out = DeclBlock(std::move(modes), Stmt::seq(body));
+  } catch (const ConstructionError&) {  // a variable declared twice in one block (program.hpp:218-225)
+    *bad_array = repeated >= 0 ? (uint32_t)repeated : 0u;
+    return false;
+  }
+  if (repeated >= 0) {  // the reference must have refused it
+    *bad_array = 0xFFu;
+    return false;
+  }
+  return true;
+}
+
+void eval_blocks(const uint16_t* recs, uint64_t n_total, uint64_t t, uint32_t n_calls, uint32_t n_arrays, int32_t fuel,
+                 const uint64_t* array_bytes, coh_trace_result& r, std::vector<bool>& bnd) {
+  Declarations decls;
+  for (uint32_t a = 0; a < n_arrays; ++a) decls.add_scalar({array_names()[a], {}});
+  std::memset(&r, 0, sizeof r);
+  Store store = initial_store(decls);
+  Schedule schedule;
+  int steps = 0;
+  RunStatus status = RunStatus::Done;
+  bnd.clear();
+  auto rec_at = [&](uint32_t i) { return recs[((uint64_t)(i / 8) * n_total + t) * 8 + i % 8]; };
+  // run_annotated (modes.hpp:105-125) over the blocks, TraceMode::Full for transfers
+  for (uint32_t b0 = 0; b0 < n_calls;) {
+    uint32_t b1 = b0 + 1;
+    while (b1 < n_calls && (rec_at(b1) & COH_REC_CONT)) ++b1;
+    DeclBlock block;
+    uint32_t bad = 0;
+    if (!make_multi_block(decls, recs, n_total, t, b0, b1, n_arrays, &block, &bad)) {
+      r.status = COH_RUN_DEFECT;
+      r.stuck_call = (uint32_t)bnd.size();
+      r.stuck_array = (uint8_t)bad;
+      break;
+    }
+    RunResult rr = run(translate_block(block, decls), std::move(store), fuel - steps, schedule, TraceMode::Full);
+    store = std::move(rr.store);
+    steps += rr.steps;
+    status = rr.status;
+    schedule.pos = rr.schedule_consumed;
+    for (const auto& ts : rr.trace)
+      if (is_sync(ts.head)) {
+        r.transfers++;
+        const uint32_t a = (uint32_t)std::stoi(ts.head.node().target.name.substr(1));
+        r.transfer_bytes += array_bytes ? array_bytes[a] : 1u;
+      }
+    if (rr.status != RunStatus::Done) {
+      r.status = (uint8_t)status;
+      r.stuck_call = (uint32_t)bnd.size();
+      r.stuck_array = (uint8_t)COH_REC_ARRAY(rec_at(b0));  // fuel exhaustion: the block's first array
+      fill_stuck(rr.stuck, r);
+      break;
+    }
+    bnd.push_back(abstraction_correct(store, decls));
+    b0 = b1;
+  }
+  r.steps = (uint32_t)steps;
+  r.calls_done = (uint32_t)bnd.size();
+  for (bool ok : bnd) r.violations += ok ? 0u : 1u;
+  for (uint32_t a = 0; a < n_arrays; ++a) {
+    const uint32_t c = pair_bits(store.at(VarKey::scalar(array_names()[a])));
+    const uint32_t ab = pair_bits(store.at(VarKey::abstract(array_names()[a])));
+    r.state[a / 8] |= (c | (ab << 2)) << (4 * (a % 8));
+  }
+  if (is_unsafe(store)) r.stuck_flags |= COH_FLAG_UNSAFE;
+}
+
 void eval_one(const uint16_t* recs, uint64_t n_total, uint64_t t, uint32_t n_calls,
               uint32_t n_arrays, int32_t fuel, const uint64_t* array_bytes, int mode,
               coh_trace_result& r, std::vector<bool>& bnd) {
@@ -159,6 +255,7 @@ void eval_one(const uint16_t* recs, uint64_t n_total, uint64_t t, uint32_t n_cal
     const uint32_t ab = pair_bits(store.at(VarKey::abstract(array_names()[a])));
     r.state[a / 8] |= (c | (ab << 2)) << (4 * (a % 8));
   }
+  if (is_unsafe(store)) r.stuck_flags |= COH_FLAG_UNSAFE;  // program.hpp:166-170
 }
 
 }  // namespace
@@ -168,6 +265,7 @@ extern "C" {
 // Evaluate traces [t_begin, t_end) of a record set laid out for n_total traces.
 // out / boundary are indexed relative to t_begin; boundary is word-major
 // [(i/32) * (t_end - t_begin) + (t - t_begin)] (may be NULL).  Returns 0 or -1.
+// mode 2: COH_BATCH_BLOCKS (records with COH_REC_CONT continue the previous block).
 int ref_eval_traces(const uint16_t* records, uint64_t n_total, uint64_t t_begin, uint64_t t_end,
                     uint32_t n_calls, uint32_t n_arrays, int32_t fuel, const uint64_t* array_bytes,
                     coh_trace_result* out, uint32_t* boundary, int n_threads, int mode) {
@@ -182,7 +280,10 @@ int ref_eval_traces(const uint16_t* records, uint64_t n_total, uint64_t t_begin,
       const uint64_t j = next.fetch_add(1);
       if (j >= m) break;
       try {
-        eval_one(records, n_total, t_begin + j, n_calls, n_arrays, fuel, array_bytes, mode, out[j], bnd);
+        if (mode == 2)
+          eval_blocks(records, n_total, t_begin + j, n_calls, n_arrays, fuel, array_bytes, out[j], bnd);
+        else
+          eval_one(records, n_total, t_begin + j, n_calls, n_arrays, fuel, array_bytes, mode, out[j], bnd);
       } catch (...) {
         failed = 1;
         continue;

@@ -10,7 +10,10 @@ generator are host code), but every evaluation goes through the CUDA library and
 is missing or fails.
 """
 from ._ffi import (  # noqa: F401
+    BATCH_BLOCKS,
     COUNTER_NAMES,
+    FLAG_UNSAFE,
+    REC_CONT,
     RESULT_DTYPE,
     CohError,
     Comm,
@@ -41,6 +44,9 @@ from .reference_api import (  # noqa: F401
 )
 
 __all__ = [
+    "BATCH_BLOCKS",
+    "FLAG_UNSAFE",
+    "REC_CONT",
     "Context",
     "CohError",
     "Comm",

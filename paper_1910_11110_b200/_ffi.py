@@ -48,7 +48,11 @@ COUNTER_NAMES = (
     "violating_blocks",
     "completed_blocks",
     "traces",
+    "unsafe_traces",
 )
+BATCH_BLOCKS = 1  # COH_BATCH_BLOCKS: records carry COH_REC_CONT (multi-mode blocks)
+REC_CONT = 1      # COH_REC_CONT
+FLAG_UNSAFE = 0x10
 N_COUNTERS = len(COUNTER_NAMES)
 
 
@@ -65,7 +69,7 @@ class _Batch(C.Structure):
         ("n_calls", C.c_uint32),
         ("n_arrays", C.c_uint32),
         ("fuel", C.c_int32),
-        ("reserved", C.c_uint32),
+        ("flags", C.c_uint32),
         ("array_bytes", C.c_void_p),
     ]
 
@@ -223,14 +227,14 @@ class Context:
         return int(self._L.coh_launch_count(self._h))
 
     @staticmethod
-    def _batch(records, n_traces, n_calls, n_arrays, fuel, array_bytes):
+    def _batch(records, n_traces, n_calls, n_arrays, fuel, array_bytes, flags=0):
         b = _Batch()
         b.records = _ptr(records)
         b.n_traces = n_traces
         b.n_calls = n_calls
         b.n_arrays = n_arrays
         b.fuel = fuel
-        b.reserved = 0
+        b.flags = flags
         if array_bytes is not None:
             ab = np.ascontiguousarray(np.asarray(array_bytes, dtype=np.uint64))
             b.array_bytes = ab.ctypes.data
@@ -245,18 +249,19 @@ class Context:
             "coh_gen_records",
         )
 
-    def eval_traces(self, d_records, n_traces, n_calls, n_arrays, fuel, d_results, d_boundary=None, array_bytes=None, stream=0):
+    def eval_traces(self, d_records, n_traces, n_calls, n_arrays, fuel, d_results, d_boundary=None, array_bytes=None, stream=0,
+                    flags=0):
         """Device-buffer entry point (coh_eval_traces); all pointers are device addresses."""
-        b = self._batch(d_records, n_traces, n_calls, n_arrays, fuel, array_bytes)
+        b = self._batch(d_records, n_traces, n_calls, n_arrays, fuel, array_bytes, flags)
         self._check(
             self._L.coh_eval_traces(self._h, C.byref(b), _ptr(d_results), _ptr(d_boundary), _ptr(stream)),
             "coh_eval_traces",
         )
 
     def eval_traces_counted(self, d_records, n_traces, n_calls, n_arrays, fuel, d_results, d_counters, d_boundary=None,
-                            array_bytes=None, stream=0):
+                            array_bytes=None, stream=0, flags=0):
         """coh_eval_traces with the COH_N_COUNTERS reduction fused into the kernel."""
-        b = self._batch(d_records, n_traces, n_calls, n_arrays, fuel, array_bytes)
+        b = self._batch(d_records, n_traces, n_calls, n_arrays, fuel, array_bytes, flags)
         self._check(
             self._L.coh_eval_traces_counted(self._h, C.byref(b), _ptr(d_results), _ptr(d_boundary), _ptr(d_counters),
                                             _ptr(stream)),
@@ -264,7 +269,8 @@ class Context:
         )
 
     def eval_traces_host(self, records: np.ndarray, n_traces, n_calls, n_arrays, fuel=10000, array_bytes=None,
-                         results: np.ndarray | None = None, boundary: np.ndarray | None = None, want_boundary=True):
+                         results: np.ndarray | None = None, boundary: np.ndarray | None = None, want_boundary=True,
+                         flags=0):
         """Host-buffer entry point (coh_eval_traces_host): H2D, kernel and D2H inside the call."""
         if records.dtype != np.uint16 or records.size < records_elems(n_traces, n_calls):
             raise ValueError("records must be uint16 in the call-major interleaved layout")
@@ -272,7 +278,7 @@ class Context:
             results = np.zeros(n_traces, dtype=RESULT_DTYPE)
         if boundary is None and want_boundary:
             boundary = np.zeros(boundary_words(n_calls) * n_traces, dtype=np.uint32)
-        b = self._batch(records, n_traces, n_calls, n_arrays, fuel, array_bytes)
+        b = self._batch(records, n_traces, n_calls, n_arrays, fuel, array_bytes, flags)
         self._check(
             self._L.coh_eval_traces_host(self._h, C.byref(b), _ptr(results), _ptr(boundary) if want_boundary else None),
             "coh_eval_traces_host",

@@ -35,6 +35,7 @@ int validate(coh_ctx* ctx, const coh_trace_batch* b) {
   if (b->n_arrays < 1 || b->n_arrays > COH_MAX_ARRAYS)
     return arg_fail(ctx, "n_arrays must be in [1, 64], got " + std::to_string(b->n_arrays));
   if (b->n_traces && b->n_calls && !b->records) return arg_fail(ctx, "records is NULL");
+  if (b->flags & ~COH_BATCH_BLOCKS) return arg_fail(ctx, "unknown batch flags");
   return COH_OK;
 }
 
@@ -94,8 +95,9 @@ int eval_device(coh_ctx* ctx, const coh_trace_batch* b, const uint16_t* d_record
     COH_CUDA(ctx, cudaMemsetAsync(ticket, 0, sizeof(unsigned int), s));
   }
   L.ticket = ticket;
+  L.flags = b->flags;
   std::string err;
-  rc = cohb::launch_trace_eval(L, s, &err);
+  rc = (b->flags & COH_BATCH_BLOCKS) ? cohb::launch_trace_blocks(L, s, &err) : cohb::launch_trace_eval(L, s, &err);
   if (ticket) cudaFreeAsync(ticket, s);
   if (d_bytes) cudaFreeAsync(d_bytes, s);
   if (rc) {

@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_counters(const coh_trace
     c[7] += q3.y;
     c[8] += q3.x;
     c[9] += 1;
+    c[10] += (q3.w >> 24) & COH_FLAG_UNSAFE ? 1u : 0u;
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll

@@ -83,6 +83,7 @@ struct TraceLaunch {
   uint32_t n_calls;
   uint32_t n_arrays;
   int32_t fuel;
+  uint32_t flags;  // COH_BATCH_*
   bool check_fuel;
   bool uniform_bytes;
   uint64_t bytes_uniform;
@@ -96,6 +97,8 @@ struct TraceLaunch {
   unsigned int* ticket;  // device, zeroed, private to this launch (dynamic trace batches)
 };
 int launch_trace_eval(const TraceLaunch& p, void* stream, std::string* err);
+// Multi-mode blocks (COH_BATCH_BLOCKS, trace_blocks.cu).
+int launch_trace_blocks(const TraceLaunch& p, void* stream, std::string* err);
 int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t n_calls, std::string* err);
 int launch_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
                        uint32_t n_arrays, uint32_t adv_per1024, uint16_t* d_records, void* stream,

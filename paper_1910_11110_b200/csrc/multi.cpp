@@ -250,6 +250,7 @@ int coh_counters_host(const coh_trace_result* results, uint64_t n_traces, uint64
     counters[7] += r.violations;
     counters[8] += r.calls_done;
     counters[9] += 1;
+    counters[10] += (r.stuck_flags & COH_FLAG_UNSAFE) != 0;
   }
   return COH_OK;
 }

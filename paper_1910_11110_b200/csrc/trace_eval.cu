@@ -485,6 +485,17 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
         if (a < (int)p.n_arrays) COH_SLOT_OUT(a)
     }
 #undef COH_SLOT_OUT
+    {  // is_unsafe (program.hpp:166-170): a live array whose concrete or abstract pair is (I,I)
+      uint32_t bad = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t live = 8 * k + 8 <= (int)p.n_arrays ? 0x55555555u
+                              : 8 * k >= (int)p.n_arrays  ? 0u
+                                                          : 0x55555555u & ((1u << (4 * (p.n_arrays - 8 * k))) - 1u);
+        bad |= ~(sw[k] | (sw[k] >> 1)) & live;
+      }
+      if (bad) stuck_flags |= COH_FLAG_UNSAFE;
+    }
     const uint64_t tb = UNIFORM ? (uint64_t)xfers * p.bytes_uniform : tbytes;
     uint4* out = reinterpret_cast<uint4*>(p.res + t);
     __stcs(out + 0, make_uint4(sw[0], sw[1], sw[2], sw[3]));
@@ -495,11 +506,12 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
     if (p.counters) {  // fused counter reduction: warp redux, one shared atomic per warp
       const uint32_t m = __activemask();
       const bool leader = (lane == (uint32_t)(__ffs(m) - 1));
-      uint32_t v[9] = {status == COH_RUN_STUCK, status == COH_RUN_FUEL_EXHAUSTED, viol_blocks != 0u,
-                       status == COH_RUN_DEFECT, steps, xfers, viol_blocks, calls_done, 1u};
-      const int slot[9] = {0, 1, 2, 3, 4, 5, 7, 8, 9};
+      uint32_t v[10] = {status == COH_RUN_STUCK, status == COH_RUN_FUEL_EXHAUSTED, viol_blocks != 0u,
+                        status == COH_RUN_DEFECT, steps, xfers, viol_blocks, calls_done, 1u,
+                        (stuck_flags & COH_FLAG_UNSAFE) != 0u};
+      const int slot[10] = {0, 1, 2, 3, 4, 5, 7, 8, 9, 10};
 #pragma unroll
-      for (int k = 0; k < 9; ++k) {
+      for (int k = 0; k < 10; ++k) {
         v[k] = __reduce_add_sync(m, v[k]);
         if (leader && v[k]) atomicAdd(&sm.cnt[slot[k]], (unsigned long long)v[k]);
       }
@@ -827,6 +839,7 @@ __global__ void __launch_bounds__(kScanNT) k_trace_scan(const KParams p) {
     return;
 #endif
     const uint64_t tb = (uint64_t)xfers * xbytes;
+    if (!(s_cur & 3u) || !(s_cur & 12u)) stuck_flags |= COH_FLAG_UNSAFE;  // is_unsafe
     uint4* out = reinterpret_cast<uint4*>(p.res + t);
     __stcs(out + 0, make_uint4(s_cur, 0u, 0u, 0u));
     __stcs(out + 1, make_uint4(0u, 0u, 0u, 0u));
@@ -834,10 +847,11 @@ __global__ void __launch_bounds__(kScanNT) k_trace_scan(const KParams p) {
     __stcs(out + 3, make_uint4(calls_done, viol_blocks, stuck_call,
                                status | (stuck_arr << 8) | (stuck_eff << 16) | (stuck_flags << 24)));
     if (p.counters) {
-      const unsigned long long v[10] = {status == COH_RUN_STUCK, status == COH_RUN_FUEL_EXHAUSTED, viol_blocks != 0u,
-                                        status == COH_RUN_DEFECT, steps, xfers, tb, viol_blocks, calls_done, 1u};
+      const unsigned long long v[COH_N_COUNTERS] = {
+          status == COH_RUN_STUCK, status == COH_RUN_FUEL_EXHAUSTED, viol_blocks != 0u, status == COH_RUN_DEFECT,
+          steps, xfers, tb, viol_blocks, calls_done, 1u, (stuck_flags & COH_FLAG_UNSAFE) != 0u};
 #pragma unroll
-      for (int k = 0; k < 10; ++k)
+      for (int k = 0; k < COH_N_COUNTERS; ++k)
         if (v[k]) atomicAdd(p.counters + k, v[k]);
     }
   }

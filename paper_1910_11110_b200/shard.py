@@ -42,6 +42,7 @@ def counters_from_results(results: np.ndarray) -> np.ndarray:
     out[7] = results["violations"].astype(np.uint64).sum()
     out[8] = results["calls_done"].astype(np.uint64).sum()
     out[9] = len(results)
+    out[10] = ((results["stuck_flags"] & 0x10) != 0).sum()
     return out
 
 

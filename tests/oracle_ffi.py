@@ -55,6 +55,8 @@ def oracle():
         L.orc_call_outcome.argtypes = [u32, u32, C.POINTER(_Outcome)]
         L.orc_eval_traces.restype = C.c_int
         L.orc_eval_traces.argtypes = [vp, u64, u64, u64, u32, u32, i32, vp, vp, vp]
+        L.orc_eval_traces_ex.restype = C.c_int
+        L.orc_eval_traces_ex.argtypes = [vp, u64, u64, u64, u32, u32, i32, vp, u32, vp, vp]
         L.orc_gen_records.restype = C.c_int
         L.orc_gen_records.argtypes = [u64, u64, u64, u32, u32, u32, vp]
         _orc = L
@@ -91,14 +93,14 @@ def _ab(array_bytes):
     return a, a.ctypes.data
 
 
-def orc_eval(records, n_total, n_calls, n_arrays, fuel=10000, array_bytes=None, t_begin=0, t_end=None):
+def orc_eval(records, n_total, n_calls, n_arrays, fuel=10000, array_bytes=None, t_begin=0, t_end=None, flags=0):
     t_end = n_total if t_end is None else t_end
     m = t_end - t_begin
     out = np.zeros(m, dtype=RESULT_DTYPE)
     bnd = np.zeros(boundary_words(n_calls) * m, dtype=np.uint32)
     keep, abp = _ab(array_bytes)
-    rc = oracle().orc_eval_traces(records.ctypes.data, n_total, t_begin, t_end, n_calls, n_arrays, fuel, abp,
-                                  out.ctypes.data, bnd.ctypes.data)
+    rc = oracle().orc_eval_traces_ex(records.ctypes.data, n_total, t_begin, t_end, n_calls, n_arrays, fuel, abp, flags,
+                                     out.ctypes.data, bnd.ctypes.data)
     assert rc == 0
     return out, bnd
 
@@ -191,3 +193,22 @@ def ref_sweep_stats(seed0, n, max_dec=6, fuel=10000):
     L.ref_sweep_stats(seed0, n, max_dec, fuel, out.ctypes.data)
     return dict(zip(["runs", "done", "stuck", "fuel_exhausted", "bad_boundary_programs", "oracle_disagreements"],
                     (int(x) for x in out)))
+
+
+def add_blocks(records, n_traces, n_calls, cont_per1024, seed, dup_per1024=0):
+    """Multi-mode blocks for tests: set COH_REC_CONT (bit 0) on call i > 0 of each trace with
+    probability cont_per1024/1024 when its array is not yet in the current block (and, with
+    probability dup_per1024/1024, even when it is: a construction defect)."""
+    rng = np.random.default_rng(seed)
+    r = records.copy().reshape(-1, n_traces, 8)
+    for t in range(n_traces):
+        cur = set()
+        for i in range(n_calls):
+            c, k = divmod(i, 8)
+            a = (int(r[c, t, k]) >> 8) & 63
+            if i > 0 and rng.integers(0, 1024) < cont_per1024 and (a not in cur or rng.integers(0, 1024) < dup_per1024):
+                r[c, t, k] |= 1
+                cur.add(a)
+            else:
+                cur = {a}
+    return r.reshape(-1)

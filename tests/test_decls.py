@@ -10,7 +10,7 @@ from paper_1910_11110_b200._ffi import COH_E_CONSTRUCTION, lib
 
 class Batch(C.Structure):  # coh_trace_batch
     _fields_ = [("records", C.c_void_p), ("n_traces", C.c_uint64), ("n_calls", C.c_uint32),
-                ("n_arrays", C.c_uint32), ("fuel", C.c_int32), ("reserved", C.c_uint32),
+                ("n_arrays", C.c_uint32), ("fuel", C.c_int32), ("flags", C.c_uint32),
                 ("array_bytes", C.c_void_p)]
 
 

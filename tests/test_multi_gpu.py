@@ -36,7 +36,7 @@ def test_comm_init_rank_allreduce_one_rank(ctx):
         comm.close()
     assert torch.equal(before, d_cnt)
     res, _ = o.orc_eval(o.orc_gen(SEED, 0, NT, NC, NA, ADV), NT, NC, NA)
-    assert np.array_equal(d_cnt.cpu().numpy().view(np.uint64)[:10], coh.counters_host(res))
+    assert np.array_equal(d_cnt.cpu().numpy().view(np.uint64)[:11], coh.counters_host(res))
 
 
 def test_eval_traces_multi_init_all(ctx):
@@ -67,7 +67,7 @@ def test_eval_traces_multi_init_all(ctx):
     got = np.concatenate([x.cpu().numpy() for x in outs])
     assert np.array_equal(got, res.view(np.uint8))
     for c in cnts:
-        assert np.array_equal(c.cpu().numpy().view(np.uint64)[:10], coh.counters_host(res))
+        assert np.array_equal(c.cpu().numpy().view(np.uint64)[:11], coh.counters_host(res))
 
 
 def test_comm_errors(ctx):

@@ -123,7 +123,7 @@ def test_fused_counters_equal_sum_of_results(ctx, cfg):
                             stream=torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     res = d_res.cpu().numpy().view(coh.RESULT_DTYPE)
-    cnt = d_cnt.cpu().numpy().view(np.uint64)[:10]
+    cnt = d_cnt.cpu().numpy().view(np.uint64)[:11]
     want, _ = o.orc_eval(recs, nt, nc, na, fuel, ab)
     assert same(res, want)
     st = want["status"]
@@ -176,10 +176,10 @@ def test_full_size_c2_properties(ctx):
     d_cnt2 = torch.zeros(16, dtype=torch.int64, device="cuda")
     ctx.reduce_counters(d_res, N, d_cnt2, s)
     torch.cuda.synchronize()
-    assert torch.equal(d_cnt[:10], d_cnt2[:10])  # fused == separate reduction
+    assert torch.equal(d_cnt[:11], d_cnt2[:11])  # fused == separate reduction
     res = d_res.cpu().numpy().view(coh.RESULT_DTYPE)
     bnd = d_bnd.cpu().numpy().view(np.uint32)
-    cnt = d_cnt.cpu().numpy().view(np.uint64)[:10]
+    cnt = d_cnt.cpu().numpy().view(np.uint64)[:11]
     # counters
     st = res["status"]
     assert cnt[0] == (st == 1).sum() and cnt[1] == (st == 2).sum() and cnt[3] == (st == 3).sum()
@@ -255,13 +255,13 @@ def test_c4_full_size_shards(ctx):
     d_cnt2 = torch.zeros(16, dtype=torch.int64, device="cuda")
     ctx.reduce_counters(d_res, N, d_cnt2, s)
     torch.cuda.synchronize()
-    assert torch.equal(d_cnt[:10], d_cnt2[:10])
+    assert torch.equal(d_cnt[:11], d_cnt2[:11])
     whole = shard.results_checksum(d_res)
     for t in range(0, N, N // 997 // 64 * 64)[:400]:  # ids = 0 mod 64 across the range
         w, _ = o.orc_eval(coh.gen_records_host(seed, t, 1, nc, na, adv), 1, nc, na, 10000)
         assert same(d_res[t * 64:(t + 1) * 64].cpu().numpy().view(coh.RESULT_DTYPE), w), t
     del d_rec
-    total, cnt_sum = 0, np.zeros(10, np.uint64)
+    total, cnt_sum = 0, np.zeros(11, np.uint64)
     for g in range(G):
         first, cnt = shard.split_range(g, G, N)
         d_r = torch.empty(coh.records_elems(cnt, nc), dtype=torch.int16, device="cuda")
@@ -272,10 +272,10 @@ def test_c4_full_size_shards(ctx):
         torch.cuda.synchronize()
         assert torch.equal(d_o, d_res[first * 64:(first + cnt) * 64])
         total = (total + shard.results_checksum(d_o)) & ((1 << 64) - 1)
-        cnt_sum += d_c.cpu().numpy().view(np.uint64)[:10]
+        cnt_sum += d_c.cpu().numpy().view(np.uint64)[:11]
         del d_r, d_o
     assert total == whole
-    assert np.array_equal(cnt_sum, d_cnt.cpu().numpy().view(np.uint64)[:10])
+    assert np.array_equal(cnt_sum, d_cnt.cpu().numpy().view(np.uint64)[:11])
     torch.cuda.empty_cache()
 
 

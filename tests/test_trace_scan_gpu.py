@@ -85,7 +85,7 @@ def test_scan_default_dispatch_and_counters(ctx):
     torch.cuda.synchronize()
     res = d_res.cpu().numpy().view(coh.RESULT_DTYPE)
     assert same(res, want)
-    cnt = d_cnt.cpu().numpy().view(np.uint64)[:10]
+    cnt = d_cnt.cpu().numpy().view(np.uint64)[:11]
     st = want["status"]
     exp = [(st == 1).sum(), (st == 2).sum(), (want["violations"] > 0).sum(), (st == 3).sum(),
            want["steps"].astype(np.uint64).sum(), want["transfers"].astype(np.uint64).sum(),
