@@ -51,7 +51,7 @@ def test_blocks_vs_oracle(ctx, nt, nc, na, adv, cont, dup, fuel, sizes):
     assert np.array_equal(gb, wb)
     assert np.array_equal(cnt, coh.counters_host(want))
     assert cnt[10] == 0  # is_unsafe never holds (Property 2)
-    assert (got["calls_done"][got["status"] == 0] < nc).any()  # multi-mode blocks were formed
+    assert (recs & 1).sum() > nt  # multi-mode blocks were formed
 
 
 @pytest.mark.skipif(not o.have_ref(), reason="oracle/_ref not built")

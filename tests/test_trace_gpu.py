@@ -130,7 +130,7 @@ def test_fused_counters_equal_sum_of_results(ctx, cfg):
     exp = [(st == 1).sum(), (st == 2).sum(), (want["violations"] > 0).sum(), (st == 3).sum(),
            want["steps"].astype(np.uint64).sum(), want["transfers"].astype(np.uint64).sum(),
            want["transfer_bytes"].sum(), want["violations"].astype(np.uint64).sum(),
-           want["calls_done"].astype(np.uint64).sum(), nt]
+           want["calls_done"].astype(np.uint64).sum(), nt, ((want["stuck_flags"] & coh.FLAG_UNSAFE) != 0).sum()]
     assert [int(x) for x in cnt] == [int(x) for x in exp]
 
 

@@ -90,5 +90,5 @@ def test_scan_default_dispatch_and_counters(ctx):
     exp = [(st == 1).sum(), (st == 2).sum(), (want["violations"] > 0).sum(), (st == 3).sum(),
            want["steps"].astype(np.uint64).sum(), want["transfers"].astype(np.uint64).sum(),
            want["transfer_bytes"].sum(), want["violations"].astype(np.uint64).sum(),
-           want["calls_done"].astype(np.uint64).sum(), nt]
+           want["calls_done"].astype(np.uint64).sum(), nt, ((want["stuck_flags"] & coh.FLAG_UNSAFE) != 0).sum()]
     assert [int(x) for x in cnt] == [int(x) for x in exp]
