@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--overlap-views", type=int, default=1 << 20, help="overlap registry views (0 = skip)")
     ap.add_argument("--overlap-blocks", type=int, default=1 << 20)
     ap.add_argument("--c4-traces", type=int, default=1 << 26, help="C4 total traces, split over the ranks (0 = skip)")
+    ap.add_argument("--checker-programs", type=int, default=20000, help="batched checker programs (0 = skip)")
     return ap.parse_args()
 
 
@@ -545,6 +546,44 @@ def run_sweep(args, ctx):
             "note": "wall includes host program generation, bytecode compile and frontier management"}
 
 
+def run_checker(args):
+    """the static checker batched over program texts on the host
+    threads (coh_cli_batch "check": parse, closure-free check, notes), gen_well_declared
+    programs; the reference's own checker (ref_cli "check", one thread) on a sample."""
+    from paper_1910_11110_b200.cli import run_cli_batch
+    from paper_1910_11110_b200.sweep import gen_program_text
+
+    srcs = [gen_program_text(s) for s in range(args.checker_programs)]
+    run_cli_batch("check", srcs[:256])  # warm
+    t0 = time.perf_counter()
+    res = run_cli_batch("check", srcs)
+    dt = time.perf_counter() - t0
+    out = {"metric": "batched static checker programs/s (host threads)", "programs": len(srcs),
+           "value": len(srcs) / dt, "unit": "programs/s", "threads": os.cpu_count(), "wall_s": dt,
+           "with_diagnostics": sum(1 for r in res if r[2] != 0)}
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+        import oracle_ffi as o
+        if o.have_ref():
+            from make_golden_cli import ref_fn
+            ref_fn()  # registers ref_cli's signature
+            R = o.reference()
+            k = min(2000, len(srcs))
+            cap = 1 << 16
+            ob, eb, code = ctypes.create_string_buffer(cap), ctypes.create_string_buffer(cap), ctypes.c_int()
+            agree = True
+            t0 = time.perf_counter()
+            for i in range(k):
+                R.ref_cli(b"check", srcs[i].encode(), 0, 0, 10000, b"", 0, ob, cap, eb, cap, ctypes.byref(code))
+                agree = agree and (ob.value.decode(), eb.value.decode(), code.value) == res[i]
+            out["cpu_reference"] = {"value": k / (time.perf_counter() - t0), "unit": "programs/s", "cores": 1,
+                                    "kind": "reference", "sample": f"first {k} programs", "agree": agree}
+    except Exception as ex:  # test infrastructure; its absence is not fatal here
+        out["cpu_reference"] = {"error": f"{type(ex).__name__}: {ex}"}
+    return out
+
+
 def run_overlap(args, ctx):
     """the batched overlap registry + closure.  1M views over 4096
     buffers of 2^20 cells (lengths up to 2^12), 1M blocks of 1-4 view modes; registry
@@ -878,6 +917,7 @@ def run_ours(args, rank, world, local):
     c1 = run_c1(ctx) if rank == 0 else None
     c4 = run_c4(args, ctx, rank, world, allreduce) if args.c4_traces > 0 else None
     overlap = run_overlap(args, ctx) if (args.overlap_views > 0 and rank == 0) else None
+    checker = run_checker(args) if (args.checker_programs > 0 and rank == 0) else None
     container = None
     if args.container_log2_floats > 0 and rank == 0:
         try:
@@ -908,6 +948,7 @@ def run_ours(args, rank, world, local):
                                             .multi_processor_count)},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
             "bitmap": bitmap, "container": container, "sweep": sweep_info, "c1": c1, "c4": c4, "overlap": overlap,
+            "checker": checker,
         }
         print(json.dumps(line), flush=True)
     if comm is not None:

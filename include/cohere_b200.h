@@ -530,6 +530,14 @@ typedef struct coh_cli_opts {
 } coh_cli_opts;
 int coh_cli(coh_ctx* ctx, const char* command, const char* src, const coh_cli_opts* opts,
             char* out, size_t out_cap, char* err, size_t err_cap, int* exit_code);
+/* Batched host passes: "check", "infer" or "translate" over n program
+ * texts on n_threads host threads (<= 0: all).  Program i's stdout is out[out_off[i] ..
+ * out_off[i+1]), its stderr err[err_off[i] .. err_off[i+1]) (offsets: n + 1 entries; the
+ * texts are not NUL-terminated), its exit code exit_codes[i] -- each exactly what coh_cli
+ * gives for it.  Returns COH_OK, COH_E_ARG, or -(needed bytes) - 1 if a buffer is short. */
+int coh_cli_batch(const char* command, const char* const* srcs, uint32_t n, const coh_cli_opts* opts,
+                  int n_threads, char* out, size_t out_cap, uint64_t* out_off, char* err, size_t err_cap,
+                  uint64_t* err_off, int* exit_codes);
 
 /* ---- batched overlap registry and mode closure -----------------
  * OverlapRegistry (overlap.hpp:33-175) and infer_overlap_closure (overlap.hpp:177-230)

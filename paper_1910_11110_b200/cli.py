@@ -27,6 +27,34 @@ def _register(L):
 
 
 _register(lib())
+lib().coh_cli_batch.restype = C.c_int
+lib().coh_cli_batch.argtypes = [C.c_char_p, C.POINTER(C.c_char_p), C.c_uint32, C.POINTER(_Opts), C.c_int, C.c_char_p,
+                                C.c_size_t, C.c_void_p, C.c_char_p, C.c_size_t, C.c_void_p, C.c_void_p]
+
+
+def run_cli_batch(command: str, srcs, raw: bool = False, json: bool = False, no_overlap: bool = False,
+                  threads: int = 0) -> list[tuple[str, str, int]]:
+    """(stdout, stderr, exit code) of `command` (check / infer / translate) for every program
+    text, evaluated on the host threads (coh_cli_batch)."""
+    import numpy as np
+
+    n = len(srcs)
+    o = _Opts(int(raw), int(json), int(no_overlap), 10000, None, 0)
+    arr = (C.c_char_p * max(1, n))(*[s.encode() for s in srcs])
+    cap = max(1 << 16, 256 * n)
+    while True:
+        out, err = C.create_string_buffer(cap), C.create_string_buffer(cap)
+        oo, eo = np.zeros(n + 1, np.uint64), np.zeros(n + 1, np.uint64)
+        codes = np.zeros(max(1, n), np.int32)
+        rc = lib().coh_cli_batch(command.encode(), arr, n, C.byref(o), threads, out, cap, oo.ctypes.data, err, cap,
+                                 eo.ctypes.data, codes.ctypes.data)
+        if rc < 0:
+            cap = -rc + 16
+            continue
+        if rc:
+            raise CohError(rc, f"coh_cli_batch({command})")
+        ob, eb = out.raw, err.raw
+        return [(ob[oo[i]:oo[i + 1]].decode(), eb[eo[i]:eo[i + 1]].decode(), int(codes[i])) for i in range(n)]
 
 
 def run_cli(command: str, src: str, ctx=None, raw: bool = False, json: bool = False, no_overlap: bool = False,

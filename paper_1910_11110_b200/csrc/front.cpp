@@ -16,12 +16,14 @@
 //     single must-write set analysis for scalars and cells (checker.hpp:16-318);
 //   * printers share one traversal for the one-line and the indented form (pretty.hpp).
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <map>
 #include <set>
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <thread>
 #include <tuple>
 #include <unordered_map>
 #include <utility>
@@ -1224,6 +1226,24 @@ void copy_out(const std::string& s, char* buf, size_t cap) {
   buf[n] = '\0';
 }
 
+// One command on one program text, every exception class mapped to its exit code
+// (tools/cohere_main.cpp:262-274).  Returns COH_OK or a COH_E_* with *fatal set.
+int one_command(coh_ctx* ctx, const std::string& cmd, std::string_view src, const coh_cli_opts& opt, Outcome& o,
+                std::string* fatal) {
+  int rc = COH_OK;
+  try {
+    if (opt.fuel < 1) throw DeclError("--fuel: value must be positive");
+    rc = command(ctx, cmd, src, opt, o, fatal);
+  } catch (const ConflictError& e) {
+    o.err += std::string("error: ") + e.what() + "\n";
+    o.exit = 1;
+  } catch (const std::exception& e) {  // SyntaxError, DeclError, std::out_of_range, ...
+    o.err += std::string("error: ") + e.what() + "\n";
+    o.exit = 2;
+  }
+  return rc;
+}
+
 }  // namespace front
 }  // namespace cohb
 
@@ -1234,17 +1254,7 @@ extern "C" int coh_cli(coh_ctx* ctx, const char* cmd, const char* src, const coh
   const coh_cli_opts opt = opts ? *opts : coh_cli_opts{0, 0, 0, 10000, nullptr, 0};
   Outcome o;
   std::string fatal;
-  int rc = COH_OK;
-  try {  // exception classes -> exit codes (tools/cohere_main.cpp:262-274)
-    if (opt.fuel < 1) throw DeclError("--fuel: value must be positive");
-    rc = command(ctx, cmd, src, opt, o, &fatal);
-  } catch (const ConflictError& e) {
-    o.err += std::string("error: ") + e.what() + "\n";
-    o.exit = 1;
-  } catch (const std::exception& e) {  // SyntaxError, DeclError, std::out_of_range, ...
-    o.err += std::string("error: ") + e.what() + "\n";
-    o.exit = 2;
-  }
+  const int rc = one_command(ctx, cmd, src, opt, o, &fatal);
   if (rc != COH_OK) {
     if (ctx) ctx->err = fatal;
     copy_out(fatal, err, err_cap);
@@ -1254,4 +1264,52 @@ extern "C" int coh_cli(coh_ctx* ctx, const char* cmd, const char* src, const coh
   copy_out(o.err, err, err_cap);
   *exit_code = o.exit;
   return (o.out.size() >= out_cap || o.err.size() >= err_cap) ? -(int)std::max(o.out.size(), o.err.size()) - 1 : COH_OK;
+}
+
+// Batched host passes: check / infer / translate over many program
+// texts on the host threads -- the reference's checker is a per-program syntactic pass
+// (checker.hpp:217-300), so the batch is its data-parallel unit.  Per program the same
+// stdout / stderr text and exit code as coh_cli, concatenated into out / err with offsets
+// (n + 1 entries each).  Returns COH_OK, COH_E_ARG (run / trace need coh_cli), or
+// -(needed bytes of the larger buffer) - 1 when out or err is too small.
+extern "C" int coh_cli_batch(const char* cmd, const char* const* srcs, uint32_t n, const coh_cli_opts* opts,
+                             int n_threads, char* out, size_t out_cap, uint64_t* out_off, char* err, size_t err_cap,
+                             uint64_t* err_off, int* exit_codes) {
+  using namespace cohb::front;
+  if (!cmd || (n && (!srcs || !out_off || !err_off || !exit_codes))) return COH_E_ARG;
+  const std::string command_name = cmd;
+  if (command_name != "check" && command_name != "infer" && command_name != "translate") return COH_E_ARG;
+  const coh_cli_opts opt = opts ? *opts : coh_cli_opts{0, 0, 0, 10000, nullptr, 0};
+  std::vector<Outcome> res(n);
+  std::vector<int> rcs(n, COH_OK);
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned nth = std::max(1u, std::min<unsigned>(n_threads > 0 ? (unsigned)n_threads : hw, n ? n : 1u));
+  std::atomic<uint32_t> next{0};
+  auto worker = [&] {
+    for (uint32_t i; (i = next.fetch_add(1)) < n;) {
+      std::string fatal;
+      rcs[i] = one_command(nullptr, command_name, srcs[i] ? srcs[i] : "", opt, res[i], &fatal);
+      if (rcs[i] != COH_OK) res[i].err = fatal;
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned k = 1; k < nth; ++k) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
+  size_t need_out = 0, need_err = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (rcs[i] != COH_OK) return rcs[i];
+    out_off[i] = need_out;
+    err_off[i] = need_err;
+    need_out += res[i].out.size();
+    need_err += res[i].err.size();
+    exit_codes[i] = res[i].exit;
+  }
+  if (n) out_off[n] = need_out, err_off[n] = need_err;
+  if (need_out > out_cap || need_err > err_cap) return -(int)std::min<size_t>(std::max(need_out, need_err), 0x7FFFFFFE) - 1;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!res[i].out.empty()) std::memcpy(out + out_off[i], res[i].out.data(), res[i].out.size());
+    if (!res[i].err.empty()) std::memcpy(err + err_off[i], res[i].err.data(), res[i].err.size());
+  }
+  return COH_OK;
 }

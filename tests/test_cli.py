@@ -158,3 +158,24 @@ def test_run_wide_programs_match_live_reference(ctx):
         out, err, code = run_cli(cmd, src, ctx, raw=bool(raw), json=True, schedule=sched or None)
         assert code == ref(cmd, src, raw, 0, 10000, sched)["exit"]
         assert all(line.startswith("{") for line in out.splitlines())
+
+
+def test_batched_host_passes_match_reference():
+    """coh_cli_batch (the batched checker): every host case of the
+    reference-made corpus, grouped by command and flags and evaluated on the host threads,
+    gives the reference's bytes and exit codes."""
+    from paper_1910_11110_b200.cli import run_cli_batch
+    groups = {}
+    for c in CASES:
+        if c["cmd"] in ("check", "infer", "translate"):
+            groups.setdefault((c["cmd"], bool(c["raw"]), bool(c["no_overlap"])), []).append(c)
+    n = 0
+    for (cmd, raw, no_ovl), cs in groups.items():
+        got_all = run_cli_batch(cmd, [c["src"] for c in cs], raw=raw, no_overlap=no_ovl)
+        for c, g in zip(cs, got_all):
+            assert g == want(c), (cmd, c["src"])
+        n += len(cs)
+    assert n > 2000
+    from paper_1910_11110_b200 import CohError
+    with pytest.raises(CohError):
+        run_cli_batch("run", ["scalar x\n"])

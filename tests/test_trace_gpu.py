@@ -257,9 +257,19 @@ def test_c4_full_size_shards(ctx):
     torch.cuda.synchronize()
     assert torch.equal(d_cnt[:11], d_cnt2[:11])
     whole = shard.results_checksum(d_res)
-    for t in range(0, N, N // 997 // 64 * 64)[:400]:  # ids = 0 mod 64 across the range
-        w, _ = o.orc_eval(coh.gen_records_host(seed, t, 1, nc, na, adv), 1, nc, na, 10000)
-        assert same(d_res[t * 64:(t + 1) * 64].cpu().numpy().view(coh.RESULT_DTYPE), w), t
+    # SURVEY §8(d) C4 parity sample: every id = 0 (mod 64), 1M traces, against the C oracle
+    # (all of them) and the reference itself (run_annotated over its std::map store, a
+    # 32K-trace subset on the host threads); the records of the sample are cut out of the
+    # device buffer (chunk-major layout: [chunk][trace][8])
+    samp_rec = d_rec.view(-1, N, 8)[:, ::64, :].contiguous().cpu().numpy().view(np.uint16).reshape(-1)
+    samp_res = d_res.view(N, 64)[::64].contiguous().cpu().numpy().view(coh.RESULT_DTYPE)
+    ns = N // 64
+    w, _ = o.orc_eval(samp_rec, ns, nc, na, 10000)
+    assert same(samp_res, w)
+    if o.have_ref():
+        m = 1 << 15
+        wr, _ = o.ref_eval(samp_rec, ns, nc, na, 10000, t_begin=0, t_end=m)
+        assert same(samp_res[:m], wr)
     del d_rec
     total, cnt_sum = 0, np.zeros(11, np.uint64)
     for g in range(G):
