@@ -486,13 +486,18 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
     }
 #undef COH_SLOT_OUT
     {  // is_unsafe (program.hpp:166-170): a live array whose concrete or abstract pair is (I,I)
+      // (bit 0 / bit 2 of ~(nibble | nibble >> 1)); arrays >= n_arrays hold nibble 0
       uint32_t bad = 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t live = 8 * k + 8 <= (int)p.n_arrays ? 0x55555555u
-                              : 8 * k >= (int)p.n_arrays  ? 0u
-                                                          : 0x55555555u & ((1u << (4 * (p.n_arrays - 8 * k))) - 1u);
-        bad |= ~(sw[k] | (sw[k] >> 1)) & live;
+      for (int k = 0; k < 8; ++k) bad |= ~(sw[k] | (sw[k] >> 1)) & 0x55555555u;
+      if (bad && p.n_arrays < COH_MAX_ARRAYS) {  // (rare) mask the undeclared arrays' empty nibbles
+        bad = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {  // constant word indices: sw stays in registers
+          const int live = (int)p.n_arrays - 8 * k;  // arrays of word k that are declared
+          const uint32_t m = live >= 8 ? 0x55555555u : live <= 0 ? 0u : 0x55555555u & ((1u << (4 * live)) - 1u);
+          bad |= ~(sw[k] | (sw[k] >> 1)) & m;
+        }
       }
       if (bad) stuck_flags |= COH_FLAG_UNSAFE;
     }

@@ -262,7 +262,7 @@ def test_c4_full_size_shards(ctx):
     # 32K-trace subset on the host threads); the records of the sample are cut out of the
     # device buffer (chunk-major layout: [chunk][trace][8])
     samp_rec = d_rec.view(-1, N, 8)[:, ::64, :].contiguous().cpu().numpy().view(np.uint16).reshape(-1)
-    samp_res = d_res.view(N, 64)[::64].contiguous().cpu().numpy().view(coh.RESULT_DTYPE)
+    samp_res = d_res.view(N, 64)[::64].contiguous().cpu().numpy().reshape(-1).view(coh.RESULT_DTYPE)
     ns = N // 64
     w, _ = o.orc_eval(samp_rec, ns, nc, na, 10000)
     assert same(samp_res, w)
