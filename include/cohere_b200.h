@@ -235,6 +235,22 @@ int coh_eval_traces_multi(coh_comm* const* comms, int n_dev, const coh_trace_bat
 int coh_shard_split(uint32_t rank, uint32_t world, uint64_t total, uint64_t* first, uint64_t* count);
 int coh_counters_host(const coh_trace_result* results, uint64_t n_traces, uint64_t* counters);
 
+/* TraceMode::Full for one trace (semantics.hpp:231-235, 279-280): every reduction step of
+ * run_annotated over the trace's blocks (records in plain call order, one trace; flags
+ * as coh_trace_batch.flags), run on the device.  Per step: the record it belongs to, the
+ * rule (cohere::StepRule ordinal: 0 effect, 1 remote-effect, 4 if-true, 5 if-false), the
+ * head statement and the key it changed.  *status = the run's COH_RUN_*.  Returns COH_OK,
+ * or -(steps) - 1 when cap was too small (the first cap steps are written). */
+typedef struct coh_trace_step {
+  uint32_t call;   /* record index                                                      */
+  uint8_t rule;    /* StepRule                                                          */
+  uint8_t array;   /* the array of the head statement                                   */
+  uint8_t head;    /* effect | site << 3 | abstract target << 4; if-steps 0x80 | gvalid  */
+  uint8_t delta;   /* bit 4: a key changed; bit 2 it is the abstract key; bits 0-1 its pair */
+} coh_trace_step;
+int coh_trace_steps(coh_ctx* ctx, const uint16_t* records, uint32_t n_calls, uint32_t n_arrays, int32_t fuel,
+                    uint32_t flags, coh_trace_step* steps, uint32_t cap, uint32_t* n_steps, uint32_t* status);
+
 /* Kernels launched by this ctx since creation (the bench's gpu_launches claim). */
 uint64_t coh_launch_count(const coh_ctx* ctx);
 

@@ -265,6 +265,66 @@ extern "C" {
 // Evaluate traces [t_begin, t_end) of a record set laid out for n_total traces.
 // out / boundary are indexed relative to t_begin; boundary is word-major
 // [(i/32) * (t_end - t_begin) + (t - t_begin)] (may be NULL).  Returns 0 or -1.
+// The reference's TraceMode::Full step list for one trace (records in plain call order),
+// in coh_trace_step form: run (semantics.hpp:253-287) per block with the trace's shared
+// fuel, each TraceStep's rule, head statement and delta (at most one key here).
+int ref_trace_steps(const uint16_t* recs, uint32_t n_calls, uint32_t n_arrays, int32_t fuel, uint32_t flags,
+                    coh_trace_step* out, uint32_t cap, uint32_t* n_steps, uint32_t* status_out) {
+  try {
+    Declarations decls;
+    for (uint32_t a = 0; a < n_arrays; ++a) decls.add_scalar({array_names()[a], {}});
+    Store store = initial_store(decls);
+    int steps = 0;
+    uint32_t n = 0;
+    RunStatus status = RunStatus::Done;
+    bool defect = false;
+    for (uint32_t b0 = 0; b0 < n_calls;) {
+      uint32_t b1 = b0 + 1;
+      if (flags & COH_BATCH_BLOCKS)
+        while (b1 < n_calls && (recs[b1] & COH_REC_CONT)) ++b1;
+      DeclBlock block;
+      uint32_t bad = 0;
+      if (!make_multi_block(decls, recs, 1, 0, b0, b1, n_arrays, &block, &bad)) {  // one trace, plain order
+        defect = true;
+        break;
+      }
+      RunResult rr = run(translate_block(block, decls), std::move(store), fuel - steps, Schedule(), TraceMode::Full);
+      store = std::move(rr.store);
+      steps += rr.steps;
+      status = rr.status;
+      for (const auto& ts : rr.trace) {
+        coh_trace_step st{};
+        const auto& h = ts.head.node();
+        std::string name;
+        if (ts.head.op() == Stmt::Op::If) {
+          name = h.cond.key.name;
+          st.head = (uint8_t)(0x80u | (h.cond.kind == Condition::Kind::RemIsValid ? 1u : 0u));
+        } else {
+          name = h.target.name;
+          st.head = (uint8_t)((uint32_t)h.effect | ((h.site == Site::Remote ? 1u : 0u) << 3) |
+                              ((h.target.kind == Target::Kind::Abstract ? 1u : 0u) << 4));
+        }
+        st.array = (uint8_t)std::stoi(name.substr(1));
+        for (uint32_t i = b0; i < b1; ++i)  // arrays are distinct within a block
+          if (COH_REC_ARRAY(recs[i]) == st.array) st.call = i;
+        st.rule = (uint8_t)ts.rule;
+        if (!ts.delta.empty())
+          st.delta = (uint8_t)(0x10u | ((ts.delta[0].first.kind == VarKey::Kind::Abstract ? 1u : 0u) << 2) |
+                               pair_bits(ts.delta[0].second));
+        if (n < cap) out[n] = st;
+        ++n;
+      }
+      if (rr.status != RunStatus::Done) break;
+      b0 = b1;
+    }
+    *n_steps = n;
+    *status_out = defect && status == RunStatus::Done ? (uint32_t)COH_RUN_DEFECT : (uint32_t)status;
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+
 // mode 2: COH_BATCH_BLOCKS (records with COH_REC_CONT continue the previous block).
 int ref_eval_traces(const uint16_t* records, uint64_t n_total, uint64_t t_begin, uint64_t t_end,
                     uint32_t n_calls, uint32_t n_arrays, int32_t fuel, const uint64_t* array_bytes,

@@ -37,6 +37,9 @@ RESULT_DTYPE = np.dtype(
 )
 assert RESULT_DTYPE.itemsize == 64
 
+STEP_DTYPE = np.dtype([("call", "<u4"), ("rule", "u1"), ("array", "u1"), ("head", "u1"), ("delta", "u1")])
+assert STEP_DTYPE.itemsize == 8
+
 COUNTER_NAMES = (
     "stuck_traces",
     "fuel_exhausted_traces",
@@ -130,6 +133,7 @@ def lib():
                                           C.POINTER(vp)]),
             "coh_shard_split": (i, [u32, u32, u64, C.POINTER(u64), C.POINTER(u64)]),
             "coh_counters_host": (i, [vp, u64, vp]),
+            "coh_trace_steps": (i, [vp, vp, u32, u32, i32, u32, vp, u32, C.POINTER(u32), C.POINTER(u32)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -284,6 +288,19 @@ class Context:
             "coh_eval_traces_host",
         )
         return results, boundary
+
+    def trace_steps(self, records: np.ndarray, n_calls: int, n_arrays: int, fuel: int = 10000, flags: int = 0,
+                    cap: int = 1 << 16):
+        """TraceMode::Full for one trace (coh_trace_steps): (steps, status); records in call
+        order.  steps is a STEP_DTYPE array (call, rule, array, head, delta)."""
+        r = np.ascontiguousarray(records, dtype=np.uint16)
+        out = np.zeros(cap, STEP_DTYPE)
+        n, st = C.c_uint32(), C.c_uint32()
+        rc = self._L.coh_trace_steps(self._h, r.ctypes.data, n_calls, n_arrays, fuel, flags, out.ctypes.data, cap,
+                                     C.byref(n), C.byref(st))
+        if rc > 0:
+            self._check(rc, "coh_trace_steps")
+        return out[: min(n.value, cap)], st.value
 
     def measure_link(self, nbytes: int, reps: int = 3) -> tuple[float, float]:
         h2d, d2h = C.c_double(), C.c_double()

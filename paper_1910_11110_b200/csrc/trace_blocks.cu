@@ -24,50 +24,14 @@ constexpr int kBT = 128;  // traces per block
 
 __device__ __forceinline__ uint32_t swap_pair(uint32_t p) { return ((p & 1u) << 1) | ((p >> 1) & 1u); }
 
-// validity.hpp:79-120 on one pair, remote = swap-apply-swap (semantics.hpp:109-130); -1 = stuck
-__device__ __forceinline__ int apply_cell(uint32_t eff, uint32_t site, uint32_t p) {
-  const uint32_t q = site ? swap_pair(p) : p;
-  int r;
-  switch (eff) {
-    case COH_PUSH: r = (q & 1u) ? 3 : -1; break;
-    case COH_PULL: r = (q & 2u) ? 3 : -1; break;
-    case COH_READ: r = (q & 1u) ? (int)q : -1; break;
-    case COH_WRITE: r = 1; break;
-    default: r = (int)q; break;
-  }
-  return r < 0 ? -1 : (int)(site ? swap_pair((uint32_t)r) : (uint32_t)r);
-}
-
 __device__ __forceinline__ uint32_t violating(uint32_t nib) {  // !leq(abstract, concrete)
   const uint32_t c = nib & 3u, a = (nib >> 2) & 3u;
   return !(a == c || (c == 3u && (a == 1u || a == 2u)));
 }
 
-// The body of one record (DESIGN.md §3 variants): op k as (effect, site); returns the count.
-__device__ __forceinline__ uint32_t body_op(uint32_t kind, uint32_t site, uint32_t variant, uint32_t k,
-                                            uint32_t* eff, uint32_t* s) {
-  const uint32_t S = site, O = site ^ 1u;
-  uint32_t n = 0, e0 = 0, s0 = 0, e1 = 0, s1 = 0;
-  switch (variant) {
-    case 0:
-      if (kind == COH_R) n = 1, e0 = COH_READ, s0 = S;
-      else if (kind == COH_W) n = 1, e0 = COH_WRITE, s0 = S;
-      else n = 2, e0 = COH_READ, s0 = S, e1 = COH_WRITE, s1 = S;
-      break;
-    case 1: break;
-    case 2: n = 1, e0 = COH_READ, s0 = O; break;
-    case 3: n = 1, e0 = COH_WRITE, s0 = O; break;
-    case 4: n = 1, e0 = COH_READ, s0 = S; break;
-    case 5: n = 2, e0 = COH_WRITE, s0 = S, e1 = COH_READ, s1 = O; break;
-    case 6: n = 1, e0 = COH_PUSH, s0 = S; break;
-    default: n = 2, e0 = COH_PULL, s0 = S, e1 = COH_WRITE, s1 = O; break;
-  }
-  *eff = k ? e1 : e0;
-  *s = k ? s1 : s0;
-  return n;
-}
-
 struct BlocksParams {
+  uint64_t prog[kCallTypes];  // per call type: its translated block as micro-ops (calltable.cpp
+                              // block_ops, one byte each: guard ops first, then the body)
   const uint16_t* rec;
   uint64_t n_traces;
   uint32_t n_calls, n_arrays;
@@ -116,43 +80,40 @@ __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
       status = COH_RUN_DEFECT;
       break;
     }
-    // translate_block: the guards of every mode (phase 0), then every body (phase 1)
+    // translate_block: the guards of every mode (phase 0), then every body (phase 1).
+    // Each record's translated block is its type's micro-op program (guard ops first);
+    // every op is decoded the same way, so lanes on different calls stay converged.
     bool stop = false;
     for (uint32_t phase = 0; phase < 2 && !stop; ++phase) {
       for (uint32_t i = b0; i < b1 && !stop; ++i) {
-        const uint32_t r = rec(i), a = COH_REC_ARRAY(r), kind = COH_REC_KIND(r), site = COH_REC_SITE(r);
-        uint32_t nops;
-        if (phase == 0) nops = (kind == COH_R ? 3u : kind == COH_W ? 1u : 4u);
-        else {
-          uint32_t e_, s_;
-          nops = body_op(kind, site, COH_REC_VARIANT(r), 0, &e_, &s_);
-        }
-        for (uint32_t k = 0; k < nops; ++k) {
+        const uint32_t r = rec(i), a = COH_REC_ARRAY(r), kind = COH_REC_KIND(r);
+        const uint64_t prog = p.prog[COH_REC_TYPE(r)];
+        const uint32_t n_guard = kind == COH_R ? 3u : kind == COH_W ? 1u : 4u;
+        uint32_t n_all = 0;
+        while (n_all < 8u && ((prog >> (8u * n_all)) & 0xFFu)) ++n_all;
+        const uint32_t k0 = phase ? n_guard : 0u, k1 = phase ? n_all : n_guard;
+        uint32_t nib = st[a][tid];
+        for (uint32_t k = k0; k < k1; ++k) {
           if ((int32_t)steps >= p.fuel) {  // an op remains: Done was not reached
             status = COH_RUN_FUEL_EXHAUSTED;
             stuck_arr = COH_REC_ARRAY(rec(b0));
             stop = true;
             break;
           }
-          uint32_t nib = st[a][tid];
-          uint32_t eff, esite, abstract;
-          if (phase == 0 && kind != COH_W && k == 0) {  // if (valid(x^)) / if (gvalid(x^)): one step
+          const uint32_t op = (uint32_t)(prog >> (8u * k)) & 0xFFu, kop = op & 3u;
+          if (kop != OP_EFFECT) {  // if (valid(x^)) / if (gvalid(x^)): one step; valid skips the two syncs
             ++steps;
-            if ((nib >> (2u + site)) & 1u) k = 2;  // flag valid: skip the two syncs
+            if ((nib >> (1u + kop)) & 1u) k += 2;
             continue;
           }
-          if (phase == 0) {
-            const bool w_op = kind == COH_W || k == 3;  // w x^ at the mode's site
-            eff = w_op ? COH_WRITE : (site ? COH_PUSH : COH_PULL);
-            esite = w_op ? site : COH_LOCAL;
-            abstract = w_op || k == 2;  // the guard's second sync is on x^
-          } else {
-            body_op(kind, site, COH_REC_VARIANT(r), k, &eff, &esite);
-            abstract = 0;
-          }
+          const uint32_t eff = (op >> 2) & 7u, esite = (op >> 5) & 1u, abstract = (op >> 6) & 1u;
           const uint32_t pair = abstract ? (nib >> 2) & 3u : nib & 3u;
-          const int after = apply_cell(eff, esite, pair);
-          if (after < 0) {
+          // validity.hpp:79-120 with the remote swap (semantics.hpp:109-130), branch-free
+          const uint32_t q = esite ? swap_pair(pair) : pair;
+          const bool sync = eff == COH_PUSH || eff == COH_PULL;
+          const uint32_t ok = eff == COH_PUSH ? (q & 1u) : eff == COH_PULL ? (q >> 1) : eff == COH_READ ? (q & 1u) : 1u;
+          const uint32_t rq = sync ? 3u : eff == COH_READ ? q : eff == COH_WRITE ? 1u : q;
+          if (!ok) {
             status = COH_RUN_STUCK;
             stuck_arr = a;
             stuck_eff = eff;
@@ -160,15 +121,17 @@ __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
             stop = true;
             break;
           }
-          const uint32_t nn = abstract ? ((nib & 3u) | ((uint32_t)after << 2)) : ((nib & 12u) | (uint32_t)after);
+          const uint32_t after = esite ? swap_pair(rq) : rq;
+          const uint32_t nn = abstract ? ((nib & 3u) | (after << 2)) : ((nib & 12u) | after);
           viol += violating(nn) - violating(nib);
-          st[a][tid] = (uint8_t)nn;
+          nib = nn;
           ++steps;
-          if (!abstract && (eff == COH_PUSH || eff == COH_PULL)) {
+          if (!abstract && sync) {
             ++xfers;
             tbytes += bytes_of(a);
           }
         }
+        st[a][tid] = (uint8_t)nib;
       }
     }
     if (stop) break;
@@ -217,6 +180,12 @@ __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
 
 int launch_trace_blocks(const TraceLaunch& L, void* stream, std::string* err) {
   BlocksParams p;
+  for (uint32_t t = 0; t < (uint32_t)kCallTypes; ++t) {  // the host call-table compiler's programs
+    uint8_t ops[8];
+    const int n = coh_calltable_program(t, ops);
+    p.prog[t] = 0;
+    for (int k = 0; k < n && k < 8; ++k) p.prog[t] |= (uint64_t)ops[k] << (8 * k);
+  }
   p.rec = L.records;
   p.n_traces = L.n_traces;
   p.n_calls = L.n_calls;

@@ -212,3 +212,19 @@ def add_blocks(records, n_traces, n_calls, cont_per1024, seed, dup_per1024=0):
             else:
                 cur = {a}
     return r.reshape(-1)
+
+
+STEP_DTYPE = np.dtype([("call", "<u4"), ("rule", "u1"), ("array", "u1"), ("head", "u1"), ("delta", "u1")])
+
+
+def ref_trace_steps(records, n_calls, n_arrays, fuel=10000, flags=0, cap=1 << 16):
+    """The reference's TraceMode::Full step list of one trace (records in call order)."""
+    L = reference()
+    L.ref_trace_steps.restype = C.c_int
+    L.ref_trace_steps.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_int32, C.c_uint32, C.c_void_p, C.c_uint32,
+                                  C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+    out = np.zeros(cap, STEP_DTYPE)
+    n, st = C.c_uint32(), C.c_uint32()
+    r = np.ascontiguousarray(records, dtype=np.uint16)
+    assert L.ref_trace_steps(r.ctypes.data, n_calls, n_arrays, fuel, flags, out.ctypes.data, cap, C.byref(n), C.byref(st)) == 0
+    return out[: min(n.value, cap)], st.value
