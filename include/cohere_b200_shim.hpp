@@ -128,21 +128,48 @@ inline AnnotatedProgram decode_records(const std::vector<uint16_t>& recs, uint32
   return p;
 }
 
-// run_annotated (modes.hpp:105) for many whole-array programs in one device batch.  All
-// programs must encode to the same number of records (one trace each); fuel is shared
-// across each program's blocks as in the reference.
+// run_annotated (modes.hpp:105) for many whole-array programs: one device batch per
+// distinct record count (a batch's traces share their length); fuel is shared across each
+// program's blocks as in the reference.
+inline std::vector<AnnotatedRun> run_annotated_batch(coh_ctx* ctx, const std::vector<AnnotatedProgram>& progs,
+                                                     int fuel);
+
+namespace detail {
+inline void run_same_length(coh_ctx* ctx, const std::vector<AnnotatedProgram>& all, const std::vector<size_t>& idx,
+                            const std::vector<std::vector<uint16_t>>& enc, uint32_t arrays, int fuel,
+                            std::vector<AnnotatedRun>& result);
+}  // namespace detail
+
 inline std::vector<AnnotatedRun> run_annotated_batch(coh_ctx* ctx, const std::vector<AnnotatedProgram>& progs,
                                                      int fuel) {
-  const uint64_t n = progs.size();
-  std::vector<std::vector<uint16_t>> tr(n);
-  uint32_t calls = 0, arrays = 1;
-  for (uint64_t t = 0; t < n; ++t) {
+  std::vector<std::vector<uint16_t>> enc(progs.size());
+  std::vector<std::pair<size_t, std::vector<size_t>>> groups;  // record count -> programs
+  uint32_t arrays = 1;
+  for (size_t t = 0; t < progs.size(); ++t) {
     uint32_t na = 0;
-    const std::string why = encode_program(progs[t], &tr[t], &na);
+    const std::string why = encode_program(progs[t], &enc[t], &na);
     if (!why.empty()) throw std::invalid_argument("program " + std::to_string(t) + ": " + why);
-    if (t && tr[t].size() != calls) throw std::invalid_argument("programs of different lengths");
-    calls = (uint32_t)tr[t].size();
     arrays = na > arrays ? na : arrays;
+    size_t g = 0;
+    while (g < groups.size() && groups[g].first != enc[t].size()) ++g;
+    if (g == groups.size()) groups.push_back({enc[t].size(), {}});
+    groups[g].second.push_back(t);
+  }
+  std::vector<AnnotatedRun> out(progs.size());
+  for (const auto& grp : groups) detail::run_same_length(ctx, progs, grp.second, enc, arrays, fuel, out);
+  return out;
+}
+
+inline void detail::run_same_length(coh_ctx* ctx, const std::vector<AnnotatedProgram>& all,
+                                    const std::vector<size_t>& idx, const std::vector<std::vector<uint16_t>>& enc,
+                                    uint32_t arrays, int fuel, std::vector<AnnotatedRun>& result) {
+  const uint64_t n = idx.size();
+  const uint32_t calls = n ? (uint32_t)enc[idx[0]].size() : 0u;
+  std::vector<AnnotatedProgram> progs;
+  std::vector<std::vector<uint16_t>> tr;
+  for (size_t k : idx) {
+    progs.push_back(all[k]);
+    tr.push_back(enc[k]);
   }
   std::vector<uint16_t> rec(coh_records_elems(n, calls));
   for (uint64_t t = 0; t < n; ++t)
@@ -152,10 +179,9 @@ inline std::vector<AnnotatedRun> run_annotated_batch(coh_ctx* ctx, const std::ve
   std::vector<uint32_t> bnd((size_t)coh_boundary_words(calls) * n);
   if (n && coh_eval_traces_host(ctx, &b, res.data(), bnd.data()) != COH_OK)
     throw std::runtime_error(coh_last_error(ctx));
-  std::vector<AnnotatedRun> out(n);
   for (uint64_t t = 0; t < n; ++t) {
     const coh_trace_result& r = res[t];
-    AnnotatedRun& ar = out[t];
+    AnnotatedRun& ar = result[idx[t]];
     if (r.status == COH_RUN_DEFECT) throw std::logic_error("program " + std::to_string(t) + ": defect");
     ar.status = static_cast<RunStatus>(r.status);
     ar.steps = (int)r.steps;
@@ -179,7 +205,6 @@ inline std::vector<AnnotatedRun> run_annotated_batch(coh_ctx* ctx, const std::ve
       ar.stuck = s;
     }
   }
-  return out;
 }
 
 }  // namespace cohere::b200
