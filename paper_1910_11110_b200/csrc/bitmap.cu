@@ -439,10 +439,7 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
       uint4 v[kRU];
 #pragma unroll
       for (int u = 0; u < kRU; ++u) v[u] = __ldcg(reinterpret_cast<const uint4*>(words) + qb + 32ull * u);
-      // the word after the iteration (the last step's right neighbour), loaded with the
-      // quads so its latency is not paid a second time (the iteration is interior, so it
-      // exists inside the range)
-      const uint32_t w_after = __ldg(words + (qa0 + base + 32ull * kRU) * 4);
+
 #pragma unroll
       for (int u = 0; u < kRU; ++u) {
         const uint32_t a4 = v[u].x & v[u].y & v[u].z & v[u].w;
@@ -452,7 +449,8 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
         const uint64_t q0 = qa0 + base + 32ull * u;  // lane 0's quad
         const uint32_t pw0 = u ? __shfl_sync(0xFFFFFFFFu, v[u ? u - 1 : 0].w, 31)
                                : (carry_ok ? carry : __ldg(words + q0 * 4 - 1));
-        const uint32_t nw31 = u < kRU - 1 ? __shfl_sync(0xFFFFFFFFu, v[u < kRU - 1 ? u + 1 : 0].x, 0) : w_after;
+        const uint32_t nw31 = u < kRU - 1 ? __shfl_sync(0xFFFFFFFFu, v[u < kRU - 1 ? u + 1 : 0].x, 0)
+                                         : __ldg(words + (q0 + 32) * 4);
         if (__all_sync(0xFFFFFFFFu, (v[u].x | v[u].y | v[u].z | v[u].w) == 0u) && !((pw0 >> 31) | (nw31 & 1u)))
           continue;  // one zero run continues through the step
         uint32_t pw = __shfl_up_sync(0xFFFFFFFFu, v[u].w, 1);
