@@ -306,9 +306,11 @@ typedef struct coh_elem_program {
   uint32_t pad;
 } coh_elem_program;
 
-/* Word w of the fragmentation mask: the AND of frag_log2 32-bit draws, so each cell is
- * set with probability 2^-frag_log2.  Draw 0 is a murmur3 finalizer of the seed and the
- * word index, draw j+1 a xorshift32 step of draw j. */
+/* Word w of the fragmentation mask (each cell set with probability 2^-frag_log2).  Draw 0
+ * is a murmur3 finalizer of the seed and the word index.  frag_log2 <= 5: the AND of
+ * frag_log2 draws (draw j+1 = a xorshift32 step of draw j), cells independent.
+ * frag_log2 > 5: at most one cell per word -- cell (x & 31) iff the top frag_log2 - 5 bits
+ * of draw 0 are all ones (probability 2^-(frag_log2-5) per word, 2^-frag_log2 per cell). */
 static inline uint32_t coh_frag_mask(uint64_t frag_seed, uint32_t frag_log2, uint32_t w) {
   if (frag_log2 == 0) return 0u;
   uint32_t x = ((uint32_t)frag_seed ^ (w * 0x9E3779B9u)) + (uint32_t)(frag_seed >> 32);
@@ -317,8 +319,12 @@ static inline uint32_t coh_frag_mask(uint64_t frag_seed, uint32_t frag_log2, uin
   x ^= x >> 13;
   x *= 0xC2B2AE35u;
   x ^= x >> 16;
+  if (frag_log2 > 5) {
+    const uint32_t t = frag_log2 - 5;  /* 1..27 */
+    return (x >> (32u - t)) == ((1u << t) - 1u) ? 1u << (x & 31u) : 0u;
+  }
   uint32_t m = x;
-  for (uint32_t j = 1; j < frag_log2 && m; ++j) {
+  for (uint32_t j = 1; j < frag_log2; ++j) {
     x ^= x << 13;
     x ^= x >> 17;
     x ^= x << 5;

@@ -595,33 +595,15 @@ __global__ void __launch_bounds__(256) k_elem_init(uint32_t* planes, uint32_t W,
   uint4* const L4 = reinterpret_cast<uint4*>(planes + (size_t)b * 2u * W);
   uint4* const R4 = L4 + W / 4u;
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < W / 4u; q += gridDim.x * blockDim.x) {
-    uint32_t l[4], r[4] = {0u, 0u, 0u, 0u}, x[4];
+    uint32_t l[4], r[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint32_t w = 4u * q + k;
       l[k] = (w + 1) * 32u <= n ? 0xFFFFFFFFu : (w * 32u < n ? (0xFFFFFFFFu >> (32u - (n - w * 32u))) : 0u);
     }
-    if (pi.y) {  // coh_frag_mask of the four words, their draw chains stepped together
+    if (pi.y) {  // coh_frag_mask of the four words (one draw each when rho <= 2^-6)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        uint32_t v = ((uint32_t)seed ^ ((4u * q + k) * 0x9E3779B9u)) + (uint32_t)(seed >> 32);
-        v ^= v >> 16;
-        v *= 0x85EBCA6Bu;
-        v ^= v >> 13;
-        v *= 0xC2B2AE35u;
-        v ^= v >> 16;
-        x[k] = v;
-        r[k] = v & l[k];
-      }
-      for (uint32_t j = 1; j < pi.y && (r[0] | r[1] | r[2] | r[3]); ++j) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {  // an emptied mask stays empty: stepping it is harmless
-          x[k] ^= x[k] << 13;
-          x[k] ^= x[k] >> 17;
-          x[k] ^= x[k] << 5;
-          r[k] &= x[k];
-        }
-      }
+      for (int k = 0; k < 4; ++k) r[k] = l[k] ? coh_frag_word(seed, pi.y, 4u * q + k) & l[k] : 0u;
     }
     __stcg(L4 + q, make_uint4(l[0], l[1], l[2], l[3]));
     __stcg(R4 + q, make_uint4(r[0], r[1], r[2], r[3]));

@@ -69,7 +69,7 @@ int elem_compile(const coh_elem_program* progs, uint32_t n, ElemPlan* plan, std:
       *err = "element program " + std::to_string(b) + ": n_cells must be >= 1 and n_views <= 16";
       return COH_E_CONSTRUCTION;
     }
-    if (P.frag_log2 > 32) {
+    if (P.frag_log2 > 32) {  // coh_frag_mask: rho = 2^-frag_log2 down to 2^-32
       *err = "element program " + std::to_string(b) + ": frag_log2 must be <= 32";
       return COH_E_CONSTRUCTION;
     }

@@ -27,8 +27,7 @@ COH_HD uint16_t coh_gen_record(uint64_t seed, uint64_t trace_id, uint32_t call_i
   return (uint16_t)((arr << 8) | (kind << 2) | (site << 4) | (var << 5));
 }
 
-// Fragmentation mask of plane word w (include/cohere_b200.h coh_frag_mask, same draws;
-// once the mask is empty further draws change nothing).
+// Fragmentation mask of plane word w (include/cohere_b200.h coh_frag_mask, same draws).
 COH_HD uint32_t coh_frag_word(uint64_t frag_seed, uint32_t frag_log2, uint32_t w) {
   if (frag_log2 == 0) return 0u;
   uint32_t x = ((uint32_t)frag_seed ^ (w * 0x9E3779B9u)) + (uint32_t)(frag_seed >> 32);
@@ -37,8 +36,12 @@ COH_HD uint32_t coh_frag_word(uint64_t frag_seed, uint32_t frag_log2, uint32_t w
   x ^= x >> 13;
   x *= 0xC2B2AE35u;
   x ^= x >> 16;
+  if (frag_log2 > 5) {
+    const uint32_t t = frag_log2 - 5;
+    return (x >> (32u - t)) == ((1u << t) - 1u) ? 1u << (x & 31u) : 0u;
+  }
   uint32_t m = x;
-  for (uint32_t j = 1; j < frag_log2 && m; ++j) {
+  for (uint32_t j = 1; j < frag_log2; ++j) {
     x ^= x << 13;
     x ^= x >> 17;
     x ^= x << 5;
