@@ -33,7 +33,8 @@ namespace {
 
 constexpr uint32_t kBT = 256;   // threads per block
 constexpr int kU = 4;           // warp steps in flight
-constexpr int kRU = 8;          // warp steps in flight in the zero-run walker (chunk_runs)
+constexpr int kRU = 4;          // warp steps in flight in the zero-run walker (chunk_runs)
+constexpr uint32_t kRunsBuf = 1024;  // dense-step staging entries per warp (two passes above)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 struct Flat {
@@ -537,8 +538,8 @@ __device__ __forceinline__ void place_step(const Flat& F, uint64_t f, uint32_t r
   const uint32_t Ts = __shfl_sync(0xFFFFFFFFu, ps, 31), Te = __shfl_sync(0xFFFFFFFFu, pe, 31);
   if (Ts + Te > kDenseStep) {  // staged in shared memory, written with coalesced stores
     const uint32_t cb = (uint32_t)((qa * 4 - F.r[r].word_off) * 32);
-    emit_staged(st, ps - ns, Ts, cb, gs, out_s, cap, wbuf);
-    emit_staged(en, pe - ne, Te, cb, ge, out_e, cap, wbuf);
+    emit_staged<kRunsBuf>(st, ps - ns, Ts, cb, gs, out_s, cap, wbuf);
+    emit_staged<kRunsBuf>(en, pe - ne, Te, cb, ge, out_e, cap, wbuf);
   } else if (ns | ne) {  // sparse step: each lane writes its few runs
     const uint64_t wbase = qa * 4 - F.r[r].word_off;
 #pragma unroll
@@ -568,11 +569,11 @@ struct RunCounts {
   uint64_t *chunk_s, *chunk_e, *block_s, *block_e;
 };
 
-__global__ void __launch_bounds__(kBT, 3) k_runs_collect(const uint32_t* words, Flat Fg, RunCounts C, uint32_t* stage,
+__global__ void __launch_bounds__(kBT, 4) k_runs_collect(const uint32_t* words, Flat Fg, RunCounts C, uint32_t* stage,
                                                          uint32_t* off_local) {
   COH_BM_PROLOGUE
-  extern __shared__ uint32_t runs_smem[];  // kBT / 32 warps x kStageBuf: dense run staging
-  uint32_t* const wbuf = runs_smem + (threadIdx.x >> 5) * kStageBuf;
+  extern __shared__ uint32_t runs_smem[];  // kBT / 32 warps x kRunsBuf: dense run staging
+  uint32_t* const wbuf = runs_smem + (threadIdx.x >> 5) * kRunsBuf;
   __shared__ uint64_t ws[2][kBT / 32];
   uint64_t f0, f1, wid;
   warp_chunk(F.qp[F.n], f0, f1, wid);
@@ -667,13 +668,13 @@ __device__ __forceinline__ void chunk_offsets(const RunCounts& C, const uint64_t
 // Place pass, plus run_off[i] = global index of range i's first run: its chunk's offset +
 // the chunk-local count staged by the collect pass; ranges starting at the end get the
 // total.
-__global__ void __launch_bounds__(kBT, 3) k_runs_place(const uint32_t* words, Flat Fg, RunCounts C,
+__global__ void __launch_bounds__(kBT, 4) k_runs_place(const uint32_t* words, Flat Fg, RunCounts C,
                                                        const uint32_t* stage, const uint32_t* off_local,
                                                        uint32_t* run_start, uint32_t* run_end, uint64_t cap,
                                                        uint64_t* run_off) {
   COH_BM_PROLOGUE
-  extern __shared__ uint32_t runs_smem[];  // kBT / 32 warps x kStageBuf: dense run staging
-  uint32_t* const wbuf = runs_smem + (threadIdx.x >> 5) * kStageBuf;
+  extern __shared__ uint32_t runs_smem[];  // kBT / 32 warps x kRunsBuf: dense run staging
+  uint32_t* const wbuf = runs_smem + (threadIdx.x >> 5) * kRunsBuf;
   __shared__ uint64_t bs[kMaxCollectBlocks + 1], be[kMaxCollectBlocks + 1];
   block_scan2(C.block_s, C.block_e, gridDim.x, bs, be);
   const uint64_t Q = F.qp[F.n], n_chunks = (uint64_t)gridDim.x * (kBT / 32);
@@ -825,7 +826,7 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   C.block_e = C.block_s + grid;
   uint32_t* stage = reinterpret_cast<uint32_t*>(static_cast<char*>(co.p) + counts_b);
   uint32_t* off_local = stage + 2 * kRunCap * n_chunks;
-  constexpr size_t kRunsSmem = (size_t)(kBT / 32) * kStageBuf * 4u;
+  constexpr size_t kRunsSmem = (size_t)(kBT / 32) * kRunsBuf * 4u;
   const bool smem_ok =  // per call: the attribute belongs to the current device
       cudaFuncSetAttribute(k_runs_collect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRunsSmem) == cudaSuccess &&
       cudaFuncSetAttribute(k_runs_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRunsSmem) == cudaSuccess;

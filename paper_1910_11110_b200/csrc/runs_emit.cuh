@@ -58,23 +58,32 @@ namespace cohb {
 // run starts (or ends).  Every lane writes its own set bits' cells, in ascending order,
 // into the warp's shared-memory buffer at S_lane + rank (independent per lane: no
 // shuffles on the critical path), then the warp copies the step's T cells to out[base ..)
-// with coalesced 128-byte stores.  Buffer index o is stored at o ^ ((o >> 5) & 31): lanes
-// whose offsets are ~32 apart (the dense case) then hit different banks.
-constexpr uint32_t kStageBuf = 2048;  // u32 entries per warp
+// with coalesced 128-byte stores.  A buffer of B entries takes the step in passes of B
+// positions.  Buffer index o is stored at o ^ ((o >> 5) & 31): lanes whose offsets are
+// ~32 apart (the dense case) then hit different banks.
+constexpr uint32_t kStageBuf = 2048;  // u32 entries per warp (the element apply)
 __device__ __forceinline__ uint32_t stage_swz(uint32_t o) { return o ^ ((o >> 5) & 31u); }
 
+template <uint32_t B = kStageBuf>
 __device__ __forceinline__ void emit_staged(const uint32_t* m, uint32_t S, uint32_t T, uint32_t cb, uint64_t base,
                                             uint32_t* out, uint64_t cap, uint32_t* buf) {
   if (base >= cap) return;  // warp-uniform: nothing of this step fits (e.g. a full staging chunk)
-  uint32_t o = S;
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    for (uint32_t x = m[k]; x; x &= x - 1) buf[stage_swz(o++)] = cb + 32u * k + (uint32_t)(__ffs(x) - 1);
-  __syncwarp();
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t lim = base >= cap ? 0 : (T < cap - base ? T : cap - base);
-  for (uint32_t p = lane; p < lim; p += 32) out[base + p] = buf[stage_swz(p)];
-  __syncwarp();  // the buffer is free again
+  const uint64_t lim = T < cap - base ? T : cap - base;
+  const uint32_t mine = __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
+  for (uint32_t p0 = 0; p0 < lim; p0 += B) {  // warp-uniform passes of B positions
+    uint32_t o = S;
+    if (S < p0 + B && S + mine > p0) {  // this lane has positions in the pass
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        for (uint32_t x = m[k]; x; x &= x - 1, ++o)
+          if (o - p0 < B) buf[stage_swz(o - p0)] = cb + 32u * k + (uint32_t)(__ffs(x) - 1);
+    }
+    __syncwarp();
+    const uint32_t n = lim - p0 < B ? (uint32_t)(lim - p0) : B;
+    for (uint32_t p = lane; p < n; p += 32) out[base + p0 + p] = buf[stage_swz(p)];
+    __syncwarp();  // the buffer is free again
+  }
 }
 
 }  // namespace cohb
