@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--overlap-blocks", type=int, default=1 << 20)
     ap.add_argument("--c4-traces", type=int, default=1 << 26, help="C4 total traces, split over the ranks (0 = skip)")
     ap.add_argument("--checker-programs", type=int, default=20000, help="batched checker programs (0 = skip)")
+    ap.add_argument("--blocks-traces", type=int, default=1 << 20, help="multi-mode block traces (0 = skip)")
     return ap.parse_args()
 
 
@@ -712,6 +713,38 @@ def run_c4(args, ctx, rank, world, allreduce):
             "note": "device time of one evaluation (best of 3, max over ranks); records generated on each device"}
 
 
+def run_blocks(args, ctx):
+    """Multi-mode blocks (COH_BATCH_BLOCKS, k_trace_blocks): the C2 shape (1M traces x 256
+    calls x 64 arrays, adv 1/1024) with ~30% of the calls continuing their predecessor's
+    DeclBlock (coh_gen_records_blocks, device-generated); device time of one evaluation
+    (best of 3, CUDA events).  Throughput in records (calls) per second."""
+    import torch
+
+    import paper_1910_11110_b200 as coh
+
+    nt, nc, na, cont = args.blocks_traces, N_CALLS, N_ARRAYS, 300
+    s = torch.cuda.current_stream()
+    d_rec = torch.empty(coh.records_elems(nt, nc), dtype=torch.int16, device="cuda")
+    ctx.gen_records_blocks(SEED, 0, nt, nc, na, ADV, cont, d_rec, s.cuda_stream)
+    d_res = torch.empty(nt * 64, dtype=torch.uint8, device="cuda")
+    d_cnt = torch.zeros(16, dtype=torch.int64, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = None
+    for _ in range(4):
+        e0.record(s)
+        ctx.eval_traces_counted(d_rec, nt, nc, na, FUEL, d_res, d_cnt, None, stream=s.cuda_stream,
+                                flags=coh.BATCH_BLOCKS)
+        e1.record(s)
+        torch.cuda.synchronize()
+        best = e0.elapsed_time(e1) if best is None else min(best, e0.elapsed_time(e1))
+    cnt = d_cnt.cpu().numpy().view(np.uint64)
+    cont_frac = float((d_rec[: 8 * nt].view(torch.int16) & 1).float().mean().item())
+    del d_rec, d_res
+    return {"metric": "multi-mode blocks: records/s (COH_BATCH_BLOCKS)", "traces": nt, "calls": nc, "arrays": na,
+            "cont_fraction": cont_frac, "ms": best, "value": nt * nc / (best / 1e3), "unit": "records/s",
+            "blocks_completed": int(cnt[8]), "stuck_traces": int(cnt[0]), "unsafe_traces": int(cnt[10])}
+
+
 def run_c1(ctx):
     """BASELINE config 1: one trace of 1000 random calls on one array (seed 0, default
     mix), the latency case.  gpu_us: the evaluation as a CUDA graph replayed between two
@@ -918,6 +951,7 @@ def run_ours(args, rank, world, local):
     c4 = run_c4(args, ctx, rank, world, allreduce) if args.c4_traces > 0 else None
     overlap = run_overlap(args, ctx) if (args.overlap_views > 0 and rank == 0) else None
     checker = run_checker(args) if (args.checker_programs > 0 and rank == 0) else None
+    blocks = run_blocks(args, ctx) if (args.blocks_traces > 0 and rank == 0) else None
     container = None
     if args.container_log2_floats > 0 and rank == 0:
         try:
@@ -948,7 +982,7 @@ def run_ours(args, rank, world, local):
                                             .multi_processor_count)},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
             "bitmap": bitmap, "container": container, "sweep": sweep_info, "c1": c1, "c4": c4, "overlap": overlap,
-            "checker": checker,
+            "checker": checker, "blocks": blocks,
         }
         print(json.dumps(line), flush=True)
     if comm is not None:

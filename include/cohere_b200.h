@@ -171,6 +171,15 @@ int coh_gen_records(coh_ctx* ctx, uint64_t seed, uint64_t trace0, uint64_t n_tra
 int coh_gen_records_host(uint64_t seed, uint64_t trace0, uint64_t n_traces,
                          uint32_t n_calls, uint32_t n_arrays, uint32_t adv_per1024,
                          uint16_t* h_records);
+/* The same records with COH_REC_CONT marks for COH_BATCH_BLOCKS: call i > 0 continues the
+ * current block with probability cont_per1024/1024 when its array is not yet in the block
+ *   cont(t, i) = (splitmix64(seed ^ 0x5851F42D4C957F2D ^ (trace_id << 20) ^ i) & 0x3ff) < cont_per1024
+ * (each trace walked in call order).  Identical on host and device. */
+int coh_gen_records_blocks(coh_ctx* ctx, uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
+                           uint32_t n_arrays, uint32_t adv_per1024, uint32_t cont_per1024, uint16_t* d_records,
+                           void* stream);
+int coh_gen_records_blocks_host(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
+                                uint32_t n_arrays, uint32_t adv_per1024, uint32_t cont_per1024, uint16_t* h_records);
 static inline size_t coh_records_elems(uint64_t n_traces, uint32_t n_calls) {
   return (size_t)((n_calls + 7u) / 8u) * (size_t)n_traces * 8u;
 }

@@ -25,6 +25,7 @@ from ._ffi import (  # noqa: F401
     shard_split,
     calltable_describe,
     calltable_program,
+    gen_records_blocks_host,
     gen_records_host,
     lib,
     lib_path,

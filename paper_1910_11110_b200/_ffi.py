@@ -115,6 +115,8 @@ def lib():
             "coh_calltable_program": (i, [u32, C.POINTER(C.c_uint8)]),
             "coh_gen_records": (i, [vp, u64, u64, u64, u32, u32, u32, vp, vp]),
             "coh_gen_records_host": (i, [u64, u64, u64, u32, u32, u32, vp]),
+            "coh_gen_records_blocks": (i, [vp, u64, u64, u64, u32, u32, u32, u32, vp, vp]),
+            "coh_gen_records_blocks_host": (i, [u64, u64, u64, u32, u32, u32, u32, vp]),
             "coh_eval_traces": (i, [vp, C.POINTER(_Batch), vp, vp, vp]),
             "coh_eval_traces_host": (i, [vp, C.POINTER(_Batch), vp, vp]),
             "coh_eval_traces_counted": (i, [vp, C.POINTER(_Batch), vp, vp, vp, vp]),
@@ -187,6 +189,17 @@ def gen_records_host(seed: int, trace0: int, n_traces: int, n_calls: int, n_arra
     return out
 
 
+def gen_records_blocks_host(seed: int, trace0: int, n_traces: int, n_calls: int, n_arrays: int, adv_per1024: int,
+                            cont_per1024: int) -> np.ndarray:
+    """coh_gen_records_blocks_host: the synthetic records with COH_REC_CONT block marks."""
+    out = np.zeros(records_elems(n_traces, n_calls), dtype=np.uint16)
+    rc = lib().coh_gen_records_blocks_host(seed, trace0, n_traces, n_calls, n_arrays, adv_per1024, cont_per1024,
+                                           out.ctypes.data)
+    if rc:
+        raise CohError(rc, "coh_gen_records_blocks_host")
+    return out
+
+
 def _ptr(x) -> int:
     """Raw address of a torch tensor / numpy array / int."""
     if x is None:
@@ -252,6 +265,12 @@ class Context:
             self._L.coh_gen_records(self._h, seed, trace0, n_traces, n_calls, n_arrays, adv_per1024, _ptr(d_records), _ptr(stream)),
             "coh_gen_records",
         )
+
+    def gen_records_blocks(self, seed, trace0, n_traces, n_calls, n_arrays, adv_per1024, cont_per1024, d_records,
+                           stream=0):
+        self._check(self._L.coh_gen_records_blocks(self._h, seed, trace0, n_traces, n_calls, n_arrays, adv_per1024,
+                                                   cont_per1024, _ptr(d_records), _ptr(stream)),
+                    "coh_gen_records_blocks")
 
     def eval_traces(self, d_records, n_traces, n_calls, n_arrays, fuel, d_results, d_boundary=None, array_bytes=None, stream=0,
                     flags=0):

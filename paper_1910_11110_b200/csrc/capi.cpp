@@ -191,6 +191,38 @@ int coh_gen_records(coh_ctx* ctx, uint64_t seed, uint64_t trace0, uint64_t n_tra
   return rc;
 }
 
+int coh_gen_records_blocks(coh_ctx* ctx, uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
+                           uint32_t n_arrays, uint32_t adv_per1024, uint32_t cont_per1024, uint16_t* d_records,
+                           void* stream) {
+  int rc = coh_gen_records(ctx, seed, trace0, n_traces, n_calls, n_arrays, adv_per1024, d_records, stream);
+  if (rc) return rc;
+  std::string err;
+  rc = cohb::launch_gen_blocks(seed, trace0, n_traces, n_calls, cont_per1024, d_records, stream, &err);
+  if (rc) ctx->err = err;
+  else if (cont_per1024 && n_traces && n_calls) ctx->launches++;
+  return rc;
+}
+
+int coh_gen_records_blocks_host(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
+                                uint32_t n_arrays, uint32_t adv_per1024, uint32_t cont_per1024, uint16_t* h_records) {
+  const int rc = coh_gen_records_host(seed, trace0, n_traces, n_calls, n_arrays, adv_per1024, h_records);
+  if (rc || !cont_per1024) return rc;
+  for (uint64_t t = 0; t < n_traces; ++t) {
+    uint64_t in_block = 0;
+    for (uint32_t i = 0; i < n_calls; ++i) {
+      uint16_t& r = h_records[((uint64_t)(i / 8u) * n_traces + t) * 8u + i % 8u];
+      const uint64_t bit = 1ull << COH_REC_ARRAY(r);
+      if (i > 0 && !(in_block & bit) && coh_gen_cont(seed, trace0 + t, i, cont_per1024)) {
+        r = (uint16_t)(r | COH_REC_CONT);
+        in_block |= bit;
+      } else {
+        in_block = bit;
+      }
+    }
+  }
+  return COH_OK;
+}
+
 int coh_gen_records_host(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
                          uint32_t n_arrays, uint32_t adv_per1024, uint16_t* h_records) {
   if (n_arrays < 1 || n_arrays > COH_MAX_ARRAYS) return COH_E_ARG;

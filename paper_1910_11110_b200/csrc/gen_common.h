@@ -49,3 +49,11 @@ COH_HD uint32_t coh_frag_word(uint64_t frag_seed, uint32_t frag_log2, uint32_t w
   }
   return m;
 }
+
+// Multi-mode blocks for synthetic traces (COH_BATCH_BLOCKS): call i > 0 continues the
+// current block with probability cont_per1024 / 1024 when its array is not in the block
+// yet (a DeclBlock names each variable once).  Applied to a trace's records in call order.
+COH_HD bool coh_gen_cont(uint64_t seed, uint64_t trace_id, uint32_t call_idx, uint32_t cont_per1024) {
+  const uint64_t h = coh_splitmix64(seed ^ 0x5851F42D4C957F2Dull ^ (trace_id << 20) ^ (uint64_t)call_idx);
+  return (uint32_t)(h & 0x3FFull) < cont_per1024;
+}

@@ -28,6 +28,42 @@ __global__ void k_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces,
   }
 }
 
+// COH_REC_CONT bits (coh_gen_cont): one thread walks one trace's calls in order, keeping the
+// set of arrays of the current block.
+__global__ void k_gen_blocks(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls, uint32_t cont,
+                             uint16_t* rec) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_traces;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long in_block = 0ull;
+    for (uint32_t i = 0; i < n_calls; ++i) {
+      uint16_t* p = rec + ((uint64_t)(i >> 3) * n_traces + t) * 8u + (i & 7u);
+      const uint16_t r = *p;
+      const unsigned long long bit = 1ull << COH_REC_ARRAY(r);
+      if (i > 0 && !(in_block & bit) && coh_gen_cont(seed, trace0 + t, i, cont)) {
+        *p = (uint16_t)(r | COH_REC_CONT);
+        in_block |= bit;
+      } else {
+        in_block = bit;
+      }
+    }
+  }
+}
+
+int launch_gen_blocks(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls, uint32_t cont,
+                      uint16_t* d_records, void* stream, std::string* err) {
+  if (!n_traces || !n_calls || !cont) return COH_OK;
+  uint64_t blocks = (n_traces + 127) / 128;
+  if (blocks > 148ull * 32) blocks = 148ull * 32;
+  k_gen_blocks<<<(unsigned)blocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(seed, trace0, n_traces, n_calls, cont,
+                                                                                d_records);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("gen_blocks launch: ") + cudaGetErrorString(e);
+    return COH_E_CUDA;
+  }
+  return COH_OK;
+}
+
 int launch_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
                        uint32_t n_arrays, uint32_t adv, uint16_t* d_records, void* stream,
                        std::string* err) {

@@ -103,6 +103,8 @@ int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t n_
 int launch_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
                        uint32_t n_arrays, uint32_t adv_per1024, uint16_t* d_records, void* stream,
                        std::string* err);
+int launch_gen_blocks(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls, uint32_t cont,
+                      uint16_t* d_records, void* stream, std::string* err);
 int launch_reduce_counters(const coh_trace_result* d_results, uint64_t n_traces,
                            uint64_t* d_counters, void* stream, std::string* err);
 

@@ -59,91 +59,104 @@ __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
   uint32_t status = COH_RUN_DONE, stuck_call = 0, stuck_arr = 0, stuck_eff = 0, stuck_flags = 0;
   uint32_t word = 0;  // boundary_ok bits of the current 32-block group
   const uint32_t n_words = (p.n_calls + 31u) / 32u;
-  uint32_t b0 = 0;
-  while (b0 < p.n_calls) {
-    // the block: b0 and the COH_REC_CONT records after it
-    uint32_t b1 = b0 + 1;
-    while (b1 < p.n_calls && (rec(b1) & COH_REC_CONT)) ++b1;
-    // DeclBlock construction (program.hpp:212-235): declared arrays, valid modes, each
-    // array once; a failure is a construction defect at this block, before any step
-    unsigned long long seen = 0ull;
-    bool defect = false;
-    for (uint32_t i = b0; i < b1 && !defect; ++i) {
-      const uint32_t r = rec(i), a = COH_REC_ARRAY(r);
-      if (a >= p.n_arrays || COH_REC_KIND(r) == 3u || ((seen >> a) & 1ull)) {
-        defect = true;
-        stuck_arr = a;
-      }
-      seen |= 1ull << a;
-    }
-    if (defect) {
-      status = COH_RUN_DEFECT;
-      break;
-    }
-    // translate_block: the guards of every mode (phase 0), then every body (phase 1).
-    // Each record's translated block is its type's micro-op program (guard ops first);
-    // every op is decoded the same way, so lanes on different calls stay converged.
-    bool stop = false;
-    for (uint32_t phase = 0; phase < 2 && !stop; ++phase) {
-      for (uint32_t i = b0; i < b1 && !stop; ++i) {
-        const uint32_t r = rec(i), a = COH_REC_ARRAY(r), kind = COH_REC_KIND(r);
-        const uint64_t prog = p.prog[COH_REC_TYPE(r)];
-        const uint32_t n_guard = kind == COH_R ? 3u : kind == COH_W ? 1u : 4u;
-        uint32_t n_all = 0;
-        while (n_all < 8u && ((prog >> (8u * n_all)) & 0xFFu)) ++n_all;
-        const uint32_t k0 = phase ? n_guard : 0u, k1 = phase ? n_all : n_guard;
-        uint32_t nib = st[a][tid];
-        for (uint32_t k = k0; k < k1; ++k) {
-          if ((int32_t)steps >= p.fuel) {  // an op remains: Done was not reached
-            status = COH_RUN_FUEL_EXHAUSTED;
-            stuck_arr = COH_REC_ARRAY(rec(b0));
-            stop = true;
-            break;
-          }
-          const uint32_t op = (uint32_t)(prog >> (8u * k)) & 0xFFu, kop = op & 3u;
-          if (kop != OP_EFFECT) {  // if (valid(x^)) / if (gvalid(x^)): one step; valid skips the two syncs
-            ++steps;
-            if ((nib >> (1u + kop)) & 1u) k += 2;
-            continue;
-          }
-          const uint32_t eff = (op >> 2) & 7u, esite = (op >> 5) & 1u, abstract = (op >> 6) & 1u;
-          const uint32_t pair = abstract ? (nib >> 2) & 3u : nib & 3u;
-          // validity.hpp:79-120 with the remote swap (semantics.hpp:109-130), branch-free
-          const uint32_t q = esite ? swap_pair(pair) : pair;
-          const bool sync = eff == COH_PUSH || eff == COH_PULL;
-          const uint32_t ok = eff == COH_PUSH ? (q & 1u) : eff == COH_PULL ? (q >> 1) : eff == COH_READ ? (q & 1u) : 1u;
-          const uint32_t rq = sync ? 3u : eff == COH_READ ? q : eff == COH_WRITE ? 1u : q;
-          if (!ok) {
-            status = COH_RUN_STUCK;
-            stuck_arr = a;
-            stuck_eff = eff;
-            stuck_flags = esite | (abstract << 1) | (pair << 2);
-            stop = true;
-            break;
-          }
-          const uint32_t after = esite ? swap_pair(rq) : rq;
-          const uint32_t nn = abstract ? ((nib & 3u) | (after << 2)) : ((nib & 12u) | after);
-          viol += violating(nn) - violating(nib);
-          nib = nn;
-          ++steps;
-          if (!abstract && sync) {
-            ++xfers;
-            tbytes += bytes_of(a);
-          }
+  // A flat state machine: every iteration executes at most one micro-op for every lane,
+  // so lanes on different blocks, phases and records run the same instruction stream
+  // (nested per-block / per-record loops diverged: ~4 of 32 lanes active per instruction).
+  // Cursor: block [b0, b1), phase (0 guards, 1 bodies), record i, op k of its program.
+  uint32_t b0 = 0, b1 = 0, i = 0, k = 0, phase = 2;  // phase 2: open the next block
+  uint32_t r = 0;
+  uint64_t prog = 0;
+  bool live = p.n_calls > 0;
+  while (live) {
+    if (phase == 2) {  // the next block: b0 and the COH_REC_CONT records after it
+      b0 = b1;
+      if (b0 >= p.n_calls) break;
+      b1 = b0 + 1;
+      while (b1 < p.n_calls && (rec(b1) & COH_REC_CONT)) ++b1;
+      // DeclBlock construction (program.hpp:212-235): declared arrays, valid modes, each
+      // array once; a failure is a construction defect at this block, before any step
+      unsigned long long seen = 0ull;
+      bool defect = false;
+      for (uint32_t j = b0; j < b1 && !defect; ++j) {
+        const uint32_t rj = rec(j), a = COH_REC_ARRAY(rj);
+        if (a >= p.n_arrays || COH_REC_KIND(rj) == 3u || ((seen >> a) & 1ull)) {
+          defect = true;
+          stuck_arr = a;
         }
-        st[a][tid] = (uint8_t)nib;
+        seen |= 1ull << a;
       }
+      if (defect) {
+        status = COH_RUN_DEFECT;
+        break;
+      }
+      phase = 0, i = b0, k = 0;
+      r = rec(i);
+      prog = p.prog[COH_REC_TYPE(r)];
     }
-    if (stop) break;
-    // abstraction_correct after the completed block
-    if (viol) ++viol_blocks;
-    else word |= 1u << (blocks_done & 31u);
-    ++blocks_done;
-    if ((blocks_done & 31u) == 0u) {
-      if (p.bnd) p.bnd[(uint64_t)(blocks_done / 32u - 1u) * n + t] = word;
-      word = 0u;
+    // the op range of record i in this phase: guard ops first, then the body
+    const uint32_t kind = COH_REC_KIND(r);
+    const uint32_t n_guard = kind == COH_R ? 3u : kind == COH_W ? 1u : 4u;
+    const uint32_t n_all = (uint32_t)(64 - __clzll((long long)prog) + 7) >> 3;  // ops are non-zero bytes
+    if (k < (phase ? n_guard : 0u)) k = n_guard;
+    if (k < (phase ? n_all : n_guard)) {
+      if ((int32_t)steps >= p.fuel) {  // an op remains: Done was not reached
+        status = COH_RUN_FUEL_EXHAUSTED;
+        stuck_arr = COH_REC_ARRAY(rec(b0));
+        break;
+      }
+      const uint32_t a = COH_REC_ARRAY(r);
+      const uint32_t nib = st[a][tid];
+      const uint32_t op = (uint32_t)(prog >> (8u * k)) & 0xFFu, kop = op & 3u;
+      if (kop != OP_EFFECT) {  // if (valid(x^)) / if (gvalid(x^)): one step; valid skips the two syncs
+        ++steps;
+        k += ((nib >> (1u + kop)) & 1u) ? 3u : 1u;
+        continue;
+      }
+      const uint32_t eff = (op >> 2) & 7u, esite = (op >> 5) & 1u, abstract = (op >> 6) & 1u;
+      const uint32_t pair = abstract ? (nib >> 2) & 3u : nib & 3u;
+      // validity.hpp:79-120 with the remote swap (semantics.hpp:109-130), branch-free
+      const uint32_t q = esite ? swap_pair(pair) : pair;
+      const bool sync = eff == COH_PUSH || eff == COH_PULL;
+      const uint32_t ok = eff == COH_PUSH ? (q & 1u) : eff == COH_PULL ? (q >> 1) : eff == COH_READ ? (q & 1u) : 1u;
+      if (!ok) {
+        status = COH_RUN_STUCK;
+        stuck_arr = a;
+        stuck_eff = eff;
+        stuck_flags = esite | (abstract << 1) | (pair << 2);
+        break;
+      }
+      const uint32_t rq = sync ? 3u : eff == COH_READ ? q : eff == COH_WRITE ? 1u : q;
+      const uint32_t after = esite ? swap_pair(rq) : rq;
+      const uint32_t nn = abstract ? ((nib & 3u) | (after << 2)) : ((nib & 12u) | after);
+      viol += violating(nn) - violating(nib);
+      st[a][tid] = (uint8_t)nn;
+      ++steps;
+      if (!abstract && sync) {
+        ++xfers;
+        tbytes += bytes_of(a);
+      }
+      ++k;
+      continue;
     }
-    b0 = b1;
+    // record i's ops of this phase are done: the next record, phase or block
+    if (++i < b1) {
+      k = 0;
+    } else if (phase == 0) {
+      phase = 1, i = b0, k = 0;
+    } else {
+      // abstraction_correct after the completed block
+      if (viol) ++viol_blocks;
+      else word |= 1u << (blocks_done & 31u);
+      ++blocks_done;
+      if ((blocks_done & 31u) == 0u) {
+        if (p.bnd) p.bnd[(uint64_t)(blocks_done / 32u - 1u) * n + t] = word;
+        word = 0u;
+      }
+      phase = 2;
+      continue;
+    }
+    r = rec(i);
+    prog = p.prog[COH_REC_TYPE(r)];
   }
   if (status != COH_RUN_DONE) stuck_call = blocks_done;
   if (p.bnd) {

@@ -68,3 +68,22 @@ def test_unknown_flags_rejected(ctx):
     recs = o.orc_gen(1, 0, 4, 8, 2, 0)
     with pytest.raises(coh.CohError):
         dev_eval(ctx, recs, 4, 8, 2, 100, 6)
+
+
+def test_generated_blocks_c2_scale_vs_oracle(ctx):
+    """Device-generated multi-mode records (coh_gen_records_blocks == the host generator) at
+    the C2 shape, 256K traces x 256 calls x 64 arrays: every trace equals the oracle."""
+    nt, nc, na, adv, cont = 1 << 18, 256, 64, 1, 300
+    s = torch.cuda.current_stream().cuda_stream
+    d_rec = torch.empty(coh.records_elems(nt, nc), dtype=torch.int16, device="cuda")
+    ctx.gen_records_blocks(1, 0, nt, nc, na, adv, cont, d_rec, s)
+    d_res = torch.empty(nt * 64, dtype=torch.uint8, device="cuda")
+    d_bnd = torch.empty(coh.boundary_words(nc) * nt, dtype=torch.int32, device="cuda")
+    ctx.eval_traces(d_rec, nt, nc, na, 10000, d_res, d_bnd, stream=s, flags=coh.BATCH_BLOCKS)
+    torch.cuda.synchronize()
+    recs = d_rec.cpu().numpy().view(np.uint16)
+    assert np.array_equal(recs, coh.gen_records_blocks_host(1, 0, nt, nc, na, adv, cont))
+    assert (recs & 1).mean() > 0.2
+    want, wb = o.orc_eval(recs, nt, nc, na, 10000, flags=coh.BATCH_BLOCKS)
+    assert np.array_equal(d_res.cpu().numpy(), want.view(np.uint8))
+    assert np.array_equal(d_bnd.cpu().numpy().view(np.uint32), wb)
