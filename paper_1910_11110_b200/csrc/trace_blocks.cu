@@ -30,6 +30,7 @@ __device__ __forceinline__ uint32_t violating(uint32_t nib) {  // !leq(abstract,
 }
 
 struct BlocksParams {
+  const uint32_t* lut;        // the fast path's call table (internal.hpp: lut_word, entry layout)
   uint64_t prog[kCallTypes];  // per call type: its translated block as micro-ops (calltable.cpp
                               // block_ops, one byte each: guard ops first, then the body)
   const uint16_t* rec;
@@ -44,121 +45,173 @@ struct BlocksParams {
   unsigned long long* counters;
 };
 
+struct Lane {  // one trace's running outcome
+  uint32_t steps = 0, xfers = 0, viol = 0;
+  uint64_t tbytes = 0;
+  uint32_t status = COH_RUN_DONE, stuck_arr = 0, stuck_eff = 0, stuck_flags = 0;
+};
+
+// The exact semantics of one block [b0, b1) from the current store, op by op: every
+// mode's guard in record order, then every body (translate_block, modes.hpp:53-59); run
+// with the trace's fuel (semantics.hpp:253-287).  Taken at most once per trace -- for the
+// block in which the trace gets stuck or runs out of fuel.  Returns true if it completed.
+__device__ bool run_block_exact(const BlocksParams& p, uint8_t (*st)[kBT], uint32_t tid, uint64_t t, uint32_t b0,
+                                uint32_t b1, Lane& L) {
+  const uint64_t n = p.n_traces;
+  for (uint32_t phase = 0; phase < 2; ++phase)
+    for (uint32_t i = b0; i < b1; ++i) {
+      const uint32_t r = __ldg(p.rec + ((uint64_t)(i >> 3) * n + t) * 8u + (i & 7u));
+      const uint32_t a = COH_REC_ARRAY(r), kind = COH_REC_KIND(r);
+      const uint64_t prog = p.prog[COH_REC_TYPE(r)];
+      const uint32_t n_guard = kind == COH_R ? 3u : kind == COH_W ? 1u : 4u;
+      const uint32_t n_all = (uint32_t)(64 - __clzll((long long)prog) + 7) >> 3;  // ops are non-zero bytes
+      uint32_t nib = st[a][tid];
+      for (uint32_t k = phase ? n_guard : 0u; k < (phase ? n_all : n_guard);) {
+        if ((int32_t)L.steps >= p.fuel) {  // an op remains: Done was not reached
+          st[a][tid] = (uint8_t)nib;
+          L.status = COH_RUN_FUEL_EXHAUSTED;
+          L.stuck_arr = COH_REC_ARRAY(__ldg(p.rec + ((uint64_t)(b0 >> 3) * n + t) * 8u + (b0 & 7u)));
+          return false;
+        }
+        const uint32_t op = (uint32_t)(prog >> (8u * k)) & 0xFFu, kop = op & 3u;
+        if (kop != OP_EFFECT) {  // if (valid(x^)) / if (gvalid(x^)): one step; valid skips the two syncs
+          ++L.steps;
+          k += ((nib >> (1u + kop)) & 1u) ? 3u : 1u;
+          continue;
+        }
+        const uint32_t eff = (op >> 2) & 7u, esite = (op >> 5) & 1u, abstract = (op >> 6) & 1u;
+        const uint32_t pair = abstract ? (nib >> 2) & 3u : nib & 3u;
+        const uint32_t q = esite ? swap_pair(pair) : pair;  // validity.hpp:79-120, remote = swapped
+        const bool sync = eff == COH_PUSH || eff == COH_PULL;
+        const uint32_t ok = eff == COH_PUSH ? (q & 1u) : eff == COH_PULL ? (q >> 1) : eff == COH_READ ? (q & 1u) : 1u;
+        if (!ok) {
+          st[a][tid] = (uint8_t)nib;
+          L.status = COH_RUN_STUCK;
+          L.stuck_arr = a;
+          L.stuck_eff = eff;
+          L.stuck_flags = esite | (abstract << 1) | (pair << 2);
+          return false;
+        }
+        const uint32_t rq = sync ? 3u : eff == COH_READ ? q : eff == COH_WRITE ? 1u : q;
+        const uint32_t after = esite ? swap_pair(rq) : rq;
+        const uint32_t nn = abstract ? ((nib & 3u) | (after << 2)) : ((nib & 12u) | after);
+        L.viol += violating(nn) - violating(nib);
+        nib = nn;
+        ++L.steps;
+        if (!abstract && sync) {
+          ++L.xfers;
+          L.tbytes += p.uniform ? p.bytes_uniform : p.array_bytes[a];
+        }
+        ++k;
+      }
+      st[a][tid] = (uint8_t)nib;
+    }
+  return true;
+}
+
+// The fast path runs the records of all lanes in lockstep (record i for every lane per
+// iteration, so the warp stays converged): each record is one lookup in the host-compiled
+// call table (new state, steps, transfers, change of the violated-array count), applied at
+// once with the old state kept for undo.  For a block without a stuck record whose steps
+// fit the fuel, the outcome equals the translate_block order's (its modes touch distinct
+// arrays, so the order of their effects does not matter and the counts add up), and the
+// block commits at its end (boundary bit from the violated count).  Otherwise the block is
+// undone and re-run exactly (run_block_exact): it is where the trace stops.
 __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
   __shared__ uint8_t st[COH_MAX_ARRAYS][kBT];
+  __shared__ uint8_t undo[COH_MAX_ARRAYS][kBT];
+  __shared__ uint32_t s_lut[kLutEntries];
   const uint32_t tid = threadIdx.x;
+  for (uint32_t k = tid; k < (uint32_t)kLutEntries; k += kBT) s_lut[k] = __ldg(p.lut + k);
+  __syncthreads();
   const uint64_t t = (uint64_t)blockIdx.x * kBT + tid;
   if (t >= p.n_traces) return;
   const uint64_t n = p.n_traces;
   for (uint32_t a = 0; a < COH_MAX_ARRAYS; ++a) st[a][tid] = a < p.n_arrays ? COH_STATE_INITIAL : 0xFFu;
-  auto rec = [&](uint32_t i) -> uint32_t { return __ldg(p.rec + ((uint64_t)(i >> 3) * n + t) * 8u + (i & 7u)); };
-  auto bytes_of = [&](uint32_t a) -> uint64_t { return p.uniform ? p.bytes_uniform : p.array_bytes[a]; };
 
-  uint32_t steps = 0, xfers = 0, blocks_done = 0, viol_blocks = 0, viol = 0;
-  uint64_t tbytes = 0;
-  uint32_t status = COH_RUN_DONE, stuck_call = 0, stuck_arr = 0, stuck_eff = 0, stuck_flags = 0;
+  Lane L;
+  uint32_t blocks_done = 0, viol_blocks = 0;
   uint32_t word = 0;  // boundary_ok bits of the current 32-block group
   const uint32_t n_words = (p.n_calls + 31u) / 32u;
-  // A flat state machine: every iteration executes at most one micro-op for every lane,
-  // so lanes on different blocks, phases and records run the same instruction stream
-  // (nested per-block / per-record loops diverged: ~4 of 32 lanes active per instruction).
-  // Cursor: block [b0, b1), phase (0 guards, 1 bodies), record i, op k of its program.
-  uint32_t b0 = 0, b1 = 0, i = 0, k = 0, phase = 2;  // phase 2: open the next block
-  uint32_t r = 0;
-  uint64_t prog = 0;
-  bool live = p.n_calls > 0;
-  while (live) {
-    if (phase == 2) {  // the next block: b0 and the COH_REC_CONT records after it
-      b0 = b1;
-      if (b0 >= p.n_calls) break;
-      b1 = b0 + 1;
-      while (b1 < p.n_calls && (rec(b1) & COH_REC_CONT)) ++b1;
-      // DeclBlock construction (program.hpp:212-235): declared arrays, valid modes, each
-      // array once; a failure is a construction defect at this block, before any step
-      unsigned long long seen = 0ull;
-      bool defect = false;
-      for (uint32_t j = b0; j < b1 && !defect; ++j) {
-        const uint32_t rj = rec(j), a = COH_REC_ARRAY(rj);
-        if (a >= p.n_arrays || COH_REC_KIND(rj) == 3u || ((seen >> a) & 1ull)) {
-          defect = true;
-          stuck_arr = a;
-        }
-        seen |= 1ull << a;
-      }
-      if (defect) {
-        status = COH_RUN_DEFECT;
-        break;
-      }
-      phase = 0, i = b0, k = 0;
-      r = rec(i);
-      prog = p.prog[COH_REC_TYPE(r)];
-    }
-    // the op range of record i in this phase: guard ops first, then the body
-    const uint32_t kind = COH_REC_KIND(r);
-    const uint32_t n_guard = kind == COH_R ? 3u : kind == COH_W ? 1u : 4u;
-    const uint32_t n_all = (uint32_t)(64 - __clzll((long long)prog) + 7) >> 3;  // ops are non-zero bytes
-    if (k < (phase ? n_guard : 0u)) k = n_guard;
-    if (k < (phase ? n_all : n_guard)) {
-      if ((int32_t)steps >= p.fuel) {  // an op remains: Done was not reached
-        status = COH_RUN_FUEL_EXHAUSTED;
-        stuck_arr = COH_REC_ARRAY(rec(b0));
-        break;
-      }
-      const uint32_t a = COH_REC_ARRAY(r);
-      const uint32_t nib = st[a][tid];
-      const uint32_t op = (uint32_t)(prog >> (8u * k)) & 0xFFu, kop = op & 3u;
-      if (kop != OP_EFFECT) {  // if (valid(x^)) / if (gvalid(x^)): one step; valid skips the two syncs
-        ++steps;
-        k += ((nib >> (1u + kop)) & 1u) ? 3u : 1u;
-        continue;
-      }
-      const uint32_t eff = (op >> 2) & 7u, esite = (op >> 5) & 1u, abstract = (op >> 6) & 1u;
-      const uint32_t pair = abstract ? (nib >> 2) & 3u : nib & 3u;
-      // validity.hpp:79-120 with the remote swap (semantics.hpp:109-130), branch-free
-      const uint32_t q = esite ? swap_pair(pair) : pair;
-      const bool sync = eff == COH_PUSH || eff == COH_PULL;
-      const uint32_t ok = eff == COH_PUSH ? (q & 1u) : eff == COH_PULL ? (q >> 1) : eff == COH_READ ? (q & 1u) : 1u;
-      if (!ok) {
-        status = COH_RUN_STUCK;
-        stuck_arr = a;
-        stuck_eff = eff;
-        stuck_flags = esite | (abstract << 1) | (pair << 2);
-        break;
-      }
-      const uint32_t rq = sync ? 3u : eff == COH_READ ? q : eff == COH_WRITE ? 1u : q;
-      const uint32_t after = esite ? swap_pair(rq) : rq;
-      const uint32_t nn = abstract ? ((nib & 3u) | (after << 2)) : ((nib & 12u) | after);
-      viol += violating(nn) - violating(nib);
-      st[a][tid] = (uint8_t)nn;
-      ++steps;
-      if (!abstract && sync) {
-        ++xfers;
-        tbytes += bytes_of(a);
-      }
-      ++k;
-      continue;
-    }
-    // record i's ops of this phase are done: the next record, phase or block
-    if (++i < b1) {
-      k = 0;
-    } else if (phase == 0) {
-      phase = 1, i = b0, k = 0;
-    } else {
-      // abstraction_correct after the completed block
-      if (viol) ++viol_blocks;
+  // the open block
+  uint32_t b0 = 0, bsteps = 0, bxfers = 0, defect_arr = 0;
+  uint64_t bbytes = 0, touched = 0, seen = 0;  // touched: arrays written (undo); seen: named
+  int bdv = 0;
+  bool slow = false, defect = false, stopped = false;
+
+  auto close_block = [&](uint32_t b1) {
+    if (!slow && !defect && (int64_t)L.steps + bsteps <= (int64_t)p.fuel) {  // commit
+      L.steps += bsteps;
+      L.xfers += bxfers;
+      L.tbytes += bbytes;
+      L.viol += (uint32_t)bdv;
+      if (L.viol) ++viol_blocks;
       else word |= 1u << (blocks_done & 31u);
       ++blocks_done;
       if ((blocks_done & 31u) == 0u) {
         if (p.bnd) p.bnd[(uint64_t)(blocks_done / 32u - 1u) * n + t] = word;
         word = 0u;
       }
-      phase = 2;
+    } else {  // undo, then the block's exact outcome (the trace stops in it)
+      for (uint64_t m = touched; m; m &= m - 1) {
+        const uint32_t a = (uint32_t)__ffsll((long long)m) - 1u;
+        st[a][tid] = undo[a][tid];
+      }
+      if (defect) {  // DeclBlock construction fails before any step
+        L.status = COH_RUN_DEFECT;
+        L.stuck_arr = defect_arr;
+      } else if (run_block_exact(p, st, tid, t, b0, b1, L)) {  // (not reached: slow or over the fuel)
+        L.status = COH_RUN_DEFECT;
+      }
+      stopped = true;
+    }
+    bsteps = bxfers = 0;
+    bbytes = 0;
+    bdv = 0;
+    touched = seen = 0;
+    slow = defect = false;
+  };
+
+  // 8 records of this trace per 128-bit load, the next chunk in flight while one is used
+  const uint4* const rec4 = reinterpret_cast<const uint4*>(p.rec) + t;
+  const uint32_t n_chunks = (p.n_calls + 7u) / 8u;
+  uint4 chunk = make_uint4(0u, 0u, 0u, 0u), next = n_chunks ? __ldcs(rec4) : chunk;
+  for (uint32_t i = 0; i < p.n_calls && !stopped; ++i) {
+    if ((i & 7u) == 0u) {
+      chunk = next;
+      if ((i >> 3) + 1u < n_chunks) next = __ldcs(rec4 + (uint64_t)((i >> 3) + 1u) * n);
+    }
+    const uint32_t wsel = (i & 4u) ? ((i & 2u) ? chunk.w : chunk.z) : ((i & 2u) ? chunk.y : chunk.x);
+    const uint32_t r = (wsel >> (16u * (i & 1u))) & 0xFFFFu;
+    if (i > 0 && !(r & COH_REC_CONT)) {
+      close_block(i);
+      if (stopped) break;
+      b0 = i;
+    }
+    const uint32_t a = COH_REC_ARRAY(r), type = COH_REC_TYPE(r);
+    if (a >= p.n_arrays || COH_REC_KIND(r) == 3u || ((seen >> a) & 1ull)) {  // DeclBlock defect (first wins)
+      if (!defect) defect_arr = a;
+      defect = true;
       continue;
     }
-    r = rec(i);
-    prog = p.prog[COH_REC_TYPE(r)];
+    seen |= 1ull << a;
+    const uint32_t s0 = st[a][tid];
+    const uint32_t e = s_lut[s0 * 64u + (type ^ ((s0 * 9u) & 63u))];  // internal.hpp lut_word
+    if ((int32_t)e < 0) {  // stuck (whatever the order of the block's modes)
+      slow = true;
+      continue;
+    }
+    undo[a][tid] = (uint8_t)s0;
+    st[a][tid] = (uint8_t)((e >> 8) & 15u);
+    touched |= 1ull << a;
+    const uint32_t x = (e >> 23) & 0x3Fu;
+    bsteps += (e >> 16) & 0x7Fu;
+    bxfers += x;
+    if (x) bbytes += (uint64_t)x * (p.uniform ? p.bytes_uniform : p.array_bytes[a]);
+    bdv += (int)((e >> 29) & 7u) - 1;
   }
-  if (status != COH_RUN_DONE) stuck_call = blocks_done;
+  if (!stopped && p.n_calls) close_block(p.n_calls);
+  const uint32_t stuck_call = L.status != COH_RUN_DONE ? blocks_done : 0u;
   if (p.bnd) {
     uint32_t w = blocks_done / 32u;
     if (blocks_done & 31u) p.bnd[(uint64_t)w++ * n + t] = word;
@@ -167,22 +220,25 @@ __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
   // the final store, nibble-packed; is_unsafe (program.hpp:166-170)
   uint32_t sw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   bool unsafe = false;
-  for (uint32_t a = 0; a < p.n_arrays; ++a) {
+#pragma unroll
+  for (uint32_t a = 0; a < COH_MAX_ARRAYS; ++a) {
+    if (a >= p.n_arrays) break;
     const uint32_t nib = st[a][tid];
     sw[a >> 3] |= nib << (4u * (a & 7u));
     unsafe |= !(nib & 3u) || !(nib & 12u);
   }
+  uint32_t stuck_flags = L.stuck_flags;
   if (unsafe) stuck_flags |= COH_FLAG_UNSAFE;
   uint4* out = reinterpret_cast<uint4*>(p.res + t);
   out[0] = make_uint4(sw[0], sw[1], sw[2], sw[3]);
   out[1] = make_uint4(sw[4], sw[5], sw[6], sw[7]);
-  out[2] = make_uint4((uint32_t)tbytes, (uint32_t)(tbytes >> 32), steps, xfers);
+  out[2] = make_uint4((uint32_t)L.tbytes, (uint32_t)(L.tbytes >> 32), L.steps, L.xfers);
   out[3] = make_uint4(blocks_done, viol_blocks, stuck_call,
-                      status | (stuck_arr << 8) | (stuck_eff << 16) | (stuck_flags << 24));
+                      L.status | (L.stuck_arr << 8) | (L.stuck_eff << 16) | (stuck_flags << 24));
   if (p.counters) {
     const unsigned long long v[COH_N_COUNTERS] = {
-        status == COH_RUN_STUCK, status == COH_RUN_FUEL_EXHAUSTED, viol_blocks != 0u, status == COH_RUN_DEFECT,
-        steps, xfers, tbytes, viol_blocks, blocks_done, 1u, unsafe ? 1u : 0u};
+        L.status == COH_RUN_STUCK, L.status == COH_RUN_FUEL_EXHAUSTED, viol_blocks != 0u, L.status == COH_RUN_DEFECT,
+        L.steps, L.xfers, L.tbytes, viol_blocks, blocks_done, 1u, unsafe ? 1u : 0u};
 #pragma unroll
     for (int k = 0; k < COH_N_COUNTERS; ++k)
       if (v[k]) atomicAdd(p.counters + k, v[k]);
@@ -193,6 +249,7 @@ __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
 
 int launch_trace_blocks(const TraceLaunch& L, void* stream, std::string* err) {
   BlocksParams p;
+  p.lut = L.d_lut;
   for (uint32_t t = 0; t < (uint32_t)kCallTypes; ++t) {  // the host call-table compiler's programs
     uint8_t ops[8];
     const int n = coh_calltable_program(t, ops);
