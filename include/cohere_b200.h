@@ -124,6 +124,16 @@ typedef struct coh_trace_batch {
  * Per-block outputs (calls_done, violations, stuck_call, boundary bits) then count and
  * index blocks, not records. */
 #define COH_BATCH_BLOCKS 0x1u
+/* COH_BATCH_PACKED12 (coh_eval_traces_host only): the host records are packed 12 bits per
+ * call, the record's two fields without the free bits -- (array << 6) | call type -- so
+ * the host->device link carries 12 bytes per 8 calls instead of 16.  Chunk c (8 calls)
+ * of trace t is the 12 bytes at ((c * n_traces + t) * 12), call k of the chunk the bits
+ * [12k, 12k + 12) of those 96 little-endian bits.  Unpacked on the device per pipeline
+ * slice.  Not combinable with COH_BATCH_BLOCKS (no room for COH_REC_CONT). */
+#define COH_BATCH_PACKED12 0x2u
+/* Pack call-major 16-bit records (layout above) into the COH_BATCH_PACKED12 form;
+ * out holds ((n_calls + 7) / 8) * n_traces * 12 bytes. */
+int coh_pack_records12(const uint16_t* records, uint64_t n_traces, uint32_t n_calls, uint8_t* out);
 
 /* boundary_ok bitmaps: word-major, boundary[(i/32)*n_traces + t] bit (i%32) is
  * boundary_ok[i] of trace t; bits for calls >= calls_done are 0. */

@@ -54,6 +54,7 @@ COUNTER_NAMES = (
     "unsafe_traces",
 )
 BATCH_BLOCKS = 1  # COH_BATCH_BLOCKS: records carry COH_REC_CONT (multi-mode blocks)
+BATCH_PACKED12 = 2  # COH_BATCH_PACKED12: host records packed 12 bits per call (coh_eval_traces_host)
 REC_CONT = 1      # COH_REC_CONT
 FLAG_UNSAFE = 0x10
 N_COUNTERS = len(COUNTER_NAMES)
@@ -135,6 +136,7 @@ def lib():
                                           C.POINTER(vp)]),
             "coh_shard_split": (i, [u32, u32, u64, C.POINTER(u64), C.POINTER(u64)]),
             "coh_counters_host": (i, [vp, u64, vp]),
+            "coh_pack_records12": (i, [vp, u64, u32, vp]),
             "coh_trace_steps": (i, [vp, vp, u32, u32, i32, u32, vp, u32, C.POINTER(u32), C.POINTER(u32)]),
         }
         for name, (res, args) in sig.items():
@@ -197,6 +199,18 @@ def gen_records_blocks_host(seed: int, trace0: int, n_traces: int, n_calls: int,
                                            out.ctypes.data)
     if rc:
         raise CohError(rc, "coh_gen_records_blocks_host")
+    return out
+
+
+def pack_records12(records: np.ndarray, n_traces: int, n_calls: int, out: np.ndarray | None = None) -> np.ndarray:
+    """coh_pack_records12: call-major 16-bit records -> the COH_BATCH_PACKED12 host form."""
+    n = ((n_calls + 7) // 8) * n_traces * 12
+    if out is None:
+        out = np.zeros(n, np.uint8)
+    r = np.ascontiguousarray(records, dtype=np.uint16)
+    rc = lib().coh_pack_records12(r.ctypes.data, n_traces, n_calls, out.ctypes.data)
+    if rc:
+        raise CohError(rc, "coh_pack_records12")
     return out
 
 
@@ -295,7 +309,10 @@ class Context:
                          results: np.ndarray | None = None, boundary: np.ndarray | None = None, want_boundary=True,
                          flags=0):
         """Host-buffer entry point (coh_eval_traces_host): H2D, kernel and D2H inside the call."""
-        if records.dtype != np.uint16 or records.size < records_elems(n_traces, n_calls):
+        if flags & BATCH_PACKED12:
+            if records.dtype != np.uint8 or records.size < records_elems(n_traces, n_calls) // 8 * 12:
+                raise ValueError("packed records must be uint8, 12 bytes per 8-call chunk")
+        elif records.dtype != np.uint16 or records.size < records_elems(n_traces, n_calls):
             raise ValueError("records must be uint16 in the call-major interleaved layout")
         if results is None:
             results = np.zeros(n_traces, dtype=RESULT_DTYPE)

@@ -35,7 +35,9 @@ int validate(coh_ctx* ctx, const coh_trace_batch* b) {
   if (b->n_arrays < 1 || b->n_arrays > COH_MAX_ARRAYS)
     return arg_fail(ctx, "n_arrays must be in [1, 64], got " + std::to_string(b->n_arrays));
   if (b->n_traces && b->n_calls && !b->records) return arg_fail(ctx, "records is NULL");
-  if (b->flags & ~COH_BATCH_BLOCKS) return arg_fail(ctx, "unknown batch flags");
+  if (b->flags & ~(COH_BATCH_BLOCKS | COH_BATCH_PACKED12)) return arg_fail(ctx, "unknown batch flags");
+  if ((b->flags & COH_BATCH_BLOCKS) && (b->flags & COH_BATCH_PACKED12))
+    return arg_fail(ctx, "COH_BATCH_PACKED12 records cannot carry COH_REC_CONT");
   return COH_OK;
 }
 
@@ -156,6 +158,7 @@ void coh_ctx_destroy(coh_ctx* ctx) {
   cudaFree(ctx->d_lut);
   cudaFree(ctx->d_slow);
   for (int k = 0; k < 2; ++k) {
+    cudaFree(ctx->d_pk[k]);
     cudaFree(ctx->d_rec[k]);
     cudaFree(ctx->d_res[k]);
     cudaFree(ctx->d_bnd[k]);
@@ -223,6 +226,23 @@ int coh_gen_records_blocks_host(uint64_t seed, uint64_t trace0, uint64_t n_trace
   return COH_OK;
 }
 
+int coh_pack_records12(const uint16_t* records, uint64_t n_traces, uint32_t n_calls, uint8_t* out) {
+  if ((n_traces && n_calls) && (!records || !out)) return COH_E_ARG;
+  const uint64_t chunks = (uint64_t)((n_calls + 7u) / 8u) * n_traces;
+  for (uint64_t q = 0; q < chunks; ++q) {
+    uint32_t w[3] = {0u, 0u, 0u};
+    for (uint32_t k = 0; k < 8; ++k) {
+      const uint16_t r = records[q * 8u + k];
+      const uint64_t v = ((uint64_t)COH_REC_ARRAY(r) << 6) | COH_REC_TYPE(r);
+      const uint32_t bit = 12u * k;
+      w[bit >> 5] |= (uint32_t)(v << (bit & 31u));
+      if ((bit & 31u) > 20u) w[(bit >> 5) + 1] |= (uint32_t)(v >> (32u - (bit & 31u)));
+    }
+    std::memcpy(out + q * 12u, w, 12);
+  }
+  return COH_OK;
+}
+
 int coh_gen_records_host(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
                          uint32_t n_arrays, uint32_t adv_per1024, uint16_t* h_records) {
   if (n_arrays < 1 || n_arrays > COH_MAX_ARRAYS) return COH_E_ARG;
@@ -242,6 +262,7 @@ int coh_eval_traces(coh_ctx* ctx, const coh_trace_batch* batch, coh_trace_result
                     uint32_t* d_boundary, void* stream) {
   int rc = validate(ctx, batch);
   if (rc) return rc;
+  if (batch->flags & COH_BATCH_PACKED12) return arg_fail(ctx, "COH_BATCH_PACKED12 is for coh_eval_traces_host");
   if (batch->n_traces && !d_results) return arg_fail(ctx, "d_results is NULL");
   return eval_device(ctx, batch, batch->records, batch->n_traces, d_results, d_boundary,
                      static_cast<cudaStream_t>(stream));
@@ -251,6 +272,7 @@ int coh_eval_traces_counted(coh_ctx* ctx, const coh_trace_batch* batch, coh_trac
                             uint32_t* d_boundary, uint64_t* d_counters, void* stream) {
   int rc = validate(ctx, batch);
   if (rc) return rc;
+  if (batch->flags & COH_BATCH_PACKED12) return arg_fail(ctx, "COH_BATCH_PACKED12 is for coh_eval_traces_host");
   if (batch->n_traces && !d_results) return arg_fail(ctx, "d_results is NULL");
   if (!d_counters) return arg_fail(ctx, "d_counters is NULL");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -270,15 +292,22 @@ int coh_eval_traces_host(coh_ctx* ctx, const coh_trace_batch* batch, coh_trace_r
   if (!h_results) return arg_fail(ctx, "h_results is NULL");
   const uint32_t n_chunks = (batch->n_calls + 7u) / 8u;
   const uint32_t n_words = coh_boundary_words(batch->n_calls);
+  const bool packed = batch->flags & COH_BATCH_PACKED12;
+  coh_trace_batch dev_batch = *batch;  // what the device sees after unpacking
+  dev_batch.flags &= ~COH_BATCH_PACKED12;
   // Slices of S traces: H2D of slice k+1 overlaps the kernel and D2H of slice k.
   uint64_t S = std::min<uint64_t>(n, 1ull << 17);
   const size_t rec_b = (size_t)n_chunks * 16u * S, res_b = sizeof(coh_trace_result) * S,
-               bnd_b = (size_t)n_words * 4u * S;
+               bnd_b = (size_t)n_words * 4u * S, pk_b = (size_t)n_chunks * 12u * S;
   for (int k = 0; k < 2; ++k) {
     if (!ctx->hs[k]) COH_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->hs[k], cudaStreamNonBlocking));
     if (ctx->rec_cap < rec_b) {
       cudaFree(ctx->d_rec[k]);
       COH_CUDA(ctx, cudaMalloc(&ctx->d_rec[k], std::max<size_t>(rec_b, 16)));
+    }
+    if (packed && ctx->pk_cap < pk_b) {
+      cudaFree(ctx->d_pk[k]);
+      COH_CUDA(ctx, cudaMalloc(&ctx->d_pk[k], std::max<size_t>(pk_b, 16)));
     }
     if (ctx->res_cap < res_b) {
       cudaFree(ctx->d_res[k]);
@@ -292,14 +321,27 @@ int coh_eval_traces_host(coh_ctx* ctx, const coh_trace_batch* batch, coh_trace_r
   ctx->rec_cap = std::max(ctx->rec_cap, rec_b);
   ctx->res_cap = std::max(ctx->res_cap, res_b);
   ctx->bnd_cap = std::max(ctx->bnd_cap, bnd_b);
+  if (packed) ctx->pk_cap = std::max(ctx->pk_cap, pk_b);
   int k = 0;
   for (uint64_t t0 = 0; t0 < n; t0 += S, k ^= 1) {
     const uint64_t m = std::min<uint64_t>(S, n - t0);
     cudaStream_t s = ctx->hs[k];
-    if (n_chunks)
+    if (n_chunks && packed) {
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(batch->records) + t0 * 12u;
+      COH_CUDA(ctx, cudaMemcpy2DAsync(ctx->d_pk[k], m * 12u, src, n * 12u, m * 12u, n_chunks,
+                                      cudaMemcpyHostToDevice, s));
+      std::string err;
+      rc = cohb::launch_unpack12(static_cast<const uint8_t*>(ctx->d_pk[k]), ctx->d_rec[k], m, n_chunks, s, &err);
+      if (rc) {
+        ctx->err = err;
+        return rc;
+      }
+      ctx->launches++;
+    } else if (n_chunks) {
       COH_CUDA(ctx, cudaMemcpy2DAsync(ctx->d_rec[k], m * 16u, batch->records + t0 * 8u, n * 16u,
                                       m * 16u, n_chunks, cudaMemcpyHostToDevice, s));
-    rc = eval_device(ctx, batch, ctx->d_rec[k], m, ctx->d_res[k], h_boundary ? ctx->d_bnd[k] : nullptr, s);
+    }
+    rc = eval_device(ctx, &dev_batch, ctx->d_rec[k], m, ctx->d_res[k], h_boundary ? ctx->d_bnd[k] : nullptr, s);
     if (rc) return rc;
     COH_CUDA(ctx, cudaMemcpyAsync(h_results + t0, ctx->d_res[k], sizeof(coh_trace_result) * m,
                                   cudaMemcpyDeviceToHost, s));

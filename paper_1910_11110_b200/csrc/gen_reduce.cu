@@ -49,6 +49,41 @@ __global__ void k_gen_blocks(uint64_t seed, uint64_t trace0, uint64_t n_traces, 
   }
 }
 
+// 12 bytes (8 calls of 12 bits) -> one 16-byte chunk of 16-bit records, per thread.
+__global__ void k_unpack12(const uint32_t* __restrict__ src, uint4* __restrict__ dst, uint64_t total) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t w0 = __ldcs(src + 3 * q), w1 = __ldcs(src + 3 * q + 1), w2 = __ldcs(src + 3 * q + 2);
+    const uint64_t lo = (uint64_t)w0 | ((uint64_t)w1 << 32);
+    uint32_t r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t bit = 12u * k;
+      uint32_t v;
+      if (bit + 12u <= 64u) v = (uint32_t)(lo >> bit) & 0xFFFu;
+      else if (bit >= 64u) v = (w2 >> (bit - 64u)) & 0xFFFu;
+      else v = (uint32_t)((lo >> bit) | ((uint64_t)w2 << (64u - bit))) & 0xFFFu;
+      r[k] = ((v >> 6) << 8) | ((v & 63u) << 2);  // array in bits 8-13, call type in bits 2-7
+    }
+    __stcs(dst + q, make_uint4(r[0] | (r[1] << 16), r[2] | (r[3] << 16), r[4] | (r[5] << 16), r[6] | (r[7] << 16)));
+  }
+}
+
+int launch_unpack12(const uint8_t* d_packed, uint16_t* d_records, uint64_t n_traces, uint32_t n_chunks, void* stream,
+                    std::string* err) {
+  const uint64_t total = (uint64_t)n_chunks * n_traces;
+  if (!total) return COH_OK;
+  uint64_t blocks = (total + 255) / 256;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  k_unpack12<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const uint32_t*>(d_packed), reinterpret_cast<uint4*>(d_records), total);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("unpack12 launch: ") + cudaGetErrorString(e);
+    return COH_E_CUDA;
+  }
+  return COH_OK;
+}
+
 int launch_gen_blocks(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls, uint32_t cont,
                       uint16_t* d_records, void* stream, std::string* err) {
   if (!n_traces || !n_calls || !cont) return COH_OK;

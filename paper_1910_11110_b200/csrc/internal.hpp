@@ -103,6 +103,9 @@ int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t n_
 int launch_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
                        uint32_t n_arrays, uint32_t adv_per1024, uint16_t* d_records, void* stream,
                        std::string* err);
+// COH_BATCH_PACKED12 slice -> the 16-bit call-major records (gen_reduce.cu).
+int launch_unpack12(const uint8_t* d_packed, uint16_t* d_records, uint64_t n_traces, uint32_t n_chunks, void* stream,
+                    std::string* err);
 int launch_gen_blocks(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls, uint32_t cont,
                       uint16_t* d_records, void* stream, std::string* err);
 int launch_reduce_counters(const coh_trace_result* d_results, uint64_t n_traces,
@@ -125,4 +128,6 @@ struct coh_ctx {
   coh_trace_result* d_res[2] = {nullptr, nullptr};
   uint32_t* d_bnd[2] = {nullptr, nullptr};
   size_t rec_cap = 0, res_cap = 0, bnd_cap = 0;  // bytes per buffer
+  void* d_pk[2] = {nullptr, nullptr};            // COH_BATCH_PACKED12 slices
+  size_t pk_cap = 0;
 };

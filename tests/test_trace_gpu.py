@@ -318,3 +318,17 @@ def test_dynamic_batches_long_launch(ctx, nc):
     for t in range(0, N, 4099)[:200]:
         w, _ = o.orc_eval(coh.gen_records_host(seed, t, 1, nc, na, adv), 1, nc, na, 10000)
         assert same(res[t:t + 1], w), t
+
+
+def test_packed12_host_entry_equals_plain(ctx):
+    """COH_BATCH_PACKED12: the host entry with 12-bit packed records (unpacked on the
+    device per slice) returns exactly what the 16-bit records give, across slices."""
+    nt, nc, na = (1 << 17) + 333, 96, 48
+    recs = coh.gen_records_host(4, 0, nt, nc, na, 64)
+    a, ab = ctx.eval_traces_host(recs, nt, nc, na)
+    pk = coh.pack_records12(recs, nt, nc)
+    assert pk.size == recs.size // 8 * 12
+    b, bb = ctx.eval_traces_host(pk, nt, nc, na, flags=coh.BATCH_PACKED12)
+    assert same(a, b) and np.array_equal(ab, bb)
+    with pytest.raises(coh.CohError):
+        ctx.eval_traces_host(pk, nt, nc, na, flags=coh.BATCH_PACKED12 | coh.BATCH_BLOCKS)
