@@ -11,13 +11,6 @@ namespace cohb {
 #endif
 constexpr uint32_t kDenseStep = COH_DENSE_STEP;  // runs per warp step above which the warp stages them
 
-}
-
-
-}  // namespace cohb
-
-namespace cohb {
-
 // Dense warp steps, staged: a step (32 lanes x 4 words = 4096 cells) has at most 2048
 // run starts (or ends).  Every lane writes its own set bits' cells, in ascending order,
 // into the warp's shared-memory buffer at S_lane + rank (independent per lane: no
