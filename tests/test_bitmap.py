@@ -140,3 +140,69 @@ def test_zero_runs_staging(ctx, pattern):
     off, st, en = zero_runs(ctx, dev, ranges, cap=cap)
     assert np.array_equal(off, want_off)
     assert np.array_equal(st, want_st[:cap]) and np.array_equal(en, want_en[:cap])
+
+
+def _ref_sync_cases(frag_log2, n_progs=12, n=1 << 14):
+    """(L, R, view range, site, sync runs or stuck cell) for whole-view syncs the reference
+    ran: for each generated element program, the longest prefix the reference completes
+    (Done), then one extra call R@site on view v with an empty body, whose guard is the
+    whole-view sync of v (site Remote: `push v`, needs L, sets R; Local: `pull v`, needs R,
+    sets L; elem_host.cpp closure/guard, ast.hpp:144)."""
+    import oracle_ffi as o
+    from paper_1910_11110_b200.elem import Program
+    out = []
+    for pid in range(n_progs):
+        g = Program.generate(51, pid, n, 8, 6, 0 if pid % 2 else 300, frag_log2=frag_log2)
+        calls = []
+        for i in range(g.n_calls):
+            c = g.calls[i]
+            calls.append((c.view, c.kind, c.site, [(c.body[k].effect, c.body[k].site, c.body[k].lo, c.body[k].hi)
+                                                  for k in range(c.n_body)]))
+        mk = lambda cs: Program(n, g.view_lo, g.view_hi, cs, frag_log2=frag_log2, frag_seed=g.frag_seed)
+        rc, r0, L0, R0, _, _, runs0 = o.elem_run("ref", mk(calls), 1 << 16)
+        assert rc == 0
+        if r0.status != 0:  # keep the prefix before the call that stopped it
+            calls = calls[: r0.stuck_call]
+            rc, r0, L0, R0, _, _, runs0 = o.elem_run("ref", mk(calls), 1 << 16)
+            assert rc == 0 and r0.status == 0
+        for v in range(len(g.view_lo)):
+            for site in (0, 1):
+                rc, r1, _, _, _, _, runs1 = o.elem_run("ref", mk(calls + [(v, 0, site, [])]), 1 << 16)
+                assert rc == 0
+                rng = (int(g.view_lo[v]), int(g.view_hi[v]))
+                if r1.status == 1 and r1.stuck_call == len(calls) and not (r1.stuck_flags & 2):
+                    out.append((L0, R0, rng, site, None, r1.stuck_index))
+                elif r1.status == 0 and r1.transfers == r0.transfers + 1:
+                    out.append((L0, R0, rng, site, runs1[len(runs0):], None))
+    return out
+
+
+@pytest.mark.parametrize("frag_log2", [8, 1])
+def test_zero_runs_equal_reference_sync_deltas(ctx, frag_log2):
+    """The primitives against syncs the reference itself ran (its own run_annotated over
+    its std::map store, from a pre-fragmented start): the transfer ranges of each sync
+    (maximal runs of its delta, semantics.hpp:155-166) equal coh_bitmap_extract_zero_runs
+    over the view on the destination plane, and a stuck sync names the cell
+    coh_bitmap_first_zero finds on the source plane (the first cell that fails, ascending)."""
+    import oracle_ffi as o
+    from paper_1910_11110_b200.bitmap import first_zero, zero_runs
+    if not o.have_ref():
+        pytest.skip("oracle/_ref not built")
+    cases = _ref_sync_cases(frag_log2)
+    n_runs = n_stuck = 0
+    for L0, R0, (lo, hi), site, runs, stuck in cases:
+        src, dst = (L0, R0) if site else (R0, L0)
+        ranges = np.zeros(1, RANGE_DTYPE)
+        ranges["word_off"], ranges["lo"], ranges["hi"] = 0, lo, hi
+        fz = int(first_zero(ctx, torch.from_numpy(src.view(np.int32).copy()).cuda(), ranges)[0])
+        if stuck is not None:
+            assert fz == stuck
+            n_stuck += 1
+            continue
+        assert fz == 0xFFFFFFFF
+        off, st, en = zero_runs(ctx, torch.from_numpy(dst.view(np.int32).copy()).cuda(), ranges, cap=1 << 16)
+        m = int(off[-1])
+        got = np.stack([st[:m], en[:m]], axis=1).astype(np.uint32)
+        assert np.array_equal(got, runs), (lo, hi, site)
+        n_runs += 1
+    assert n_runs >= 40 and n_stuck >= 2, (n_runs, n_stuck)
