@@ -45,6 +45,9 @@ namespace cohb {
 #ifndef COH_TE_MINB
 #define COH_TE_MINB 5
 #endif
+#ifndef COH_TE_MINB_LEAN
+#define COH_TE_MINB_LEAN 6
+#endif
 constexpr int kNT = COH_TE_NT;  // traces (threads) per block
 static_assert(kNT % 128 == 0 && kNT <= 512, "store regions hold 128 threads each");
 constexpr uint32_t kStoreBytes = COH_MAX_ARRAYS * kNT * 2u;
@@ -79,6 +82,7 @@ struct KParams {
   uint32_t* bnd;
   unsigned long long* counters;  // optional fused COH_N_COUNTERS reduction (zeroed by the launcher)
   unsigned int* ticket;          // dynamic trace batches handed out after the first round (zeroed)
+  uint32_t k65536;               // 65536, opaque to ptxas: the accumulate stays an IMAD.HI (FMA pipe)
 };
 
 // bnd = 2*bnd + (acc >= 0x2000): with the accumulator clean (steps | transfers << 7 |
@@ -122,9 +126,13 @@ __host__ __device__ constexpr uint32_t viol_threshold_addend(int c) { return (ui
   "setp.lt.or.s32 p, ev, 0, p;\n\t"                   \
   COH_PTX_ACC                                          \
   "st.shared.u16 [so+%5], ev;\n\t"                    \
-  "add.cc.u32 cy, %0, " T ";\n\t"                     \
-  "addc.u32 %1, %1, %1;\n\t"                          \
+  COH_PTX_BND(T)                                       \
   "SKIP:\n\t}\n\t"
+#ifdef COH_KO_BND
+#define COH_PTX_BND(T) ""
+#else
+#define COH_PTX_BND(T) "add.cc.u32 cy, %0, " T ";\n\taddc.u32 %1, %1, %1;\n\t"
+#endif
 #define COH_PTX_PAIR(R, T0, T1)        \
   COH_PTX_CALL(R, T0)                  \
   "mul.hi.u32 th, " R ", 65536;\n\t"  \
@@ -141,12 +149,12 @@ __host__ __device__ constexpr uint32_t viol_threshold_addend(int c) { return (ui
     "n"(viol_threshold_addend(8 * H + 0)), "n"(viol_threshold_addend(8 * H + 1)),                    \
     "n"(viol_threshold_addend(8 * H + 2)), "n"(viol_threshold_addend(8 * H + 3)),                    \
     "n"(viol_threshold_addend(8 * H + 4)), "n"(viol_threshold_addend(8 * H + 5)),                    \
-    "n"(viol_threshold_addend(8 * H + 6)), "n"(viol_threshold_addend(8 * H + 7))                     \
+    "n"(viol_threshold_addend(8 * H + 6)), "n"(viol_threshold_addend(8 * H + 7)), "r"(k65536)        \
   : "memory"
 
 template <bool FUEL, int H>
 __device__ __forceinline__ uint32_t run_chunk(const uint4 v, uint32_t toff, uint32_t& acc, uint32_t& bnd,
-                                              int fuel_left) {
+                                              int fuel_left, uint32_t k65536) {
   uint32_t stop;
   if (FUEL) {  // the call's steps must fit the remaining fuel, else it is the slow call
 #define COH_PTX_ACC                                 \
@@ -159,7 +167,13 @@ __device__ __forceinline__ uint32_t run_chunk(const uint4 v, uint32_t toff, uint
     asm volatile(COH_PTX_CHUNK COH_PTX_OPERANDS(H));
 #undef COH_PTX_ACC
   } else {
+#if defined(COH_KO_ACC)
+#define COH_PTX_ACC "@p bra SKIP;\n\t"
+#elif defined(COH_FMA_ACC)
+#define COH_PTX_ACC "@p bra SKIP;\n\tmad.hi.s32 %0, ev, %19, %0;\n\t"
+#else
 #define COH_PTX_ACC "@p bra SKIP;\n\tmul.hi.s32 cy, ev, 65536;\n\tadd.s32 %0, %0, cy;\n\t"
+#endif
     asm volatile(COH_PTX_CHUNK COH_PTX_OPERANDS(H));
 #undef COH_PTX_ACC
   }
@@ -177,14 +191,23 @@ __device__ __forceinline__ uint32_t pin_zero(uint32_t x) {
 // FLAGS: kFuel = fuel may run out (fuel < 6 x n_calls), kBytes = non-uniform array
 // sizes (per-call byte accumulation), kRing = n_calls % 32 == 0 (the record ring runs on
 // into the next trace).
-enum : int { kFuel = 1, kBytes = 2, kRing = 4, kDouble = 8 };
+enum : int { kFuel = 1, kBytes = 2, kRing = 4, kDouble = 8, kLean = 16 };
+
+// L2 prefetch of the 128-byte line holding a (no registers held until the data is needed).
+__device__ __forceinline__ void prefetch_l2(const void* a) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
 
 template <int FLAGS>
-__global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : COH_TE_MINB) k_trace_eval(const KParams p) {
+__global__ void __launch_bounds__(kNT, (FLAGS & kDouble)  ? COH_TE_MINB_DOUBLE
+                                       : (FLAGS & kLean) ? COH_TE_MINB_LEAN
+                                                         : COH_TE_MINB) k_trace_eval(const KParams p) {
   constexpr bool CHECK_FUEL = FLAGS & kFuel;
   constexpr bool UNIFORM = !(FLAGS & kBytes);
   constexpr bool RING = FLAGS & kRing;
   constexpr bool DOUBLE = FLAGS & kDouble;  // n_calls % 64 == 0: two register rings
+  constexpr bool LEAN = FLAGS & kLean;      // n_calls % 32 == 0: a 2-chunk ring fed from L2 prefetches
+  constexpr int kRingLen = LEAN ? 2 : 4;
   __shared__ TraceSmem sm;
   char* const stb = reinterpret_cast<char*>(sm.store);
   const char* const lutb = reinterpret_cast<const char*>(sm.lut);
@@ -202,11 +225,11 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
 #define COH_REC(C, U) __ldcs(p.rec + (uint64_t)(C) * n + (U))
   // The first trace's record loads and the table loads go out before the block's set-up,
   // so their latency overlaps it (the launch's fixed cost).
-  uint4 ring[4];
-  bool ring_ok = false;  // ring already holds chunks 0..3 of this thread's next trace
+  uint4 ring[kRingLen];
+  bool ring_ok = false;  // ring already holds chunks 0..kRingLen-1 of this thread's next trace
   if (blockIdx.x * kNT + tid < n) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < kRingLen; ++j)
       ring[j] = (uint32_t)j < n_chunks ? COH_REC(j, blockIdx.x * kNT + tid) : make_uint4(0u, 0u, 0u, 0u);
     ring_ok = true;
   }
@@ -236,6 +259,10 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
 #endif
 
   const uint32_t warp = tid >> 5, lane = tid & 31u;
+  const uint32_t k65536 = p.k65536;
+  // counters: packed warp sums need n_calls <= 256 (6 steps per call per lane fit 16 bits)
+  const bool packed_cnt = n_calls <= 256u;
+  uint32_t cnt_acc = 0;  // lane k < 10: warp total of counter k over this warp's traces
   // this thread's u16 column: 128 threads share a 16 KB region (64 array rows of 256 B);
   // region r sits at r << 14, so (record & 0x3F00) | toff addresses the slot
   const uint32_t toff = ((warp >> 2) << 14) | ((warp >> 1) & 1u) * 128u + 4u * lane + 2u * (warp & 1u);
@@ -295,7 +322,7 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
   COH_CALL(__umulhi((W), 0x10000u), (C) + 1)
 #define COH_CHUNK(V, H)                                                                   \
   if (UNIFORM) {                                                                          \
-    stop = run_chunk<CHECK_FUEL, H>((V), toff, acc, bnd, fuel_left);                      \
+    stop = run_chunk<CHECK_FUEL, H>((V), toff, acc, bnd, fuel_left, k65536);                      \
   } else {                                                                                \
     COH_PAIR((V).x, 8 * H) COH_PAIR((V).y, 8 * H + 2) COH_PAIR((V).z, 8 * H + 4)           \
     COH_PAIR((V).w, 8 * H + 6)                                                            \
@@ -313,7 +340,7 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
     {
       if (!ring_ok) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ring[j] = (uint32_t)j < n_chunks ? COH_REC(j, t) : make_uint4(0u, 0u, 0u, 0u);
+        for (int j = 0; j < kRingLen; ++j) ring[j] = (uint32_t)j < n_chunks ? COH_REC(j, t) : make_uint4(0u, 0u, 0u, 0u);
       }
       ring_ok = false;
 #define COH_GROUP_END(G)                                                          \
@@ -322,7 +349,39 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
   if (p.bnd) p.bnd[(uint64_t)(G) * n + t] = bnd;                                  \
   viol_blocks += 32u - __popc(bnd);                                               \
   bnd = 1u;
-      if (DOUBLE) {
+      if (LEAN) {
+        // One ring of two chunks, refilled right after each use (one chunk of lead); the
+        // lead is enough because the rows were prefetched into L2 two groups earlier
+        // (lanes 0-3 of the warp, one 512-byte bulk prefetch per chunk row of the warp's
+        // 32 traces).  Frees the registers of the deep rings for occupancy.
+        const uint64_t nb = 16ull * n;
+        const char* gp = reinterpret_cast<const char*>(p.rec + t) + 2u * nb;  // chunk 2
+        const char* const gnext = reinterpret_cast<const char*>(p.rec + (RING && tn < n ? tn : t));
+        const uint32_t wbase = t - lane;  // this warp's batch
+        for (uint32_t g = 0; g < n_groups; ++g) {
+          i0 = g * 32u;
+#ifndef COH_TE_NO_PF
+          if (lane < 16u) {  // rows of group g + 2 (the next batch's first rows near the end)
+            uint32_t row = 4u * (g + 2u) + (lane >> 2), b = wbase + 8u * (lane & 3u);
+            if (row >= n_chunks) row -= n_chunks, b = nxt + 8u * (lane & 3u);
+            if (row < n_chunks && b < n) prefetch_l2(p.rec + (uint64_t)row * n + b);
+          }
+#endif
+          COH_CHUNK(ring[0], 0)
+          ring[0] = __ldcs(reinterpret_cast<const uint4*>(gp + pin_zero(bnd)));
+          gp += nb;
+          COH_CHUNK(ring[1], 1) COH_FLUSH
+          ring[1] = __ldcs(reinterpret_cast<const uint4*>(gp + pin_zero(bnd)));
+          gp = g + 1u == n_groups ? gnext : gp + nb;
+          COH_CHUNK(ring[0], 0)
+          ring[0] = __ldcs(reinterpret_cast<const uint4*>(gp + pin_zero(bnd)));
+          gp += nb;
+          COH_CHUNK(ring[1], 1) COH_FLUSH
+          ring[1] = __ldcs(reinterpret_cast<const uint4*>(gp + pin_zero(bnd)));
+          gp += nb;
+          COH_GROUP_END(g)
+        }
+      } else if (DOUBLE) {
         // Two register rings, A = even groups, B = odd groups.  A group's four loads are
         // issued together right after its predecessor's first chunk, so every first use
         // (which waits for all outstanding loads: they share one scoreboard) has three
@@ -387,7 +446,7 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
       }
 #undef COH_GROUP_END
       if (RING) ring_ok = true;
-      if (!RING) {
+      if constexpr (!RING) {
         const uint32_t tail = n_calls - n_groups * 32u;
         if (tail) {
           i0 = n_groups * 32u;
@@ -466,12 +525,17 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
   finished : {
     // the final store, nibble-packed, and every slot reset for this thread's next trace
     uint32_t sw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#ifdef COH_KO_EPI_LDS
+#define COH_EPI_READ(P) init
+#else
+#define COH_EPI_READ(P) (*(P))
+#endif
     uint32_t init;  // kInit in a register (else ptxas rematerialises it before every store)
     asm volatile("mov.u32 %0, %1;" : "=r"(init) : "n"(kInit));
 #define COH_SLOT_OUT(A)                                                                \
   {                                                                                    \
     uint16_t* const wp = reinterpret_cast<uint16_t*>(stb + (A) * 256 + toff);          \
-    const uint32_t w = *wp;                                                            \
+    const uint32_t w = COH_EPI_READ(wp);                                               \
     *wp = (uint16_t)init;                                                              \
     const int sh = 4 * ((A) & 7) - 8; /* state nibble at slot bits 8-11 */             \
     sw[(A) >> 3] |= (sh >= 0 ? (w << sh) : (w >> -sh)) & (15u << (4 * ((A) & 7)));    \
@@ -508,8 +572,25 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
     __stcs(out + 2, make_uint4((uint32_t)tb, (uint32_t)(tb >> 32), steps, xfers));
     __stcs(out + 3, make_uint4(calls_done, viol_blocks, stuck_call,
                                status | (stuck_arr << 8) | (stuck_eff << 16) | (stuck_flags << 24)));
-    if (p.counters) {  // fused counter reduction: warp redux, one shared atomic per warp
-      const uint32_t m = __activemask();
+    const uint32_t m = p.counters ? __activemask() : 0u;
+    if (packed_cnt && m == 0xFFFFFFFFu) {
+      // a full warp: three warp reductions of packed fields (per-warp sums fit their 6 /
+      // 16 bits for n_calls <= 256), then lane k keeps counter k's running warp total in
+      // a register; the shared atomics happen once per thread, after the last trace
+      const uint32_t fl = __reduce_add_sync(
+          m, (status == COH_RUN_STUCK) | (uint32_t)(status == COH_RUN_FUEL_EXHAUSTED) << 6 |
+                 (uint32_t)(viol_blocks != 0u) << 12 | (uint32_t)(status == COH_RUN_DEFECT) << 18 |
+                 (uint32_t)((stuck_flags & COH_FLAG_UNSAFE) != 0u) << 24);
+      const uint32_t sx = __reduce_add_sync(m, steps | xfers << 16);
+      const uint32_t vc = __reduce_add_sync(m, viol_blocks | calls_done << 16);
+      // lanes 0-3 stuck / fuel / violating traces / defect, 4-5 steps / transfers,
+      // 6-7 violating blocks / calls done, 8 traces, 9 unsafe
+      const uint32_t w = lane < 4u || lane == 9u ? fl : lane < 6u ? sx : vc;
+      const uint32_t sh = lane < 4u ? 6u * lane : lane == 9u ? 24u : 16u * (lane & 1u);
+      const uint32_t v = lane == 8u ? (uint32_t)__popc(m) : (w >> sh) & (lane < 4u || lane == 9u ? 63u : 0xFFFFu);
+      cnt_acc += lane < 10u ? v : 0u;
+      if (!UNIFORM && tb) atomicAdd(&sm.cnt[6], (unsigned long long)tb);
+    } else if (m) {  // partial warps: per-counter warp reductions, one shared atomic per warp
       const bool leader = (lane == (uint32_t)(__ffs(m) - 1));
       uint32_t v[10] = {status == COH_RUN_STUCK, status == COH_RUN_FUEL_EXHAUSTED, viol_blocks != 0u,
                         status == COH_RUN_DEFECT, steps, xfers, viol_blocks, calls_done, 1u,
@@ -530,6 +611,11 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : 
   }
 #undef COH_REC
   if (p.counters) {
+    if (packed_cnt && lane < 10u && cnt_acc) {
+      const int slot = lane < 6u ? (int)lane : (int)lane + 1;  // 6 = bytes, below
+      atomicAdd(&sm.cnt[slot], (unsigned long long)cnt_acc);
+      if (UNIFORM && lane == 5u) atomicAdd(&sm.cnt[6], (unsigned long long)cnt_acc * p.bytes_uniform);
+    }
     __syncthreads();
     if (tid < COH_N_COUNTERS && sm.cnt[tid]) atomicAdd(p.counters + tid, sm.cnt[tid]);
   }
@@ -871,6 +957,8 @@ template <int F>
 static int launch_one(const TraceLaunch& L, const KParams& kp, cudaStream_t s, std::string* err) {
   static int occ = 0;  // resident blocks per SM of this variant
   if (!occ) {
+    // all of the SM's shared memory for the resident blocks (the store is 128 B per trace)
+    cudaFuncSetAttribute(k_trace_eval<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trace_eval<F>, kNT, 0);
     if (e != cudaSuccess || occ < 1) {
       *err = std::string("trace_eval occupancy: ") + cudaGetErrorString(e);
@@ -927,6 +1015,7 @@ int launch_trace_eval(const TraceLaunch& L, void* stream, std::string* err) {
   kp.bnd = L.boundary;
   kp.counters = reinterpret_cast<unsigned long long*>(L.counters);
   kp.ticket = L.ticket;
+  kp.k65536 = 65536u;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (L.counters) {
     cudaError_t e = cudaMemsetAsync(L.counters, 0, sizeof(uint64_t) * COH_N_COUNTERS, s);
@@ -950,14 +1039,16 @@ int launch_trace_eval(const TraceLaunch& L, void* stream, std::string* err) {
     }
     return COH_OK;
   }
-  const int f = (L.check_fuel ? kFuel : 0) | (L.uniform_bytes ? 0 : kBytes) |
-                (L.n_calls % 32u == 0u && L.n_calls >= 32u ? kRing : 0) |
-                (L.n_calls % 64u == 0u && L.n_calls >= 64u && !getenv_flag("COH_TE_SINGLE") ? kDouble : 0);
+  const bool ring = L.n_calls % 32u == 0u && L.n_calls >= 32u;
+  const bool lean = ring && getenv_flag("COH_TE_LEAN");
+  const int f = (L.check_fuel ? kFuel : 0) | (L.uniform_bytes ? 0 : kBytes) | (ring ? kRing : 0) | (lean ? kLean : 0) |
+                (!lean && L.n_calls % 64u == 0u && L.n_calls >= 64u && !getenv_flag("COH_TE_SINGLE") ? kDouble : 0);
   switch (f) {
 #define COH_CASE(F) \
   case F: return launch_one<F>(L, kp, s, err);
     COH_CASE(0) COH_CASE(1) COH_CASE(2) COH_CASE(3) COH_CASE(4) COH_CASE(5) COH_CASE(6) COH_CASE(7)
     COH_CASE(12) COH_CASE(13) COH_CASE(14) COH_CASE(15)
+    COH_CASE(20) COH_CASE(21) COH_CASE(22) COH_CASE(23)
 #undef COH_CASE
   }
   return COH_E_ARG;
