@@ -139,6 +139,26 @@ def ncu_issue(n_traces, kernel_ms, sm_mhz, sms):
                                               "peak = 4 x SMs x sampled SM clock"}
 
 
+def ncu_l1_pipe(n_traces, kernel_ms, sm_mhz, sms):
+    """The shared-memory / L1 data pipe of k_trace_eval (3 LDS/STS per call + the record
+    loads): wavefronts per launch from the committed ncu capture (scaled to this launch's
+    traces) over the measured kernel time, against one wavefront per clock per SM."""
+    p = os.path.join(ROOT, "profiles", "ncu_trace_eval.json")
+    if not os.path.exists(p) or not kernel_ms or not sm_mhz:
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    wf = d.get("metrics", {}).get("l1tex__data_pipe_lsu_wavefronts.sum")
+    if not wf or not d.get("traces_per_launch"):
+        return None
+    wf = wf * n_traces / d["traces_per_launch"]
+    achieved = wf / (kernel_ms / 1e3)
+    peak = 1.0 * sms * sm_mhz * 1e6
+    return {"bound": "l1_data_pipe", "achieved": achieved, "peak": peak, "unit": "wavefronts/s", "frac": achieved / peak,
+            "wavefronts_per_launch": wf, "source": "profiles/ncu_trace_eval.json l1tex__data_pipe_lsu_wavefronts.sum, "
+                                                   "peak = 1 x SMs x sampled SM clock"}
+
+
 def ncu_traffic():
     """dram bytes per trace_eval launch from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_trace_eval.json")
@@ -983,9 +1003,13 @@ def run_ours(args, rank, world, local):
             "roofline": {"bound": "hbm", "kernel": "k_trace_eval", "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms": k_ms,
-                         "note": "INT/LSU-issue bound in practice: see `issue` (the binding roofline) and profiles/",
+                         "note": "bound in practice by the L1 data pipe (shared-memory wavefronts, ~80% is its "
+                                 "practical ceiling) together with instruction issue: see `l1_data_pipe`, `issue` "
+                                 "and profiles/",
                          "issue": ncu_issue(N, k_ms, (clk or {}).get("sm_mhz"), torch.cuda.get_device_properties(dev)
-                                            .multi_processor_count)},
+                                            .multi_processor_count),
+                         "l1_data_pipe": ncu_l1_pipe(N, k_ms, (clk or {}).get("sm_mhz"),
+                                                     torch.cuda.get_device_properties(dev).multi_processor_count)},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
             "bitmap": bitmap, "container": container, "sweep": sweep_info, "c1": c1, "c4": c4, "overlap": overlap,
             "checker": checker, "blocks": blocks,

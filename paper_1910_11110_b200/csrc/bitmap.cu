@@ -33,8 +33,18 @@ namespace {
 
 constexpr uint32_t kBT = 256;   // threads per block
 constexpr int kU = 4;           // warp steps in flight
-constexpr int kRU = 4;          // warp steps in flight in the zero-run walker (chunk_runs)
-constexpr uint32_t kRunsBuf = 1024;  // dense-step staging entries per warp (two passes above)
+#ifndef COH_RUNS_RU
+#define COH_RUNS_RU 4
+#endif
+#ifndef COH_RUNS_MINB
+#define COH_RUNS_MINB 4
+#endif
+constexpr int kRU = COH_RUNS_RU;  // warp steps in flight in the zero-run walker (chunk_runs)
+#ifndef COH_RUNS_PF
+#define COH_RUNS_PF 1
+#endif
+constexpr int kRunsPf = COH_RUNS_PF;  // walker iterations between an L2 prefetch and its loads
+constexpr uint32_t kRunsBuf = kStageBuf16 / 2;  // dense-step staging per warp, u32 words (2048 u16 entries)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 struct Flat {
@@ -437,9 +447,36 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
     // per-quad range tracking, masks or edge loads.
     if (interior_iteration<kRU>(base, f1, qend, qa0, qtf, qtl)) {
       const uint64_t qb = qa0 + base + lane;
+#ifndef COH_RUNS_NO_PF
+      {  // L2 prefetch of the iteration kRunsPf ahead (16 lanes x one 128-byte line), when it
+         // still lies in this chunk and range: the loads then wait on L2, not HBM
+        const uint64_t b2 = base + 32ull * kRU * kRunsPf;
+        if (lane < 4u * kRU && b2 + 32ull * kRU <= f1 && b2 + 32ull * kRU <= qend)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint4*>(words) + qa0 + b2 + 8u * lane));
+      }
+#endif
       uint4 v[kRU];
 #pragma unroll
       for (int u = 0; u < kRU; ++u) v[u] = __ldcg(reinterpret_cast<const uint4*>(words) + qb + 32ull * u);
+      // the word after the iteration (inside the range: the iteration's quads are interior),
+      // loaded with the others so that no step waits on it
+      const uint32_t nw_it = __ldg(words + (qa0 + base + 32ull * kRU) * 4);
+      const uint32_t pw_it = carry_ok ? carry : __ldg(words + (qa0 + base) * 4 - 1);
+      {  // whole-iteration fast exits (one vote pair for kRU steps): no zero cell at all, or
+         // all zero cells with set cells on neither side (one run continues through)
+        uint32_t o = 0u, a = 0xFFFFFFFFu;
+#pragma unroll
+        for (int u = 0; u < kRU; ++u) {
+          o |= v[u].x | v[u].y | v[u].z | v[u].w;
+          a &= v[u].x & v[u].y & v[u].z & v[u].w;
+        }
+        if (__all_sync(0xFFFFFFFFu, a == 0xFFFFFFFFu) ||
+            (__all_sync(0xFFFFFFFFu, o == 0u) && !((pw_it >> 31) | (nw_it & 1u)))) {
+          carry = __shfl_sync(0xFFFFFFFFu, v[kRU - 1].w, 31);
+          carry_ok = true;
+          continue;
+        }
+      }
 
 #pragma unroll
       for (int u = 0; u < kRU; ++u) {
@@ -447,11 +484,8 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
         if (__all_sync(0xFFFFFFFFu, a4 == 0xFFFFFFFFu)) continue;
         // the words just before and after the step (warp-uniform; the iteration lies
         // inside the range, so both exist)
-        const uint64_t q0 = qa0 + base + 32ull * u;  // lane 0's quad
-        const uint32_t pw0 = u ? __shfl_sync(0xFFFFFFFFu, v[u ? u - 1 : 0].w, 31)
-                               : (carry_ok ? carry : __ldg(words + q0 * 4 - 1));
-        const uint32_t nw31 = u < kRU - 1 ? __shfl_sync(0xFFFFFFFFu, v[u < kRU - 1 ? u + 1 : 0].x, 0)
-                                         : __ldg(words + (q0 + 32) * 4);
+        const uint32_t pw0 = u ? __shfl_sync(0xFFFFFFFFu, v[u ? u - 1 : 0].w, 31) : pw_it;
+        const uint32_t nw31 = u < kRU - 1 ? __shfl_sync(0xFFFFFFFFu, v[u < kRU - 1 ? u + 1 : 0].x, 0) : nw_it;
         if (__all_sync(0xFFFFFFFFu, (v[u].x | v[u].y | v[u].z | v[u].w) == 0u) && !((pw0 >> 31) | (nw31 & 1u)))
           continue;  // one zero run continues through the step
         uint32_t pw = __shfl_up_sync(0xFFFFFFFFu, v[u].w, 1);
@@ -508,12 +542,42 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
 // at the first quad of every range that begins in the chunk.  An exclusive scan of the
 // chunk counts gives every chunk its global offsets.  Place: each warp copies its staged
 // runs to their global positions; only a chunk with more than kRunCap runs walks its
-// quads again.  Sparse planes (the usual sync destination) are therefore read once.  (A
-// single-pass decoupled look-back over ticketed chunks was measured slower on B200: the
-// first wave's look-backs walk back over thousands of aggregates.)
+// quads again.  Sparse planes (the usual sync destination) are therefore read once.
+// (Measured alternatives on B200: a single-pass decoupled look-back over ticketed chunks
+// -- the first wave's look-backs walk back over thousands of aggregates; a count-only
+// first pass with a step bitmap and a place pass visiting the marked steps -- the place
+// pass then waits on a dependent chain of loads per marked step, 54 us at rho = 2^-16
+// against 16 us for copying staged runs; one cooperative kernel with a grid barrier
+// between the passes -- no faster than the two launches.)
 constexpr uint32_t kRunCap = 4096;
+// Sparse emission of one lane's starts (or ends) m[0..3] at out[pos ..) (pos = the lane's
+// first position): the lowest set bit of every word goes out without a loop (its position
+// is known from the popcounts of the words before it), the rare further bits of a word in
+// a warp-uniform second round.
+__device__ __forceinline__ void emit_sparse(const uint32_t* m, uint64_t pos, uint32_t cb, uint32_t* out, uint64_t cap) {
+  uint32_t rest = 0;
+  uint64_t p = pos;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (m[k] && p < cap) out[p] = cb + 32u * k + (uint32_t)(__ffs(m[k]) - 1);
+    rest |= m[k] & (m[k] - 1u);
+    p += (uint32_t)__popc(m[k]);
+  }
+  if (!__any_sync(0xFFFFFFFFu, rest != 0u)) return;
+  p = pos;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t x = m[k] & (m[k] - 1u);
+    uint64_t q = p + 1u;
+    for (; x; x &= x - 1u, ++q)
+      if (q < cap) out[q] = cb + 32u * k + (uint32_t)(__ffs(x) - 1);
+    p += (uint32_t)__popc(m[k]);
+  }
+}
+
 // Places the starts / ends of one warp step at chunk-relative (STAGE) or global positions
-// s.., e.. (warp-synchronous; s and e advance by the warp's totals).
+// s.., e.. (warp-synchronous; s and e advance by the warp's totals).  STAGE also records,
+// at the first flat quad of a range (at_start), the chunk-local start count before it.
 template <bool STAGE>
 __device__ __forceinline__ void place_step(const Flat& F, uint64_t f, uint32_t r, uint64_t qa, bool at_start,
                                            const uint32_t* st, const uint32_t* en, uint64_t& gs, uint64_t& ge,
@@ -523,40 +587,30 @@ __device__ __forceinline__ void place_step(const Flat& F, uint64_t f, uint32_t r
   const uint32_t ns = __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
   const uint32_t ne = __popc(en[0]) + __popc(en[1]) + __popc(en[2]) + __popc(en[3]);
   if (!__any_sync(0xFFFFFFFFu, ns || ne || (STAGE && at_start))) return;  // nothing to place in this step
-  uint32_t ps = ns, pe = ne;  // inclusive warp scans
+  // inclusive warp scan of both counts packed in one word (a step has at most 2048 of each)
+  const uint32_t nse = ns | (ne << 16);
+  uint32_t pse = nse;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, ps, o), b = __shfl_up_sync(0xFFFFFFFFu, pe, o);
-    if (lane >= (uint32_t)o) {
-      ps += a;
-      pe += b;
-    }
+    const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, pse, o);
+    if (lane >= (uint32_t)o) pse += a;
   }
-  uint64_t s = gs + ps - ns, e = ge + pe - ne;
+  const uint32_t xs = (pse - nse) & 0xFFFFu, xe = (pse - nse) >> 16;  // exclusive
   if (STAGE && at_start)  // the first flat quad of range r (and of the empty ranges just before it)
-    for (int64_t q = r; q >= 0 && F.qp[q] == f; --q) off_local[q] = (uint32_t)s;
-  const uint32_t Ts = __shfl_sync(0xFFFFFFFFu, ps, 31), Te = __shfl_sync(0xFFFFFFFFu, pe, 31);
+    for (int64_t q = r; q >= 0 && F.qp[q] == f; --q) off_local[q] = (uint32_t)(gs + xs);
+  const uint32_t T = __shfl_sync(0xFFFFFFFFu, pse, 31), Ts = T & 0xFFFFu, Te = T >> 16;
+  const uint32_t cb = (uint32_t)((qa * 4 - F.r[r].word_off) * 32);  // the lane's first cell
   if (Ts + Te > kDenseStep) {  // staged in shared memory, written with coalesced stores
-    const uint32_t cb = (uint32_t)((qa * 4 - F.r[r].word_off) * 32);
-    emit_staged<kRunsBuf>(st, ps - ns, Ts, cb, gs, out_s, cap, wbuf);
-    emit_staged<kRunsBuf>(en, pe - ne, Te, cb, ge, out_e, cap, wbuf);
-  } else if (ns | ne) {  // sparse step: each lane writes its few runs
-    const uint64_t wbase = qa * 4 - F.r[r].word_off;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint64_t cell0 = (wbase + k) * 32;
-      uint32_t a = st[k], b = en[k];
-      while (a) {
-        if (s < cap) out_s[s] = (uint32_t)(cell0 + __ffs(a) - 1);
-        ++s;
-        a &= a - 1;
-      }
-      while (b) {
-        if (e < cap) out_e[e] = (uint32_t)(cell0 + __ffs(b) - 1);
-        ++e;
-        b &= b - 1;
-      }
+    if (__all_sync(0xFFFFFFFFu, cb - __shfl_sync(0xFFFFFFFFu, cb, 0) < 4096u)) {  // lanes on consecutive quads
+      emit_dense16(st, xs, Ts, cb, gs, out_s, cap, reinterpret_cast<uint16_t*>(wbuf));
+      emit_dense16(en, xe, Te, cb, ge, out_e, cap, reinterpret_cast<uint16_t*>(wbuf));
+    } else {  // lanes in different ranges (edge steps): u32 entries, in passes
+      emit_staged<kRunsBuf>(st, xs, Ts, cb, gs, out_s, cap, wbuf);
+      emit_staged<kRunsBuf>(en, xe, Te, cb, ge, out_e, cap, wbuf);
     }
+  } else {  // sparse step: each lane writes its few runs
+    if (__any_sync(0xFFFFFFFFu, ns != 0u)) emit_sparse(st, gs + xs, cb, out_s, cap);
+    if (__any_sync(0xFFFFFFFFu, ne != 0u)) emit_sparse(en, ge + xe, cb, out_e, cap);
   }
   gs += Ts;
   ge += Te;
@@ -564,13 +618,19 @@ __device__ __forceinline__ void place_step(const Flat& F, uint64_t f, uint32_t r
 
 // Collect pass.  Per warp chunk: start / end counts (chunk_s, chunk_e) and staged runs;
 // per block: its totals (block_s, block_e).  Every place block scans the block totals
-// itself (a few hundred entries), so neither a ticket nor a zeroing memset is needed.
+// itself (a few hundred entries), so neither a ticket nor a zeroing memset is needed.  The
+// place pass is launched as its programmatic dependent: it may start (and scan the range
+// list) while the last collect blocks finish.
 struct RunCounts {
   uint64_t *chunk_s, *chunk_e, *block_s, *block_e;
 };
 
-__global__ void __launch_bounds__(kBT, 4) k_runs_collect(const uint32_t* words, Flat Fg, RunCounts C, uint32_t* stage,
-                                                         uint32_t* off_local) {
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+__global__ void __launch_bounds__(kBT, COH_RUNS_MINB) k_runs_collect(const uint32_t* words, Flat Fg, RunCounts C,
+                                                                     uint32_t* stage, uint32_t* off_local) {
+  griddep_launch();
   COH_BM_PROLOGUE
   extern __shared__ uint32_t runs_smem[];  // kBT / 32 warps x kRunsBuf: dense run staging
   uint32_t* const wbuf = runs_smem + (threadIdx.x >> 5) * kRunsBuf;
@@ -607,7 +667,7 @@ __global__ void __launch_bounds__(kBT, 4) k_runs_collect(const uint32_t* words, 
 
 // Exclusive scans of a[0..n) and b[0..n) into sa / sb (n + 1 entries, the last = totals),
 // one block of kBT threads, n <= kBT * kPer.
-constexpr uint32_t kMaxCollectBlocks = 2048;
+constexpr uint32_t kMaxCollectBlocks = 2048;  // count-pass blocks (one wave)
 __device__ void block_scan2(const uint64_t* a, const uint64_t* b, uint32_t n, uint64_t* sa, uint64_t* sb) {
   constexpr uint32_t kPer = kMaxCollectBlocks / kBT;
   __shared__ uint64_t wsum[2][kBT / 32];
@@ -667,15 +727,18 @@ __device__ __forceinline__ void chunk_offsets(const RunCounts& C, const uint64_t
 
 // Place pass, plus run_off[i] = global index of range i's first run: its chunk's offset +
 // the chunk-local count staged by the collect pass; ranges starting at the end get the
-// total.
-__global__ void __launch_bounds__(kBT, 4) k_runs_place(const uint32_t* words, Flat Fg, RunCounts C,
-                                                       const uint32_t* stage, const uint32_t* off_local,
-                                                       uint32_t* run_start, uint32_t* run_end, uint64_t cap,
-                                                       uint64_t* run_off) {
-  COH_BM_PROLOGUE
-  extern __shared__ uint32_t runs_smem[];  // kBT / 32 warps x kRunsBuf: dense run staging
+// total.  Dynamic shared memory: kBT / 32 warps x kRunsBuf (dense run staging), then the
+// exclusive scans of the collect blocks' totals (gridDim.x + 1 each).
+__global__ void __launch_bounds__(kBT, COH_RUNS_MINB) k_runs_place(const uint32_t* words, Flat Fg, RunCounts C,
+                                                                   const uint32_t* stage, const uint32_t* off_local,
+                                                                   uint32_t* run_start, uint32_t* run_end, uint64_t cap,
+                                                                   uint64_t* run_off) {
+  COH_BM_PROLOGUE  // the range list is an input of both passes: scanned before the wait
+  griddep_wait();  // the collect pass is complete and its writes are visible
+  extern __shared__ __align__(16) uint32_t runs_smem[];
   uint32_t* const wbuf = runs_smem + (threadIdx.x >> 5) * kRunsBuf;
-  __shared__ uint64_t bs[kMaxCollectBlocks + 1], be[kMaxCollectBlocks + 1];
+  uint64_t* const bs = reinterpret_cast<uint64_t*>(runs_smem + (kBT / 32) * kRunsBuf);
+  uint64_t* const be = bs + gridDim.x + 1;
   block_scan2(C.block_s, C.block_e, gridDim.x, bs, be);
   const uint64_t Q = F.qp[F.n], n_chunks = (uint64_t)gridDim.x * (kBT / 32);
   const uint64_t cper = (((Q + n_chunks - 1) / n_chunks) + 31) & ~31ull;  // as warp_chunk
@@ -694,7 +757,7 @@ __global__ void __launch_bounds__(kBT, 4) k_runs_place(const uint32_t* words, Fl
   uint64_t gs, ge;
   chunk_offsets(C, bs, be, wid, gs, ge);
   const uint64_t cs = C.chunk_s[wid], ce = C.chunk_e[wid];
-  if (cs <= kRunCap && ce <= kRunCap) {
+  if (cs <= kRunCap && ce <= kRunCap) {  // staged by the collect pass: copy
     const uint32_t* const ss = stage + wid * (2 * kRunCap);
     for (uint32_t i = threadIdx.x & 31; i < cs; i += 32)
       if (gs + i < cap) run_start[gs + i] = ss[i];
@@ -805,12 +868,13 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   COH_BM_FLAT(ctx, d_ranges, n, s)
   // one wave of the collect pass (the place pass reuses its warp -> chunk mapping)
+  constexpr size_t kRunsSmem = (size_t)(kBT / 32) * kRunsBuf * 4u;
   int occ = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_runs_collect, kBT, 0);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_runs_collect, kBT, kRunsSmem);
   if (e != cudaSuccess) return fail(ctx, "zero_runs occupancy", e);
   const int grid = ctx->sms * (occ > 0 ? occ : 1);
-  const uint64_t n_chunks = (uint64_t)grid * (kBT / 32);
   if (grid > (int)kMaxCollectBlocks) return fail(ctx, "zero_runs grid", cudaErrorInvalidConfiguration);
+  const uint64_t n_chunks = (uint64_t)grid * (kBT / 32);
   // scratch: run counts (see RunCounts, all written by the collect pass), staged runs,
   // chunk-local range offsets
   const size_t counts_b = sizeof(uint64_t) * (2 * n_chunks + 2 * (size_t)grid);
@@ -826,13 +890,30 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   C.block_e = C.block_s + grid;
   uint32_t* stage = reinterpret_cast<uint32_t*>(static_cast<char*>(co.p) + counts_b);
   uint32_t* off_local = stage + 2 * kRunCap * n_chunks;
-  constexpr size_t kRunsSmem = (size_t)(kBT / 32) * kRunsBuf * 4u;
-  const bool smem_ok =  // per call: the attribute belongs to the current device
-      cudaFuncSetAttribute(k_runs_collect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRunsSmem) == cudaSuccess &&
-      cudaFuncSetAttribute(k_runs_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRunsSmem) == cudaSuccess;
-  if (!smem_ok) return fail(ctx, "zero runs: shared memory attribute", cudaErrorInvalidValue);
+  const size_t place_smem = kRunsSmem + sizeof(uint64_t) * 2 * ((size_t)grid + 1);
+  if ((e = cudaFuncSetAttribute(k_runs_collect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRunsSmem)) !=
+          cudaSuccess ||
+      (e = cudaFuncSetAttribute(k_runs_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)place_smem)) !=
+          cudaSuccess)
+    return fail(ctx, "zero runs: shared memory attribute", e);
   k_runs_collect<<<grid, kBT, kRunsSmem, s>>>(d_words, F, C, stage, off_local);
-  k_runs_place<<<grid, kBT, kRunsSmem, s>>>(d_words, F, C, stage, off_local, d_run_start, d_run_end, cap, d_run_off);
+  {  // the place pass as the collect pass's programmatic dependent
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kBT);
+    cfg.dynamicSmemBytes = place_smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const Flat Fc = F;
+    const uint32_t* stage_c = stage;
+    const uint32_t* off_c = off_local;
+    e = cudaLaunchKernelEx(&cfg, k_runs_place, d_words, Fc, C, stage_c, off_c, d_run_start, d_run_end, cap, d_run_off);
+    if (e != cudaSuccess) return fail(ctx, "zero_runs place launch", e);
+  }
   ctx->launches += 2;
   return check(ctx, "zero_runs");
 }

@@ -43,4 +43,35 @@ __device__ __forceinline__ void emit_staged(const uint32_t* m, uint32_t S, uint3
   }
 }
 
+// The same for one warp step whose lanes cover consecutive 128-cell spans (lane L's first
+// cell = lane 0's + 128 L): entries are u16 offsets from lane 0's first cell, so a whole
+// step (at most 2048 starts or ends) fits one pass of a 4 KB buffer -- no lane re-walks its
+// bits for a second pass.  Bits are taken lowest first (x & -x, FLO).  Buffer index o is
+// stored at o ^ (((o >> 6) & 31) << 1): lanes whose offsets are ~32 apart hit different
+// banks.
+constexpr uint32_t kStageBuf16 = 2048;  // u16 entries per warp
+__device__ __forceinline__ uint32_t stage_swz16(uint32_t o) { return o ^ (((o >> 6) & 31u) << 1); }
+
+__device__ __forceinline__ void emit_dense16(const uint32_t* m, uint32_t S, uint32_t T, uint32_t cb, uint64_t base,
+                                             uint32_t* out, uint64_t cap, uint16_t* buf) {
+  if (base >= cap) return;  // warp-uniform: nothing of this step fits
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t cell0 = __shfl_sync(0xFFFFFFFFu, cb, 0);
+  const uint32_t rel = cb - cell0;
+  uint32_t o = S;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t rk = rel + 32u * k;
+    for (uint32_t x = m[k]; x; ++o) {
+      const uint32_t low = x & (0u - x);
+      buf[stage_swz16(o)] = (uint16_t)(rk + (31u - __clz(low)));
+      x ^= low;
+    }
+  }
+  __syncwarp();
+  const uint32_t n = (uint64_t)T < cap - base ? T : (uint32_t)(cap - base);
+  for (uint32_t p = lane; p < n; p += 32) out[base + p] = cell0 + buf[stage_swz16(p)];
+  __syncwarp();  // the buffer is free again
+}
+
 }  // namespace cohb

@@ -19,6 +19,10 @@ KEYS = [
     "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
     "sm__cycles_elapsed.avg.per_second",
+    "l1tex__data_pipe_lsu_wavefronts.sum", "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
+    "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
 ]
 
 
@@ -40,6 +44,15 @@ def main():
                 except ValueError:
                     d[k] = v
                 d[k + ".unit"] = units[i]
+        # the per-SM average is all the raw page has for the whole data pipe: x SMs
+        ka, kn = "SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts.avg", "device__attribute_multiprocessor_count"
+        if ka in hdr and kn in hdr and "l1tex__data_pipe_lsu_wavefronts.sum" not in hdr:
+            try:
+                d["l1tex__data_pipe_lsu_wavefronts.sum"] = float(vals[hdr.index(ka)].replace(",", "")) * \
+                    float(vals[hdr.index(kn)].replace(",", ""))
+                d["l1tex__data_pipe_lsu_wavefronts.sum.unit"] = "wavefront (per-SM avg x SMs)"
+            except ValueError:
+                pass
         kernels.append(d)
     pick = sys.argv[4] if len(sys.argv) > 4 else ""
     k = next(kk for kk in kernels if pick in kk["kernel"])

@@ -22,6 +22,9 @@ ranges["hi"] = n - 1 - rng.integers(0, n // 5, P)
 plane = torch.full((P * words,), -1, dtype=torch.int32, device="cuda")
 for _ in range(ands):
     plane &= torch.randint(-(1 << 31), 1 << 31, (P * words,), dtype=torch.int32, device="cuda")
+# argv[2] == "full": room for every run (rho = 1/2 has a run every ~4 cells)
+m = int((ranges["hi"].astype(np.int64) - ranges["lo"] + 1).sum())
+cap = m // 3 + 16 if len(sys.argv) > 2 and sys.argv[2] == "full" else 1 << 26
 for _ in range(2):
-    off, st, en = zero_runs(ctx, plane, ranges, cap=1 << 26)
+    off, st, en = zero_runs(ctx, plane, ranges, cap=cap)
 print("runs", int(off[-1]))
