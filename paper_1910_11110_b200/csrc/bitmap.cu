@@ -37,7 +37,7 @@ constexpr int kU = 4;           // warp steps in flight
 #define COH_RUNS_RU 4
 #endif
 #ifndef COH_RUNS_MINB
-#define COH_RUNS_MINB 4
+#define COH_RUNS_MINB 3
 #endif
 constexpr int kRU = COH_RUNS_RU;  // warp steps in flight in the zero-run walker (chunk_runs)
 #ifndef COH_RUNS_PF
@@ -449,7 +449,8 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
       const uint64_t qb = qa0 + base + lane;
 #ifndef COH_RUNS_NO_PF
       {  // L2 prefetch of the iteration kRunsPf ahead (16 lanes x one 128-byte line), when it
-         // still lies in this chunk and range: the loads then wait on L2, not HBM
+         // still lies in this chunk and range: the loads then wait on L2, not HBM.  (Loading
+         // the next iteration into a second register ring instead was measured no faster.)
         const uint64_t b2 = base + 32ull * kRU * kRunsPf;
         if (lane < 4u * kRU && b2 + 32ull * kRU <= f1 && b2 + 32ull * kRU <= qend)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint4*>(words) + qa0 + b2 + 8u * lane));
@@ -550,31 +551,6 @@ __device__ __forceinline__ void chunk_runs(const uint32_t* words, const Flat& F,
 // against 16 us for copying staged runs; one cooperative kernel with a grid barrier
 // between the passes -- no faster than the two launches.)
 constexpr uint32_t kRunCap = 4096;
-// Sparse emission of one lane's starts (or ends) m[0..3] at out[pos ..) (pos = the lane's
-// first position): the lowest set bit of every word goes out without a loop (its position
-// is known from the popcounts of the words before it), the rare further bits of a word in
-// a warp-uniform second round.
-__device__ __forceinline__ void emit_sparse(const uint32_t* m, uint64_t pos, uint32_t cb, uint32_t* out, uint64_t cap) {
-  uint32_t rest = 0;
-  uint64_t p = pos;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (m[k] && p < cap) out[p] = cb + 32u * k + (uint32_t)(__ffs(m[k]) - 1);
-    rest |= m[k] & (m[k] - 1u);
-    p += (uint32_t)__popc(m[k]);
-  }
-  if (!__any_sync(0xFFFFFFFFu, rest != 0u)) return;
-  p = pos;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    uint32_t x = m[k] & (m[k] - 1u);
-    uint64_t q = p + 1u;
-    for (; x; x &= x - 1u, ++q)
-      if (q < cap) out[q] = cb + 32u * k + (uint32_t)(__ffs(x) - 1);
-    p += (uint32_t)__popc(m[k]);
-  }
-}
-
 // Places the starts / ends of one warp step at chunk-relative (STAGE) or global positions
 // s.., e.. (warp-synchronous; s and e advance by the warp's totals).  STAGE also records,
 // at the first flat quad of a range (at_start), the chunk-local start count before it.
@@ -587,18 +563,10 @@ __device__ __forceinline__ void place_step(const Flat& F, uint64_t f, uint32_t r
   const uint32_t ns = __popc(st[0]) + __popc(st[1]) + __popc(st[2]) + __popc(st[3]);
   const uint32_t ne = __popc(en[0]) + __popc(en[1]) + __popc(en[2]) + __popc(en[3]);
   if (!__any_sync(0xFFFFFFFFu, ns || ne || (STAGE && at_start))) return;  // nothing to place in this step
-  // inclusive warp scan of both counts packed in one word (a step has at most 2048 of each)
-  const uint32_t nse = ns | (ne << 16);
-  uint32_t pse = nse;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, pse, o);
-    if (lane >= (uint32_t)o) pse += a;
-  }
-  const uint32_t xs = (pse - nse) & 0xFFFFu, xe = (pse - nse) >> 16;  // exclusive
+  uint32_t xs, xe, Ts, Te;  // exclusive positions of the lane's first start / end, step totals
+  step_positions(ns, ne, xs, xe, Ts, Te);
   if (STAGE && at_start)  // the first flat quad of range r (and of the empty ranges just before it)
     for (int64_t q = r; q >= 0 && F.qp[q] == f; --q) off_local[q] = (uint32_t)(gs + xs);
-  const uint32_t T = __shfl_sync(0xFFFFFFFFu, pse, 31), Ts = T & 0xFFFFu, Te = T >> 16;
   const uint32_t cb = (uint32_t)((qa * 4 - F.r[r].word_off) * 32);  // the lane's first cell
   if (Ts + Te > kDenseStep) {  // staged in shared memory, written with coalesced stores
     if (__all_sync(0xFFFFFFFFu, cb - __shfl_sync(0xFFFFFFFFu, cb, 0) < 4096u)) {  // lanes on consecutive quads

@@ -386,9 +386,9 @@ constexpr int kApplyWarps = 8;
 constexpr int kApplyU = 4;  // warp steps of an edge tile loaded together
 constexpr int kWPL = kElemTileWords / 32;  // 64 words per lane
 __global__ void __launch_bounds__(32 * kApplyWarps, 3) k_elem_apply(const ElemDev d, uint32_t n_sync_tiles) {
-  extern __shared__ uint32_t apply_smem[];  // kApplyWarps x kStageBuf: dense run staging
+  extern __shared__ uint16_t apply_smem[];  // kApplyWarps x kStageBuf16: dense run staging
   const uint32_t lane = threadIdx.x & 31;
-  uint32_t* const wbuf = apply_smem + (threadIdx.x >> 5) * kStageBuf;
+  uint16_t* const wbuf = apply_smem + (threadIdx.x >> 5) * kStageBuf16;
   const uint32_t gw = blockIdx.x * kApplyWarps + (threadIdx.x >> 5), nw = gridDim.x * kApplyWarps;
   // descriptors are host-built: the first one loads while the predecessor drains
   ElemTile next = gw < n_sync_tiles ? d.sync_desc[gw] : ElemTile{};
@@ -511,28 +511,14 @@ __global__ void __launch_bounds__(32 * kApplyWarps, 3) k_elem_apply(const ElemDe
           ne += __popc(en[k]);
         }
         if (__any_sync(0xffffffffu, ns | ne)) {
-          uint32_t ps = ns, pe = ne;  // inclusive warp scans
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t x = __shfl_up_sync(0xffffffffu, ps, o), y = __shfl_up_sync(0xffffffffu, pe, o);
-            if (lane >= (uint32_t)o) {
-              ps += x;
-              pe += y;
-            }
-          }
-          const uint32_t Ts = __shfl_sync(0xffffffffu, ps, 31), Te = __shfl_sync(0xffffffffu, pe, 31);
-          if (Ts + Te > kDenseStep) {
-            emit_staged(st, ps - ns, Ts, w0 * 32u, gs, out_s, d.runs_cap, wbuf);
-            emit_staged(en, pe - ne, Te, w0 * 32u, ge, out_e, d.runs_cap, wbuf);
-          } else if (ns | ne) {
-            uint64_t os = gs + ps - ns, oe = ge + pe - ne;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              for (uint32_t x = st[k]; x; x &= x - 1, ++os)
-                if (os < d.runs_cap) out_s[os] = (w0 + k) * 32u + (__ffs(x) - 1);
-              for (uint32_t x = en[k]; x; x &= x - 1, ++oe)
-                if (oe < d.runs_cap) out_e[oe] = (w0 + k) * 32u + (__ffs(x) - 1);
-            }
+          uint32_t xs, xe, Ts, Te;
+          step_positions(ns, ne, xs, xe, Ts, Te);
+          if (Ts + Te > kDenseStep) {  // lanes on consecutive quads: u16 staging, one pass
+            emit_dense16(st, xs, Ts, w0 * 32u, gs, out_s, d.runs_cap, wbuf);
+            emit_dense16(en, xe, Te, w0 * 32u, ge, out_e, d.runs_cap, wbuf);
+          } else {
+            if (__any_sync(0xffffffffu, ns != 0u)) emit_sparse(st, gs + xs, w0 * 32u, out_s, d.runs_cap);
+            if (__any_sync(0xffffffffu, ne != 0u)) emit_sparse(en, ge + xe, w0 * 32u, out_e, d.runs_cap);
           }
           gs += Ts;
           ge += Te;
@@ -563,7 +549,7 @@ static cudaError_t launch_pdl(void (*kernel)(KArgs...), uint32_t grid, uint32_t 
 int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, uint32_t n_sync_tiles, void* stream, std::string* err) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
-  constexpr size_t kApplySmem = (size_t)kApplyWarps * kStageBuf * 4u;
+  constexpr size_t kApplySmem = (size_t)kApplyWarps * kStageBuf16 * 2u;
   const cudaError_t attr =  // per call: the attribute belongs to the current device
       cudaFuncSetAttribute(k_elem_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem);
   if (attr != cudaSuccess) e = attr;

@@ -18,7 +18,7 @@ constexpr uint32_t kDenseStep = COH_DENSE_STEP;  // runs per warp step above whi
 // with coalesced 128-byte stores.  A buffer of B entries takes the step in passes of B
 // positions.  Buffer index o is stored at o ^ ((o >> 5) & 31): lanes whose offsets are
 // ~32 apart (the dense case) then hit different banks.
-constexpr uint32_t kStageBuf = 2048;  // u32 entries per warp (the element apply)
+constexpr uint32_t kStageBuf = 2048;  // u32 entries per warp per pass (default)
 __device__ __forceinline__ uint32_t stage_swz(uint32_t o) { return o ^ ((o >> 5) & 31u); }
 
 template <uint32_t B = kStageBuf>
@@ -72,6 +72,56 @@ __device__ __forceinline__ void emit_dense16(const uint32_t* m, uint32_t S, uint
   const uint32_t n = (uint64_t)T < cap - base ? T : (uint32_t)(cap - base);
   for (uint32_t p = lane; p < n; p += 32) out[base + p] = cell0 + buf[stage_swz16(p)];
   __syncwarp();  // the buffer is free again
+}
+
+// Sparse emission of one lane's starts (or ends) m[0..3] at out[pos ..) (pos = the lane's
+// first position): the lowest set bit of every word goes out without a loop (its position
+// is known from the popcounts of the words before it), the rare further bits of a word in
+// a warp-uniform second round.
+__device__ __forceinline__ void emit_sparse(const uint32_t* m, uint64_t pos, uint32_t cb, uint32_t* out, uint64_t cap) {
+  uint32_t rest = 0;
+  uint64_t p = pos;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (m[k] && p < cap) out[p] = cb + 32u * k + (uint32_t)(__ffs(m[k]) - 1);
+    rest |= m[k] & (m[k] - 1u);
+    p += (uint32_t)__popc(m[k]);
+  }
+  if (!__any_sync(0xFFFFFFFFu, rest != 0u)) return;
+  p = pos;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t x = m[k] & (m[k] - 1u);
+    uint64_t q = p + 1u;
+    for (; x; x &= x - 1u, ++q)
+      if (q < cap) out[q] = cb + 32u * k + (uint32_t)(__ffs(x) - 1);
+    p += (uint32_t)__popc(m[k]);
+  }
+}
+
+// Positions of one warp step's starts / ends (st / en: the lane's four words, ns / ne their
+// popcounts): the lane's exclusive offsets xs / xe and the step totals Ts / Te.  Ballots
+// when every lane holds at most one of each (sparse planes), else a warp scan of both
+// counts packed in one word (a step has at most 2048 of each).
+__device__ __forceinline__ void step_positions(uint32_t ns, uint32_t ne, uint32_t& xs, uint32_t& xe, uint32_t& Ts,
+                                               uint32_t& Te) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (__all_sync(0xFFFFFFFFu, (ns | ne) <= 1u)) {
+    const uint32_t bs = __ballot_sync(0xFFFFFFFFu, ns != 0u), be = __ballot_sync(0xFFFFFFFFu, ne != 0u);
+    const uint32_t lt = (1u << lane) - 1u;
+    xs = __popc(bs & lt), xe = __popc(be & lt), Ts = __popc(bs), Te = __popc(be);
+    return;
+  }
+  const uint32_t nse = ns | (ne << 16);
+  uint32_t pse = nse;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, pse, o);
+    if (lane >= (uint32_t)o) pse += a;
+  }
+  xs = (pse - nse) & 0xFFFFu, xe = (pse - nse) >> 16;
+  const uint32_t T = __shfl_sync(0xFFFFFFFFu, pse, 31);
+  Ts = T & 0xFFFFu, Te = T >> 16;
 }
 
 }  // namespace cohb
