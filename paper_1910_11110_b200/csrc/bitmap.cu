@@ -44,7 +44,7 @@ constexpr int kRU = COH_RUNS_RU;  // warp steps in flight in the zero-run walker
 #define COH_RUNS_PF 1
 #endif
 constexpr int kRunsPf = COH_RUNS_PF;  // walker iterations between an L2 prefetch and its loads
-constexpr uint32_t kRunsBuf = kStageBuf16 / 2;  // dense-step staging per warp, u32 words (2048 u16 entries)
+constexpr uint32_t kRunsBuf = kStageBuf16 / 2;  // dense-step staging per warp, u32 words (kStageBuf16 u16 slots)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 struct Flat {

@@ -45,12 +45,13 @@ __device__ __forceinline__ void emit_staged(const uint32_t* m, uint32_t S, uint3
 
 // The same for one warp step whose lanes cover consecutive 128-cell spans (lane L's first
 // cell = lane 0's + 128 L): entries are u16 offsets from lane 0's first cell, so a whole
-// step (at most 2048 starts or ends) fits one pass of a 4 KB buffer -- no lane re-walks its
-// bits for a second pass.  Bits are taken lowest first (x & -x, FLO).  Buffer index o is
-// stored at o ^ (((o >> 6) & 31) << 1): lanes whose offsets are ~32 apart hit different
-// banks.
-constexpr uint32_t kStageBuf16 = 2048;  // u16 entries per warp
-__device__ __forceinline__ uint32_t stage_swz16(uint32_t o) { return o ^ (((o >> 6) & 31u) << 1); }
+// step (at most 2048 starts or ends) fits one pass of a ~4 KB buffer -- no lane re-walks
+// its bits for a second pass.  Each lane fills its slots [S, S + n) from the top, highest
+// bit first (one FLO per bit, no lowest-bit isolation).  Entry o is stored at o + (o >> 5)
+// (one pad slot per 32): lanes whose slots are ~32 apart (the dense case) land in
+// different banks, and the copy-out reads 32 consecutive slots per warp load.
+constexpr uint32_t kStageBuf16 = 2048 + 64;  // u16 slots per warp
+__device__ __forceinline__ uint32_t stage_skew(uint32_t o) { return o + (o >> 5); }
 
 __device__ __forceinline__ void emit_dense16(const uint32_t* m, uint32_t S, uint32_t T, uint32_t cb, uint64_t base,
                                              uint32_t* out, uint64_t cap, uint16_t* buf) {
@@ -58,19 +59,29 @@ __device__ __forceinline__ void emit_dense16(const uint32_t* m, uint32_t S, uint
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t cell0 = __shfl_sync(0xFFFFFFFFu, cb, 0);
   const uint32_t rel = cb - cell0;
-  uint32_t o = S;
+  uint32_t o = S + __popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 3; k >= 0; --k) {
     const uint32_t rk = rel + 32u * k;
-    for (uint32_t x = m[k]; x; ++o) {
-      const uint32_t low = x & (0u - x);
-      buf[stage_swz16(o)] = (uint16_t)(rk + (31u - __clz(low)));
-      x ^= low;
+    for (uint32_t x = m[k]; x;) {
+      const uint32_t pos = 31u - __clz(x);
+      buf[stage_skew(--o)] = (uint16_t)(rk + pos);
+      x ^= 1u << pos;
     }
   }
   __syncwarp();
   const uint32_t n = (uint64_t)T < cap - base ? T : (uint32_t)(cap - base);
-  for (uint32_t p = lane; p < n; p += 32) out[base + p] = cell0 + buf[stage_swz16(p)];
+  uint32_t* const ob = out + base;
+  uint32_t p = lane;
+  for (; p + 96u < n; p += 128u) {  // four coalesced stores per lane per round
+    const uint32_t v0 = buf[stage_skew(p)], v1 = buf[stage_skew(p + 32u)], v2 = buf[stage_skew(p + 64u)],
+                   v3 = buf[stage_skew(p + 96u)];
+    ob[p] = cell0 + v0;
+    ob[p + 32u] = cell0 + v1;
+    ob[p + 64u] = cell0 + v2;
+    ob[p + 96u] = cell0 + v3;
+  }
+  for (; p < n; p += 32u) ob[p] = cell0 + buf[stage_skew(p)];
   __syncwarp();  // the buffer is free again
 }
 
