@@ -131,6 +131,14 @@ typedef struct coh_trace_batch {
  * [12k, 12k + 12) of those 96 little-endian bits.  Unpacked on the device per pipeline
  * slice.  Not combinable with COH_BATCH_BLOCKS (no room for COH_REC_CONT). */
 #define COH_BATCH_PACKED12 0x2u
+/* COH_BATCH_OVERLAP (coh_eval_traces / _counted, whole-array batches): the launch may begin
+ * before the previous kernel on the same stream has finished (programmatic dependent
+ * launch: its blocks take the SMs the previous launch's last blocks free, so a stream of
+ * batches does not drain the GPU between launches).  The caller guarantees that the
+ * previous kernel on the stream writes nothing this batch reads, and reads or writes none
+ * of this batch's outputs (results, boundary words, counters) -- e.g. consecutive batches
+ * with their own output buffers.  Without the flag a launch is ordered as usual. */
+#define COH_BATCH_OVERLAP 0x4u
 /* Pack call-major 16-bit records (layout above) into the COH_BATCH_PACKED12 form;
  * out holds ((n_calls + 7) / 8) * n_traces * 12 bytes. */
 int coh_pack_records12(const uint16_t* records, uint64_t n_traces, uint32_t n_calls, uint8_t* out);

@@ -11,6 +11,7 @@ is missing or fails.
 """
 from ._ffi import (  # noqa: F401
     BATCH_BLOCKS,
+    BATCH_OVERLAP,
     BATCH_PACKED12,
     pack_records12,
     COUNTER_NAMES,

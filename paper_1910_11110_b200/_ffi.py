@@ -55,6 +55,7 @@ COUNTER_NAMES = (
 )
 BATCH_BLOCKS = 1  # COH_BATCH_BLOCKS: records carry COH_REC_CONT (multi-mode blocks)
 BATCH_PACKED12 = 2  # COH_BATCH_PACKED12: host records packed 12 bits per call (coh_eval_traces_host)
+BATCH_OVERLAP = 4  # COH_BATCH_OVERLAP: may start before the previous kernel on the stream ends (own outputs)
 REC_CONT = 1      # COH_REC_CONT
 FLAG_UNSAFE = 0x10
 N_COUNTERS = len(COUNTER_NAMES)

@@ -35,7 +35,7 @@ int validate(coh_ctx* ctx, const coh_trace_batch* b) {
   if (b->n_arrays < 1 || b->n_arrays > COH_MAX_ARRAYS)
     return arg_fail(ctx, "n_arrays must be in [1, 64], got " + std::to_string(b->n_arrays));
   if (b->n_traces && b->n_calls && !b->records) return arg_fail(ctx, "records is NULL");
-  if (b->flags & ~(COH_BATCH_BLOCKS | COH_BATCH_PACKED12)) return arg_fail(ctx, "unknown batch flags");
+  if (b->flags & ~(COH_BATCH_BLOCKS | COH_BATCH_PACKED12 | COH_BATCH_OVERLAP)) return arg_fail(ctx, "unknown batch flags");
   if ((b->flags & COH_BATCH_BLOCKS) && (b->flags & COH_BATCH_PACKED12))
     return arg_fail(ctx, "COH_BATCH_PACKED12 records cannot carry COH_REC_CONT");
   return COH_OK;
@@ -88,19 +88,15 @@ int eval_device(coh_ctx* ctx, const coh_trace_batch* b, const uint16_t* d_record
   L.boundary = d_boundary;
   L.counters = d_counters;
   L.sms = ctx->sms;  // the launcher sizes a persistent grid for the chosen variant
-  // the work-distribution ticket of long launches (more than five rounds of traces per
-  // thread): stream-ordered from the pool, private to this launch (launches of one
-  // context on different streams may run concurrently)
-  unsigned int* ticket = nullptr;
-  if (n_traces > 5ull * 1024ull * (uint64_t)ctx->sms) {
-    COH_CUDA(ctx, cudaMallocAsync(reinterpret_cast<void**>(&ticket), sizeof(unsigned int), s));
-    COH_CUDA(ctx, cudaMemsetAsync(ticket, 0, sizeof(unsigned int), s));
-  }
-  L.ticket = ticket;
+  // the launch's ticket and counter sums: the next slot of the context's ring, private
+  // to this launch (launches of one context on different streams may run concurrently);
+  // long launches (more than five rounds of traces per thread) hand out trace batches
+  L.slot = ctx->d_slots + (ctx->slot_next++ % cohb::kLaunchSlots);
+  L.dynamic = n_traces > 5ull * 1024ull * (uint64_t)ctx->sms;
+  L.overlap = (b->flags & COH_BATCH_OVERLAP) && uniform;
   L.flags = b->flags;
   std::string err;
   rc = (b->flags & COH_BATCH_BLOCKS) ? cohb::launch_trace_blocks(L, s, &err) : cohb::launch_trace_eval(L, s, &err);
-  if (ticket) cudaFreeAsync(ticket, s);
   if (d_bytes) cudaFreeAsync(d_bytes, s);
   if (rc) {
     ctx->err = err;
@@ -135,6 +131,8 @@ int coh_ctx_create(int device, coh_ctx** out) {
     if ((e = cudaMemcpy(ctx->d_lut, table.lut, sizeof table.lut, cudaMemcpyHostToDevice)) != cudaSuccess) break;
     if ((e = cudaMemcpy(ctx->d_slow, table.slow, sizeof table.slow, cudaMemcpyHostToDevice)) != cudaSuccess) break;
     if ((e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&ctx->d_slots, sizeof(cohb::LaunchSlot) * cohb::kLaunchSlots)) != cudaSuccess) break;
+    if ((e = cudaMemset(ctx->d_slots, 0, sizeof(cohb::LaunchSlot) * cohb::kLaunchSlots)) != cudaSuccess) break;
     {  // stream-ordered scratch (cudaMallocAsync) stays in the pool instead of being unmapped at every sync
       cudaMemPool_t pool;
       uint64_t keep = ~0ull;
@@ -157,6 +155,7 @@ void coh_ctx_destroy(coh_ctx* ctx) {
   if (!ctx) return;
   cudaFree(ctx->d_lut);
   cudaFree(ctx->d_slow);
+  cudaFree(ctx->d_slots);
   for (int k = 0; k < 2; ++k) {
     cudaFree(ctx->d_pk[k]);
     cudaFree(ctx->d_rec[k]);

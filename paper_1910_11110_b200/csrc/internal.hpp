@@ -77,6 +77,16 @@ void build_call_table(CallTable* t);
 coh_call_outcome simulate_block(uint32_t call_type, uint32_t state, int fuel);
 
 // ---- device entry points (defined in .cu files) ------------------------------------
+// Per-launch device state of k_trace_eval, from a ring owned by the context (zeroed once
+// at creation): the work-distribution ticket and the counter sums.  The last block of the
+// launch copies the sums to the caller's counters and zeroes the slot for its next use, so
+// a launch needs no memset before it (and can follow its predecessor without a gap).
+struct LaunchSlot {
+  unsigned int ticket;  // dynamic trace batches handed out after the first round
+  unsigned int done;    // blocks finished
+  unsigned long long cnt[COH_N_COUNTERS];
+};
+constexpr uint32_t kLaunchSlots = 256;
 struct TraceLaunch {
   const uint16_t* records;
   uint64_t n_traces;
@@ -94,7 +104,9 @@ struct TraceLaunch {
   uint32_t* boundary;
   uint64_t* counters;  // optional fused counter reduction (device, COH_N_COUNTERS)
   int sms;  // SM count (persistent grid)
-  unsigned int* ticket;  // device, zeroed, private to this launch (dynamic trace batches)
+  LaunchSlot* slot;  // device, zeroed, private to this launch (ring of the context)
+  bool dynamic;      // hand out trace batches from slot->ticket (long launches)
+  bool overlap;      // COH_BATCH_OVERLAP: programmatic dependent launch
 };
 int launch_trace_eval(const TraceLaunch& p, void* stream, std::string* err);
 // Multi-mode blocks (COH_BATCH_BLOCKS, trace_blocks.cu).
@@ -130,4 +142,6 @@ struct coh_ctx {
   size_t rec_cap = 0, res_cap = 0, bnd_cap = 0;  // bytes per buffer
   void* d_pk[2] = {nullptr, nullptr};            // COH_BATCH_PACKED12 slices
   size_t pk_cap = 0;
+  cohb::LaunchSlot* d_slots = nullptr;           // kLaunchSlots, zeroed at creation
+  uint32_t slot_next = 0;
 };

@@ -61,6 +61,7 @@ struct __align__(16) TraceSmem {
   uint16_t store[kStoreBytes / 2];
   unsigned long long cnt[COH_N_COUNTERS];
   uint64_t bytes[COH_MAX_ARRAYS];
+  uint32_t last;  // this block finished the launch
 };
 constexpr uint32_t kSmemBase = 0x400u;
 constexpr uint32_t kLutAddr = kSmemBase;
@@ -80,8 +81,9 @@ struct KParams {
   const uint32_t* slow;
   coh_trace_result* res;
   uint32_t* bnd;
-  unsigned long long* counters;  // optional fused COH_N_COUNTERS reduction (zeroed by the launcher)
-  unsigned int* ticket;          // dynamic trace batches handed out after the first round (zeroed)
+  unsigned long long* counters;  // optional fused COH_N_COUNTERS reduction (k_trace_eval: written, not added)
+  unsigned int* ticket;          // dynamic trace batches handed out after the first round (in *slot)
+  LaunchSlot* slot;              // this launch's ticket / counter sums (zero on entry, zeroed again on exit)
   uint32_t k65536;               // 65536, opaque to ptxas: the accumulate stays an IMAD.HI (FMA pipe)
 };
 
@@ -214,6 +216,9 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble)  ? COH_TE_MINB_DOUBLE
   if ((uint32_t)__cvta_generic_to_shared(&sm) != kSmemBase) __trap();  // layout assumption
 
   const uint32_t tid = threadIdx.x;
+  // a COH_BATCH_OVERLAP successor may be scheduled as soon as every block of this launch
+  // has started (its blocks then take the SMs this launch's last blocks free)
+  asm volatile("griddepcontrol.launch_dependents;" :::);
 #ifdef COH_TE_TIMELINE
   unsigned long long tl0, tl1, tl2;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl0));
@@ -617,7 +622,24 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble)  ? COH_TE_MINB_DOUBLE
       if (UNIFORM && lane == 5u) atomicAdd(&sm.cnt[6], (unsigned long long)cnt_acc * p.bytes_uniform);
     }
     __syncthreads();
-    if (tid < COH_N_COUNTERS && sm.cnt[tid]) atomicAdd(p.counters + tid, sm.cnt[tid]);
+    if (tid < COH_N_COUNTERS && sm.cnt[tid]) atomicAdd(&p.slot->cnt[tid], sm.cnt[tid]);
+  }
+  if (p.counters || p.ticket) {  // the last block publishes the sums and zeroes the slot
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) sm.last = atomicAdd(&p.slot->done, 1u) == gridDim.x - 1u;
+    __syncthreads();
+    if (sm.last) {
+      __threadfence();
+      if (tid < COH_N_COUNTERS) {
+        const unsigned long long v = atomicExch(&p.slot->cnt[tid], 0ull);
+        if (p.counters) p.counters[tid] = v;
+      }
+      if (tid == 0) {
+        p.slot->ticket = 0u;
+        p.slot->done = 0u;
+      }
+    }
   }
 #ifdef COH_TE_TIMELINE  // per block: entry, after set-up, exit (debug builds only)
   __syncthreads();
@@ -971,7 +993,20 @@ static int launch_one(const TraceLaunch& L, const KParams& kp, cudaStream_t s, s
   const uint64_t cap = (uint64_t)L.sms * (uint64_t)occ;
   const uint64_t rounds = (need + cap - 1) / cap;
   const int grid = (int)((need + rounds - 1) / rounds);
-  k_trace_eval<F><<<grid, kNT, 0, s>>>(kp);
+  if (L.overlap) {  // COH_BATCH_OVERLAP: programmatic dependent of the previous kernel
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kNT);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_trace_eval<F>, kp);
+  } else {
+    k_trace_eval<F><<<grid, kNT, 0, s>>>(kp);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("trace_eval launch: ") + cudaGetErrorString(e);
@@ -1014,16 +1049,10 @@ int launch_trace_eval(const TraceLaunch& L, void* stream, std::string* err) {
   kp.res = L.results;
   kp.bnd = L.boundary;
   kp.counters = reinterpret_cast<unsigned long long*>(L.counters);
-  kp.ticket = L.ticket;
+  kp.slot = L.slot;
+  kp.ticket = L.dynamic ? &L.slot->ticket : nullptr;
   kp.k65536 = 65536u;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (L.counters) {
-    cudaError_t e = cudaMemsetAsync(L.counters, 0, sizeof(uint64_t) * COH_N_COUNTERS, s);
-    if (e != cudaSuccess) {
-      *err = std::string("counter memset: ") + cudaGetErrorString(e);
-      return COH_E_CUDA;
-    }
-  }
   // Latency path: too few single-array traces to fill the GPU -> a block per trace.
   // COH_TE_PATH=thread|scan forces one path (tests compare both).
   const char* path = std::getenv("COH_TE_PATH");
@@ -1031,6 +1060,13 @@ int launch_trace_eval(const TraceLaunch& L, void* stream, std::string* err) {
   if (path && std::strcmp(path, "thread") == 0) scan = false;
   if (path && std::strcmp(path, "scan") == 0) scan = L.n_arrays == 1u;
   if (scan) {
+    if (L.counters) {  // the scan path adds into the caller's counters
+      cudaError_t e = cudaMemsetAsync(L.counters, 0, sizeof(uint64_t) * COH_N_COUNTERS, s);
+      if (e != cudaSuccess) {
+        *err = std::string("counter memset: ") + cudaGetErrorString(e);
+        return COH_E_CUDA;
+      }
+    }
     k_trace_scan<<<(unsigned)L.n_traces, kScanNT, 0, s>>>(kp);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {

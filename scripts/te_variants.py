@@ -42,8 +42,27 @@ def child():
         if i >= 10:
             ts.append(e0.elapsed_time(e1) * 1e3)
     h = hashlib.sha256(d_res.cpu().numpy().tobytes() + d_bnd.cpu().numpy().tobytes()).hexdigest()[:16]
+    # back-to-back stream of K launches (the bench's step loop), plain and COH_BATCH_OVERLAP
+    # with double-buffered outputs
+    res2 = [d_res, torch.empty_like(d_res)]
+    bnd2 = [d_bnd, torch.empty_like(d_bnd)]
+    cnt2 = [d_cnt, torch.zeros_like(d_cnt)]
+    stream_us = {}
+    for name, flags in (("plain", 0), ("overlap", coh.BATCH_OVERLAP)):
+        for i in range(5):
+            ctx.eval_traces_counted(d_rec, N, NC, NA, 10000, res2[i & 1], cnt2[i & 1], bnd2[i & 1], stream=s, flags=flags)
+        torch.cuda.synchronize()
+        K = 40
+        e0.record()
+        for i in range(K):
+            ctx.eval_traces_counted(d_rec, N, NC, NA, 10000, res2[i & 1], cnt2[i & 1], bnd2[i & 1], stream=s, flags=flags)
+        e1.record()
+        torch.cuda.synchronize()
+        stream_us[name] = e0.elapsed_time(e1) * 1e3 / K
+    h2 = hashlib.sha256(res2[1].cpu().numpy().tobytes() + bnd2[1].cpu().numpy().tobytes()).hexdigest()[:16]
     print(json.dumps({"us_median": float(np.median(ts)), "us_min": float(np.min(ts)), "digest": h,
-                      "counters": d_cnt.cpu().tolist()[:11]}))
+                      "stream_us_per_launch": stream_us, "digest_overlap": h2,
+                      "counters": d_cnt.cpu().tolist()[:11], "counters_overlap": cnt2[1].cpu().tolist()[:11]}))
 
 
 def main(argv):

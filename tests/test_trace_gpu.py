@@ -332,3 +332,44 @@ def test_packed12_host_entry_equals_plain(ctx):
     assert same(a, b) and np.array_equal(ab, bb)
     with pytest.raises(coh.CohError):
         ctx.eval_traces_host(pk, nt, nc, na, flags=coh.BATCH_PACKED12 | coh.BATCH_BLOCKS)
+
+
+def test_overlapped_launch_stream(ctx):
+    """COH_BATCH_OVERLAP: a stream of back-to-back launches (each may start on the SMs its
+    predecessor frees) with their own outputs gives every batch the results, boundary words
+    and counters of a plain launch; more launches than the context's ring of launch slots,
+    mixing batch sizes (short launches: static striding; long ones: the slot's ticket)."""
+    s = torch.cuda.current_stream().cuda_stream
+    sizes = [20000, 1 << 20, 7000, 1 << 20]
+    nc, na = 256, 64
+    recs = {}
+    want = {}
+    for n in set(sizes):
+        d_rec = torch.empty(coh.records_elems(n, nc), dtype=torch.int16, device="cuda")
+        ctx.gen_records(5, 0, n, nc, na, 8, d_rec, s)
+        d_res = torch.empty(n * 64, dtype=torch.uint8, device="cuda")
+        d_bnd = torch.empty(coh.boundary_words(nc) * n, dtype=torch.int32, device="cuda")
+        d_cnt = torch.zeros(16, dtype=torch.int64, device="cuda")
+        ctx.eval_traces_counted(d_rec, n, nc, na, 10000, d_res, d_cnt, d_bnd, stream=s)
+        torch.cuda.synchronize()
+        recs[n] = d_rec
+        want[n] = (d_res.clone(), d_bnd.clone(), d_cnt.clone())
+    outs = [(torch.empty(n * 64, dtype=torch.uint8, device="cuda"),
+             torch.empty(coh.boundary_words(nc) * n, dtype=torch.int32, device="cuda"),
+             torch.full((16,), 7, dtype=torch.int64, device="cuda")) for n in sizes]
+    for k in range(300):  # > 256 launch slots
+        i = k % len(sizes)
+        n = sizes[i]
+        ctx.eval_traces_counted(recs[n], n, nc, na, 10000, outs[i][0], outs[i][2], outs[i][1], stream=s,
+                                flags=coh.BATCH_OVERLAP)
+        if k % 37 == 36:  # check the latest launch of every size
+            torch.cuda.synchronize()
+            for j, m in enumerate(sizes):
+                assert torch.equal(outs[j][0], want[m][0]) and torch.equal(outs[j][1], want[m][1])
+                assert torch.equal(outs[j][2][:11], want[m][2][:11])
+    torch.cuda.synchronize()
+    # the ring is clean: a plain launch after the stream counts from zero
+    d_cnt = torch.full((16,), 7, dtype=torch.int64, device="cuda")
+    ctx.eval_traces_counted(recs[7000], 7000, nc, na, 10000, outs[2][0], d_cnt, outs[2][1], stream=s)
+    torch.cuda.synchronize()
+    assert torch.equal(d_cnt[:11], want[7000][2][:11])
