@@ -45,9 +45,6 @@ namespace cohb {
 #ifndef COH_TE_MINB
 #define COH_TE_MINB 5
 #endif
-#ifndef COH_TE_MINB_LEAN
-#define COH_TE_MINB_LEAN 6
-#endif
 constexpr int kNT = COH_TE_NT;  // traces (threads) per block
 static_assert(kNT % 128 == 0 && kNT <= 512, "store regions hold 128 threads each");
 constexpr uint32_t kStoreBytes = COH_MAX_ARRAYS * kNT * 2u;
@@ -84,7 +81,6 @@ struct KParams {
   unsigned long long* counters;  // optional fused COH_N_COUNTERS reduction (k_trace_eval: written, not added)
   unsigned int* ticket;          // dynamic trace batches handed out after the first round (in *slot)
   LaunchSlot* slot;              // this launch's ticket / counter sums (zero on entry, zeroed again on exit)
-  uint32_t k65536;               // 65536, opaque to ptxas: the accumulate stays an IMAD.HI (FMA pipe)
 };
 
 // bnd = 2*bnd + (acc >= 0x2000): with the accumulator clean (steps | transfers << 7 |
@@ -128,13 +124,9 @@ __host__ __device__ constexpr uint32_t viol_threshold_addend(int c) { return (ui
   "setp.lt.or.s32 p, ev, 0, p;\n\t"                   \
   COH_PTX_ACC                                          \
   "st.shared.u16 [so+%5], ev;\n\t"                    \
-  COH_PTX_BND(T)                                       \
+  "add.cc.u32 cy, %0, " T ";\n\t"                     \
+  "addc.u32 %1, %1, %1;\n\t"                          \
   "SKIP:\n\t}\n\t"
-#ifdef COH_KO_BND
-#define COH_PTX_BND(T) ""
-#else
-#define COH_PTX_BND(T) "add.cc.u32 cy, %0, " T ";\n\taddc.u32 %1, %1, %1;\n\t"
-#endif
 #define COH_PTX_PAIR(R, T0, T1)        \
   COH_PTX_CALL(R, T0)                  \
   "mul.hi.u32 th, " R ", 65536;\n\t"  \
@@ -151,12 +143,12 @@ __host__ __device__ constexpr uint32_t viol_threshold_addend(int c) { return (ui
     "n"(viol_threshold_addend(8 * H + 0)), "n"(viol_threshold_addend(8 * H + 1)),                    \
     "n"(viol_threshold_addend(8 * H + 2)), "n"(viol_threshold_addend(8 * H + 3)),                    \
     "n"(viol_threshold_addend(8 * H + 4)), "n"(viol_threshold_addend(8 * H + 5)),                    \
-    "n"(viol_threshold_addend(8 * H + 6)), "n"(viol_threshold_addend(8 * H + 7)), "r"(k65536)        \
+    "n"(viol_threshold_addend(8 * H + 6)), "n"(viol_threshold_addend(8 * H + 7))                    \
   : "memory"
 
 template <bool FUEL, int H>
 __device__ __forceinline__ uint32_t run_chunk(const uint4 v, uint32_t toff, uint32_t& acc, uint32_t& bnd,
-                                              int fuel_left, uint32_t k65536) {
+                                              int fuel_left) {
   uint32_t stop;
   if (FUEL) {  // the call's steps must fit the remaining fuel, else it is the slow call
 #define COH_PTX_ACC                                 \
@@ -169,13 +161,7 @@ __device__ __forceinline__ uint32_t run_chunk(const uint4 v, uint32_t toff, uint
     asm volatile(COH_PTX_CHUNK COH_PTX_OPERANDS(H));
 #undef COH_PTX_ACC
   } else {
-#if defined(COH_KO_ACC)
-#define COH_PTX_ACC "@p bra SKIP;\n\t"
-#elif defined(COH_FMA_ACC)
-#define COH_PTX_ACC "@p bra SKIP;\n\tmad.hi.s32 %0, ev, %19, %0;\n\t"
-#else
 #define COH_PTX_ACC "@p bra SKIP;\n\tmul.hi.s32 cy, ev, 65536;\n\tadd.s32 %0, %0, cy;\n\t"
-#endif
     asm volatile(COH_PTX_CHUNK COH_PTX_OPERANDS(H));
 #undef COH_PTX_ACC
   }
@@ -193,23 +179,15 @@ __device__ __forceinline__ uint32_t pin_zero(uint32_t x) {
 // FLAGS: kFuel = fuel may run out (fuel < 6 x n_calls), kBytes = non-uniform array
 // sizes (per-call byte accumulation), kRing = n_calls % 32 == 0 (the record ring runs on
 // into the next trace).
-enum : int { kFuel = 1, kBytes = 2, kRing = 4, kDouble = 8, kLean = 16 };
-
-// L2 prefetch of the 128-byte line holding a (no registers held until the data is needed).
-__device__ __forceinline__ void prefetch_l2(const void* a) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-}
+enum : int { kFuel = 1, kBytes = 2, kRing = 4, kDouble = 8 };
 
 template <int FLAGS>
-__global__ void __launch_bounds__(kNT, (FLAGS & kDouble)  ? COH_TE_MINB_DOUBLE
-                                       : (FLAGS & kLean) ? COH_TE_MINB_LEAN
-                                                         : COH_TE_MINB) k_trace_eval(const KParams p) {
+__global__ void __launch_bounds__(kNT, (FLAGS & kDouble) ? COH_TE_MINB_DOUBLE : COH_TE_MINB) k_trace_eval(const KParams p) {
   constexpr bool CHECK_FUEL = FLAGS & kFuel;
   constexpr bool UNIFORM = !(FLAGS & kBytes);
   constexpr bool RING = FLAGS & kRing;
   constexpr bool DOUBLE = FLAGS & kDouble;  // n_calls % 64 == 0: two register rings
-  constexpr bool LEAN = FLAGS & kLean;      // n_calls % 32 == 0: a 2-chunk ring fed from L2 prefetches
-  constexpr int kRingLen = LEAN ? 2 : 4;
+  constexpr int kRingLen = 4;
   __shared__ TraceSmem sm;
   char* const stb = reinterpret_cast<char*>(sm.store);
   const char* const lutb = reinterpret_cast<const char*>(sm.lut);
@@ -264,7 +242,6 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble)  ? COH_TE_MINB_DOUBLE
 #endif
 
   const uint32_t warp = tid >> 5, lane = tid & 31u;
-  const uint32_t k65536 = p.k65536;
   // counters: packed warp sums need n_calls <= 256 (6 steps per call per lane fit 16 bits)
   const bool packed_cnt = n_calls <= 256u;
   uint32_t cnt_acc = 0;  // lane k < 10: warp total of counter k over this warp's traces
@@ -327,7 +304,7 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble)  ? COH_TE_MINB_DOUBLE
   COH_CALL(__umulhi((W), 0x10000u), (C) + 1)
 #define COH_CHUNK(V, H)                                                                   \
   if (UNIFORM) {                                                                          \
-    stop = run_chunk<CHECK_FUEL, H>((V), toff, acc, bnd, fuel_left, k65536);                      \
+    stop = run_chunk<CHECK_FUEL, H>((V), toff, acc, bnd, fuel_left);                      \
   } else {                                                                                \
     COH_PAIR((V).x, 8 * H) COH_PAIR((V).y, 8 * H + 2) COH_PAIR((V).z, 8 * H + 4)           \
     COH_PAIR((V).w, 8 * H + 6)                                                            \
@@ -354,39 +331,7 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble)  ? COH_TE_MINB_DOUBLE
   if (p.bnd) p.bnd[(uint64_t)(G) * n + t] = bnd;                                  \
   viol_blocks += 32u - __popc(bnd);                                               \
   bnd = 1u;
-      if (LEAN) {
-        // One ring of two chunks, refilled right after each use (one chunk of lead); the
-        // lead is enough because the rows were prefetched into L2 two groups earlier
-        // (lanes 0-3 of the warp, one 512-byte bulk prefetch per chunk row of the warp's
-        // 32 traces).  Frees the registers of the deep rings for occupancy.
-        const uint64_t nb = 16ull * n;
-        const char* gp = reinterpret_cast<const char*>(p.rec + t) + 2u * nb;  // chunk 2
-        const char* const gnext = reinterpret_cast<const char*>(p.rec + (RING && tn < n ? tn : t));
-        const uint32_t wbase = t - lane;  // this warp's batch
-        for (uint32_t g = 0; g < n_groups; ++g) {
-          i0 = g * 32u;
-#ifndef COH_TE_NO_PF
-          if (lane < 16u) {  // rows of group g + 2 (the next batch's first rows near the end)
-            uint32_t row = 4u * (g + 2u) + (lane >> 2), b = wbase + 8u * (lane & 3u);
-            if (row >= n_chunks) row -= n_chunks, b = nxt + 8u * (lane & 3u);
-            if (row < n_chunks && b < n) prefetch_l2(p.rec + (uint64_t)row * n + b);
-          }
-#endif
-          COH_CHUNK(ring[0], 0)
-          ring[0] = __ldcs(reinterpret_cast<const uint4*>(gp + pin_zero(bnd)));
-          gp += nb;
-          COH_CHUNK(ring[1], 1) COH_FLUSH
-          ring[1] = __ldcs(reinterpret_cast<const uint4*>(gp + pin_zero(bnd)));
-          gp = g + 1u == n_groups ? gnext : gp + nb;
-          COH_CHUNK(ring[0], 0)
-          ring[0] = __ldcs(reinterpret_cast<const uint4*>(gp + pin_zero(bnd)));
-          gp += nb;
-          COH_CHUNK(ring[1], 1) COH_FLUSH
-          ring[1] = __ldcs(reinterpret_cast<const uint4*>(gp + pin_zero(bnd)));
-          gp += nb;
-          COH_GROUP_END(g)
-        }
-      } else if (DOUBLE) {
+      if (DOUBLE) {
         // Two register rings, A = even groups, B = odd groups.  A group's four loads are
         // issued together right after its predecessor's first chunk, so every first use
         // (which waits for all outstanding loads: they share one scoreboard) has three
@@ -530,17 +475,12 @@ __global__ void __launch_bounds__(kNT, (FLAGS & kDouble)  ? COH_TE_MINB_DOUBLE
   finished : {
     // the final store, nibble-packed, and every slot reset for this thread's next trace
     uint32_t sw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#ifdef COH_KO_EPI_LDS
-#define COH_EPI_READ(P) init
-#else
-#define COH_EPI_READ(P) (*(P))
-#endif
     uint32_t init;  // kInit in a register (else ptxas rematerialises it before every store)
     asm volatile("mov.u32 %0, %1;" : "=r"(init) : "n"(kInit));
 #define COH_SLOT_OUT(A)                                                                \
   {                                                                                    \
     uint16_t* const wp = reinterpret_cast<uint16_t*>(stb + (A) * 256 + toff);          \
-    const uint32_t w = COH_EPI_READ(wp);                                               \
+    const uint32_t w = *wp;                                                            \
     *wp = (uint16_t)init;                                                              \
     const int sh = 4 * ((A) & 7) - 8; /* state nibble at slot bits 8-11 */             \
     sw[(A) >> 3] |= (sh >= 0 ? (w << sh) : (w >> -sh)) & (15u << (4 * ((A) & 7)));    \
@@ -1051,7 +991,6 @@ int launch_trace_eval(const TraceLaunch& L, void* stream, std::string* err) {
   kp.counters = reinterpret_cast<unsigned long long*>(L.counters);
   kp.slot = L.slot;
   kp.ticket = L.dynamic ? &L.slot->ticket : nullptr;
-  kp.k65536 = 65536u;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // Latency path: too few single-array traces to fill the GPU -> a block per trace.
   // COH_TE_PATH=thread|scan forces one path (tests compare both).
@@ -1076,15 +1015,13 @@ int launch_trace_eval(const TraceLaunch& L, void* stream, std::string* err) {
     return COH_OK;
   }
   const bool ring = L.n_calls % 32u == 0u && L.n_calls >= 32u;
-  const bool lean = ring && getenv_flag("COH_TE_LEAN");
-  const int f = (L.check_fuel ? kFuel : 0) | (L.uniform_bytes ? 0 : kBytes) | (ring ? kRing : 0) | (lean ? kLean : 0) |
-                (!lean && L.n_calls % 64u == 0u && L.n_calls >= 64u && !getenv_flag("COH_TE_SINGLE") ? kDouble : 0);
+  const int f = (L.check_fuel ? kFuel : 0) | (L.uniform_bytes ? 0 : kBytes) | (ring ? kRing : 0) |
+                (L.n_calls % 64u == 0u && L.n_calls >= 64u && !getenv_flag("COH_TE_SINGLE") ? kDouble : 0);
   switch (f) {
 #define COH_CASE(F) \
   case F: return launch_one<F>(L, kp, s, err);
     COH_CASE(0) COH_CASE(1) COH_CASE(2) COH_CASE(3) COH_CASE(4) COH_CASE(5) COH_CASE(6) COH_CASE(7)
     COH_CASE(12) COH_CASE(13) COH_CASE(14) COH_CASE(15)
-    COH_CASE(20) COH_CASE(21) COH_CASE(22) COH_CASE(23)
 #undef COH_CASE
   }
   return COH_E_ARG;

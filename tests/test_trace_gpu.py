@@ -334,13 +334,14 @@ def test_packed12_host_entry_equals_plain(ctx):
         ctx.eval_traces_host(pk, nt, nc, na, flags=coh.BATCH_PACKED12 | coh.BATCH_BLOCKS)
 
 
-def test_overlapped_launch_stream(ctx):
+@pytest.mark.parametrize("sizes,launches", [([20000, 1 << 20, 7000, 1 << 20], 300), ([20000, 7000], 260),
+                                            ([1 << 20], 3)], ids=["mixed", "ring", "ticket"])
+def test_overlapped_launch_stream(ctx, sizes, launches):
     """COH_BATCH_OVERLAP: a stream of back-to-back launches (each may start on the SMs its
     predecessor frees) with their own outputs gives every batch the results, boundary words
     and counters of a plain launch; more launches than the context's ring of launch slots,
     mixing batch sizes (short launches: static striding; long ones: the slot's ticket)."""
     s = torch.cuda.current_stream().cuda_stream
-    sizes = [20000, 1 << 20, 7000, 1 << 20]
     nc, na = 256, 64
     recs = {}
     want = {}
@@ -357,19 +358,20 @@ def test_overlapped_launch_stream(ctx):
     outs = [(torch.empty(n * 64, dtype=torch.uint8, device="cuda"),
              torch.empty(coh.boundary_words(nc) * n, dtype=torch.int32, device="cuda"),
              torch.full((16,), 7, dtype=torch.int64, device="cuda")) for n in sizes]
-    for k in range(300):  # > 256 launch slots
+    for k in range(launches):  # mixed / ring: > 256 launch slots
         i = k % len(sizes)
         n = sizes[i]
         ctx.eval_traces_counted(recs[n], n, nc, na, 10000, outs[i][0], outs[i][2], outs[i][1], stream=s,
                                 flags=coh.BATCH_OVERLAP)
-        if k % 37 == 36:  # check the latest launch of every size
+        if k % 37 == 36 or k == launches - 1:  # check the latest launch of every size
             torch.cuda.synchronize()
             for j, m in enumerate(sizes):
                 assert torch.equal(outs[j][0], want[m][0]) and torch.equal(outs[j][1], want[m][1])
                 assert torch.equal(outs[j][2][:11], want[m][2][:11])
     torch.cuda.synchronize()
     # the ring is clean: a plain launch after the stream counts from zero
+    m = sizes[-1]
     d_cnt = torch.full((16,), 7, dtype=torch.int64, device="cuda")
-    ctx.eval_traces_counted(recs[7000], 7000, nc, na, 10000, outs[2][0], d_cnt, outs[2][1], stream=s)
+    ctx.eval_traces_counted(recs[m], m, nc, na, 10000, outs[-1][0], d_cnt, outs[-1][1], stream=s)
     torch.cuda.synchronize()
-    assert torch.equal(d_cnt[:11], want[7000][2][:11])
+    assert torch.equal(d_cnt[:11], want[m][2][:11])
