@@ -465,7 +465,8 @@ int coh_rt_buffer_planes(coh_rt* rt, uint32_t buffer, uint32_t* planes_out) {
 int coh_rt_copy_log(const coh_rt* rt, coh_rt_copy* out, uint64_t cap, uint64_t* n) {
   if (!rt || !n || (cap && !out)) return COH_E_ARG;
   *n = rt->log.size();
-  std::memcpy(out, rt->log.data(), sizeof(coh_rt_copy) * (size_t)std::min<uint64_t>(cap, rt->log.size()));
+  const size_t k = (size_t)std::min<uint64_t>(cap, rt->log.size());
+  if (k) std::memcpy(out, rt->log.data(), sizeof(coh_rt_copy) * k);  // (out may be NULL when cap == 0)
   return COH_OK;
 }
 

@@ -121,11 +121,14 @@ __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
   __shared__ uint8_t st[COH_MAX_ARRAYS][kBT];
   __shared__ uint8_t undo[COH_MAX_ARRAYS][kBT];
   __shared__ uint32_t s_lut[kLutEntries];
+  __shared__ unsigned long long s_cnt[COH_N_COUNTERS];
   const uint32_t tid = threadIdx.x;
   for (uint32_t k = tid; k < (uint32_t)kLutEntries; k += kBT) s_lut[k] = __ldg(p.lut + k);
+  if (tid < COH_N_COUNTERS) s_cnt[tid] = 0ull;
   __syncthreads();
   const uint64_t t = (uint64_t)blockIdx.x * kBT + tid;
-  if (t >= p.n_traces) return;
+  unsigned long long cv[COH_N_COUNTERS] = {};  // this thread's counter contributions
+  if (t < p.n_traces) {
   const uint64_t n = p.n_traces;
   for (uint32_t a = 0; a < COH_MAX_ARRAYS; ++a) st[a][tid] = a < p.n_arrays ? COH_STATE_INITIAL : 0xFFu;
 
@@ -235,13 +238,23 @@ __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
   out[2] = make_uint4((uint32_t)L.tbytes, (uint32_t)(L.tbytes >> 32), L.steps, L.xfers);
   out[3] = make_uint4(blocks_done, viol_blocks, stuck_call,
                       L.status | (L.stuck_arr << 8) | (L.stuck_eff << 16) | (stuck_flags << 24));
-  if (p.counters) {
-    const unsigned long long v[COH_N_COUNTERS] = {
-        L.status == COH_RUN_STUCK, L.status == COH_RUN_FUEL_EXHAUSTED, viol_blocks != 0u, L.status == COH_RUN_DEFECT,
-        L.steps, L.xfers, L.tbytes, viol_blocks, blocks_done, 1u, unsafe ? 1u : 0u};
+  const unsigned long long v[COH_N_COUNTERS] = {
+      L.status == COH_RUN_STUCK, L.status == COH_RUN_FUEL_EXHAUSTED, viol_blocks != 0u, L.status == COH_RUN_DEFECT,
+      L.steps, L.xfers, L.tbytes, viol_blocks, blocks_done, 1u, unsafe ? 1u : 0u};
 #pragma unroll
-    for (int k = 0; k < COH_N_COUNTERS; ++k)
-      if (v[k]) atomicAdd(p.counters + k, v[k]);
+  for (int k = 0; k < COH_N_COUNTERS; ++k) cv[k] = v[k];
+  }  // t < n_traces
+  if (p.counters) {  // warp sums, one shared atomic per warp, one global atomic per block
+    const uint32_t lane = tid & 31u;
+#pragma unroll
+    for (int k = 0; k < COH_N_COUNTERS; ++k) {
+      unsigned long long x = cv[k];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+      if (lane == 0 && x) atomicAdd(&s_cnt[k], x);
+    }
+    __syncthreads();
+    if (tid < COH_N_COUNTERS && s_cnt[tid]) atomicAdd(p.counters + tid, s_cnt[tid]);
   }
 }
 

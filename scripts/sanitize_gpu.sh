@@ -14,5 +14,6 @@ timeout 1500 $CS --tool memcheck python -m pytest tests/test_bitmap.py tests/tes
 echo; echo "## racecheck: zero-run primitives (dense u16 staging) and the element apply"
 timeout 1500 $CS --tool racecheck python -m pytest tests/test_bitmap.py -q -p no:cacheprovider -k "not 16777216" 2>&1 | tail -2
 echo; echo "## host ASan + UBSan (lib/variants/asan.so): GPU tests' host side"
-timeout 1500 bash scripts/host_sanitize.sh -m gpu -k "not 1048576 and not c4 and not full and not 67108864" 2>&1 | tail -3
+SAN_LOG=none timeout 1500 bash scripts/host_sanitize.sh -m gpu -k "not 1048576 and not c4 and not full and not 67108864 and not 2p24 and not large and not 16777216 and not shim and not facade" 2>&1 | tail -2
+echo "(tests that run a separately built binary in a subprocess -- the shim test, the C++ facade build -- are left out: the preloaded ASan runtime is inherited by nvcc and by binaries that are not instrumented)"
 } > "$OUT" 2>&1
