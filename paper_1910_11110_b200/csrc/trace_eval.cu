@@ -937,8 +937,9 @@ template <int F>
 static int launch_one(const TraceLaunch& L, const KParams& kp, cudaStream_t s, std::string* err) {
   static int occ = 0;  // resident blocks per SM of this variant
   if (!occ) {
-    // all of the SM's shared memory for the resident blocks (the store is 128 B per trace)
-    cudaFuncSetAttribute(k_trace_eval<F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+#ifdef COH_TE_CARVEOUT
+    cudaFuncSetAttribute(k_trace_eval<F>, cudaFuncAttributePreferredSharedMemoryCarveout, COH_TE_CARVEOUT);
+#endif
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trace_eval<F>, kNT, 0);
     if (e != cudaSuccess || occ < 1) {
       *err = std::string("trace_eval occupancy: ") + cudaGetErrorString(e);
