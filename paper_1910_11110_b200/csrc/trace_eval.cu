@@ -121,9 +121,10 @@ __host__ __device__ constexpr uint32_t viol_threshold_addend(int c) { return (ui
   "and.b32 ix, " W ", 0xFC;\n\t"                      \
   "xor.b32 ix, ix, sv;\n\t"                           \
   "ld.shared.u32 ev, [ix+%6];\n\t"                    \
+  COH_PTX_STORE_EARLY                                  \
   "setp.lt.or.s32 p, ev, 0, p;\n\t"                   \
   COH_PTX_ACC                                          \
-  "st.shared.u16 [so+%5], ev;\n\t"                    \
+  COH_PTX_STORE_LATE                                   \
   "add.cc.u32 cy, %0, " T ";\n\t"                     \
   "addc.u32 %1, %1, %1;\n\t"                          \
   "SKIP:\n\t}\n\t"
@@ -151,6 +152,8 @@ __device__ __forceinline__ uint32_t run_chunk(const uint4 v, uint32_t toff, uint
                                               int fuel_left) {
   uint32_t stop;
   if (FUEL) {  // the call's steps must fit the remaining fuel, else it is the slow call
+#define COH_PTX_STORE_EARLY ""
+#define COH_PTX_STORE_LATE "st.shared.u16 [so+%5], ev;\n\t"
 #define COH_PTX_ACC                                 \
   "mul.hi.s32 cy, ev, 65536;\n\t"                   \
   "add.s32 an, %0, cy;\n\t"                         \
@@ -160,10 +163,27 @@ __device__ __forceinline__ uint32_t run_chunk(const uint4 v, uint32_t toff, uint
   "mov.u32 %0, an;\n\t"
     asm volatile(COH_PTX_CHUNK COH_PTX_OPERANDS(H));
 #undef COH_PTX_ACC
+#undef COH_PTX_STORE_EARLY
+#undef COH_PTX_STORE_LATE
   } else {
+#ifdef COH_TE_LATE_STS
+#define COH_PTX_STORE_EARLY ""
+#define COH_PTX_STORE_LATE "st.shared.u16 [so+%5], ev;\n\t"
+#else
+    // The store goes out before this call's own stop test, predicated on the stop of the
+    // calls before it: a slow entry's low half is the slot word it was read from (the store
+    // is unchanged by a stuck call / a missing key), so writing it back is harmless, and the
+    // next call's slot load no longer waits for the sign test (one ALU latency less per call
+    // on the store -> load chain).  Not with fuel: a call stopped by the fuel has a regular
+    // entry.
+#define COH_PTX_STORE_EARLY "@!p st.shared.u16 [so+%5], ev;\n\t"
+#define COH_PTX_STORE_LATE ""
+#endif
 #define COH_PTX_ACC "@p bra SKIP;\n\tmul.hi.s32 cy, ev, 65536;\n\tadd.s32 %0, %0, cy;\n\t"
     asm volatile(COH_PTX_CHUNK COH_PTX_OPERANDS(H));
 #undef COH_PTX_ACC
+#undef COH_PTX_STORE_EARLY
+#undef COH_PTX_STORE_LATE
   }
   return stop;
 }
