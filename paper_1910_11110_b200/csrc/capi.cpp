@@ -91,7 +91,7 @@ int eval_device(coh_ctx* ctx, const coh_trace_batch* b, const uint16_t* d_record
   // the launch's ticket and counter sums: the next slot of the context's ring, private
   // to this launch (launches of one context on different streams may run concurrently);
   // long launches (more than five rounds of traces per thread) hand out trace batches
-  L.slot = ctx->d_slots + (ctx->slot_next++ % cohb::kLaunchSlots);
+  L.slot = ctx->d_slots + (ctx->slot_next.fetch_add(1u, std::memory_order_relaxed) % cohb::kLaunchSlots);
   L.dynamic = n_traces > 5ull * 1024ull * (uint64_t)ctx->sms;
   L.overlap = (b->flags & COH_BATCH_OVERLAP) && uniform;
   L.flags = b->flags;

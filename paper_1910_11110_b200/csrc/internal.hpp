@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <string>
 
@@ -143,5 +144,5 @@ struct coh_ctx {
   void* d_pk[2] = {nullptr, nullptr};            // COH_BATCH_PACKED12 slices
   size_t pk_cap = 0;
   cohb::LaunchSlot* d_slots = nullptr;           // kLaunchSlots, zeroed at creation
-  uint32_t slot_next = 0;
+  std::atomic<uint32_t> slot_next{0};          // host threads may share a context
 };
