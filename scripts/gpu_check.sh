@@ -27,8 +27,10 @@ for k in 0 16 8 1; do
     --cache-control none --csv --log-file $OUT/ncu_elem_whole_k${k}_$TAG.csv python scripts/bench_elem.py --reps 1 --frag-log2 $k \
     > $OUT/ncu_elem_whole_k${k}_$TAG.txt 2>&1
 done
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_runs_collect -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_runs_collect -s 1 -c 1 \
   -o $OUT/prof_runs_collect_$TAG -f python scripts/runs_rho.py 16 > $OUT/ncu_prims_$TAG.txt 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_runs_place -s 1 -c 1 \
+  -o $OUT/prof_runs_place_$TAG -f python scripts/runs_rho.py 1 full >> $OUT/ncu_prims_$TAG.txt 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_trace_blocks -c 1 \
   -o $OUT/prof_trace_blocks_$TAG -f python -m pytest tests/test_trace_blocks_gpu.py -q -m gpu -k "vs_oracle and 20000" >> $OUT/ncu_prims_$TAG.txt 2>&1
 echo done
