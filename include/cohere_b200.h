@@ -131,7 +131,8 @@ typedef struct coh_trace_batch {
  * [12k, 12k + 12) of those 96 little-endian bits.  Unpacked on the device per pipeline
  * slice.  Not combinable with COH_BATCH_BLOCKS (no room for COH_REC_CONT). */
 #define COH_BATCH_PACKED12 0x2u
-/* COH_BATCH_OVERLAP (coh_eval_traces / _counted, whole-array batches): the launch may begin
+/* COH_BATCH_OVERLAP (coh_eval_traces / _counted, whole-array batches; ignored by
+ * coh_eval_traces_host, whose kernels read what its own copies wrote): the launch may begin
  * before the previous kernel on the same stream has finished (programmatic dependent
  * launch: its blocks take the SMs the previous launch's last blocks free, so a stream of
  * batches does not drain the GPU between launches).  The caller guarantees that the

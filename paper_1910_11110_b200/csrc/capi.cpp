@@ -294,7 +294,8 @@ int coh_eval_traces_host(coh_ctx* ctx, const coh_trace_batch* batch, coh_trace_r
   const uint32_t n_words = coh_boundary_words(batch->n_calls);
   const bool packed = batch->flags & COH_BATCH_PACKED12;
   coh_trace_batch dev_batch = *batch;  // what the device sees after unpacking
-  dev_batch.flags &= ~COH_BATCH_PACKED12;
+  // (no COH_BATCH_OVERLAP here: a slice's kernel reads what the copy / unpack before it wrote)
+  dev_batch.flags &= ~(COH_BATCH_PACKED12 | COH_BATCH_OVERLAP);
   // Slices of S traces: H2D of slice k+1 overlaps the kernel and D2H of slice k.
   static const uint64_t slice = [] {  // COH_HOST_SLICE: traces per slice (A/B timing)
     const char* v = std::getenv("COH_HOST_SLICE");
