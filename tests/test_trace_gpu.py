@@ -330,6 +330,9 @@ def test_packed12_host_entry_equals_plain(ctx):
     assert pk.size == recs.size // 8 * 12
     b, bb = ctx.eval_traces_host(pk, nt, nc, na, flags=coh.BATCH_PACKED12)
     assert same(a, b) and np.array_equal(ab, bb)
+    # COH_BATCH_OVERLAP is ignored by the host entry (its kernels read what its copies wrote)
+    c, cb = ctx.eval_traces_host(pk, nt, nc, na, flags=coh.BATCH_PACKED12 | coh.BATCH_OVERLAP)
+    assert same(a, c) and np.array_equal(ab, cb)
     with pytest.raises(coh.CohError):
         ctx.eval_traces_host(pk, nt, nc, na, flags=coh.BATCH_PACKED12 | coh.BATCH_BLOCKS)
 
