@@ -117,6 +117,9 @@ __device__ bool run_block_exact(const BlocksParams& p, uint8_t (*st)[kBT], uint3
 // arrays, so the order of their effects does not matter and the counts add up), and the
 // block commits at its end (boundary bit from the violated count).  Otherwise the block is
 // undone and re-run exactly (run_block_exact): it is where the trace stops.
+// UNIFORM: one element size (bytes = transfers x size, folded in at the end); FUEL: the fuel
+// can run out within the batch (else the commit needs no fuel test).
+template <bool UNIFORM, bool FUEL>
 __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
   __shared__ uint8_t st[COH_MAX_ARRAYS][kBT];
   __shared__ uint8_t undo[COH_MAX_ARRAYS][kBT];
@@ -138,15 +141,15 @@ __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
   const uint32_t n_words = (p.n_calls + 31u) / 32u;
   // the open block
   uint32_t b0 = 0, bsteps = 0, bxfers = 0, defect_arr = 0;
-  uint64_t bbytes = 0, touched = 0, seen = 0;  // touched: arrays written (undo); seen: named
+  uint64_t bbytes = 0, seen = 0;  // seen: arrays named by the block (undo holds their states before it)
   int bdv = 0;
   bool slow = false, defect = false, stopped = false;
 
   auto close_block = [&](uint32_t b1) {
-    if (!slow && !defect && (int64_t)L.steps + bsteps <= (int64_t)p.fuel) {  // commit
+    if (!slow && !defect && (!FUEL || (int64_t)L.steps + bsteps <= (int64_t)p.fuel)) {  // commit
       L.steps += bsteps;
       L.xfers += bxfers;
-      L.tbytes += bbytes;
+      if (!UNIFORM) L.tbytes += bbytes;
       L.viol += (uint32_t)bdv;
       if (L.viol) ++viol_blocks;
       else word |= 1u << (blocks_done & 31u);
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
         word = 0u;
       }
     } else {  // undo, then the block's exact outcome (the trace stops in it)
-      for (uint64_t m = touched; m; m &= m - 1) {
+      for (uint64_t m = seen; m; m &= m - 1) {
         const uint32_t a = (uint32_t)__ffsll((long long)m) - 1u;
         st[a][tid] = undo[a][tid];
       }
@@ -169,9 +172,9 @@ __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
       stopped = true;
     }
     bsteps = bxfers = 0;
-    bbytes = 0;
+    if (!UNIFORM) bbytes = 0;
     bdv = 0;
-    touched = seen = 0;
+    seen = 0;
     slow = defect = false;
   };
 
@@ -199,18 +202,17 @@ __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
     }
     seen |= 1ull << a;
     const uint32_t s0 = st[a][tid];
+    undo[a][tid] = (uint8_t)s0;
     const uint32_t e = s_lut[s0 * 64u + (type ^ ((s0 * 9u) & 63u))];  // internal.hpp lut_word
     if ((int32_t)e < 0) {  // stuck (whatever the order of the block's modes)
       slow = true;
       continue;
     }
-    undo[a][tid] = (uint8_t)s0;
     st[a][tid] = (uint8_t)((e >> 8) & 15u);
-    touched |= 1ull << a;
     const uint32_t x = (e >> 23) & 0x3Fu;
     bsteps += (e >> 16) & 0x7Fu;
     bxfers += x;
-    if (x) bbytes += (uint64_t)x * (p.uniform ? p.bytes_uniform : p.array_bytes[a]);
+    if (!UNIFORM && x) bbytes += (uint64_t)x * p.array_bytes[a];
     bdv += (int)((e >> 29) & 7u) - 1;
   }
   if (!stopped && p.n_calls) close_block(p.n_calls);
@@ -230,6 +232,7 @@ __global__ void __launch_bounds__(kBT) k_trace_blocks(const BlocksParams p) {
     sw[a >> 3] |= nib << (4u * (a & 7u));
     unsafe |= !(nib & 3u) || !(nib & 12u);
   }
+  if (UNIFORM) L.tbytes = (uint64_t)L.xfers * p.bytes_uniform;
   uint32_t stuck_flags = L.stuck_flags;
   if (unsafe) stuck_flags |= COH_FLAG_UNSAFE;
   uint4* out = reinterpret_cast<uint4*>(p.res + t);
@@ -293,7 +296,11 @@ int launch_trace_blocks(const TraceLaunch& L, void* stream, std::string* err) {
     *err = "trace_blocks: too many traces";
     return COH_E_ARG;
   }
-  k_trace_blocks<<<(uint32_t)grid, kBT, 0, s>>>(p);
+  const bool fuel = L.check_fuel;
+  if (p.uniform && !fuel) k_trace_blocks<true, false><<<(uint32_t)grid, kBT, 0, s>>>(p);
+  else if (p.uniform) k_trace_blocks<true, true><<<(uint32_t)grid, kBT, 0, s>>>(p);
+  else if (!fuel) k_trace_blocks<false, false><<<(uint32_t)grid, kBT, 0, s>>>(p);
+  else k_trace_blocks<false, true><<<(uint32_t)grid, kBT, 0, s>>>(p);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("trace_blocks launch: ") + cudaGetErrorString(e);
