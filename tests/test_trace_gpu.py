@@ -378,3 +378,30 @@ def test_overlapped_launch_stream(ctx, sizes, launches):
     ctx.eval_traces_counted(recs[m], m, nc, na, 10000, outs[-1][0], d_cnt, outs[-1][1], stream=s)
     torch.cuda.synchronize()
     assert torch.equal(d_cnt[:11], want[m][2][:11])
+
+
+@pytest.mark.parametrize("fuel,ab", [(700, None), (10000, list(range(1, 65))), (700, [4096] * 64)],
+                         ids=["fuel", "bytes", "fuel_uniform_bytes"])
+def test_overlap_flag_other_variants(ctx, fuel, ab):
+    """COH_BATCH_OVERLAP on the kernel variants it does not change: fuel-limited batches
+    (the slot store stays after the stop test) and non-uniform sizes (launched in order):
+    back-to-back launches with their own outputs equal a plain launch."""
+    s = torch.cuda.current_stream().cuda_stream
+    n, nc, na = 30000, 256, 64
+    d_rec = torch.empty(coh.records_elems(n, nc), dtype=torch.int16, device="cuda")
+    ctx.gen_records(9, 0, n, nc, na, 16, d_rec, s)
+    outs = [(torch.empty(n * 64, dtype=torch.uint8, device="cuda"),
+             torch.empty(coh.boundary_words(nc) * n, dtype=torch.int32, device="cuda"),
+             torch.zeros(16, dtype=torch.int64, device="cuda")) for _ in range(3)]
+    ctx.eval_traces_counted(d_rec, n, nc, na, fuel, outs[0][0], outs[0][2], outs[0][1], array_bytes=ab, stream=s)
+    for k in range(6):
+        ob = outs[1 + (k & 1)]
+        ctx.eval_traces_counted(d_rec, n, nc, na, fuel, ob[0], ob[2], ob[1], array_bytes=ab, stream=s,
+                                flags=coh.BATCH_OVERLAP)
+    torch.cuda.synchronize()
+    recs = d_rec.cpu().numpy().view(np.uint16)
+    want, want_b = o.orc_eval(recs, n, nc, na, fuel, ab)
+    for res, bnd, cnt in outs:
+        assert same(res.cpu().numpy().view(coh.RESULT_DTYPE), want)
+        assert np.array_equal(bnd.cpu().numpy().view(np.uint32), want_b)
+        assert torch.equal(cnt[:11], outs[0][2][:11])
