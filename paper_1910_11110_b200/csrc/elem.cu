@@ -12,6 +12,7 @@
 //          sync changes, ascending) and set the destination plane
 // Words move as 128-bit loads (8 consecutive words per thread), warp/block reductions
 // via shuffles; every kernel is HBM-streaming.
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <string>
@@ -550,9 +551,16 @@ int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, uint32_t n_sync_tiles,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
   constexpr size_t kApplySmem = (size_t)kApplyWarps * kStageBuf16 * 2u;
-  const cudaError_t attr =  // per call: the attribute belongs to the current device
-      cudaFuncSetAttribute(k_elem_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem);
-  if (attr != cudaSuccess) e = attr;
+  {  // once per device (the attribute belongs to the current device; host work on every call otherwise)
+    static std::atomic<bool> attr_set[64];
+    int dev = 0;
+    e = cudaGetDevice(&dev);
+    if (e == cudaSuccess && (dev < 0 || dev >= 64)) e = cudaErrorInvalidDevice;
+    if (e == cudaSuccess && !attr_set[dev].load(std::memory_order_acquire)) {
+      e = cudaFuncSetAttribute(k_elem_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem);
+      if (e == cudaSuccess) attr_set[dev].store(true, std::memory_order_release);
+    }
+  }
   if (n_tiles && e == cudaSuccess) e = launch_pdl(k_elem_pass1, n_tiles, kET, 0, s, d);
   if (n_tiles && e == cudaSuccess)  // a stage with only WRITE ops has nothing to decide (writes cannot get stuck)
     e = launch_pdl(k_elem_decide, (d.n_progs + kDecideWarps - 1) / kDecideWarps, 32 * kDecideWarps, 0, s, d);
