@@ -695,6 +695,24 @@ __device__ __forceinline__ void chunk_offsets(const RunCounts& C, const uint64_t
   }
 }
 
+// One warp copies n staged entries to out[at ..) (clipped at cap): eight independent L2
+// loads in flight per lane, coalesced stores (a chunk stages up to kRunCap entries; one
+// load at a time left the copy latency-bound at 1.8 TB/s).
+__device__ __forceinline__ void copy_staged(const uint32_t* src, uint32_t n, uint32_t* out, uint64_t at, uint64_t cap) {
+  if (at >= cap) return;
+  const uint32_t m = (uint64_t)n < cap - at ? n : (uint32_t)(cap - at);
+  uint32_t* const dst = out + at;
+  uint32_t i = threadIdx.x & 31;
+  for (; i + 224u < m; i += 256u) {
+    uint32_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcg(src + i + 32u * k);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dst[i + 32u * k] = v[k];
+  }
+  for (; i < m; i += 32u) dst[i] = __ldcg(src + i);
+}
+
 // Place pass, plus run_off[i] = global index of range i's first run: its chunk's offset +
 // the chunk-local count staged by the collect pass; ranges starting at the end get the
 // total.  Dynamic shared memory: kBT / 32 warps x kRunsBuf (dense run staging), then the
@@ -729,10 +747,8 @@ __global__ void __launch_bounds__(kBT, COH_RUNS_MINB) k_runs_place(const uint32_
   const uint64_t cs = C.chunk_s[wid], ce = C.chunk_e[wid];
   if (cs <= kRunCap && ce <= kRunCap) {  // staged by the collect pass: copy
     const uint32_t* const ss = stage + wid * (2 * kRunCap);
-    for (uint32_t i = threadIdx.x & 31; i < cs; i += 32)
-      if (gs + i < cap) run_start[gs + i] = ss[i];
-    for (uint32_t i = threadIdx.x & 31; i < ce; i += 32)
-      if (ge + i < cap) run_end[ge + i] = ss[kRunCap + i];
+    copy_staged(ss, (uint32_t)cs, run_start, gs, cap);
+    copy_staged(ss + kRunCap, (uint32_t)ce, run_end, ge, cap);
     return;
   }
   chunk_runs(words, F, f0, f1,
