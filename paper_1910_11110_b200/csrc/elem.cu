@@ -518,8 +518,8 @@ __global__ void __launch_bounds__(32 * kApplyWarps, 3) k_elem_apply(const ElemDe
             emit_dense16(st, xs, Ts, w0 * 32u, gs, out_s, d.runs_cap, wbuf);
             emit_dense16(en, xe, Te, w0 * 32u, ge, out_e, d.runs_cap, wbuf);
           } else {
-            if (__any_sync(0xffffffffu, ns != 0u)) emit_sparse(st, gs + xs, w0 * 32u, out_s, d.runs_cap);
-            if (__any_sync(0xffffffffu, ne != 0u)) emit_sparse(en, ge + xe, w0 * 32u, out_e, d.runs_cap);
+            if (__any_sync(0xffffffffu, ns != 0u)) emit_sparse_bits(st, ns, gs + xs, w0 * 32u, out_s, d.runs_cap);
+            if (__any_sync(0xffffffffu, ne != 0u)) emit_sparse_bits(en, ne, ge + xe, w0 * 32u, out_e, d.runs_cap);
           }
           gs += Ts;
           ge += Te;

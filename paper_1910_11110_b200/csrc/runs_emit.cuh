@@ -88,7 +88,8 @@ __device__ __forceinline__ void emit_dense16(const uint32_t* m, uint32_t S, uint
 // Sparse emission of one lane's starts (or ends) m[0..3] at out[pos ..) (pos = the lane's
 // first position): the lowest set bit of every word goes out without a loop (its position
 // is known from the popcounts of the words before it), the rare further bits of a word in
-// a warp-uniform second round.
+// a warp-uniform second round.  (The zero-run walker's form: a loop per bit, below, costs
+// it 17 us at rho 2^-16 -- its register allocation shifts.)
 __device__ __forceinline__ void emit_sparse(const uint32_t* m, uint64_t pos, uint32_t cb, uint32_t* out, uint64_t cap) {
   uint32_t rest = 0;
   uint64_t p = pos;
@@ -107,6 +108,23 @@ __device__ __forceinline__ void emit_sparse(const uint32_t* m, uint64_t pos, uin
     for (; x; x &= x - 1u, ++q)
       if (q < cap) out[q] = cb + 32u * k + (uint32_t)(__ffs(x) - 1);
     p += (uint32_t)__popc(m[k]);
+  }
+}
+
+// The same for the element path's apply (2% faster there at rho 2^-8 and 1/2): the lane's
+// n bits, one loop trip per bit, lowest first, over its 128 cells as two 64-bit words (the
+// warp runs max-n trips, 1-3 on a sparse step; the positions need no per-store test).
+__device__ __forceinline__ void emit_sparse_bits(const uint32_t* m, uint32_t n, uint64_t pos, uint32_t cb,
+                                                 uint32_t* out, uint64_t cap) {
+  const uint32_t nn = pos >= cap ? 0u : (cap - pos < n ? (uint32_t)(cap - pos) : n);
+  uint64_t lo = (uint64_t)m[1] << 32 | m[0], hi = (uint64_t)m[3] << 32 | m[2];
+  uint32_t* const o = out + pos;
+  for (uint32_t j = 0; j < nn; ++j) {
+    const bool in_lo = lo != 0ull;
+    const uint64_t x = in_lo ? lo : hi;
+    o[j] = cb + (in_lo ? 0u : 64u) + (uint32_t)(__ffsll((long long)x) - 1);
+    if (in_lo) lo &= lo - 1ull;
+    else hi &= hi - 1ull;
   }
 }
 
