@@ -107,19 +107,22 @@ def ref_runs(bits, ranges, n_cells):
     return np.array(off, np.uint64), np.concatenate(st).astype(np.uint32), np.concatenate(en).astype(np.uint32)
 
 
-@pytest.mark.parametrize("pattern", ["sparse", "dense", "mixed"])
+@pytest.mark.parametrize("pattern", ["sparse", "medium", "dense", "mixed"])
 def test_zero_runs_staging(ctx, pattern):
     """Zero runs on 2^22-cell planes whose chunks hold few runs (staged once and copied),
-    many runs (over the per-chunk staging capacity: the chunk is walked again) or both,
+    hundreds (staged, copied eight loads per lane at a time), many runs (over the per-chunk
+    staging capacity: the chunk is walked again) or both,
     with whole-plane, ragged and empty ranges; plus output truncated at `cap`."""
     from paper_1910_11110_b200.bitmap import zero_runs
-    rng = np.random.default_rng({"sparse": 1, "dense": 2, "mixed": 3}[pattern])
+    rng = np.random.default_rng({"sparse": 1, "dense": 2, "mixed": 3, "medium": 4}[pattern])
     n_cells, n_planes = 1 << 22, 4
     n = n_planes * n_cells
     if pattern == "sparse":
         bits = (rng.random(n) < 0.99995).astype(np.uint8)
     elif pattern == "dense":
         bits = (rng.random(n) < 0.5).astype(np.uint8)
+    elif pattern == "medium":  # ~2.7M runs: several hundred per warp chunk, under its staging cap
+        bits = (rng.random(n) < 0.8).astype(np.uint8)
     else:  # dense and sparse stretches alternate
         bits = np.ones(n, np.uint8)
         for a in range(0, n, 1 << 18):

@@ -68,6 +68,18 @@ def test_runs_capacity_overflow_counts_everything(ctx):
     assert np.array_equal(small["runs"][0][:4], full["runs"][0][:4])
 
 
+@pytest.mark.parametrize("frag_log2,cap", [(8, 5), (8, 333), (1, 7), (1, 4099)])
+def test_runs_capacity_fragmented(ctx, frag_log2, cap):
+    """Truncation at runs_cap inside sparse (rho 2^-8) and dense (rho 1/2) steps: the
+    written prefix equals the uncapped output, the run count is the full count."""
+    p = Program.generate(9, 2, 1 << 18, 8, 8, 64, frag_log2=frag_log2)
+    full = elem_eval(ctx, [p], runs_cap=1 << 20)
+    small = elem_eval(ctx, [p], runs_cap=cap)
+    n = int(full["results"][0].n_runs)
+    assert n > cap and int(small["results"][0].n_runs) == n
+    assert np.array_equal(small["runs"][0][:cap], full["runs"][0][:cap])
+
+
 def test_malformed_program_is_construction_error(ctx):
     import paper_1910_11110_b200 as coh
 
