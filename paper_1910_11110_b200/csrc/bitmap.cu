@@ -592,6 +592,7 @@ __device__ __forceinline__ void place_step(const Flat& F, uint64_t f, uint32_t r
 // list) while the last collect blocks finish.
 struct RunCounts {
   uint64_t *chunk_s, *chunk_e, *block_s, *block_e;
+  uint64_t *chunk_xs, *chunk_xe;  // exclusive prefix of the chunk counts inside their block
 };
 
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -622,15 +623,18 @@ __global__ void __launch_bounds__(kBT, COH_RUNS_MINB) k_runs_collect(const uint3
     ws[1][warp] = le;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint64_t bs = 0, be = 0;
-#pragma unroll
-    for (int w = 0; w < (int)(kBT / 32); ++w) {
-      bs += ws[0][w];
-      be += ws[1][w];
+  if (lane == 0) {  // the chunk's offsets inside the block (the place pass then loads one word)
+    uint64_t xs = 0, xe = 0;
+    for (uint32_t w = 0; w < warp; ++w) {
+      xs += ws[0][w];
+      xe += ws[1][w];
     }
-    C.block_s[blockIdx.x] = bs;
-    C.block_e[blockIdx.x] = be;
+    C.chunk_xs[wid] = xs;
+    C.chunk_xe[wid] = xe;
+    if (warp == kBT / 32 - 1) {
+      C.block_s[blockIdx.x] = xs + ls;
+      C.block_e[blockIdx.x] = xe + le;
+    }
   }
 }
 
@@ -687,12 +691,8 @@ __device__ void block_scan2(const uint64_t* a, const uint64_t* b, uint32_t n, ui
 __device__ __forceinline__ void chunk_offsets(const RunCounts& C, const uint64_t* bs, const uint64_t* be, uint64_t wid,
                                               uint64_t& gs, uint64_t& ge) {
   const uint64_t blk = wid / (kBT / 32);
-  gs = bs[blk];
-  ge = be[blk];
-  for (uint64_t w = blk * (kBT / 32); w < wid; ++w) {
-    gs += __ldcg(C.chunk_s + w);
-    ge += __ldcg(C.chunk_e + w);
-  }
+  gs = bs[blk] + __ldcg(C.chunk_xs + wid);
+  ge = be[blk] + __ldcg(C.chunk_xe + wid);
 }
 
 // One warp copies n staged entries to out[at ..) (clipped at cap): eight independent L2
@@ -727,8 +727,13 @@ __global__ void __launch_bounds__(kBT, COH_RUNS_MINB) k_runs_place(const uint32_
   uint32_t* const wbuf = runs_smem + (threadIdx.x >> 5) * kRunsBuf;
   uint64_t* const bs = reinterpret_cast<uint64_t*>(runs_smem + (kBT / 32) * kRunsBuf);
   uint64_t* const be = bs + gridDim.x + 1;
-  block_scan2(C.block_s, C.block_e, gridDim.x, bs, be);
   const uint64_t Q = F.qp[F.n], n_chunks = (uint64_t)gridDim.x * (kBT / 32);
+  uint64_t f0, f1, wid;
+  warp_chunk(Q, f0, f1, wid);
+  // this warp's chunk words, loaded ahead of the block scan (independent of it)
+  const uint64_t cs = __ldcg(C.chunk_s + wid), ce = __ldcg(C.chunk_e + wid);
+  const uint64_t xs = __ldcg(C.chunk_xs + wid), xe = __ldcg(C.chunk_xe + wid);
+  block_scan2(C.block_s, C.block_e, gridDim.x, bs, be);
   const uint64_t cper = (((Q + n_chunks - 1) / n_chunks) + 31) & ~31ull;  // as warp_chunk
   for (uint64_t i = (uint64_t)blockIdx.x * kBT + threadIdx.x; i <= F.n; i += (uint64_t)gridDim.x * kBT) {
     const uint64_t f = F.qp[i];
@@ -739,12 +744,9 @@ __global__ void __launch_bounds__(kBT, COH_RUNS_MINB) k_runs_place(const uint32_
     }
     run_off[i] = gs;
   }
-  uint64_t f0, f1, wid;
-  warp_chunk(Q, f0, f1, wid);
   if (f0 >= f1) return;
-  uint64_t gs, ge;
-  chunk_offsets(C, bs, be, wid, gs, ge);
-  const uint64_t cs = C.chunk_s[wid], ce = C.chunk_e[wid];
+  const uint64_t blk = wid / (kBT / 32);
+  uint64_t gs = bs[blk] + xs, ge = be[blk] + xe;
   if (cs <= kRunCap && ce <= kRunCap) {  // staged by the collect pass: copy
     const uint32_t* const ss = stage + wid * (2 * kRunCap);
     copy_staged(ss, (uint32_t)cs, run_start, gs, cap);
@@ -879,7 +881,7 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   const uint64_t n_chunks = (uint64_t)grid * (kBT / 32);
   // scratch: run counts (see RunCounts, all written by the collect pass), staged runs,
   // chunk-local range offsets
-  const size_t counts_b = sizeof(uint64_t) * (2 * n_chunks + 2 * (size_t)grid);
+  const size_t counts_b = (sizeof(uint64_t) * (4 * n_chunks + 2 * (size_t)grid) + 255u) & ~(size_t)255u;  // stage: whole lines
   const size_t stage_b = sizeof(uint32_t) * 2 * kRunCap * n_chunks;
   Scratch co;
   co.s = s;
@@ -890,6 +892,8 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   C.chunk_e = C.chunk_s + n_chunks;
   C.block_s = C.chunk_e + n_chunks;
   C.block_e = C.block_s + grid;
+  C.chunk_xs = C.block_e + grid;
+  C.chunk_xe = C.chunk_xs + n_chunks;
   uint32_t* stage = reinterpret_cast<uint32_t*>(static_cast<char*>(co.p) + counts_b);
   uint32_t* off_local = stage + 2 * kRunCap * n_chunks;
   const size_t place_smem = kRunsSmem + sizeof(uint64_t) * 2 * ((size_t)grid + 1);
