@@ -21,7 +21,6 @@
 // warp chunks (counts + staged runs), a scan of the chunk counts, and a place pass putting
 // each start / end at its global ascending position (the k-th start and the k-th end are
 // the same run: runs never cross ranges).
-#include <atomic>
 #include <cuda_runtime.h>
 
 #include <string>
@@ -46,6 +45,7 @@ constexpr int kRU = COH_RUNS_RU;  // warp steps in flight in the zero-run walker
 #endif
 constexpr int kRunsPf = COH_RUNS_PF;  // walker iterations between an L2 prefetch and its loads
 constexpr uint32_t kRunsBuf = kStageBuf16 / 2;  // dense-step staging per warp, u32 words (kStageBuf16 u16 slots)
+constexpr size_t kRunsSmem = (size_t)(kBT / 32) * kRunsBuf * 4u;  // both zero-run passes: dense staging
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 struct Flat {
@@ -640,8 +640,7 @@ __global__ void __launch_bounds__(kBT, COH_RUNS_MINB) k_runs_collect(const uint3
 
 // Exclusive scans of a[0..n) and b[0..n) into sa / sb (n + 1 entries, the last = totals),
 // one block of kBT threads, n <= kBT * kPer.
-constexpr uint32_t kMaxCollectBlocks = 2048;
-constexpr uint32_t kMaxDevices = 64;  // per-device launch setup cache (extract_zero_runs)  // count-pass blocks (one wave)
+constexpr uint32_t kMaxCollectBlocks = 2048;  // count-pass blocks (one wave)
 __device__ void block_scan2(const uint64_t* a, const uint64_t* b, uint32_t n, uint64_t* sa, uint64_t* sb) {
   constexpr uint32_t kPer = kMaxCollectBlocks / kBT;
   __shared__ uint64_t wsum[2][kBT / 32];
@@ -780,6 +779,23 @@ int check(coh_ctx* ctx, const char* what) {
 }
 
 }  // namespace
+
+cudaError_t runs_ctx_init(int sms, int* grid) {
+  int occ = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_runs_collect, kBT, kRunsSmem);
+  if (e != cudaSuccess) return e;
+  const int g = sms * (occ > 0 ? occ : 1);
+  if (g > (int)kMaxCollectBlocks) return cudaErrorInvalidConfiguration;
+  if ((e = cudaFuncSetAttribute(k_runs_collect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRunsSmem)) !=
+      cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(k_runs_place, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(kRunsSmem + sizeof(uint64_t) * 2 * ((size_t)g + 1)))) != cudaSuccess)
+    return e;
+  *grid = g;
+  return cudaSuccess;
+}
+
 }  // namespace cohb
 
 using namespace cohb;
@@ -855,29 +871,10 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   if (!n) return COH_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   COH_BM_FLAT(ctx, d_ranges, n, s)
-  // one wave of the collect pass (the place pass reuses its warp -> chunk mapping); the
-  // occupancy query and the shared-memory attributes are host work on every call's
-  // critical path, so they run once per device (the attributes belong to the current one)
-  constexpr size_t kRunsSmem = (size_t)(kBT / 32) * kRunsBuf * 4u;
-  static std::atomic<int> runs_grid[kMaxDevices];
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return fail(ctx, "zero_runs device", e);
-  if (dev < 0 || dev >= (int)kMaxDevices) return fail(ctx, "zero_runs device", cudaErrorInvalidDevice);
-  int grid = runs_grid[dev].load(std::memory_order_acquire);
-  if (!grid) {
-    int occ = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_runs_collect, kBT, kRunsSmem)) != cudaSuccess)
-      return fail(ctx, "zero_runs occupancy", e);
-    grid = ctx->sms * (occ > 0 ? occ : 1);
-    if (grid > (int)kMaxCollectBlocks) return fail(ctx, "zero_runs grid", cudaErrorInvalidConfiguration);
-    if ((e = cudaFuncSetAttribute(k_runs_collect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRunsSmem)) !=
-            cudaSuccess ||
-        (e = cudaFuncSetAttribute(k_runs_place, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(kRunsSmem + sizeof(uint64_t) * 2 * ((size_t)grid + 1)))) != cudaSuccess)
-      return fail(ctx, "zero runs: shared memory attribute", e);
-    runs_grid[dev].store(grid, std::memory_order_release);
-  }
+  // one wave of the collect pass (the place pass reuses its warp -> chunk mapping); grid and
+  // shared-memory attributes are set up once per context (runs_ctx_init)
+  const int grid = ctx->runs_grid;
+  if (grid <= 0 || grid > (int)kMaxCollectBlocks) return fail(ctx, "zero_runs grid", cudaErrorInvalidConfiguration);
   const uint64_t n_chunks = (uint64_t)grid * (kBT / 32);
   // scratch: run counts (see RunCounts, all written by the collect pass), staged runs,
   // chunk-local range offsets
@@ -885,7 +882,7 @@ extern "C" int coh_bitmap_extract_zero_runs(coh_ctx* ctx, const uint32_t* d_word
   const size_t stage_b = sizeof(uint32_t) * 2 * kRunCap * n_chunks;
   Scratch co;
   co.s = s;
-  e = cudaMallocAsync(&co.p, counts_b + stage_b + sizeof(uint32_t) * ((size_t)n + 1), s);
+  cudaError_t e = cudaMallocAsync(&co.p, counts_b + stage_b + sizeof(uint32_t) * ((size_t)n + 1), s);
   if (e != cudaSuccess) return fail(ctx, "zero_runs scratch", e);
   RunCounts C;
   C.chunk_s = static_cast<uint64_t*>(co.p);

@@ -140,6 +140,8 @@ int coh_ctx_create(int device, coh_ctx** out) {
       if ((e = cudaDeviceGetDefaultMemPool(&pool, device)) != cudaSuccess) break;
       if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess) break;
     }
+    if ((e = cohb::runs_ctx_init(ctx->sms, &ctx->runs_grid)) != cudaSuccess) break;
+    if ((e = cohb::elem_ctx_init()) != cudaSuccess) break;
     int tpb = 0;
     std::string err;
     rc = cohb::trace_eval_occupancy(&ctx->blocks_per_sm, &tpb, 256, &err);

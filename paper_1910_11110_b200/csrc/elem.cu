@@ -12,7 +12,6 @@
 //          sync changes, ascending) and set the destination plane
 // Words move as 128-bit loads (8 consecutive words per thread), warp/block reductions
 // via shuffles; every kernel is HBM-streaming.
-#include <atomic>
 #include <cuda_runtime.h>
 
 #include <string>
@@ -547,20 +546,15 @@ static cudaError_t launch_pdl(void (*kernel)(KArgs...), uint32_t grid, uint32_t 
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+cudaError_t elem_ctx_init() {  // at context creation: the apply kernel's dynamic shared memory
+  return cudaFuncSetAttribute(k_elem_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)((size_t)kApplyWarps * kStageBuf16 * 2u));
+}
+
 int launch_elem_stage(const ElemDev& d, uint32_t n_tiles, uint32_t n_sync_tiles, void* stream, std::string* err) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
   constexpr size_t kApplySmem = (size_t)kApplyWarps * kStageBuf16 * 2u;
-  {  // once per device (the attribute belongs to the current device; host work on every call otherwise)
-    static std::atomic<bool> attr_set[64];
-    int dev = 0;
-    e = cudaGetDevice(&dev);
-    if (e == cudaSuccess && (dev < 0 || dev >= 64)) e = cudaErrorInvalidDevice;
-    if (e == cudaSuccess && !attr_set[dev].load(std::memory_order_acquire)) {
-      e = cudaFuncSetAttribute(k_elem_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem);
-      if (e == cudaSuccess) attr_set[dev].store(true, std::memory_order_release);
-    }
-  }
   if (n_tiles && e == cudaSuccess) e = launch_pdl(k_elem_pass1, n_tiles, kET, 0, s, d);
   if (n_tiles && e == cudaSuccess)  // a stage with only WRITE ops has nothing to decide (writes cannot get stuck)
     e = launch_pdl(k_elem_decide, (d.n_progs + kDecideWarps - 1) / kDecideWarps, 32 * kDecideWarps, 0, s, d);

@@ -113,6 +113,10 @@ int launch_trace_eval(const TraceLaunch& p, void* stream, std::string* err);
 // Multi-mode blocks (COH_BATCH_BLOCKS, trace_blocks.cu).
 int launch_trace_blocks(const TraceLaunch& p, void* stream, std::string* err);
 int trace_eval_occupancy(int* blocks_per_sm, int* threads_per_block, uint32_t n_calls, std::string* err);
+// Launch setup done once per context at creation (the device is current): shared-memory
+// attributes of the zero-run and element-apply kernels, the zero-run grid.
+cudaError_t runs_ctx_init(int sms, int* grid);
+cudaError_t elem_ctx_init();
 int launch_gen_records(uint64_t seed, uint64_t trace0, uint64_t n_traces, uint32_t n_calls,
                        uint32_t n_arrays, uint32_t adv_per1024, uint16_t* d_records, void* stream,
                        std::string* err);
@@ -145,4 +149,5 @@ struct coh_ctx {
   size_t pk_cap = 0;
   cohb::LaunchSlot* d_slots = nullptr;           // kLaunchSlots, zeroed at creation
   std::atomic<uint32_t> slot_next{0};          // host threads may share a context
+  int runs_grid = 0;                            // zero-run passes: one wave (runs_ctx_init)
 };
