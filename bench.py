@@ -913,6 +913,7 @@ def run_ours(args, rank, world, local):
         dist.barrier()
     torch.cuda.synchronize()
     ms = t_start.elapsed_time(t_end)
+    ms_local = ms  # this rank's timed region: args.steps launches of k_trace_eval, back to back
     # one launch alone (events on both sides, no overlap), for the kernel's roofline
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
     for k in range(10):
@@ -931,9 +932,13 @@ def run_ours(args, rank, world, local):
     # launch = 2 B per evaluated call (records) + 64 B result + 4 B per boundary word
     local_calls = calls_per_step // world
     alg_bytes = 2 * local_calls + N * (64 + 4 * coh.boundary_words(N_CALLS))
-    k_ms = statistics.mean(kern_ms)
+    k_ms_iso = statistics.mean(kern_ms)
+    # the kernel's average launch duration over the timed region (one launch per step; with
+    # COH_BATCH_OVERLAP a launch's tail overlaps the next one's start)
+    k_ms = ms_local / args.steps
     peak, peak_src = peaks()
     achieved = alg_bytes / (k_ms / 1e3) / 1e9
+    achieved_iso = alg_bytes / (k_ms_iso / 1e3) / 1e9
     traffic, traffic_traces = ncu_traffic()
     if traffic is not None and traffic_traces:
         traffic = traffic * N / traffic_traces
@@ -1012,16 +1017,24 @@ def run_ours(args, rank, world, local):
             "roofline": {"bound": "hbm", "kernel": "k_trace_eval", "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms": k_ms,
-                         "note": "bound in practice by the L1 data pipe (shared-memory wavefronts, ~80% is its "
-                                 "practical ceiling) together with instruction issue: see `l1_data_pipe`, `issue` "
-                                 "and profiles/",
+                         "kernel_ms_basis": "timed region / launches (one k_trace_eval per step)",
+                         "note": "bound in practice by the L1 data pipe (shared-memory wavefronts) together with "
+                                 "instruction issue: see `l1_data_pipe`, `issue` and profiles/; `isolated_launch` = "
+                                 "the same for one launch with nothing around it (its whole tail exposed)",
+                         "isolated_launch": {
+                             "kernel_ms": k_ms_iso, "achieved": achieved_iso, "frac": achieved_iso / peak,
+                             "issue": ncu_issue(N, k_ms_iso, (clk or {}).get("sm_mhz"),
+                                                torch.cuda.get_device_properties(dev).multi_processor_count),
+                             "l1_data_pipe": ncu_l1_pipe(N, k_ms_iso, (clk or {}).get("sm_mhz"),
+                                                         torch.cuda.get_device_properties(dev).multi_processor_count)},
                          "issue": ncu_issue(N, k_ms, (clk or {}).get("sm_mhz"), torch.cuda.get_device_properties(dev)
                                             .multi_processor_count),
                          "l1_data_pipe": ncu_l1_pipe(N, k_ms, (clk or {}).get("sm_mhz"),
                                                      torch.cuda.get_device_properties(dev).multi_processor_count)},
             "step_launch": "one coh_eval_traces_counted per step with COH_BATCH_OVERLAP: a step may start on the "
                            "SMs its predecessor's last blocks free (programmatic dependent launch); step outputs "
-                           "double-buffered; roofline kernel_ms from separate non-overlapped launches",
+                           "double-buffered; roofline kernel_ms = the timed region per launch (isolated_launch: separate "
+                           "non-overlapped launches)",
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
             "bitmap": bitmap, "container": container, "sweep": sweep_info, "c1": c1, "c4": c4, "overlap": overlap,
             "checker": checker, "blocks": blocks,
